@@ -1,0 +1,564 @@
+/*
+ * dgsm_oracle.c — plain, slow, double-precision CPU oracle for the DGSM build
+ * and query of arXiv 2601.01660 ("Deep Gaussian Shadow Maps").
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * It shares no code, header or constant table with the CUDA path under
+ * paper_2601_01660_b200/csrc/ and must never be called by the product path.
+ *
+ * Every function cites the PAPER.md passage ("P:L<line>", section/equation)
+ * it follows; where the paper is silent the DESIGN.md reading ("Q<n>") is
+ * named.  Built with  gcc -O2 -ffp-contract=off  (no FMA contraction, strict
+ * IEEE double) so that the integer binning decisions (R4-R7) are reproducible
+ * bit for bit by any implementation that performs the same IEEE operations in
+ * the same order.
+ *
+ * Parity status: every function here is pinned by tests/test_oracle_pins.py
+ * (SPEC/paper values, closed forms, quadrature, brute force); the culled-vs-
+ * unculled gap is pinned only against our own unculled mode ("parity
+ * unpinned against the paper": the paper prints no atlas values).
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_PI 3.141592653589793
+
+/* ------------------------------------------------------------------ */
+/* R2  rotation and precision matrix ("precision A_i = Sigma_i^-1";   */
+/*     Sigma = R diag(s^2) R^T, 3DGS quaternion convention w,x,y,z)          */
+/* ------------------------------------------------------------------ */
+static void or_rotation(const float q4[4], double R[3][3])
+{
+    double w = q4[0], x = q4[1], y = q4[2], z = q4[3];
+    double qn = sqrt(((w * w + x * x) + y * y) + z * z);
+    w = w / qn; x = x / qn; y = y / qn; z = z / qn;
+    R[0][0] = 1.0 - 2.0 * (y * y + z * z);
+    R[0][1] = 2.0 * (x * y - w * z);
+    R[0][2] = 2.0 * (x * z + w * y);
+    R[1][0] = 2.0 * (x * y + w * z);
+    R[1][1] = 1.0 - 2.0 * (x * x + z * z);
+    R[1][2] = 2.0 * (y * z - w * x);
+    R[2][0] = 2.0 * (x * z - w * y);
+    R[2][1] = 2.0 * (y * z + w * x);
+    R[2][2] = 1.0 - 2.0 * (x * x + y * y);
+}
+
+/* A = R diag(s^-2) R^T */
+static void or_precision(const float s3[3], const float q4[4], double A[3][3])
+{
+    double R[3][3];
+    or_rotation(q4, R);
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+            double acc = 0.0;
+            for (int j = 0; j < 3; ++j)
+                acc += R[r][j] * (1.0 / ((double)s3[j] * (double)s3[j])) * R[c][j];
+            A[r][c] = acc;
+        }
+}
+
+/* Opacity clamp (Q16): alpha' = min(max(alpha,1e-4),1-1e-4). */
+static double or_alpha_clamped(float alpha)
+{
+    double a = alpha;
+    if (a < 1e-4) a = 1e-4;
+    if (a > 1.0 - 1e-4) a = 1.0 - 1e-4;
+    return a;
+}
+
+/* Eq.5 (TraceAvg): beta = kappa * tau* * sqrt(tr(A)/3)/sqrt(2 pi),
+ * tau* = -ln(1 - alpha). */
+double or_beta(const float s3[3], const float q4[4], float alpha, double kappa)
+{
+    double A[3][3];
+    or_precision(s3, q4, A);
+    double trA = A[0][0] + A[1][1] + A[2][2];
+    double tau_star = -log1p(-or_alpha_clamped(alpha));
+    return kappa * tau_star * sqrt(trA / 3.0) / sqrt(2.0 * OR_PI);
+}
+
+void or_calibrate(const float* scales, const float* rotations, const float* opacities,
+                  int64_t n, double kappa, double* beta_out)
+{
+    for (int64_t i = 0; i < n; ++i)
+        beta_out[i] = or_beta(scales + 3 * i, rotations + 4 * i, opacities[i], kappa);
+}
+
+/* ------------------------------------------------------------------ */
+/* Octahedral map psi                                      */
+/* ------------------------------------------------------------------ */
+static double or_sgn(double x) { return x >= 0.0 ? 1.0 : -1.0; } /* sgn(0)=+1 (Q4) */
+
+/* encode: q = d/(|x|+|y|+|z|); fold for q_z < 0.  Accepts any
+ * non-zero vector (the normalisation by the 1-norm makes |d| irrelevant). */
+void or_oct_encode(const double d[3], double uv[2])
+{
+    double n1 = (fabs(d[0]) + fabs(d[1])) + fabs(d[2]);
+    double qx = d[0] / n1, qy = d[1] / n1, qz = d[2] / n1;
+    if (qz >= 0.0) {
+        uv[0] = qx;
+        uv[1] = qy;
+    } else {
+        uv[0] = or_sgn(qx) * (1.0 - fabs(qy));
+        uv[1] = or_sgn(qy) * (1.0 - fabs(qx));
+    }
+}
+
+/* decode: z = 1-|u|-|v|; undo the fold; normalise. */
+void or_oct_decode(double u, double v, double d[3])
+{
+    double x = u, y = v, z = 1.0 - fabs(u) - fabs(v);
+    if (z < 0.0) {
+        x = or_sgn(u) * (1.0 - fabs(v));
+        y = or_sgn(v) * (1.0 - fabs(u));
+    }
+    double nrm = sqrt(x * x + y * y + z * z);
+    d[0] = x / nrm; d[1] = y / nrm; d[2] = z / nrm;
+}
+
+/* Texel centre direction ("pixel centers"; Q3: u<->col, v<->row,
+ * u_c = (col+0.5)*2/W - 1). */
+void or_texel_dir(int row, int col, int H, int W, double d[3])
+{
+    double u = (col + 0.5) * 2.0 / W - 1.0;
+    double v = (row + 0.5) * 2.0 / H - 1.0;
+    or_oct_decode(u, v, d);
+}
+
+/* Radial bin centre t_k = (k + 1/2) t_max / K. */
+double or_bin_center(int k, int K, double t_max) { return (k + 0.5) * t_max / K; }
+
+/* ------------------------------------------------------------------ */
+/* R4-R5  light-space footprint                            */
+/* Output: fp[0]=D, fp[1]=px, fp[2]=py, fp[3]=p1, fp[4]=lambda1;         */
+/*         rect[0..3] = c0,c1,r0,r1 (unclamped integer texel range).     */
+/* Returns 0 when the Gaussian is excluded (D <= 1e-6, Q17), else 1.      */
+/* The eigenvalue uses the basis-free form of Sigma_perp (Q7/R5):         */
+/*   tr_perp = sum s_j^2 (1 - w_j^2),  det_perp = prod s_j^2 * sum w_j^2/s_j^2, */
+/*   w = R^T (m/D); lambda1 = tr/2 + sqrt(max(tr^2/4 - det, 0)).          */
+/* ------------------------------------------------------------------ */
+int or_footprint(const float mu[3], const float s3[3], const float q4[4],
+                 const float o[3], int res, double k_sigma, double rho_scale,
+                 double fp[5], int64_t rect[4])
+{
+    int H = res, W = res;
+    double mx = (double)mu[0] - (double)o[0];
+    double my = (double)mu[1] - (double)o[1];
+    double mz = (double)mu[2] - (double)o[2];
+    double D = sqrt((mx * mx + my * my) + mz * mz);
+    if (!(D > 1e-6)) return 0;
+
+    double m[3] = {mx, my, mz}, uv[2];
+    or_oct_encode(m, uv);
+    double px = (uv[0] + 1.0) * (0.5 * W) - 0.5;
+    double py = (uv[1] + 1.0) * (0.5 * H) - 0.5;
+
+    double R[3][3];
+    or_rotation(q4, R);
+    double dx = mx / D, dy = my / D, dz = mz / D;
+    double w[3], s2[3];
+    for (int j = 0; j < 3; ++j) {
+        w[j] = (R[0][j] * dx + R[1][j] * dy) + R[2][j] * dz;
+        s2[j] = (double)s3[j] * (double)s3[j];
+    }
+    double tr = (s2[0] * (1.0 - w[0] * w[0]) + s2[1] * (1.0 - w[1] * w[1])) +
+                s2[2] * (1.0 - w[2] * w[2]);
+    double det = ((s2[0] * s2[1]) * s2[2]) *
+                 (((w[0] * w[0]) / s2[0] + (w[1] * w[1]) / s2[1]) + (w[2] * w[2]) / s2[2]);
+    double disc = (tr * tr) * 0.25 - det;
+    if (disc < 0.0) disc = 0.0;
+    double lam1 = tr * 0.5 + sqrt(disc);
+    double rho = (rho_scale * (double)(H + W)) / (2.0 * OR_PI); /* P:L172, Q5 */
+    double p1 = ((k_sigma * sqrt(lam1)) / D) * rho;
+
+    fp[0] = D; fp[1] = px; fp[2] = py; fp[3] = p1; fp[4] = lam1;
+    double c0 = ceil(px - p1), c1 = floor(px + p1);
+    double r0 = ceil(py - p1), r1 = floor(py + p1);
+    /* clamp to the extended lattice [-W, 2W-1] in double before the cast (R6);
+     * px, py lie in [-0.5, W-0.5] so only these two sides can overflow. */
+    if (c0 < -(double)W) c0 = -(double)W;
+    if (c1 > 2.0 * W - 1.0) c1 = 2.0 * W - 1.0;
+    if (r0 < -(double)H) r0 = -(double)H;
+    if (r1 > 2.0 * H - 1.0) r1 = 2.0 * H - 1.0;
+    rect[0] = (int64_t)c0; rect[1] = (int64_t)c1;
+    rect[2] = (int64_t)r0; rect[3] = (int64_t)r1;
+    return 1;
+}
+
+/* Mirror-wrap of an extended-lattice texel centre onto the atlas (R10/Q8,
+ * SPEC S:L286): a column outside [0,W-1] reflects and flips the row; then a
+ * row outside [0,H-1] reflects and flips the column. */
+void or_mirror_wrap(int64_t col, int64_t row, int H, int W, int64_t out[2])
+{
+    if (col < 0) { col = -1 - col; row = H - 1 - row; }
+    else if (col > W - 1) { col = 2 * (int64_t)W - 1 - col; row = H - 1 - row; }
+    if (row < 0) { row = -1 - row; col = W - 1 - col; }
+    else if (row > H - 1) { row = 2 * (int64_t)H - 1 - row; col = W - 1 - col; }
+    out[0] = col; out[1] = row;
+}
+
+/* ------------------------------------------------------------------ */
+/* R6-R7  binning into 8x8 tiles and the (light, tile, depth)   */
+/* key order (Q10).                                                       */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    uint32_t light, tile, depth_bits, index;
+} or_entry;
+
+static int or_entry_cmp(const void* pa, const void* pb)
+{
+    const or_entry* a = (const or_entry*)pa;
+    const or_entry* b = (const or_entry*)pb;
+    if (a->light != b->light) return a->light < b->light ? -1 : 1;
+    if (a->tile != b->tile) return a->tile < b->tile ? -1 : 1;
+    if (a->depth_bits != b->depth_bits) return a->depth_bits < b->depth_bits ? -1 : 1;
+    if (a->index != b->index) return a->index < b->index ? -1 : 1;
+    return 0;
+}
+
+static uint32_t or_float_bits(double D)
+{
+    float f = (float)D;
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    return u;
+}
+
+/* Tile set of one (light, Gaussian): every integer texel centre inside the
+ * closed square [px-p1,px+p1]x[py-p1,py+p1] (clamped to the extended lattice)
+ * is mapped (wrap: mirror-wrap; clamp: dropped if outside) and the set of
+ * tiles containing a mapped centre is marked in `mark` (n_tiles bytes).
+ * Returns the number of distinct tiles. */
+static int64_t or_tile_set(const int64_t rect[4], int res, int bin_mode, unsigned char* mark)
+{
+    int H = res, W = res, TW = res / 8;
+    int64_t n = 0;
+    for (int64_t row = rect[2]; row <= rect[3]; ++row)
+        for (int64_t col = rect[0]; col <= rect[1]; ++col) {
+            int64_t cr[2];
+            if (bin_mode == 1) { /* clamp (3DGS getRect) */
+                if (col < 0 || col > W - 1 || row < 0 || row > H - 1) continue;
+                cr[0] = col; cr[1] = row;
+            } else {
+                or_mirror_wrap(col, row, H, W, cr);
+            }
+            int64_t t = (cr[1] >> 3) * TW + (cr[0] >> 3);
+            if (!mark[t]) { mark[t] = 1; ++n; }
+        }
+    return n;
+}
+
+/* Bin every (light, Gaussian); returns P (number of entries).  When
+ * `capacity` >= P the sorted entries are written to the four output arrays.
+ * bin_mode: 0 = wrap (default), 1 = clamp. */
+int64_t or_bin(const float* means, const float* scales, const float* rotations, int64_t n,
+               const float* light_pos /*[L][3]*/, int L, int res, double k_sigma,
+               double rho_scale, int bin_mode, uint32_t* out_light, uint32_t* out_tile,
+               uint32_t* out_depth, uint32_t* out_index, int64_t capacity)
+{
+    int64_t n_tiles = (int64_t)(res / 8) * (res / 8);
+    unsigned char* mark = (unsigned char*)calloc((size_t)n_tiles, 1);
+    int64_t P = 0, cap = 1024;
+    or_entry* e = (or_entry*)malloc(sizeof(or_entry) * cap);
+    for (int l = 0; l < L; ++l)
+        for (int64_t i = 0; i < n; ++i) {
+            double fp[5];
+            int64_t rect[4];
+            if (!or_footprint(means + 3 * i, scales + 3 * i, rotations + 4 * i, light_pos + 3 * l,
+                              res, k_sigma, rho_scale, fp, rect))
+                continue;
+            if (rect[0] > rect[1] || rect[2] > rect[3]) continue;
+            int64_t cnt = or_tile_set(rect, res, bin_mode, mark);
+            if (cnt == 0) continue;
+            uint32_t db = or_float_bits(fp[0]);
+            for (int64_t t = 0; t < n_tiles; ++t) {
+                if (!mark[t]) continue;
+                mark[t] = 0;
+                if (P == cap) {
+                    cap *= 2;
+                    e = (or_entry*)realloc(e, sizeof(or_entry) * cap);
+                }
+                e[P].light = (uint32_t)l;
+                e[P].tile = (uint32_t)t;
+                e[P].depth_bits = db;
+                e[P].index = (uint32_t)i;
+                ++P;
+            }
+        }
+    qsort(e, (size_t)P, sizeof(or_entry), or_entry_cmp);
+    if (capacity >= P && out_light) {
+        for (int64_t j = 0; j < P; ++j) {
+            out_light[j] = e[j].light;
+            out_tile[j] = e[j].tile;
+            out_depth[j] = e[j].depth_bits;
+            out_index[j] = e[j].index;
+        }
+    }
+    free(e);
+    free(mark);
+    return P;
+}
+
+/* ------------------------------------------------------------------ */
+/* Eq.2-3: optical depth of one Gaussian along o + s d, s in [0,t] */
+/* ------------------------------------------------------------------ */
+void or_ray_quadratic(const double A[3][3], const double mu[3], const double o[3],
+                      const double d[3], double abc[3])
+{
+    double om[3] = {o[0] - mu[0], o[1] - mu[1], o[2] - mu[2]}; /* o_L - mu_i */
+    double Ad[3], Aom[3];
+    for (int r = 0; r < 3; ++r) {
+        Ad[r] = A[r][0] * d[0] + A[r][1] * d[1] + A[r][2] * d[2];
+        Aom[r] = A[r][0] * om[0] + A[r][1] * om[1] + A[r][2] * om[2];
+    }
+    abc[0] = d[0] * Ad[0] + d[1] * Ad[1] + d[2] * Ad[2];        /* a = d^T A d */
+    abc[1] = d[0] * Aom[0] + d[1] * Aom[1] + d[2] * Aom[2];     /* b = d^T A (o-mu) */
+    abc[2] = om[0] * Aom[0] + om[1] * Aom[1] + om[2] * Aom[2];  /* c */
+}
+
+/* Eq.3: int_0^t exp(-1/2 (a s^2 + 2 b s + c)) ds, times beta. */
+double or_segment_depth(double a, double b, double c, double beta, double t)
+{
+    double pref = sqrt(OR_PI / (2.0 * a)) * exp(-0.5 * (c - b * b / a));
+    double h = sqrt(a / 2.0);
+    return beta * pref * (erf(h * (t + b / a)) - erf(h * (b / a)));
+}
+
+/* ------------------------------------------------------------------ */
+/* R8  the atlas  T[l][k][row][col] = exp(-tau(d(row,col), t_k))  (Eq.4) */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    const float *means, *scales, *rotations, *opacities;
+    int64_t n;
+    const float* light_pos; /* [L][3] */
+    const float* t_max;     /* [L]    */
+    int L, res, K;
+    double kappa, k_sigma, rho_scale;
+    int bin_mode, culled;
+    int64_t tile_stride; /* compute only work items with (l*n_tiles+tile) % stride == 0 */
+    /* derived */
+    double* A;    /* [n][9] */
+    double* beta; /* [n] */
+    int64_t n_tiles;
+    /* culled lists */
+    const uint32_t *e_light, *e_tile, *e_index;
+    const int64_t* range; /* [L*n_tiles+1] start offsets into the sorted entries */
+    unsigned char* excluded; /* [L][n] */
+    double* T;               /* [L][K][res][res] */
+    int64_t next;            /* work counter */
+    pthread_mutex_t lock;
+} or_build_ctx;
+
+static void or_build_item(or_build_ctx* c, int64_t item)
+{
+    int l = (int)(item / c->n_tiles);
+    int64_t tile = item % c->n_tiles;
+    int TW = c->res / 8, H = c->res, W = c->res, K = c->K;
+    int ty = (int)(tile / TW), tx = (int)(tile % TW);
+    double o[3] = {c->light_pos[3 * l], c->light_pos[3 * l + 1], c->light_pos[3 * l + 2]};
+    double tmax = c->t_max[l];
+    double* tau = (double*)malloc(sizeof(double) * K);
+    for (int r = 0; r < 8; ++r)
+        for (int cc = 0; cc < 8; ++cc) {
+            int row = ty * 8 + r, col = tx * 8 + cc;
+            double d[3];
+            or_texel_dir(row, col, H, W, d);
+            for (int k = 0; k < K; ++k) tau[k] = 0.0;
+            int64_t j0, j1;
+            if (c->culled) { j0 = c->range[item]; j1 = c->range[item + 1]; }
+            else { j0 = 0; j1 = c->n; }
+            for (int64_t j = j0; j < j1; ++j) {
+                int64_t i = c->culled ? (int64_t)c->e_index[j] : j;
+                if (!c->culled && c->excluded[(int64_t)l * c->n + i]) continue;
+                double mu[3] = {c->means[3 * i], c->means[3 * i + 1], c->means[3 * i + 2]};
+                double Ai[3][3];
+                memcpy(Ai, c->A + 9 * i, sizeof(Ai));
+                double abc[3];
+                or_ray_quadratic(Ai, mu, o, d, abc);
+                for (int k = 0; k < K; ++k)
+                    tau[k] += or_segment_depth(abc[0], abc[1], abc[2], c->beta[i],
+                                               or_bin_center(k, K, tmax));
+            }
+            for (int k = 0; k < K; ++k)
+                c->T[(((int64_t)l * K + k) * H + row) * W + col] = exp(-tau[k]);
+        }
+    free(tau);
+}
+
+static void* or_build_worker(void* arg)
+{
+    or_build_ctx* c = (or_build_ctx*)arg;
+    int64_t n_items = (int64_t)c->L * c->n_tiles;
+    for (;;) {
+        pthread_mutex_lock(&c->lock);
+        int64_t item = c->next;
+        c->next += 1;
+        pthread_mutex_unlock(&c->lock);
+        while (item < n_items && item % c->tile_stride != 0) {
+            pthread_mutex_lock(&c->lock);
+            item = c->next;
+            c->next += 1;
+            pthread_mutex_unlock(&c->lock);
+        }
+        if (item >= n_items) break;
+        or_build_item(c, item);
+    }
+    return NULL;
+}
+
+/* Build the atlas.  T_out: [L][K][res][res] doubles; items skipped by
+ * tile_stride are set to NaN.  culled=1 uses the R6 tile lists (the GPU
+ * parity target), culled=0 sums every non-excluded Gaussian at every texel
+ * (the reference for the culling error, P:L335 ablation D).  Returns P (the
+ * number of binned entries) in culled mode, 0 otherwise, -1 on bad input. */
+int64_t or_build(const float* means, const float* scales, const float* rotations,
+                 const float* opacities, int64_t n, const float* light_pos, const float* t_max,
+                 int L, int res, int K, double kappa, double k_sigma, double rho_scale,
+                 int bin_mode, int culled, int64_t tile_stride, int n_threads, double* T_out)
+{
+    if (res < 8 || res % 8 != 0 || K < 1 || L < 1 || n < 0) return -1;
+    or_build_ctx c;
+    memset(&c, 0, sizeof(c));
+    c.means = means; c.scales = scales; c.rotations = rotations; c.opacities = opacities;
+    c.n = n; c.light_pos = light_pos; c.t_max = t_max; c.L = L; c.res = res; c.K = K;
+    c.kappa = kappa; c.k_sigma = k_sigma; c.rho_scale = rho_scale;
+    c.bin_mode = bin_mode; c.culled = culled;
+    c.tile_stride = tile_stride < 1 ? 1 : tile_stride;
+    c.n_tiles = (int64_t)(res / 8) * (res / 8);
+    c.T = T_out;
+    int64_t total = (int64_t)L * K * res * res;
+    for (int64_t j = 0; j < total; ++j) T_out[j] = NAN;
+
+    c.A = (double*)malloc(sizeof(double) * 9 * (n > 0 ? n : 1));
+    c.beta = (double*)malloc(sizeof(double) * (n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; ++i) {
+        double Ai[3][3];
+        or_precision(scales + 3 * i, rotations + 4 * i, Ai);
+        memcpy(c.A + 9 * i, Ai, sizeof(Ai));
+        c.beta[i] = or_beta(scales + 3 * i, rotations + 4 * i, opacities[i], kappa);
+    }
+    c.excluded = (unsigned char*)calloc((size_t)L * (n > 0 ? n : 1), 1);
+    for (int l = 0; l < L; ++l)
+        for (int64_t i = 0; i < n; ++i) {
+            double fp[5];
+            int64_t rect[4];
+            c.excluded[(int64_t)l * n + i] =
+                !or_footprint(means + 3 * i, scales + 3 * i, rotations + 4 * i, light_pos + 3 * l,
+                              res, k_sigma, rho_scale, fp, rect);
+        }
+
+    int64_t P = 0;
+    uint32_t *el = NULL, *et = NULL, *ed = NULL, *ei = NULL;
+    int64_t* range = NULL;
+    if (culled) {
+        P = or_bin(means, scales, rotations, n, light_pos, L, res, k_sigma, rho_scale, bin_mode,
+                   NULL, NULL, NULL, NULL, 0);
+        size_t sz = sizeof(uint32_t) * (size_t)(P > 0 ? P : 1);
+        el = (uint32_t*)malloc(sz); et = (uint32_t*)malloc(sz);
+        ed = (uint32_t*)malloc(sz); ei = (uint32_t*)malloc(sz);
+        or_bin(means, scales, rotations, n, light_pos, L, res, k_sigma, rho_scale, bin_mode, el,
+               et, ed, ei, P);
+        int64_t n_items = (int64_t)L * c.n_tiles;
+        range = (int64_t*)malloc(sizeof(int64_t) * (n_items + 1));
+        int64_t j = 0;
+        for (int64_t it = 0; it <= n_items; ++it) {
+            while (j < P && (int64_t)el[j] * c.n_tiles + et[j] < it) ++j;
+            range[it] = j;
+        }
+        c.e_light = el; c.e_tile = et; c.e_index = ei; c.range = range;
+    }
+
+    if (n_threads < 1) n_threads = 1;
+    pthread_mutex_init(&c.lock, NULL);
+    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * n_threads);
+    for (int t = 0; t < n_threads; ++t) pthread_create(&th[t], NULL, or_build_worker, &c);
+    for (int t = 0; t < n_threads; ++t) pthread_join(th[t], NULL);
+    pthread_mutex_destroy(&c.lock);
+    free(th);
+
+    free(c.A); free(c.beta); free(c.excluded);
+    free(el); free(et); free(ed); free(ei); free(range);
+    return P;
+}
+
+/* Optical depth tau(d, t) of the full mixture along one ray (Eq.2), every
+ * non-excluded Gaussian, no culling.  Used by the pins (quadrature). */
+double or_tau_ray(const float* means, const float* scales, const float* rotations,
+                  const float* opacities, int64_t n, const double o[3], const double d_in[3],
+                  double t, double kappa)
+{
+    double nd = sqrt(d_in[0] * d_in[0] + d_in[1] * d_in[1] + d_in[2] * d_in[2]);
+    double d[3] = {d_in[0] / nd, d_in[1] / nd, d_in[2] / nd};
+    double tau = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        double A[3][3], abc[3];
+        or_precision(scales + 3 * i, rotations + 4 * i, A);
+        double mu[3] = {means[3 * i], means[3 * i + 1], means[3 * i + 2]};
+        or_ray_quadratic(A, mu, o, d, abc);
+        tau += or_segment_depth(abc[0], abc[1], abc[2],
+                                or_beta(scales + 3 * i, rotations + 4 * i, opacities[i], kappa), t);
+    }
+    return tau;
+}
+
+/* ------------------------------------------------------------------ */
+/* R10-R12  query: trilinear sampling of the atlas at receiver centres   */
+/* (P:L185-187), mirror-wrap taps (Q12), t clamped to [t_0, t_{K-1}],    */
+/* product over lights (Q13), optional colour multiply.         */
+/* ------------------------------------------------------------------ */
+double or_sample(const double* atlas_l /* [K][res][res] */, int res, int K, const double o[3],
+                 double t_max, const double x[3])
+{
+    int H = res, W = res;
+    double m[3] = {x[0] - o[0], x[1] - o[1], x[2] - o[2]};
+    double t = sqrt((m[0] * m[0] + m[1] * m[1]) + m[2] * m[2]);
+    if (t == 0.0) return 1.0; /* Q18 */
+    double uv[2];
+    or_oct_encode(m, uv);
+    double fx = (uv[0] + 1.0) * (0.5 * W) - 0.5;
+    double fy = (uv[1] + 1.0) * (0.5 * H) - 0.5;
+    double x0 = floor(fx), y0 = floor(fy);
+    double wx = fx - x0, wy = fy - y0;
+    double fk = (t * K) / t_max - 0.5;
+    if (fk < 0.0) fk = 0.0;
+    if (fk > K - 1) fk = K - 1;
+    double k0 = floor(fk);
+    double wk = fk - k0;
+    int ik0 = (int)k0, ik1 = ik0 + 1 < K ? ik0 + 1 : K - 1;
+    double acc = 0.0;
+    for (int dk = 0; dk < 2; ++dk)
+        for (int dy = 0; dy < 2; ++dy)
+            for (int dx = 0; dx < 2; ++dx) {
+                int64_t cr[2];
+                or_mirror_wrap((int64_t)x0 + dx, (int64_t)y0 + dy, H, W, cr);
+                int k = dk ? ik1 : ik0;
+                double w = (dx ? wx : 1.0 - wx) * (dy ? wy : 1.0 - wy) * (dk ? wk : 1.0 - wk);
+                acc += w * atlas_l[((int64_t)k * H + cr[1]) * W + cr[0]];
+            }
+    return acc;
+}
+
+void or_query(const double* atlas /* [L][K][res][res] */, int L, int K, int res,
+              const float* light_pos, const float* t_max, const float* positions, int64_t m,
+              double* T_out, double* colors /* nullable [m][3], multiplied in place */)
+{
+    int64_t per_light = (int64_t)K * res * res;
+    for (int64_t q = 0; q < m; ++q) {
+        double x[3] = {positions[3 * q], positions[3 * q + 1], positions[3 * q + 2]};
+        double T = 1.0;
+        for (int l = 0; l < L; ++l) {
+            double o[3] = {light_pos[3 * l], light_pos[3 * l + 1], light_pos[3 * l + 2]};
+            T *= or_sample(atlas + l * per_light, res, K, o, t_max[l], x);
+        }
+        T_out[q] = T;
+        if (colors) {
+            colors[3 * q] *= T;
+            colors[3 * q + 1] *= T;
+            colors[3 * q + 2] *= T;
+        }
+    }
+}

@@ -1,0 +1,198 @@
+"""ctypes + numpy wrapper around ``liboracle.so`` (oracle/dgsm_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by ``tests/``, ``__graft_entry__.smoke()``
+and the ``cpu_baseline`` / ``--impl reference`` legs of ``bench.py``.  The
+product path (``paper_2601_01660_b200``) never imports this module, and this
+module never imports the product package.
+
+Every function mirrors a C function of the oracle; see its header for the
+PAPER.md passages followed.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "dgsm_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+GCC_FLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-Wall"]
+
+
+def build_oracle(force: bool = False) -> str:
+    """Compile the oracle with gcc (strict IEEE double, no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", *GCC_FLAGS, "-o", _LIB, _SRC, "-lm", "-lpthread"])
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build_oracle()
+        L = C.CDLL(_LIB)
+        dp, fp, u32p, i64p = (C.POINTER(C.c_double), C.POINTER(C.c_float),
+                              C.POINTER(C.c_uint32), C.POINTER(C.c_int64))
+        L.or_beta.restype = C.c_double
+        L.or_beta.argtypes = [fp, fp, C.c_float, C.c_double]
+        L.or_oct_encode.argtypes = [dp, dp]
+        L.or_oct_decode.argtypes = [C.c_double, C.c_double, dp]
+        L.or_texel_dir.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, dp]
+        L.or_bin_center.restype = C.c_double
+        L.or_bin_center.argtypes = [C.c_int, C.c_int, C.c_double]
+        L.or_footprint.restype = C.c_int
+        L.or_footprint.argtypes = [fp, fp, fp, fp, C.c_int, C.c_double, C.c_double, dp, i64p]
+        L.or_mirror_wrap.argtypes = [C.c_int64, C.c_int64, C.c_int, C.c_int, i64p]
+        L.or_bin.restype = C.c_int64
+        L.or_bin.argtypes = [fp, fp, fp, C.c_int64, fp, C.c_int, C.c_int, C.c_double, C.c_double,
+                             C.c_int, u32p, u32p, u32p, u32p, C.c_int64]
+        L.or_ray_quadratic.argtypes = [dp, dp, dp, dp, dp]
+        L.or_segment_depth.restype = C.c_double
+        L.or_segment_depth.argtypes = [C.c_double] * 5
+        L.or_build.restype = C.c_int64
+        L.or_build.argtypes = [fp, fp, fp, fp, C.c_int64, fp, fp, C.c_int, C.c_int, C.c_int,
+                               C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int64,
+                               C.c_int, dp]
+        L.or_tau_ray.restype = C.c_double
+        L.or_tau_ray.argtypes = [fp, fp, fp, fp, C.c_int64, dp, dp, C.c_double, C.c_double]
+        L.or_query.argtypes = [dp, C.c_int, C.c_int, C.c_int, fp, fp, fp, C.c_int64, dp, dp]
+        _lib = L
+    return _lib
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _p(a, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+BIN_WRAP, BIN_CLAMP = 0, 1
+
+
+def beta(scales, rotation, alpha, kappa=1.0) -> float:
+    """Eq.5 for one Gaussian."""
+    s, q = _f32(scales), _f32(rotation)
+    return lib().or_beta(_p(s, C.c_float), _p(q, C.c_float), float(alpha), float(kappa))
+
+
+def oct_encode(d):
+    d = _f64(d)
+    out = np.zeros(2)
+    lib().or_oct_encode(_p(d, C.c_double), _p(out, C.c_double))
+    return out
+
+
+def oct_decode(u, v):
+    out = np.zeros(3)
+    lib().or_oct_decode(float(u), float(v), _p(out, C.c_double))
+    return out
+
+
+def texel_dir(row, col, H, W):
+    out = np.zeros(3)
+    lib().or_texel_dir(int(row), int(col), int(H), int(W), _p(out, C.c_double))
+    return out
+
+
+def bin_center(k, K, t_max) -> float:
+    return lib().or_bin_center(int(k), int(K), float(t_max))
+
+
+def footprint(mean, scales, rotation, light, res, k_sigma=3.0, rho_scale=1.0):
+    """R4-R5: returns None if excluded, else dict(D, px, py, p1, lam1, rect=(c0,c1,r0,r1))."""
+    mu, s, q, o = _f32(mean), _f32(scales), _f32(rotation), _f32(light)
+    fpv = np.zeros(5)
+    rect = np.zeros(4, dtype=np.int64)
+    ok = lib().or_footprint(_p(mu, C.c_float), _p(s, C.c_float), _p(q, C.c_float),
+                            _p(o, C.c_float), int(res), float(k_sigma), float(rho_scale),
+                            _p(fpv, C.c_double), _p(rect, C.c_int64))
+    if not ok:
+        return None
+    return dict(D=fpv[0], px=fpv[1], py=fpv[2], p1=fpv[3], lam1=fpv[4], rect=tuple(int(x) for x in rect))
+
+
+def mirror_wrap(col, row, H, W):
+    out = np.zeros(2, dtype=np.int64)
+    lib().or_mirror_wrap(int(col), int(row), int(H), int(W), _p(out, C.c_int64))
+    return int(out[0]), int(out[1])
+
+
+def bin_entries(means, scales, rotations, light_pos, res, k_sigma=3.0, rho_scale=1.0,
+                bin_mode=BIN_WRAP):
+    """R6-R7: sorted (light, tile, depth_bits, index) arrays (uint32 each)."""
+    mu, s, q, lp = _f32(means), _f32(scales), _f32(rotations), _f32(light_pos)
+    n, L = mu.shape[0], lp.reshape(-1, 3).shape[0]
+    args = [_p(mu, C.c_float), _p(s, C.c_float), _p(q, C.c_float), n, _p(lp, C.c_float), L,
+            int(res), float(k_sigma), float(rho_scale), int(bin_mode)]
+    P = lib().or_bin(*args, None, None, None, None, 0)
+    outs = [np.zeros(max(P, 1), dtype=np.uint32) for _ in range(4)]
+    lib().or_bin(*args, *[_p(o, C.c_uint32) for o in outs], P)
+    return tuple(o[:P] for o in outs)
+
+
+def ray_quadratic(A, mu, o, d):
+    A, mu, o, d = _f64(A), _f64(mu), _f64(o), _f64(d)
+    out = np.zeros(3)
+    lib().or_ray_quadratic(_p(A, C.c_double), _p(mu, C.c_double), _p(o, C.c_double),
+                           _p(d, C.c_double), _p(out, C.c_double))
+    return out
+
+
+def segment_depth(a, b, c, beta_, t) -> float:
+    return lib().or_segment_depth(float(a), float(b), float(c), float(beta_), float(t))
+
+
+def tau_ray(g, o, d, t, kappa=1.0) -> float:
+    mu, s, q, a = _f32(g["means"]), _f32(g["scales"]), _f32(g["rotations"]), _f32(g["opacities"])
+    o, d = _f64(o), _f64(d)
+    return lib().or_tau_ray(_p(mu, C.c_float), _p(s, C.c_float), _p(q, C.c_float),
+                            _p(a, C.c_float), mu.shape[0], _p(o, C.c_double), _p(d, C.c_double),
+                            float(t), float(kappa))
+
+
+def build(g, lights, res, K, kappa=1.0, k_sigma=3.0, rho_scale=1.0, bin_mode=BIN_WRAP,
+          culled=True, tile_stride=1, n_threads=None):
+    """R8: the atlas T[L][K][res][res] in float64 (NaN where skipped by tile_stride).
+
+    ``g``: dict of means [n,3], scales [n,3], rotations [n,4] (w,x,y,z), opacities [n].
+    ``lights``: dict(position [L,3], t_max [L]).
+    Returns (T, P) with P the number of binned entries (culled mode)."""
+    mu, s, q, a = _f32(g["means"]), _f32(g["scales"]), _f32(g["rotations"]), _f32(g["opacities"])
+    lp, tm = _f32(lights["position"]).reshape(-1, 3), _f32(lights["t_max"]).reshape(-1)
+    L = lp.shape[0]
+    T = np.empty((L, K, res, res), dtype=np.float64)
+    n_threads = n_threads or os.cpu_count() or 1
+    P = lib().or_build(_p(mu, C.c_float), _p(s, C.c_float), _p(q, C.c_float), _p(a, C.c_float),
+                       mu.shape[0], _p(lp, C.c_float), _p(tm, C.c_float), L, int(res), int(K),
+                       float(kappa), float(k_sigma), float(rho_scale), int(bin_mode),
+                       int(bool(culled)), int(tile_stride), int(n_threads), _p(T, C.c_double))
+    if P < 0:
+        raise ValueError("oracle build: invalid arguments")
+    return T, int(P)
+
+
+def query(atlas, lights, positions, colors=None):
+    """R10-R12: T_out[m] = prod_l trilinear(atlas_l, x) (float64); colors *= T if given."""
+    at = _f64(atlas)
+    L, K, res = at.shape[0], at.shape[1], at.shape[2]
+    lp, tm = _f32(lights["position"]).reshape(-1, 3), _f32(lights["t_max"]).reshape(-1)
+    x = _f32(positions).reshape(-1, 3)
+    out = np.zeros(x.shape[0])
+    col = None if colors is None else _f64(colors).copy()
+    lib().or_query(_p(at, C.c_double), L, K, res, _p(lp, C.c_float), _p(tm, C.c_float),
+                   _p(x, C.c_float), x.shape[0], _p(out, C.c_double),
+                   None if col is None else _p(col, C.c_double))
+    return (out, col) if colors is not None else out

@@ -1,0 +1,426 @@
+"""Pins of the CPU oracle to things other than itself (CPU only, -m "not gpu").
+
+Each test names the PAPER.md passage (P:L<line>) or the mathematical fact it
+pins.  Chosen so that a plausible slip (a dropped term, a wrong sign or index,
+a transposed operand) fails at least one of them:
+
+* SPEC/paper worked values (tests/golden/spec_examples.json);
+* brute-force quadrature of the mixture density (scipy / mpmath);
+* closed forms (isotropic on-axis Gaussian: T(inf) = (1-alpha)^kappa);
+* invariants (T in (0,1], monotone in k, empty -> 1, duplication -> T^2,
+  culled >= unculled, 90-degree rotation equivariance);
+* brute force of the binning over all tiles via the inverse mirror map;
+* geometric checks of the octahedral map and its seam rule.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from paper_2601_01660_b200 import synth
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+# ----------------------------------------------------------- worked values
+def test_ray_quadratic_spec(oracle_mod):
+    g = GOLD["ray_quadratic_unit_iso"]
+    abc = oracle_mod.ray_quadratic(np.eye(3), g["mu"], g["o"], g["d"])
+    assert np.allclose(abc, g["abc"], atol=1e-15)
+
+
+def test_ray_quadratic_is_the_quadratic_form(oracle_mod):
+    """Eq.2: (o+sd-mu)^T A (o+sd-mu) == a s^2 + 2 b s + c, at any s."""
+    rng = np.random.default_rng(1)
+    for _ in range(20):
+        M = rng.standard_normal((3, 3))
+        A = M @ M.T + 0.1 * np.eye(3)
+        mu, o = rng.standard_normal(3), rng.standard_normal(3)
+        d = rng.standard_normal(3); d /= np.linalg.norm(d)
+        a, b, c = oracle_mod.ray_quadratic(A, mu, o, d)
+        for s in (0.0, 0.7, 2.5):
+            x = o + s * d - mu
+            assert math.isclose(x @ A @ x, a * s * s + 2 * b * s + c, rel_tol=1e-12, abs_tol=1e-12)
+
+
+@pytest.mark.parametrize("key", ["segment_depth_0_1", "segment_depth_0_inf"])
+def test_segment_depth_spec(oracle_mod, key):
+    g = GOLD[key]
+    v = oracle_mod.segment_depth(*g["abc"], g["beta"], g["t"])
+    assert round(v, g["digits"]) == pytest.approx(g["value"], abs=10 ** -g["digits"])
+    assert oracle_mod.segment_depth(*g["abc"], 0.0, g["t"]) == 0.0  # beta = 0 -> 0
+
+
+def test_segment_depth_vs_mpmath(oracle_mod):
+    """Eq.3 closed form == numerical quadrature of Eq.2's integrand."""
+    import mpmath as mp
+    mp.mp.dps = 30
+    rng = np.random.default_rng(2)
+    for _ in range(25):
+        a = float(np.exp(rng.uniform(-2, 6)))
+        s_star = rng.uniform(-1, 5)           # closest approach, possibly behind
+        r = rng.uniform(0, 6)                 # c - b^2/a >= 0
+        b = -a * s_star
+        c = r + b * b / a
+        t = rng.uniform(0.1, 8)
+        beta = rng.uniform(0.1, 3)
+        f = lambda s: mp.e ** (-0.5 * (a * s * s + 2 * b * s + c))
+        pts = [0, t] if not (0 < s_star < t) else [0, s_star, t]
+        ref = beta * mp.quad(f, pts)
+        v = oracle_mod.segment_depth(a, b, c, beta, t)
+        assert abs(v - float(ref)) <= 1e-9 * (1 + abs(float(ref)))
+
+
+def test_transmittance_value():
+    g = GOLD["transmittance_tau1"]
+    assert round(math.exp(-g["tau"]), g["digits"]) == g["value"]  # Eq.4 is exp(-tau)
+
+
+def test_beta_spec(oracle_mod):
+    g = GOLD["beta_traceavg"]
+    v = oracle_mod.beta(g["scales"], [1, 0, 0, 0], g["alpha"], g["kappa"])
+    assert round(v, g["digits"]) == pytest.approx(g["value"], abs=1e-6)
+
+
+def test_beta_properties(oracle_mod):
+    """Eq.5: beta -> 0 as alpha -> 0 (clamped at 1e-4); rotation
+    invariant; proportional to kappa; for isotropic s, beta * sqrt(2 pi) s =
+    kappa tau* (TraceAvg full-line depth through the centre is kappa tau* for
+    every s)."""
+    rng = np.random.default_rng(3)
+    assert oracle_mod.beta([0.1, 0.2, 0.3], [1, 0, 0, 0], 0.0) < 1e-3
+    for _ in range(10):
+        s = np.exp(rng.uniform(-5, 0, 3))
+        q = synth.random_quaternions(rng, 1)[0]
+        al = rng.uniform(0.05, 0.95)
+        b1 = oracle_mod.beta(s, [1, 0, 0, 0], al)
+        b2 = oracle_mod.beta(s, q, al)
+        assert math.isclose(b1, b2, rel_tol=1e-6)
+        assert math.isclose(oracle_mod.beta(s, q, al, 2.5), 2.5 * b2, rel_tol=1e-12)
+        tr = float(np.sum(1.0 / s.astype(np.float32).astype(np.float64) ** 2))
+        assert math.isclose(b1, -math.log(1 - float(np.float32(al))) * math.sqrt(tr / 3) / math.sqrt(2 * math.pi),
+                            rel_tol=1e-9)
+    for s in (0.01, 0.1, 1.0):
+        g = dict(means=[[0, 0, 10.0]], scales=[[s, s, s]], rotations=[[1, 0, 0, 0]], opacities=[0.4])
+        full = oracle_mod.tau_ray(g, [0, 0, 0], [0, 0, 1], 20.0)
+        assert math.isclose(full, -math.log(1 - float(np.float32(0.4))), rel_tol=1e-9)
+
+
+# ------------------------------------------------------------ octahedral
+def test_oct_spec(oracle_mod):
+    for d, uv in GOLD["oct_encode"]["cases"]:
+        assert np.allclose(oracle_mod.oct_encode(d), uv, atol=0)
+    for uv, d in GOLD["oct_decode"]["cases"]:
+        assert np.allclose(oracle_mod.oct_decode(*uv), d, atol=1e-15)
+
+
+def test_oct_roundtrip_and_pixel_centres(oracle_mod):
+    rng = np.random.default_rng(4)
+    for _ in range(2000):
+        d = rng.standard_normal(3); d /= np.linalg.norm(d)
+        assert np.abs(oracle_mod.oct_decode(*oracle_mod.oct_encode(d)) - d).max() < 1e-12
+    g = GOLD["pixel_centers_W2"]
+    for col, u in enumerate(g["u_cols"]):
+        d = oracle_mod.texel_dir(0, col, 2, 2)
+        assert np.allclose(oracle_mod.oct_encode(d)[0], u, atol=1e-15)
+    assert oracle_mod.bin_center(GOLD["bin_center"]["k"], GOLD["bin_center"]["K"],
+                                 GOLD["bin_center"]["t_max"]) == GOLD["bin_center"]["value"]
+    assert oracle_mod.bin_center(3, 4, 4.0) == 4.0 - 4.0 / 8
+
+
+def test_footprint_centre_is_pixel_of_direction(oracle_mod):
+    """pixel -> direction -> footprint centre pixel is the identity."""
+    for res in (8, 64):
+        for row, col in [(0, 0), (3, 5), (res - 1, 0), (res // 2, res // 2 - 1), (res - 1, res - 1)]:
+            d = oracle_mod.texel_dir(row, col, res, res)
+            f = oracle_mod.footprint(3.0 * d, [0.05] * 3, [1, 0, 0, 0], [0, 0, 0], res)
+            assert abs(f["px"] - col) < 1e-5 and abs(f["py"] - row) < 1e-5
+
+
+def test_mirror_wrap_is_the_octahedral_seam(oracle_mod):
+    """Q8/Q12: the mirror-wrap neighbour of a border texel is its angular
+    neighbour on the sphere (about one texel pitch), which the naive clamp is not."""
+    res = 32
+    pitch = 2 * math.pi / (2 * res)  # nominal angular pitch ~ 2pi / (H+W)
+    for j in range(res):
+        for (c, r, c2, r2) in [(res - 1, j, res, j), (0, j, -1, j), (j, 0, j, -1), (j, res - 1, j, res)]:
+            a = oracle_mod.texel_dir(r, c, res, res)
+            cw, rw = oracle_mod.mirror_wrap(c2, r2, res, res)
+            b = oracle_mod.texel_dir(rw, cw, res, res)
+            ang = math.acos(max(-1.0, min(1.0, float(a @ b))))
+            assert ang < 1.6 * pitch, (c, r, c2, r2, ang / pitch)
+    # corner: diagonal neighbour beyond (-1,-1) is the opposite corner (all corners = south pole)
+    assert oracle_mod.mirror_wrap(-1, -1, res, res) == (res - 1, res - 1)
+
+
+# ------------------------------------------------------------- footprint
+def test_footprint_isotropic_closed_form(oracle_mod):
+    """isotropic s at distance D -> p1 = k_sigma * s/D * rho, rho=(H+W)/(2 pi);
+    doubling D halves p1."""
+    for res in (64, 512):
+        for D in (1.0, 2.0, 7.5):
+            f = oracle_mod.footprint([0, 0, D], [0.1] * 3, [1, 0, 0, 0], [0, 0, 0], res)
+            rho = 2 * res / (2 * math.pi)
+            assert math.isclose(f["p1"], 3.0 * float(np.float32(0.1)) / D * rho, rel_tol=1e-12)
+        f1 = oracle_mod.footprint([1, 2, 2.0], [0.1, 0.05, 0.2], [0.9, 0.1, 0.3, 0.2], [0, 0, 0], res)
+        f2 = oracle_mod.footprint([2, 4, 4.0], [0.1, 0.05, 0.2], [0.9, 0.1, 0.3, 0.2], [0, 0, 0], res)
+        assert math.isclose(f1["p1"], 2 * f2["p1"], rel_tol=1e-12)
+
+
+def test_footprint_eigenvalue_vs_explicit_basis(oracle_mod):
+    """R5's basis-free lambda1 == largest eigenvalue of [u v]^T Sigma [u v]
+    computed with an explicit tangent basis and numpy.linalg.eigvalsh."""
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        s = np.exp(rng.uniform(-5, -1, 3)).astype(np.float32)
+        q = synth.random_quaternions(rng, 1)[0].astype(np.float32)
+        mu = (rng.standard_normal(3) * 3).astype(np.float32)
+        f = oracle_mod.footprint(mu, s, q, [0, 0, 0], 64)
+        R = synth.quaternion_to_matrix(q[None].astype(np.float64))[0]
+        Sig = R @ np.diag(s.astype(np.float64) ** 2) @ R.T
+        d = mu.astype(np.float64) / np.linalg.norm(mu.astype(np.float64))
+        a = np.array([1.0, 0, 0]) if abs(d[0]) < 0.9 else np.array([0, 1.0, 0])
+        u = np.cross(d, a); u /= np.linalg.norm(u)
+        v = np.cross(d, u)
+        B = np.stack([u, v], 1)
+        lam = np.linalg.eigvalsh(B.T @ Sig @ B)
+        assert math.isclose(f["lam1"], lam[-1], rel_tol=1e-9, abs_tol=1e-18)
+    # an axis along d vanishes: scales (1, 0.1, 0.2) with the big axis along +z
+    f = oracle_mod.footprint([0, 0, 5.0], [0.1, 0.2, 1.0], [1, 0, 0, 0], [0, 0, 0], 64)
+    assert math.isclose(f["lam1"], float(np.float32(0.2)) ** 2, rel_tol=1e-9)
+
+
+def test_exclusion_at_light(oracle_mod):
+    assert oracle_mod.footprint([1, 1, 1], [0.1] * 3, [1, 0, 0, 0], [1, 1, 1], 64) is None
+
+
+# --------------------------------------------------------------- binning
+def _inverse_images(c, r, H, W):
+    """All extended-lattice points mapping to grid texel (c, r) under the
+    mirror-wrap (inverting each region of R6/R10 separately)."""
+    return [(c, r), (-1 - c, H - 1 - r), (2 * W - 1 - c, H - 1 - r), (W - 1 - c, -1 - r),
+            (W - 1 - c, 2 * H - 1 - r), (c - W, r - H), (c - W, r + H), (c + W, r - H), (c + W, r + H)]
+
+
+def _brute_tiles(f, res, wrap=True):
+    """Tiles containing a grid texel that is the image of a lattice point inside the
+    closed square [px-p1,px+p1]^2 clamped to [-W,2W-1]^2 (R6), by brute force."""
+    px, py, p1 = f["px"], f["py"], f["p1"]
+    tiles = set()
+    for r in range(res):
+        for c in range(res):
+            pre = _inverse_images(c, r, res, res) if wrap else [(c, r)]
+            for (x, y) in pre:
+                if -res <= x <= 2 * res - 1 and -res <= y <= 2 * res - 1 and \
+                        px - p1 <= x <= px + p1 and py - p1 <= y <= py + p1:
+                    tiles.add((r // 8) * (res // 8) + c // 8)
+                    break
+    return tiles
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+@pytest.mark.parametrize("mode", ["wrap", "clamp"])
+def test_binning_brute_force(oracle_mod, seed, mode):
+    res = 32
+    sc = synth.random_scene(seed, 60, res=res, dist=(0.4, 3.0), scale=(0.02, 0.6))
+    g = sc.gaussians
+    lights = sc.lights["position"]
+    L_, T_, D_, I_ = oracle_mod.bin_entries(g["means"], g["scales"], g["rotations"], lights, res,
+                                            bin_mode=oracle_mod.BIN_WRAP if mode == "wrap" else oracle_mod.BIN_CLAMP)
+    # sorted by (light, tile, depth bits, index)
+    key = np.stack([L_, T_, D_, I_], 1).astype(np.int64)
+    assert np.all(np.diff(key[:, 0] * 2**40 + key[:, 1] * 2**32 + key[:, 2]) >= 0)
+    got = {}
+    for l, t, d, i in zip(L_, T_, D_, I_):
+        got.setdefault(int(i), set()).add(int(t))
+        assert (l, i) not in [] and True
+    for i in range(g["means"].shape[0]):
+        f = oracle_mod.footprint(g["means"][i], g["scales"][i], g["rotations"][i], lights[0], res)
+        want = _brute_tiles(f, res, wrap=(mode == "wrap")) if f else set()
+        assert got.get(i, set()) == want, i
+        if f:
+            sel = I_ == i
+            assert np.all(D_[sel] == np.float32(f["D"]).view(np.uint32))
+
+
+def test_binning_counts_simple(oracle_mod):
+    """a footprint inside one tile -> 1 entry; spanning 2x2 tiles -> 4."""
+    res = 64
+    d = oracle_mod.texel_dir(11, 11, res, res)  # texel (11,11): tile (1,1), 3 texels from the edges
+    g = dict(means=[3.0 * d], scales=[[0.005] * 3], rotations=[[1, 0, 0, 0]])
+    _, T_, _, _ = oracle_mod.bin_entries(g["means"], g["scales"], g["rotations"], [[0, 0, 0]], res)
+    assert list(T_) == [1 * 8 + 1]
+    d = oracle_mod.texel_dir(15, 15, res, res)  # on the corner shared by 4 tiles
+    g = dict(means=[3.0 * d], scales=[[0.06] * 3], rotations=[[1, 0, 0, 0]])
+    _, T_, _, _ = oracle_mod.bin_entries(g["means"], g["scales"], g["rotations"], [[0, 0, 0]], res)
+    assert sorted(T_) == [9, 10, 17, 18]
+
+
+# ----------------------------------------------------------------- build
+def test_single_isotropic_on_axis_closed_form(oracle_mod):
+    """Eq.3-5 for an isotropic Gaussian on the ray: tau(t) = kappa tau*/2 [erf((t-D)/(s sqrt2)) + erf(D/(s sqrt2))],
+    T(D) = (1-alpha)^(kappa/2), T(inf) = (1-alpha)^kappa."""
+    g0 = GOLD["isotropic_on_axis"]
+    g = dict(means=[[0, 0, g0["D"]]], scales=[[g0["s"]] * 3], rotations=[[1, 0, 0, 0]], opacities=[g0["alpha"]])
+    for t, want in ((g0["D"], g0["T_at_D"]), (10.0, g0["T_at_10"])):
+        T = math.exp(-oracle_mod.tau_ray(g, [0, 0, 0], [0, 0, 1], t))
+        assert round(T, g0["digits"]) == pytest.approx(want, abs=1e-7)
+    # through the full culled build: occluder centred on a texel direction
+    res, K, tmax = 32, 16, 6.0
+    d = oracle_mod.texel_dir(9, 20, res, res)
+    for kappa in (1.0, 2.0):
+        g = dict(means=[2.5 * d], scales=[[0.05] * 3], rotations=[[1, 0, 0, 0]], opacities=[0.6])
+        T, P = oracle_mod.build(g, dict(position=[[0, 0, 0]], t_max=[tmax]), res, K, kappa=kappa)
+        mu = np.float32(2.5 * d).astype(np.float64)
+        D = np.linalg.norm(mu)
+        s = float(np.float32(0.05))
+        tstar = -math.log1p(-float(np.float32(0.6)))
+        for k in range(K):
+            tk = (k + 0.5) * tmax / K
+            # ray direction = texel direction; closest approach parameter = d.mu
+            sc = float(d @ mu)
+            r2 = float(mu @ mu - sc * sc) / (s * s)
+            tau = kappa * tstar / 2 * math.exp(-0.5 * r2) * (math.erf((tk - sc) / (s * math.sqrt(2))) + math.erf(sc / (s * math.sqrt(2))))
+            assert abs(T[0, k, 9, 20] - math.exp(-tau)) < 1e-12
+
+
+def test_build_vs_quadrature(oracle_mod):
+    """Atlas texels == exp(-quadrature of the mixture density along the texel ray)
+    (Eq.1-4), unculled, random 16-Gaussian mixture, incl. anisotropic
+    Gaussians with condition numbers up to 1e4."""
+    from scipy.integrate import quad
+    rng = np.random.default_rng(6)
+    n = 16
+    mu = np.stack([rng.uniform(-0.4, 0.4, n), rng.uniform(-0.4, 0.4, n), rng.uniform(1, 3, n)], 1)
+    s = np.exp(rng.uniform(np.log(0.01), np.log(0.3), (n, 3)))
+    s[0] = [0.3, 0.003, 0.01]  # condition number 1e4 in covariance
+    q = synth.random_quaternions(rng, n)
+    al = rng.uniform(0.1, 0.9, n)
+    g = {k: np.asarray(v, np.float32) for k, v in dict(means=mu, scales=s, rotations=q, opacities=al).items()}
+    res, K, tmax = 16, 8, 4.0
+    T, _ = oracle_mod.build(g, dict(position=[[0, 0, 0]], t_max=[tmax]), res, K, culled=False)
+    R = synth.quaternion_to_matrix(g["rotations"].astype(np.float64))
+    A = np.einsum("nij,nj,nkj->nik", R, 1.0 / g["scales"].astype(np.float64) ** 2, R)
+    betas = np.array([oracle_mod.beta(g["scales"][i], g["rotations"][i], g["opacities"][i]) for i in range(n)])
+    M = g["means"].astype(np.float64)
+    for (row, col) in [(8, 8), (7, 8), (6, 9), (9, 6), (8, 7)]:
+        d = oracle_mod.texel_dir(row, col, res, res)
+
+        def sigma(t):
+            x = t * d - M
+            return float(np.sum(betas * np.exp(-0.5 * np.einsum("ni,nij,nj->n", x, A, x))))
+        brk = sorted(set(float(np.clip(d @ m, 0, tmax)) for m in M))
+        for k in range(K):
+            tk = (k + 0.5) * tmax / K
+            pts = [p for p in brk if 0 < p < tk]
+            tau = quad(sigma, 0, tk, points=pts or None, limit=400, epsabs=1e-13, epsrel=1e-11)[0]
+            assert abs(T[0, k, row, col] - math.exp(-tau)) <= 1e-8 * (1 + tau), (row, col, k)
+
+
+@pytest.fixture(scope="module")
+def cfg1_atlases(oracle_mod):
+    s = synth.config1()
+    Tc, P = oracle_mod.build(s.gaussians, s.lights, s.res, s.K)
+    Tu, _ = oracle_mod.build(s.gaussians, s.lights, s.res, s.K, culled=False)
+    return s, Tc, Tu, P
+
+
+def test_build_invariants(oracle_mod, cfg1_atlases):
+    s, Tc, Tu, P = cfg1_atlases
+    for T in (Tc, Tu):
+        assert np.all(T > 0) and np.all(T <= 1)
+        assert np.all(np.diff(T, axis=1) <= 1e-15)  # non-increasing along k
+    assert np.all(Tc >= Tu - 1e-15)                 # culling only drops occluders
+    assert P > 0
+    # empty scene -> T == 1 exactly
+    e = {k: v[:0] for k, v in s.gaussians.items()}
+    T0, P0 = oracle_mod.build(e, s.lights, s.res, s.K)
+    assert P0 == 0 and np.all(T0 == 1.0)
+
+
+def test_build_duplication_and_kappa(oracle_mod):
+    s = synth.random_scene(3, 40, res=16, K=8)
+    T1, _ = oracle_mod.build(s.gaussians, s.lights, s.res, s.K)
+    g2 = synth.concat_gaussians(s.gaussians, s.gaussians)
+    T2, _ = oracle_mod.build(g2, s.lights, s.res, s.K)
+    Tk, _ = oracle_mod.build(s.gaussians, s.lights, s.res, s.K, kappa=2.0)
+    assert np.abs(T2 - T1 ** 2).max() < 1e-12
+    assert np.abs(Tk - T1 ** 2).max() < 1e-12
+
+
+def test_culling_gap_conservative_rho(oracle_mod, cfg1_atlases):
+    """Culling error pinned to our own unculled mode only ("parity unpinned
+    against the paper"): with rho_scale 2.6 the gap is < 1e-4; with the
+    paper's rho it is a reported metric (~1e-2)."""
+    s, Tc, Tu, _ = cfg1_atlases
+    Tr, _ = oracle_mod.build(s.gaussians, s.lights, s.res, s.K, rho_scale=2.6)
+    assert np.abs(Tr - Tu).max() < 1e-4
+    assert 1e-4 < np.abs(Tc - Tu).max() < 0.1
+
+
+def test_rotation_equivariance_unculled(oracle_mod):
+    """(x,y,z)->(-y,x,z) about the light maps (u,v)->(-v,u): texel (col,row) ->
+    (W-1-row, col) for square atlases (SURVEY §8(c) pins)."""
+    s = synth.config1()
+    sub = {k: v[:250] for k, v in s.gaussians.items()}
+    s = synth.Scene("c", sub, s.lights, 32, 8, s.queries)
+    R = np.array([[0, -1.0, 0], [1.0, 0, 0], [0, 0, 1.0]])
+    s2 = synth.rotate_scene(s, R)
+    T1, _ = oracle_mod.build(s.gaussians, s.lights, s.res, s.K, culled=False)
+    T2, _ = oracle_mod.build(s2.gaussians, s2.lights, s.res, s.K, culled=False)
+    W = s.res
+    rows, cols = np.meshgrid(np.arange(W), np.arange(W), indexing="ij")
+    assert np.abs(T2[:, :, cols, W - 1 - rows] - T1).max() < 2e-5
+
+
+# ----------------------------------------------------------------- query
+def test_query_constant_and_centres(oracle_mod):
+    L, K, res = 2, 4, 16
+    lights = dict(position=np.array([[0, 0, 0], [1, 0, 0.5]], np.float32), t_max=np.array([4.0, 5.0], np.float32))
+    x = synth.random_queries(0, lights, 500, 6.0)
+    assert np.allclose(oracle_mod.query(np.full((L, K, res, res), 0.5), lights, x), 0.25, atol=1e-15)
+    at = synth.random_atlas(0, 1, K, res).astype(np.float64)
+    l1 = dict(position=lights["position"][:1], t_max=lights["t_max"][:1])
+    for (row, col, k) in [(0, 0, 0), (5, 9, 2), (15, 15, 3), (7, 0, 1)]:
+        d = oracle_mod.texel_dir(row, col, res, res)
+        t = (k + 0.5) * 4.0 / K
+        v = oracle_mod.query(at, l1, (t * d)[None])[0]
+        assert abs(v - at[0, k, row, col]) < 1e-6
+    assert oracle_mod.query(at, l1, np.zeros((1, 3)))[0] == 1.0  # at the light (Q18)
+
+
+def test_query_analytic_field(oracle_mod):
+    """a tabulated exp(-t/t_max) is reproduced within the linear
+    interpolation bound; t outside [t_0, t_{K-1}] is clamped."""
+    K, res, tmax = 16, 32, 4.0
+    tk = (np.arange(K) + 0.5) * tmax / K
+    at = np.broadcast_to(np.exp(-tk / tmax)[None, :, None, None], (1, K, res, res)).copy()
+    lights = dict(position=np.zeros((1, 3), np.float32), t_max=np.array([tmax], np.float32))
+    x = synth.random_queries(1, lights, 2000, tmax * 1.2)
+    t = np.linalg.norm(x.astype(np.float64), axis=1)
+    v = oracle_mod.query(at, lights, x)
+    tc = np.clip(t, tk[0], tk[-1])
+    bound = (tmax / K) ** 2 / 8 / tmax ** 2  # |f''| h^2/8
+    assert np.abs(v - np.exp(-tc / tmax)).max() <= bound + 1e-12
+
+
+def test_query_seam_continuity(oracle_mod):
+    """Sampling a smooth direction field across the atlas border is continuous
+    (the octahedral map 'avoids inter-face seams')."""
+    res, K = 64, 2
+    at = np.zeros((1, K, res, res))
+    for r in range(res):
+        for c in range(res):
+            d = oracle_mod.texel_dir(r, c, res, res)
+            at[0, :, r, c] = 0.5 + 0.4 * d[0] - 0.3 * d[1] + 0.2 * d[2]
+    lights = dict(position=np.zeros((1, 3), np.float32), t_max=np.array([4.0], np.float32))
+    rng = np.random.default_rng(7)
+    for _ in range(200):
+        d = rng.standard_normal(3)
+        # push onto the equator / x=0 / y=0 seams region
+        d[rng.integers(0, 3)] *= 1e-3
+        d /= np.linalg.norm(d)
+        v = oracle_mod.query(at, lights, (2.0 * d)[None])[0]
+        assert abs(v - (0.5 + 0.4 * d[0] - 0.3 * d[1] + 0.2 * d[2])) < 0.02
