@@ -1,0 +1,178 @@
+/*
+ * dgsm.h — C ABI of libdgsm.so, the B200-native (sm_100a) Deep Gaussian Shadow
+ * Map build + query of arXiv 2601.01660.
+ *
+ * Citations "P:L<n>" are PAPER.md lines (§3.2 build, §3.3 sampling);
+ * "Q<n>"/"R<n>" are the readings listed in DESIGN.md.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Device pointers are CUDA global-memory addresses in the caller's current
+ *    context; host pointers are plain process memory.  Every buffer is
+ *    caller-owned: the library never allocates or frees device memory and keeps
+ *    no pointer after the call's stream work has completed.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    All work is enqueued on it; only dgsm_build_plan synchronises it (once, to
+ *    read the key count P back to the host).
+ *  - Functions are re-entrant; concurrent calls on different streams need
+ *    different workspaces.
+ *  - Return value: DGSM_OK (0) or a positive DGSM_E* code; dgsm_last_error()
+ *    returns a thread-local message for the last failure on this thread.
+ *    Arguments are validated before any work is enqueued.  A CUDA launch or
+ *    runtime error yields DGSM_ECUDA (the stream may then hold partial work).
+ *    Data errors (non-finite means, scales <= 0) are not checked: the results
+ *    for such Gaussians are unspecified.  Opacities outside [1e-4, 1-1e-4] are
+ *    clamped (Q16), not rejected.
+ */
+#ifndef DGSM_H
+#define DGSM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define DGSM_OK 0
+#define DGSM_EINVAL 1   /* null pointer, n<0, atlas_res%8!=0 or <8 or >2048, n_shells<1 or >DGSM_MAX_SHELLS,
+                           n_lights outside [1, DGSM_MAX_LIGHTS], t_max<=0, bad opts, plan/run mismatch */
+#define DGSM_ENOSPC 2   /* workspace smaller than required (required size is returned) */
+#define DGSM_ECUDA 3    /* CUDA launch/runtime error */
+#define DGSM_ERANGE 4   /* problem too large: > 2^30 keys for one light, or > 2^32-1 keys in total */
+
+#define DGSM_MAX_LIGHTS 64
+#define DGSM_MAX_SHELLS 256
+
+/* ---- binning mode (R6, Q8) ---------------------------------------------- */
+#define DGSM_BIN_WRAP 0   /* default: footprints crossing the atlas border are mirror-wrapped
+                             onto the octahedral neighbours (the seam rule of the query, Q12) */
+#define DGSM_BIN_CLAMP 1  /* 3DGS getRect semantics: the square is intersected with the grid */
+
+/* ---- build flags --------------------------------------------------------- */
+#define DGSM_OUTPUT_TAU 1u /* write optical depth tau (Eq.2) instead of T = exp(-tau) (Eq.4);
+                              used by Gaussian-sharded multi-GPU builds before the reduce-scatter */
+
+/* Occluder Gaussians, structure of arrays, DEVICE pointers (mean mu_i,
+ * covariance Sigma_i = R diag(s^2) R^T, precision A_i = Sigma_i^-1, opacity alpha_i). */
+typedef struct dgsm_gaussians {
+    const float* means;     /* [n][3] world metres */
+    const float* scales;    /* [n][3] per-axis standard deviations s (activated, > 0) */
+    const float* rotations; /* [n][4] quaternion (w, x, y, z), any norm > 0 (normalised in fp64) */
+    const float* opacities; /* [n] alpha in (0,1), clamped to [1e-4, 1-1e-4] */
+    int64_t n;              /* number of Gaussians, >= 0 (n = 0 gives T == 1 exactly) */
+} dgsm_gaussians_t;
+
+/* Point light o_L and the radial range of its atlas: shells
+ * t_k = (k + 1/2) t_max / K.  HOST memory. */
+typedef struct dgsm_light {
+    float position[3]; /* o_L, world metres */
+    float t_max;       /* > 0, metres (Q2) */
+} dgsm_light_t;
+
+/* Build options.  dgsm_default_opts() gives the paper's setting. */
+typedef struct dgsm_build_opts {
+    float kappa;       /* Eq.5 global strength knob, default 1 (Q15); > 0 */
+    float k_sigma;     /* footprint k_sigma rule, default 3 (Q6); > 0 */
+    float rho_scale;   /* multiplies rho = (H+W)/(2 pi) pixels per radian, default 1 (Q5); > 0 */
+    int32_t bin_mode;  /* DGSM_BIN_WRAP (default) or DGSM_BIN_CLAMP */
+    uint32_t flags;    /* DGSM_OUTPUT_TAU or 0 */
+} dgsm_build_opts_t;
+
+/* Host-side plan: filled by dgsm_build_plan, consumed by dgsm_build_run.
+ * Caller-owned plain struct; treat the fields as read-only. */
+typedef struct dgsm_plan {
+    int64_t n;
+    int32_t n_lights, atlas_res, n_shells, chunk;
+    int64_t n_keys;                                /* P = total (light, Gaussian, tile) keys */
+    int64_t light_key_begin[DGSM_MAX_LIGHTS + 1];  /* per-light key segment [begin, begin') */
+    uint32_t depth_min[DGSM_MAX_LIGHTS];           /* fp32 bit patterns of min/max D per light */
+    uint32_t depth_max[DGSM_MAX_LIGHTS];
+    int32_t depth_bits[DGSM_MAX_LIGHTS];           /* key bits used for (D bits - depth_min) */
+    int32_t tile_bits;
+    size_t run_workspace_bytes;                    /* size dgsm_build_run needs */
+    uint64_t signature;                            /* ties a plan to its arguments */
+} dgsm_plan_t;
+
+/* Fill opts with the defaults: kappa=1, k_sigma=3, rho_scale=1, WRAP, flags=0. */
+void dgsm_default_opts(dgsm_build_opts_t* opts);
+
+/* Size in bytes of the plan workspace for n Gaussians and n_lights lights
+ * (per-(light, Gaussian) footprint records, tile counts and their scan). */
+size_t dgsm_plan_workspace_bytes(int64_t n, int n_lights);
+
+/* DGSM build, step 1: per (light, Gaussian) calibration (Eq.5,
+ * P:L128-136), light-space footprint and its 8x8 tile count;
+ * exclusive scan of the counts.  Synchronises `stream` once to read P back.
+ *   g, lights[n_lights]   occluders (device) and lights (host)
+ *   atlas_res             H = W = atlas_res texels, multiple of 8, 8..2048
+ *   n_shells              K radial shells, 1..DGSM_MAX_SHELLS
+ *   opts                  NULL = defaults
+ *   plan_ws               device, >= dgsm_plan_workspace_bytes(n, n_lights) bytes, 256-B aligned;
+ *                         must stay untouched until dgsm_build_run has been enqueued
+ *   plan                  host, filled on success (plan->run_workspace_bytes is the run size) */
+int dgsm_build_plan(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_lights,
+                    int atlas_res, int n_shells, const dgsm_build_opts_t* opts, void* plan_ws,
+                    size_t plan_ws_bytes, dgsm_plan_t* plan, void* stream);
+
+/* DGSM build, step 2 (Eq.2-4): key duplication into (tile, light
+ * distance) pairs, onesweep radix sort, per-tile ranges, per-tile accumulation
+ * of Eq.3 over K shells and T = exp(-tau).  Same g/lights/opts as the plan.
+ *   run_ws     device, >= plan->run_workspace_bytes, 256-B aligned, scratch
+ *   atlas_out  device float [n_lights][n_shells][atlas_res][atlas_res], k-major then
+ *              row-major (row = v, col = u; Q3); fully overwritten with T (or tau). */
+int dgsm_build_run(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_lights,
+                   const dgsm_build_opts_t* opts, const dgsm_plan_t* plan, void* plan_ws,
+                   size_t plan_ws_bytes, void* run_ws, size_t run_ws_bytes, float* atlas_out,
+                   void* stream);
+
+/* Binning only (a3-a5 of the build, for inspection and tests): runs the key
+ * duplication, the onesweep sort and the tile ranges of dgsm_build_run, then
+ * decodes the sorted keys.  Outputs (device, caller-owned):
+ *   light_out, tile_out, depth_bits_out, index_out   uint32 [plan->n_keys]: entry j of the
+ *       ascending (light, tile, fp32 bits of D, Gaussian index) order (R7); tile = row-major
+ *       8x8 tile index ty*(res/8)+tx
+ *   tile_start_out, tile_end_out   uint32 [n_lights*(res/8)^2] or NULL: [start, end) of each
+ *       (light, tile) in that order (0, 0 for an empty tile) */
+int dgsm_build_bins(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_lights,
+                    const dgsm_build_opts_t* opts, const dgsm_plan_t* plan, void* plan_ws,
+                    size_t plan_ws_bytes, void* run_ws, size_t run_ws_bytes, uint32_t* light_out,
+                    uint32_t* tile_out, uint32_t* depth_bits_out, uint32_t* index_out,
+                    uint32_t* tile_start_out, uint32_t* tile_end_out, void* stream);
+
+/* Convenience: plan + run with one caller workspace `ws` laid out as
+ * [plan workspace | run workspace].  If ws_bytes is too small, returns
+ * DGSM_ENOSPC and stores the required size in *ws_required (after the plan
+ * step, so the call synchronises the stream either way). */
+int dgsm_build(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_lights,
+               int atlas_res, int n_shells, const dgsm_build_opts_t* opts, void* ws,
+               size_t ws_bytes, size_t* ws_required, float* atlas_out, void* stream);
+
+/* T = exp(-tau) elementwise (Eq.4), in place allowed (tau == T). Device pointers. */
+int dgsm_exp_epilogue(const float* tau, float* T, int64_t count, void* stream);
+
+/* DGSM sampling: for each receiver x_q (device [m][3]),
+ *   T_out[q] = prod_l trilinear(atlas_l, psi(x_q - o_l), |x_q - o_l|)
+ * octahedral bilinear with mirror-wrapped taps (Q12) x radial linear with t
+ * clamped to [t_0, t_{K-1}]; T_l = 1 at the light itself (Q18); product over
+ * lights (Q13).  If colors_inout (device [m][3]) is not NULL it is multiplied
+ * by T_out in place ("multiply the direct term").
+ *   atlas  device float [n_lights][n_shells][atlas_res][atlas_res] (as written by dgsm_build_run)
+ *   T_out  device float [m] */
+int dgsm_query(const float* atlas, const dgsm_light_t* lights, int n_lights, int atlas_res,
+               int n_shells, const float* positions, int64_t m, float* T_out, float* colors_inout,
+               void* stream);
+
+/* Message for a status code / for the last failure on the calling thread. */
+const char* dgsm_strerror(int code);
+const char* dgsm_last_error(void);
+
+/* Number of kernel launches enqueued by the last dgsm_build_run / dgsm_query /
+ * dgsm_exp_epilogue on the calling thread (for the benchmark's gpu_launches). */
+int dgsm_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DGSM_H */

@@ -79,6 +79,12 @@ def _p(a, ct):
     return a.ctypes.data_as(C.POINTER(ct))
 
 
+def _opt(x) -> float:
+    """Build options are fp32 quantities in the problem statement's C ABI
+    (kappa, k_sigma, rho_scale); the oracle takes the same fp32 values."""
+    return float(np.float32(x))
+
+
 BIN_WRAP, BIN_CLAMP = 0, 1
 
 
@@ -117,7 +123,7 @@ def footprint(mean, scales, rotation, light, res, k_sigma=3.0, rho_scale=1.0):
     fpv = np.zeros(5)
     rect = np.zeros(4, dtype=np.int64)
     ok = lib().or_footprint(_p(mu, C.c_float), _p(s, C.c_float), _p(q, C.c_float),
-                            _p(o, C.c_float), int(res), float(k_sigma), float(rho_scale),
+                            _p(o, C.c_float), int(res), _opt(k_sigma), _opt(rho_scale),
                             _p(fpv, C.c_double), _p(rect, C.c_int64))
     if not ok:
         return None
@@ -136,7 +142,7 @@ def bin_entries(means, scales, rotations, light_pos, res, k_sigma=3.0, rho_scale
     mu, s, q, lp = _f32(means), _f32(scales), _f32(rotations), _f32(light_pos)
     n, L = mu.shape[0], lp.reshape(-1, 3).shape[0]
     args = [_p(mu, C.c_float), _p(s, C.c_float), _p(q, C.c_float), n, _p(lp, C.c_float), L,
-            int(res), float(k_sigma), float(rho_scale), int(bin_mode)]
+            int(res), _opt(k_sigma), _opt(rho_scale), int(bin_mode)]
     P = lib().or_bin(*args, None, None, None, None, 0)
     outs = [np.zeros(max(P, 1), dtype=np.uint32) for _ in range(4)]
     lib().or_bin(*args, *[_p(o, C.c_uint32) for o in outs], P)
@@ -177,7 +183,7 @@ def build(g, lights, res, K, kappa=1.0, k_sigma=3.0, rho_scale=1.0, bin_mode=BIN
     n_threads = n_threads or os.cpu_count() or 1
     P = lib().or_build(_p(mu, C.c_float), _p(s, C.c_float), _p(q, C.c_float), _p(a, C.c_float),
                        mu.shape[0], _p(lp, C.c_float), _p(tm, C.c_float), L, int(res), int(K),
-                       float(kappa), float(k_sigma), float(rho_scale), int(bin_mode),
+                       _opt(kappa), _opt(k_sigma), _opt(rho_scale), int(bin_mode),
                        int(bool(culled)), int(tile_stride), int(n_threads), _p(T, C.c_double))
     if P < 0:
         raise ValueError("oracle build: invalid arguments")

@@ -1,0 +1,384 @@
+// dgsm_api.cu — the C ABI of include/dgsm.h: argument validation, workspace
+// layout (caller-owned memory only), stream-ordered launches, error strings.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "dgsm_internal.cuh"
+
+using namespace dgsm;
+
+namespace {
+thread_local char g_err[512] = "";
+thread_local int g_launches = 0;
+
+int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int cuda_check(const char* where) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(DGSM_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+    return DGSM_OK;
+}
+
+constexpr size_t kAlign = 256;
+constexpr int kChunk = 1024;  // Gaussians per accumulation work unit
+
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Carver {
+    char* base;
+    size_t off = 0;
+    explicit Carver(void* b) : base((char*)b) {}
+    template <typename T>
+    T* take(size_t count) {
+        T* p = base ? (T*)(base + off) : nullptr;
+        off += align_up(sizeof(T) * (count ? count : 1));
+        return p;
+    }
+};
+
+struct PlanLayout {
+    PairRec* recs;
+    uint32_t* counts;
+    uint64_t* offsets;
+    void* scan_temp;
+    PlanStats* stats;
+    size_t bytes;
+};
+
+PlanLayout plan_layout(void* ws, int64_t n, int L) {
+    Carver c(ws);
+    PlanLayout p;
+    const int64_t m = (int64_t)L * n;
+    p.recs = c.take<PairRec>(m);
+    p.counts = c.take<uint32_t>(m);
+    p.offsets = c.take<uint64_t>(m + 1);
+    p.scan_temp = c.take<char>(scan_u32_to_u64_temp_bytes(m));
+    p.stats = c.take<PlanStats>(1);
+    p.bytes = c.off;
+    return p;
+}
+
+struct RunLayout {
+    uint64_t *keys_a, *keys_b;
+    uint32_t *vals_a, *vals_b;
+    void* sort_temp;
+    uint32_t *tile_start, *tile_end;
+    uint64_t *unit_cnt, *unit_off;
+    void* unit_scan_temp;
+    WorkUnit* units;
+    uint32_t* counters;  // [0] n_units, [1] unit counter
+    uint32_t* tile_arrive;
+    float* scratch;
+    size_t bytes;
+    uint32_t max_units;
+};
+
+RunLayout run_layout(void* ws, const dgsm_plan_t& pl) {
+    Carver c(ws);
+    RunLayout r;
+    const int64_t P = pl.n_keys;
+    int64_t pmax = 0;
+    for (int l = 0; l < pl.n_lights; ++l)
+        pmax = std::max<int64_t>(pmax, pl.light_key_begin[l + 1] - pl.light_key_begin[l]);
+    const int64_t nt = (int64_t)pl.n_lights * (pl.atlas_res / kTile) * (pl.atlas_res / kTile);
+    r.keys_a = c.take<uint64_t>(P);
+    r.keys_b = c.take<uint64_t>(P);
+    r.vals_a = c.take<uint32_t>(P);
+    r.vals_b = c.take<uint32_t>(P);
+    r.sort_temp = c.take<char>(onesweep_temp_bytes(pmax));
+    r.tile_start = c.take<uint32_t>(nt);
+    r.tile_end = c.take<uint32_t>(nt);
+    r.unit_cnt = c.take<uint64_t>(nt);
+    r.unit_off = c.take<uint64_t>(nt + 1);
+    r.unit_scan_temp = c.take<char>(scan_u32_to_u64_temp_bytes(nt));
+    const int64_t max_units = nt + P / pl.chunk + 1;
+    r.max_units = (uint32_t)max_units;
+    r.units = c.take<WorkUnit>(max_units);
+    r.counters = c.take<uint32_t>(64);
+    r.tile_arrive = c.take<uint32_t>(nt);
+    const int64_t max_slots = 2 * (P / pl.chunk) + 1;
+    r.scratch = c.take<float>((size_t)max_slots * pl.n_shells * kTexels);
+    r.bytes = c.off;
+    return r;
+}
+
+int bits_for(uint64_t v) {  // bits needed to represent 0..v
+    int b = 0;
+    while (b < 64 && (v >> b) != 0) ++b;
+    return b;
+}
+
+uint64_t signature(const dgsm_gaussians_t* g, int L, int res, int K, const dgsm_build_opts_t& o,
+                   const dgsm_light_t* lights) {
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](const void* p, size_t n) {
+        const unsigned char* b = (const unsigned char*)p;
+        for (size_t i = 0; i < n; ++i) { h ^= b[i]; h *= 1099511628211ull; }
+    };
+    mix(&g->n, sizeof(g->n));
+    mix(&g->means, sizeof(void*) * 4);
+    mix(&L, sizeof(L)); mix(&res, sizeof(res)); mix(&K, sizeof(K));
+    mix(&o, sizeof(o));
+    mix(lights, sizeof(dgsm_light_t) * (size_t)L);
+    return h;
+}
+
+int validate(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int L, int res, int K,
+             const dgsm_build_opts_t& o) {
+    if (!g || !lights) return fail(DGSM_EINVAL, "null gaussians or lights");
+    if (g->n < 0) return fail(DGSM_EINVAL, "n < 0");
+    if (g->n > 0 && (!g->means || !g->scales || !g->rotations || !g->opacities))
+        return fail(DGSM_EINVAL, "null Gaussian array");
+    if (g->n >= (int64_t)1 << 32) return fail(DGSM_ERANGE, "n >= 2^32");
+    if (L < 1 || L > DGSM_MAX_LIGHTS) return fail(DGSM_EINVAL, "n_lights %d outside [1, %d]", L, DGSM_MAX_LIGHTS);
+    if (res < 8 || res % 8 != 0 || res > 2048) return fail(DGSM_EINVAL, "atlas_res %d: need 8..2048, multiple of 8", res);
+    if (K < 1 || K > DGSM_MAX_SHELLS) return fail(DGSM_EINVAL, "n_shells %d outside [1, %d]", K, DGSM_MAX_SHELLS);
+    for (int l = 0; l < L; ++l)
+        if (!(lights[l].t_max > 0.0f)) return fail(DGSM_EINVAL, "light %d: t_max <= 0", l);
+    if (!(o.kappa > 0.0f) || !(o.k_sigma > 0.0f) || !(o.rho_scale > 0.0f))
+        return fail(DGSM_EINVAL, "kappa, k_sigma, rho_scale must be > 0");
+    if (o.bin_mode != DGSM_BIN_WRAP && o.bin_mode != DGSM_BIN_CLAMP) return fail(DGSM_EINVAL, "bad bin_mode");
+    if (o.flags & ~DGSM_OUTPUT_TAU) return fail(DGSM_EINVAL, "unknown flags");
+    return DGSM_OK;
+}
+
+LightsParam lights_param(const dgsm_light_t* lights, int L) {
+    LightsParam lp;
+    memset(&lp, 0, sizeof(lp));
+    for (int l = 0; l < L; ++l)
+        lp.l[l] = make_float4(lights[l].position[0], lights[l].position[1], lights[l].position[2],
+                              lights[l].t_max);
+    return lp;
+}
+}  // namespace
+
+extern "C" {
+
+void dgsm_default_opts(dgsm_build_opts_t* o) {
+    if (!o) return;
+    o->kappa = 1.0f;
+    o->k_sigma = 3.0f;
+    o->rho_scale = 1.0f;
+    o->bin_mode = DGSM_BIN_WRAP;
+    o->flags = 0u;
+}
+
+size_t dgsm_plan_workspace_bytes(int64_t n, int n_lights) {
+    if (n < 0 || n_lights < 1) return 0;
+    return plan_layout(nullptr, n, n_lights).bytes;
+}
+
+int dgsm_build_plan(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_lights, int atlas_res,
+                    int n_shells, const dgsm_build_opts_t* opts, void* plan_ws, size_t plan_ws_bytes,
+                    dgsm_plan_t* plan, void* stream) {
+    g_launches = 0;
+    dgsm_build_opts_t o;
+    if (opts) o = *opts; else dgsm_default_opts(&o);
+    int rc = validate(g, lights, n_lights, atlas_res, n_shells, o);
+    if (rc) return rc;
+    if (!plan || !plan_ws) return fail(DGSM_EINVAL, "null plan or plan workspace");
+    if ((uintptr_t)plan_ws % kAlign) return fail(DGSM_EINVAL, "plan workspace not 256-B aligned");
+    const size_t need = plan_layout(nullptr, g->n, n_lights).bytes;
+    if (plan_ws_bytes < need) return fail(DGSM_ENOSPC, "plan workspace %zu < %zu bytes", plan_ws_bytes, need);
+    cudaStream_t s = (cudaStream_t)stream;
+    PlanLayout p = plan_layout(plan_ws, g->n, n_lights);
+    const LightsParam lp = lights_param(lights, n_lights);
+    const int64_t m = (int64_t)n_lights * g->n;
+
+    launch_project(*g, lp, n_lights, atlas_res, n_shells, o, p.recs, p.counts, p.stats, s);
+    launch_scan_u32_to_u64(p.counts, p.offsets, m, p.scan_temp, s);
+    launch_plan_stats(p.offsets, g->n, n_lights, p.stats, s);
+    g_launches += 6;
+    if ((rc = cuda_check("plan launch"))) return rc;
+    PlanStats hs;
+    cudaMemcpyAsync(&hs, p.stats, sizeof(PlanStats), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_check("plan sync");
+
+    memset(plan, 0, sizeof(*plan));
+    plan->n = g->n;
+    plan->n_lights = n_lights;
+    plan->atlas_res = atlas_res;
+    plan->n_shells = n_shells;
+    plan->chunk = kChunk;
+    plan->n_keys = (int64_t)hs.light_key_begin[n_lights];
+    const int64_t n_tiles = (int64_t)(atlas_res / kTile) * (atlas_res / kTile);
+    plan->tile_bits = bits_for((uint64_t)(n_tiles - 1));
+    for (int l = 0; l <= n_lights; ++l) plan->light_key_begin[l] = (int64_t)hs.light_key_begin[l];
+    for (int l = 0; l < n_lights; ++l) {
+        const int64_t pl = plan->light_key_begin[l + 1] - plan->light_key_begin[l];
+        if (pl >= ((int64_t)1 << 30)) return fail(DGSM_ERANGE, "light %d has %lld keys (>= 2^30)", l, (long long)pl);
+        plan->depth_min[l] = pl ? hs.depth_min[l] : 0u;
+        plan->depth_max[l] = pl ? hs.depth_max[l] : 0u;
+        plan->depth_bits[l] = pl ? bits_for((uint64_t)(hs.depth_max[l] - hs.depth_min[l])) : 0;
+    }
+    if (plan->n_keys >= ((int64_t)1 << 32) - 1) return fail(DGSM_ERANGE, "%lld keys (>= 2^32)", (long long)plan->n_keys);
+    plan->run_workspace_bytes = run_layout(nullptr, *plan).bytes;
+    plan->signature = signature(g, n_lights, atlas_res, n_shells, o, lights);
+    return DGSM_OK;
+}
+
+static int check_run_args(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_lights,
+                          const dgsm_build_opts_t& o, const dgsm_plan_t* plan, void* plan_ws,
+                          size_t plan_ws_bytes, void* run_ws, size_t run_ws_bytes) {
+    if (!plan) return fail(DGSM_EINVAL, "null plan");
+    int rc = validate(g, lights, n_lights, plan->atlas_res, plan->n_shells, o);
+    if (rc) return rc;
+    if (plan->signature != signature(g, n_lights, plan->atlas_res, plan->n_shells, o, lights))
+        return fail(DGSM_EINVAL, "plan does not match these arguments");
+    if (!plan_ws) return fail(DGSM_EINVAL, "null plan workspace");
+    if (plan_ws_bytes < plan_layout(nullptr, g->n, n_lights).bytes) return fail(DGSM_ENOSPC, "plan workspace too small");
+    if (plan->run_workspace_bytes > 0 && (!run_ws || run_ws_bytes < plan->run_workspace_bytes))
+        return fail(DGSM_ENOSPC, "run workspace %zu < %zu bytes", run_ws_bytes, plan->run_workspace_bytes);
+    if ((uintptr_t)run_ws % kAlign) return fail(DGSM_EINVAL, "run workspace not 256-B aligned");
+    return DGSM_OK;
+}
+
+// a3-a5: duplicate, onesweep per light, ranges.  Sorted result in keys_a/vals_a.
+static void run_binning(const dgsm_gaussians_t* g, int n_lights, const dgsm_build_opts_t& o,
+                        const dgsm_plan_t* plan, const PlanLayout& p, const RunLayout& r, cudaStream_t s) {
+    const int res = plan->atlas_res;
+    const int64_t n_tiles = (int64_t)(res / kTile) * (res / kTile);
+    const int64_t nt = n_lights * n_tiles;
+    launch_duplicate(p.recs, p.counts, p.offsets, g->n, n_lights, res, o.bin_mode, *plan, r.keys_a, r.vals_a, s);
+    g_launches += 1;
+    for (int l = 0; l < n_lights; ++l) {
+        const int64_t b = plan->light_key_begin[l], e = plan->light_key_begin[l + 1];
+        if (e - b < 2) continue;
+        const int nbits = plan->tile_bits + plan->depth_bits[l];
+        const int flipped = launch_onesweep(r.keys_a + b, r.vals_a + b, r.keys_b + b, r.vals_b + b, e - b,
+                                            nbits, r.sort_temp, s, &g_launches);
+        if (flipped) {
+            cudaMemcpyAsync(r.keys_a + b, r.keys_b + b, sizeof(uint64_t) * (e - b), cudaMemcpyDeviceToDevice, s);
+            cudaMemcpyAsync(r.vals_a + b, r.vals_b + b, sizeof(uint32_t) * (e - b), cudaMemcpyDeviceToDevice, s);
+        }
+    }
+    cudaMemsetAsync(r.tile_start, 0, sizeof(uint32_t) * nt, s);
+    cudaMemsetAsync(r.tile_end, 0, sizeof(uint32_t) * nt, s);
+    for (int l = 0; l < n_lights; ++l) {
+        launch_ranges(r.keys_a, plan->light_key_begin[l], plan->light_key_begin[l + 1], plan->depth_bits[l],
+                      (uint32_t)(l * n_tiles), r.tile_start, r.tile_end, s);
+        g_launches += 1;
+    }
+}
+
+int dgsm_build_run(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_lights,
+                   const dgsm_build_opts_t* opts, const dgsm_plan_t* plan, void* plan_ws,
+                   size_t plan_ws_bytes, void* run_ws, size_t run_ws_bytes, float* atlas_out, void* stream) {
+    g_launches = 0;
+    dgsm_build_opts_t o;
+    if (opts) o = *opts; else dgsm_default_opts(&o);
+    int rc = check_run_args(g, lights, n_lights, o, plan, plan_ws, plan_ws_bytes, run_ws, run_ws_bytes);
+    if (rc) return rc;
+    if (!atlas_out) return fail(DGSM_EINVAL, "null atlas");
+    cudaStream_t s = (cudaStream_t)stream;
+    const PlanLayout p = plan_layout(plan_ws, g->n, n_lights);
+    const RunLayout r = run_layout(run_ws, *plan);
+    const LightsParam lp = lights_param(lights, n_lights);
+    const int res = plan->atlas_res, K = plan->n_shells;
+    const int64_t nt = n_lights * (int64_t)(res / kTile) * (res / kTile);
+
+    run_binning(g, n_lights, o, plan, p, r, s);
+    launch_units(r.tile_start, r.tile_end, nt, plan->chunk, r.unit_cnt, r.unit_off, r.unit_scan_temp, r.units,
+                 r.counters, s, &g_launches);
+    cudaMemsetAsync(r.counters + 1, 0, sizeof(uint32_t), s);
+    cudaMemsetAsync(r.tile_arrive, 0, sizeof(uint32_t) * nt, s);
+    // a6: accumulate + exp
+    launch_accumulate(r.units, r.counters, r.max_units, r.vals_a, p.recs, g->n, lp, n_lights, res, K, o.flags,
+                      r.scratch, r.tile_arrive, r.counters + 1, atlas_out, s);
+    g_launches += 1;
+    return cuda_check("build run");
+}
+
+int dgsm_build_bins(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_lights,
+                    const dgsm_build_opts_t* opts, const dgsm_plan_t* plan, void* plan_ws,
+                    size_t plan_ws_bytes, void* run_ws, size_t run_ws_bytes, uint32_t* light_out,
+                    uint32_t* tile_out, uint32_t* depth_bits_out, uint32_t* index_out,
+                    uint32_t* tile_start_out, uint32_t* tile_end_out, void* stream) {
+    g_launches = 0;
+    dgsm_build_opts_t o;
+    if (opts) o = *opts; else dgsm_default_opts(&o);
+    int rc = check_run_args(g, lights, n_lights, o, plan, plan_ws, plan_ws_bytes, run_ws, run_ws_bytes);
+    if (rc) return rc;
+    if (plan->n_keys > 0 && (!light_out || !tile_out || !depth_bits_out || !index_out))
+        return fail(DGSM_EINVAL, "null output array");
+    cudaStream_t s = (cudaStream_t)stream;
+    const PlanLayout p = plan_layout(plan_ws, g->n, n_lights);
+    const RunLayout r = run_layout(run_ws, *plan);
+    const int res = plan->atlas_res;
+    const int64_t nt = n_lights * (int64_t)(res / kTile) * (res / kTile);
+    run_binning(g, n_lights, o, plan, p, r, s);
+    launch_decode_keys(r.keys_a, r.vals_a, *plan, light_out, tile_out, depth_bits_out, index_out, s);
+    g_launches += 1;
+    if (tile_start_out) cudaMemcpyAsync(tile_start_out, r.tile_start, sizeof(uint32_t) * nt, cudaMemcpyDeviceToDevice, s);
+    if (tile_end_out) cudaMemcpyAsync(tile_end_out, r.tile_end, sizeof(uint32_t) * nt, cudaMemcpyDeviceToDevice, s);
+    return cuda_check("build bins");
+}
+
+int dgsm_build(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_lights, int atlas_res,
+               int n_shells, const dgsm_build_opts_t* opts, void* ws, size_t ws_bytes, size_t* ws_required,
+               float* atlas_out, void* stream) {
+    if (!g) return fail(DGSM_EINVAL, "null gaussians");
+    const size_t pb = dgsm_plan_workspace_bytes(g->n, n_lights);
+    if (ws_bytes < pb) {
+        if (ws_required) *ws_required = pb;
+        return fail(DGSM_ENOSPC, "workspace %zu < plan size %zu", ws_bytes, pb);
+    }
+    dgsm_plan_t plan;
+    int rc = dgsm_build_plan(g, lights, n_lights, atlas_res, n_shells, opts, ws, pb, &plan, stream);
+    if (rc) return rc;
+    const size_t need = pb + plan.run_workspace_bytes;
+    if (ws_required) *ws_required = need;
+    if (ws_bytes < need) return fail(DGSM_ENOSPC, "workspace %zu < %zu bytes", ws_bytes, need);
+    return dgsm_build_run(g, lights, n_lights, opts, &plan, ws, pb, (char*)ws + pb, ws_bytes - pb, atlas_out,
+                          stream);
+}
+
+int dgsm_exp_epilogue(const float* tau, float* T, int64_t count, void* stream) {
+    g_launches = 0;
+    if (count < 0) return fail(DGSM_EINVAL, "count < 0");
+    if (count > 0 && (!tau || !T)) return fail(DGSM_EINVAL, "null tau or T");
+    launch_exp(tau, T, count, (cudaStream_t)stream);
+    g_launches = count > 0 ? 1 : 0;
+    return cuda_check("exp epilogue");
+}
+
+int dgsm_query(const float* atlas, const dgsm_light_t* lights, int n_lights, int atlas_res, int n_shells,
+               const float* positions, int64_t m, float* T_out, float* colors_inout, void* stream) {
+    g_launches = 0;
+    if (!lights) return fail(DGSM_EINVAL, "null lights");
+    if (n_lights < 1 || n_lights > DGSM_MAX_LIGHTS) return fail(DGSM_EINVAL, "n_lights %d outside [1, %d]", n_lights, DGSM_MAX_LIGHTS);
+    if (atlas_res < 8 || atlas_res % 8 != 0 || atlas_res > 2048) return fail(DGSM_EINVAL, "bad atlas_res %d", atlas_res);
+    if (n_shells < 1 || n_shells > DGSM_MAX_SHELLS) return fail(DGSM_EINVAL, "bad n_shells %d", n_shells);
+    if (m < 0) return fail(DGSM_EINVAL, "m < 0");
+    if (m > 0 && (!atlas || !positions || !T_out)) return fail(DGSM_EINVAL, "null atlas, positions or T_out");
+    for (int l = 0; l < n_lights; ++l)
+        if (!(lights[l].t_max > 0.0f)) return fail(DGSM_EINVAL, "light %d: t_max <= 0", l);
+    const LightsParam lp = lights_param(lights, n_lights);
+    launch_query(atlas, lp, n_lights, atlas_res, n_shells, positions, m, T_out, colors_inout, (cudaStream_t)stream);
+    g_launches = m > 0 ? 1 : 0;
+    return cuda_check("query");
+}
+
+const char* dgsm_strerror(int code) {
+    switch (code) {
+        case DGSM_OK: return "success";
+        case DGSM_EINVAL: return "invalid argument";
+        case DGSM_ENOSPC: return "workspace too small";
+        case DGSM_ECUDA: return "CUDA error";
+        case DGSM_ERANGE: return "problem too large";
+        default: return "unknown error";
+    }
+}
+
+const char* dgsm_last_error(void) { return g_err; }
+
+int dgsm_last_launch_count(void) { return g_launches; }
+
+}  // extern "C"

@@ -1,0 +1,155 @@
+// dgsm_internal.cuh — internal layouts and launch helpers of libdgsm.so.
+// Nothing here is shared with oracle/ (which has its own independent code).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/dgsm.h"
+
+namespace dgsm {
+
+constexpr int kTile = 8;             // 8x8 atlas tiles
+constexpr int kTexels = kTile * kTile;
+
+// Per-(light, Gaussian) footprint record written by the projection kernel and
+// gathered (by TMA bulk copy) into shared memory by the accumulation kernel.
+// 96 B = 6 x 16 B; array base is 256-B aligned so every record is 32-B aligned.
+struct __align__(16) PairRec {
+    double di[3];     // d_i = (mu - o)/D in fp64: the delta-formulation anchor (R9)
+    float g[3];       // g = W d_i, W = diag(1/s) R^T (whitening: A = W^T W)
+    float W[9];       // row-major W
+    float D;          // |mu - o| (its fp32 bits are the depth key)
+    float eD;         // t_{kD} - D (fp64 -> fp32), anchors the shell arguments
+    int32_t kD;       // anchor shell
+    float betap;      // beta * sqrt(pi/2) = kappa tau* sqrt(tr A / 3) / 2  (Eq.3 x Eq.5)
+    int16_t c0, c1, r0, r1;  // clamped integer texel range of the footprint square (R6)
+};
+static_assert(sizeof(PairRec) == 96, "PairRec must be 96 B");
+
+struct LightsParam {
+    float4 l[DGSM_MAX_LIGHTS];  // xyz = o_L, w = t_max
+};
+
+// Device-side statistics of a plan, copied back to the host once.
+struct PlanStats {
+    uint32_t depth_min[DGSM_MAX_LIGHTS];
+    uint32_t depth_max[DGSM_MAX_LIGHTS];
+    uint64_t light_key_begin[DGSM_MAX_LIGHTS + 1];
+};
+
+// Work unit of the accumulation kernel: one chunk of one (light, tile) list.
+struct __align__(16) WorkUnit {
+    uint32_t tile;      // l * n_tiles + tile
+    uint32_t jbeg, jend;  // [jbeg, jend) into the sorted (key, value) arrays
+    uint32_t chunk;     // chunk index within the tile
+    uint32_t nchunks;   // chunks of this tile (1 = write T directly)
+    uint32_t slot;      // scratch slot of chunk 0 (multi-chunk tiles only)
+    uint32_t pad0, pad1;
+};
+
+// Region decomposition of the clamped footprint square on the extended lattice
+// [-W, 2W-1]^2 into at most 9 pieces, each mapped by the mirror-wrap rule
+// (R6/R10) onto a rectangle of tiles.  Integer-only: shared by the projection
+// (tile count) and duplication (key emission) kernels so both enumerate the
+// same tile set in the same order.
+struct TileRects {
+    int n;
+    int tx0[9], tx1[9], ty0[9], ty1[9];
+};
+
+__host__ __device__ inline void make_tile_rects(int c0, int c1, int r0, int r1, int res, int bin_mode,
+                                                TileRects& R) {
+    R.n = 0;
+    if (c0 > c1 || r0 > r1) return;
+    const int W = res, H = res;
+    if (bin_mode == DGSM_BIN_CLAMP) {
+        int a = c0 < 0 ? 0 : c0, b = c1 > W - 1 ? W - 1 : c1;
+        int c = r0 < 0 ? 0 : r0, d = r1 > H - 1 ? H - 1 : r1;
+        if (a > b || c > d) return;
+        R.tx0[0] = a >> 3; R.tx1[0] = b >> 3; R.ty0[0] = c >> 3; R.ty1[0] = d >> 3;
+        R.n = 1;
+        return;
+    }
+    // column regions: 0 = in-grid, 1 = left (<0), 2 = right (>W-1); rows: 0 in, 1 top (<0), 2 bottom (>H-1)
+    int xa[3], xb[3], ya[3], yb[3];
+    xa[0] = c0 < 0 ? 0 : c0;       xb[0] = c1 > W - 1 ? W - 1 : c1;
+    xa[1] = c0;                    xb[1] = c1 < -1 ? c1 : -1;
+    xa[2] = c0 > W ? c0 : W;       xb[2] = c1;
+    ya[0] = r0 < 0 ? 0 : r0;       yb[0] = r1 > H - 1 ? H - 1 : r1;
+    ya[1] = r0;                    yb[1] = r1 < -1 ? r1 : -1;
+    ya[2] = r0 > H ? r0 : H;       yb[2] = r1;
+    // fixed order: (in,in), then (x-overflow, in), (in, y-overflow), then corners
+    const int order[9][2] = {{0, 0}, {1, 0}, {2, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 1}, {2, 2}};
+    for (int o = 0; o < 9; ++o) {
+        int rx = order[o][0], ry = order[o][1];
+        int a = xa[rx], b = xb[rx], c = ya[ry], d = yb[ry];
+        if (a > b || c > d) continue;
+        int ma, mb, mc, md;  // mapped texel rectangle (inclusive)
+        if (rx == 0 && ry == 0) { ma = a; mb = b; mc = c; md = d; }
+        else if (ry == 0) {  // x overflow: col reflects, row flips
+            if (rx == 1) { ma = -1 - b; mb = -1 - a; } else { ma = 2 * W - 1 - b; mb = 2 * W - 1 - a; }
+            mc = H - 1 - d; md = H - 1 - c;
+        } else if (rx == 0) {  // y overflow: row reflects, col flips
+            if (ry == 1) { mc = -1 - d; md = -1 - c; } else { mc = 2 * H - 1 - d; md = 2 * H - 1 - c; }
+            ma = W - 1 - b; mb = W - 1 - a;
+        } else {  // corners: translation by (+-W, +-H)
+            int sx = rx == 1 ? W : -W, sy = ry == 1 ? H : -H;
+            ma = a + sx; mb = b + sx; mc = c + sy; md = d + sy;
+        }
+        R.tx0[R.n] = ma >> 3; R.tx1[R.n] = mb >> 3; R.ty0[R.n] = mc >> 3; R.ty1[R.n] = md >> 3;
+        R.n++;
+    }
+}
+
+__host__ __device__ inline bool in_earlier_rect(const TileRects& R, int j, int tx, int ty) {
+    for (int q = 0; q < j; ++q)
+        if (tx >= R.tx0[q] && tx <= R.tx1[q] && ty >= R.ty0[q] && ty <= R.ty1[q]) return true;
+    return false;
+}
+
+// Number of distinct tiles in the union of the rectangles.
+__host__ __device__ inline uint32_t count_tiles(const TileRects& R) {
+    if (R.n == 0) return 0;
+    uint32_t cnt = (uint32_t)(R.tx1[0] - R.tx0[0] + 1) * (uint32_t)(R.ty1[0] - R.ty0[0] + 1);
+    for (int j = 1; j < R.n; ++j)
+        for (int ty = R.ty0[j]; ty <= R.ty1[j]; ++ty)
+            for (int tx = R.tx0[j]; tx <= R.tx1[j]; ++tx)
+                if (!in_earlier_rect(R, j, tx, ty)) ++cnt;
+    return cnt;
+}
+
+}  // namespace dgsm
+
+// ---------------------------------------------------------------- kernels
+// (declared here, defined in the .cu files, launched from dgsm_api.cu)
+namespace dgsm {
+void launch_project(const dgsm_gaussians_t& g, const LightsParam& lp, int n_lights, int res, int K,
+                    const dgsm_build_opts_t& o, PairRec* recs, uint32_t* counts, PlanStats* stats,
+                    cudaStream_t s);
+size_t scan_u32_to_u64_temp_bytes(int64_t n);
+void launch_scan_u32_to_u64(const uint32_t* in, uint64_t* out, int64_t n, void* temp, cudaStream_t s);
+void launch_scan_u64(const uint64_t* in, uint64_t* out, int64_t n, void* temp, cudaStream_t s);
+void launch_plan_stats(const uint64_t* offsets, int64_t n, int n_lights, PlanStats* stats, cudaStream_t s);
+void launch_duplicate(const PairRec* recs, const uint32_t* counts, const uint64_t* offsets, int64_t n,
+                      int n_lights, int res, int bin_mode, const dgsm_plan_t& plan, uint64_t* keys,
+                      uint32_t* vals, cudaStream_t s);
+size_t onesweep_temp_bytes(int64_t n_max);
+// returns 1 if the sorted result ended in the *_alt buffers
+int launch_onesweep(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int64_t n,
+                    int nbits, void* temp, cudaStream_t s, int* launches);
+void launch_decode_keys(const uint64_t* keys, const uint32_t* vals, const dgsm_plan_t& plan, uint32_t* light_out,
+                        uint32_t* tile_out, uint32_t* depth_out, uint32_t* index_out, cudaStream_t s);
+void launch_ranges(const uint64_t* keys, int64_t begin, int64_t end, int depth_bits, uint32_t tile_base,
+                   uint32_t* tile_start, uint32_t* tile_end, cudaStream_t s);
+void launch_units(const uint32_t* tile_start, const uint32_t* tile_end, int64_t n_tiles_total, int chunk,
+                  uint64_t* unit_counts, uint64_t* unit_offsets, void* scan_temp, WorkUnit* units,
+                  uint32_t* n_units_dev, cudaStream_t s, int* launches);
+size_t accumulate_smem_bytes(int K);
+void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint32_t max_units,
+                       const uint32_t* vals, const PairRec* recs, int64_t n, const LightsParam& lp,
+                       int n_lights, int res, int K, uint32_t flags, float* scratch, uint32_t* tile_arrive,
+                       uint32_t* unit_counter, float* atlas, cudaStream_t s);
+void launch_exp(const float* tau, float* T, int64_t count, cudaStream_t s);
+void launch_query(const float* atlas, const LightsParam& lp, int n_lights, int res, int K,
+                  const float* positions, int64_t m, float* T_out, float* colors, cudaStream_t s);
+}  // namespace dgsm

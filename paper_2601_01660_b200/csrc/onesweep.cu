@@ -1,0 +1,228 @@
+// onesweep.cu — stable LSD radix sort of (u64 key, u32 value) pairs in the
+// "onesweep" style: one histogram pass over all digits, then ONE kernel per
+// 8-bit digit that ranks a 4096-key tile in shared memory (warp multi-split
+// via match.any), obtains its global digit offsets by decoupled look-back over
+// earlier tiles, and scatters through shared memory for coalesced writes.
+// Partition ids come from an atomic counter, so a CTA only ever waits on tiles
+// that are already running (forward progress without co-residency).
+//
+// Used per light segment on the keys (tile << depth_bits | depth); stability +
+// emission in ascending Gaussian index make the result the sort by
+// (tile, depth bits, Gaussian index) of DESIGN.md R7.
+#include "dgsm_internal.cuh"
+
+namespace dgsm {
+
+namespace {
+constexpr int kThreads = 256;
+constexpr int kItems = 16;
+constexpr int kTileKeys = kThreads * kItems;  // 4096
+constexpr int kRadix = 256;
+constexpr int kMaxPasses = 8;
+constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
+
+__global__ void __launch_bounds__(256) k_hist(const uint64_t* __restrict__ keys, int64_t n, int passes,
+                                              uint32_t* __restrict__ hist) {
+    __shared__ uint32_t sh[kMaxPasses][kRadix];
+    for (int t = threadIdx.x; t < kMaxPasses * kRadix; t += blockDim.x) (&sh[0][0])[t] = 0;
+    __syncthreads();
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = keys[j];
+        for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(k >> (8 * p)) & 255u], 1u);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < passes * kRadix; t += blockDim.x) {
+        const uint32_t c = (&sh[0][0])[t];
+        if (c) atomicAdd(&hist[t], c);
+    }
+}
+
+__device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t x, uint32_t* warp_sums) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) warp_sums[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t v = lane < kThreads / 32 ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        if (lane < kThreads / 32) warp_sums[lane] = v;
+    }
+    __syncthreads();
+    const uint32_t r = (wid ? warp_sums[wid - 1] : 0) + inc - x;
+    __syncthreads();
+    return r;
+}
+
+// Exclusive scan of each pass's 256-bin histogram, in place (one CTA per pass).
+__global__ void __launch_bounds__(256) k_hist_scan(uint32_t* hist) {
+    __shared__ uint32_t ws[kThreads / 32];
+    uint32_t* h = hist + blockIdx.x * kRadix;
+    const uint32_t v = h[threadIdx.x];
+    const uint32_t e = block_excl_scan_u32(v, ws);
+    h[threadIdx.x] = e;
+}
+
+__global__ void __launch_bounds__(kThreads) k_pass(const uint64_t* __restrict__ kin,
+                                                   const uint32_t* __restrict__ vin,
+                                                   uint64_t* __restrict__ kout,
+                                                   uint32_t* __restrict__ vout, int64_t n, int shift,
+                                                   const uint32_t* __restrict__ gofs,
+                                                   uint32_t* status, uint32_t* part_ctr) {
+    extern __shared__ __align__(16) unsigned char os_smem[];
+    uint64_t* s_keys = reinterpret_cast<uint64_t*>(os_smem);
+    uint32_t* s_vals = reinterpret_cast<uint32_t*>(os_smem + sizeof(uint64_t) * kTileKeys);
+    __shared__ uint32_t s_warp_hist[kThreads / 32][kRadix];
+    __shared__ uint32_t s_tile_start[kRadix];
+    __shared__ uint32_t s_global[kRadix];
+    __shared__ uint32_t s_ws[kThreads / 32];
+    __shared__ uint32_t s_part;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_part = atomicAdd(part_ctr, 1u);
+    for (int t = tid; t < (kThreads / 32) * kRadix; t += kThreads) (&s_warp_hist[0][0])[t] = 0;
+    __syncthreads();
+    const uint32_t part = s_part;
+    const int64_t base = (int64_t)part * kTileKeys + warp * (32 * kItems);
+
+    uint64_t k[kItems];
+    uint32_t v[kItems], dig[kItems], rank[kItems];
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+        const int64_t idx = base + j * 32 + lane;
+        const bool valid = idx < n;
+        k[j] = valid ? kin[idx] : 0ull;
+        v[j] = valid ? vin[idx] : 0u;
+        dig[j] = valid ? (uint32_t)((k[j] >> shift) & 255u) : 256u;
+    }
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+        const uint32_t d = dig[j];
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        uint32_t cnt = 0;
+        if (d < 256u) cnt = s_warp_hist[warp][d];
+        rank[j] = cnt + __popc(peers & lt);
+        __syncwarp();
+        if (d < 256u && lane == (__ffs(peers) - 1)) s_warp_hist[warp][d] = cnt + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+
+    // per digit: exclusive prefix over warps, tile total
+    const uint32_t d = tid;
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+        const uint32_t c = s_warp_hist[w][d];
+        s_warp_hist[w][d] = run;
+        run += c;
+    }
+    const uint32_t tile_count = run;
+
+    // decoupled look-back (one thread per digit)
+    volatile uint32_t* st = status;
+    if (part == 0) {
+        st[d] = kFlagInc | tile_count;
+        s_global[d] = gofs[d];
+    } else {
+        st[(size_t)part * kRadix + d] = kFlagAgg | tile_count;
+        uint32_t excl = 0;
+        int64_t q = (int64_t)part - 1;
+        while (true) {
+            const uint32_t s = st[(size_t)q * kRadix + d];
+            const uint32_t f = s & ~kValMask;
+            if (f == 0) continue;
+            excl += s & kValMask;
+            if (f == kFlagInc) break;
+            --q;
+        }
+        st[(size_t)part * kRadix + d] = kFlagInc | (excl + tile_count);
+        s_global[d] = gofs[d] + excl;
+    }
+    s_tile_start[d] = block_excl_scan_u32(tile_count, s_ws);
+    __syncthreads();
+
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+        if (dig[j] < 256u) {
+            const uint32_t pos = s_tile_start[dig[j]] + s_warp_hist[warp][dig[j]] + rank[j];
+            s_keys[pos] = k[j];
+            s_vals[pos] = v[j];
+        }
+    }
+    __syncthreads();
+    const int64_t rem = n - (int64_t)part * kTileKeys;
+    const int n_valid = rem < kTileKeys ? (int)rem : kTileKeys;
+    for (int x = tid; x < n_valid; x += kThreads) {
+        const uint64_t key = s_keys[x];
+        const uint32_t dd = (uint32_t)((key >> shift) & 255u);
+        const uint32_t o = s_global[dd] + (uint32_t)x - s_tile_start[dd];
+        kout[o] = key;
+        vout[o] = s_vals[x];
+    }
+}
+
+struct OnesweepTemp {
+    uint32_t* hist;      // [kMaxPasses][256]
+    uint32_t* part_ctr;  // [kMaxPasses]
+    uint32_t* status;    // [parts][256]
+};
+
+OnesweepTemp carve(void* temp, int64_t n_max) {
+    OnesweepTemp t;
+    char* p = (char*)temp;
+    t.hist = (uint32_t*)p; p += sizeof(uint32_t) * kMaxPasses * kRadix;
+    t.part_ctr = (uint32_t*)p; p += 256;
+    t.status = (uint32_t*)p;
+    (void)n_max;
+    return t;
+}
+}  // namespace
+
+size_t onesweep_temp_bytes(int64_t n_max) {
+    const int64_t parts = (n_max + kTileKeys - 1) / kTileKeys;
+    return sizeof(uint32_t) * kMaxPasses * kRadix + 256 + sizeof(uint32_t) * kRadix * (size_t)(parts + 1);
+}
+
+int launch_onesweep(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int64_t n,
+                    int nbits, void* temp, cudaStream_t s, int* launches) {
+    if (n <= 1 || nbits <= 0) return 0;
+    const int passes = (nbits + 7) / 8;
+    OnesweepTemp t = carve(temp, n);
+    static bool attr_set = false;
+    const int dyn = (int)(sizeof(uint64_t) + sizeof(uint32_t)) * kTileKeys;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+        attr_set = true;
+    }
+    cudaMemsetAsync(t.hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix + 256, s);
+    k_hist<<<148 * 4, 256, 0, s>>>(keys, n, passes, t.hist);
+    k_hist_scan<<<passes, 256, 0, s>>>(t.hist);
+    *launches += 2;
+    const int64_t parts = (n + kTileKeys - 1) / kTileKeys;
+    uint64_t *ki = keys, *ko = keys_alt;
+    uint32_t *vi = vals, *vo = vals_alt;
+    int flipped = 0;
+    for (int p = 0; p < passes; ++p) {
+        cudaMemsetAsync(t.status, 0, sizeof(uint32_t) * kRadix * (size_t)parts, s);
+        k_pass<<<(unsigned)parts, kThreads, dyn, s>>>(ki, vi, ko, vo, n, 8 * p, t.hist + p * kRadix,
+                                                     t.status, t.part_ctr + p);
+        *launches += 1;
+        uint64_t* tk = ki; ki = ko; ko = tk;
+        uint32_t* tv = vi; vi = vo; vo = tv;
+        flipped ^= 1;
+    }
+    return flipped;
+}
+
+}  // namespace dgsm

@@ -1,0 +1,142 @@
+// project.cu — N1: per (light, Gaussian) calibration + light-space footprint +
+// 8x8 tile count (§3.2, Eq.5 and P:L162-173).
+//
+// Compiled with -fmad=false: the binning decisions (tile rectangle, tile count,
+// depth key) are made in IEEE fp64 with the exact operation order of DESIGN.md's
+// "binning arithmetic contract" (R4-R6) so that they are bit-identical to any
+// implementation performing the same IEEE operations (the oracle is one).
+#include "dgsm_internal.cuh"
+
+namespace dgsm {
+
+namespace {
+constexpr double kPi = 3.141592653589793;
+
+__device__ __forceinline__ double sgn_pos(double x) { return x >= 0.0 ? 1.0 : -1.0; }  // sgn(0)=+1 (Q4)
+
+__global__ void __launch_bounds__(256) k_project(
+    const float* __restrict__ means, const float* __restrict__ scales,
+    const float* __restrict__ rotations, const float* __restrict__ opacities, int64_t n,
+    LightsParam lp, int n_lights, int res, int K, double kappa, double k_sigma, double rho_scale,
+    int bin_mode, PairRec* __restrict__ recs, uint32_t* __restrict__ counts, PlanStats* stats) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)n_lights * n) return;
+    const int l = (int)(idx / n);
+    const int64_t i = idx - (int64_t)l * n;
+    const float4 L = lp.l[l];
+    const int W = res, H = res;
+
+    // R4: m = mu - o, D = |m|; excluded when D <= 1e-6 (Q17)
+    const double mx = (double)means[3 * i] - (double)L.x;
+    const double my = (double)means[3 * i + 1] - (double)L.y;
+    const double mz = (double)means[3 * i + 2] - (double)L.z;
+    const double D = sqrt((mx * mx + my * my) + mz * mz);
+    uint32_t cnt = 0;
+    PairRec rec;
+    rec.c0 = 1; rec.c1 = 0; rec.r0 = 1; rec.r1 = 0;
+    if (D > 1e-6) {
+        // footprint centre: octahedral encode psi(m) -> texel coords (pixel centres, Q3)
+        const double n1 = (fabs(mx) + fabs(my)) + fabs(mz);
+        const double qx = mx / n1, qy = my / n1, qz = mz / n1;
+        double u, v;
+        if (qz >= 0.0) { u = qx; v = qy; }
+        else { u = sgn_pos(qx) * (1.0 - fabs(qy)); v = sgn_pos(qy) * (1.0 - fabs(qx)); }
+        const double px = (u + 1.0) * (0.5 * W) - 0.5;
+        const double py = (v + 1.0) * (0.5 * H) - 0.5;
+
+        // rotation from the quaternion (w,x,y,z), normalised in fp64
+        double qw = rotations[4 * i], qxr = rotations[4 * i + 1], qyr = rotations[4 * i + 2],
+               qzr = rotations[4 * i + 3];
+        const double qn = sqrt(((qw * qw + qxr * qxr) + qyr * qyr) + qzr * qzr);
+        qw = qw / qn; qxr = qxr / qn; qyr = qyr / qn; qzr = qzr / qn;
+        double R[3][3];
+        R[0][0] = 1.0 - 2.0 * (qyr * qyr + qzr * qzr);
+        R[0][1] = 2.0 * (qxr * qyr - qw * qzr);
+        R[0][2] = 2.0 * (qxr * qzr + qw * qyr);
+        R[1][0] = 2.0 * (qxr * qyr + qw * qzr);
+        R[1][1] = 1.0 - 2.0 * (qxr * qxr + qzr * qzr);
+        R[1][2] = 2.0 * (qyr * qzr - qw * qxr);
+        R[2][0] = 2.0 * (qxr * qzr - qw * qyr);
+        R[2][1] = 2.0 * (qyr * qzr + qw * qxr);
+        R[2][2] = 1.0 - 2.0 * (qxr * qxr + qyr * qyr);
+
+        // R5: lambda1 of Sigma_perp = [u v]^T Sigma [u v], basis-free form
+        const double dx = mx / D, dy = my / D, dz = mz / D;
+        double w[3], s2[3], s[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            w[j] = (R[0][j] * dx + R[1][j] * dy) + R[2][j] * dz;
+            s[j] = (double)scales[3 * i + j];
+            s2[j] = s[j] * s[j];
+        }
+        const double tr = (s2[0] * (1.0 - w[0] * w[0]) + s2[1] * (1.0 - w[1] * w[1])) +
+                          s2[2] * (1.0 - w[2] * w[2]);
+        const double det = ((s2[0] * s2[1]) * s2[2]) *
+                           (((w[0] * w[0]) / s2[0] + (w[1] * w[1]) / s2[1]) + (w[2] * w[2]) / s2[2]);
+        double disc = (tr * tr) * 0.25 - det;
+        if (disc < 0.0) disc = 0.0;
+        const double lam1 = tr * 0.5 + sqrt(disc);
+        const double rho = (rho_scale * (double)(H + W)) / (2.0 * kPi);  // P:L172 (Q5)
+        const double p1 = ((k_sigma * sqrt(lam1)) / D) * rho;
+
+        // R6: integer texel range of the closed square, clamped to [-W, 2W-1]
+        double c0 = ceil(px - p1), c1 = floor(px + p1), r0 = ceil(py - p1), r1 = floor(py + p1);
+        if (c0 < -(double)W) c0 = -(double)W;
+        if (c1 > 2.0 * W - 1.0) c1 = 2.0 * W - 1.0;
+        if (r0 < -(double)H) r0 = -(double)H;
+        if (r1 > 2.0 * H - 1.0) r1 = 2.0 * H - 1.0;
+        TileRects TR;
+        make_tile_rects((int)c0, (int)c1, (int)r0, (int)r1, res, bin_mode, TR);
+        cnt = count_tiles(TR);
+
+        if (cnt > 0) {
+            rec.c0 = (int16_t)c0; rec.c1 = (int16_t)c1; rec.r0 = (int16_t)r0; rec.r1 = (int16_t)r1;
+            rec.di[0] = dx; rec.di[1] = dy; rec.di[2] = dz;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                rec.g[j] = (float)(w[j] / s[j]);  // g = W d_i = diag(1/s) R^T d_i
+#pragma unroll
+                for (int c = 0; c < 3; ++c) rec.W[3 * j + c] = (float)(R[c][j] / s[j]);
+            }
+            const float Df = (float)D;
+            rec.D = Df;
+            const double dt = (double)L.w / K;
+            int kD = (int)(D / dt);
+            kD = kD < 0 ? 0 : (kD > K - 1 ? K - 1 : kD);
+            rec.kD = kD;
+            rec.eD = (float)((kD + 0.5) * dt - D);
+            // Eq.5 with the clamp of Q16; times sqrt(pi/2) from Eq.3's prefactor
+            double alpha = (double)opacities[i];
+            alpha = alpha < 1e-4 ? 1e-4 : (alpha > 1.0 - 1e-4 ? 1.0 - 1e-4 : alpha);
+            const double tau_star = -log1p(-alpha);
+            const double trA = 1.0 / s2[0] + 1.0 / s2[1] + 1.0 / s2[2];
+            rec.betap = (float)(kappa * tau_star * sqrt(trA / 3.0) * 0.5);
+            const uint32_t bits = __float_as_uint(Df);
+            atomicMin(&stats->depth_min[l], bits);
+            atomicMax(&stats->depth_max[l], bits);
+        }
+    }
+    counts[idx] = cnt;
+    recs[idx] = rec;
+}
+
+__global__ void k_init_stats(PlanStats* stats) {
+    int t = threadIdx.x;
+    if (t < DGSM_MAX_LIGHTS) { stats->depth_min[t] = 0xffffffffu; stats->depth_max[t] = 0u; }
+}
+}  // namespace
+
+void launch_project(const dgsm_gaussians_t& g, const LightsParam& lp, int n_lights, int res, int K,
+                    const dgsm_build_opts_t& o, PairRec* recs, uint32_t* counts, PlanStats* stats,
+                    cudaStream_t s) {
+    k_init_stats<<<1, DGSM_MAX_LIGHTS, 0, s>>>(stats);
+    const int64_t total = (int64_t)n_lights * g.n;
+    if (total == 0) return;
+    const int bs = 256;
+    const int64_t grid = (total + bs - 1) / bs;
+    k_project<<<(unsigned)grid, bs, 0, s>>>(g.means, g.scales, g.rotations, g.opacities, g.n, lp,
+                                            n_lights, res, K, (double)o.kappa, (double)o.k_sigma,
+                                            (double)o.rho_scale, o.bin_mode, recs, counts, stats);
+}
+
+}  // namespace dgsm

@@ -1,0 +1,297 @@
+"""Thin ctypes binding of libdgsm.so (include/dgsm.h).
+
+Argument marshalling only: every step of the DGSM build and query runs in the
+library's CUDA kernels.  PyTorch supplies device memory (the caching
+allocator), the current stream and nothing else.  There is no CPU fallback:
+if the extension is missing or the tensors are not on a CUDA device, the calls
+raise.
+
+    atlas = build(gaussians, lights, atlas_res=512, n_shells=64)     # [L,K,H,W] T
+    T = query(atlas, lights, positions)                               # [m]
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Dict, Optional, Sequence
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdgsm.so")
+
+DGSM_MAX_LIGHTS = 64
+DGSM_BIN_WRAP, DGSM_BIN_CLAMP = 0, 1
+DGSM_OUTPUT_TAU = 1
+_STATUS = {0: "DGSM_OK", 1: "DGSM_EINVAL", 2: "DGSM_ENOSPC", 3: "DGSM_ECUDA", 4: "DGSM_ERANGE"}
+
+EXPORTED = ["dgsm_default_opts", "dgsm_plan_workspace_bytes", "dgsm_build_plan", "dgsm_build_run",
+            "dgsm_build_bins", "dgsm_build", "dgsm_exp_epilogue", "dgsm_query", "dgsm_strerror",
+            "dgsm_last_error", "dgsm_last_launch_count"]
+
+
+class Gaussians(C.Structure):
+    _fields_ = [("means", C.c_void_p), ("scales", C.c_void_p), ("rotations", C.c_void_p),
+                ("opacities", C.c_void_p), ("n", C.c_int64)]
+
+
+class Light(C.Structure):
+    _fields_ = [("position", C.c_float * 3), ("t_max", C.c_float)]
+
+
+class BuildOpts(C.Structure):
+    _fields_ = [("kappa", C.c_float), ("k_sigma", C.c_float), ("rho_scale", C.c_float),
+                ("bin_mode", C.c_int32), ("flags", C.c_uint32)]
+
+
+class Plan(C.Structure):
+    _fields_ = [("n", C.c_int64), ("n_lights", C.c_int32), ("atlas_res", C.c_int32),
+                ("n_shells", C.c_int32), ("chunk", C.c_int32), ("n_keys", C.c_int64),
+                ("light_key_begin", C.c_int64 * (DGSM_MAX_LIGHTS + 1)),
+                ("depth_min", C.c_uint32 * DGSM_MAX_LIGHTS), ("depth_max", C.c_uint32 * DGSM_MAX_LIGHTS),
+                ("depth_bits", C.c_int32 * DGSM_MAX_LIGHTS), ("tile_bits", C.c_int32),
+                ("run_workspace_bytes", C.c_size_t), ("signature", C.c_uint64)]
+
+
+class DgsmError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libdgsm.so (built by paper_2601_01660_b200.build_ext).  Raises if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DgsmError(f"{LIB_PATH} not found: build it with `python -m paper_2601_01660_b200.build_ext` "
+                            "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, i64, sz = C.c_void_p, C.c_int64, C.c_size_t
+        P = C.POINTER
+        L.dgsm_default_opts.argtypes = [P(BuildOpts)]
+        L.dgsm_default_opts.restype = None
+        L.dgsm_plan_workspace_bytes.argtypes = [i64, C.c_int]
+        L.dgsm_plan_workspace_bytes.restype = sz
+        L.dgsm_build_plan.argtypes = [P(Gaussians), P(Light), C.c_int, C.c_int, C.c_int, P(BuildOpts),
+                                      vp, sz, P(Plan), vp]
+        L.dgsm_build_run.argtypes = [P(Gaussians), P(Light), C.c_int, P(BuildOpts), P(Plan), vp, sz, vp,
+                                     sz, vp, vp]
+        L.dgsm_build_bins.argtypes = [P(Gaussians), P(Light), C.c_int, P(BuildOpts), P(Plan), vp, sz, vp,
+                                      sz, vp, vp, vp, vp, vp, vp, vp]
+        L.dgsm_build.argtypes = [P(Gaussians), P(Light), C.c_int, C.c_int, C.c_int, P(BuildOpts), vp, sz,
+                                 P(sz), vp, vp]
+        L.dgsm_exp_epilogue.argtypes = [vp, vp, i64, vp]
+        L.dgsm_query.argtypes = [vp, P(Light), C.c_int, C.c_int, C.c_int, vp, i64, vp, vp, vp]
+        L.dgsm_strerror.argtypes = [C.c_int]
+        L.dgsm_strerror.restype = C.c_char_p
+        L.dgsm_last_error.argtypes = []
+        L.dgsm_last_error.restype = C.c_char_p
+        L.dgsm_last_launch_count.argtypes = []
+        L.dgsm_last_launch_count.restype = C.c_int
+        for f in ("dgsm_build_plan", "dgsm_build_run", "dgsm_build_bins", "dgsm_build",
+                  "dgsm_exp_epilogue", "dgsm_query"):
+            getattr(L, f).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        msg = lib().dgsm_last_error().decode(errors="replace")
+        raise DgsmError(f"{what}: {_STATUS.get(rc, rc)}: {msg}")
+
+
+def last_launch_count() -> int:
+    return int(lib().dgsm_last_launch_count())
+
+
+# ----------------------------------------------------------------- helpers
+def _dev_f32(t: torch.Tensor, name: str, shape_tail) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise DgsmError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != torch.float32:
+        raise DgsmError(f"{name} must be float32")
+    if tuple(t.shape[1:]) != tuple(shape_tail):
+        raise DgsmError(f"{name} has shape {tuple(t.shape)}, expected [n, {shape_tail}]")
+    return t.contiguous()
+
+
+def _gaussians(g: Dict[str, torch.Tensor]):
+    m = _dev_f32(g["means"], "means", (3,))
+    s = _dev_f32(g["scales"], "scales", (3,))
+    q = _dev_f32(g["rotations"], "rotations", (4,))
+    a = g["opacities"]
+    if a.dim() == 2:
+        a = a.reshape(-1)
+    a = _dev_f32(a, "opacities", ())
+    n = m.shape[0]
+    if not (s.shape[0] == q.shape[0] == a.shape[0] == n):
+        raise DgsmError("Gaussian arrays disagree on n")
+    keep = (m, s, q, a)
+    return Gaussians(m.data_ptr(), s.data_ptr(), q.data_ptr(), a.data_ptr(), n), keep
+
+
+def lights_array(lights) -> np.ndarray:
+    """lights: dict(position [L,3], t_max [L]) or array [L,4] (x, y, z, t_max)."""
+    if isinstance(lights, dict):
+        pos = np.asarray(lights["position"], np.float32).reshape(-1, 3)
+        tm = np.asarray(lights["t_max"], np.float32).reshape(-1)
+        return np.concatenate([pos, tm[:, None]], 1).astype(np.float32)
+    a = np.asarray(lights, np.float32)
+    return a.reshape(-1, 4)
+
+
+def _lights(lights):
+    a = lights_array(lights)
+    L = a.shape[0]
+    if not 1 <= L <= DGSM_MAX_LIGHTS:
+        raise DgsmError(f"n_lights={L} outside [1, {DGSM_MAX_LIGHTS}]")
+    arr = (Light * L)()
+    for l in range(L):
+        arr[l].position[0], arr[l].position[1], arr[l].position[2] = (float(x) for x in a[l, :3])
+        arr[l].t_max = float(a[l, 3])
+    return arr, L
+
+
+@dataclass
+class Options:
+    """Build options (include/dgsm.h dgsm_build_opts_t)."""
+    kappa: float = 1.0
+    k_sigma: float = 3.0
+    rho_scale: float = 1.0
+    bin_mode: str = "wrap"
+    output_tau: bool = False
+
+    def c(self) -> BuildOpts:
+        return BuildOpts(self.kappa, self.k_sigma, self.rho_scale,
+                         DGSM_BIN_WRAP if self.bin_mode == "wrap" else DGSM_BIN_CLAMP,
+                         DGSM_OUTPUT_TAU if self.output_tau else 0)
+
+
+def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _alloc(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+class BuildPlan:
+    """Result of dgsm_build_plan: keeps the device workspace and the host plan."""
+
+    def __init__(self, gaussians, lights, atlas_res: int, n_shells: int, opts: Optional[Options] = None,
+                 stream=None):
+        self.opts = opts or Options()
+        self._g, self._keep = _gaussians(gaussians)
+        self._lights, self.n_lights = _lights(lights)
+        self._opts_c = self.opts.c()
+        self.device = self._keep[0].device
+        self.atlas_res, self.n_shells = int(atlas_res), int(n_shells)
+        nbytes = lib().dgsm_plan_workspace_bytes(self._g.n, self.n_lights)
+        self.plan_ws = _alloc(nbytes, self.device)
+        self.plan = Plan()
+        rc = lib().dgsm_build_plan(C.byref(self._g), self._lights, self.n_lights, self.atlas_res,
+                                   self.n_shells, C.byref(self._opts_c), C.c_void_p(self.plan_ws.data_ptr()),
+                                   self.plan_ws.numel(), C.byref(self.plan), C.c_void_p(_stream_ptr(stream)))
+        _check(rc, "dgsm_build_plan")
+        self.plan_launches = last_launch_count()
+        self.run_ws = None
+
+    @property
+    def n_keys(self) -> int:
+        return int(self.plan.n_keys)
+
+    def light_key_ranges(self):
+        return [(int(self.plan.light_key_begin[l]), int(self.plan.light_key_begin[l + 1]))
+                for l in range(self.n_lights)]
+
+    def _ensure_run_ws(self):
+        need = int(self.plan.run_workspace_bytes)
+        if self.run_ws is None or self.run_ws.numel() < need:
+            self.run_ws = _alloc(need, self.device)
+        return self.run_ws
+
+    def run(self, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        shape = (self.n_lights, self.n_shells, self.atlas_res, self.atlas_res)
+        if out is None:
+            out = torch.empty(shape, dtype=torch.float32, device=self.device)
+        elif tuple(out.shape) != shape or out.dtype != torch.float32 or not out.is_contiguous():
+            raise DgsmError(f"out must be contiguous float32 {shape}")
+        ws = self._ensure_run_ws()
+        rc = lib().dgsm_build_run(C.byref(self._g), self._lights, self.n_lights, C.byref(self._opts_c),
+                                  C.byref(self.plan), C.c_void_p(self.plan_ws.data_ptr()), self.plan_ws.numel(),
+                                  C.c_void_p(ws.data_ptr()), ws.numel(), C.c_void_p(out.data_ptr()),
+                                  C.c_void_p(_stream_ptr(stream)))
+        _check(rc, "dgsm_build_run")
+        self.run_launches = last_launch_count()
+        return out
+
+    def bins(self, stream=None):
+        """Sorted (light, tile, depth_bits, index) uint32 arrays + tile ranges (device int64 views)."""
+        P = self.n_keys
+        outs = [torch.empty(max(P, 1), dtype=torch.int32, device=self.device) for _ in range(4)]
+        nt = self.n_lights * (self.atlas_res // 8) ** 2
+        ts = torch.empty(nt, dtype=torch.int32, device=self.device)
+        te = torch.empty(nt, dtype=torch.int32, device=self.device)
+        ws = self._ensure_run_ws()
+        rc = lib().dgsm_build_bins(C.byref(self._g), self._lights, self.n_lights, C.byref(self._opts_c),
+                                   C.byref(self.plan), C.c_void_p(self.plan_ws.data_ptr()), self.plan_ws.numel(),
+                                   C.c_void_p(ws.data_ptr()), ws.numel(),
+                                   *[C.c_void_p(o.data_ptr()) for o in outs],
+                                   C.c_void_p(ts.data_ptr()), C.c_void_p(te.data_ptr()),
+                                   C.c_void_p(_stream_ptr(stream)))
+        _check(rc, "dgsm_build_bins")
+        u32 = lambda t: (t.to(torch.int64) & 0xFFFFFFFF)
+        return tuple(u32(o[:P]) for o in outs), (u32(ts), u32(te))
+
+
+def build(gaussians: Dict[str, torch.Tensor], lights, atlas_res: int, n_shells: int,
+          opts: Optional[Options] = None, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """DGSM build (§3.2): atlas [L, K, H, W] float32 of T = exp(-tau) (or tau)."""
+    return BuildPlan(gaussians, lights, atlas_res, n_shells, opts, stream).run(out, stream)
+
+
+def exp_epilogue(tau: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """T = exp(-tau) (Eq.4), elementwise on the device; out may alias tau."""
+    if not tau.is_cuda or tau.dtype != torch.float32 or not tau.is_contiguous():
+        raise DgsmError("tau must be a contiguous float32 CUDA tensor")
+    out = torch.empty_like(tau) if out is None else out
+    rc = lib().dgsm_exp_epilogue(C.c_void_p(tau.data_ptr()), C.c_void_p(out.data_ptr()), tau.numel(),
+                                 C.c_void_p(_stream_ptr(stream)))
+    _check(rc, "dgsm_exp_epilogue")
+    return out
+
+
+def query(atlas: torch.Tensor, lights, positions: torch.Tensor, colors: Optional[torch.Tensor] = None,
+          out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """DGSM sampling (§3.3): T[m] = prod_l trilinear(atlas_l, x); colors *= T in place."""
+    if not atlas.is_cuda or atlas.dtype != torch.float32 or atlas.dim() != 4 or not atlas.is_contiguous():
+        raise DgsmError("atlas must be a contiguous float32 CUDA tensor [L, K, H, W]")
+    L, K, H, W = atlas.shape
+    if H != W:
+        raise DgsmError("square atlases only")
+    arr, nl = _lights(lights)
+    if nl != L:
+        raise DgsmError(f"atlas has {L} lights, got {nl}")
+    x = _dev_f32(positions, "positions", (3,))
+    m = x.shape[0]
+    out = torch.empty(m, dtype=torch.float32, device=x.device) if out is None else out
+    cptr = None
+    if colors is not None:
+        if colors.dtype != torch.float32 or not colors.is_contiguous() or tuple(colors.shape) != (m, 3):
+            raise DgsmError("colors must be contiguous float32 [m, 3]")
+        cptr = C.c_void_p(colors.data_ptr())
+    rc = lib().dgsm_query(C.c_void_p(atlas.data_ptr()), arr, nl, int(H), int(K), C.c_void_p(x.data_ptr()), m,
+                          C.c_void_p(out.data_ptr()), cptr, C.c_void_p(_stream_ptr(stream)))
+    _check(rc, "dgsm_query")
+    return out
+
+
+def to_device(g: Dict[str, np.ndarray], device="cuda") -> Dict[str, torch.Tensor]:
+    """numpy Gaussian dict -> CUDA float32 tensors."""
+    return {k: torch.from_numpy(np.ascontiguousarray(v, np.float32)).to(device) for k, v in g.items()}

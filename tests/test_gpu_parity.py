@@ -1,0 +1,201 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.
+
+Bars:
+  * binning (P, sorted (light, tile, depth bits, index), tile ranges): bit-exact;
+  * transmittance atlas: |T_gpu - T_oracle| <= 1e-4 (BASELINE.json north_star);
+  * query on a seeded atlas: <= 2e-6 (fp32 weights and taps); end to end <= 1e-4.
+"""
+import numpy as np
+import pytest
+
+from paper_2601_01660_b200 import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL_T = 1e-4
+
+
+@pytest.fixture(scope="module")
+def dg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2601_01660_b200 import build_ext, dgsm
+    build_ext.build()
+    dgsm.lib()
+    return dgsm
+
+
+def _opts(dg, **kw):
+    return dg.Options(**kw)
+
+
+def gpu_bins(dg, scene, **opt):
+    plan = dg.BuildPlan(dg.to_device(scene.gaussians), scene.lights, scene.res, scene.K, _opts(dg, **opt))
+    (l, t, d, i), (ts, te) = plan.bins()
+    return plan, [x.cpu().numpy().astype(np.uint32) for x in (l, t, d, i)], ts.cpu().numpy(), te.cpu().numpy()
+
+
+def oracle_bins(oracle, scene, **opt):
+    mode = oracle.BIN_CLAMP if opt.get("bin_mode") == "clamp" else oracle.BIN_WRAP
+    return oracle.bin_entries(scene.gaussians["means"], scene.gaussians["scales"], scene.gaussians["rotations"],
+                              scene.lights["position"], scene.res, k_sigma=opt.get("k_sigma", 3.0),
+                              rho_scale=opt.get("rho_scale", 1.0), bin_mode=mode)
+
+
+def ranges_from_entries(L_, T_, n_lights, res):
+    nt = (res // 8) ** 2
+    g = L_.astype(np.int64) * nt + T_.astype(np.int64)
+    ts = np.zeros(n_lights * nt, np.int64)
+    te = np.zeros(n_lights * nt, np.int64)
+    if len(g):
+        starts = np.r_[0, np.nonzero(np.diff(g))[0] + 1]
+        ends = np.r_[starts[1:], len(g)]
+        ts[g[starts]] = starts
+        te[g[starts]] = ends
+    return ts, te
+
+
+def assert_bins_equal(dg, oracle, scene, **opt):
+    plan, got, ts, te = gpu_bins(dg, scene, **opt)
+    want = oracle_bins(oracle, scene, **opt)
+    assert plan.n_keys == len(want[0]), (plan.n_keys, len(want[0]))
+    for name, a, b in zip(("light", "tile", "depth", "index"), got, want):
+        assert np.array_equal(a, b), f"{name} differs at {np.nonzero(a != b)[0][:10]}"
+    wts, wte = ranges_from_entries(want[0], want[1], scene.L, scene.res)
+    assert np.array_equal(ts, wts) and np.array_equal(te, wte)
+    return plan.n_keys
+
+
+def build_both(dg, oracle, scene, **opt):
+    g = dg.to_device(scene.gaussians)
+    T = dg.build(g, scene.lights, scene.res, scene.K, _opts(dg, **opt)).cpu().numpy()
+    mode = oracle.BIN_CLAMP if opt.get("bin_mode") == "clamp" else oracle.BIN_WRAP
+    To, P = oracle.build(scene.gaussians, scene.lights, scene.res, scene.K, kappa=opt.get("kappa", 1.0),
+                         k_sigma=opt.get("k_sigma", 3.0), rho_scale=opt.get("rho_scale", 1.0), bin_mode=mode)
+    return T, To
+
+
+SCENES = {
+    "cfg1": lambda: synth.config1(),
+    "cfg1-seam-z": lambda: synth.config1_seam("-z"),
+    "cfg1-seam-x": lambda: synth.config1_seam("+x"),
+    "cfg1-seam-corner": lambda: synth.config1_seam("corner"),
+    "random-3lights": lambda: synth.random_scene(11, 400, res=32, K=8, L=3, dist=(0.3, 3.0), scale=(0.01, 0.5)),
+    "random-res8-K1": lambda: synth.random_scene(12, 150, res=8, K=1, dist=(0.5, 3.0)),
+    "random-big-footprints": lambda: synth.random_scene(13, 60, res=64, K=12, dist=(0.1, 1.0), scale=(0.05, 0.8)),
+    "cfg2-small": lambda: synth.config2(scale=0.004, res=64, K=16),
+}
+
+
+@pytest.mark.parametrize("name", sorted(SCENES))
+def test_binning_bit_exact(dg, oracle_mod, name):
+    P = assert_bins_equal(dg, oracle_mod, SCENES[name]())
+    assert P > 0
+
+
+@pytest.mark.parametrize("opt", [dict(bin_mode="clamp"), dict(rho_scale=2.6), dict(k_sigma=1.5)])
+def test_binning_options_bit_exact(dg, oracle_mod, opt):
+    assert_bins_equal(dg, oracle_mod, synth.config1_seam("corner"), **opt)
+
+
+@pytest.mark.parametrize("name", sorted(SCENES))
+def test_build_parity(dg, oracle_mod, name):
+    T, To = build_both(dg, oracle_mod, SCENES[name]())
+    err = np.abs(T - To).max()
+    assert err <= TOL_T, err
+
+
+@pytest.mark.parametrize("opt", [dict(kappa=2.0), dict(bin_mode="clamp"), dict(rho_scale=2.6)])
+def test_build_parity_options(dg, oracle_mod, opt):
+    T, To = build_both(dg, oracle_mod, synth.config1_seam("+x"), **opt)
+    assert np.abs(T - To).max() <= TOL_T
+
+
+def test_build_invariants_and_determinism(dg):
+    s = synth.config1()
+    g = dg.to_device(s.gaussians)
+    T1 = dg.build(g, s.lights, s.res, s.K)
+    T2 = dg.build(g, s.lights, s.res, s.K)
+    assert torch.equal(T1, T2)  # deterministic (fixed depth-order summation)
+    T = T1.cpu().numpy()
+    assert (T >= 0).all() and (T <= 1).all()
+    assert (np.diff(T, axis=1) <= 1e-6).all()
+    g2 = dg.to_device(synth.concat_gaussians(s.gaussians, s.gaussians))
+    Td = dg.build(g2, s.lights, s.res, s.K).cpu().numpy()
+    assert np.abs(Td - T ** 2).max() < 2e-5
+
+
+def test_empty_scene_is_exactly_one(dg):
+    s = synth.config1()
+    g = {k: torch.zeros((0,) + v.shape[1:], dtype=torch.float32, device="cuda") for k, v in s.gaussians.items()}
+    T = dg.build(g, s.lights, s.res, s.K)
+    assert torch.all(T == 1.0)
+    # all Gaussians excluded (at the light) -> 1 as well
+    e = {k: v[:3].copy() for k, v in s.gaussians.items()}
+    e["means"][:] = 0.0
+    T = dg.build(dg.to_device(e), s.lights, s.res, s.K)
+    assert torch.all(T == 1.0)
+
+
+def test_multichunk_tiles(dg, oracle_mod):
+    """> 1024 Gaussians in one tile: chunked work units + deterministic combine."""
+    rng = np.random.default_rng(5)
+    n = 3000
+    d = np.array([0.2, 0.1, 1.0]); d /= np.linalg.norm(d)
+    mu = d[None] * rng.uniform(1.0, 3.0, n)[:, None] + rng.normal(0, 0.004, (n, 3))
+    g = dict(means=mu.astype(np.float32), scales=np.full((n, 3), 0.01, np.float32),
+             rotations=synth.random_quaternions(rng, n).astype(np.float32),
+             opacities=rng.uniform(0.01, 0.1, n).astype(np.float32))
+    s = synth.Scene("dense", g, dict(position=np.zeros((1, 3), np.float32), t_max=np.array([4.0], np.float32)),
+                    32, 16, mu.astype(np.float32))
+    assert_bins_equal(dg, oracle_mod, s)
+    T, To = build_both(dg, oracle_mod, s)
+    assert np.abs(T - To).max() <= TOL_T
+    gd = dg.to_device(g)
+    assert torch.equal(dg.build(gd, s.lights, 32, 16), dg.build(gd, s.lights, 32, 16))
+
+
+def test_output_tau_and_exp_epilogue(dg, oracle_mod):
+    s = synth.config1_seam("-z")
+    g = dg.to_device(s.gaussians)
+    tau = dg.build(g, s.lights, s.res, s.K, dg.Options(output_tau=True))
+    T = dg.exp_epilogue(tau)
+    To, _ = oracle_mod.build(s.gaussians, s.lights, s.res, s.K)
+    assert np.abs(T.cpu().numpy() - To).max() <= TOL_T
+    dg.exp_epilogue(tau, out=tau)  # in place
+    assert torch.equal(tau, T)
+
+
+@pytest.mark.parametrize("L,K,res", [(1, 16, 64), (3, 8, 32), (2, 1, 8)])
+def test_query_parity_random_atlas(dg, oracle_mod, L, K, res):
+    atlas = synth.random_atlas(L + K + res, L, K, res)
+    rng = np.random.default_rng(L * 100 + K)
+    lights = dict(position=rng.uniform(-1, 1, (L, 3)).astype(np.float32),
+                  t_max=rng.uniform(2, 5, L).astype(np.float32))
+    x = synth.random_queries(K, lights, 20000, 6.0)
+    x[:5] = lights["position"][0]  # at the light -> T_l = 1
+    want = oracle_mod.query(atlas.astype(np.float64), lights, x)
+    got = dg.query(torch.from_numpy(atlas).cuda(), lights, torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.abs(got - want).max() <= 2e-6
+    col = np.random.default_rng(1).random((x.shape[0], 3)).astype(np.float32)
+    ct = torch.from_numpy(col).cuda()
+    dg.query(torch.from_numpy(atlas).cuda(), lights, torch.from_numpy(x).cuda(), colors=ct)
+    assert np.abs(ct.cpu().numpy() - col * want[:, None]).max() <= 2e-6
+
+
+def test_query_empty(dg):
+    atlas = torch.ones(1, 4, 16, 16, device="cuda")
+    out = dg.query(atlas, dict(position=[[0, 0, 0]], t_max=[1.0]), torch.zeros(0, 3, device="cuda"))
+    assert out.numel() == 0
+
+
+def test_end_to_end_cfg1(dg, oracle_mod):
+    s = synth.config1()
+    g = dg.to_device(s.gaussians)
+    atlas = dg.build(g, s.lights, s.res, s.K)
+    T = dg.query(atlas, s.lights, torch.from_numpy(s.queries).cuda()).cpu().numpy()
+    To, _ = oracle_mod.build(s.gaussians, s.lights, s.res, s.K)
+    Tq = oracle_mod.query(To, s.lights, s.queries)
+    assert np.abs(T - Tq).max() <= TOL_T
