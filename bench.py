@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""DGSM build + query benchmark (BASELINE.json metric) — one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dgsm|reference] [--config 2]
+
+A step is one pass of the whole hot path (SURVEY.md §8(a) rows a1-a6 + a8) over
+one synthetic frame: dgsm_build_plan + dgsm_build_run (project, scan, duplicate,
+onesweep sort, ranges, accumulate + exp) + dgsm_query over the receivers.
+
+* value  = Gaussian-ray evaluations per second of the whole step,
+           64 * P (texel x listed Gaussian pairs, K shells each) / step time,
+           inputs resident in HBM; L2 flushed (256 MiB write) before every step.
+* e2e    = the same metric through the public API with the step's inputs copied
+           from pinned host memory and T_out copied back inside the timed region.
+* roofline = the accumulation kernel (a6, dominant), timed live with CUDA
+           events recorded by the library around its launch; algorithmic FP32
+           work per launch from an instrumented (untimed) run.
+* cpu_baseline = the oracle (oracle/, fp64 C, all host cores) on a bounded
+           sample: full binning + every s-th tile accumulated.
+N > 1 (torchrun): weak scaling — every rank builds and queries its own frame
+(independent light, no data-path collective); time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DGSM build Gaussian-ray evals/s and query Gaussians/s at 1/2/4/8 B200"
+UNIT = "Gaussian-ray evals/s"
+
+# algorithmic FP32-pipe operations of the a6 accumulation (FMA = 1 op; MUFU ops
+# counted as 1), from the formulas of DESIGN.md "a6 algorithmic work"
+OPS_PAIR = 31     # delta, W delta, u, a, g x W delta, |.|^2, 1/a, r
+OPS_LIVE = 30     # u.W delta, s*-D, rsqrt, h, x0, erf(x0), prefactor, window bounds
+OPS_SHELL = 16    # t_k - s*, x_k, erf(x_k), w_k, difference update
+OPS_STEP = 3      # pref (1 - erf(x0)) - prev, update
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="dgsm", choices=["dgsm", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--scale", type=float, default=1.0, help="shrink the scene (debug only)")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle sample time")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload(cfg: int, scale: float, rank: int):
+    from paper_2601_01660_b200 import synth
+    if cfg == 2:
+        s = synth.config2(scale=scale)
+    elif cfg == 1:
+        s = synth.config1()
+    elif cfg == 4:
+        s = synth.config4(frame=rank % 120, scale=scale)
+    else:
+        s = synth.make_config(cfg, scale=scale)
+    if rank and cfg != 4:
+        # weak scaling: an independent frame per rank (light moved by 5 cm per rank)
+        lp = s.lights["position"].copy()
+        lp[:, 0] += 0.05 * rank
+        s.lights = dict(position=lp, t_max=s.lights["t_max"] + np.float32(0.05 * rank))
+    return s
+
+
+def cfg_desc(s, cfg):
+    return {"workload": f"cfg{cfg}: {s.note}", "n_gaussians": s.n, "n_lights": s.L,
+            "atlas": f"{s.res}x{s.res}x{s.K}", "queries": int(s.queries.shape[0]),
+            "l2": "flushed before every step (256 MiB write)", "data": "synthetic, seeded (synth.py)"}
+
+
+def cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0])); smax = float(p[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ oracle legs
+def oracle_sample(s, seconds: float, threads: int):
+    """Oracle culled build of the scene: full binning + every stride-th tile.
+    Returns dict(value evals/s, seconds, evals, stride)."""
+    from oracle import oracle
+
+    def run(stride):
+        t0 = time.perf_counter()
+        _, P, ev = oracle.build(s.gaussians, s.lights, s.res, s.K, tile_stride=stride, n_threads=threads,
+                                return_evals=True)
+        return time.perf_counter() - t0, P, ev
+
+    n_items = s.L * (s.res // 8) ** 2
+    # two pilots separate the fixed binning cost from the per-evaluation cost
+    t1, P, ev1 = run(n_items)
+    t2, _, ev2 = run(max(1, n_items // 64))
+    per_eval = max(t2 - t1, 1e-6) / max(ev2 - ev1, 1)
+    t_bin = max(t1, 0.0)
+    acc_budget = max(seconds - t_bin, t_bin, 1.0)
+    want = acc_budget / per_eval
+    total_evals = 64.0 * P
+    stride = int(max(1, min(n_items, round(total_evals / max(want, 1.0)))))
+    dt, P, ev = run(stride)
+    return {"value": ev / dt, "seconds": dt, "evals": ev, "stride": stride, "P": P,
+            "est_full_build_s": t_bin + per_eval * total_evals}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    s = workload(args.config, args.scale, 0)
+    thr = cores()
+    budget = max(1.0, 150.0 / max(1, args.steps + args.warmup))
+    vals, evs, secs, stride = [], 0, 0.0, None
+    pilot = oracle_sample(s, budget, thr)
+    stride = pilot["stride"]
+    from oracle import oracle
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        _, P, ev = oracle.build(s.gaussians, s.lights, s.res, s.K, tile_stride=stride, n_threads=thr,
+                                return_evals=True)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            evs += ev; secs += dt
+    value = evs / secs
+    sample = (f"cfg{args.config}: full oracle binning of all {P} keys + Eq.3 accumulation on every "
+              f"{stride}-th (light, tile) ({evs // max(args.steps, 1)} evals per step)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": cfg_desc(s, args.config),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU leg
+def run_dgsm(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_01660_b200 import build_ext, dgsm
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if rank == 0:
+        build_ext.build()
+    if world > 1:
+        dist.barrier()
+    s = workload(args.config, args.scale, rank)
+    g_host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in s.gaussians.items()}
+    q_host = torch.from_numpy(np.ascontiguousarray(s.queries)).pin_memory()
+    g = {k: v.to(dev) for k, v in g_host.items()}
+    xq = q_host.to(dev)
+    m = xq.shape[0]
+    atlas = torch.empty((s.L, s.K, s.res, s.res), dtype=torch.float32, device=dev)
+    T_out = torch.empty(m, dtype=torch.float32, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+
+    def step():
+        plan = dgsm.BuildPlan(g, s.lights, s.res, s.K)
+        plan.run(out=atlas)
+        nl = plan.plan_launches + plan.run_launches
+        dgsm.query(atlas, s.lights, xq, out=T_out)
+        return plan, nl + dgsm.last_launch_count()
+
+    # instrumented (untimed) run: algorithmic work of the accumulation kernel
+    sp = dgsm.BuildPlan(g, s.lights, s.res, s.K, dgsm.Options(collect_stats=True))
+    sp.run(out=atlas)
+    st = sp.stats()
+    del sp
+    alg_ops = (OPS_PAIR * st["pairs"] + OPS_LIVE * st["pairs_live"] + OPS_SHELL * st["window_shells"]
+               + OPS_STEP * st["steps"])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K)]
+    for e in ev:  # create the CUDA events now (torch creates them lazily on record)
+        for x in e:
+            x.record()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.2)
+    P = 0
+    launches = 0
+    for i in range(K):
+        flush.zero_()
+        e0, e_acc0, e_acc1, e_q, e1 = ev[i]
+        dgsm.set_accumulate_events(e_acc0, e_acc1)
+        e0.record()
+        plan, nl = step()
+        e1.record()
+        launches += nl
+        P = plan.n_keys
+        # query boundary: the query is the last launch of the step
+    dgsm.set_accumulate_events(None, None)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    t_step = [ev[i][0].elapsed_time(ev[i][4]) for i in range(K)]          # ms
+    t_acc = [ev[i][1].elapsed_time(ev[i][2]) for i in range(K)]
+    # query time: separate short timing loop (same kernel, L2 flushed)
+    tq = []
+    for i in range(K):
+        flush.zero_()
+        a, b = ev[i][0], ev[i][4]
+        a.record()
+        dgsm.query(atlas, s.lights, xq, out=T_out)
+        b.record()
+    torch.cuda.synchronize()
+    tq = [ev[i][0].elapsed_time(ev[i][4]) for i in range(K)]
+    total_ms = float(np.sum(t_step))
+    if world > 1:
+        t = torch.tensor([total_ms, float(64 * P)], device=dev, dtype=torch.float64)
+        tmax = t.clone(); dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+        units = t[1:].clone(); dist.all_reduce(units, op=dist.ReduceOp.SUM)
+        total_ms_max, units_all = float(tmax[0]), float(units[0])
+    else:
+        total_ms_max, units_all = total_ms, float(64 * P)
+    value = units_all * K / (total_ms_max * 1e-3)
+
+    # e2e through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        T_host = torch.empty(m, dtype=torch.float32).pin_memory()
+        te = []
+        for i in range(K):
+            flush.zero_()
+            a, b = ev[i][0], ev[i][4]
+            a.record()
+            gd = {k: v.to(dev, non_blocking=True) for k, v in g_host.items()}
+            xd = q_host.to(dev, non_blocking=True)
+            plan = dgsm.BuildPlan(gd, s.lights, s.res, s.K)
+            at = plan.run()
+            Tq = dgsm.query(at, s.lights, xd)
+            T_host.copy_(Tq, non_blocking=True)
+            b.record()
+            te.append((a, b))
+        torch.cuda.synchronize()
+        te_ms = float(np.sum([a.elapsed_time(b) for a, b in te]))
+        if world > 1:
+            t = torch.tensor([te_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te_ms = float(t[0])
+        h2d = sum(v.numel() * 4 for v in g_host.values()) + q_host.numel() * 4
+        e2e = {"value": units_all * K / (te_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(m * 4), "ms_per_step": te_ms / K}
+
+    if rank == 0:
+        peaks = {}
+        pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        if os.path.exists(pk_path):
+            peaks = json.load(open(pk_path))
+        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+        props = torch.cuda.get_device_properties(dev)
+        n_sm = props.multi_processor_count
+        peak_tops = n_sm * 128 * sm_mhz * 1e6 / 1e12   # FP32 lanes x clock
+        acc_ms = float(np.mean(t_acc))
+        achieved = alg_ops / (acc_ms * 1e-3) / 1e12
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "accumulate_traffic.json")
+        if os.path.exists(prof):
+            try:
+                pj = json.load(open(prof))
+                if pj.get("config") == f"cfg{args.config}" and abs(pj.get("scale", 1.0) - args.scale) < 1e-9:
+                    traffic = pj.get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": total_ms_max / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 geometry)", "data": "synthetic",
+            "config": cfg_desc(s, args.config),
+            "build_ms": float(np.mean(t_step)) , "accumulate_ms": acc_ms,
+            "accumulate_share": acc_ms / float(np.mean(t_step)),
+            "query_ms": float(np.mean(tq)),
+            "query_gaussians_per_s": m / (float(np.mean(tq)) * 1e-3) * world,
+            "keys_P": int(P), "gaussian_ray_evals_per_step": int(64 * P),
+            "accumulate_work": {k: int(v) for k, v in st.items()},
+            "gpu_launches": int(launches),
+            "roofline": {"kernel": "k_accumulate (a6)", "bound": "alu", "achieved": achieved,
+                         "peak": peak_tops, "unit": "TFLOP/s",
+                         "peak_def": f"{n_sm} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (FMA = 1 op)",
+                         "frac": achieved / peak_tops, "traffic": traffic,
+                         "alg_ops_per_launch": int(alg_ops)},
+            "clocks": clocks,
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if not args.no_cpu_baseline and world == 1:
+            cb = oracle_sample(s, args.cpu_seconds, cores())
+            line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": cores(), "kind": "oracle",
+                                    "sample": f"cfg{args.config}: full oracle binning ({cb['P']} keys) + Eq.3 "
+                                              f"accumulation on every {cb['stride']}-th (light, tile): "
+                                              f"{cb['evals']} evals in {cb['seconds']:.1f} s; "
+                                              f"full oracle build estimated {cb['est_full_build_s']:.0f} s"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_dgsm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -53,6 +53,16 @@ extern "C" {
 /* ---- build flags --------------------------------------------------------- */
 #define DGSM_OUTPUT_TAU 1u /* write optical depth tau (Eq.2) instead of T = exp(-tau) (Eq.4);
                               used by Gaussian-sharded multi-GPU builds before the reduce-scatter */
+#define DGSM_COLLECT_STATS 2u /* count the accumulation work into the run workspace (read it with
+                                 dgsm_build_stats); instrumented kernel variant, for roofline accounting */
+
+/* Work counted by a DGSM_COLLECT_STATS build. */
+typedef struct dgsm_build_stats {
+    uint64_t pairs;         /* (texel, listed Gaussian) evaluations = 64 * P */
+    uint64_t pairs_live;    /* pairs whose Eq.3 prefactor is non-zero in fp32 (r <= 180, x0 < 3.92) */
+    uint64_t window_shells; /* shells evaluated with an erf (|x_k| < 3.92) */
+    uint64_t steps;         /* saturated tails added as one step */
+} dgsm_build_stats_t;
 
 /* Occluder Gaussians, structure of arrays, DEVICE pointers (mean mu_i,
  * covariance Sigma_i = R diag(s^2) R^T, precision A_i = Sigma_i^-1, opacity alpha_i). */
@@ -163,6 +173,17 @@ int dgsm_exp_epilogue(const float* tau, float* T, int64_t count, void* stream);
 int dgsm_query(const float* atlas, const dgsm_light_t* lights, int n_lights, int atlas_res,
                int n_shells, const float* positions, int64_t m, float* T_out, float* colors_inout,
                void* stream);
+
+/* Read the counters of the last DGSM_COLLECT_STATS dgsm_build_run that used
+ * this run workspace (synchronises `stream`). */
+int dgsm_build_stats(const dgsm_plan_t* plan, void* run_ws, size_t run_ws_bytes,
+                     dgsm_build_stats_t* out, void* stream);
+
+/* Benchmark instrumentation: caller-owned cudaEvent_t handles (as void*) that
+ * subsequent dgsm_build_run calls on this thread record on their stream
+ * immediately before and after the accumulation kernel (a6).  NULL, NULL
+ * disables.  Always returns DGSM_OK. */
+int dgsm_set_accumulate_events(void* before, void* after);
 
 /* Message for a status code / for the last failure on the calling thread. */
 const char* dgsm_strerror(int code);

@@ -350,6 +350,7 @@ typedef struct {
     unsigned char* excluded; /* [L][n] */
     double* T;               /* [L][K][res][res] */
     int64_t next;            /* work counter */
+    int64_t evals;           /* (texel, Gaussian) evaluations performed */
     pthread_mutex_t lock;
 } or_build_ctx;
 
@@ -406,6 +407,10 @@ static void* or_build_worker(void* arg)
         }
         if (item >= n_items) break;
         or_build_item(c, item);
+        int64_t ev = 64 * (c->culled ? (c->range[item + 1] - c->range[item]) : c->n);
+        pthread_mutex_lock(&c->lock);
+        c->evals += ev;
+        pthread_mutex_unlock(&c->lock);
     }
     return NULL;
 }
@@ -418,7 +423,8 @@ static void* or_build_worker(void* arg)
 int64_t or_build(const float* means, const float* scales, const float* rotations,
                  const float* opacities, int64_t n, const float* light_pos, const float* t_max,
                  int L, int res, int K, double kappa, double k_sigma, double rho_scale,
-                 int bin_mode, int culled, int64_t tile_stride, int n_threads, double* T_out)
+                 int bin_mode, int culled, int64_t tile_stride, int n_threads, double* T_out,
+                 int64_t* evals_out /* nullable: (texel, Gaussian) evaluations performed */)
 {
     if (res < 8 || res % 8 != 0 || K < 1 || L < 1 || n < 0) return -1;
     or_build_ctx c;
@@ -481,6 +487,7 @@ int64_t or_build(const float* means, const float* scales, const float* rotations
     free(th);
 
     free(c.A); free(c.beta); free(c.excluded);
+    if (evals_out) *evals_out = c.evals;
     free(el); free(et); free(ed); free(ei); free(range);
     return P;
 }

@@ -59,7 +59,7 @@ def lib():
         L.or_build.restype = C.c_int64
         L.or_build.argtypes = [fp, fp, fp, fp, C.c_int64, fp, fp, C.c_int, C.c_int, C.c_int,
                                C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int64,
-                               C.c_int, dp]
+                               C.c_int, dp, i64p]
         L.or_tau_ray.restype = C.c_double
         L.or_tau_ray.argtypes = [fp, fp, fp, fp, C.c_int64, dp, dp, C.c_double, C.c_double]
         L.or_query.argtypes = [dp, C.c_int, C.c_int, C.c_int, fp, fp, fp, C.c_int64, dp, dp]
@@ -170,7 +170,7 @@ def tau_ray(g, o, d, t, kappa=1.0) -> float:
 
 
 def build(g, lights, res, K, kappa=1.0, k_sigma=3.0, rho_scale=1.0, bin_mode=BIN_WRAP,
-          culled=True, tile_stride=1, n_threads=None):
+          culled=True, tile_stride=1, n_threads=None, return_evals=False):
     """R8: the atlas T[L][K][res][res] in float64 (NaN where skipped by tile_stride).
 
     ``g``: dict of means [n,3], scales [n,3], rotations [n,4] (w,x,y,z), opacities [n].
@@ -181,12 +181,16 @@ def build(g, lights, res, K, kappa=1.0, k_sigma=3.0, rho_scale=1.0, bin_mode=BIN
     L = lp.shape[0]
     T = np.empty((L, K, res, res), dtype=np.float64)
     n_threads = n_threads or os.cpu_count() or 1
+    evals = C.c_int64(0)
     P = lib().or_build(_p(mu, C.c_float), _p(s, C.c_float), _p(q, C.c_float), _p(a, C.c_float),
                        mu.shape[0], _p(lp, C.c_float), _p(tm, C.c_float), L, int(res), int(K),
                        _opt(kappa), _opt(k_sigma), _opt(rho_scale), int(bin_mode),
-                       int(bool(culled)), int(tile_stride), int(n_threads), _p(T, C.c_double))
+                       int(bool(culled)), int(tile_stride), int(n_threads), _p(T, C.c_double),
+                       C.byref(evals))
     if P < 0:
         raise ValueError("oracle build: invalid arguments")
+    if return_evals:
+        return T, int(P), int(evals.value)
     return T, int(P)
 
 

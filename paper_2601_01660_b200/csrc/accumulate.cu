@@ -105,11 +105,14 @@ struct AccLights {
     float idt[DGSM_MAX_LIGHTS];    // 1 / dt
 };
 
+// kStats: count the work (live pairs, window shells, steps) for the benchmark's
+// roofline accounting; the timed path is <false>.
+template <bool kStats>
 __global__ void __launch_bounds__(kThreads) k_accumulate(
     const WorkUnit* __restrict__ units, const uint32_t* __restrict__ n_units_dev,
     const uint32_t* __restrict__ vals, const PairRec* __restrict__ recs, int64_t n, AccLights al,
     int res, int K, uint32_t flags, float* __restrict__ scratch, uint32_t* tile_arrive,
-    uint32_t* unit_counter, float* __restrict__ atlas) {
+    uint32_t* unit_counter, float* __restrict__ atlas, unsigned long long* __restrict__ stats) {
     extern __shared__ __align__(128) unsigned char acc_smem[];
     PairRec* s_rec = reinterpret_cast<PairRec*>(acc_smem);                       // [2][kStage]
     float* s_acc = reinterpret_cast<float*>(acc_smem + 2 * kStage * sizeof(PairRec));  // [K][64]
@@ -155,6 +158,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
             d0 = x * inv; d1 = y * inv; d2 = z * inv;
         }
         for (int k = 0; k < K; ++k) s_acc[k * kThreads + tid] = 0.0f;
+        uint32_t st_live = 0, st_win = 0, st_step = 0;
 
         const float dt = al.dt[l], dtlo = al.dtlo[l], idt = al.idt[l];
         const uint32_t n_rec = wu.jend - wu.jbeg;
@@ -208,6 +212,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
                 const float x0 = -h * (D + sD);                    // sqrt(a/2) * (b/a) of Eq.3
                 const float e0 = erf_fast(x0);
                 if (e0 >= 1.0f) continue;  // whole Gaussian behind the light
+                if (kStats) ++st_live;
                 // Eq.3 prefactor beta sqrt(pi/(2a)) exp(-(c - b^2/a)/2)
                 const float pref = R.betap * ra * ex2_approx(-0.72134752044448170f * rr);
                 // t_k - s* = (k - kD) dt + e
@@ -220,6 +225,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
                 int khi = R.kD + (int)ceilf(fhi);
                 klo = max(klo, 0);
                 khi = min(max(khi, klo), K);
+                if (kStats) { st_win += (uint32_t)(khi - klo); st_step += khi < K ? 1u : 0u; }
                 float prev = 0.0f;
                 for (int k = klo; k < khi; ++k) {
                     const float fk = (float)(k - R.kD);
@@ -234,6 +240,12 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
             if (b + 2 < n_batches) issue(b + 2);
         }
 
+        if (kStats) {
+            atomicAdd(&stats[1], (unsigned long long)st_live);
+            atomicAdd(&stats[2], (unsigned long long)st_win);
+            atomicAdd(&stats[3], (unsigned long long)st_step);
+            if (tid == 0) atomicAdd(&stats[0], (unsigned long long)n_rec * kThreads);
+        }
         // prefix sum over shells -> tau_k; epilogue T = exp(-tau) (Eq.4)
         const bool want_tau = (flags & DGSM_OUTPUT_TAU) != 0;
         const size_t plane = (size_t)H * W;
@@ -285,7 +297,9 @@ size_t accumulate_smem_bytes(int K) {
 void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint32_t max_units,
                        const uint32_t* vals, const PairRec* recs, int64_t n, const LightsParam& lp,
                        int n_lights, int res, int K, uint32_t flags, float* scratch,
-                       uint32_t* tile_arrive, uint32_t* unit_counter, float* atlas, cudaStream_t s) {
+                       uint32_t* tile_arrive, uint32_t* unit_counter, float* atlas,
+                       unsigned long long* stats, cudaEvent_t ev_before, cudaEvent_t ev_after,
+                       cudaStream_t s) {
     AccLights al;
     for (int l = 0; l < DGSM_MAX_LIGHTS; ++l) {
         const double dt = l < n_lights ? (double)lp.l[l].w / K : 1.0;
@@ -304,17 +318,24 @@ void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint3
         smem_set = 0;
     }
     if (smem > smem_set) {
-        cudaFuncSetAttribute(k_accumulate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_accumulate<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_accumulate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         smem_set = smem;
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_accumulate, kThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_accumulate<false>, kThreads, smem);
     if (per_sm < 1) per_sm = 1;
     uint32_t grid = (uint32_t)per_sm * (uint32_t)n_sm;
     if (grid > max_units) grid = max_units;
     if (grid == 0) grid = 1;
-    k_accumulate<<<grid, kThreads, smem, s>>>(units, n_units_dev, vals, recs, n, al, res, K, flags,
-                                              scratch, tile_arrive, unit_counter, atlas);
+    if (ev_before) cudaEventRecord(ev_before, s);
+    if (flags & DGSM_COLLECT_STATS)
+        k_accumulate<true><<<grid, kThreads, smem, s>>>(units, n_units_dev, vals, recs, n, al, res, K, flags,
+                                                        scratch, tile_arrive, unit_counter, atlas, stats);
+    else
+        k_accumulate<false><<<grid, kThreads, smem, s>>>(units, n_units_dev, vals, recs, n, al, res, K, flags,
+                                                         scratch, tile_arrive, unit_counter, atlas, stats);
+    if (ev_after) cudaEventRecord(ev_after, s);
 }
 
 void launch_exp(const float* tau, float* T, int64_t count, cudaStream_t s) {

@@ -11,6 +11,7 @@ using namespace dgsm;
 namespace {
 thread_local char g_err[512] = "";
 thread_local int g_launches = 0;
+thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;
 
 int fail(int code, const char* fmt, ...) {
     va_list ap;
@@ -75,6 +76,7 @@ struct RunLayout {
     WorkUnit* units;
     uint32_t* counters;  // [0] n_units, [1] unit counter
     uint32_t* tile_arrive;
+    unsigned long long* stats;  // [4] pairs, live pairs, window shells, steps (DGSM_COLLECT_STATS)
     float* scratch;
     size_t bytes;
     uint32_t max_units;
@@ -103,6 +105,7 @@ RunLayout run_layout(void* ws, const dgsm_plan_t& pl) {
     r.units = c.take<WorkUnit>(max_units);
     r.counters = c.take<uint32_t>(64);
     r.tile_arrive = c.take<uint32_t>(nt);
+    r.stats = c.take<unsigned long long>(8);
     const int64_t max_slots = 2 * (P / pl.chunk) + 1;
     r.scratch = c.take<float>((size_t)max_slots * pl.n_shells * kTexels);
     r.bytes = c.off;
@@ -145,7 +148,7 @@ int validate(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int L, int r
     if (!(o.kappa > 0.0f) || !(o.k_sigma > 0.0f) || !(o.rho_scale > 0.0f))
         return fail(DGSM_EINVAL, "kappa, k_sigma, rho_scale must be > 0");
     if (o.bin_mode != DGSM_BIN_WRAP && o.bin_mode != DGSM_BIN_CLAMP) return fail(DGSM_EINVAL, "bad bin_mode");
-    if (o.flags & ~DGSM_OUTPUT_TAU) return fail(DGSM_EINVAL, "unknown flags");
+    if (o.flags & ~(DGSM_OUTPUT_TAU | DGSM_COLLECT_STATS)) return fail(DGSM_EINVAL, "unknown flags");
     return DGSM_OK;
 }
 
@@ -289,9 +292,10 @@ int dgsm_build_run(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_
                  r.counters, s, &g_launches);
     cudaMemsetAsync(r.counters + 1, 0, sizeof(uint32_t), s);
     cudaMemsetAsync(r.tile_arrive, 0, sizeof(uint32_t) * nt, s);
+    if (o.flags & DGSM_COLLECT_STATS) cudaMemsetAsync(r.stats, 0, sizeof(unsigned long long) * 8, s);
     // a6: accumulate + exp
     launch_accumulate(r.units, r.counters, r.max_units, r.vals_a, p.recs, g->n, lp, n_lights, res, K, o.flags,
-                      r.scratch, r.tile_arrive, r.counters + 1, atlas_out, s);
+                      r.scratch, r.tile_arrive, r.counters + 1, atlas_out, r.stats, g_ev_before, g_ev_after, s);
     g_launches += 1;
     return cuda_check("build run");
 }
@@ -364,6 +368,27 @@ int dgsm_query(const float* atlas, const dgsm_light_t* lights, int n_lights, int
     launch_query(atlas, lp, n_lights, atlas_res, n_shells, positions, m, T_out, colors_inout, (cudaStream_t)stream);
     g_launches = m > 0 ? 1 : 0;
     return cuda_check("query");
+}
+
+int dgsm_set_accumulate_events(void* before, void* after) {
+    g_ev_before = (cudaEvent_t)before;
+    g_ev_after = (cudaEvent_t)after;
+    return DGSM_OK;
+}
+
+int dgsm_build_stats(const dgsm_plan_t* plan, void* run_ws, size_t run_ws_bytes, dgsm_build_stats_t* out,
+                     void* stream) {
+    if (!plan || !run_ws || !out) return fail(DGSM_EINVAL, "null argument");
+    if (run_ws_bytes < plan->run_workspace_bytes) return fail(DGSM_ENOSPC, "run workspace too small");
+    const RunLayout r = run_layout(run_ws, *plan);
+    unsigned long long h[4];
+    cudaMemcpyAsync(h, r.stats, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+    if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return cuda_check("stats");
+    out->pairs = h[0];
+    out->pairs_live = h[1];
+    out->window_shells = h[2];
+    out->steps = h[3];
+    return DGSM_OK;
 }
 
 const char* dgsm_strerror(int code) {

@@ -148,7 +148,8 @@ size_t accumulate_smem_bytes(int K);
 void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint32_t max_units,
                        const uint32_t* vals, const PairRec* recs, int64_t n, const LightsParam& lp,
                        int n_lights, int res, int K, uint32_t flags, float* scratch, uint32_t* tile_arrive,
-                       uint32_t* unit_counter, float* atlas, cudaStream_t s);
+                       uint32_t* unit_counter, float* atlas, unsigned long long* stats,
+                       cudaEvent_t ev_before, cudaEvent_t ev_after, cudaStream_t s);
 void launch_exp(const float* tau, float* T, int64_t count, cudaStream_t s);
 void launch_query(const float* atlas, const LightsParam& lp, int n_lights, int res, int K,
                   const float* positions, int64_t m, float* T_out, float* colors, cudaStream_t s);

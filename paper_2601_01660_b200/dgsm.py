@@ -25,11 +25,12 @@ LIB_PATH = os.path.join(_HERE, "libdgsm.so")
 DGSM_MAX_LIGHTS = 64
 DGSM_BIN_WRAP, DGSM_BIN_CLAMP = 0, 1
 DGSM_OUTPUT_TAU = 1
+DGSM_COLLECT_STATS = 2
 _STATUS = {0: "DGSM_OK", 1: "DGSM_EINVAL", 2: "DGSM_ENOSPC", 3: "DGSM_ECUDA", 4: "DGSM_ERANGE"}
 
 EXPORTED = ["dgsm_default_opts", "dgsm_plan_workspace_bytes", "dgsm_build_plan", "dgsm_build_run",
             "dgsm_build_bins", "dgsm_build", "dgsm_exp_epilogue", "dgsm_query", "dgsm_strerror",
-            "dgsm_last_error", "dgsm_last_launch_count"]
+            "dgsm_last_error", "dgsm_last_launch_count", "dgsm_build_stats", "dgsm_set_accumulate_events"]
 
 
 class Gaussians(C.Structure):
@@ -53,6 +54,11 @@ class Plan(C.Structure):
                 ("depth_min", C.c_uint32 * DGSM_MAX_LIGHTS), ("depth_max", C.c_uint32 * DGSM_MAX_LIGHTS),
                 ("depth_bits", C.c_int32 * DGSM_MAX_LIGHTS), ("tile_bits", C.c_int32),
                 ("run_workspace_bytes", C.c_size_t), ("signature", C.c_uint64)]
+
+
+class BuildStats(C.Structure):
+    _fields_ = [("pairs", C.c_uint64), ("pairs_live", C.c_uint64), ("window_shells", C.c_uint64),
+                ("steps", C.c_uint64)]
 
 
 class DgsmError(RuntimeError):
@@ -92,6 +98,10 @@ def lib() -> C.CDLL:
         L.dgsm_last_error.restype = C.c_char_p
         L.dgsm_last_launch_count.argtypes = []
         L.dgsm_last_launch_count.restype = C.c_int
+        L.dgsm_build_stats.argtypes = [P(Plan), vp, sz, P(BuildStats), vp]
+        L.dgsm_build_stats.restype = C.c_int
+        L.dgsm_set_accumulate_events.argtypes = [vp, vp]
+        L.dgsm_set_accumulate_events.restype = C.c_int
         for f in ("dgsm_build_plan", "dgsm_build_run", "dgsm_build_bins", "dgsm_build",
                   "dgsm_exp_epilogue", "dgsm_query"):
             getattr(L, f).restype = C.c_int
@@ -165,11 +175,13 @@ class Options:
     rho_scale: float = 1.0
     bin_mode: str = "wrap"
     output_tau: bool = False
+    collect_stats: bool = False
 
     def c(self) -> BuildOpts:
         return BuildOpts(self.kappa, self.k_sigma, self.rho_scale,
                          DGSM_BIN_WRAP if self.bin_mode == "wrap" else DGSM_BIN_CLAMP,
-                         DGSM_OUTPUT_TAU if self.output_tau else 0)
+                         (DGSM_OUTPUT_TAU if self.output_tau else 0) |
+                         (DGSM_COLLECT_STATS if self.collect_stats else 0))
 
 
 def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
@@ -231,6 +243,15 @@ class BuildPlan:
         self.run_launches = last_launch_count()
         return out
 
+    def stats(self, stream=None) -> dict:
+        """Work counters of the last run (needs Options(collect_stats=True))."""
+        st = BuildStats()
+        ws = self._ensure_run_ws()
+        rc = lib().dgsm_build_stats(C.byref(self.plan), C.c_void_p(ws.data_ptr()), ws.numel(), C.byref(st),
+                                    C.c_void_p(_stream_ptr(stream)))
+        _check(rc, "dgsm_build_stats")
+        return dict(pairs=st.pairs, pairs_live=st.pairs_live, window_shells=st.window_shells, steps=st.steps)
+
     def bins(self, stream=None):
         """Sorted (light, tile, depth_bits, index) uint32 arrays + tile ranges (device int64 views)."""
         P = self.n_keys
@@ -290,6 +311,14 @@ def query(atlas: torch.Tensor, lights, positions: torch.Tensor, colors: Optional
                           C.c_void_p(out.data_ptr()), cptr, C.c_void_p(_stream_ptr(stream)))
     _check(rc, "dgsm_query")
     return out
+
+
+def set_accumulate_events(before: Optional[torch.cuda.Event], after: Optional[torch.cuda.Event]):
+    """Record these (already created) CUDA events around the accumulation kernel of
+    subsequent builds on this thread; None, None disables."""
+    b = C.c_void_p(before.cuda_event) if before is not None else None
+    a = C.c_void_p(after.cuda_event) if after is not None else None
+    lib().dgsm_set_accumulate_events(b, a)
 
 
 def to_device(g: Dict[str, np.ndarray], device="cuda") -> Dict[str, torch.Tensor]:
