@@ -231,7 +231,9 @@ def run_dgsm(args):
     alg_ops = (OPS_PAIR * st["pairs"] + OPS_LIVE * st["pairs_live"] + OPS_SHELL * st["window_shells"]
                + OPS_STEP * st["steps"])
 
+    flush.zero_()  # first touch of the flush buffer is slow (page mapping): keep it out of the timing
     for _ in range(args.warmup):
+        flush.zero_()
         step()
     torch.cuda.synchronize()
 
@@ -249,23 +251,33 @@ def run_dgsm(args):
     time.sleep(0.2)
     P = 0
     launches = 0
+    host_ms = []
+    wall0 = time.perf_counter()
+    flush_ms = []
     for i in range(K):
-        flush.zero_()
         e0, e_acc0, e_acc1, e_q, e1 = ev[i]
+        e_q.record()  # before the L2 flush (not part of the step)
+        f0 = time.perf_counter()
+        flush.zero_()
+        flush_ms.append((time.perf_counter() - f0) * 1e3)
         dgsm.set_accumulate_events(e_acc0, e_acc1)
         e0.record()
+        h0 = time.perf_counter()
         plan, nl = step()
+        host_ms.append((time.perf_counter() - h0) * 1e3)
         e1.record()
         launches += nl
         P = plan.n_keys
-        # query boundary: the query is the last launch of the step
     dgsm.set_accumulate_events(None, None)
     torch.cuda.synchronize()
+    wall_ms = (time.perf_counter() - wall0) * 1e3
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
     t_step = [ev[i][0].elapsed_time(ev[i][4]) for i in range(K)]          # ms
     t_acc = [ev[i][1].elapsed_time(ev[i][2]) for i in range(K)]
+    t_flush = [ev[i][3].elapsed_time(ev[i][0]) for i in range(K)]
+    t_gap = [ev[i][4].elapsed_time(ev[i + 1][3]) for i in range(K - 1)]
     # query time: separate short timing loop (same kernel, L2 flushed)
     tq = []
     for i in range(K):
@@ -338,6 +350,10 @@ def run_dgsm(args):
             "warmup": args.warmup, "ms_per_step": total_ms_max / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 geometry)", "data": "synthetic",
             "config": cfg_desc(s, args.config),
+            "step_ms_each": [round(x, 3) for x in t_step], "host_enqueue_ms_each": [round(x, 3) for x in host_ms],
+            "wall_ms_per_step_incl_flush": wall_ms / K,
+            "flush_gpu_ms_each": [round(x, 3) for x in t_flush], "flush_host_ms_each": [round(x, 3) for x in flush_ms],
+            "gap_gpu_ms_each": [round(x, 3) for x in t_gap],
             "build_ms": float(np.mean(t_step)) , "accumulate_ms": acc_ms,
             "accumulate_share": acc_ms / float(np.mean(t_step)),
             "query_ms": float(np.mean(tq)),

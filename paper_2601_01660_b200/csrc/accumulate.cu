@@ -2,7 +2,7 @@
 // (Eq.2-4) over the bucketed occluders of each 8x8 tile
 // (P:L173), then T = exp(-tau) (Eq.4) into the atlas [L][K][H][W].
 //
-// Design (DESIGN.md §"a6"):
+// Design (DESIGN.md §6 "a6"):
 //  * one CTA = 64 threads = one 8x8 tile; thread <-> texel; each thread owns
 //    one column acc[k][texel] of a K x 64 shared-memory table (conflict-free:
 //    the bank is the texel index);
@@ -12,21 +12,25 @@
 //    finishes last;
 //  * the 96-B footprint records of the listed Gaussians are gathered into
 //    shared memory with TMA bulk copies (cp.async.bulk ... mbarrier::complete_tx),
-//    64 records per stage, double-buffered;
-//  * per (texel, Gaussian) pair the delta-formulation (R9) gives a, r = c - b^2/a
-//    and s* - D without cancellation; fp32 erf saturates to +-1 exactly for
-//    |x| >= 3.92, so a pair contributes pref*(erf(x_k) - erf(x_0)) only on the
-//    few shells of its "window" and the constant pref*(1 - erf(x_0)) beyond it:
-//    the window shells and the step are written as differences into acc and a
-//    prefix sum over k at the end restores tau_k.  No tensor cores: this is not
-//    a dense contraction (FP32 FMA + MUFU bound).
+//    32 per stage; a transform pass rewrites each staged record once per work
+//    unit into a compact fp32 form relative to the tile's reference direction
+//    (f = fl32(d_i - d_c)), which frees the TMA buffer for the next stage while
+//    the CTA computes on the compact copy;
+//  * per (texel, Gaussian) pair the delta-formulation (R9): delta = e_t - f,
+//    a = |g + W delta|^2, r = c - b^2/a = D^2 |g x W delta|^2 / a and s* - D =
+//    -D (u . W delta)/a, all without cancellation in fp32;
+//  * fp32 erf saturates to +-1 exactly for |x| >= 3.92, so a pair contributes
+//    pref*(erf(x_k) - erf(x_0)) only on the few shells of its "window" and the
+//    constant pref*(1 - erf(x_0)) beyond it: window shells and the step are
+//    written as differences into acc and a prefix sum over k restores tau_k.
+//    No tensor cores: this is not a dense contraction (FP32 FMA + MUFU bound).
 #include "dgsm_internal.cuh"
 
 namespace dgsm {
 
 namespace {
 constexpr int kThreads = 64;      // one 8x8 tile
-constexpr int kStage = 64;        // records per pipeline stage
+constexpr int kStage = 32;        // records per pipeline stage
 constexpr float kXS = 3.92f;      // |x| >= kXS  ->  erf_fast(x) == +-1 exactly
 constexpr float kRCut = 180.0f;   // r > kRCut -> ex2.approx.ftz(-r/(2 ln 2)) == 0 exactly
 
@@ -35,32 +39,33 @@ __device__ __forceinline__ float ex2_approx(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
-// fp32 erf with max abs error ~1.3e-7 on [0, 3.92) and exactly +-1 beyond.
-// |x| < 0.75: x * P(x^2); 0.75 <= |x| < 3.92: 1 - 2^Q(|x|).  Coefficients from
-// tools/fit_erf.py (weighted least squares toward minimax, fp32 Horner).
+// fp32 erf, branch-free: 1 - 2^Q(|x|) with Q of degree 9 on [0, 3.92]
+// (max abs error 1.1e-7, tools/fit_erf.py), exactly +-1 for |x| >= 3.92.
 __device__ __forceinline__ float erf_fast(float x) {
-    const float t = fabsf(x);
-    if (t >= kXS) return copysignf(1.0f, x);
-    if (t < 0.75f) {
-        const float z = x * x;
-        float p = -6.768997409e-04f;
-        p = fmaf(p, z, 5.116294138e-03f);
-        p = fmaf(p, z, -2.683510073e-02f);
-        p = fmaf(p, z, 1.128337309e-01f);
-        p = fmaf(p, z, -3.761261702e-01f);
-        p = fmaf(p, z, 1.128379107e+00f);
-        return x * p;
-    }
-    float q = -2.865754504e-05f;
-    q = fmaf(q, t, 6.052364479e-04f);
-    q = fmaf(q, t, -5.908878520e-03f);
-    q = fmaf(q, t, 3.594445437e-02f);
-    q = fmaf(q, t, -1.557482034e-01f);
-    q = fmaf(q, t, -9.141569138e-01f);
-    q = fmaf(q, t, -1.629331112e+00f);
-    q = fmaf(q, t, 2.074461663e-04f);
-    return copysignf(1.0f - ex2_approx(q), x);
+    const float t = fminf(fabsf(x), kXS);
+    float q = 1.063312357e-05f;
+    q = fmaf(q, t, -1.446070382e-04f);
+    q = fmaf(q, t, 8.202550816e-04f);
+    q = fmaf(q, t, -2.228778088e-03f);
+    q = fmaf(q, t, 4.658136095e-05f);
+    q = fmaf(q, t, 2.773877792e-02f);
+    q = fmaf(q, t, -1.483091265e-01f);
+    q = fmaf(q, t, -9.184432626e-01f);
+    q = fmaf(q, t, -1.627907276e+00f);
+    q = fmaf(q, t, 4.901340445e-10f);
+    const float r = t >= kXS ? 1.0f : 1.0f - ex2_approx(q);
+    return copysignf(r, x);
 }
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -99,11 +104,33 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// Texel-centre direction d(u_c, v_c) (R3), fp64.
+__device__ __forceinline__ void texel_dir(int row, int col, int W, int H, double& d0, double& d1,
+                                          double& d2) {
+    const double uc = (col + 0.5) * 2.0 / W - 1.0;
+    const double vc = (row + 0.5) * 2.0 / H - 1.0;
+    double x = uc, y = vc;
+    const double z = 1.0 - fabs(uc) - fabs(vc);
+    if (z < 0.0) {
+        x = (uc >= 0.0 ? 1.0 : -1.0) * (1.0 - fabs(vc));
+        y = (vc >= 0.0 ? 1.0 : -1.0) * (1.0 - fabs(uc));
+    }
+    const double inv = 1.0 / sqrt(x * x + y * y + z * z);
+    d0 = x * inv; d1 = y * inv; d2 = z * inv;
+}
+
 struct AccLights {
     float dt[DGSM_MAX_LIGHTS];     // t_max / K (fp32)
     float dtlo[DGSM_MAX_LIGHTS];   // t_max / K - dt (fp64 remainder)
     float idt[DGSM_MAX_LIGHTS];    // 1 / dt
 };
+
+// Compact per-(record, work unit) form, 5 x float4 (80 B):
+//  q0 = (f0, f1, f2, D^2)   f = fl32(d_i - d_c), d_c = tile reference direction
+//  q1 = (g0, g1, g2, D)
+//  q2 = (W0, W1, W2, W3), q3 = (W4, W5, W6, W7)
+//  q4 = (W8, eD, betap, kD as int bits)
+constexpr int kCompact = 5;
 
 // kStats: count the work (live pairs, window shells, steps) for the benchmark's
 // roofline accounting; the timed path is <false>.
@@ -114,19 +141,20 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
     int res, int K, uint32_t flags, float* __restrict__ scratch, uint32_t* tile_arrive,
     uint32_t* unit_counter, float* __restrict__ atlas, unsigned long long* __restrict__ stats) {
     extern __shared__ __align__(128) unsigned char acc_smem[];
-    PairRec* s_rec = reinterpret_cast<PairRec*>(acc_smem);                       // [2][kStage]
-    float* s_acc = reinterpret_cast<float*>(acc_smem + 2 * kStage * sizeof(PairRec));  // [K][64]
-    __shared__ __align__(8) uint64_t s_bar[2];
+    PairRec* s_raw = reinterpret_cast<PairRec*>(acc_smem);                                   // [kStage]
+    float4* s_cr = reinterpret_cast<float4*>(acc_smem + kStage * sizeof(PairRec));           // [kStage][5]
+    float* s_acc = reinterpret_cast<float*>(acc_smem + kStage * sizeof(PairRec) +
+                                            kStage * kCompact * sizeof(float4));             // [K][64]
+    __shared__ __align__(8) uint64_t s_bar;
     __shared__ uint32_t s_unit, s_last;
 
     const int tid = threadIdx.x;
     if (tid == 0) {
-        mbar_init(&s_bar[0], 1);
-        mbar_init(&s_bar[1], 1);
+        mbar_init(&s_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    uint32_t phase[2] = {0u, 0u};
+    uint32_t phase = 0u;
     const uint32_t n_units = *n_units_dev;
     const int TW = res / kTile;
     const int n_tiles = TW * TW;
@@ -140,23 +168,15 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
         const WorkUnit wu = units[u];
         const int l = (int)(wu.tile / (uint32_t)n_tiles);
         const int tile = (int)(wu.tile - (uint32_t)l * n_tiles);
-        const int row = (tile / TW) * kTile + (tid >> 3);
-        const int col = (tile % TW) * kTile + (tid & 7);
+        const int row0 = (tile / TW) * kTile, col0 = (tile % TW) * kTile;
+        const int row = row0 + (tid >> 3);
+        const int col = col0 + (tid & 7);
 
-        // texel-centre direction d(u_c, v_c) in fp64 (R3)
-        double d0, d1, d2;
-        {
-            const double uc = (col + 0.5) * 2.0 / W - 1.0;
-            const double vc = (row + 0.5) * 2.0 / H - 1.0;
-            double x = uc, y = vc;
-            const double z = 1.0 - fabs(uc) - fabs(vc);
-            if (z < 0.0) {
-                x = (uc >= 0.0 ? 1.0 : -1.0) * (1.0 - fabs(vc));
-                y = (vc >= 0.0 ? 1.0 : -1.0) * (1.0 - fabs(uc));
-            }
-            const double inv = 1.0 / sqrt(x * x + y * y + z * z);
-            d0 = x * inv; d1 = y * inv; d2 = z * inv;
-        }
+        // texel direction relative to the tile reference direction d_c (fp64 -> fp32)
+        double c0, c1, c2, t0, t1, t2;
+        texel_dir(row0 + 4, col0 + 4, W, H, c0, c1, c2);
+        texel_dir(row, col, W, H, t0, t1, t2);
+        const float etx = (float)(t0 - c0), ety = (float)(t1 - c1), etz = (float)(t2 - c2);
         for (int k = 0; k < K; ++k) s_acc[k * kThreads + tid] = 0.0f;
         uint32_t st_live = 0, st_win = 0, st_step = 0;
 
@@ -168,67 +188,87 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
         auto issue = [&](uint32_t b) {
             const uint32_t j0 = wu.jbeg + b * kStage;
             const uint32_t nb = min((uint32_t)kStage, wu.jend - j0);
-            PairRec* dst = s_rec + (b & 1) * kStage;
-            if (tid == 0) mbar_arrive_expect_tx(&s_bar[b & 1], nb * (uint32_t)sizeof(PairRec));
+            if (tid == 0) mbar_arrive_expect_tx(&s_bar, nb * (uint32_t)sizeof(PairRec));
             if ((uint32_t)tid < nb) {
                 const uint32_t gi = vals[j0 + tid];
-                bulk_g2s(dst + tid, lrecs + gi, (uint32_t)sizeof(PairRec), &s_bar[b & 1]);
+                bulk_g2s(s_raw + tid, lrecs + gi, (uint32_t)sizeof(PairRec), &s_bar);
             }
         };
         if (n_batches > 0) issue(0);
-        if (n_batches > 1) issue(1);
 
         for (uint32_t b = 0; b < n_batches; ++b) {
-            const int buf = b & 1;
-            mbar_wait(&s_bar[buf], phase[buf]);
-            phase[buf] ^= 1u;
+            mbar_wait(&s_bar, phase);
+            phase ^= 1u;
             const uint32_t nb = min((uint32_t)kStage, n_rec - b * kStage);
-            const PairRec* sr = s_rec + buf * kStage;
+            if ((uint32_t)tid < nb) {  // transform: raw record -> compact, relative to d_c
+                const PairRec& R = s_raw[tid];
+                float4* q = s_cr + tid * kCompact;
+                // negligible-pair cut (R8'): a pair contributes at most
+                // 2 pref <= 2 betap s_max exp(-r/2) to any tau_k (1/sqrt(a) <= s_max);
+                // skip it when that bound is < 2^-32, i.e. r > r_cut; never above 180
+                // (beyond which exp(-r/2) is exactly 0 in fp32 anyway).
+                const float w0 = R.W[0] * R.W[0] + R.W[1] * R.W[1] + R.W[2] * R.W[2];  // 1/s_0^2
+                const float w1 = R.W[3] * R.W[3] + R.W[4] * R.W[4] + R.W[5] * R.W[5];
+                const float w2 = R.W[6] * R.W[6] + R.W[7] * R.W[7] + R.W[8] * R.W[8];
+                const float smax = rsqrtf(fminf(w0, fminf(w1, w2)));
+                const float rcut = fminf(2.0f * logf(2.0f * R.betap * smax) + 44.3614195558365f, kRCut);
+                q[0] = make_float4((float)(R.di[0] - c0), (float)(R.di[1] - c1), (float)(R.di[2] - c2),
+                                   rcut / (R.D * R.D));
+                q[1] = make_float4(R.g[0], R.g[1], R.g[2], R.D);
+                q[2] = make_float4(R.W[0], R.W[1], R.W[2], R.W[3]);
+                q[3] = make_float4(R.W[4], R.W[5], R.W[6], R.W[7]);
+                q[4] = make_float4(R.W[8], R.eD, R.betap, __int_as_float(R.kD));
+            }
+            __syncthreads();  // compact copy ready; raw buffer free
+            if (b + 1 < n_batches) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(b + 1);
+            }
             for (uint32_t r = 0; r < nb; ++r) {
-                const PairRec& R = sr[r];
-                // delta = d - d_i (fp64 difference, rounded to fp32)
-                const float ex = (float)(d0 - R.di[0]);
-                const float ey = (float)(d1 - R.di[1]);
-                const float ez = (float)(d2 - R.di[2]);
+                const float4* q = s_cr + r * kCompact;
+                const float4 q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3], q4 = q[4];
+                // delta = d - d_i = e_t - f  (both small, fp32-exact to ~1e-7 relative)
+                const float ex = etx - q0.x, ey = ety - q0.y, ez = etz - q0.z;
                 // W delta, u = W d = g + W delta, a = |u|^2 = d^T A d (Eq.2)
-                const float wx = fmaf(R.W[0], ex, fmaf(R.W[1], ey, R.W[2] * ez));
-                const float wy = fmaf(R.W[3], ex, fmaf(R.W[4], ey, R.W[5] * ez));
-                const float wz = fmaf(R.W[6], ex, fmaf(R.W[7], ey, R.W[8] * ez));
-                const float gx = R.g[0], gy = R.g[1], gz = R.g[2];
+                const float wx = fmaf(q2.x, ex, fmaf(q2.y, ey, q2.z * ez));
+                const float wy = fmaf(q2.w, ex, fmaf(q3.x, ey, q3.y * ez));
+                const float wz = fmaf(q3.z, ex, fmaf(q3.w, ey, q4.x * ez));
+                const float gx = q1.x, gy = q1.y, gz = q1.z;
                 const float ux = gx + wx, uy = gy + wy, uz = gz + wz;
                 const float a = fmaf(ux, ux, fmaf(uy, uy, uz * uz));
                 // r = c - b^2/a = D^2 |g x W delta|^2 / a  (Lagrange identity)
                 const float cx = fmaf(gy, wz, -gz * wy);
                 const float cy = fmaf(gz, wx, -gx * wz);
                 const float cz = fmaf(gx, wy, -gy * wx);
-                const float ia = __frcp_rn(a);
-                const float D = R.D;
-                const float rr = D * D * fmaf(cx, cx, fmaf(cy, cy, cz * cz)) * ia;
-                if (!(rr <= kRCut)) continue;  // exp(-r/2) == 0 in fp32: no contribution
+                const float ia = rcp_approx(a);
+                const float r_over_D2 = fmaf(cx, cx, fmaf(cy, cy, cz * cz)) * ia;
+                if (!(r_over_D2 <= q0.w)) continue;  // negligible pair (R8'): r > r_cut
+                const float D = q1.w;
+                const float rr = r_over_D2 * D * D;
                 // s* - D = -D (u . W delta)/a: closest approach relative to D
                 const float sD = -D * fmaf(ux, wx, fmaf(uy, wy, uz * wz)) * ia;
-                const float ra = rsqrtf(a);
+                const float ra = rsqrt_approx(a);
                 const float h = 0.70710678118654752f * a * ra;  // sqrt(a/2)
                 const float x0 = -h * (D + sD);                    // sqrt(a/2) * (b/a) of Eq.3
-                const float e0 = erf_fast(x0);
+                const float e0 = x0 <= -kXS ? -1.0f : erf_fast(x0);
                 if (e0 >= 1.0f) continue;  // whole Gaussian behind the light
                 if (kStats) ++st_live;
                 // Eq.3 prefactor beta sqrt(pi/(2a)) exp(-(c - b^2/a)/2)
-                const float pref = R.betap * ra * ex2_approx(-0.72134752044448170f * rr);
-                // t_k - s* = (k - kD) dt + e
-                const float e = R.eD - sD;
-                const float xsh = kXS / h;
+                const float pref = q4.z * ra * ex2_approx(-0.72134752044448170f * rr);
+                // t_k - s* = (k - kD) dt + e ; window |x_k| < kXS <=> |t_k - s*| < kXS / h
+                const int kD = __float_as_int(q4.w);
+                const float e = q4.y - sD;
+                const float xsh = (kXS * 1.41421356237309505f) * ra;  // kXS / h
                 float flo = (-xsh - e) * idt, fhi = (xsh - e) * idt;
                 flo = fminf(fmaxf(flo, -(float)(K + 2)), (float)(K + 2));
                 fhi = fminf(fmaxf(fhi, -(float)(K + 2)), (float)(K + 2));
-                int klo = R.kD + (int)floorf(flo) + 1;
-                int khi = R.kD + (int)ceilf(fhi);
-                klo = max(klo, 0);
-                khi = min(max(khi, klo), K);
+                const int klo = min(max(kD + (int)floorf(flo) + 1, 0), K);
+                const int khi = min(max(kD + (int)ceilf(fhi), klo), K);
                 if (kStats) { st_win += (uint32_t)(khi - klo); st_step += khi < K ? 1u : 0u; }
                 float prev = 0.0f;
+#pragma unroll 1
                 for (int k = klo; k < khi; ++k) {
-                    const float fk = (float)(k - R.kD);
+                    const float fk = (float)(k - kD);
                     const float tk = fmaf(fk, dt, fmaf(fk, dtlo, e));
                     const float w = pref * (erf_fast(h * tk) - e0);
                     s_acc[k * kThreads + tid] += w - prev;
@@ -236,8 +276,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
                 }
                 if (khi < K) s_acc[khi * kThreads + tid] += fmaf(pref, 1.0f - e0, -prev);
             }
-            __syncthreads();  // everyone is done with this buffer
-            if (b + 2 < n_batches) issue(b + 2);
+            __syncthreads();  // compact copy consumed
         }
 
         if (kStats) {
@@ -291,7 +330,8 @@ __global__ void k_exp(const float* tau, float* T, int64_t count) {
 }  // namespace
 
 size_t accumulate_smem_bytes(int K) {
-    return 2 * kStage * sizeof(PairRec) + (size_t)K * kThreads * sizeof(float);
+    return kStage * sizeof(PairRec) + kStage * kCompact * sizeof(float4) +
+           (size_t)K * kThreads * sizeof(float);
 }
 
 void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint32_t max_units,
@@ -333,8 +373,9 @@ void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint3
         k_accumulate<true><<<grid, kThreads, smem, s>>>(units, n_units_dev, vals, recs, n, al, res, K, flags,
                                                         scratch, tile_arrive, unit_counter, atlas, stats);
     else
-        k_accumulate<false><<<grid, kThreads, smem, s>>>(units, n_units_dev, vals, recs, n, al, res, K, flags,
-                                                         scratch, tile_arrive, unit_counter, atlas, stats);
+        k_accumulate<false><<<grid, kThreads, smem, s>>>(units, n_units_dev, vals, recs, n, al, res, K,
+                                                         flags, scratch, tile_arrive, unit_counter, atlas,
+                                                         stats);
     if (ev_after) cudaEventRecord(ev_after, s);
 }
 

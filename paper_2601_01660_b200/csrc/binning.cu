@@ -31,10 +31,20 @@ __global__ void __launch_bounds__(256) k_duplicate(const PairRec* __restrict__ r
     const PairRec& r = recs[idx];
     const uint64_t depth = (uint64_t)(__float_as_uint(r.D) - dp.depth_min[l]);
     const int db = dp.depth_bits[l];
-    TileRects TR;
-    make_tile_rects(r.c0, r.c1, r.r0, r.r1, res, bin_mode, TR);
     const int TW = res / kTile;
     uint64_t o = offsets[idx];
+    const int c0 = r.c0, c1 = r.c1, r0 = r.r0, r1 = r.r1;
+    if (c0 >= 0 && c1 <= res - 1 && r0 >= 0 && r1 <= res - 1) {  // common case: inside the grid
+        for (int ty = r0 >> 3; ty <= (r1 >> 3); ++ty)
+            for (int tx = c0 >> 3; tx <= (c1 >> 3); ++tx) {
+                keys[o] = ((uint64_t)(ty * TW + tx) << db) | depth;
+                vals[o] = i;
+                ++o;
+            }
+        return;
+    }
+    TileRects TR;
+    make_tile_rects(c0, c1, r0, r1, res, bin_mode, TR);
     for (int j = 0; j < TR.n; ++j)
         for (int ty = TR.ty0[j]; ty <= TR.ty1[j]; ++ty)
             for (int tx = TR.tx0[j]; tx <= TR.tx1[j]; ++tx) {

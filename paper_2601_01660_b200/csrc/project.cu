@@ -19,10 +19,15 @@ __global__ void __launch_bounds__(256) k_project(
     const float* __restrict__ rotations, const float* __restrict__ opacities, int64_t n,
     LightsParam lp, int n_lights, int res, int K, double kappa, double k_sigma, double rho_scale,
     int bin_mode, PairRec* __restrict__ recs, uint32_t* __restrict__ counts, PlanStats* stats) {
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (int64_t)n_lights * n) return;
+    __shared__ uint32_t s_dmin[DGSM_MAX_LIGHTS], s_dmax[DGSM_MAX_LIGHTS];
+    if (threadIdx.x < DGSM_MAX_LIGHTS) { s_dmin[threadIdx.x] = 0xffffffffu; s_dmax[threadIdx.x] = 0u; }
+    __syncthreads();
+    int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool active = idx < (int64_t)n_lights * n;
+    if (!active) idx = (int64_t)n_lights * n - 1;  // recompute the last element; results not stored twice
     const int l = (int)(idx / n);
     const int64_t i = idx - (int64_t)l * n;
+    uint32_t dbits = 0u;
     const float4 L = lp.l[l];
     const int W = res, H = res;
 
@@ -85,9 +90,16 @@ __global__ void __launch_bounds__(256) k_project(
         if (c1 > 2.0 * W - 1.0) c1 = 2.0 * W - 1.0;
         if (r0 < -(double)H) r0 = -(double)H;
         if (r1 > 2.0 * H - 1.0) r1 = 2.0 * H - 1.0;
-        TileRects TR;
-        make_tile_rects((int)c0, (int)c1, (int)r0, (int)r1, res, bin_mode, TR);
-        cnt = count_tiles(TR);
+        const int ic0 = (int)c0, ic1 = (int)c1, ir0 = (int)r0, ir1 = (int)r1;
+        if (ic0 > ic1 || ir0 > ir1) {
+            cnt = 0;
+        } else if (ic0 >= 0 && ic1 <= W - 1 && ir0 >= 0 && ir1 <= H - 1) {  // common case: inside the grid
+            cnt = (uint32_t)((ic1 >> 3) - (ic0 >> 3) + 1) * (uint32_t)((ir1 >> 3) - (ir0 >> 3) + 1);
+        } else {
+            TileRects TR;
+            make_tile_rects(ic0, ic1, ir0, ir1, res, bin_mode, TR);
+            cnt = count_tiles(TR);
+        }
 
         if (cnt > 0) {
             rec.c0 = (int16_t)c0; rec.c1 = (int16_t)c1; rec.r0 = (int16_t)r0; rec.r1 = (int16_t)r1;
@@ -111,13 +123,24 @@ __global__ void __launch_bounds__(256) k_project(
             const double tau_star = -log1p(-alpha);
             const double trA = 1.0 / s2[0] + 1.0 / s2[1] + 1.0 / s2[2];
             rec.betap = (float)(kappa * tau_star * sqrt(trA / 3.0) * 0.5);
-            const uint32_t bits = __float_as_uint(Df);
-            atomicMin(&stats->depth_min[l], bits);
-            atomicMax(&stats->depth_max[l], bits);
+            dbits = __float_as_uint(Df);
         }
     }
-    counts[idx] = cnt;
-    recs[idx] = rec;
+    if (active) {
+        counts[idx] = cnt;
+        recs[idx] = rec;
+    }
+    // per-light min/max of the depth key over binned Gaussians: shared-memory
+    // atomics per block, one global atomic per (block, light)
+    if (cnt > 0) {
+        atomicMin(&s_dmin[l], dbits);
+        atomicMax(&s_dmax[l], dbits);
+    }
+    __syncthreads();
+    if (threadIdx.x < DGSM_MAX_LIGHTS && s_dmax[threadIdx.x] != 0u) {
+        atomicMin(&stats->depth_min[threadIdx.x], s_dmin[threadIdx.x]);
+        atomicMax(&stats->depth_max[threadIdx.x], s_dmax[threadIdx.x]);
+    }
 }
 
 __global__ void k_init_stats(PlanStats* stats) {
