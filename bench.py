@@ -101,22 +101,47 @@ class ClockSampler:
         self.proc = None
 
     def start(self):
+        """Start sampling every 20 ms; return once nvidia-smi has produced its first
+        sample (its start-up takes the driver lock and must not land in the timing)."""
+        import threading
+        self.lines = []
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
+            return
 
-    def stop(self):
+        def reader():
+            for line in self.proc.stdout:
+                self.lines.append((time.perf_counter(), line))
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+        t0 = time.perf_counter()
+        while not self.lines and time.perf_counter() - t0 < 10.0:
+            time.sleep(0.01)
+        time.sleep(0.05)
+
+    def mark(self):
+        return time.perf_counter()
+
+    def stop(self, t_begin=None, t_end=None):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
+        time.sleep(0.05)
         self.proc.terminate()
-        out, _ = self.proc.communicate(timeout=10)
+        try:
+            self.proc.wait(timeout=10)
+        except Exception:
+            pass
+        self.thread.join(timeout=2)
+        sel = [l for (t, l) in self.lines if (t_begin is None or t >= t_begin) and (t_end is None or t <= t_end + 0.03)]
+        if not sel:  # timed region shorter than one sample period: nearest samples
+            sel = [l for (_, l) in self.lines[-3:]]
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
+        for line in sel:
             p = [x.strip() for x in line.split(",")]
             if len(p) < 7:
                 continue
@@ -244,11 +269,10 @@ def run_dgsm(args):
             x.record()
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
+    sampler.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler.start()
-    time.sleep(0.2)
     P = 0
     launches = 0
     host_ms = []
@@ -270,10 +294,11 @@ def run_dgsm(args):
         P = plan.n_keys
     dgsm.set_accumulate_events(None, None)
     torch.cuda.synchronize()
-    wall_ms = (time.perf_counter() - wall0) * 1e3
+    wall1 = time.perf_counter()
+    wall_ms = (wall1 - wall0) * 1e3
     if world > 1:
         dist.barrier()
-    clocks = sampler.stop()
+    clocks = sampler.stop(wall0, wall1)
     t_step = [ev[i][0].elapsed_time(ev[i][4]) for i in range(K)]          # ms
     t_acc = [ev[i][1].elapsed_time(ev[i][2]) for i in range(K)]
     t_flush = [ev[i][3].elapsed_time(ev[i][0]) for i in range(K)]

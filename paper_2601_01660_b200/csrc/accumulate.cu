@@ -132,6 +132,75 @@ struct AccLights {
 //  q4 = (W8, eD, betap, kD as int bits)
 constexpr int kCompact = 5;
 
+// ---- per (texel, Gaussian) pair ---------------------------------------------
+struct PairTest {
+    float wx, wy, wz, ux, uy, uz, a, ia, r_over_D2;
+    bool live;
+};
+
+// delta-formulation (R9) up to the negligible-pair test (R8'): r/D^2 = |g x W delta|^2 / a.
+__device__ __forceinline__ PairTest pair_test(const float4* q, float etx, float ety, float etz) {
+    const float4 q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3], q4 = q[4];
+    PairTest p;
+    // delta = d - d_i = e_t - f  (both small, fp32-exact to ~1e-7 relative)
+    const float ex = etx - q0.x, ey = ety - q0.y, ez = etz - q0.z;
+    // W delta, u = W d = g + W delta, a = |u|^2 = d^T A d (Eq.2)
+    p.wx = fmaf(q2.x, ex, fmaf(q2.y, ey, q2.z * ez));
+    p.wy = fmaf(q2.w, ex, fmaf(q3.x, ey, q3.y * ez));
+    p.wz = fmaf(q3.z, ex, fmaf(q3.w, ey, q4.x * ez));
+    const float gx = q1.x, gy = q1.y, gz = q1.z;
+    p.ux = gx + p.wx; p.uy = gy + p.wy; p.uz = gz + p.wz;
+    p.a = fmaf(p.ux, p.ux, fmaf(p.uy, p.uy, p.uz * p.uz));
+    // r = c - b^2/a = D^2 |g x W delta|^2 / a  (Lagrange identity)
+    const float cx = fmaf(gy, p.wz, -gz * p.wy);
+    const float cy = fmaf(gz, p.wx, -gx * p.wz);
+    const float cz = fmaf(gx, p.wy, -gy * p.wx);
+    p.ia = rcp_approx(p.a);
+    p.r_over_D2 = fmaf(cx, cx, fmaf(cy, cy, cz * cz)) * p.ia;
+    p.live = p.r_over_D2 <= q0.w;  // negligible pair (R8'): r > r_cut
+    return p;
+}
+
+// Eq.3 over the shells for a live pair: window shells (|x_k| < kXS) as differences,
+// then the saturated step pref (1 - erf(x_0)) at the first saturated shell.
+template <bool kStats>
+__device__ __forceinline__ void pair_live(const PairTest& p, const float4* q, float* s_acc, int tid, int K,
+                                          float dt, float dtlo, float idt, uint32_t& st_live,
+                                          uint32_t& st_win, uint32_t& st_step) {
+    const float4 q1 = q[1], q4 = q[4];
+    const float D = q1.w;
+    const float rr = p.r_over_D2 * D * D;
+    // s* - D = -D (u . W delta)/a: closest approach relative to D
+    const float sD = -D * fmaf(p.ux, p.wx, fmaf(p.uy, p.wy, p.uz * p.wz)) * p.ia;
+    const float ra = rsqrt_approx(p.a);
+    const float h = 0.70710678118654752f * p.a * ra;  // sqrt(a/2)
+    const float x0 = -h * (D + sD);                      // sqrt(a/2) * (b/a) of Eq.3
+    const float e0 = x0 <= -kXS ? -1.0f : erf_fast(x0);
+    if (e0 >= 1.0f) return;  // whole Gaussian behind the light
+    if (kStats) ++st_live;
+    // Eq.3 prefactor beta sqrt(pi/(2a)) exp(-(c - b^2/a)/2)
+    const float pref = q4.z * ra * ex2_approx(-0.72134752044448170f * rr);
+    // t_k - s* = (k - kD) dt + e ; window |x_k| < kXS <=> |t_k - s*| < kXS / h
+    const int kD = __float_as_int(q4.w);
+    const float e = q4.y - sD;
+    const float xsh = (kXS * 1.41421356237309505f) * ra;  // kXS / h
+    const float kf_lo = fmaf(-xsh - e, idt, (float)kD);   // x_k <= -kXS for k <= kf_lo
+    const float kf_hi = fmaf(xsh - e, idt, (float)kD);    // x_k >= +kXS for k >= kf_hi
+    const int klo = (int)ceilf(fminf(fmaxf(kf_lo, 0.0f), (float)K));
+    const int khi = max((int)ceilf(fminf(fmaxf(kf_hi, 0.0f), (float)K)), klo);
+    if (kStats) { st_win += (uint32_t)(khi - klo); st_step += khi < K ? 1u : 0u; }
+    float prev = 0.0f;
+#pragma unroll 1
+    for (int k = klo; k < khi; ++k) {
+        const float fk = (float)(k - kD);
+        const float tk = fmaf(fk, dt, fmaf(fk, dtlo, e));
+        const float w = pref * (erf_fast(h * tk) - e0);
+        s_acc[k * kThreads + tid] += w - prev;
+        prev = w;
+    }
+    if (khi < K) s_acc[khi * kThreads + tid] += fmaf(pref, 1.0f - e0, -prev);
+}
+
 // kStats: count the work (live pairs, window shells, steps) for the benchmark's
 // roofline accounting; the timed path is <false>.
 template <bool kStats>
@@ -224,57 +293,14 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 issue(b + 1);
             }
-            for (uint32_t r = 0; r < nb; ++r) {
-                const float4* q = s_cr + r * kCompact;
-                const float4 q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3], q4 = q[4];
-                // delta = d - d_i = e_t - f  (both small, fp32-exact to ~1e-7 relative)
-                const float ex = etx - q0.x, ey = ety - q0.y, ez = etz - q0.z;
-                // W delta, u = W d = g + W delta, a = |u|^2 = d^T A d (Eq.2)
-                const float wx = fmaf(q2.x, ex, fmaf(q2.y, ey, q2.z * ez));
-                const float wy = fmaf(q2.w, ex, fmaf(q3.x, ey, q3.y * ez));
-                const float wz = fmaf(q3.z, ex, fmaf(q3.w, ey, q4.x * ez));
-                const float gx = q1.x, gy = q1.y, gz = q1.z;
-                const float ux = gx + wx, uy = gy + wy, uz = gz + wz;
-                const float a = fmaf(ux, ux, fmaf(uy, uy, uz * uz));
-                // r = c - b^2/a = D^2 |g x W delta|^2 / a  (Lagrange identity)
-                const float cx = fmaf(gy, wz, -gz * wy);
-                const float cy = fmaf(gz, wx, -gx * wz);
-                const float cz = fmaf(gx, wy, -gy * wx);
-                const float ia = rcp_approx(a);
-                const float r_over_D2 = fmaf(cx, cx, fmaf(cy, cy, cz * cz)) * ia;
-                if (!(r_over_D2 <= q0.w)) continue;  // negligible pair (R8'): r > r_cut
-                const float D = q1.w;
-                const float rr = r_over_D2 * D * D;
-                // s* - D = -D (u . W delta)/a: closest approach relative to D
-                const float sD = -D * fmaf(ux, wx, fmaf(uy, wy, uz * wz)) * ia;
-                const float ra = rsqrt_approx(a);
-                const float h = 0.70710678118654752f * a * ra;  // sqrt(a/2)
-                const float x0 = -h * (D + sD);                    // sqrt(a/2) * (b/a) of Eq.3
-                const float e0 = x0 <= -kXS ? -1.0f : erf_fast(x0);
-                if (e0 >= 1.0f) continue;  // whole Gaussian behind the light
-                if (kStats) ++st_live;
-                // Eq.3 prefactor beta sqrt(pi/(2a)) exp(-(c - b^2/a)/2)
-                const float pref = q4.z * ra * ex2_approx(-0.72134752044448170f * rr);
-                // t_k - s* = (k - kD) dt + e ; window |x_k| < kXS <=> |t_k - s*| < kXS / h
-                const int kD = __float_as_int(q4.w);
-                const float e = q4.y - sD;
-                const float xsh = (kXS * 1.41421356237309505f) * ra;  // kXS / h
-                float flo = (-xsh - e) * idt, fhi = (xsh - e) * idt;
-                flo = fminf(fmaxf(flo, -(float)(K + 2)), (float)(K + 2));
-                fhi = fminf(fmaxf(fhi, -(float)(K + 2)), (float)(K + 2));
-                const int klo = min(max(kD + (int)floorf(flo) + 1, 0), K);
-                const int khi = min(max(kD + (int)ceilf(fhi), klo), K);
-                if (kStats) { st_win += (uint32_t)(khi - klo); st_step += khi < K ? 1u : 0u; }
-                float prev = 0.0f;
-#pragma unroll 1
-                for (int k = klo; k < khi; ++k) {
-                    const float fk = (float)(k - kD);
-                    const float tk = fmaf(fk, dt, fmaf(fk, dtlo, e));
-                    const float w = pref * (erf_fast(h * tk) - e0);
-                    s_acc[k * kThreads + tid] += w - prev;
-                    prev = w;
-                }
-                if (khi < K) s_acc[khi * kThreads + tid] += fmaf(pref, 1.0f - e0, -prev);
+            // two records per iteration: independent dependency chains for the pair test
+            for (uint32_t r = 0; r < nb; r += 2) {
+                const uint32_t r2 = min(r + 1, nb - 1);
+                PairTest A = pair_test(s_cr + r * kCompact, etx, ety, etz);
+                PairTest B = pair_test(s_cr + r2 * kCompact, etx, ety, etz);
+                B.live = B.live && (r + 1 < nb);
+                if (A.live) pair_live<kStats>(A, s_cr + r * kCompact, s_acc, tid, K, dt, dtlo, idt, st_live, st_win, st_step);
+                if (B.live) pair_live<kStats>(B, s_cr + r2 * kCompact, s_acc, tid, K, dt, dtlo, idt, st_live, st_win, st_step);
             }
             __syncthreads();  // compact copy consumed
         }

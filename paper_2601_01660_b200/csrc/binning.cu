@@ -2,42 +2,65 @@
 // the accumulation kernel.  "We bucket occluders into 8x8 atlas tiles using
 // these rectangles"; the (tile, light-distance) key order is
 // DESIGN.md reading Q10/R7.
+//
+// Per light the order (tile, D bits, Gaussian index) is produced by an LSD
+// radix sort whose low digits run on the un-duplicated Gaussians:
+//   1. k_depth_keys + onesweep on N (D bits - D_min, index)  -> depth rank order
+//   2. k_gather_counts + scan                                 -> emission offsets in that order
+//   3. k_duplicate_ranked: each Gaussian, in depth-rank order, emits (tile, index)
+//   4. onesweep (stable) on the P tile keys                   -> (tile, D bits, index)
 #include "dgsm_internal.cuh"
 
 namespace dgsm {
 
 namespace {
 
-struct DupParams {
-    uint32_t depth_min[DGSM_MAX_LIGHTS];
-    int32_t depth_bits[DGSM_MAX_LIGHTS];
-};
+__device__ __forceinline__ void unpack_rect(const uint4& r, int& c0, int& c1, int& r0, int& r1) {
+    c0 = (int16_t)(r.y & 0xffffu); c1 = (int16_t)(r.y >> 16);
+    r0 = (int16_t)(r.z & 0xffffu); r1 = (int16_t)(r.z >> 16);
+}
 
-// One thread per (light, Gaussian): emit its tiles in the fixed rectangle order
-// (the same enumeration that produced its count).  Key (per light segment):
-//   (tile << depth_bits) | (fp32 bits of D - depth_min)     value: Gaussian index
-__global__ void __launch_bounds__(256) k_duplicate(const PairRec* __restrict__ recs,
-                                                   const uint32_t* __restrict__ counts,
-                                                   const uint64_t* __restrict__ offsets, int64_t n,
-                                                   int n_lights, int res, int bin_mode, DupParams dp,
-                                                   uint64_t* __restrict__ keys,
-                                                   uint32_t* __restrict__ vals) {
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (int64_t)n_lights * n) return;
-    const uint32_t cnt = counts[idx];
-    if (cnt == 0) return;
-    const int l = (int)(idx / n);
-    const uint32_t i = (uint32_t)(idx - (int64_t)l * n);
-    const PairRec& r = recs[idx];
-    const uint64_t depth = (uint64_t)(__float_as_uint(r.D) - dp.depth_min[l]);
-    const int db = dp.depth_bits[l];
+// Depth key of each Gaussian of one light (0 for Gaussians that bin no tile:
+// they emit nothing, their position in the order is irrelevant).
+__global__ void __launch_bounds__(256) k_depth_keys(const uint4* __restrict__ dup, int64_t n, uint32_t dmin,
+                                                    uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint4 r = dup[i];
+    keys[i] = r.w ? r.x - dmin : 0u;
+    vals[i] = (uint32_t)i;
+}
+
+__global__ void __launch_bounds__(256) k_gather_counts(const uint4* __restrict__ dup,
+                                                       const uint32_t* __restrict__ perm, int64_t n,
+                                                       uint32_t* __restrict__ cperm) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    cperm[j] = dup[perm[j]].w;
+}
+
+// One thread per Gaussian in depth-rank order: emit its tiles in the fixed
+// rectangle order (the same enumeration that produced its count) as
+// (key = tile, value = Gaussian index) at base + offs[j].
+__global__ void __launch_bounds__(256) k_duplicate_ranked(const uint4* __restrict__ dup,
+                                                          const uint32_t* __restrict__ perm,
+                                                          const uint64_t* __restrict__ offs, int64_t n,
+                                                          int res, int bin_mode, uint64_t base,
+                                                          uint32_t* __restrict__ keys,
+                                                          uint32_t* __restrict__ vals) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const uint32_t i = perm[j];
+    const uint4 r = dup[i];
+    if (r.w == 0) return;  // no tile
     const int TW = res / kTile;
-    uint64_t o = offsets[idx];
-    const int c0 = r.c0, c1 = r.c1, r0 = r.r0, r1 = r.r1;
+    uint64_t o = base + offs[j];
+    int c0, c1, r0, r1;
+    unpack_rect(r, c0, c1, r0, r1);
     if (c0 >= 0 && c1 <= res - 1 && r0 >= 0 && r1 <= res - 1) {  // common case: inside the grid
         for (int ty = r0 >> 3; ty <= (r1 >> 3); ++ty)
             for (int tx = c0 >> 3; tx <= (c1 >> 3); ++tx) {
-                keys[o] = ((uint64_t)(ty * TW + tx) << db) | depth;
+                keys[o] = (uint32_t)(ty * TW + tx);
                 vals[o] = i;
                 ++o;
             }
@@ -45,27 +68,26 @@ __global__ void __launch_bounds__(256) k_duplicate(const PairRec* __restrict__ r
     }
     TileRects TR;
     make_tile_rects(c0, c1, r0, r1, res, bin_mode, TR);
-    for (int j = 0; j < TR.n; ++j)
-        for (int ty = TR.ty0[j]; ty <= TR.ty1[j]; ++ty)
-            for (int tx = TR.tx0[j]; tx <= TR.tx1[j]; ++tx) {
-                if (j > 0 && in_earlier_rect(TR, j, tx, ty)) continue;
-                const uint64_t tile = (uint64_t)(ty * TW + tx);
-                keys[o] = (tile << db) | depth;
+    for (int q = 0; q < TR.n; ++q)
+        for (int ty = TR.ty0[q]; ty <= TR.ty1[q]; ++ty)
+            for (int tx = TR.tx0[q]; tx <= TR.tx1[q]; ++tx) {
+                if (q > 0 && in_earlier_rect(TR, q, tx, ty)) continue;
+                keys[o] = (uint32_t)(ty * TW + tx);
                 vals[o] = i;
                 ++o;
             }
 }
 
 // Tile ranges over one light's sorted segment [begin, end): absolute positions.
-__global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ keys, int64_t begin,
-                                                int64_t end, int db, uint32_t tile_base,
+__global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ keys, int64_t begin,
+                                                int64_t end, uint32_t tile_base,
                                                 uint32_t* __restrict__ tile_start,
                                                 uint32_t* __restrict__ tile_end) {
     const int64_t j = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= end) return;
-    const uint32_t t = (uint32_t)(keys[j] >> db);
-    if (j == begin || (uint32_t)(keys[j - 1] >> db) != t) tile_start[tile_base + t] = (uint32_t)j;
-    if (j == end - 1 || (uint32_t)(keys[j + 1] >> db) != t) tile_end[tile_base + t] = (uint32_t)(j + 1);
+    const uint32_t t = keys[j];
+    if (j == begin || keys[j - 1] != t) tile_start[tile_base + t] = (uint32_t)j;
+    if (j == end - 1 || keys[j + 1] != t) tile_end[tile_base + t] = (uint32_t)(j + 1);
 }
 
 // Per (light, tile): number of chunks (>= 1, an empty tile still writes T = 1)
@@ -105,71 +127,72 @@ __global__ void __launch_bounds__(256) k_units(const uint32_t* __restrict__ ts,
         units[u0 + c] = w;
     }
 }
+
 struct DecodeParams {
     int64_t begin[DGSM_MAX_LIGHTS + 1];
-    uint32_t depth_min[DGSM_MAX_LIGHTS];
-    int32_t depth_bits[DGSM_MAX_LIGHTS];
     int n_lights;
 };
 
-__global__ void __launch_bounds__(256) k_decode(const uint64_t* __restrict__ keys,
-                                                const uint32_t* __restrict__ vals, int64_t P, DecodeParams dp,
-                                                uint32_t* lo, uint32_t* to, uint32_t* dout, uint32_t* io) {
+// sorted (tile key, Gaussian index) -> (light, tile, fp32 bits of D, index)
+__global__ void __launch_bounds__(256) k_decode(const uint32_t* __restrict__ keys,
+                                                const uint32_t* __restrict__ vals,
+                                                const uint4* __restrict__ dup, int64_t n, int64_t P,
+                                                DecodeParams dp, uint32_t* lo, uint32_t* to, uint32_t* dout,
+                                                uint32_t* io) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= P) return;
     int l = 0;
     while (l + 1 < dp.n_lights && j >= dp.begin[l + 1]) ++l;
-    const uint64_t k = keys[j];
-    const int db = dp.depth_bits[l];
+    const uint32_t i = vals[j];
     lo[j] = (uint32_t)l;
-    to[j] = (uint32_t)(k >> db);
-    dout[j] = (uint32_t)(k & ((db ? (~0ull >> (64 - db)) : 0ull))) + dp.depth_min[l];
-    io[j] = vals[j];
+    to[j] = keys[j];
+    dout[j] = dup[(int64_t)l * n + i].x;
+    io[j] = i;
 }
 }  // namespace
 
-void launch_decode_keys(const uint64_t* keys, const uint32_t* vals, const dgsm_plan_t& plan, uint32_t* light_out,
-                        uint32_t* tile_out, uint32_t* depth_out, uint32_t* index_out, cudaStream_t s) {
+void launch_depth_keys(const uint4* dup, int64_t n, uint32_t dmin, uint32_t* keys, uint32_t* vals,
+                       cudaStream_t s) {
+    if (n <= 0) return;
+    k_depth_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dup, n, dmin, keys, vals);
+}
+
+void launch_gather_counts(const uint4* dup, const uint32_t* perm, int64_t n, uint32_t* cperm, cudaStream_t s) {
+    if (n <= 0) return;
+    k_gather_counts<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dup, perm, n, cperm);
+}
+
+void launch_duplicate_ranked(const uint4* dup, const uint32_t* perm, const uint64_t* offs, int64_t n, int res,
+                             int bin_mode, uint64_t base, uint32_t* keys, uint32_t* vals, cudaStream_t s) {
+    if (n <= 0) return;
+    k_duplicate_ranked<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dup, perm, offs, n, res, bin_mode, base,
+                                                                    keys, vals);
+}
+
+void launch_decode_keys(const uint32_t* keys, const uint32_t* vals, const uint4* dup, const dgsm_plan_t& plan,
+                        uint32_t* light_out, uint32_t* tile_out, uint32_t* depth_out, uint32_t* index_out,
+                        cudaStream_t s) {
     if (plan.n_keys <= 0) return;
     DecodeParams dp;
     dp.n_lights = plan.n_lights;
     for (int l = 0; l <= DGSM_MAX_LIGHTS; ++l) dp.begin[l] = l <= plan.n_lights ? plan.light_key_begin[l] : 0;
-    for (int l = 0; l < DGSM_MAX_LIGHTS; ++l) {
-        dp.depth_min[l] = plan.depth_min[l];
-        dp.depth_bits[l] = plan.depth_bits[l];
-    }
-    k_decode<<<(unsigned)((plan.n_keys + 255) / 256), 256, 0, s>>>(keys, vals, plan.n_keys, dp, light_out, tile_out,
-                                                                  depth_out, index_out);
+    k_decode<<<(unsigned)((plan.n_keys + 255) / 256), 256, 0, s>>>(keys, vals, dup, plan.n, plan.n_keys, dp,
+                                                                  light_out, tile_out, depth_out, index_out);
 }
 
-void launch_duplicate(const PairRec* recs, const uint32_t* counts, const uint64_t* offsets, int64_t n,
-                      int n_lights, int res, int bin_mode, const dgsm_plan_t& plan, uint64_t* keys,
-                      uint32_t* vals, cudaStream_t s) {
-    const int64_t total = (int64_t)n_lights * n;
-    if (total == 0 || plan.n_keys == 0) return;
-    DupParams dp;
-    for (int l = 0; l < DGSM_MAX_LIGHTS; ++l) {
-        dp.depth_min[l] = l < n_lights ? plan.depth_min[l] : 0;
-        dp.depth_bits[l] = l < n_lights ? plan.depth_bits[l] : 0;
-    }
-    k_duplicate<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(recs, counts, offsets, n, n_lights, res,
-                                                                  bin_mode, dp, keys, vals);
-}
-
-void launch_ranges(const uint64_t* keys, int64_t begin, int64_t end, int depth_bits, uint32_t tile_base,
-                   uint32_t* tile_start, uint32_t* tile_end, cudaStream_t s) {
+void launch_ranges(const uint32_t* keys, int64_t begin, int64_t end, uint32_t tile_base, uint32_t* tile_start,
+                   uint32_t* tile_end, cudaStream_t s) {
     if (end <= begin) return;
-    k_ranges<<<(unsigned)((end - begin + 255) / 256), 256, 0, s>>>(keys, begin, end, depth_bits,
-                                                                    tile_base, tile_start, tile_end);
+    k_ranges<<<(unsigned)((end - begin + 255) / 256), 256, 0, s>>>(keys, begin, end, tile_base, tile_start,
+                                                                    tile_end);
 }
 
 void launch_units(const uint32_t* tile_start, const uint32_t* tile_end, int64_t n_tiles_total, int chunk,
                   uint64_t* unit_counts, uint64_t* unit_offsets, void* scan_temp, WorkUnit* units,
                   uint32_t* n_units_dev, cudaStream_t s, int* launches) {
-    uint64_t* cnt = unit_counts;
     const unsigned g = (unsigned)((n_tiles_total + 255) / 256);
-    k_unit_counts<<<g, 256, 0, s>>>(tile_start, tile_end, n_tiles_total, chunk, cnt);
-    launch_scan_u64(cnt, unit_offsets, n_tiles_total, scan_temp, s);
+    k_unit_counts<<<g, 256, 0, s>>>(tile_start, tile_end, n_tiles_total, chunk, unit_counts);
+    launch_scan_u64(unit_counts, unit_offsets, n_tiles_total, scan_temp, s);
     k_units<<<g, 256, 0, s>>>(tile_start, tile_end, unit_offsets, n_tiles_total, chunk, units, n_units_dev);
     *launches += 5;
 }

@@ -47,6 +47,7 @@ struct Carver {
 struct PlanLayout {
     PairRec* recs;
     uint32_t* counts;
+    uint4* dup;
     uint64_t* offsets;
     void* scan_temp;
     PlanStats* stats;
@@ -59,6 +60,7 @@ PlanLayout plan_layout(void* ws, int64_t n, int L) {
     const int64_t m = (int64_t)L * n;
     p.recs = c.take<PairRec>(m);
     p.counts = c.take<uint32_t>(m);
+    p.dup = c.take<uint4>(m);
     p.offsets = c.take<uint64_t>(m + 1);
     p.scan_temp = c.take<char>(scan_u32_to_u64_temp_bytes(m));
     p.stats = c.take<PlanStats>(1);
@@ -67,8 +69,13 @@ PlanLayout plan_layout(void* ws, int64_t n, int L) {
 }
 
 struct RunLayout {
-    uint64_t *keys_a, *keys_b;
-    uint32_t *vals_a, *vals_b;
+    uint32_t *keys_a, *keys_b;   // tile keys (P), ping-pong
+    uint32_t *vals_a, *vals_b;   // Gaussian indices (P)
+    uint32_t *gkeys_a, *gkeys_b; // per-light depth keys of the N Gaussians, ping-pong
+    uint32_t *gvals_a, *gvals_b; // Gaussian indices -> depth-rank permutation
+    uint32_t* cperm;             // tile counts in depth-rank order (N)
+    uint64_t* offs_perm;         // their exclusive scan (N + 1)
+    void* gscan_temp;
     void* sort_temp;
     uint32_t *tile_start, *tile_end;
     uint64_t *unit_cnt, *unit_off;
@@ -90,11 +97,19 @@ RunLayout run_layout(void* ws, const dgsm_plan_t& pl) {
     for (int l = 0; l < pl.n_lights; ++l)
         pmax = std::max<int64_t>(pmax, pl.light_key_begin[l + 1] - pl.light_key_begin[l]);
     const int64_t nt = (int64_t)pl.n_lights * (pl.atlas_res / kTile) * (pl.atlas_res / kTile);
-    r.keys_a = c.take<uint64_t>(P);
-    r.keys_b = c.take<uint64_t>(P);
+    const int64_t n = pl.n;
+    r.keys_a = c.take<uint32_t>(P);
+    r.keys_b = c.take<uint32_t>(P);
     r.vals_a = c.take<uint32_t>(P);
     r.vals_b = c.take<uint32_t>(P);
-    r.sort_temp = c.take<char>(onesweep_temp_bytes(pmax));
+    r.gkeys_a = c.take<uint32_t>(n);
+    r.gkeys_b = c.take<uint32_t>(n);
+    r.gvals_a = c.take<uint32_t>(n);
+    r.gvals_b = c.take<uint32_t>(n);
+    r.cperm = c.take<uint32_t>(n);
+    r.offs_perm = c.take<uint64_t>(n + 1);
+    r.gscan_temp = c.take<char>(scan_u32_to_u64_temp_bytes(n));
+    r.sort_temp = c.take<char>(onesweep_temp_bytes(std::max<int64_t>(pmax, n)));
     r.tile_start = c.take<uint32_t>(nt);
     r.tile_end = c.take<uint32_t>(nt);
     r.unit_cnt = c.take<uint64_t>(nt);
@@ -195,7 +210,7 @@ int dgsm_build_plan(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n
     const LightsParam lp = lights_param(lights, n_lights);
     const int64_t m = (int64_t)n_lights * g->n;
 
-    launch_project(*g, lp, n_lights, atlas_res, n_shells, o, p.recs, p.counts, p.stats, s);
+    launch_project(*g, lp, n_lights, atlas_res, n_shells, o, p.recs, p.counts, p.dup, p.stats, s);
     launch_scan_u32_to_u64(p.counts, p.offsets, m, p.scan_temp, s);
     launch_plan_stats(p.offsets, g->n, n_lights, p.stats, s);
     g_launches += 6;
@@ -243,30 +258,41 @@ static int check_run_args(const dgsm_gaussians_t* g, const dgsm_light_t* lights,
     return DGSM_OK;
 }
 
-// a3-a5: duplicate, onesweep per light, ranges.  Sorted result in keys_a/vals_a.
+// a3-a5 per light: depth sort of the N Gaussians (low LSD digits), key
+// duplication in depth-rank order, stable onesweep on the tile digits, tile
+// ranges.  Sorted (tile, index) result in keys_a/vals_a.
 static void run_binning(const dgsm_gaussians_t* g, int n_lights, const dgsm_build_opts_t& o,
                         const dgsm_plan_t* plan, const PlanLayout& p, const RunLayout& r, cudaStream_t s) {
     const int res = plan->atlas_res;
+    const int64_t n = g->n;
     const int64_t n_tiles = (int64_t)(res / kTile) * (res / kTile);
     const int64_t nt = n_lights * n_tiles;
-    launch_duplicate(p.recs, p.counts, p.offsets, g->n, n_lights, res, o.bin_mode, *plan, r.keys_a, r.vals_a, s);
-    g_launches += 1;
-    for (int l = 0; l < n_lights; ++l) {
-        const int64_t b = plan->light_key_begin[l], e = plan->light_key_begin[l + 1];
-        if (e - b < 2) continue;
-        const int nbits = plan->tile_bits + plan->depth_bits[l];
-        const int flipped = launch_onesweep(r.keys_a + b, r.vals_a + b, r.keys_b + b, r.vals_b + b, e - b,
-                                            nbits, r.sort_temp, s, &g_launches);
-        if (flipped) {
-            cudaMemcpyAsync(r.keys_a + b, r.keys_b + b, sizeof(uint64_t) * (e - b), cudaMemcpyDeviceToDevice, s);
-            cudaMemcpyAsync(r.vals_a + b, r.vals_b + b, sizeof(uint32_t) * (e - b), cudaMemcpyDeviceToDevice, s);
-        }
-    }
     cudaMemsetAsync(r.tile_start, 0, sizeof(uint32_t) * nt, s);
     cudaMemsetAsync(r.tile_end, 0, sizeof(uint32_t) * nt, s);
     for (int l = 0; l < n_lights; ++l) {
-        launch_ranges(r.keys_a, plan->light_key_begin[l], plan->light_key_begin[l + 1], plan->depth_bits[l],
-                      (uint32_t)(l * n_tiles), r.tile_start, r.tile_end, s);
+        const int64_t b = plan->light_key_begin[l], e = plan->light_key_begin[l + 1];
+        if (e == b) continue;
+        const uint4* dup = p.dup + (int64_t)l * n;
+        // 1. light-distance digits on the Gaussians
+        launch_depth_keys(dup, n, plan->depth_min[l], r.gkeys_a, r.gvals_a, s);
+        const int fl = launch_onesweep_u32(r.gkeys_a, r.gvals_a, r.gkeys_b, r.gvals_b, n, plan->depth_bits[l],
+                                           r.sort_temp, s, &g_launches);
+        const uint32_t* perm = fl ? r.gvals_b : r.gvals_a;
+        // 2. emission offsets in depth-rank order
+        launch_gather_counts(dup, perm, n, r.cperm, s);
+        launch_scan_u32_to_u64(r.cperm, r.offs_perm, n, r.gscan_temp, s);
+        // 3. key duplication (key = tile, value = Gaussian index)
+        launch_duplicate_ranked(dup, perm, r.offs_perm, n, res, o.bin_mode, (uint64_t)b, r.keys_a, r.vals_a, s);
+        g_launches += 6;
+        // 4. stable sort of the tile digits
+        const int ft = launch_onesweep_u32(r.keys_a + b, r.vals_a + b, r.keys_b + b, r.vals_b + b, e - b,
+                                           plan->tile_bits, r.sort_temp, s, &g_launches);
+        if (ft) {
+            cudaMemcpyAsync(r.keys_a + b, r.keys_b + b, sizeof(uint32_t) * (e - b), cudaMemcpyDeviceToDevice, s);
+            cudaMemcpyAsync(r.vals_a + b, r.vals_b + b, sizeof(uint32_t) * (e - b), cudaMemcpyDeviceToDevice, s);
+        }
+        // 5. tile ranges
+        launch_ranges(r.keys_a, b, e, (uint32_t)(l * n_tiles), r.tile_start, r.tile_end, s);
         g_launches += 1;
     }
 }
@@ -318,7 +344,7 @@ int dgsm_build_bins(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n
     const int res = plan->atlas_res;
     const int64_t nt = n_lights * (int64_t)(res / kTile) * (res / kTile);
     run_binning(g, n_lights, o, plan, p, r, s);
-    launch_decode_keys(r.keys_a, r.vals_a, *plan, light_out, tile_out, depth_bits_out, index_out, s);
+    launch_decode_keys(r.keys_a, r.vals_a, p.dup, *plan, light_out, tile_out, depth_bits_out, index_out, s);
     g_launches += 1;
     if (tile_start_out) cudaMemcpyAsync(tile_start_out, r.tile_start, sizeof(uint32_t) * nt, cudaMemcpyDeviceToDevice, s);
     if (tile_end_out) cudaMemcpyAsync(tile_end_out, r.tile_end, sizeof(uint32_t) * nt, cudaMemcpyDeviceToDevice, s);

@@ -124,23 +124,29 @@ __host__ __device__ inline uint32_t count_tiles(const TileRects& R) {
 // (declared here, defined in the .cu files, launched from dgsm_api.cu)
 namespace dgsm {
 void launch_project(const dgsm_gaussians_t& g, const LightsParam& lp, int n_lights, int res, int K,
-                    const dgsm_build_opts_t& o, PairRec* recs, uint32_t* counts, PlanStats* stats,
-                    cudaStream_t s);
+                    const dgsm_build_opts_t& o, PairRec* recs, uint32_t* counts, uint4* dup,
+                    PlanStats* stats, cudaStream_t s);
 size_t scan_u32_to_u64_temp_bytes(int64_t n);
 void launch_scan_u32_to_u64(const uint32_t* in, uint64_t* out, int64_t n, void* temp, cudaStream_t s);
 void launch_scan_u64(const uint64_t* in, uint64_t* out, int64_t n, void* temp, cudaStream_t s);
 void launch_plan_stats(const uint64_t* offsets, int64_t n, int n_lights, PlanStats* stats, cudaStream_t s);
-void launch_duplicate(const PairRec* recs, const uint32_t* counts, const uint64_t* offsets, int64_t n,
-                      int n_lights, int res, int bin_mode, const dgsm_plan_t& plan, uint64_t* keys,
-                      uint32_t* vals, cudaStream_t s);
+// dup[l*n + i] = {fp32 bits of D, c0 | c1 << 16, r0 | r1 << 16, tile count} (16 B per (light, Gaussian))
+void launch_depth_keys(const uint4* dup, int64_t n, uint32_t dmin, uint32_t* keys, uint32_t* vals,
+                       cudaStream_t s);
+void launch_gather_counts(const uint4* dup, const uint32_t* perm, int64_t n, uint32_t* cperm, cudaStream_t s);
+void launch_duplicate_ranked(const uint4* dup, const uint32_t* perm, const uint64_t* offs, int64_t n, int res,
+                             int bin_mode, uint64_t base, uint32_t* keys, uint32_t* vals, cudaStream_t s);
 size_t onesweep_temp_bytes(int64_t n_max);
 // returns 1 if the sorted result ended in the *_alt buffers
 int launch_onesweep(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int64_t n,
                     int nbits, void* temp, cudaStream_t s, int* launches);
-void launch_decode_keys(const uint64_t* keys, const uint32_t* vals, const dgsm_plan_t& plan, uint32_t* light_out,
-                        uint32_t* tile_out, uint32_t* depth_out, uint32_t* index_out, cudaStream_t s);
-void launch_ranges(const uint64_t* keys, int64_t begin, int64_t end, int depth_bits, uint32_t tile_base,
-                   uint32_t* tile_start, uint32_t* tile_end, cudaStream_t s);
+int launch_onesweep_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n,
+                        int nbits, void* temp, cudaStream_t s, int* launches);
+void launch_decode_keys(const uint32_t* keys, const uint32_t* vals, const uint4* dup, const dgsm_plan_t& plan,
+                        uint32_t* light_out, uint32_t* tile_out, uint32_t* depth_out, uint32_t* index_out,
+                        cudaStream_t s);
+void launch_ranges(const uint32_t* keys, int64_t begin, int64_t end, uint32_t tile_base, uint32_t* tile_start,
+                   uint32_t* tile_end, cudaStream_t s);
 void launch_units(const uint32_t* tile_start, const uint32_t* tile_end, int64_t n_tiles_total, int chunk,
                   uint64_t* unit_counts, uint64_t* unit_offsets, void* scan_temp, WorkUnit* units,
                   uint32_t* n_units_dev, cudaStream_t s, int* launches);

@@ -1,35 +1,50 @@
-// onesweep.cu — stable LSD radix sort of (u64 key, u32 value) pairs in the
-// "onesweep" style: one histogram pass over all digits, then ONE kernel per
-// 8-bit digit that ranks a 4096-key tile in shared memory (warp multi-split
-// via match.any), obtains its global digit offsets by decoupled look-back over
-// earlier tiles, and scatters through shared memory for coalesced writes.
-// Partition ids come from an atomic counter, so a CTA only ever waits on tiles
-// that are already running (forward progress without co-residency).
+// onesweep.cu — stable LSD radix sort of (key, u32 value) pairs, key = u32 or
+// u64, in the "onesweep" style: one histogram pass over all digits, then ONE
+// kernel per 8-bit digit that ranks a 2048-key partition in shared memory (warp
+// multi-split via match.any), obtains its global digit offsets by decoupled
+// look-back over earlier partitions (8 predecessors per round trip), and
+// scatters through shared memory for coalesced writes.  Partition ids come from
+// an atomic counter, so a CTA only ever waits on partitions that are already
+// running (forward progress without co-residency).
 //
-// Used per light segment on the keys (tile << depth_bits | depth); stability +
-// emission in ascending Gaussian index make the result the sort by
-// (tile, depth bits, Gaussian index) of DESIGN.md R7.
+// The build uses it twice per light (binning.cu / dgsm_api.cu): the low digits
+// (fp32 bits of the light distance D) are sorted on the N Gaussians before key
+// duplication, the high digits (tile index) on the P duplicated keys emitted in
+// that depth order — an LSD radix sort whose low passes run on the
+// un-duplicated array.  Stability gives the order (tile, D bits, Gaussian index)
+// of DESIGN.md R7.
 #include "dgsm_internal.cuh"
 
 namespace dgsm {
 
 namespace {
 constexpr int kThreads = 256;
-constexpr int kItems = 16;
-constexpr int kTileKeys = kThreads * kItems;  // 4096
+constexpr int kItems = 8;
+constexpr int kTileKeys = kThreads * kItems;  // 2048 keys per partition (<= 64 regs: 4 CTAs/SM)
 constexpr int kRadix = 256;
 constexpr int kMaxPasses = 8;
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
 
-__global__ void __launch_bounds__(256) k_hist(const uint64_t* __restrict__ keys, int64_t n, int passes,
+template <typename KeyT>
+__global__ void __launch_bounds__(256) k_hist(const KeyT* __restrict__ keys, int64_t n, int passes,
                                               uint32_t* __restrict__ hist) {
     __shared__ uint32_t sh[kMaxPasses][kRadix];
     for (int t = threadIdx.x; t < kMaxPasses * kRadix; t += blockDim.x) (&sh[0][0])[t] = 0;
     __syncthreads();
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
-         j += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t k = keys[j];
-        for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(k >> (8 * p)) & 255u], 1u);
+    // 8 keys per thread per round, loads issued together (memory-level parallelism)
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j0 < n; j0 += 8 * stride) {
+        KeyT k[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t j = j0 + u * stride;
+            k[u] = j < n ? keys[j] : (KeyT)0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (j0 + u * stride >= n) break;
+            for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(uint32_t)(k[u] >> (8 * p)) & 255u], 1u);
+        }
     }
     __syncthreads();
     for (int t = threadIdx.x; t < passes * kRadix; t += blockDim.x) {
@@ -72,15 +87,15 @@ __global__ void __launch_bounds__(256) k_hist_scan(uint32_t* hist) {
     h[threadIdx.x] = e;
 }
 
-__global__ void __launch_bounds__(kThreads) k_pass(const uint64_t* __restrict__ kin,
-                                                   const uint32_t* __restrict__ vin,
-                                                   uint64_t* __restrict__ kout,
-                                                   uint32_t* __restrict__ vout, int64_t n, int shift,
-                                                   const uint32_t* __restrict__ gofs,
-                                                   uint32_t* status, uint32_t* part_ctr) {
+template <typename KeyT>
+__global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ kin,
+                                                      const uint32_t* __restrict__ vin,
+                                                      KeyT* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                      int64_t n, int shift, const uint32_t* __restrict__ gofs,
+                                                      uint32_t* status, uint32_t* part_ctr) {
     extern __shared__ __align__(16) unsigned char os_smem[];
-    uint64_t* s_keys = reinterpret_cast<uint64_t*>(os_smem);
-    uint32_t* s_vals = reinterpret_cast<uint32_t*>(os_smem + sizeof(uint64_t) * kTileKeys);
+    KeyT* s_keys = reinterpret_cast<KeyT*>(os_smem);
+    uint32_t* s_vals = reinterpret_cast<uint32_t*>(os_smem + sizeof(KeyT) * kTileKeys);
     __shared__ uint32_t s_warp_hist[kThreads / 32][kRadix];
     __shared__ uint32_t s_tile_start[kRadix];
     __shared__ uint32_t s_global[kRadix];
@@ -94,15 +109,15 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t* __restrict__ 
     const uint32_t part = s_part;
     const int64_t base = (int64_t)part * kTileKeys + warp * (32 * kItems);
 
-    uint64_t k[kItems];
+    KeyT k[kItems];
     uint32_t v[kItems], dig[kItems], rank[kItems];
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
         const int64_t idx = base + j * 32 + lane;
         const bool valid = idx < n;
-        k[j] = valid ? kin[idx] : 0ull;
+        k[j] = valid ? kin[idx] : (KeyT)0;
         v[j] = valid ? vin[idx] : 0u;
-        dig[j] = valid ? (uint32_t)((k[j] >> shift) & 255u) : 256u;
+        dig[j] = valid ? ((uint32_t)(k[j] >> shift) & 255u) : 256u;
     }
     const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
@@ -118,7 +133,7 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t* __restrict__ 
     }
     __syncthreads();
 
-    // per digit: exclusive prefix over warps, tile total
+    // per digit: exclusive prefix over warps, partition total
     const uint32_t d = tid;
     uint32_t run = 0;
 #pragma unroll
@@ -136,15 +151,29 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t* __restrict__ 
         s_global[d] = gofs[d];
     } else {
         st[(size_t)part * kRadix + d] = kFlagAgg | tile_count;
+        // look back through a window of 8 predecessors per round trip: sum their
+        // aggregates until an inclusive prefix is found; re-poll from the first
+        // predecessor that has not published yet
         uint32_t excl = 0;
         int64_t q = (int64_t)part - 1;
+        constexpr int kWin = 8;
         while (true) {
-            const uint32_t s = st[(size_t)q * kRadix + d];
-            const uint32_t f = s & ~kValMask;
-            if (f == 0) continue;
-            excl += s & kValMask;
-            if (f == kFlagInc) break;
-            --q;
+            uint32_t s[kWin];
+#pragma unroll
+            for (int i = 0; i < kWin; ++i) s[i] = (q - i >= 0) ? st[(size_t)(q - i) * kRadix + d] : 0u;
+            int i = 0;
+            bool done = false;
+#pragma unroll
+            for (int w = 0; w < kWin; ++w) {
+                if (done || w != i) continue;
+                const uint32_t f = s[w] & ~kValMask;
+                if (f == 0) continue;  // not ready: stop consuming this window
+                excl += s[w] & kValMask;
+                if (f == kFlagInc) done = true;
+                ++i;
+            }
+            if (done) break;
+            q -= i;
         }
         st[(size_t)part * kRadix + d] = kFlagInc | (excl + tile_count);
         s_global[d] = gofs[d] + excl;
@@ -164,8 +193,8 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t* __restrict__ 
     const int64_t rem = n - (int64_t)part * kTileKeys;
     const int n_valid = rem < kTileKeys ? (int)rem : kTileKeys;
     for (int x = tid; x < n_valid; x += kThreads) {
-        const uint64_t key = s_keys[x];
-        const uint32_t dd = (uint32_t)((key >> shift) & 255u);
+        const KeyT key = s_keys[x];
+        const uint32_t dd = (uint32_t)(key >> shift) & 255u;
         const uint32_t o = s_global[dd] + (uint32_t)x - s_tile_start[dd];
         kout[o] = key;
         vout[o] = s_vals[x];
@@ -178,14 +207,46 @@ struct OnesweepTemp {
     uint32_t* status;    // [parts][256]
 };
 
-OnesweepTemp carve(void* temp, int64_t n_max) {
+OnesweepTemp carve(void* temp) {
     OnesweepTemp t;
     char* p = (char*)temp;
     t.hist = (uint32_t*)p; p += sizeof(uint32_t) * kMaxPasses * kRadix;
     t.part_ctr = (uint32_t*)p; p += 256;
     t.status = (uint32_t*)p;
-    (void)n_max;
     return t;
+}
+
+template <typename KeyT>
+int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt, int64_t n, int nbits,
+                  void* temp, cudaStream_t s, int* launches) {
+    if (n <= 1 || nbits <= 0) return 0;
+    const int passes = (nbits + 7) / 8;
+    OnesweepTemp t = carve(temp);
+    static bool attr_set = false;
+    const int dyn = (int)(sizeof(KeyT) + sizeof(uint32_t)) * kTileKeys;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_pass<KeyT>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+        attr_set = true;
+    }
+    cudaMemsetAsync(t.hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix + 256, s);
+    const int64_t parts = (n + kTileKeys - 1) / kTileKeys;
+    const int hist_grid = (int)std::min<int64_t>(148 * 4, (n + 2047) / 2048);
+    k_hist<KeyT><<<hist_grid, 256, 0, s>>>(keys, n, passes, t.hist);
+    k_hist_scan<<<passes, 256, 0, s>>>(t.hist);
+    *launches += 2;
+    KeyT *ki = keys, *ko = keys_alt;
+    uint32_t *vi = vals, *vo = vals_alt;
+    int flipped = 0;
+    for (int p = 0; p < passes; ++p) {
+        cudaMemsetAsync(t.status, 0, sizeof(uint32_t) * kRadix * (size_t)parts, s);
+        k_pass<KeyT><<<(unsigned)parts, kThreads, dyn, s>>>(ki, vi, ko, vo, n, 8 * p, t.hist + p * kRadix,
+                                                           t.status, t.part_ctr + p);
+        *launches += 1;
+        KeyT* tk = ki; ki = ko; ko = tk;
+        uint32_t* tv = vi; vi = vo; vo = tv;
+        flipped ^= 1;
+    }
+    return flipped;
 }
 }  // namespace
 
@@ -196,33 +257,12 @@ size_t onesweep_temp_bytes(int64_t n_max) {
 
 int launch_onesweep(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int64_t n,
                     int nbits, void* temp, cudaStream_t s, int* launches) {
-    if (n <= 1 || nbits <= 0) return 0;
-    const int passes = (nbits + 7) / 8;
-    OnesweepTemp t = carve(temp, n);
-    static bool attr_set = false;
-    const int dyn = (int)(sizeof(uint64_t) + sizeof(uint32_t)) * kTileKeys;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-        attr_set = true;
-    }
-    cudaMemsetAsync(t.hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix + 256, s);
-    k_hist<<<148 * 4, 256, 0, s>>>(keys, n, passes, t.hist);
-    k_hist_scan<<<passes, 256, 0, s>>>(t.hist);
-    *launches += 2;
-    const int64_t parts = (n + kTileKeys - 1) / kTileKeys;
-    uint64_t *ki = keys, *ko = keys_alt;
-    uint32_t *vi = vals, *vo = vals_alt;
-    int flipped = 0;
-    for (int p = 0; p < passes; ++p) {
-        cudaMemsetAsync(t.status, 0, sizeof(uint32_t) * kRadix * (size_t)parts, s);
-        k_pass<<<(unsigned)parts, kThreads, dyn, s>>>(ki, vi, ko, vo, n, 8 * p, t.hist + p * kRadix,
-                                                     t.status, t.part_ctr + p);
-        *launches += 1;
-        uint64_t* tk = ki; ki = ko; ko = tk;
-        uint32_t* tv = vi; vi = vo; vo = tv;
-        flipped ^= 1;
-    }
-    return flipped;
+    return onesweep_impl<uint64_t>(keys, vals, keys_alt, vals_alt, n, nbits, temp, s, launches);
+}
+
+int launch_onesweep_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n,
+                        int nbits, void* temp, cudaStream_t s, int* launches) {
+    return onesweep_impl<uint32_t>(keys, vals, keys_alt, vals_alt, n, nbits, temp, s, launches);
 }
 
 }  // namespace dgsm

@@ -14,11 +14,12 @@ constexpr double kPi = 3.141592653589793;
 
 __device__ __forceinline__ double sgn_pos(double x) { return x >= 0.0 ? 1.0 : -1.0; }  // sgn(0)=+1 (Q4)
 
-__global__ void __launch_bounds__(256) k_project(
+__global__ void __launch_bounds__(256, 3) k_project(
     const float* __restrict__ means, const float* __restrict__ scales,
     const float* __restrict__ rotations, const float* __restrict__ opacities, int64_t n,
-    LightsParam lp, int n_lights, int res, int K, double kappa, double k_sigma, double rho_scale,
-    int bin_mode, PairRec* __restrict__ recs, uint32_t* __restrict__ counts, PlanStats* stats) {
+    LightsParam lp, int n_lights, int res, int K, double kappa, double k_sigma, double rho,
+    int bin_mode, PairRec* __restrict__ recs, uint32_t* __restrict__ counts, uint4* __restrict__ dup,
+    PlanStats* stats) {
     __shared__ uint32_t s_dmin[DGSM_MAX_LIGHTS], s_dmax[DGSM_MAX_LIGHTS];
     if (threadIdx.x < DGSM_MAX_LIGHTS) { s_dmin[threadIdx.x] = 0xffffffffu; s_dmax[threadIdx.x] = 0u; }
     __syncthreads();
@@ -81,8 +82,8 @@ __global__ void __launch_bounds__(256) k_project(
         double disc = (tr * tr) * 0.25 - det;
         if (disc < 0.0) disc = 0.0;
         const double lam1 = tr * 0.5 + sqrt(disc);
-        const double rho = (rho_scale * (double)(H + W)) / (2.0 * kPi);  // P:L172 (Q5)
-        const double p1 = ((k_sigma * sqrt(lam1)) / D) * rho;           // P:L173
+        // rho = (rho_scale * (H + W)) / (2 pi) (Q5), the same IEEE double computed on the host
+        const double p1 = ((k_sigma * sqrt(lam1)) / D) * rho;  // P:L173
 
         // R6: integer texel range of the closed square, clamped to [-W, 2W-1]
         double c0 = ceil(px - p1), c1 = floor(px + p1), r0 = ceil(py - p1), r1 = floor(py + p1);
@@ -104,16 +105,20 @@ __global__ void __launch_bounds__(256) k_project(
         if (cnt > 0) {
             rec.c0 = (int16_t)c0; rec.c1 = (int16_t)c1; rec.r0 = (int16_t)r0; rec.r1 = (int16_t)r1;
             rec.di[0] = dx; rec.di[1] = dy; rec.di[2] = dz;
+            // record fields (not part of the binning contract): reciprocal multiplies
+            double inv_s[3];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) inv_s[j] = 1.0 / s[j];
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
-                rec.g[j] = (float)(w[j] / s[j]);  // g = W d_i = diag(1/s) R^T d_i
+                rec.g[j] = (float)(w[j] * inv_s[j]);  // g = W d_i = diag(1/s) R^T d_i
 #pragma unroll
-                for (int c = 0; c < 3; ++c) rec.W[3 * j + c] = (float)(R[c][j] / s[j]);
+                for (int c = 0; c < 3; ++c) rec.W[3 * j + c] = (float)(R[c][j] * inv_s[j]);
             }
             const float Df = (float)D;
             rec.D = Df;
             const double dt = (double)L.w / K;
-            int kD = (int)(D / dt);
+            int kD = (int)(D * ((double)K / (double)L.w));
             kD = kD < 0 ? 0 : (kD > K - 1 ? K - 1 : kD);
             rec.kD = kD;
             rec.eD = (float)((kD + 0.5) * dt - D);
@@ -121,7 +126,7 @@ __global__ void __launch_bounds__(256) k_project(
             double alpha = (double)opacities[i];
             alpha = alpha < 1e-4 ? 1e-4 : (alpha > 1.0 - 1e-4 ? 1.0 - 1e-4 : alpha);
             const double tau_star = -log1p(-alpha);
-            const double trA = 1.0 / s2[0] + 1.0 / s2[1] + 1.0 / s2[2];
+            const double trA = inv_s[0] * inv_s[0] + inv_s[1] * inv_s[1] + inv_s[2] * inv_s[2];
             rec.betap = (float)(kappa * tau_star * sqrt(trA / 3.0) * 0.5);
             dbits = __float_as_uint(Df);
         }
@@ -129,6 +134,8 @@ __global__ void __launch_bounds__(256) k_project(
     if (active) {
         counts[idx] = cnt;
         recs[idx] = rec;
+        dup[idx] = make_uint4(dbits, (uint32_t)(uint16_t)rec.c0 | ((uint32_t)(uint16_t)rec.c1 << 16),
+                              (uint32_t)(uint16_t)rec.r0 | ((uint32_t)(uint16_t)rec.r1 << 16), cnt);
     }
     // per-light min/max of the depth key over binned Gaussians: shared-memory
     // atomics per block, one global atomic per (block, light)
@@ -150,8 +157,8 @@ __global__ void k_init_stats(PlanStats* stats) {
 }  // namespace
 
 void launch_project(const dgsm_gaussians_t& g, const LightsParam& lp, int n_lights, int res, int K,
-                    const dgsm_build_opts_t& o, PairRec* recs, uint32_t* counts, PlanStats* stats,
-                    cudaStream_t s) {
+                    const dgsm_build_opts_t& o, PairRec* recs, uint32_t* counts, uint4* dup,
+                    PlanStats* stats, cudaStream_t s) {
     k_init_stats<<<1, DGSM_MAX_LIGHTS, 0, s>>>(stats);
     const int64_t total = (int64_t)n_lights * g.n;
     if (total == 0) return;
@@ -159,7 +166,8 @@ void launch_project(const dgsm_gaussians_t& g, const LightsParam& lp, int n_ligh
     const int64_t grid = (total + bs - 1) / bs;
     k_project<<<(unsigned)grid, bs, 0, s>>>(g.means, g.scales, g.rotations, g.opacities, g.n, lp,
                                             n_lights, res, K, (double)o.kappa, (double)o.k_sigma,
-                                            (double)o.rho_scale, o.bin_mode, recs, counts, stats);
+                                            (double)o.rho_scale * (double)(2 * res) / (2.0 * kPi), o.bin_mode,
+                                            recs, counts, dup, stats);
 }
 
 }  // namespace dgsm
