@@ -231,25 +231,60 @@ def run_dgsm(args):
         build_ext.build()
     if world > 1:
         dist.barrier()
-    s = workload(args.config, args.scale, rank)
+    from paper_2601_01660_b200 import distributed as Dd
+
+    # multi-light configs (3, 5): strong scaling over the node: lights
+    # dealt to ranks; with fewer lights than ranks, Gaussian shards + partial-tau
+    # reduce-scatter over K + exp epilogue; the query product is an all-reduce(PRODUCT).
+    strong = args.config in (3, 5)
+    s = workload(args.config, args.scale, 0 if strong else rank)
     g_host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in s.gaussians.items()}
     q_host = torch.from_numpy(np.ascontiguousarray(s.queries)).pin_memory()
     g = {k: v.to(dev) for k, v in g_host.items()}
     xq = q_host.to(dev)
     m = xq.shape[0]
-    atlas = torch.empty((s.L, s.K, s.res, s.res), dtype=torch.float32, device=dev)
+    lights_b, g_b, gsz, first_of_group, pgroup = s.lights, g, 1, True, None
+    if strong:
+        lay = Dd.plan_layout(s.L, world)
+        pgroups = Dd.make_groups(lay) if world > 1 else [None] * len(lay.groups)
+        j = lay.group_index(rank)
+        my = lay.lights_of[j] if j >= 0 else []
+        idx, gsz = lay.shard_of(rank)
+        first_of_group = j >= 0 and lay.groups[j][0] == rank
+        pgroup = pgroups[j] if j >= 0 else None
+        lights_b = dict(position=s.lights["position"][my], t_max=s.lights["t_max"][my])
+        if gsz > 1:
+            s0, s1 = Dd.shard_range(s.n, idx, gsz)
+            g_b = {k: v[s0:s1] for k, v in g.items()}
+    L_b = int(np.asarray(lights_b["position"]).reshape(-1, 3).shape[0])
+    atlas = torch.empty((L_b, s.K, s.res, s.res), dtype=torch.float32, device=dev)
+    chunk = torch.empty((s.K // gsz, s.res, s.res), dtype=torch.float32, device=dev) if gsz > 1 else None
     T_out = torch.empty(m, dtype=torch.float32, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
 
     def step():
-        plan = dgsm.BuildPlan(g, s.lights, s.res, s.K)
+        plan = dgsm.BuildPlan(g_b, lights_b, s.res, s.K, dgsm.Options(output_tau=gsz > 1))
         plan.run(out=atlas)
         nl = plan.plan_launches + plan.run_launches
-        dgsm.query(atlas, s.lights, xq, out=T_out)
-        return plan, nl + dgsm.last_launch_count()
+        if gsz > 1:  # partial tau -> reduce-scatter over K -> exp on the owned shells -> all-gather
+            for q in range(L_b):
+                dist.reduce_scatter_tensor(chunk, atlas[q], op=dist.ReduceOp.SUM, group=pgroup)
+                dgsm.exp_epilogue(chunk, out=chunk)
+                nl += dgsm.last_launch_count()
+                dist.all_gather_into_tensor(atlas[q], chunk, group=pgroup)
+        if first_of_group:
+            dgsm.query(atlas, lights_b, xq, out=T_out)
+            nl += dgsm.last_launch_count()
+        else:
+            T_out.fill_(1.0)
+        if strong and world > 1:
+            dist.all_reduce(T_out, op=dist.ReduceOp.PRODUCT)
+        # return plain numbers: keeping the plan alive into the next step would hold a
+        # second set of workspaces and force a cudaMalloc inside the timed region
+        return plan.n_keys, nl
 
     # instrumented (untimed) run: algorithmic work of the accumulation kernel
-    sp = dgsm.BuildPlan(g, s.lights, s.res, s.K, dgsm.Options(collect_stats=True))
+    sp = dgsm.BuildPlan(g_b, lights_b, s.res, s.K, dgsm.Options(collect_stats=True))
     sp.run(out=atlas)
     st = sp.stats()
     del sp
@@ -287,11 +322,11 @@ def run_dgsm(args):
         dgsm.set_accumulate_events(e_acc0, e_acc1)
         e0.record()
         h0 = time.perf_counter()
-        plan, nl = step()
+        n_keys, nl = step()
         host_ms.append((time.perf_counter() - h0) * 1e3)
         e1.record()
         launches += nl
-        P = plan.n_keys
+        P = n_keys
     dgsm.set_accumulate_events(None, None)
     torch.cuda.synchronize()
     wall1 = time.perf_counter()
@@ -309,7 +344,7 @@ def run_dgsm(args):
         flush.zero_()
         a, b = ev[i][0], ev[i][4]
         a.record()
-        dgsm.query(atlas, s.lights, xq, out=T_out)
+        dgsm.query(atlas, lights_b, xq, out=T_out)
         b.record()
     torch.cuda.synchronize()
     tq = [ev[i][0].elapsed_time(ev[i][4]) for i in range(K)]
@@ -332,12 +367,11 @@ def run_dgsm(args):
             flush.zero_()
             a, b = ev[i][0], ev[i][4]
             a.record()
-            gd = {k: v.to(dev, non_blocking=True) for k, v in g_host.items()}
-            xd = q_host.to(dev, non_blocking=True)
-            plan = dgsm.BuildPlan(gd, s.lights, s.res, s.K)
-            at = plan.run()
-            Tq = dgsm.query(at, s.lights, xd)
-            T_host.copy_(Tq, non_blocking=True)
+            for k_, v_ in g_host.items():          # this step's inputs, host -> device
+                g[k_].copy_(v_, non_blocking=True)
+            xq.copy_(q_host, non_blocking=True)
+            step()
+            T_host.copy_(T_out, non_blocking=True)  # the step's result, device -> host
             b.record()
             te.append((a, b))
         torch.cuda.synchronize()
@@ -373,16 +407,19 @@ def run_dgsm(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": total_ms_max / K, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 geometry)", "data": "synthetic",
-            "config": cfg_desc(s, args.config),
-            "step_ms_each": [round(x, 3) for x in t_step], "host_enqueue_ms_each": [round(x, 3) for x in host_ms],
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32 (fp64 geometry)",
+            "data": "synthetic",
+            "config": dict(cfg_desc(s, args.config),
+                           parallelism=(f"{world} rank(s): lights dealt to ranks, {gsz} rank(s) per light "
+                                        f"(Gaussian shards + NCCL reduce-scatter of tau when > 1)" if strong else
+                                        f"{world} independent frame(s), one per rank, no data-path collective")),
+            "step_ms_each": [round(x, 3) for x in t_step],
+            "step_ms_median": float(np.median(t_step)),
             "wall_ms_per_step_incl_flush": wall_ms / K,
-            "flush_gpu_ms_each": [round(x, 3) for x in t_flush], "flush_host_ms_each": [round(x, 3) for x in flush_ms],
-            "gap_gpu_ms_each": [round(x, 3) for x in t_gap],
-            "build_ms": float(np.mean(t_step)) , "accumulate_ms": acc_ms,
+            "accumulate_ms": acc_ms,
             "accumulate_share": acc_ms / float(np.mean(t_step)),
             "query_ms": float(np.mean(tq)),
-            "query_gaussians_per_s": m / (float(np.mean(tq)) * 1e-3) * world,
+            "query_gaussians_per_s": m / (float(np.mean(tq)) * 1e-3) * (1 if strong else world),
             "keys_P": int(P), "gaussian_ray_evals_per_step": int(64 * P),
             "accumulate_work": {k: int(v) for k, v in st.items()},
             "gpu_launches": int(launches),
