@@ -126,7 +126,7 @@ struct AccLights {
 };
 
 // Compact per-(record, work unit) form, 5 x float4 (80 B):
-//  q0 = (f0, f1, f2, D^2)   f = fl32(d_i - d_c), d_c = tile reference direction
+//  q0 = (f0, f1, f2, r_cut / D^2)   f = fl32(d_i - d_c), d_c = tile reference direction
 //  q1 = (g0, g1, g2, D)
 //  q2 = (W0, W1, W2, W3), q3 = (W4, W5, W6, W7)
 //  q4 = (W8, eD, betap, kD as int bits)
