@@ -37,12 +37,17 @@ sys.path.insert(0, ROOT)
 METRIC = "DGSM build Gaussian-ray evals/s and query Gaussians/s at 1/2/4/8 B200"
 UNIT = "Gaussian-ray evals/s"
 
-# algorithmic FP32-pipe operations of the a6 accumulation (FMA = 1 op; MUFU ops
-# counted as 1), from the formulas of DESIGN.md "a6 algorithmic work"
-OPS_PAIR = 31     # delta, W delta, u, a, g x W delta, |.|^2, 1/a, r
-OPS_LIVE = 30     # u.W delta, s*-D, rsqrt, h, x0, erf(x0), prefactor, window bounds
-OPS_SHELL = 16    # t_k - s*, x_k, erf(x_k), w_k, difference update
-OPS_STEP = 3      # pref (1 - erf(x0)) - prev, update
+# Roofline numerator of the a6 accumulation: SURVEY.md §8(d)'s per-unit figure for
+# the saturation-aware evaluation of one Gaussian-ray pair (texel x listed Gaussian,
+# all K shells): ~70 FP32 ops + ~4 MUFU ops (FMA = 1 op), i.e. 74 ops per pair,
+# times the 64 * P pairs one launch processes.
+OPS_PER_PAIR_SURVEY = 74
+# Work actually needed per pair class (informational): every pair
+# 31 (delta-form test), live pair +30, window shell +16, saturated step +3.
+OPS_PAIR = 31
+OPS_LIVE = 30
+OPS_SHELL = 16
+OPS_STEP = 3
 
 
 def parse():
@@ -288,8 +293,9 @@ def run_dgsm(args):
     sp.run(out=atlas)
     st = sp.stats()
     del sp
-    alg_ops = (OPS_PAIR * st["pairs"] + OPS_LIVE * st["pairs_live"] + OPS_SHELL * st["window_shells"]
-               + OPS_STEP * st["steps"])
+    alg_ops = OPS_PER_PAIR_SURVEY * st["pairs"]
+    needed_ops = (OPS_PAIR * st["pairs"] + OPS_LIVE * st["pairs_live"] + OPS_SHELL * st["window_shells"]
+                  + OPS_STEP * st["steps"])
 
     flush.zero_()  # first touch of the flush buffer is slow (page mapping): keep it out of the timing
     for _ in range(args.warmup):
@@ -427,7 +433,11 @@ def run_dgsm(args):
                          "peak": peak_tops, "unit": "TFLOP/s",
                          "peak_def": f"{n_sm} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (FMA = 1 op)",
                          "frac": achieved / peak_tops, "traffic": traffic,
-                         "alg_ops_per_launch": int(alg_ops)},
+                         "alg_ops_per_launch": int(alg_ops),
+                         "alg_def": f"SURVEY §8(d): {OPS_PER_PAIR_SURVEY} FP32+MUFU ops per Gaussian-ray pair "
+                                    f"x {int(st['pairs'])} pairs",
+                         "needed_ops_per_launch": int(needed_ops),
+                         "needed_ops_frac": needed_ops / (acc_ms * 1e-3) / 1e12 / peak_tops},
             "clocks": clocks,
         }
         if e2e:
