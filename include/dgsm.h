@@ -55,6 +55,8 @@ extern "C" {
                               used by Gaussian-sharded multi-GPU builds before the reduce-scatter */
 #define DGSM_COLLECT_STATS 2u /* count the accumulation work into the run workspace (read it with
                                  dgsm_build_stats); instrumented kernel variant, for roofline accounting */
+#define DGSM_NO_TILE_CULL 4u  /* ablation D: bin every non-excluded Gaussian into every
+                                 tile (no light-space culling); P = L * n * (res/8)^2 keys */
 
 /* Work counted by a DGSM_COLLECT_STATS build. */
 typedef struct dgsm_build_stats {
@@ -87,8 +89,15 @@ typedef struct dgsm_build_opts {
     float k_sigma;     /* footprint k_sigma rule, default 3 (Q6); > 0 */
     float rho_scale;   /* multiplies rho = (H+W)/(2 pi) pixels per radian, default 1 (Q5); > 0 */
     int32_t bin_mode;  /* DGSM_BIN_WRAP (default) or DGSM_BIN_CLAMP */
-    uint32_t flags;    /* DGSM_OUTPUT_TAU or 0 */
+    uint32_t flags;    /* DGSM_OUTPUT_TAU | DGSM_COLLECT_STATS | DGSM_NO_TILE_CULL, or 0 */
+    int32_t absorption; /* DGSM_ABS_* alpha -> beta mapping (ablation B), default TRACEAVG */
 } dgsm_build_opts_t;
+
+/* ---- alpha -> beta mappings, tau* = -ln(1 - alpha) ----------- */
+#define DGSM_ABS_TRACEAVG 0 /* kappa tau* sqrt(tr A / 3) / sqrt(2 pi)       (Eq.5, default)      */
+#define DGSM_ABS_SIMPLE 1   /* kappa tau*                                   (mapping 1)          */
+#define DGSM_ABS_MASS 2     /* kappa tau* / ((2 pi)^{3/2} sqrt(det Sigma))  (mapping 3, Q14)     */
+#define DGSM_ABS_DIAG 3     /* kappa tau* / ((2 pi)^{3/2} s_x s_y s_z)      (mapping 4)          */
 
 /* Host-side plan: filled by dgsm_build_plan, consumed by dgsm_build_run.
  * Caller-owned plain struct; treat the fields as read-only. */

@@ -81,6 +81,39 @@ double or_beta(const float s3[3], const float q4[4], float alpha, double kappa)
     return kappa * tau_star * sqrt(trA / 3.0) / sqrt(2.0 * OR_PI);
 }
 
+/* Ablation B alpha -> beta mappings, tau* = -ln(1 - alpha):
+ *   0 TraceAvg  beta = kappa tau* sqrt(tr(A)/3) / sqrt(2 pi)       (Eq.5, the default)
+ *   1 Simple    beta = kappa tau*                                   (mapping 1)
+ *   2 Mass      beta = kappa tau* / ((2 pi)^{3/2} sqrt(det Sigma))  (mapping 3, unit-mass
+ *               reading of the garbled "A is the covariance", Q14)
+ *   3 Diag      beta = kappa tau* / ((2 pi)^{3/2} s_x s_y s_z)      (mapping 4)
+ * Mass and Diag coincide for Sigma = R diag(s^2) R^T; both are kept because
+ * the paper lists both. */
+double or_beta_mode(const float s3[3], const float q4[4], float alpha, double kappa, int mode)
+{
+    double tau_star = -log1p(-or_alpha_clamped(alpha));
+    if (mode == 0) return or_beta(s3, q4, alpha, kappa);
+    if (mode == 1) return kappa * tau_star;
+    double two_pi_32 = pow(2.0 * OR_PI, 1.5);
+    if (mode == 2) {
+        /* det Sigma from the explicit covariance R diag(s^2) R^T */
+        double R[3][3], S[3][3];
+        or_rotation(q4, R);
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) {
+                double acc = 0.0;
+                for (int j = 0; j < 3; ++j)
+                    acc += R[r][j] * ((double)s3[j] * (double)s3[j]) * R[c][j];
+                S[r][c] = acc;
+            }
+        double det = S[0][0] * (S[1][1] * S[2][2] - S[1][2] * S[2][1]) -
+                     S[0][1] * (S[1][0] * S[2][2] - S[1][2] * S[2][0]) +
+                     S[0][2] * (S[1][0] * S[2][1] - S[1][1] * S[2][0]);
+        return kappa * tau_star / (two_pi_32 * sqrt(det));
+    }
+    return kappa * tau_star / (two_pi_32 * ((double)s3[0] * (double)s3[1] * (double)s3[2]));
+}
+
 void or_calibrate(const float* scales, const float* rotations, const float* opacities,
                   int64_t n, double kappa, double* beta_out)
 {
@@ -423,8 +456,8 @@ static void* or_build_worker(void* arg)
 int64_t or_build(const float* means, const float* scales, const float* rotations,
                  const float* opacities, int64_t n, const float* light_pos, const float* t_max,
                  int L, int res, int K, double kappa, double k_sigma, double rho_scale,
-                 int bin_mode, int culled, int64_t tile_stride, int n_threads, double* T_out,
-                 int64_t* evals_out /* nullable: (texel, Gaussian) evaluations performed */)
+                 int bin_mode, int culled, int absorption, int64_t tile_stride, int n_threads,
+                 double* T_out, int64_t* evals_out /* nullable: (texel, Gaussian) evaluations performed */)
 {
     if (res < 8 || res % 8 != 0 || K < 1 || L < 1 || n < 0) return -1;
     or_build_ctx c;
@@ -445,7 +478,7 @@ int64_t or_build(const float* means, const float* scales, const float* rotations
         double Ai[3][3];
         or_precision(scales + 3 * i, rotations + 4 * i, Ai);
         memcpy(c.A + 9 * i, Ai, sizeof(Ai));
-        c.beta[i] = or_beta(scales + 3 * i, rotations + 4 * i, opacities[i], kappa);
+        c.beta[i] = or_beta_mode(scales + 3 * i, rotations + 4 * i, opacities[i], kappa, absorption);
     }
     c.excluded = (unsigned char*)calloc((size_t)L * (n > 0 ? n : 1), 1);
     for (int l = 0; l < L; ++l)

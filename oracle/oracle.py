@@ -58,8 +58,10 @@ def lib():
         L.or_segment_depth.argtypes = [C.c_double] * 5
         L.or_build.restype = C.c_int64
         L.or_build.argtypes = [fp, fp, fp, fp, C.c_int64, fp, fp, C.c_int, C.c_int, C.c_int,
-                               C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int64,
+                               C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int64,
                                C.c_int, dp, i64p]
+        L.or_beta_mode.restype = C.c_double
+        L.or_beta_mode.argtypes = [fp, fp, C.c_float, C.c_double, C.c_int]
         L.or_tau_ray.restype = C.c_double
         L.or_tau_ray.argtypes = [fp, fp, fp, fp, C.c_int64, dp, dp, C.c_double, C.c_double]
         L.or_query.argtypes = [dp, C.c_int, C.c_int, C.c_int, fp, fp, fp, C.c_int64, dp, dp]
@@ -86,12 +88,16 @@ def _opt(x) -> float:
 
 
 BIN_WRAP, BIN_CLAMP = 0, 1
+ABS_TRACEAVG, ABS_SIMPLE, ABS_MASS, ABS_DIAG = 0, 1, 2, 3
+ABSORPTION = {"traceavg": 0, "simple": 1, "mass": 2, "diag": 3}
 
 
-def beta(scales, rotation, alpha, kappa=1.0) -> float:
-    """Eq.5 for one Gaussian."""
+def beta(scales, rotation, alpha, kappa=1.0, mode=ABS_TRACEAVG) -> float:
+    """Eq.5 for one Gaussian; other modes: ablation B."""
     s, q = _f32(scales), _f32(rotation)
-    return lib().or_beta(_p(s, C.c_float), _p(q, C.c_float), float(alpha), float(kappa))
+    if mode == ABS_TRACEAVG:
+        return lib().or_beta(_p(s, C.c_float), _p(q, C.c_float), float(alpha), float(kappa))
+    return lib().or_beta_mode(_p(s, C.c_float), _p(q, C.c_float), float(alpha), float(kappa), int(mode))
 
 
 def oct_encode(d):
@@ -170,12 +176,14 @@ def tau_ray(g, o, d, t, kappa=1.0) -> float:
 
 
 def build(g, lights, res, K, kappa=1.0, k_sigma=3.0, rho_scale=1.0, bin_mode=BIN_WRAP,
-          culled=True, tile_stride=1, n_threads=None, return_evals=False):
+          culled=True, tile_stride=1, n_threads=None, return_evals=False, absorption="traceavg"):
     """R8: the atlas T[L][K][res][res] in float64 (NaN where skipped by tile_stride).
 
     ``g``: dict of means [n,3], scales [n,3], rotations [n,4] (w,x,y,z), opacities [n].
     ``lights``: dict(position [L,3], t_max [L]).
+    ``absorption``: traceavg (Eq.5) | simple | mass | diag (ablation B).
     Returns (T, P) with P the number of binned entries (culled mode)."""
+    mode = ABSORPTION[absorption] if isinstance(absorption, str) else int(absorption)
     mu, s, q, a = _f32(g["means"]), _f32(g["scales"]), _f32(g["rotations"]), _f32(g["opacities"])
     lp, tm = _f32(lights["position"]).reshape(-1, 3), _f32(lights["t_max"]).reshape(-1)
     L = lp.shape[0]
@@ -185,7 +193,7 @@ def build(g, lights, res, K, kappa=1.0, k_sigma=3.0, rho_scale=1.0, bin_mode=BIN
     P = lib().or_build(_p(mu, C.c_float), _p(s, C.c_float), _p(q, C.c_float), _p(a, C.c_float),
                        mu.shape[0], _p(lp, C.c_float), _p(tm, C.c_float), L, int(res), int(K),
                        _opt(kappa), _opt(k_sigma), _opt(rho_scale), int(bin_mode),
-                       int(bool(culled)), int(tile_stride), int(n_threads), _p(T, C.c_double),
+                       int(bool(culled)), mode, int(tile_stride), int(n_threads), _p(T, C.c_double),
                        C.byref(evals))
     if P < 0:
         raise ValueError("oracle build: invalid arguments")

@@ -163,7 +163,9 @@ int validate(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int L, int r
     if (!(o.kappa > 0.0f) || !(o.k_sigma > 0.0f) || !(o.rho_scale > 0.0f))
         return fail(DGSM_EINVAL, "kappa, k_sigma, rho_scale must be > 0");
     if (o.bin_mode != DGSM_BIN_WRAP && o.bin_mode != DGSM_BIN_CLAMP) return fail(DGSM_EINVAL, "bad bin_mode");
-    if (o.flags & ~(DGSM_OUTPUT_TAU | DGSM_COLLECT_STATS)) return fail(DGSM_EINVAL, "unknown flags");
+    if (o.flags & ~(DGSM_OUTPUT_TAU | DGSM_COLLECT_STATS | DGSM_NO_TILE_CULL))
+        return fail(DGSM_EINVAL, "unknown flags");
+    if (o.absorption < DGSM_ABS_TRACEAVG || o.absorption > DGSM_ABS_DIAG) return fail(DGSM_EINVAL, "bad absorption");
     return DGSM_OK;
 }
 
@@ -186,6 +188,7 @@ void dgsm_default_opts(dgsm_build_opts_t* o) {
     o->rho_scale = 1.0f;
     o->bin_mode = DGSM_BIN_WRAP;
     o->flags = 0u;
+    o->absorption = DGSM_ABS_TRACEAVG;
 }
 
 size_t dgsm_plan_workspace_bytes(int64_t n, int n_lights) {

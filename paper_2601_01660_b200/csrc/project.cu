@@ -18,7 +18,8 @@ __global__ void __launch_bounds__(256, 3) k_project(
     const float* __restrict__ means, const float* __restrict__ scales,
     const float* __restrict__ rotations, const float* __restrict__ opacities, int64_t n,
     LightsParam lp, int n_lights, int res, int K, double kappa, double k_sigma, double rho,
-    int bin_mode, PairRec* __restrict__ recs, uint32_t* __restrict__ counts, uint4* __restrict__ dup,
+    int bin_mode, int absorption, bool no_cull, PairRec* __restrict__ recs, uint32_t* __restrict__ counts,
+    uint4* __restrict__ dup,
     PlanStats* stats) {
     __shared__ uint32_t s_dmin[DGSM_MAX_LIGHTS], s_dmax[DGSM_MAX_LIGHTS];
     if (threadIdx.x < DGSM_MAX_LIGHTS) { s_dmin[threadIdx.x] = 0xffffffffu; s_dmax[threadIdx.x] = 0u; }
@@ -91,6 +92,9 @@ __global__ void __launch_bounds__(256, 3) k_project(
         if (c1 > 2.0 * W - 1.0) c1 = 2.0 * W - 1.0;
         if (r0 < -(double)H) r0 = -(double)H;
         if (r1 > 2.0 * H - 1.0) r1 = 2.0 * H - 1.0;
+        if (no_cull) {  // ablation D: every tile of the atlas
+            c0 = 0.0; c1 = W - 1.0; r0 = 0.0; r1 = H - 1.0;
+        }
         const int ic0 = (int)c0, ic1 = (int)c1, ir0 = (int)r0, ir1 = (int)r1;
         if (ic0 > ic1 || ir0 > ir1) {
             cnt = 0;
@@ -127,7 +131,12 @@ __global__ void __launch_bounds__(256, 3) k_project(
             alpha = alpha < 1e-4 ? 1e-4 : (alpha > 1.0 - 1e-4 ? 1.0 - 1e-4 : alpha);
             const double tau_star = -log1p(-alpha);
             const double trA = inv_s[0] * inv_s[0] + inv_s[1] * inv_s[1] + inv_s[2] * inv_s[2];
-            rec.betap = (float)(kappa * tau_star * sqrt(trA / 3.0) * 0.5);
+            // beta * sqrt(pi/2) for the chosen alpha -> beta mapping (ablation B)
+            double betap;
+            if (absorption == DGSM_ABS_SIMPLE) betap = kappa * tau_star * 1.2533141373155003;  // sqrt(pi/2)
+            else if (absorption == DGSM_ABS_TRACEAVG) betap = kappa * tau_star * sqrt(trA / 3.0) * 0.5;
+            else betap = kappa * tau_star * (inv_s[0] * inv_s[1] * inv_s[2]) * (1.0 / (4.0 * kPi));  // MASS, DIAG
+            rec.betap = (float)betap;
             dbits = __float_as_uint(Df);
         }
     }
@@ -167,7 +176,8 @@ void launch_project(const dgsm_gaussians_t& g, const LightsParam& lp, int n_ligh
     k_project<<<(unsigned)grid, bs, 0, s>>>(g.means, g.scales, g.rotations, g.opacities, g.n, lp,
                                             n_lights, res, K, (double)o.kappa, (double)o.k_sigma,
                                             (double)o.rho_scale * (double)(2 * res) / (2.0 * kPi), o.bin_mode,
-                                            recs, counts, dup, stats);
+                                            o.absorption, (o.flags & DGSM_NO_TILE_CULL) != 0, recs, counts, dup,
+                                            stats);
 }
 
 }  // namespace dgsm

@@ -26,6 +26,8 @@ DGSM_MAX_LIGHTS = 64
 DGSM_BIN_WRAP, DGSM_BIN_CLAMP = 0, 1
 DGSM_OUTPUT_TAU = 1
 DGSM_COLLECT_STATS = 2
+DGSM_NO_TILE_CULL = 4
+ABSORPTION = {"traceavg": 0, "simple": 1, "mass": 2, "diag": 3}
 _STATUS = {0: "DGSM_OK", 1: "DGSM_EINVAL", 2: "DGSM_ENOSPC", 3: "DGSM_ECUDA", 4: "DGSM_ERANGE"}
 
 EXPORTED = ["dgsm_default_opts", "dgsm_plan_workspace_bytes", "dgsm_build_plan", "dgsm_build_run",
@@ -44,7 +46,7 @@ class Light(C.Structure):
 
 class BuildOpts(C.Structure):
     _fields_ = [("kappa", C.c_float), ("k_sigma", C.c_float), ("rho_scale", C.c_float),
-                ("bin_mode", C.c_int32), ("flags", C.c_uint32)]
+                ("bin_mode", C.c_int32), ("flags", C.c_uint32), ("absorption", C.c_int32)]
 
 
 class Plan(C.Structure):
@@ -176,12 +178,18 @@ class Options:
     bin_mode: str = "wrap"
     output_tau: bool = False
     collect_stats: bool = False
+    absorption: str = "traceavg"   # traceavg (Eq.5) | simple | mass | diag (ablation B)
+    tile_cull: bool = True         # False: ablation D, every Gaussian in every tile
 
     def c(self) -> BuildOpts:
+        if self.absorption not in ABSORPTION:
+            raise DgsmError(f"absorption must be one of {sorted(ABSORPTION)}")
         return BuildOpts(self.kappa, self.k_sigma, self.rho_scale,
                          DGSM_BIN_WRAP if self.bin_mode == "wrap" else DGSM_BIN_CLAMP,
                          (DGSM_OUTPUT_TAU if self.output_tau else 0) |
-                         (DGSM_COLLECT_STATS if self.collect_stats else 0))
+                         (DGSM_COLLECT_STATS if self.collect_stats else 0) |
+                         (0 if self.tile_cull else DGSM_NO_TILE_CULL),
+                         ABSORPTION[self.absorption])
 
 
 def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:

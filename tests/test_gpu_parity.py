@@ -113,6 +113,25 @@ def test_build_parity_options(dg, oracle_mod, opt):
     assert np.abs(T - To).max() <= TOL_T
 
 
+@pytest.mark.parametrize("mode", ["simple", "mass", "diag"])
+def test_build_parity_absorption_modes(dg, oracle_mod, mode):
+    """Ablation B alpha -> beta mappings through the C ABI."""
+    s = synth.config1_seam("corner")
+    T = dg.build(dg.to_device(s.gaussians), s.lights, s.res, s.K, dg.Options(absorption=mode)).cpu().numpy()
+    To, _ = oracle_mod.build(s.gaussians, s.lights, s.res, s.K, absorption=mode)
+    assert np.abs(T - To).max() <= TOL_T
+
+
+def test_build_parity_unculled(dg, oracle_mod):
+    """Ablation D: no light-space culling, every Gaussian at every texel."""
+    s = synth.random_scene(21, 150, res=32, K=8, L=2, dist=(0.4, 3.0), scale=(0.02, 0.4))
+    T = dg.build(dg.to_device(s.gaussians), s.lights, s.res, s.K, dg.Options(tile_cull=False)).cpu().numpy()
+    To, _ = oracle_mod.build(s.gaussians, s.lights, s.res, s.K, culled=False)
+    assert np.abs(T - To).max() <= TOL_T
+    Tc = dg.build(dg.to_device(s.gaussians), s.lights, s.res, s.K).cpu().numpy()
+    assert (Tc >= T - 1e-6).all()  # culling only drops occluders
+
+
 def test_build_invariants_and_determinism(dg):
     s = synth.config1()
     g = dg.to_device(s.gaussians)

@@ -108,6 +108,33 @@ def test_beta_properties(oracle_mod):
         assert math.isclose(full, -math.log(1 - float(np.float32(0.4))), rel_tol=1e-9)
 
 
+def test_beta_ablation_modes(oracle_mod):
+    """Ablation B (P:L319-329): Simple ignores the covariance (SPEC S:L211);
+    Mass/Diag are the unit-mass calibration: the 3D integral of
+    beta exp(-x^T A x / 2) is kappa tau* (checked by a grid sum over a rotated,
+    anisotropic Gaussian); Mass == Diag for Sigma = R diag(s^2) R^T."""
+    al, kappa = 0.37, 1.7
+    tstar = -math.log1p(-float(np.float32(al)))
+    b1 = oracle_mod.beta([1, 1, 1], [1, 0, 0, 0], al, kappa, oracle_mod.ABS_SIMPLE)
+    b2 = oracle_mod.beta([5, 1, 0.1], [0.3, 0.2, 0.1, 0.9], al, kappa, oracle_mod.ABS_SIMPLE)
+    assert b1 == b2 and math.isclose(b1, float(np.float32(kappa)) * tstar, rel_tol=1e-6)
+    rng = np.random.default_rng(8)
+    for _ in range(3):
+        s = np.exp(rng.uniform(np.log(0.3), np.log(1.0), 3)).astype(np.float32)
+        q = synth.random_quaternions(rng, 1)[0].astype(np.float32)
+        bm = oracle_mod.beta(s, q, al, kappa, oracle_mod.ABS_MASS)
+        bd = oracle_mod.beta(s, q, al, kappa, oracle_mod.ABS_DIAG)
+        assert math.isclose(bm, bd, rel_tol=1e-9)
+        R = synth.quaternion_to_matrix(q[None].astype(np.float64))[0]
+        A = R @ np.diag(1.0 / s.astype(np.float64) ** 2) @ R.T
+        h = 0.05
+        g = np.arange(-6.5, 6.5 + h / 2, h)
+        X, Y, Z = np.meshgrid(g, g, g, indexing="ij")
+        P = np.stack([X, Y, Z], -1)
+        mass = bd * np.exp(-0.5 * np.einsum("...i,ij,...j->...", P, A, P)).sum() * h ** 3
+        assert math.isclose(mass, kappa * tstar, rel_tol=1e-6)
+
+
 # ------------------------------------------------------------ octahedral
 def test_oct_spec(oracle_mod):
     for d, uv in GOLD["oct_encode"]["cases"]:
