@@ -44,6 +44,7 @@ extern "C" {
 
 #define DGSM_MAX_LIGHTS 64
 #define DGSM_MAX_SHELLS 256
+#define DGSM_MAX_FOOTPRINT_SAMPLES 64
 
 /* ---- binning mode (R6, Q8) ---------------------------------------------- */
 #define DGSM_BIN_WRAP 0   /* default: footprints crossing the atlas border are mirror-wrapped
@@ -182,6 +183,26 @@ int dgsm_exp_epilogue(const float* tau, float* T, int64_t count, void* stream);
 int dgsm_query(const float* atlas, const dgsm_light_t* lights, int n_lights, int atlas_res,
                int n_shells, const float* positions, int64_t m, float* T_out, float* colors_inout,
                void* stream);
+
+/* Footprint-sampled query ("rather than
+ * integrating over each receiver's footprint", "sampling only the
+ * Gaussian center ... tends to underestimate soft shadowing").  For receiver
+ * Gaussian g (mean mu_g, scales s_g, quaternion q_g = (w, x, y, z), normalised
+ * here, R_g its rotation):
+ *   T_out[g] = prod_l sum_i weights[i] * T_l(mu_g + R_g (s_g . offsets[i]))
+ * with T_l the trilinear sample of dgsm_query.  offsets are standard-normal
+ * points z_i (e.g. a 7-point stencil {0, +-delta e_j} or Monte Carlo draws),
+ * weights w_i (normally summing to 1); both are HOST arrays copied into the
+ * kernel parameters, 1 <= n_samples <= DGSM_MAX_FOOTPRINT_SAMPLES.
+ * offsets = {0,0,0}, weights = {1}, n_samples = 1 equals dgsm_query at mu_g.
+ *   means/scales device float [m][3], rotations device float [m][4],
+ *   T_out device float [m], colors_inout as in dgsm_query.
+ * Errors: DGSM_EINVAL as dgsm_query, plus null offsets/weights or n_samples
+ * outside [1, DGSM_MAX_FOOTPRINT_SAMPLES]. */
+int dgsm_query_footprint(const float* atlas, const dgsm_light_t* lights, int n_lights, int atlas_res,
+                         int n_shells, const float* means, const float* scales, const float* rotations,
+                         int64_t m, const float* offsets, const float* weights, int n_samples,
+                         float* T_out, float* colors_inout, void* stream);
 
 /* Read the counters of the last DGSM_COLLECT_STATS dgsm_build_run that used
  * this run workspace (synchronises `stream`). */

@@ -602,3 +602,38 @@ void or_query(const double* atlas /* [L][K][res][res] */, int L, int K, int res,
         }
     }
 }
+
+/* ------------------------------------------------------------------ */
+/* NEXT-2: footprint-sampled query ("sampling a small footprint  */
+/* around each Gaussian center and averaging deep-shadow lookups";       */
+/* P:L308-317 ablation A: x_{g,i} = mu_g + R_g (s_g (.) z_i),            */
+/* T_g = sum_i w_i T(x_{g,i}), sum_i w_i = 1).  Per light the footprint   */
+/* average, then the product over lights (Q13).  The        */
+/* offsets z_i and weights w_i are inputs (stencil or Monte Carlo draws). */
+/* ------------------------------------------------------------------ */
+void or_query_footprint(const double* atlas, int L, int K, int res, const float* light_pos,
+                        const float* t_max, const float* means, const float* scales,
+                        const float* rotations, int64_t m, const double* z /* [n][3] */,
+                        const double* w /* [n] */, int n, double* T_out)
+{
+    int64_t per_light = (int64_t)K * res * res;
+    for (int64_t g = 0; g < m; ++g) {
+        double R[3][3];
+        or_rotation(rotations + 4 * g, R);
+        double T = 1.0;
+        for (int l = 0; l < L; ++l) {
+            double o[3] = {light_pos[3 * l], light_pos[3 * l + 1], light_pos[3 * l + 2]};
+            double acc = 0.0;
+            for (int i = 0; i < n; ++i) {
+                double x[3];
+                for (int r = 0; r < 3; ++r) {
+                    x[r] = means[3 * g + r];
+                    for (int c = 0; c < 3; ++c) x[r] += R[r][c] * ((double)scales[3 * g + c] * z[3 * i + c]);
+                }
+                acc += w[i] * or_sample(atlas + l * per_light, res, K, o, t_max[l], x);
+            }
+            T *= acc;
+        }
+        T_out[g] = T;
+    }
+}

@@ -60,6 +60,8 @@ def lib():
         L.or_build.argtypes = [fp, fp, fp, fp, C.c_int64, fp, fp, C.c_int, C.c_int, C.c_int,
                                C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int64,
                                C.c_int, dp, i64p]
+        L.or_query_footprint.argtypes = [dp, C.c_int, C.c_int, C.c_int, fp, fp, fp, fp, fp, C.c_int64,
+                                         dp, dp, C.c_int, dp]
         L.or_beta_mode.restype = C.c_double
         L.or_beta_mode.argtypes = [fp, fp, C.c_float, C.c_double, C.c_int]
         L.or_tau_ray.restype = C.c_double
@@ -214,3 +216,32 @@ def query(atlas, lights, positions, colors=None):
                    _p(x, C.c_float), x.shape[0], _p(out, C.c_double),
                    None if col is None else _p(col, C.c_double))
     return (out, col) if colors is not None else out
+
+
+def stencil7(delta=1.0):
+    """Deterministic 7-point footprint stencil: offsets
+    {0, +-delta e_1, +-delta e_2, +-delta e_3} in the principal-axes frame,
+    weights proportional to exp(-|z|^2/2), normalised to sum 1."""
+    z = [[0.0, 0.0, 0.0]]
+    for j in range(3):
+        for sgn in (1.0, -1.0):
+            e = [0.0, 0.0, 0.0]
+            e[j] = sgn * delta
+            z.append(e)
+    z = np.array(z)
+    w = np.exp(-0.5 * (z ** 2).sum(1))
+    return z, w / w.sum()
+
+
+def query_footprint(atlas, lights, g, z, w):
+    """NEXT-2: T_g = prod_l sum_i w_i T_l(mu_g + R_g (s_g * z_i))."""
+    at = _f64(atlas)
+    L, K, res = at.shape[0], at.shape[1], at.shape[2]
+    lp, tm = _f32(lights["position"]).reshape(-1, 3), _f32(lights["t_max"]).reshape(-1)
+    mu, s, q = _f32(g["means"]).reshape(-1, 3), _f32(g["scales"]).reshape(-1, 3), _f32(g["rotations"]).reshape(-1, 4)
+    z, w = _f64(z).reshape(-1, 3), _f64(w).reshape(-1)
+    out = np.zeros(mu.shape[0])
+    lib().or_query_footprint(_p(at, C.c_double), L, K, res, _p(lp, C.c_float), _p(tm, C.c_float),
+                             _p(mu, C.c_float), _p(s, C.c_float), _p(q, C.c_float), mu.shape[0],
+                             _p(z, C.c_double), _p(w, C.c_double), z.shape[0], _p(out, C.c_double))
+    return out

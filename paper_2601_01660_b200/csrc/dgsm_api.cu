@@ -382,21 +382,50 @@ int dgsm_exp_epilogue(const float* tau, float* T, int64_t count, void* stream) {
     return cuda_check("exp epilogue");
 }
 
-int dgsm_query(const float* atlas, const dgsm_light_t* lights, int n_lights, int atlas_res, int n_shells,
-               const float* positions, int64_t m, float* T_out, float* colors_inout, void* stream) {
-    g_launches = 0;
+static int check_query_args(const float* atlas, const dgsm_light_t* lights, int n_lights, int atlas_res,
+                            int n_shells, int64_t m) {
     if (!lights) return fail(DGSM_EINVAL, "null lights");
     if (n_lights < 1 || n_lights > DGSM_MAX_LIGHTS) return fail(DGSM_EINVAL, "n_lights %d outside [1, %d]", n_lights, DGSM_MAX_LIGHTS);
     if (atlas_res < 8 || atlas_res % 8 != 0 || atlas_res > 2048) return fail(DGSM_EINVAL, "bad atlas_res %d", atlas_res);
     if (n_shells < 1 || n_shells > DGSM_MAX_SHELLS) return fail(DGSM_EINVAL, "bad n_shells %d", n_shells);
     if (m < 0) return fail(DGSM_EINVAL, "m < 0");
-    if (m > 0 && (!atlas || !positions || !T_out)) return fail(DGSM_EINVAL, "null atlas, positions or T_out");
+    if (m > 0 && !atlas) return fail(DGSM_EINVAL, "null atlas");
     for (int l = 0; l < n_lights; ++l)
         if (!(lights[l].t_max > 0.0f)) return fail(DGSM_EINVAL, "light %d: t_max <= 0", l);
+    return DGSM_OK;
+}
+
+int dgsm_query(const float* atlas, const dgsm_light_t* lights, int n_lights, int atlas_res, int n_shells,
+               const float* positions, int64_t m, float* T_out, float* colors_inout, void* stream) {
+    g_launches = 0;
+    if (int rc = check_query_args(atlas, lights, n_lights, atlas_res, n_shells, m)) return rc;
+    if (m > 0 && (!positions || !T_out)) return fail(DGSM_EINVAL, "null positions or T_out");
     const LightsParam lp = lights_param(lights, n_lights);
     launch_query(atlas, lp, n_lights, atlas_res, n_shells, positions, m, T_out, colors_inout, (cudaStream_t)stream);
     g_launches = m > 0 ? 1 : 0;
     return cuda_check("query");
+}
+
+int dgsm_query_footprint(const float* atlas, const dgsm_light_t* lights, int n_lights, int atlas_res,
+                         int n_shells, const float* means, const float* scales, const float* rotations, int64_t m,
+                         const float* offsets, const float* weights, int n_samples, float* T_out,
+                         float* colors_inout, void* stream) {
+    g_launches = 0;
+    if (int rc = check_query_args(atlas, lights, n_lights, atlas_res, n_shells, m)) return rc;
+    if (m > 0 && (!means || !scales || !rotations || !T_out))
+        return fail(DGSM_EINVAL, "null means, scales, rotations or T_out");
+    if (!offsets || !weights) return fail(DGSM_EINVAL, "null offsets or weights");
+    if (n_samples < 1 || n_samples > DGSM_MAX_FOOTPRINT_SAMPLES)
+        return fail(DGSM_EINVAL, "n_samples %d outside [1, %d]", n_samples, DGSM_MAX_FOOTPRINT_SAMPLES);
+    FootprintParam fp;
+    fp.n = n_samples;
+    for (int i = 0; i < n_samples; ++i)
+        fp.zw[i] = make_float4(offsets[3 * i], offsets[3 * i + 1], offsets[3 * i + 2], weights[i]);
+    const LightsParam lp = lights_param(lights, n_lights);
+    launch_query_footprint(atlas, lp, fp, n_lights, atlas_res, n_shells, means, scales, rotations, m, T_out,
+                           colors_inout, (cudaStream_t)stream);
+    g_launches = m > 0 ? 1 : 0;
+    return cuda_check("query footprint");
 }
 
 int dgsm_set_accumulate_events(void* before, void* after) {

@@ -30,6 +30,12 @@ struct LightsParam {
     float4 l[DGSM_MAX_LIGHTS];  // xyz = o_L, w = t_max
 };
 
+// Footprint-query samples (NEXT-2): xyz = standard-normal offset z_i, w = weight.
+struct FootprintParam {
+    int n;
+    float4 zw[DGSM_MAX_FOOTPRINT_SAMPLES];
+};
+
 // Device-side statistics of a plan, copied back to the host once.
 struct PlanStats {
     uint32_t depth_min[DGSM_MAX_LIGHTS];
@@ -159,4 +165,7 @@ void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint3
 void launch_exp(const float* tau, float* T, int64_t count, cudaStream_t s);
 void launch_query(const float* atlas, const LightsParam& lp, int n_lights, int res, int K,
                   const float* positions, int64_t m, float* T_out, float* colors, cudaStream_t s);
+void launch_query_footprint(const float* atlas, const LightsParam& lp, const FootprintParam& fp, int n_lights,
+                            int res, int K, const float* means, const float* scales, const float* rotations,
+                            int64_t m, float* T_out, float* colors, cudaStream_t s);
 }  // namespace dgsm

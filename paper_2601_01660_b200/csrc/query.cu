@@ -17,62 +17,118 @@ __device__ __forceinline__ void wrap_tap(int& col, int& row, int W, int H) {
     else if (row > H - 1) { row = 2 * H - 1 - row; col = W - 1 - col; }
 }
 
+// Trilinear T_l at x (fp64 position): octahedral bilinear x radial linear.
+__device__ __forceinline__ float sample_light(const float* __restrict__ A, const float4 L, int res, int K,
+                                              double px, double py, double pz) {
+    const int W = res, H = res;
+    const size_t plane = (size_t)H * W;
+    const double mx = px - (double)L.x;
+    const double my = py - (double)L.y;
+    const double mz = pz - (double)L.z;
+    const double t = sqrt((mx * mx + my * my) + mz * mz);
+    if (t == 0.0) return 1.0f;
+    const double n1 = (fabs(mx) + fabs(my)) + fabs(mz);
+    const double qx = mx / n1, qy = my / n1, qz = mz / n1;
+    double u, v;
+    if (qz >= 0.0) { u = qx; v = qy; }
+    else {
+        u = (qx >= 0.0 ? 1.0 : -1.0) * (1.0 - fabs(qy));
+        v = (qy >= 0.0 ? 1.0 : -1.0) * (1.0 - fabs(qx));
+    }
+    const double fx = (u + 1.0) * (0.5 * W) - 0.5;
+    const double fy = (v + 1.0) * (0.5 * H) - 0.5;
+    const double x0 = floor(fx), y0 = floor(fy);
+    const float wx = (float)(fx - x0), wy = (float)(fy - y0);
+    double fk = (t * K) / (double)L.w - 0.5;
+    fk = fk < 0.0 ? 0.0 : (fk > K - 1 ? (double)(K - 1) : fk);
+    const double k0d = floor(fk);
+    const float wk = (float)(fk - k0d);
+    const int k0 = (int)k0d, k1 = k0 + 1 < K ? k0 + 1 : K - 1;
+    const float* A0 = A + (size_t)k0 * plane;
+    const float* A1 = A + (size_t)k1 * plane;
+    float acc = 0.0f;
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx) {
+            int c = (int)x0 + dx, r = (int)y0 + dy;
+            wrap_tap(c, r, W, H);
+            const size_t o = (size_t)r * W + c;
+            const float wxy = (dx ? wx : 1.0f - wx) * (dy ? wy : 1.0f - wy);
+            acc = fmaf(wxy * (1.0f - wk), __ldg(A0 + o), acc);
+            acc = fmaf(wxy * wk, __ldg(A1 + o), acc);
+        }
+    return acc;
+}
+
+__device__ __forceinline__ void apply_colors(float* colors, int64_t q, float T) {
+    if (colors) {
+        colors[3 * q] *= T;
+        colors[3 * q + 1] *= T;
+        colors[3 * q + 2] *= T;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_query(const float* __restrict__ atlas, LightsParam lp,
                                                int n_lights, int res, int K,
                                                const float* __restrict__ pos, int64_t m,
                                                float* __restrict__ T_out, float* __restrict__ colors) {
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= m) return;
-    const float px = __ldg(pos + 3 * q), py = __ldg(pos + 3 * q + 1), pz = __ldg(pos + 3 * q + 2);
-    const int W = res, H = res;
-    const size_t plane = (size_t)H * W;
+    const double px = __ldg(pos + 3 * q), py = __ldg(pos + 3 * q + 1), pz = __ldg(pos + 3 * q + 2);
+    const size_t per_light = (size_t)K * res * res;
+    float T = 1.0f;
+    for (int l = 0; l < n_lights; ++l) T *= sample_light(atlas + l * per_light, lp.l[l], res, K, px, py, pz);
+    T_out[q] = T;
+    apply_colors(colors, q, T);
+}
+
+// NEXT-2 ("sampling only at Gaussian centers ... rather than integrating
+// over each receiver's footprint"; "sampling only the Gaussian center
+// ... tends to underestimate soft shadowing"): the receiver's transmittance is
+// the footprint average  T_g = prod_l sum_i w_i T_l(mu_g + R_g (s_g . z_i))
+// over caller-given standard-normal offsets z_i (a quadrature stencil or Monte
+// Carlo draws).  R_g and the sample points in fp64, like the oracle; the
+// offsets live in the kernel parameters (<= 64 samples).
+__global__ void __launch_bounds__(128) k_query_footprint(const float* __restrict__ atlas, LightsParam lp,
+                                                         FootprintParam fp, int n_lights, int res, int K,
+                                                         const float* __restrict__ means,
+                                                         const float* __restrict__ scales,
+                                                         const float* __restrict__ rots, int64_t m,
+                                                         float* __restrict__ T_out, float* __restrict__ colors) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= m) return;
+    const double mx = __ldg(means + 3 * g), my = __ldg(means + 3 * g + 1), mz = __ldg(means + 3 * g + 2);
+    const double sx = __ldg(scales + 3 * g), sy = __ldg(scales + 3 * g + 1), sz = __ldg(scales + 3 * g + 2);
+    double qw = __ldg(rots + 4 * g), qx = __ldg(rots + 4 * g + 1), qy = __ldg(rots + 4 * g + 2),
+           qz = __ldg(rots + 4 * g + 3);
+    const double qn = sqrt(((qw * qw + qx * qx) + qy * qy) + qz * qz);
+    qw /= qn; qx /= qn; qy /= qn; qz /= qn;
+    // columns of R scaled by s: M = R diag(s)
+    const double m00 = (1.0 - 2.0 * (qy * qy + qz * qz)) * sx, m01 = 2.0 * (qx * qy - qw * qz) * sy,
+                 m02 = 2.0 * (qx * qz + qw * qy) * sz;
+    const double m10 = 2.0 * (qx * qy + qw * qz) * sx, m11 = (1.0 - 2.0 * (qx * qx + qz * qz)) * sy,
+                 m12 = 2.0 * (qy * qz - qw * qx) * sz;
+    const double m20 = 2.0 * (qx * qz - qw * qy) * sx, m21 = 2.0 * (qy * qz + qw * qx) * sy,
+                 m22 = (1.0 - 2.0 * (qx * qx + qy * qy)) * sz;
+    const size_t per_light = (size_t)K * res * res;
     float T = 1.0f;
     for (int l = 0; l < n_lights; ++l) {
+        const float* A = atlas + l * per_light;
         const float4 L = lp.l[l];
-        const double mx = (double)px - (double)L.x;
-        const double my = (double)py - (double)L.y;
-        const double mz = (double)pz - (double)L.z;
-        const double t = sqrt((mx * mx + my * my) + mz * mz);
-        if (t == 0.0) continue;
-        const double n1 = (fabs(mx) + fabs(my)) + fabs(mz);
-        const double qx = mx / n1, qy = my / n1, qz = mz / n1;
-        double u, v;
-        if (qz >= 0.0) { u = qx; v = qy; }
-        else {
-            u = (qx >= 0.0 ? 1.0 : -1.0) * (1.0 - fabs(qy));
-            v = (qy >= 0.0 ? 1.0 : -1.0) * (1.0 - fabs(qx));
-        }
-        const double fx = (u + 1.0) * (0.5 * W) - 0.5;
-        const double fy = (v + 1.0) * (0.5 * H) - 0.5;
-        const double x0 = floor(fx), y0 = floor(fy);
-        const float wx = (float)(fx - x0), wy = (float)(fy - y0);
-        double fk = (t * K) / (double)L.w - 0.5;
-        fk = fk < 0.0 ? 0.0 : (fk > K - 1 ? (double)(K - 1) : fk);
-        const double k0d = floor(fk);
-        const float wk = (float)(fk - k0d);
-        const int k0 = (int)k0d, k1 = k0 + 1 < K ? k0 + 1 : K - 1;
-        const float* A0 = atlas + ((size_t)l * K + k0) * plane;
-        const float* A1 = atlas + ((size_t)l * K + k1) * plane;
         float acc = 0.0f;
-#pragma unroll
-        for (int dy = 0; dy < 2; ++dy)
-#pragma unroll
-            for (int dx = 0; dx < 2; ++dx) {
-                int c = (int)x0 + dx, r = (int)y0 + dy;
-                wrap_tap(c, r, W, H);
-                const size_t o = (size_t)r * W + c;
-                const float wxy = (dx ? wx : 1.0f - wx) * (dy ? wy : 1.0f - wy);
-                acc = fmaf(wxy * (1.0f - wk), __ldg(A0 + o), acc);
-                acc = fmaf(wxy * wk, __ldg(A1 + o), acc);
-            }
+        for (int i = 0; i < fp.n; ++i) {
+            const float4 z = fp.zw[i];
+            const double zx = z.x, zy = z.y, zz = z.z;
+            const double x = mx + ((m00 * zx + m01 * zy) + m02 * zz);
+            const double y = my + ((m10 * zx + m11 * zy) + m12 * zz);
+            const double w = mz + ((m20 * zx + m21 * zy) + m22 * zz);
+            acc = fmaf(z.w, sample_light(A, L, res, K, x, y, w), acc);
+        }
         T *= acc;
     }
-    T_out[q] = T;
-    if (colors) {
-        colors[3 * q] *= T;
-        colors[3 * q + 1] *= T;
-        colors[3 * q + 2] *= T;
-    }
+    T_out[g] = T;
+    apply_colors(colors, g, T);
 }
 }  // namespace
 
@@ -81,6 +137,14 @@ void launch_query(const float* atlas, const LightsParam& lp, int n_lights, int r
     if (m <= 0) return;
     k_query<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(atlas, lp, n_lights, res, K, positions, m, T_out,
                                                         colors);
+}
+
+void launch_query_footprint(const float* atlas, const LightsParam& lp, const FootprintParam& fp, int n_lights,
+                            int res, int K, const float* means, const float* scales, const float* rotations,
+                            int64_t m, float* T_out, float* colors, cudaStream_t s) {
+    if (m <= 0) return;
+    k_query_footprint<<<(unsigned)((m + 127) / 128), 128, 0, s>>>(atlas, lp, fp, n_lights, res, K, means, scales,
+                                                                  rotations, m, T_out, colors);
 }
 
 }  // namespace dgsm

@@ -31,7 +31,7 @@ ABSORPTION = {"traceavg": 0, "simple": 1, "mass": 2, "diag": 3}
 _STATUS = {0: "DGSM_OK", 1: "DGSM_EINVAL", 2: "DGSM_ENOSPC", 3: "DGSM_ECUDA", 4: "DGSM_ERANGE"}
 
 EXPORTED = ["dgsm_default_opts", "dgsm_plan_workspace_bytes", "dgsm_build_plan", "dgsm_build_run",
-            "dgsm_build_bins", "dgsm_build", "dgsm_exp_epilogue", "dgsm_query", "dgsm_strerror",
+            "dgsm_build_bins", "dgsm_build", "dgsm_exp_epilogue", "dgsm_query", "dgsm_query_footprint", "dgsm_strerror",
             "dgsm_last_error", "dgsm_last_launch_count", "dgsm_build_stats", "dgsm_set_accumulate_events"]
 
 
@@ -94,6 +94,8 @@ def lib() -> C.CDLL:
                                  P(sz), vp, vp]
         L.dgsm_exp_epilogue.argtypes = [vp, vp, i64, vp]
         L.dgsm_query.argtypes = [vp, P(Light), C.c_int, C.c_int, C.c_int, vp, i64, vp, vp, vp]
+        L.dgsm_query_footprint.argtypes = [vp, P(Light), C.c_int, C.c_int, C.c_int, vp, vp, vp, i64, vp, vp,
+                                           C.c_int, vp, vp, vp]
         L.dgsm_strerror.argtypes = [C.c_int]
         L.dgsm_strerror.restype = C.c_char_p
         L.dgsm_last_error.argtypes = []
@@ -105,7 +107,7 @@ def lib() -> C.CDLL:
         L.dgsm_set_accumulate_events.argtypes = [vp, vp]
         L.dgsm_set_accumulate_events.restype = C.c_int
         for f in ("dgsm_build_plan", "dgsm_build_run", "dgsm_build_bins", "dgsm_build",
-                  "dgsm_exp_epilogue", "dgsm_query"):
+                  "dgsm_exp_epilogue", "dgsm_query", "dgsm_query_footprint"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -318,6 +320,65 @@ def query(atlas: torch.Tensor, lights, positions: torch.Tensor, colors: Optional
     rc = lib().dgsm_query(C.c_void_p(atlas.data_ptr()), arr, nl, int(H), int(K), C.c_void_p(x.data_ptr()), m,
                           C.c_void_p(out.data_ptr()), cptr, C.c_void_p(_stream_ptr(stream)))
     _check(rc, "dgsm_query")
+    return out
+
+
+DGSM_MAX_FOOTPRINT_SAMPLES = 64
+
+
+def footprint_stencil(kind: str = "stencil7", delta: float = 1.0):
+    """Standard-normal footprint samples for query_footprint (NEXT-2).
+    "center": the single point z = 0 (equals query at the means).  "stencil7":
+    {0, +-delta e_j} weighted by the standard normal density exp(-|z|^2/2),
+    normalised to sum 1 (the SPEC's 7-point soft-shadow stencil)."""
+    if kind == "center":
+        return np.zeros((1, 3), np.float32), np.ones(1, np.float32)
+    if kind != "stencil7":
+        raise DgsmError(f"unknown footprint stencil {kind!r}")
+    z = np.zeros((7, 3))
+    for j in range(3):
+        z[1 + 2 * j, j] = delta
+        z[2 + 2 * j, j] = -delta
+    w = np.exp(-0.5 * (z * z).sum(1))
+    return z.astype(np.float32), (w / w.sum()).astype(np.float32)
+
+
+def query_footprint(atlas: torch.Tensor, lights, gaussians, offsets, weights,
+                    colors: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+                    stream=None) -> torch.Tensor:
+    """Footprint-averaged DGSM sampling (NEXT-2): for receiver Gaussian g,
+    T[g] = prod_l sum_i w_i T_l(mu_g + R_g (s_g * z_i)).  `gaussians` is a dict
+    of CUDA float32 means [m,3], scales [m,3], rotations [m,4]; offsets [n,3]
+    and weights [n] are host arrays (n <= 64)."""
+    if not atlas.is_cuda or atlas.dtype != torch.float32 or atlas.dim() != 4 or not atlas.is_contiguous():
+        raise DgsmError("atlas must be a contiguous float32 CUDA tensor [L, K, H, W]")
+    L, K, H, W = atlas.shape
+    if H != W:
+        raise DgsmError("square atlases only")
+    arr, nl = _lights(lights)
+    if nl != L:
+        raise DgsmError(f"atlas has {L} lights, got {nl}")
+    mu = _dev_f32(gaussians["means"], "means", (3,))
+    sc = _dev_f32(gaussians["scales"], "scales", (3,))
+    q = _dev_f32(gaussians["rotations"], "rotations", (4,))
+    m = mu.shape[0]
+    if sc.shape[0] != m or q.shape[0] != m:
+        raise DgsmError("means, scales and rotations must have the same length")
+    z = np.ascontiguousarray(np.asarray(offsets, np.float32).reshape(-1, 3))
+    w = np.ascontiguousarray(np.asarray(weights, np.float32).reshape(-1))
+    if len(z) != len(w) or not 1 <= len(w) <= DGSM_MAX_FOOTPRINT_SAMPLES:
+        raise DgsmError(f"need 1..{DGSM_MAX_FOOTPRINT_SAMPLES} offsets with one weight each")
+    out = torch.empty(m, dtype=torch.float32, device=mu.device) if out is None else out
+    cptr = None
+    if colors is not None:
+        if colors.dtype != torch.float32 or not colors.is_contiguous() or tuple(colors.shape) != (m, 3):
+            raise DgsmError("colors must be contiguous float32 [m, 3]")
+        cptr = C.c_void_p(colors.data_ptr())
+    rc = lib().dgsm_query_footprint(C.c_void_p(atlas.data_ptr()), arr, nl, int(H), int(K),
+                                    C.c_void_p(mu.data_ptr()), C.c_void_p(sc.data_ptr()), C.c_void_p(q.data_ptr()),
+                                    m, z.ctypes.data_as(C.c_void_p), w.ctypes.data_as(C.c_void_p), len(w),
+                                    C.c_void_p(out.data_ptr()), cptr, C.c_void_p(_stream_ptr(stream)))
+    _check(rc, "dgsm_query_footprint")
     return out
 
 

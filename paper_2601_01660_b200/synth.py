@@ -519,3 +519,11 @@ def random_queries(seed: int, lights, m: int, r_max: float) -> np.ndarray:
     v = rng.standard_normal((m, 3)); v /= np.linalg.norm(v, axis=1, keepdims=True)
     x = lp[rng.integers(0, lp.shape[0], m)] + v * rng.uniform(0.0, r_max, m)[:, None]
     return x.astype(np.float32)
+
+
+def mc_offsets(n: int, seed: int = 0) -> np.ndarray:
+    """Monte Carlo footprint offsets z_i ~ N(0, I_3) (the paper's default receiver
+    footprint sampling), seeded; the same draws feed both the CUDA query
+    and the oracle.  Weights are 1/n."""
+    rng = np.random.Generator(np.random.PCG64(SEED_BASE + 31337 * (seed + 1)))
+    return rng.standard_normal((n, 3)).astype(np.float32)

@@ -101,6 +101,12 @@ def test_validation_fails_before_device_work(lib):
     # query validation
     assert lib.dgsm_query(None, lights, 1, 16, 4, None, 10, None, None, None) == 1
     assert lib.dgsm_exp_epilogue(None, None, -1, None) == 1
+    # footprint query validation (NEXT-2): sample count and null host arrays
+    z = (C.c_float * (3 * 65))()
+    w = (C.c_float * 65)()
+    for n in (0, 65):
+        assert lib.dgsm_query_footprint(None, lights, 1, 16, 4, None, None, None, 0, z, w, n, None, None, None) == 1
+    assert lib.dgsm_query_footprint(None, lights, 1, 16, 4, None, None, None, 0, None, w, 1, None, None, None) == 1
 
 
 def test_binding_refuses_cpu_tensors():

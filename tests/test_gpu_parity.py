@@ -204,6 +204,41 @@ def test_query_parity_random_atlas(dg, oracle_mod, L, K, res):
     assert np.abs(ct.cpu().numpy() - col * want[:, None]).max() <= 2e-6
 
 
+def _receivers(seed, lights, m, K):
+    rng = np.random.default_rng(seed)
+    return dict(means=synth.random_queries(K, lights, m, 6.0),
+                scales=np.exp(rng.uniform(np.log(0.005), np.log(0.5), (m, 3))).astype(np.float32),
+                rotations=synth.random_quaternions(rng, m).astype(np.float32))
+
+
+@pytest.mark.parametrize("kind", ["center", "stencil7", "mc32"])
+def test_query_footprint_parity(dg, oracle_mod, kind):
+    """NEXT-2 footprint-averaged query against the oracle."""
+    L, K, res = 2, 12, 64
+    atlas = synth.random_atlas(77, L, K, res)
+    rng = np.random.default_rng(4)
+    lights = dict(position=rng.uniform(-1, 1, (L, 3)).astype(np.float32),
+                  t_max=rng.uniform(3, 5, L).astype(np.float32))
+    g = _receivers(8, lights, 5000, K)
+    if kind == "mc32":
+        z, w = synth.mc_offsets(32, 3), np.full(32, 1 / 32, np.float32)
+    else:
+        z, w = dg.footprint_stencil(kind)
+    zo, wo = oracle_mod.stencil7(1.0) if kind == "stencil7" else (z.astype(np.float64), w.astype(np.float64))
+    assert np.abs(zo - z).max() == 0 and np.abs(wo - w).max() < 1e-7
+    want = oracle_mod.query_footprint(atlas.astype(np.float64), lights, g, zo, wo)
+    gd = dg.to_device(g)
+    at = torch.from_numpy(atlas).cuda()
+    got = dg.query_footprint(at, lights, gd, z, w).cpu().numpy()
+    assert np.abs(got - want).max() <= 4e-6
+    if kind == "center":
+        assert torch.equal(torch.from_numpy(got), dg.query(at, lights, gd["means"]).cpu())
+    col = np.random.default_rng(2).random((5000, 3)).astype(np.float32)
+    ct = torch.from_numpy(col).cuda()
+    dg.query_footprint(at, lights, gd, z, w, colors=ct)
+    assert np.abs(ct.cpu().numpy() - col * want[:, None]).max() <= 4e-6
+
+
 def test_query_empty(dg):
     atlas = torch.ones(1, 4, 16, 16, device="cuda")
     out = dg.query(atlas, dict(position=[[0, 0, 0]], t_max=[1.0]), torch.zeros(0, 3, device="cuda"))

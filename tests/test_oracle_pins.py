@@ -433,6 +433,43 @@ def test_query_analytic_field(oracle_mod):
     assert np.abs(v - np.exp(-tc / tmax)).max() <= bound + 1e-12
 
 
+def test_query_footprint_pins(oracle_mod):
+    """NEXT-2: the 7-point stencil weights (centre weight
+    1/(1 + 6 e^{-1/2}) = 0.2156); a centre-only footprint equals
+    the plain query; zero scales collapse any footprint onto the centre; and
+    the footprint average equals the weighted plain queries at sample points
+    computed independently (numpy rotation)."""
+    z, w = oracle_mod.stencil7(1.0)
+    assert abs(w[0] - 1.0 / (1.0 + 6.0 * math.exp(-0.5))) < 1e-15 and abs(w.sum() - 1) < 1e-15
+    assert round(w[0], 4) == 0.2156
+    L, K, res = 2, 6, 16
+    at = synth.random_atlas(3, L, K, res).astype(np.float64)
+    lights = dict(position=np.array([[0, 0, 0], [0.5, -0.3, 0.2]], np.float32), t_max=np.array([5.0, 6.0], np.float32))
+    rng = np.random.default_rng(9)
+    m = 40
+    g = dict(means=synth.random_queries(5, lights, m, 4.0),
+             scales=np.exp(rng.uniform(np.log(0.01), np.log(0.3), (m, 3))).astype(np.float32),
+             rotations=synth.random_quaternions(rng, m).astype(np.float32))
+    Tc = oracle_mod.query_footprint(at, lights, g, np.zeros((1, 3)), np.ones(1))
+    assert np.abs(Tc - oracle_mod.query(at, lights, g["means"])).max() == 0.0
+    g0 = dict(g, scales=np.zeros_like(g["scales"]))
+    assert np.abs(oracle_mod.query_footprint(at, lights, g0, z, w) - Tc).max() < 1e-12
+    zm = synth.mc_offsets(16, 1).astype(np.float64)
+    wm = np.full(16, 1 / 16)
+    got = oracle_mod.query_footprint(at, lights, g, zm, wm)
+    R = synth.quaternion_to_matrix(g["rotations"].astype(np.float64))
+    want = np.ones(m)
+    for l in range(L):
+        l1 = dict(position=lights["position"][l:l + 1], t_max=lights["t_max"][l:l + 1])
+        acc = np.zeros(m)
+        for i in range(16):
+            x = g["means"].astype(np.float64) + np.einsum("mij,mj->mi", R, g["scales"].astype(np.float64) * zm[i])
+            acc += wm[i] * oracle_mod.query(at[l:l + 1], l1, x.astype(np.float32))
+        want *= acc
+    # sample points rounded to fp32 in the independent path: compare loosely
+    assert np.abs(got - want).max() < 1e-4
+
+
 def test_query_seam_continuity(oracle_mod):
     """Sampling a smooth direction field across the atlas border is continuous
     (the octahedral map 'avoids inter-face seams')."""
