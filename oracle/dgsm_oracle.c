@@ -382,6 +382,8 @@ typedef struct {
     const int64_t* range; /* [L*n_tiles+1] start offsets into the sorted entries */
     unsigned char* excluded; /* [L][n] */
     double* T;               /* [L][K][res][res] */
+    const unsigned char* slab_mask; /* [L][res][res] or NULL: the ROI pixel set P */
+    const int32_t* slab_krange;     /* [L][2] k_min, k_max (k_min > k_max: empty) */
     int64_t next;            /* work counter */
     int64_t evals;           /* (texel, Gaussian) evaluations performed */
     pthread_mutex_t lock;
@@ -399,6 +401,17 @@ static void or_build_item(or_build_ctx* c, int64_t item)
     for (int r = 0; r < 8; ++r)
         for (int cc = 0; cc < 8; ++cc) {
             int row = ty * 8 + r, col = tx * 8 + cc;
+            int klo = 0, khi = K - 1;
+            if (c->slab_mask) {
+                /* "initialize T = 1 and only accumulate optical depth on the voxel
+                 * slab R = P x {k_min..k_max}" */
+                klo = c->slab_krange[2 * l];
+                khi = c->slab_krange[2 * l + 1];
+                if (!c->slab_mask[((int64_t)l * H + row) * W + col]) khi = -1;
+                for (int k = 0; k < K; ++k)
+                    if (k < klo || k > khi) c->T[(((int64_t)l * K + k) * H + row) * W + col] = 1.0;
+                if (klo > khi) continue;
+            }
             double d[3];
             or_texel_dir(row, col, H, W, d);
             for (int k = 0; k < K; ++k) tau[k] = 0.0;
@@ -413,11 +426,11 @@ static void or_build_item(or_build_ctx* c, int64_t item)
                 memcpy(Ai, c->A + 9 * i, sizeof(Ai));
                 double abc[3];
                 or_ray_quadratic(Ai, mu, o, d, abc);
-                for (int k = 0; k < K; ++k)
+                for (int k = klo; k <= khi; ++k)
                     tau[k] += or_segment_depth(abc[0], abc[1], abc[2], c->beta[i],
                                                or_bin_center(k, K, tmax));
             }
-            for (int k = 0; k < K; ++k)
+            for (int k = klo; k <= khi; ++k)
                 c->T[(((int64_t)l * K + k) * H + row) * W + col] = exp(-tau[k]);
         }
     free(tau);
@@ -453,11 +466,32 @@ static void* or_build_worker(void* arg)
  * parity target), culled=0 sums every non-excluded Gaussian at every texel
  * (the reference for the culling error, P:L335 ablation D).  Returns P (the
  * number of binned entries) in culled mode, 0 otherwise, -1 on bad input. */
+int64_t or_build_slab(const float* means, const float* scales, const float* rotations,
+                      const float* opacities, int64_t n, const float* light_pos, const float* t_max,
+                      int L, int res, int K, double kappa, double k_sigma, double rho_scale,
+                      int bin_mode, int culled, int absorption, int64_t tile_stride, int n_threads,
+                      const unsigned char* slab_mask, const int32_t* slab_krange,
+                      double* T_out, int64_t* evals_out);
+
 int64_t or_build(const float* means, const float* scales, const float* rotations,
                  const float* opacities, int64_t n, const float* light_pos, const float* t_max,
                  int L, int res, int K, double kappa, double k_sigma, double rho_scale,
                  int bin_mode, int culled, int absorption, int64_t tile_stride, int n_threads,
                  double* T_out, int64_t* evals_out /* nullable: (texel, Gaussian) evaluations performed */)
+{
+    return or_build_slab(means, scales, rotations, opacities, n, light_pos, t_max, L, res, K, kappa,
+                         k_sigma, rho_scale, bin_mode, culled, absorption, tile_stride, n_threads,
+                         NULL, NULL, T_out, evals_out);
+}
+
+/* As or_build, restricted to the ROI slab (slab_mask [L][res][res], slab_krange
+ * [L][2] from or_active_slab); NULL slab_mask = the full atlas. */
+int64_t or_build_slab(const float* means, const float* scales, const float* rotations,
+                      const float* opacities, int64_t n, const float* light_pos, const float* t_max,
+                      int L, int res, int K, double kappa, double k_sigma, double rho_scale,
+                      int bin_mode, int culled, int absorption, int64_t tile_stride, int n_threads,
+                      const unsigned char* slab_mask, const int32_t* slab_krange,
+                      double* T_out, int64_t* evals_out)
 {
     if (res < 8 || res % 8 != 0 || K < 1 || L < 1 || n < 0) return -1;
     or_build_ctx c;
@@ -469,6 +503,8 @@ int64_t or_build(const float* means, const float* scales, const float* rotations
     c.tile_stride = tile_stride < 1 ? 1 : tile_stride;
     c.n_tiles = (int64_t)(res / 8) * (res / 8);
     c.T = T_out;
+    c.slab_mask = slab_mask;
+    c.slab_krange = slab_krange;
     int64_t total = (int64_t)L * K * res * res;
     for (int64_t j = 0; j < total; ++j) T_out[j] = NAN;
 
@@ -636,4 +672,59 @@ void or_query_footprint(const double* atlas, int L, int K, int res, const float*
         }
         T_out[g] = T;
     }
+}
+
+/* ------------------------------------------------------------------ */
+/* NEXT-1  receiver-driven ROI and active voxel slab        */
+/* ------------------------------------------------------------------ */
+/* Receivers x (float [m][3]) inside B = {x : ||(x - c)_xy||_inf <= R,
+ * z_min <= x_z <= z_max} are projected per light into atlas pixels
+ * (psi: the pixel whose cell holds u, col = floor((u+1) W/2),
+ * clamped to W-1) and collected into the set P (mask[L][res][res] = 1); the
+ * radial range is their bin floor(t K / t_max) (clamped to [0, K-1]) min/max
+ * (P:L159).  Readings (DESIGN.md R-ROI): P is dilated by one pixel, each
+ * neighbour mirror-wrapped like the sampler's taps (Q12), and the bin range
+ * widened by one each side, so that every trilinear tap of a query
+ * at a receiver in B lies in the slab.  A receiver at the light itself is
+ * skipped (T = 1 there, Q18).  No receiver: k_min = K, k_max = -1.
+ * roi = {c_x, c_y, c_z, R, z_min, z_max}.  Returns the receivers in B. */
+int64_t or_active_slab(const float* x, int64_t m, const float* roi, const float* light_pos,
+                       const float* t_max, int L, int res, int K, unsigned char* mask,
+                       int32_t* krange)
+{
+    int H = res, W = res;
+    memset(mask, 0, (size_t)L * H * W);
+    for (int l = 0; l < L; ++l) { krange[2 * l] = K; krange[2 * l + 1] = -1; }
+    int64_t inside = 0;
+    for (int64_t q = 0; q < m; ++q) {
+        double px = x[3 * q], py = x[3 * q + 1], pz = x[3 * q + 2];
+        double ex = fabs(px - (double)roi[0]), ey = fabs(py - (double)roi[1]);
+        double inf = ex > ey ? ex : ey;
+        if (!(inf <= (double)roi[3] && pz >= (double)roi[4] && pz <= (double)roi[5])) continue;
+        ++inside;
+        for (int l = 0; l < L; ++l) {
+            double d[3] = {px - (double)light_pos[3 * l], py - (double)light_pos[3 * l + 1],
+                           pz - (double)light_pos[3 * l + 2]};
+            double t = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+            if (t == 0.0) continue;
+            double uv[2];
+            or_oct_encode(d, uv);
+            int64_t col = (int64_t)floor((uv[0] + 1.0) * (0.5 * W));
+            int64_t row = (int64_t)floor((uv[1] + 1.0) * (0.5 * H));
+            if (col > W - 1) col = W - 1;
+            if (row > H - 1) row = H - 1;
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    int64_t cr[2];
+                    or_mirror_wrap(col + dx, row + dy, H, W, cr);
+                    mask[((int64_t)l * H + cr[1]) * W + cr[0]] = 1;
+                }
+            double fb = floor((t * K) / (double)t_max[l]);
+            int b = fb > K - 1 ? K - 1 : (int)fb;
+            int lo = b - 1 < 0 ? 0 : b - 1, hi = b + 1 > K - 1 ? K - 1 : b + 1;
+            if (lo < krange[2 * l]) krange[2 * l] = lo;
+            if (hi > krange[2 * l + 1]) krange[2 * l + 1] = hi;
+        }
+    }
+    return inside;
 }

@@ -60,6 +60,13 @@ def lib():
         L.or_build.argtypes = [fp, fp, fp, fp, C.c_int64, fp, fp, C.c_int, C.c_int, C.c_int,
                                C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int64,
                                C.c_int, dp, i64p]
+        L.or_build_slab.restype = C.c_int64
+        L.or_build_slab.argtypes = [fp, fp, fp, fp, C.c_int64, fp, fp, C.c_int, C.c_int, C.c_int,
+                                    C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int64,
+                                    C.c_int, C.POINTER(C.c_ubyte), C.POINTER(C.c_int32), dp, i64p]
+        L.or_active_slab.restype = C.c_int64
+        L.or_active_slab.argtypes = [fp, C.c_int64, fp, fp, fp, C.c_int, C.c_int, C.c_int,
+                                     C.POINTER(C.c_ubyte), C.POINTER(C.c_int32)]
         L.or_query_footprint.argtypes = [dp, C.c_int, C.c_int, C.c_int, fp, fp, fp, fp, fp, C.c_int64,
                                          dp, dp, C.c_int, dp]
         L.or_beta_mode.restype = C.c_double
@@ -178,12 +185,15 @@ def tau_ray(g, o, d, t, kappa=1.0) -> float:
 
 
 def build(g, lights, res, K, kappa=1.0, k_sigma=3.0, rho_scale=1.0, bin_mode=BIN_WRAP,
-          culled=True, tile_stride=1, n_threads=None, return_evals=False, absorption="traceavg"):
+          culled=True, tile_stride=1, n_threads=None, return_evals=False, absorption="traceavg",
+          slab=None):
     """R8: the atlas T[L][K][res][res] in float64 (NaN where skipped by tile_stride).
 
     ``g``: dict of means [n,3], scales [n,3], rotations [n,4] (w,x,y,z), opacities [n].
     ``lights``: dict(position [L,3], t_max [L]).
     ``absorption``: traceavg (Eq.5) | simple | mass | diag (ablation B).
+    ``slab``: (mask [L,res,res], krange [L,2]) from active_slab: T = 1 outside
+    the slab, else the full atlas.
     Returns (T, P) with P the number of binned entries (culled mode)."""
     mode = ABSORPTION[absorption] if isinstance(absorption, str) else int(absorption)
     mu, s, q, a = _f32(g["means"]), _f32(g["scales"]), _f32(g["rotations"]), _f32(g["opacities"])
@@ -192,16 +202,37 @@ def build(g, lights, res, K, kappa=1.0, k_sigma=3.0, rho_scale=1.0, bin_mode=BIN
     T = np.empty((L, K, res, res), dtype=np.float64)
     n_threads = n_threads or os.cpu_count() or 1
     evals = C.c_int64(0)
-    P = lib().or_build(_p(mu, C.c_float), _p(s, C.c_float), _p(q, C.c_float), _p(a, C.c_float),
-                       mu.shape[0], _p(lp, C.c_float), _p(tm, C.c_float), L, int(res), int(K),
-                       _opt(kappa), _opt(k_sigma), _opt(rho_scale), int(bin_mode),
-                       int(bool(culled)), mode, int(tile_stride), int(n_threads), _p(T, C.c_double),
-                       C.byref(evals))
+    sm = sk = None
+    if slab is not None:
+        mk = np.ascontiguousarray(slab[0], dtype=np.uint8).reshape(L, res, res)
+        kr = np.ascontiguousarray(slab[1], dtype=np.int32).reshape(L, 2)
+        sm, sk = _p(mk, C.c_ubyte), _p(kr, C.c_int32)
+    P = lib().or_build_slab(_p(mu, C.c_float), _p(s, C.c_float), _p(q, C.c_float), _p(a, C.c_float),
+                            mu.shape[0], _p(lp, C.c_float), _p(tm, C.c_float), L, int(res), int(K),
+                            _opt(kappa), _opt(k_sigma), _opt(rho_scale), int(bin_mode),
+                            int(bool(culled)), mode, int(tile_stride), int(n_threads), sm, sk,
+                            _p(T, C.c_double), C.byref(evals))
     if P < 0:
         raise ValueError("oracle build: invalid arguments")
     if return_evals:
         return T, int(P), int(evals.value)
     return T, int(P)
+
+
+def active_slab(receivers, roi, lights, res, K):
+    """NEXT-1: the ROI pixel set P and radial range of receivers in
+    B.  ``roi`` = (c_x, c_y, c_z, R, z_min, z_max).  Returns (mask bool
+    [L,res,res], krange int32 [L,2], receivers inside B)."""
+    x = _f32(receivers).reshape(-1, 3)
+    r = _f32(roi).reshape(6)
+    lp, tm = _f32(lights["position"]).reshape(-1, 3), _f32(lights["t_max"]).reshape(-1)
+    L = lp.shape[0]
+    mask = np.zeros((L, res, res), np.uint8)
+    kr = np.zeros((L, 2), np.int32)
+    inside = lib().or_active_slab(_p(x, C.c_float), x.shape[0], _p(r, C.c_float), _p(lp, C.c_float),
+                                  _p(tm, C.c_float), L, int(res), int(K), _p(mask, C.c_ubyte),
+                                  _p(kr, C.c_int32))
+    return mask.astype(bool), kr, int(inside)
 
 
 def query(atlas, lights, positions, colors=None):

@@ -470,6 +470,55 @@ def test_query_footprint_pins(oracle_mod):
     assert np.abs(got - want).max() < 1e-4
 
 
+def test_active_slab_hand_cases(oracle_mod):
+    """NEXT-1 slab on cases worked by hand: a receiver straight
+    above the light (+z: u = v = 0 -> pixel (W/2, W/2), 3x3 dilation, bin
+    floor(2.3*8/4) = 4 widened to [3, 5]); the same receiver above z_max (empty
+    slab, T = 1 everywhere); the box test of SPEC S:L325; and a receiver on the
+    -x direction (u = -1 -> col 0) whose dilation mirror-wraps across the left
+    edge (col -1 -> col 0, row -> H-1-row), giving 7 pixels."""
+    lights = dict(position=np.zeros((1, 3), np.float32), t_max=np.array([4.0], np.float32))
+    roi = (0, 0, 0, 2.0, 0.0, 3.0)
+    mask, kr, inside = oracle_mod.active_slab(np.array([[0, 0, 2.3]]), roi, lights, 16, 8)
+    want = np.zeros((16, 16), bool)
+    want[7:10, 7:10] = True
+    assert inside == 1 and np.array_equal(mask[0], want) and tuple(kr[0]) == (3, 5)
+    mask, kr, inside = oracle_mod.active_slab(np.array([[0, 0, 2.3]]), (0, 0, 0, 2.0, 0.0, 2.0), lights, 16, 8)
+    assert inside == 0 and not mask.any() and tuple(kr[0]) == (8, -1)
+    _, _, inside = oracle_mod.active_slab(np.array([[1.9, 0, 1.0], [2.1, 0, 1.0], [0, -1.99, 1.0]]), roi, lights, 16, 8)
+    assert inside == 2
+    mask, kr, _ = oracle_mod.active_slab(np.array([[-1.5, 0, 0.5]]), (0, 0, 0, 2.0, 0.0, 3.0),
+                                         dict(position=np.array([[0, 0, 0.5]], np.float32), t_max=np.array([4.0], np.float32)),
+                                         16, 8)
+    want = np.zeros((16, 16), bool)
+    want[7:10, 0:2] = True          # rows 7..9 (v = 0 -> row 8), cols 0..1
+    want[[6, 7, 8], 0] = True       # col -1 wrapped: rows 15-7, 15-8, 15-9
+    assert np.array_equal(mask[0], want) and mask.sum() == 7
+    assert tuple(kr[0]) == (2, 4)   # t = 1.5 -> bin 3
+
+
+def test_slab_build_exact_for_receivers(oracle_mod):
+    """P:L160 "outside R the table remains T = 1 by construction": the slab
+    build is exactly 1 outside P x [k_min, k_max] and equals the full build
+    inside, so a query at any receiver in B reads identical values."""
+    s = synth.random_scene(31, 200, res=32, K=10, L=2, dist=(0.4, 3.0), scale=(0.02, 0.3))
+    rng = np.random.default_rng(3)
+    rec = rng.uniform(-2.5, 2.5, (400, 3)).astype(np.float32)
+    roi = (0.3, -0.2, 0.0, 1.2, -0.8, 1.0)
+    mask, kr, inside = oracle_mod.active_slab(rec, roi, s.lights, s.res, s.K)
+    assert 0 < inside < 400 and mask.any() and not mask.all()
+    Tf, _ = oracle_mod.build(s.gaussians, s.lights, s.res, s.K)
+    Ts, _ = oracle_mod.build(s.gaussians, s.lights, s.res, s.K, slab=(mask, kr))
+    kk = np.arange(s.K)[None, :, None, None]
+    in_slab = mask[:, None] & (kk >= kr[:, 0, None, None, None]) & (kk <= kr[:, 1, None, None, None])
+    assert (Ts[~in_slab] == 1.0).all() and np.array_equal(Ts[in_slab], Tf[in_slab])
+    assert (Tf[~in_slab] < 1.0).any()  # the slab really dropped work
+    ins = (np.maximum(np.abs(rec[:, 0] - 0.3), np.abs(rec[:, 1] + 0.2)) <= 1.2) & (rec[:, 2] >= -0.8) & (rec[:, 2] <= 1.0)
+    assert ins.sum() == inside
+    assert np.array_equal(oracle_mod.query(Ts, s.lights, rec[ins]), oracle_mod.query(Tf, s.lights, rec[ins]))
+    assert not np.array_equal(oracle_mod.query(Ts, s.lights, rec[~ins]), oracle_mod.query(Tf, s.lights, rec[~ins]))
+
+
 def test_query_seam_continuity(oracle_mod):
     """Sampling a smooth direction field across the atlas border is continuous
     (the octahedral map 'avoids inter-face seams')."""
