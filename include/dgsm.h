@@ -92,6 +92,13 @@ typedef struct dgsm_build_opts {
     int32_t bin_mode;  /* DGSM_BIN_WRAP (default) or DGSM_BIN_CLAMP */
     uint32_t flags;    /* DGSM_OUTPUT_TAU | DGSM_COLLECT_STATS | DGSM_NO_TILE_CULL, or 0 */
     int32_t absorption; /* DGSM_ABS_* alpha -> beta mapping (ablation B), default TRACEAVG */
+    const void* slab;   /* NULL (default): the full atlas.  Else a device slab written by
+                           dgsm_active_slab for the same n_lights, atlas_res and n_shells: only
+                           the voxel slab R = P x {k_min..k_max} is accumulated and T = 1 (tau = 0
+                           with DGSM_OUTPUT_TAU) everywhere else; tiles without a
+                           texel of P are not binned at all.  8-B aligned, read-only; like the
+                           Gaussian arrays it must not change between dgsm_build_plan and
+                           dgsm_build_run and must stay valid until the run has completed. */
 } dgsm_build_opts_t;
 
 /* ---- alpha -> beta mappings, tau* = -ln(1 - alpha) ----------- */
@@ -203,6 +210,46 @@ int dgsm_query_footprint(const float* atlas, const dgsm_light_t* lights, int n_l
                          int n_shells, const float* means, const float* scales, const float* rotations,
                          int64_t m, const float* offsets, const float* weights, int n_samples,
                          float* T_out, float* colors_inout, void* stream);
+
+/* ------------------------------------------------------------------
+ * Receiver-driven region of interest and active voxel slab (SURVEY §8(f)
+ * NEXT-1; §3.2).
+ * ------------------------------------------------------------------ */
+/* B = {x : ||(x - center)_xy||_inf <= radius, z_min <= x_z <= z_max}.
+ * The paper leaves the centre (alpha-weighted avatar centroid) and the "robust
+ * height bounds" to the caller; so does this ABI. */
+typedef struct {
+    float center[3];
+    float radius;      /* R > 0 (the paper's example: 2 m) */
+    float z_min, z_max;
+} dgsm_roi_t;
+
+/* Bytes of a slab buffer for n_lights lights at atlas_res (0 on bad input).
+ * Layout (device, caller-owned, 256-B aligned sections):
+ *   uint64_t texel_mask[n_lights][(atlas_res/8)^2]  bit (row%8)*8 + col%8 of
+ *            word tile = (row/8)*(atlas_res/8) + col/8 is set iff texel
+ *            (row, col) is in the pixel set P;
+ *   int32_t  k_range[n_lights][2]                   k_min, k_max (k_min > k_max:
+ *            no receiver for that light, the light's atlas stays 1). */
+size_t dgsm_slab_bytes(int n_lights, int atlas_res);
+
+/* Write the slab of the receivers x (device float [m][3], e.g. scene Gaussian
+ * centres) for the lights: "For scene Gaussians whose centers lie in B, we
+ * project their light rays into atlas pixels, collect the unique set P, and
+ * infer a tight radial range k in [k_min, k_max] from their light-space
+ * distances".  Pixel of a receiver = the texel whose cell holds
+ * psi(x - o_L) (col = floor((u+1) W/2), clamped to W-1); its bin =
+ * floor(|x - o_L| K / t_max), clamped to [0, K-1].  DESIGN.md reading R-ROI:
+ * P is dilated by one pixel (neighbours mirror-wrapped like the sampler's
+ * taps) and the bin range widened by one each side, so every trilinear tap
+ * of a dgsm_query at a receiver in B lies in the slab and reads the value
+ * the full build would have written.  A receiver exactly at a light is
+ * skipped for that light.  fp64 decisions, bit-exact with the oracle.
+ * Errors: DGSM_EINVAL (null/invalid arguments, radius <= 0, z_min > z_max),
+ * DGSM_ENOSPC (slab_bytes < dgsm_slab_bytes). */
+int dgsm_active_slab(const float* receivers, int64_t m, const dgsm_roi_t* roi, const dgsm_light_t* lights,
+                     int n_lights, int atlas_res, int n_shells, void* slab, size_t slab_bytes,
+                     void* stream);
 
 /* Read the counters of the last DGSM_COLLECT_STATS dgsm_build_run that used
  * this run workspace (synchronises `stream`). */

@@ -2,7 +2,7 @@
 
 ``python -m paper_2601_01660_b200.build_ext [--force] [--verbose]``
 
-project.cu is compiled with ``-fmad=false`` (no FMA contraction: the binning
+project.cu and slab.cu are compiled with ``-fmad=false`` (no FMA contraction: the binning
 decisions follow DESIGN.md's fp64 "binning arithmetic contract"); every other
 translation unit uses the default contraction.
 """
@@ -22,8 +22,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
           "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
-SOURCES = ["project.cu", "scan.cu", "binning.cu", "onesweep.cu", "accumulate.cu", "query.cu", "dgsm_api.cu"]
-PER_FILE = {"project.cu": ["-fmad=false"]}
+SOURCES = ["project.cu", "slab.cu", "scan.cu", "binning.cu", "onesweep.cu", "accumulate.cu", "query.cu", "dgsm_api.cu"]
+PER_FILE = {"project.cu": ["-fmad=false"], "slab.cu": ["-fmad=false"]}
 HEADERS = ["dgsm_internal.cuh"]
 
 

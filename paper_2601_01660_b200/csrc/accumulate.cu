@@ -208,7 +208,8 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
     const WorkUnit* __restrict__ units, const uint32_t* __restrict__ n_units_dev,
     const uint32_t* __restrict__ vals, const PairRec* __restrict__ recs, int64_t n, AccLights al,
     int res, int K, uint32_t flags, float* __restrict__ scratch, uint32_t* tile_arrive,
-    uint32_t* unit_counter, float* __restrict__ atlas, unsigned long long* __restrict__ stats) {
+    uint32_t* unit_counter, float* __restrict__ atlas, unsigned long long* __restrict__ stats,
+    const uint64_t* __restrict__ slab_mask, const int2* __restrict__ slab_k) {
     extern __shared__ __align__(128) unsigned char acc_smem[];
     PairRec* s_raw = reinterpret_cast<PairRec*>(acc_smem);                                   // [kStage]
     float4* s_cr = reinterpret_cast<float4*>(acc_smem + kStage * sizeof(PairRec));           // [kStage][5]
@@ -315,11 +316,19 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
         const bool want_tau = (flags & DGSM_OUTPUT_TAU) != 0;
         const size_t plane = (size_t)H * W;
         float* out = atlas + ((size_t)l * K) * plane + (size_t)row * W + col;
+        // NEXT-1 slab: outside P x [k_min, k_max] the table stays T = 1
+        int klo = 0, khi = K - 1;
+        if (slab_mask) {
+            const int2 kr = slab_k[l];
+            klo = kr.x;
+            khi = ((slab_mask[wu.tile] >> tid) & 1ull) ? kr.y : -1;
+        }
+        const float one = want_tau ? 0.0f : 1.0f;
         if (wu.nchunks == 1) {
             float tau = 0.0f;
             for (int k = 0; k < K; ++k) {
                 tau += s_acc[k * kThreads + tid];
-                out[(size_t)k * plane] = want_tau ? tau : expf(-tau);
+                out[(size_t)k * plane] = (k < klo || k > khi) ? one : (want_tau ? tau : expf(-tau));
             }
         } else {
             float* part = scratch + ((size_t)(wu.slot + wu.chunk) * K) * kThreads + tid;
@@ -339,7 +348,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
                     float t = 0.0f;
                     for (uint32_t c = 0; c < wu.nchunks; ++c)
                         t += __ldcg(base + ((size_t)c * K + k) * kThreads);
-                    out[(size_t)k * plane] = want_tau ? t : expf(-t);
+                    out[(size_t)k * plane] = (k < klo || k > khi) ? one : (want_tau ? t : expf(-t));
                 }
                 if (tid == 0) tile_arrive[wu.tile] = 0u;
             }
@@ -364,8 +373,8 @@ void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint3
                        const uint32_t* vals, const PairRec* recs, int64_t n, const LightsParam& lp,
                        int n_lights, int res, int K, uint32_t flags, float* scratch,
                        uint32_t* tile_arrive, uint32_t* unit_counter, float* atlas,
-                       unsigned long long* stats, cudaEvent_t ev_before, cudaEvent_t ev_after,
-                       cudaStream_t s) {
+                       unsigned long long* stats, const uint64_t* slab_mask, const int2* slab_k,
+                       cudaEvent_t ev_before, cudaEvent_t ev_after, cudaStream_t s) {
     AccLights al;
     for (int l = 0; l < DGSM_MAX_LIGHTS; ++l) {
         const double dt = l < n_lights ? (double)lp.l[l].w / K : 1.0;
@@ -397,11 +406,12 @@ void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint3
     if (ev_before) cudaEventRecord(ev_before, s);
     if (flags & DGSM_COLLECT_STATS)
         k_accumulate<true><<<grid, kThreads, smem, s>>>(units, n_units_dev, vals, recs, n, al, res, K, flags,
-                                                        scratch, tile_arrive, unit_counter, atlas, stats);
+                                                        scratch, tile_arrive, unit_counter, atlas, stats,
+                                                        slab_mask, slab_k);
     else
         k_accumulate<false><<<grid, kThreads, smem, s>>>(units, n_units_dev, vals, recs, n, al, res, K,
                                                          flags, scratch, tile_arrive, unit_counter, atlas,
-                                                         stats);
+                                                         stats, slab_mask, slab_k);
     if (ev_after) cudaEventRecord(ev_after, s);
 }
 

@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(256) k_duplicate_ranked(const uint4* __restric
                                                           const uint32_t* __restrict__ perm,
                                                           const uint64_t* __restrict__ offs, int64_t n,
                                                           int res, int bin_mode, uint64_t base,
+                                                          const uint64_t* __restrict__ tm,
                                                           uint32_t* __restrict__ keys,
                                                           uint32_t* __restrict__ vals) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -55,11 +56,13 @@ __global__ void __launch_bounds__(256) k_duplicate_ranked(const uint4* __restric
     if (r.w == 0) return;  // no tile
     const int TW = res / kTile;
     uint64_t o = base + offs[j];
+    const uint64_t end = o + r.w;  // never more keys than the plan counted (a slab changed since the plan)
     int c0, c1, r0, r1;
     unpack_rect(r, c0, c1, r0, r1);
     if (c0 >= 0 && c1 <= res - 1 && r0 >= 0 && r1 <= res - 1) {  // common case: inside the grid
         for (int ty = r0 >> 3; ty <= (r1 >> 3); ++ty)
             for (int tx = c0 >> 3; tx <= (c1 >> 3); ++tx) {
+                if (tm && (tm[ty * TW + tx] == 0ull || o == end)) continue;  // outside the ROI slab
                 keys[o] = (uint32_t)(ty * TW + tx);
                 vals[o] = i;
                 ++o;
@@ -72,6 +75,7 @@ __global__ void __launch_bounds__(256) k_duplicate_ranked(const uint4* __restric
         for (int ty = TR.ty0[q]; ty <= TR.ty1[q]; ++ty)
             for (int tx = TR.tx0[q]; tx <= TR.tx1[q]; ++tx) {
                 if (q > 0 && in_earlier_rect(TR, q, tx, ty)) continue;
+                if (tm && (tm[ty * TW + tx] == 0ull || o == end)) continue;
                 keys[o] = (uint32_t)(ty * TW + tx);
                 vals[o] = i;
                 ++o;
@@ -163,10 +167,11 @@ void launch_gather_counts(const uint4* dup, const uint32_t* perm, int64_t n, uin
 }
 
 void launch_duplicate_ranked(const uint4* dup, const uint32_t* perm, const uint64_t* offs, int64_t n, int res,
-                             int bin_mode, uint64_t base, uint32_t* keys, uint32_t* vals, cudaStream_t s) {
+                             int bin_mode, uint64_t base, const uint64_t* tile_mask, uint32_t* keys,
+                             uint32_t* vals, cudaStream_t s) {
     if (n <= 0) return;
     k_duplicate_ranked<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dup, perm, offs, n, res, bin_mode, base,
-                                                                    keys, vals);
+                                                                    tile_mask, keys, vals);
 }
 
 void launch_decode_keys(const uint32_t* keys, const uint32_t* vals, const uint4* dup, const dgsm_plan_t& plan,

@@ -166,6 +166,7 @@ int validate(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int L, int r
     if (o.flags & ~(DGSM_OUTPUT_TAU | DGSM_COLLECT_STATS | DGSM_NO_TILE_CULL))
         return fail(DGSM_EINVAL, "unknown flags");
     if (o.absorption < DGSM_ABS_TRACEAVG || o.absorption > DGSM_ABS_DIAG) return fail(DGSM_EINVAL, "bad absorption");
+    if ((uintptr_t)o.slab % 8) return fail(DGSM_EINVAL, "slab not 8-B aligned");
     return DGSM_OK;
 }
 
@@ -189,6 +190,33 @@ void dgsm_default_opts(dgsm_build_opts_t* o) {
     o->bin_mode = DGSM_BIN_WRAP;
     o->flags = 0u;
     o->absorption = DGSM_ABS_TRACEAVG;
+    o->slab = nullptr;
+}
+
+size_t dgsm_slab_bytes(int n_lights, int atlas_res) {
+    if (n_lights < 1 || n_lights > DGSM_MAX_LIGHTS || atlas_res < 8 || atlas_res % 8 || atlas_res > 2048) return 0;
+    return slab_mask_bytes(n_lights, atlas_res) + sizeof(int2) * (size_t)n_lights;
+}
+
+int dgsm_active_slab(const float* receivers, int64_t m, const dgsm_roi_t* roi, const dgsm_light_t* lights,
+                     int n_lights, int atlas_res, int n_shells, void* slab, size_t slab_bytes, void* stream) {
+    g_launches = 0;
+    if (!roi || !lights || !slab) return fail(DGSM_EINVAL, "null roi, lights or slab");
+    if (n_lights < 1 || n_lights > DGSM_MAX_LIGHTS) return fail(DGSM_EINVAL, "n_lights %d outside [1, %d]", n_lights, DGSM_MAX_LIGHTS);
+    if (atlas_res < 8 || atlas_res % 8 != 0 || atlas_res > 2048) return fail(DGSM_EINVAL, "bad atlas_res %d", atlas_res);
+    if (n_shells < 1 || n_shells > DGSM_MAX_SHELLS) return fail(DGSM_EINVAL, "bad n_shells %d", n_shells);
+    if (m < 0 || (m > 0 && !receivers)) return fail(DGSM_EINVAL, "bad receivers");
+    if (!(roi->radius > 0.0f) || !(roi->z_min <= roi->z_max)) return fail(DGSM_EINVAL, "roi: need radius > 0, z_min <= z_max");
+    for (int l = 0; l < n_lights; ++l)
+        if (!(lights[l].t_max > 0.0f)) return fail(DGSM_EINVAL, "light %d: t_max <= 0", l);
+    if ((uintptr_t)slab % 256) return fail(DGSM_EINVAL, "slab not 256-B aligned");
+    const size_t need = dgsm_slab_bytes(n_lights, atlas_res);
+    if (slab_bytes < need) return fail(DGSM_ENOSPC, "slab %zu < %zu bytes", slab_bytes, need);
+    const LightsParam lp = lights_param(lights, n_lights);
+    launch_active_slab(receivers, m, *roi, lp, n_lights, atlas_res, n_shells, (uint64_t*)slab,
+                       (int2*)((char*)slab + slab_mask_bytes(n_lights, atlas_res)), (cudaStream_t)stream,
+                       &g_launches);
+    return cuda_check("active slab");
 }
 
 size_t dgsm_plan_workspace_bytes(int64_t n, int n_lights) {
@@ -285,7 +313,9 @@ static void run_binning(const dgsm_gaussians_t* g, int n_lights, const dgsm_buil
         launch_gather_counts(dup, perm, n, r.cperm, s);
         launch_scan_u32_to_u64(r.cperm, r.offs_perm, n, r.gscan_temp, s);
         // 3. key duplication (key = tile, value = Gaussian index)
-        launch_duplicate_ranked(dup, perm, r.offs_perm, n, res, o.bin_mode, (uint64_t)b, r.keys_a, r.vals_a, s);
+        const uint64_t* tm = o.slab ? slab_mask_ptr(o.slab) + (int64_t)l * n_tiles : nullptr;
+        launch_duplicate_ranked(dup, perm, r.offs_perm, n, res, o.bin_mode, (uint64_t)b, tm, r.keys_a, r.vals_a,
+                                s);
         g_launches += 6;
         // 4. stable sort of the tile digits
         const int ft = launch_onesweep_u32(r.keys_a + b, r.vals_a + b, r.keys_b + b, r.vals_b + b, e - b,
@@ -324,7 +354,8 @@ int dgsm_build_run(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_
     if (o.flags & DGSM_COLLECT_STATS) cudaMemsetAsync(r.stats, 0, sizeof(unsigned long long) * 8, s);
     // a6: accumulate + exp
     launch_accumulate(r.units, r.counters, r.max_units, r.vals_a, p.recs, g->n, lp, n_lights, res, K, o.flags,
-                      r.scratch, r.tile_arrive, r.counters + 1, atlas_out, r.stats, g_ev_before, g_ev_after, s);
+                      r.scratch, r.tile_arrive, r.counters + 1, atlas_out, r.stats, slab_mask_ptr(o.slab),
+                      slab_k_ptr(o.slab, n_lights, res), g_ev_before, g_ev_after, s);
     g_launches += 1;
     return cuda_check("build run");
 }

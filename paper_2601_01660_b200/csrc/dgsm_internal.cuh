@@ -124,6 +124,40 @@ __host__ __device__ inline uint32_t count_tiles(const TileRects& R) {
     return cnt;
 }
 
+// ROI slab buffer (include/dgsm.h dgsm_slab_bytes): per-tile texel masks, then k ranges.
+inline size_t slab_mask_bytes(int n_lights, int res) {
+    const size_t b = sizeof(uint64_t) * (size_t)n_lights * (res / kTile) * (res / kTile);
+    return (b + 255) / 256 * 256;
+}
+inline const uint64_t* slab_mask_ptr(const void* slab) { return (const uint64_t*)slab; }
+inline const int2* slab_k_ptr(const void* slab, int n_lights, int res) {
+    return slab ? (const int2*)((const char*)slab + slab_mask_bytes(n_lights, res)) : nullptr;
+}
+
+// Number of distinct tiles of the footprint that are active in the ROI slab
+// (tm = the light's per-tile texel masks, nonzero = active, NEXT-1); the same
+// enumeration order as the key duplication.
+__device__ inline uint32_t count_active_tiles(int c0, int c1, int r0, int r1, int res, int bin_mode,
+                                              const uint64_t* __restrict__ tm) {
+    const int TW = res / kTile;
+    uint32_t cnt = 0;
+    if (c0 > c1 || r0 > r1) return 0;
+    if (c0 >= 0 && c1 <= res - 1 && r0 >= 0 && r1 <= res - 1) {
+        for (int ty = r0 >> 3; ty <= (r1 >> 3); ++ty)
+            for (int tx = c0 >> 3; tx <= (c1 >> 3); ++tx) cnt += tm[ty * TW + tx] != 0ull;
+        return cnt;
+    }
+    TileRects TR;
+    make_tile_rects(c0, c1, r0, r1, res, bin_mode, TR);
+    for (int q = 0; q < TR.n; ++q)
+        for (int ty = TR.ty0[q]; ty <= TR.ty1[q]; ++ty)
+            for (int tx = TR.tx0[q]; tx <= TR.tx1[q]; ++tx) {
+                if (q > 0 && in_earlier_rect(TR, q, tx, ty)) continue;
+                cnt += tm[ty * TW + tx] != 0ull;
+            }
+    return cnt;
+}
+
 }  // namespace dgsm
 
 // ---------------------------------------------------------------- kernels
@@ -141,7 +175,8 @@ void launch_depth_keys(const uint4* dup, int64_t n, uint32_t dmin, uint32_t* key
                        cudaStream_t s);
 void launch_gather_counts(const uint4* dup, const uint32_t* perm, int64_t n, uint32_t* cperm, cudaStream_t s);
 void launch_duplicate_ranked(const uint4* dup, const uint32_t* perm, const uint64_t* offs, int64_t n, int res,
-                             int bin_mode, uint64_t base, uint32_t* keys, uint32_t* vals, cudaStream_t s);
+                             int bin_mode, uint64_t base, const uint64_t* tile_mask, uint32_t* keys,
+                             uint32_t* vals, cudaStream_t s);
 size_t onesweep_temp_bytes(int64_t n_max);
 // returns 1 if the sorted result ended in the *_alt buffers
 int launch_onesweep(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int64_t n,
@@ -161,7 +196,10 @@ void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint3
                        const uint32_t* vals, const PairRec* recs, int64_t n, const LightsParam& lp,
                        int n_lights, int res, int K, uint32_t flags, float* scratch, uint32_t* tile_arrive,
                        uint32_t* unit_counter, float* atlas, unsigned long long* stats,
+                       const uint64_t* slab_mask, const int2* slab_k,
                        cudaEvent_t ev_before, cudaEvent_t ev_after, cudaStream_t s);
+void launch_active_slab(const float* x, int64_t m, const dgsm_roi_t& roi, const LightsParam& lp, int n_lights,
+                        int res, int K, uint64_t* mask, int2* kr, cudaStream_t s, int* launches);
 void launch_exp(const float* tau, float* T, int64_t count, cudaStream_t s);
 void launch_query(const float* atlas, const LightsParam& lp, int n_lights, int res, int K,
                   const float* positions, int64_t m, float* T_out, float* colors, cudaStream_t s);

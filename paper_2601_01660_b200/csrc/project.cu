@@ -18,7 +18,8 @@ __global__ void __launch_bounds__(256, 3) k_project(
     const float* __restrict__ means, const float* __restrict__ scales,
     const float* __restrict__ rotations, const float* __restrict__ opacities, int64_t n,
     LightsParam lp, int n_lights, int res, int K, double kappa, double k_sigma, double rho,
-    int bin_mode, int absorption, bool no_cull, PairRec* __restrict__ recs, uint32_t* __restrict__ counts,
+    int bin_mode, int absorption, bool no_cull, const uint64_t* __restrict__ slab_mask,
+    PairRec* __restrict__ recs, uint32_t* __restrict__ counts,
     uint4* __restrict__ dup,
     PlanStats* stats) {
     __shared__ uint32_t s_dmin[DGSM_MAX_LIGHTS], s_dmax[DGSM_MAX_LIGHTS];
@@ -98,6 +99,9 @@ __global__ void __launch_bounds__(256, 3) k_project(
         const int ic0 = (int)c0, ic1 = (int)c1, ir0 = (int)r0, ir1 = (int)r1;
         if (ic0 > ic1 || ir0 > ir1) {
             cnt = 0;
+        } else if (slab_mask) {  // NEXT-1: only the tiles holding a texel of the ROI pixel set
+            cnt = count_active_tiles(ic0, ic1, ir0, ir1, res, bin_mode,
+                                     slab_mask + (int64_t)l * (res / kTile) * (res / kTile));
         } else if (ic0 >= 0 && ic1 <= W - 1 && ir0 >= 0 && ir1 <= H - 1) {  // common case: inside the grid
             cnt = (uint32_t)((ic1 >> 3) - (ic0 >> 3) + 1) * (uint32_t)((ir1 >> 3) - (ir0 >> 3) + 1);
         } else {
@@ -176,7 +180,8 @@ void launch_project(const dgsm_gaussians_t& g, const LightsParam& lp, int n_ligh
     k_project<<<(unsigned)grid, bs, 0, s>>>(g.means, g.scales, g.rotations, g.opacities, g.n, lp,
                                             n_lights, res, K, (double)o.kappa, (double)o.k_sigma,
                                             (double)o.rho_scale * (double)(2 * res) / (2.0 * kPi), o.bin_mode,
-                                            o.absorption, (o.flags & DGSM_NO_TILE_CULL) != 0, recs, counts, dup,
+                                            o.absorption, (o.flags & DGSM_NO_TILE_CULL) != 0,
+                                            slab_mask_ptr(o.slab), recs, counts, dup,
                                             stats);
 }
 

@@ -32,7 +32,8 @@ _STATUS = {0: "DGSM_OK", 1: "DGSM_EINVAL", 2: "DGSM_ENOSPC", 3: "DGSM_ECUDA", 4:
 
 EXPORTED = ["dgsm_default_opts", "dgsm_plan_workspace_bytes", "dgsm_build_plan", "dgsm_build_run",
             "dgsm_build_bins", "dgsm_build", "dgsm_exp_epilogue", "dgsm_query", "dgsm_query_footprint", "dgsm_strerror",
-            "dgsm_last_error", "dgsm_last_launch_count", "dgsm_build_stats", "dgsm_set_accumulate_events"]
+            "dgsm_last_error", "dgsm_last_launch_count", "dgsm_build_stats", "dgsm_set_accumulate_events",
+            "dgsm_slab_bytes", "dgsm_active_slab"]
 
 
 class Gaussians(C.Structure):
@@ -46,7 +47,12 @@ class Light(C.Structure):
 
 class BuildOpts(C.Structure):
     _fields_ = [("kappa", C.c_float), ("k_sigma", C.c_float), ("rho_scale", C.c_float),
-                ("bin_mode", C.c_int32), ("flags", C.c_uint32), ("absorption", C.c_int32)]
+                ("bin_mode", C.c_int32), ("flags", C.c_uint32), ("absorption", C.c_int32),
+                ("slab", C.c_void_p)]
+
+
+class Roi(C.Structure):
+    _fields_ = [("center", C.c_float * 3), ("radius", C.c_float), ("z_min", C.c_float), ("z_max", C.c_float)]
 
 
 class Plan(C.Structure):
@@ -96,6 +102,10 @@ def lib() -> C.CDLL:
         L.dgsm_query.argtypes = [vp, P(Light), C.c_int, C.c_int, C.c_int, vp, i64, vp, vp, vp]
         L.dgsm_query_footprint.argtypes = [vp, P(Light), C.c_int, C.c_int, C.c_int, vp, vp, vp, i64, vp, vp,
                                            C.c_int, vp, vp, vp]
+        L.dgsm_slab_bytes.argtypes = [C.c_int, C.c_int]
+        L.dgsm_slab_bytes.restype = sz
+        L.dgsm_active_slab.argtypes = [vp, i64, P(Roi), P(Light), C.c_int, C.c_int, C.c_int, vp, sz, vp]
+        L.dgsm_active_slab.restype = C.c_int
         L.dgsm_strerror.argtypes = [C.c_int]
         L.dgsm_strerror.restype = C.c_char_p
         L.dgsm_last_error.argtypes = []
@@ -182,6 +192,7 @@ class Options:
     collect_stats: bool = False
     absorption: str = "traceavg"   # traceavg (Eq.5) | simple | mass | diag (ablation B)
     tile_cull: bool = True         # False: ablation D, every Gaussian in every tile
+    slab: Optional[torch.Tensor] = None  # NEXT-1 ROI slab from active_slab(); None = full atlas
 
     def c(self) -> BuildOpts:
         if self.absorption not in ABSORPTION:
@@ -191,7 +202,8 @@ class Options:
                          (DGSM_OUTPUT_TAU if self.output_tau else 0) |
                          (DGSM_COLLECT_STATS if self.collect_stats else 0) |
                          (0 if self.tile_cull else DGSM_NO_TILE_CULL),
-                         ABSORPTION[self.absorption])
+                         ABSORPTION[self.absorption],
+                         None if self.slab is None else C.c_void_p(self.slab.data_ptr()))
 
 
 def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
@@ -324,6 +336,28 @@ def query(atlas: torch.Tensor, lights, positions: torch.Tensor, colors: Optional
 
 
 DGSM_MAX_FOOTPRINT_SAMPLES = 64
+
+
+def active_slab(receivers: torch.Tensor, roi, lights, atlas_res: int, n_shells: int,
+                out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """NEXT-1: the voxel slab of the receivers (CUDA
+    float32 [m, 3]) inside B = {||(x - c)_xy||_inf <= R, z_min <= z <= z_max}.
+    ``roi`` = (c_x, c_y, c_z, R, z_min, z_max).  Returns the device slab buffer
+    (uint8, include/dgsm.h layout) to pass as Options(slab=...)."""
+    x = _dev_f32(receivers, "receivers", (3,))
+    arr, nl = _lights(lights)
+    need = int(lib().dgsm_slab_bytes(nl, int(atlas_res)))
+    if need == 0:
+        raise DgsmError("bad n_lights or atlas_res for a slab")
+    if out is None:
+        out = torch.empty(need, dtype=torch.uint8, device=x.device)
+    r = [float(v) for v in roi]
+    croi = Roi((C.c_float * 3)(*r[:3]), r[3], r[4], r[5])
+    rc = lib().dgsm_active_slab(C.c_void_p(x.data_ptr()), x.shape[0], C.byref(croi), arr, nl, int(atlas_res),
+                                int(n_shells), C.c_void_p(out.data_ptr()), out.numel(),
+                                C.c_void_p(_stream_ptr(stream)))
+    _check(rc, "dgsm_active_slab")
+    return out
 
 
 def footprint_stencil(kind: str = "stencil7", delta: float = 1.0):

@@ -107,6 +107,20 @@ def test_validation_fails_before_device_work(lib):
     for n in (0, 65):
         assert lib.dgsm_query_footprint(None, lights, 1, 16, 4, None, None, None, 0, z, w, n, None, None, None) == 1
     assert lib.dgsm_query_footprint(None, lights, 1, 16, 4, None, None, None, 0, None, w, 1, None, None, None) == 1
+    # ROI slab (NEXT-1): sizes and validation
+    assert lib.dgsm_slab_bytes(1, 16) == 256 + 8 and lib.dgsm_slab_bytes(2, 2048) == 8 * 2 * 256 * 256 + 16
+    assert lib.dgsm_slab_bytes(0, 16) == 0 and lib.dgsm_slab_bytes(1, 12) == 0
+    roi = dgsm.Roi((C.c_float * 3)(0, 0, 0), 2.0, 0.0, 1.0)
+    buf = C.c_void_p(256)
+    assert lib.dgsm_active_slab(None, 0, C.byref(roi), lights, 1, 16, 4, buf, 16, None) == 2
+    assert lib.dgsm_active_slab(None, 0, C.byref(roi), lights, 1, 16, 4, None, 1 << 20, None) == 1
+    assert lib.dgsm_active_slab(None, 5, C.byref(roi), lights, 1, 16, 4, buf, 1 << 20, None) == 1
+    roi.radius = 0.0
+    assert lib.dgsm_active_slab(None, 0, C.byref(roi), lights, 1, 16, 4, buf, 1 << 20, None) == 1
+    roi.radius, roi.z_min = 2.0, 2.0
+    assert lib.dgsm_active_slab(None, 0, C.byref(roi), lights, 1, 16, 4, buf, 1 << 20, None) == 1
+    o = dgsm.BuildOpts(1.0, 3.0, 1.0, 0, 0, 0, C.c_void_p(12))  # misaligned slab
+    assert lib.dgsm_build_plan(C.byref(g), lights, 1, 16, 4, C.byref(o), ws, 1 << 20, C.byref(plan), None) == 1
 
 
 def test_binding_refuses_cpu_tensors():

@@ -239,6 +239,88 @@ def test_query_footprint_parity(dg, oracle_mod, kind):
     assert np.abs(ct.cpu().numpy() - col * want[:, None]).max() <= 4e-6
 
 
+def unpack_slab(buf, L, res):
+    """include/dgsm.h slab layout -> (mask bool [L, res, res], krange int32 [L, 2])."""
+    TW = res // 8
+    raw = buf.cpu().numpy()
+    nb = 8 * L * TW * TW
+    words = np.frombuffer(raw[:nb].tobytes(), np.uint64).reshape(L, TW, TW)
+    bits = (words[..., None] >> np.arange(64, dtype=np.uint64)) & np.uint64(1)
+    mask = bits.reshape(L, TW, TW, 8, 8).transpose(0, 1, 3, 2, 4).reshape(L, res, res).astype(bool)
+    off = (nb + 255) // 256 * 256
+    kr = np.frombuffer(raw[off:off + 8 * L].tobytes(), np.int32).reshape(L, 2)
+    return mask, kr
+
+
+def _slab_case(seed):
+    s = synth.random_scene(seed, 300, res=32, K=12, L=3, dist=(0.3, 3.0), scale=(0.02, 0.4))
+    rng = np.random.default_rng(seed + 100)
+    rec = rng.uniform(-3, 3, (3000, 3)).astype(np.float32)
+    rec[:3] = s.lights["position"][0]  # receivers at a light: skipped for that light
+    rec[3:6] = s.lights["position"][0] + np.array([[-1.0, 0, 0], [0, 1.0, 0], [0, 0, -1.0]], np.float32)  # seams
+    roi = (0.2, -0.1, 0.3, 1.4, -1.0, 1.5)
+    return s, rec, roi
+
+
+@pytest.mark.parametrize("seed", [41, 42])
+def test_active_slab_bit_exact(dg, oracle_mod, seed):
+    """NEXT-1 pixel set P and k range: bit-exact against the oracle (fp64 decisions)."""
+    s, rec, roi = _slab_case(seed)
+    slab = dg.active_slab(torch.from_numpy(rec).cuda(), roi, s.lights, s.res, s.K)
+    mask, kr = unpack_slab(slab, s.L, s.res)
+    wm, wk, inside = oracle_mod.active_slab(rec, roi, s.lights, s.res, s.K)
+    assert inside > 0 and np.array_equal(mask, wm) and np.array_equal(kr, wk)
+    # empty ROI: nothing marked, every light empty
+    slab = dg.active_slab(torch.from_numpy(rec).cuda(), (50, 50, 0, 0.1, 0, 0), s.lights, s.res, s.K)
+    mask, kr = unpack_slab(slab, s.L, s.res)
+    assert not mask.any() and (kr[:, 0] == s.K).all() and (kr[:, 1] == -1).all()
+
+
+def test_slab_build_parity_and_exactness(dg, oracle_mod):
+    """Slab build against the oracle's slab build; 1 outside the slab
+    bit-exactly; queries at receivers in B equal those on the full GPU atlas
+    bit-for-bit; binning restricted to the active tiles, bit-exact."""
+    s, rec, roi = _slab_case(43)
+    rt = torch.from_numpy(rec).cuda()
+    slab = dg.active_slab(rt, roi, s.lights, s.res, s.K)
+    g = dg.to_device(s.gaussians)
+    Ts = dg.build(g, s.lights, s.res, s.K, dg.Options(slab=slab))
+    Tf = dg.build(g, s.lights, s.res, s.K)
+    mask, kr, inside = oracle_mod.active_slab(rec, roi, s.lights, s.res, s.K)
+    To, _ = oracle_mod.build(s.gaussians, s.lights, s.res, s.K, slab=(mask, kr))
+    Tsn = Ts.cpu().numpy()
+    assert np.abs(Tsn - To).max() <= TOL_T
+    kk = np.arange(s.K)[None, :, None, None]
+    in_slab = mask[:, None] & (kk >= kr[:, 0, None, None, None]) & (kk <= kr[:, 1, None, None, None])
+    assert (Tsn[~in_slab] == 1.0).all()
+    assert np.array_equal(Tsn[in_slab], Tf.cpu().numpy()[in_slab])
+    ins = (np.maximum(np.abs(rec[:, 0] - roi[0]), np.abs(rec[:, 1] - roi[1])) <= roi[3]) & \
+          (rec[:, 2] >= roi[4]) & (rec[:, 2] <= roi[5])
+    xin = torch.from_numpy(rec[ins]).cuda()
+    assert torch.equal(dg.query(Ts, s.lights, xin), dg.query(Tf, s.lights, xin))
+    # tau output honours the slab too (tau = 0 outside)
+    tau = dg.build(g, s.lights, s.res, s.K, dg.Options(slab=slab, output_tau=True)).cpu().numpy()
+    assert (tau[~in_slab] == 0.0).all()
+    # binning: the oracle's entries restricted to tiles holding a texel of P
+    plan, got, ts, te = gpu_bins(dg, s, slab=slab)
+    want = oracle_bins(oracle_mod, s)
+    tile_on = mask.reshape(s.L, s.res // 8, 8, s.res // 8, 8).any(axis=(2, 4)).reshape(s.L, -1)
+    keep = tile_on[want[0].astype(np.int64), want[1].astype(np.int64)]
+    want = [w[keep] for w in want]
+    assert plan.n_keys == len(want[0]) and plan.n_keys < len(keep)
+    for a, b in zip(got, want):
+        assert np.array_equal(a, b)
+
+
+def test_slab_empty_roi_all_ones(dg):
+    s, rec, _ = _slab_case(44)
+    slab = dg.active_slab(torch.from_numpy(rec).cuda(), (50, 50, 0, 0.1, 0, 0), s.lights, s.res, s.K)
+    plan = dg.BuildPlan(dg.to_device(s.gaussians), s.lights, s.res, s.K, dg.Options(slab=slab))
+    assert plan.n_keys == 0
+    T = dg.build(dg.to_device(s.gaussians), s.lights, s.res, s.K, dg.Options(slab=slab))
+    assert torch.all(T == 1.0)
+
+
 def test_query_empty(dg):
     atlas = torch.ones(1, 4, 16, 16, device="cuda")
     out = dg.query(atlas, dict(position=[[0, 0, 0]], t_max=[1.0]), torch.zeros(0, 3, device="cuda"))
