@@ -65,6 +65,9 @@ typedef struct dgsm_build_stats {
     uint64_t pairs_live;    /* pairs whose Eq.3 prefactor is non-zero in fp32 (r <= 180, x0 < 3.92) */
     uint64_t window_shells; /* shells evaluated with an erf (|x_k| < 3.92) */
     uint64_t steps;         /* saturated tails added as one step */
+    uint64_t warp_records;  /* (warp, listed Gaussian) iterations = 2 * P (two warps per tile) */
+    uint64_t warp_live_any; /* of those, with at least one live lane (the warp runs the live path) */
+    uint64_t warp_live_max; /* sum over (warp, stage) of the max live count of one lane */
 } dgsm_build_stats_t;
 
 /* Occluder Gaussians, structure of arrays, DEVICE pointers (mean mu_i,

@@ -64,7 +64,9 @@ __device__ __forceinline__ float erf_fast(float x) {
     q = fmaf(q, t, -9.184432626e-01f);
     q = fmaf(q, t, -1.627907276e+00f);
     q = fmaf(q, t, 4.901340445e-10f);
-    const float r = t >= kXS ? 1.0f : 1.0f - ex2_approx(q);
+    // saturated: 2^-256 flushes to 0, so r == 1 exactly without a branch
+    q = t >= kXS ? -256.0f : q;
+    const float r = 1.0f - ex2_approx(q);
     return copysignf(r, x);
 }
 
@@ -132,6 +134,30 @@ struct AccLights {
 //  q4 = (W8, eD, betap, kD as int bits)
 constexpr int kCompact = 5;
 
+// Shared-memory float4 load by 32-bit shared address (keeps the per-record
+// address arithmetic to one integer add; see DESIGN.md a6 notes).
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(a)
+                 : "memory");
+    return v;
+}
+
+struct Compact {
+    float4 q0, q1, q2, q3, q4;
+};
+__device__ __forceinline__ Compact load_compact(uint32_t a) {
+    Compact c;
+    c.q0 = lds4(a);
+    c.q1 = lds4(a + 16);
+    c.q2 = lds4(a + 32);
+    c.q3 = lds4(a + 48);
+    c.q4 = lds4(a + 64);
+    return c;
+}
+
 // ---- per (texel, Gaussian) pair ---------------------------------------------
 struct PairTest {
     float wx, wy, wz, ux, uy, uz, a, ia, r_over_D2;
@@ -139,8 +165,8 @@ struct PairTest {
 };
 
 // delta-formulation (R9) up to the negligible-pair test (R8'): r/D^2 = |g x W delta|^2 / a.
-__device__ __forceinline__ PairTest pair_test(const float4* q, float etx, float ety, float etz) {
-    const float4 q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3], q4 = q[4];
+__device__ __forceinline__ PairTest pair_test(const Compact& c, float etx, float ety, float etz) {
+    const float4 q0 = c.q0, q1 = c.q1, q2 = c.q2, q3 = c.q3, q4 = c.q4;
     PairTest p;
     // delta = d - d_i = e_t - f  (both small, fp32-exact to ~1e-7 relative)
     const float ex = etx - q0.x, ey = ety - q0.y, ez = etz - q0.z;
@@ -164,10 +190,10 @@ __device__ __forceinline__ PairTest pair_test(const float4* q, float etx, float 
 // Eq.3 over the shells for a live pair: window shells (|x_k| < kXS) as differences,
 // then the saturated step pref (1 - erf(x_0)) at the first saturated shell.
 template <bool kStats>
-__device__ __forceinline__ void pair_live(const PairTest& p, const float4* q, float* s_acc, int tid, int K,
+__device__ __forceinline__ void pair_live(const PairTest& p, const Compact& c, float* s_acc, int tid, int K,
                                           float dt, float dtlo, float idt, uint32_t& st_live,
                                           uint32_t& st_win, uint32_t& st_step) {
-    const float4 q1 = q[1], q4 = q[4];
+    const float4 q1 = c.q1, q4 = c.q4;
     const float D = q1.w;
     const float rr = p.r_over_D2 * D * D;
     // s* - D = -D (u . W delta)/a: closest approach relative to D
@@ -190,12 +216,13 @@ __device__ __forceinline__ void pair_live(const PairTest& p, const float4* q, fl
     const int khi = max((int)ceilf(fminf(fmaxf(kf_hi, 0.0f), (float)K)), klo);
     if (kStats) { st_win += (uint32_t)(khi - klo); st_step += khi < K ? 1u : 0u; }
     float prev = 0.0f;
+    float fk = (float)(klo - kD);  // k - kD, exact in fp32
+    float* ap = s_acc + klo * kThreads + tid;
 #pragma unroll 1
-    for (int k = klo; k < khi; ++k) {
-        const float fk = (float)(k - kD);
+    for (int k = klo; k < khi; ++k, fk += 1.0f, ap += kThreads) {
         const float tk = fmaf(fk, dt, fmaf(fk, dtlo, e));
         const float w = pref * (erf_fast(h * tk) - e0);
-        s_acc[k * kThreads + tid] += w - prev;
+        *ap += w - prev;
         prev = w;
     }
     if (khi < K) s_acc[khi * kThreads + tid] += fmaf(pref, 1.0f - e0, -prev);
@@ -248,7 +275,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
         texel_dir(row, col, W, H, t0, t1, t2);
         const float etx = (float)(t0 - c0), ety = (float)(t1 - c1), etz = (float)(t2 - c2);
         for (int k = 0; k < K; ++k) s_acc[k * kThreads + tid] = 0.0f;
-        uint32_t st_live = 0, st_win = 0, st_step = 0;
+        uint32_t st_live = 0, st_win = 0, st_step = 0, st_wany = 0, st_wmax = 0;
 
         const float dt = al.dt[l], dtlo = al.dtlo[l], idt = al.idt[l];
         const uint32_t n_rec = wu.jend - wu.jbeg;
@@ -295,14 +322,24 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
                 issue(b + 1);
             }
             // two records per iteration: independent dependency chains for the pair test
-            for (uint32_t r = 0; r < nb; r += 2) {
-                const uint32_t r2 = min(r + 1, nb - 1);
-                PairTest A = pair_test(s_cr + r * kCompact, etx, ety, etz);
-                PairTest B = pair_test(s_cr + r2 * kCompact, etx, ety, etz);
+            uint32_t my_live = 0;
+            uint32_t ra_addr = smem_addr(s_cr);  // induction variable: record r's compact form
+            for (uint32_t r = 0; r < nb; r += 2, ra_addr += 2 * kCompact * 16) {
+                const uint32_t rb_addr = r + 1 < nb ? ra_addr + kCompact * 16 : ra_addr;
+                const Compact ca = load_compact(ra_addr);
+                const Compact cb = load_compact(rb_addr);
+                PairTest A = pair_test(ca, etx, ety, etz);
+                PairTest B = pair_test(cb, etx, ety, etz);
                 B.live = B.live && (r + 1 < nb);
-                if (A.live) pair_live<kStats>(A, s_cr + r * kCompact, s_acc, tid, K, dt, dtlo, idt, st_live, st_win, st_step);
-                if (B.live) pair_live<kStats>(B, s_cr + r2 * kCompact, s_acc, tid, K, dt, dtlo, idt, st_live, st_win, st_step);
+                if (kStats) {
+                    const uint32_t ba = __ballot_sync(0xffffffffu, A.live), bb = __ballot_sync(0xffffffffu, B.live);
+                    my_live += (uint32_t)A.live + (uint32_t)B.live;
+                    st_wany += (ba != 0u) + (bb != 0u);
+                }
+                if (A.live) pair_live<kStats>(A, ca, s_acc, tid, K, dt, dtlo, idt, st_live, st_win, st_step);
+                if (B.live) pair_live<kStats>(B, cb, s_acc, tid, K, dt, dtlo, idt, st_live, st_win, st_step);
             }
+            if (kStats) st_wmax += __reduce_max_sync(0xffffffffu, my_live);
             __syncthreads();  // compact copy consumed
         }
 
@@ -311,6 +348,13 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
             atomicAdd(&stats[2], (unsigned long long)st_win);
             atomicAdd(&stats[3], (unsigned long long)st_step);
             if (tid == 0) atomicAdd(&stats[0], (unsigned long long)n_rec * kThreads);
+            // warp-level: records entering the live path (any lane live) and the
+            // per-stage max over lanes of live records (what a per-lane loop would cost)
+            if ((tid & 31) == 0) {
+                atomicAdd(&stats[4], (unsigned long long)n_rec);
+                atomicAdd(&stats[5], (unsigned long long)st_wany);
+                atomicAdd(&stats[6], (unsigned long long)st_wmax);
+            }
         }
         // prefix sum over shells -> tau_k; epilogue T = exp(-tau) (Eq.4)
         const bool want_tau = (flags & DGSM_OUTPUT_TAU) != 0;

@@ -107,13 +107,21 @@ __global__ void __launch_bounds__(256) k_unit_counts(const uint32_t* __restrict_
     cnt[t] = (uint64_t)c | ((uint64_t)(c > 1 ? c : 0) << 32);
 }
 
+// Size class of a work unit for the longest-first dispatch order: 0 for an
+// empty tile, else 1 + floor(log2(keys)) (<= 31).
+__device__ __forceinline__ int unit_class(uint32_t len) { return len ? 32 - __clz(len) : 0; }
+
 __global__ void __launch_bounds__(256) k_units(const uint32_t* __restrict__ ts,
                                                const uint32_t* __restrict__ te,
                                                const uint64_t* __restrict__ off, int64_t nt, int chunk,
-                                               WorkUnit* __restrict__ units, uint32_t* n_units) {
+                                               WorkUnit* __restrict__ units, uint32_t* n_units,
+                                               uint32_t* __restrict__ class_hist) {
+    __shared__ uint32_t s_hist[kUnitClasses];
+    if (threadIdx.x < kUnitClasses) s_hist[threadIdx.x] = 0u;
+    __syncthreads();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t == 0) *n_units = (uint32_t)(off[nt] & 0xffffffffu);
-    if (t >= nt) return;
+    if (t < nt) {
     const uint32_t s = ts[t], e = te[t];
     const uint64_t o = off[t];
     const uint32_t u0 = (uint32_t)(o & 0xffffffffu), slot = (uint32_t)(o >> 32);
@@ -129,6 +137,32 @@ __global__ void __launch_bounds__(256) k_units(const uint32_t* __restrict__ ts,
         w.slot = slot;
         w.pad0 = w.pad1 = 0;
         units[u0 + c] = w;
+        atomicAdd(&s_hist[unit_class(w.jend - w.jbeg)], 1u);
+    }
+    }
+    __syncthreads();
+    if (threadIdx.x < kUnitClasses && s_hist[threadIdx.x]) atomicAdd(&class_hist[threadIdx.x], s_hist[threadIdx.x]);
+}
+
+// Longest-processing-time-first order of the persistent accumulation grid:
+// units are scattered by size class, largest class first, so the tail of the
+// grid is made of the smallest units (results do not depend on this order:
+// every unit writes its own tile or its own scratch slot).
+__global__ void __launch_bounds__(256) k_units_lpt(const WorkUnit* __restrict__ in, const uint32_t* n_units,
+                                                   const uint32_t* __restrict__ class_hist,
+                                                   uint32_t* __restrict__ class_fill,
+                                                   WorkUnit* __restrict__ out) {
+    __shared__ uint32_t s_base[kUnitClasses];
+    if (threadIdx.x == 0) {
+        uint32_t b = 0;
+        for (int c = kUnitClasses - 1; c >= 0; --c) { s_base[c] = b; b += class_hist[c]; }
+    }
+    __syncthreads();
+    const uint32_t n = *n_units;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const WorkUnit w = in[j];
+        const int c = unit_class(w.jend - w.jbeg);
+        out[s_base[c] + atomicAdd(&class_fill[c], 1u)] = w;
     }
 }
 
@@ -193,13 +227,17 @@ void launch_ranges(const uint32_t* keys, int64_t begin, int64_t end, uint32_t ti
 }
 
 void launch_units(const uint32_t* tile_start, const uint32_t* tile_end, int64_t n_tiles_total, int chunk,
-                  uint64_t* unit_counts, uint64_t* unit_offsets, void* scan_temp, WorkUnit* units,
-                  uint32_t* n_units_dev, cudaStream_t s, int* launches) {
+                  uint64_t* unit_counts, uint64_t* unit_offsets, void* scan_temp, WorkUnit* units_tmp,
+                  WorkUnit* units, uint32_t max_units, uint32_t* n_units_dev, uint32_t* class_hist,
+                  uint32_t* class_fill, cudaStream_t s, int* launches) {
     const unsigned g = (unsigned)((n_tiles_total + 255) / 256);
     k_unit_counts<<<g, 256, 0, s>>>(tile_start, tile_end, n_tiles_total, chunk, unit_counts);
     launch_scan_u64(unit_counts, unit_offsets, n_tiles_total, scan_temp, s);
-    k_units<<<g, 256, 0, s>>>(tile_start, tile_end, unit_offsets, n_tiles_total, chunk, units, n_units_dev);
-    *launches += 5;
+    k_units<<<g, 256, 0, s>>>(tile_start, tile_end, unit_offsets, n_tiles_total, chunk, units_tmp, n_units_dev,
+                              class_hist);
+    const unsigned gl = (unsigned)std::min<uint32_t>((max_units + 255) / 256, 148u * 8u);
+    k_units_lpt<<<gl, 256, 0, s>>>(units_tmp, n_units_dev, class_hist, class_fill, units);
+    *launches += 6;
 }
 
 }  // namespace dgsm

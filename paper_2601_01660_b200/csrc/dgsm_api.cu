@@ -80,8 +80,8 @@ struct RunLayout {
     uint32_t *tile_start, *tile_end;
     uint64_t *unit_cnt, *unit_off;
     void* unit_scan_temp;
-    WorkUnit* units;
-    uint32_t* counters;  // [0] n_units, [1] unit counter
+    WorkUnit *units, *units_tmp;
+    uint32_t* counters;  // [0] n_units, [1] unit counter, [32..63] unit class histogram, [64..95] class fill
     uint32_t* tile_arrive;
     unsigned long long* stats;  // [4] pairs, live pairs, window shells, steps (DGSM_COLLECT_STATS)
     float* scratch;
@@ -118,7 +118,8 @@ RunLayout run_layout(void* ws, const dgsm_plan_t& pl) {
     const int64_t max_units = nt + P / pl.chunk + 1;
     r.max_units = (uint32_t)max_units;
     r.units = c.take<WorkUnit>(max_units);
-    r.counters = c.take<uint32_t>(64);
+    r.units_tmp = c.take<WorkUnit>(max_units);
+    r.counters = c.take<uint32_t>(96);
     r.tile_arrive = c.take<uint32_t>(nt);
     r.stats = c.take<unsigned long long>(8);
     const int64_t max_slots = 2 * (P / pl.chunk) + 1;
@@ -347,9 +348,9 @@ int dgsm_build_run(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_
     const int64_t nt = n_lights * (int64_t)(res / kTile) * (res / kTile);
 
     run_binning(g, n_lights, o, plan, p, r, s);
-    launch_units(r.tile_start, r.tile_end, nt, plan->chunk, r.unit_cnt, r.unit_off, r.unit_scan_temp, r.units,
-                 r.counters, s, &g_launches);
-    cudaMemsetAsync(r.counters + 1, 0, sizeof(uint32_t), s);
+    cudaMemsetAsync(r.counters, 0, sizeof(uint32_t) * 96, s);
+    launch_units(r.tile_start, r.tile_end, nt, plan->chunk, r.unit_cnt, r.unit_off, r.unit_scan_temp, r.units_tmp,
+                 r.units, r.max_units, r.counters, r.counters + 32, r.counters + 64, s, &g_launches);
     cudaMemsetAsync(r.tile_arrive, 0, sizeof(uint32_t) * nt, s);
     if (o.flags & DGSM_COLLECT_STATS) cudaMemsetAsync(r.stats, 0, sizeof(unsigned long long) * 8, s);
     // a6: accumulate + exp
@@ -470,13 +471,16 @@ int dgsm_build_stats(const dgsm_plan_t* plan, void* run_ws, size_t run_ws_bytes,
     if (!plan || !run_ws || !out) return fail(DGSM_EINVAL, "null argument");
     if (run_ws_bytes < plan->run_workspace_bytes) return fail(DGSM_ENOSPC, "run workspace too small");
     const RunLayout r = run_layout(run_ws, *plan);
-    unsigned long long h[4];
+    unsigned long long h[7];
     cudaMemcpyAsync(h, r.stats, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
     if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return cuda_check("stats");
     out->pairs = h[0];
     out->pairs_live = h[1];
     out->window_shells = h[2];
     out->steps = h[3];
+    out->warp_records = h[4];
+    out->warp_live_any = h[5];
+    out->warp_live_max = h[6];
     return DGSM_OK;
 }
 

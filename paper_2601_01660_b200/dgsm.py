@@ -66,7 +66,8 @@ class Plan(C.Structure):
 
 class BuildStats(C.Structure):
     _fields_ = [("pairs", C.c_uint64), ("pairs_live", C.c_uint64), ("window_shells", C.c_uint64),
-                ("steps", C.c_uint64)]
+                ("steps", C.c_uint64), ("warp_records", C.c_uint64), ("warp_live_any", C.c_uint64),
+                ("warp_live_max", C.c_uint64)]
 
 
 class DgsmError(RuntimeError):
@@ -272,7 +273,7 @@ class BuildPlan:
         rc = lib().dgsm_build_stats(C.byref(self.plan), C.c_void_p(ws.data_ptr()), ws.numel(), C.byref(st),
                                     C.c_void_p(_stream_ptr(stream)))
         _check(rc, "dgsm_build_stats")
-        return dict(pairs=st.pairs, pairs_live=st.pairs_live, window_shells=st.window_shells, steps=st.steps)
+        return {f: int(getattr(st, f)) for f, _ in BuildStats._fields_}
 
     def bins(self, stream=None):
         """Sorted (light, tile, depth_bits, index) uint32 arrays + tile ranges (device int64 views)."""
