@@ -29,8 +29,14 @@
 namespace dgsm {
 
 namespace {
-constexpr int kThreads = 64;      // one 8x8 tile
+constexpr int kThreads = kTexels / kTileSplit;  // one warp = one half of an 8x8 tile
 constexpr int kStage = 32;        // records per pipeline stage
+
+// One-warp CTAs synchronise with __syncwarp (no CTA barrier between the halves
+// of a tile: each half is an independent work unit).
+__device__ __forceinline__ void cta_sync() {
+    if (kThreads == 32) __syncwarp(); else __syncthreads();
+}
 constexpr float kXS = 3.92f;      // |x| >= kXS  ->  erf_fast(x) == +-1 exactly
 constexpr float kRCut = 180.0f;   // r > kRCut -> ex2.approx.ftz(-r/(2 ln 2)) == 0 exactly
 
@@ -250,7 +256,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
         mbar_init(&s_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();
+    cta_sync();
     uint32_t phase = 0u;
     const uint32_t n_units = *n_units_dev;
     const int TW = res / kTile;
@@ -259,15 +265,17 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
 
     for (;;) {
         if (tid == 0) s_unit = atomicAdd(unit_counter, 1u);
-        __syncthreads();
+        cta_sync();
         const uint32_t u = s_unit;
         if (u >= n_units) break;
         const WorkUnit wu = units[u];
         const int l = (int)(wu.tile / (uint32_t)n_tiles);
         const int tile = (int)(wu.tile - (uint32_t)l * n_tiles);
         const int row0 = (tile / TW) * kTile, col0 = (tile % TW) * kTile;
-        const int row = row0 + (tid >> 3);
-        const int col = col0 + (tid & 7);
+        const int tt = (int)wu.part * kThreads + tid;  // texel index within the tile
+        const int row = row0 + (tt >> 3);
+        const int col = col0 + (tt & 7);
+        const uint32_t tslot = wu.tile * kTileSplit + wu.part;  // (tile, part) arrival counter
 
         // texel direction relative to the tile reference direction d_c (fp64 -> fp32)
         double c0, c1, c2, t0, t1, t2;
@@ -316,7 +324,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
                 q[3] = make_float4(R.W[4], R.W[5], R.W[6], R.W[7]);
                 q[4] = make_float4(R.W[8], R.eD, R.betap, __int_as_float(R.kD));
             }
-            __syncthreads();  // compact copy ready; raw buffer free
+            cta_sync();  // compact copy ready; raw buffer free
             if (b + 1 < n_batches) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 issue(b + 1);
@@ -340,7 +348,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
                 if (B.live) pair_live<kStats>(B, cb, s_acc, tid, K, dt, dtlo, idt, st_live, st_win, st_step);
             }
             if (kStats) st_wmax += __reduce_max_sync(0xffffffffu, my_live);
-            __syncthreads();  // compact copy consumed
+            cta_sync();  // compact copy consumed
         }
 
         if (kStats) {
@@ -365,7 +373,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
         if (slab_mask) {
             const int2 kr = slab_k[l];
             klo = kr.x;
-            khi = ((slab_mask[wu.tile] >> tid) & 1ull) ? kr.y : -1;
+            khi = ((slab_mask[wu.tile] >> tt) & 1ull) ? kr.y : -1;
         }
         const float one = want_tau ? 0.0f : 1.0f;
         if (wu.nchunks == 1) {
@@ -382,9 +390,9 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
                 part[(size_t)k * kThreads] = tau;
             }
             __threadfence();
-            __syncthreads();
-            if (tid == 0) s_last = (atomicAdd(&tile_arrive[wu.tile], 1u) == wu.nchunks - 1) ? 1u : 0u;
-            __syncthreads();
+            cta_sync();
+            if (tid == 0) s_last = (atomicAdd(&tile_arrive[tslot], 1u) == wu.nchunks - 1) ? 1u : 0u;
+            cta_sync();
             if (s_last) {
                 __threadfence();
                 const float* base = scratch + ((size_t)wu.slot * K) * kThreads + tid;
@@ -394,10 +402,10 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
                         t += __ldcg(base + ((size_t)c * K + k) * kThreads);
                     out[(size_t)k * plane] = (k < klo || k > khi) ? one : (want_tau ? t : expf(-t));
                 }
-                if (tid == 0) tile_arrive[wu.tile] = 0u;
+                if (tid == 0) tile_arrive[tslot] = 0u;
             }
         }
-        __syncthreads();
+        cta_sync();
     }
 }
 

@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(256) k_unit_counts(const uint32_t* __restrict_
     const uint32_t len = te[t] - ts[t];
     uint32_t c = (len + chunk - 1) / chunk;
     if (c == 0) c = 1;
-    cnt[t] = (uint64_t)c | ((uint64_t)(c > 1 ? c : 0) << 32);
+    cnt[t] = (uint64_t)(c * kTileSplit) | ((uint64_t)(c > 1 ? c * kTileSplit : 0) << 32);
 }
 
 // Size class of a work unit for the longest-first dispatch order: 0 for an
@@ -125,7 +125,8 @@ __global__ void __launch_bounds__(256) k_units(const uint32_t* __restrict__ ts,
     const uint32_t s = ts[t], e = te[t];
     const uint64_t o = off[t];
     const uint32_t u0 = (uint32_t)(o & 0xffffffffu), slot = (uint32_t)(o >> 32);
-    const uint32_t nc = (uint32_t)((off[t + 1] & 0xffffffffu) - u0);
+    const uint32_t nc = (uint32_t)((off[t + 1] & 0xffffffffu) - u0) / kTileSplit;
+    for (uint32_t part = 0; part < (uint32_t)kTileSplit; ++part)
     for (uint32_t c = 0; c < nc; ++c) {
         WorkUnit w;
         w.tile = (uint32_t)t;
@@ -134,9 +135,10 @@ __global__ void __launch_bounds__(256) k_units(const uint32_t* __restrict__ ts,
         if (w.jbeg > e) w.jbeg = e;
         w.chunk = c;
         w.nchunks = nc;
-        w.slot = slot;
-        w.pad0 = w.pad1 = 0;
-        units[u0 + c] = w;
+        w.slot = slot + part * nc;
+        w.part = part;
+        w.pad1 = 0;
+        units[u0 + part * nc + c] = w;
         atomicAdd(&s_hist[unit_class(w.jend - w.jbeg)], 1u);
     }
     }

@@ -115,15 +115,15 @@ RunLayout run_layout(void* ws, const dgsm_plan_t& pl) {
     r.unit_cnt = c.take<uint64_t>(nt);
     r.unit_off = c.take<uint64_t>(nt + 1);
     r.unit_scan_temp = c.take<char>(scan_u32_to_u64_temp_bytes(nt));
-    const int64_t max_units = nt + P / pl.chunk + 1;
+    const int64_t max_units = kTileSplit * (nt + P / pl.chunk + 1);
     r.max_units = (uint32_t)max_units;
     r.units = c.take<WorkUnit>(max_units);
     r.units_tmp = c.take<WorkUnit>(max_units);
     r.counters = c.take<uint32_t>(96);
-    r.tile_arrive = c.take<uint32_t>(nt);
+    r.tile_arrive = c.take<uint32_t>(kTileSplit * nt);
     r.stats = c.take<unsigned long long>(8);
-    const int64_t max_slots = 2 * (P / pl.chunk) + 1;
-    r.scratch = c.take<float>((size_t)max_slots * pl.n_shells * kTexels);
+    const int64_t max_slots = kTileSplit * (2 * (P / pl.chunk) + 1);
+    r.scratch = c.take<float>((size_t)max_slots * pl.n_shells * (kTexels / kTileSplit));
     r.bytes = c.off;
     return r;
 }
@@ -351,7 +351,7 @@ int dgsm_build_run(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_
     cudaMemsetAsync(r.counters, 0, sizeof(uint32_t) * 96, s);
     launch_units(r.tile_start, r.tile_end, nt, plan->chunk, r.unit_cnt, r.unit_off, r.unit_scan_temp, r.units_tmp,
                  r.units, r.max_units, r.counters, r.counters + 32, r.counters + 64, s, &g_launches);
-    cudaMemsetAsync(r.tile_arrive, 0, sizeof(uint32_t) * nt, s);
+    cudaMemsetAsync(r.tile_arrive, 0, sizeof(uint32_t) * kTileSplit * nt, s);
     if (o.flags & DGSM_COLLECT_STATS) cudaMemsetAsync(r.stats, 0, sizeof(unsigned long long) * 8, s);
     // a6: accumulate + exp
     launch_accumulate(r.units, r.counters, r.max_units, r.vals_a, p.recs, g->n, lp, n_lights, res, K, o.flags,

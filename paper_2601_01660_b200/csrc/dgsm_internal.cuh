@@ -10,6 +10,7 @@ namespace dgsm {
 
 constexpr int kTile = 8;             // 8x8 atlas tiles
 constexpr int kTexels = kTile * kTile;
+constexpr int kTileSplit = 1;         // accumulation work units per (tile, chunk) (2 = one warp per half tile: measured slower)
 
 // Per-(light, Gaussian) footprint record written by the projection kernel and
 // gathered (by TMA bulk copy) into shared memory by the accumulation kernel.
@@ -50,7 +51,8 @@ struct __align__(16) WorkUnit {
     uint32_t chunk;     // chunk index within the tile
     uint32_t nchunks;   // chunks of this tile (1 = write T directly)
     uint32_t slot;      // scratch slot of chunk 0 (multi-chunk tiles only)
-    uint32_t pad0, pad1;
+    uint32_t part;      // which kTexels / kTileSplit texels of the tile (0 .. kTileSplit-1)
+    uint32_t pad1;
 };
 
 // Region decomposition of the clamped footprint square on the extended lattice
