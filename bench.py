@@ -88,6 +88,22 @@ def cfg_desc(s, cfg):
             "l2": "flushed before every step (256 MiB write)", "data": "synthetic, seeded (synth.py)"}
 
 
+def query_roofline(ms: float, m: int, L: int, peaks: dict):
+    """a8 against HBM: algorithmic bytes and the sector-realistic
+    count of a random-order gather (each row of taps is its own 32-B sector)."""
+    peak = float(peaks.get("hbm_gbs", 7700.0))
+    alg = m * (16 + 32 * L) * 1.0
+    sec = m * (16 + 128 * L) * 1.0
+    ach = alg / (ms * 1e-3) / 1e9
+    return {"kernel": "k_query (a8)", "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+            "frac": ach / peak, "alg_bytes_per_query": 16 + 32 * L,
+            "alg_def": "SURVEY §8(d): 12 B position + 4 B T + 8 x 4 B taps per light",
+            "sector_bytes_per_query": 16 + 128 * L,
+            "sector_frac": sec / (ms * 1e-3) / 1e9 / peak,
+            "peak_src": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md 7.7 TB/s",
+            "timing": "L2 flushed before each launch, CUDA events, host launch overhead excluded"}
+
+
 def cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -440,6 +456,7 @@ def run_dgsm(args):
                                     f"x {int(st['pairs'])} pairs",
                          "needed_ops_per_launch": int(needed_ops),
                          "needed_ops_frac": needed_ops / (acc_ms * 1e-3) / 1e12 / peak_tops},
+            "query_roofline": query_roofline(float(np.mean(tq)), m, s.L, peaks),
             "clocks": clocks,
         }
         if e2e:

@@ -27,8 +27,8 @@ __device__ __forceinline__ float sample_light(const float* __restrict__ A, const
     const double mz = pz - (double)L.z;
     const double t = sqrt((mx * mx + my * my) + mz * mz);
     if (t == 0.0) return 1.0f;
-    const double n1 = (fabs(mx) + fabs(my)) + fabs(mz);
-    const double qx = mx / n1, qy = my / n1, qz = mz / n1;
+    const double inv1 = 1.0 / ((fabs(mx) + fabs(my)) + fabs(mz));
+    const double qx = mx * inv1, qy = my * inv1, qz = mz * inv1;
     double u, v;
     if (qz >= 0.0) { u = qx; v = qy; }
     else {
@@ -47,6 +47,32 @@ __device__ __forceinline__ float sample_light(const float* __restrict__ A, const
     const float* A0 = A + (size_t)k0 * plane;
     const float* A1 = A + (size_t)k1 * plane;
     float acc = 0.0f;
+    const int ix = (int)x0, iy = (int)y0;
+    if (ix >= 0 && ix + 1 <= W - 1 && iy >= 0 && iy + 1 <= H - 1) {
+        // interior: both column taps of a row from one aligned 16-B load (one L1
+        // wavefront per row instead of two; the gather is L1-wavefront bound),
+        // a second load only when the pair straddles the 16-B boundary
+        const int c4 = ix & ~3, sub = ix & 3;
+        float v[2][2][2];  // [shell][row][col]
+#pragma unroll
+        for (int dk = 0; dk < 2; ++dk)
+#pragma unroll
+            for (int dy = 0; dy < 2; ++dy) {
+                const float* rp = (dk ? A1 : A0) + (size_t)(iy + dy) * W;
+                const float4 q = __ldg(reinterpret_cast<const float4*>(rp + c4));
+                v[dk][dy][0] = sub == 0 ? q.x : sub == 1 ? q.y : sub == 2 ? q.z : q.w;
+                v[dk][dy][1] = sub == 0 ? q.y : sub == 1 ? q.z : sub == 2 ? q.w : __ldg(rp + ix + 1);
+            }
+#pragma unroll
+        for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < 2; ++dx) {
+                const float wxy = (dx ? wx : 1.0f - wx) * (dy ? wy : 1.0f - wy);
+                acc = fmaf(wxy * (1.0f - wk), v[0][dy][dx], acc);
+                acc = fmaf(wxy * wk, v[1][dy][dx], acc);
+            }
+        return acc;
+    }
 #pragma unroll
     for (int dy = 0; dy < 2; ++dy)
 #pragma unroll
@@ -69,18 +95,37 @@ __device__ __forceinline__ void apply_colors(float* colors, int64_t q, float T) 
     }
 }
 
-__global__ void __launch_bounds__(256) k_query(const float* __restrict__ atlas, LightsParam lp,
+// kQPT receivers per thread: independent fp64 index chains and tap gathers in
+// flight together (the kernel is latency bound, not bandwidth bound).
+constexpr int kQPT = 1;
+
+__global__ void __launch_bounds__(256, 6) k_query(const float* __restrict__ atlas, LightsParam lp,
                                                int n_lights, int res, int K,
                                                const float* __restrict__ pos, int64_t m,
                                                float* __restrict__ T_out, float* __restrict__ colors) {
-    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= m) return;
-    const double px = __ldg(pos + 3 * q), py = __ldg(pos + 3 * q + 1), pz = __ldg(pos + 3 * q + 2);
+    const int64_t q0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kQPT;
+    if (q0 >= m) return;
     const size_t per_light = (size_t)K * res * res;
-    float T = 1.0f;
-    for (int l = 0; l < n_lights; ++l) T *= sample_light(atlas + l * per_light, lp.l[l], res, K, px, py, pz);
-    T_out[q] = T;
-    apply_colors(colors, q, T);
+    double px[kQPT], py[kQPT], pz[kQPT];
+    float T[kQPT];
+#pragma unroll
+    for (int j = 0; j < kQPT; ++j) {
+        const int64_t q = q0 + j < m ? q0 + j : m - 1;
+        px[j] = __ldg(pos + 3 * q); py[j] = __ldg(pos + 3 * q + 1); pz[j] = __ldg(pos + 3 * q + 2);
+        T[j] = 1.0f;
+    }
+    for (int l = 0; l < n_lights; ++l) {
+#pragma unroll
+        for (int j = 0; j < kQPT; ++j)
+            T[j] *= sample_light(atlas + l * per_light, lp.l[l], res, K, px[j], py[j], pz[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < kQPT; ++j) {
+        if (q0 + j < m) {
+            T_out[q0 + j] = T[j];
+            apply_colors(colors, q0 + j, T[j]);
+        }
+    }
 }
 
 // NEXT-2 ("sampling only at Gaussian centers ... rather than integrating
@@ -135,8 +180,9 @@ __global__ void __launch_bounds__(128) k_query_footprint(const float* __restrict
 void launch_query(const float* atlas, const LightsParam& lp, int n_lights, int res, int K,
                   const float* positions, int64_t m, float* T_out, float* colors, cudaStream_t s) {
     if (m <= 0) return;
-    k_query<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(atlas, lp, n_lights, res, K, positions, m, T_out,
-                                                        colors);
+    const int64_t threads = (m + kQPT - 1) / kQPT;
+    k_query<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(atlas, lp, n_lights, res, K, positions, m, T_out,
+                                                              colors);
 }
 
 void launch_query_footprint(const float* atlas, const LightsParam& lp, const FootprintParam& fp, int n_lights,
