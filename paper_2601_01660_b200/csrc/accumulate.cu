@@ -193,17 +193,82 @@ __device__ __forceinline__ PairTest pair_test(const Compact& c, float etx, float
     return p;
 }
 
+// ---- two records at once on the paired-FP32 pipe (sm_100 FFMA2/FADD2/FMUL2) --
+// A packed value holds record A (even) in the low half and record B (odd) in
+// the high half; one f32x2 instruction does both records' operation, halving
+// the issue slots of the pair test (the kernel is issue/latency bound).
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2add(f2_t a, f2_t b) { f2_t d; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ f2_t f2sub(f2_t a, f2_t b) { f2_t d; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ f2_t f2mul(f2_t a, f2_t b) { f2_t d; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ f2_t f2fma(f2_t a, f2_t b, f2_t c) {
+    f2_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f2_t f2pack(float lo, float hi) { f2_t r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi)); return r; }
+__device__ __forceinline__ float f2lo(f2_t r) { float lo, hi; asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r)); return lo; }
+__device__ __forceinline__ float f2hi(f2_t r) { float lo, hi; asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r)); return hi; }
+__device__ __forceinline__ void lds_f2x2(uint32_t a, f2_t& x, f2_t& y) {
+    asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(a) : "memory");
+}
+
+// Compact record pair: 20 packed fields (A, B), 160 B; field order
+//  0-2 f = fl32(d_i - d_c), 3 r_cut/D^2, 4-6 g = W d_i, 7 D, 8-16 W (row-major),
+//  17 e_D, 18 beta sqrt(pi/2), 19 k_D (int bits)
+constexpr int kPairFields = 20;
+constexpr int kPairBytes = kPairFields * 8;
+
+struct PairTest2 {
+    PairTest A, B;
+    float DA, DB, eDA, eDB, bpA, bpB;
+    int kDA, kDB;
+};
+
+__device__ __forceinline__ PairTest2 pair_test2(uint32_t addr, f2_t ETX, f2_t ETY, f2_t ETZ) {
+    f2_t F[kPairFields];
+#pragma unroll
+    for (int j = 0; j < kPairFields / 2; ++j) lds_f2x2(addr + 16 * j, F[2 * j], F[2 * j + 1]);
+    const f2_t EX = f2sub(ETX, F[0]), EY = f2sub(ETY, F[1]), EZ = f2sub(ETZ, F[2]);
+    const f2_t WX = f2fma(F[8], EX, f2fma(F[9], EY, f2mul(F[10], EZ)));
+    const f2_t WY = f2fma(F[11], EX, f2fma(F[12], EY, f2mul(F[13], EZ)));
+    const f2_t WZ = f2fma(F[14], EX, f2fma(F[15], EY, f2mul(F[16], EZ)));
+    const f2_t UX = f2add(F[4], WX), UY = f2add(F[5], WY), UZ = f2add(F[6], WZ);
+    const f2_t A = f2fma(UX, UX, f2fma(UY, UY, f2mul(UZ, UZ)));
+    const f2_t Z = 0ull;
+    const f2_t NGX = f2sub(Z, F[4]), NGY = f2sub(Z, F[5]), NGZ = f2sub(Z, F[6]);
+    const f2_t CX = f2fma(F[5], WZ, f2mul(NGZ, WY));  // gy wz - gz wy
+    const f2_t CY = f2fma(F[6], WX, f2mul(NGX, WZ));  // gz wx - gx wz
+    const f2_t CZ = f2fma(F[4], WY, f2mul(NGY, WX));  // gx wy - gy wx
+    const f2_t C2 = f2fma(CX, CX, f2fma(CY, CY, f2mul(CZ, CZ)));
+    const f2_t T = f2mul(F[3], A);  // live  <=>  |g x W delta|^2 <= (r_cut/D^2) a
+    PairTest2 R;
+    R.A.wx = f2lo(WX); R.A.wy = f2lo(WY); R.A.wz = f2lo(WZ);
+    R.A.ux = f2lo(UX); R.A.uy = f2lo(UY); R.A.uz = f2lo(UZ);
+    R.A.a = f2lo(A); R.A.ia = f2lo(C2);  // ia holds |c|^2 until the live path
+    R.A.live = f2lo(C2) <= f2lo(T);
+    R.B.wx = f2hi(WX); R.B.wy = f2hi(WY); R.B.wz = f2hi(WZ);
+    R.B.ux = f2hi(UX); R.B.uy = f2hi(UY); R.B.uz = f2hi(UZ);
+    R.B.a = f2hi(A); R.B.ia = f2hi(C2);
+    R.B.live = f2hi(C2) <= f2hi(T);
+    R.DA = f2lo(F[7]); R.DB = f2hi(F[7]);
+    R.eDA = f2lo(F[17]); R.eDB = f2hi(F[17]);
+    R.bpA = f2lo(F[18]); R.bpB = f2hi(F[18]);
+    R.kDA = __float_as_int(f2lo(F[19])); R.kDB = __float_as_int(f2hi(F[19]));
+    return R;
+}
+
 // Eq.3 over the shells for a live pair: window shells (|x_k| < kXS) as differences,
 // then the saturated step pref (1 - erf(x_0)) at the first saturated shell.
 template <bool kStats>
-__device__ __forceinline__ void pair_live(const PairTest& p, const Compact& c, float* s_acc, int tid, int K,
-                                          float dt, float dtlo, float idt, uint32_t& st_live,
+__device__ __forceinline__ void pair_live(const PairTest& p, float D, float eD, float betap, int kD, float* s_acc,
+                                          int tid, int K, float dt, float dtlo, float idt, uint32_t& st_live,
                                           uint32_t& st_win, uint32_t& st_step) {
-    const float4 q1 = c.q1, q4 = c.q4;
-    const float D = q1.w;
-    const float rr = p.r_over_D2 * D * D;
+    const float ia = rcp_approx(p.a);
+    const float r_over_D2 = p.ia * ia;  // p.ia carries |g x W delta|^2 from the test
+    const float rr = r_over_D2 * D * D;
     // s* - D = -D (u . W delta)/a: closest approach relative to D
-    const float sD = -D * fmaf(p.ux, p.wx, fmaf(p.uy, p.wy, p.uz * p.wz)) * p.ia;
+    const float sD = -D * fmaf(p.ux, p.wx, fmaf(p.uy, p.wy, p.uz * p.wz)) * ia;
     const float ra = rsqrt_approx(p.a);
     const float h = 0.70710678118654752f * p.a * ra;  // sqrt(a/2)
     const float x0 = -h * (D + sD);                      // sqrt(a/2) * (b/a) of Eq.3
@@ -211,10 +276,9 @@ __device__ __forceinline__ void pair_live(const PairTest& p, const Compact& c, f
     if (e0 >= 1.0f) return;  // whole Gaussian behind the light
     if (kStats) ++st_live;
     // Eq.3 prefactor beta sqrt(pi/(2a)) exp(-(c - b^2/a)/2)
-    const float pref = q4.z * ra * ex2_approx(-0.72134752044448170f * rr);
+    const float pref = betap * ra * ex2_approx(-0.72134752044448170f * rr);
     // t_k - s* = (k - kD) dt + e ; window |x_k| < kXS <=> |t_k - s*| < kXS / h
-    const int kD = __float_as_int(q4.w);
-    const float e = q4.y - sD;
+    const float e = eD - sD;
     const float xsh = (kXS * 1.41421356237309505f) * ra;  // kXS / h
     const float kf_lo = fmaf(-xsh - e, idt, (float)kD);   // x_k <= -kXS for k <= kf_lo
     const float kf_hi = fmaf(xsh - e, idt, (float)kD);    // x_k >= +kXS for k >= kf_hi
@@ -282,6 +346,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
         texel_dir(row0 + 4, col0 + 4, W, H, c0, c1, c2);
         texel_dir(row, col, W, H, t0, t1, t2);
         const float etx = (float)(t0 - c0), ety = (float)(t1 - c1), etz = (float)(t2 - c2);
+        const f2_t ETX = f2pack(etx, etx), ETY = f2pack(ety, ety), ETZ = f2pack(etz, etz);
         for (int k = 0; k < K; ++k) s_acc[k * kThreads + tid] = 0.0f;
         uint32_t st_live = 0, st_win = 0, st_step = 0, st_wany = 0, st_wmax = 0;
 
@@ -307,7 +372,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
             const uint32_t nb = min((uint32_t)kStage, n_rec - b * kStage);
             if ((uint32_t)tid < nb) {  // transform: raw record -> compact, relative to d_c
                 const PairRec& R = s_raw[tid];
-                float4* q = s_cr + tid * kCompact;
+                float* q = reinterpret_cast<float*>(s_cr) + (tid >> 1) * (2 * kPairFields) + (tid & 1);
                 // negligible-pair cut (R8'): a pair contributes at most
                 // 2 pref <= 2 betap s_max exp(-r/2) to any tau_k (1/sqrt(a) <= s_max);
                 // skip it when that bound is < 2^-32, i.e. r > r_cut; never above 180
@@ -317,12 +382,12 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
                 const float w2 = R.W[6] * R.W[6] + R.W[7] * R.W[7] + R.W[8] * R.W[8];
                 const float smax = rsqrtf(fminf(w0, fminf(w1, w2)));
                 const float rcut = fminf(2.0f * logf(2.0f * R.betap * smax) + 44.3614195558365f, kRCut);
-                q[0] = make_float4((float)(R.di[0] - c0), (float)(R.di[1] - c1), (float)(R.di[2] - c2),
-                                   rcut / (R.D * R.D));
-                q[1] = make_float4(R.g[0], R.g[1], R.g[2], R.D);
-                q[2] = make_float4(R.W[0], R.W[1], R.W[2], R.W[3]);
-                q[3] = make_float4(R.W[4], R.W[5], R.W[6], R.W[7]);
-                q[4] = make_float4(R.W[8], R.eD, R.betap, __int_as_float(R.kD));
+                float v[kPairFields] = {(float)(R.di[0] - c0), (float)(R.di[1] - c1), (float)(R.di[2] - c2),
+                                        rcut / (R.D * R.D), R.g[0], R.g[1], R.g[2], R.D,
+                                        R.W[0], R.W[1], R.W[2], R.W[3], R.W[4], R.W[5], R.W[6], R.W[7], R.W[8],
+                                        R.eD, R.betap, __int_as_float(R.kD)};
+#pragma unroll
+                for (int f = 0; f < kPairFields; ++f) q[2 * f] = v[f];
             }
             cta_sync();  // compact copy ready; raw buffer free
             if (b + 1 < n_batches) {
@@ -331,21 +396,17 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
             }
             // two records per iteration: independent dependency chains for the pair test
             uint32_t my_live = 0;
-            uint32_t ra_addr = smem_addr(s_cr);  // induction variable: record r's compact form
-            for (uint32_t r = 0; r < nb; r += 2, ra_addr += 2 * kCompact * 16) {
-                const uint32_t rb_addr = r + 1 < nb ? ra_addr + kCompact * 16 : ra_addr;
-                const Compact ca = load_compact(ra_addr);
-                const Compact cb = load_compact(rb_addr);
-                PairTest A = pair_test(ca, etx, ety, etz);
-                PairTest B = pair_test(cb, etx, ety, etz);
-                B.live = B.live && (r + 1 < nb);
+            uint32_t pr_addr = smem_addr(s_cr);  // induction variable: record pair (r, r+1)
+            for (uint32_t r = 0; r < nb; r += 2, pr_addr += kPairBytes) {
+                PairTest2 T2 = pair_test2(pr_addr, ETX, ETY, ETZ);
+                T2.B.live = T2.B.live && (r + 1 < nb);
                 if (kStats) {
-                    const uint32_t ba = __ballot_sync(0xffffffffu, A.live), bb = __ballot_sync(0xffffffffu, B.live);
-                    my_live += (uint32_t)A.live + (uint32_t)B.live;
+                    const uint32_t ba = __ballot_sync(0xffffffffu, T2.A.live), bb = __ballot_sync(0xffffffffu, T2.B.live);
+                    my_live += (uint32_t)T2.A.live + (uint32_t)T2.B.live;
                     st_wany += (ba != 0u) + (bb != 0u);
                 }
-                if (A.live) pair_live<kStats>(A, ca, s_acc, tid, K, dt, dtlo, idt, st_live, st_win, st_step);
-                if (B.live) pair_live<kStats>(B, cb, s_acc, tid, K, dt, dtlo, idt, st_live, st_win, st_step);
+                if (T2.A.live) pair_live<kStats>(T2.A, T2.DA, T2.eDA, T2.bpA, T2.kDA, s_acc, tid, K, dt, dtlo, idt, st_live, st_win, st_step);
+                if (T2.B.live) pair_live<kStats>(T2.B, T2.DB, T2.eDB, T2.bpB, T2.kDB, s_acc, tid, K, dt, dtlo, idt, st_live, st_win, st_step);
             }
             if (kStats) st_wmax += __reduce_max_sync(0xffffffffu, my_live);
             cta_sync();  // compact copy consumed
