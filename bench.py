@@ -386,16 +386,29 @@ def run_dgsm(args):
     e2e = None
     if not args.no_e2e:
         T_host = torch.empty(m, dtype=torch.float32).pin_memory()
+        # one rank per frame (no collective in the step): the library's host-buffer
+        # entry point dgsm_frame_host (chunked upload overlapped with projection,
+        # receivers uploaded under the build, T copied back); otherwise torch copies
+        # around the collective step
+        use_frame = gsz == 1 and (not strong or world == 1)
+        if use_frame:
+            fr = dgsm.FrameHost(lights_b, s.res, s.K)
+            for _ in range(2):
+                fr(g_host, q_host, T_host)
+            torch.cuda.synchronize()
         te = []
         for i in range(K):
             flush.zero_()
             a, b = ev[i][0], ev[i][4]
             a.record()
-            for k_, v_ in g_host.items():          # this step's inputs, host -> device
-                g[k_].copy_(v_, non_blocking=True)
-            xq.copy_(q_host, non_blocking=True)
-            step()
-            T_host.copy_(T_out, non_blocking=True)  # the step's result, device -> host
+            if use_frame:
+                fr(g_host, q_host, T_host)
+            else:
+                for k_, v_ in g_host.items():          # this step's inputs, host -> device
+                    g[k_].copy_(v_, non_blocking=True)
+                xq.copy_(q_host, non_blocking=True)
+                step()
+                T_host.copy_(T_out, non_blocking=True)  # the step's result, device -> host
             b.record()
             te.append((a, b))
         torch.cuda.synchronize()
@@ -406,7 +419,8 @@ def run_dgsm(args):
             te_ms = float(t[0])
         h2d = sum(v.numel() * 4 for v in g_host.values()) + q_host.numel() * 4
         e2e = {"value": units_all * K / (te_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(m * 4), "ms_per_step": te_ms / K}
+               "d2h_bytes_per_step": int(m * 4), "ms_per_step": te_ms / K,
+               "api": "dgsm_frame_host (host buffers)" if use_frame else "torch copies + dgsm_build_plan/run/query"}
 
     if rank == 0:
         peaks = {}

@@ -194,6 +194,25 @@ int dgsm_query(const float* atlas, const dgsm_light_t* lights, int n_lights, int
                int n_shells, const float* positions, int64_t m, float* T_out, float* colors_inout,
                void* stream);
 
+/* One frame end to end from HOST memory (the benchmark's e2e path): upload the
+ * occluder Gaussians (g_host: HOST arrays, pinned for copy/compute overlap) in
+ * chunks, each projected as soon as it lands; build the atlas (plan + run, as
+ * dgsm_build) into atlas_out (DEVICE, [L][K][H][W]); upload the receivers
+ * (receivers_host, HOST float [m][3]) on a side stream while the atlas is
+ * built; query them (dgsm_query) and copy T (HOST float [m]) back.  Stream-
+ * ordered on `stream`: T_host is valid once `stream` has completed.
+ *   ws, ws_bytes  caller-owned DEVICE workspace (256-B aligned).  *ws_required
+ *                 receives the bytes needed: the plan part is known up front,
+ *                 the run part after the plan — a call that returns
+ *                 DGSM_ENOSPC has done no device work beyond the plan; grow the
+ *                 workspace to *ws_required and call again.
+ * Errors: as dgsm_build_plan / dgsm_build_run / dgsm_query; DGSM_EINVAL for null
+ * host arrays, DGSM_ENOSPC as above.  One host synchronisation (the plan). */
+int dgsm_frame_host(const dgsm_gaussians_t* g_host, const dgsm_light_t* lights, int n_lights, int atlas_res,
+                    int n_shells, const dgsm_build_opts_t* opts, const float* receivers_host, int64_t m,
+                    float* T_host, void* ws, size_t ws_bytes, size_t* ws_required, float* atlas_out,
+                    void* stream);
+
 /* Footprint-sampled query ("rather than
  * integrating over each receiver's footprint", "sampling only the
  * Gaussian center ... tends to underestimate soft shadowing").  For receiver

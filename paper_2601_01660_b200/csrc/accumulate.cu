@@ -133,65 +133,18 @@ struct AccLights {
     float idt[DGSM_MAX_LIGHTS];    // 1 / dt
 };
 
-// Compact per-(record, work unit) form, 5 x float4 (80 B):
-//  q0 = (f0, f1, f2, r_cut / D^2)   f = fl32(d_i - d_c), d_c = tile reference direction
-//  q1 = (g0, g1, g2, D)
-//  q2 = (W0, W1, W2, W3), q3 = (W4, W5, W6, W7)
-//  q4 = (W8, eD, betap, kD as int bits)
-constexpr int kCompact = 5;
-
-// Shared-memory float4 load by 32-bit shared address (keeps the per-record
-// address arithmetic to one integer add; see DESIGN.md a6 notes).
-__device__ __forceinline__ float4 lds4(uint32_t a) {
-    float4 v;
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "r"(a)
-                 : "memory");
-    return v;
-}
-
-struct Compact {
-    float4 q0, q1, q2, q3, q4;
-};
-__device__ __forceinline__ Compact load_compact(uint32_t a) {
-    Compact c;
-    c.q0 = lds4(a);
-    c.q1 = lds4(a + 16);
-    c.q2 = lds4(a + 32);
-    c.q3 = lds4(a + 48);
-    c.q4 = lds4(a + 64);
-    return c;
-}
+// Compact per-(record, work unit) form: 20 fp32 fields (80 B) relative to the
+// tile reference direction d_c, stored interleaved by record pairs (below).
+constexpr int kCompact = 5;  // float4 per record
 
 // ---- per (texel, Gaussian) pair ---------------------------------------------
+// delta-formulation (R9) of one (texel, record) pair up to the negligible-pair
+// test (R8'): W delta, u = g + W delta, a = |u|^2, and |g x W delta|^2 (in `ia`
+// until the live path turns it into r/D^2 = |g x W delta|^2 / a).
 struct PairTest {
-    float wx, wy, wz, ux, uy, uz, a, ia, r_over_D2;
+    float wx, wy, wz, ux, uy, uz, a, ia;
     bool live;
 };
-
-// delta-formulation (R9) up to the negligible-pair test (R8'): r/D^2 = |g x W delta|^2 / a.
-__device__ __forceinline__ PairTest pair_test(const Compact& c, float etx, float ety, float etz) {
-    const float4 q0 = c.q0, q1 = c.q1, q2 = c.q2, q3 = c.q3, q4 = c.q4;
-    PairTest p;
-    // delta = d - d_i = e_t - f  (both small, fp32-exact to ~1e-7 relative)
-    const float ex = etx - q0.x, ey = ety - q0.y, ez = etz - q0.z;
-    // W delta, u = W d = g + W delta, a = |u|^2 = d^T A d (Eq.2)
-    p.wx = fmaf(q2.x, ex, fmaf(q2.y, ey, q2.z * ez));
-    p.wy = fmaf(q2.w, ex, fmaf(q3.x, ey, q3.y * ez));
-    p.wz = fmaf(q3.z, ex, fmaf(q3.w, ey, q4.x * ez));
-    const float gx = q1.x, gy = q1.y, gz = q1.z;
-    p.ux = gx + p.wx; p.uy = gy + p.wy; p.uz = gz + p.wz;
-    p.a = fmaf(p.ux, p.ux, fmaf(p.uy, p.uy, p.uz * p.uz));
-    // r = c - b^2/a = D^2 |g x W delta|^2 / a  (Lagrange identity)
-    const float cx = fmaf(gy, p.wz, -gz * p.wy);
-    const float cy = fmaf(gz, p.wx, -gx * p.wz);
-    const float cz = fmaf(gx, p.wy, -gy * p.wx);
-    p.ia = rcp_approx(p.a);
-    p.r_over_D2 = fmaf(cx, cx, fmaf(cy, cy, cz * cz)) * p.ia;
-    p.live = p.r_over_D2 <= q0.w;  // negligible pair (R8'): r > r_cut
-    return p;
-}
 
 // ---- two records at once on the paired-FP32 pipe (sm_100 FFMA2/FADD2/FMUL2) --
 // A packed value holds record A (even) in the low half and record B (odd) in
@@ -207,8 +160,8 @@ __device__ __forceinline__ f2_t f2fma(f2_t a, f2_t b, f2_t c) {
     return d;
 }
 __device__ __forceinline__ f2_t f2pack(float lo, float hi) { f2_t r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi)); return r; }
-__device__ __forceinline__ float f2lo(f2_t r) { float lo, hi; asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r)); return lo; }
-__device__ __forceinline__ float f2hi(f2_t r) { float lo, hi; asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r)); return hi; }
+__device__ __forceinline__ float f2lo(f2_t r) { float lo; asm("mov.b64 {%0, _}, %1;" : "=f"(lo) : "l"(r)); return lo; }
+__device__ __forceinline__ float f2hi(f2_t r) { float hi; asm("mov.b64 {_, %0}, %1;" : "=f"(hi) : "l"(r)); return hi; }
 __device__ __forceinline__ void lds_f2x2(uint32_t a, f2_t& x, f2_t& y) {
     asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(a) : "memory");
 }

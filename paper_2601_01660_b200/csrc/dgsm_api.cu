@@ -1,5 +1,6 @@
 // dgsm_api.cu — the C ABI of include/dgsm.h: argument validation, workspace
 // layout (caller-owned memory only), stream-ordered launches, error strings.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -225,9 +226,25 @@ size_t dgsm_plan_workspace_bytes(int64_t n, int n_lights) {
     return plan_layout(nullptr, n, n_lights).bytes;
 }
 
+// The plan; with g_host != NULL the Gaussian arrays are first uploaded from
+// host memory into the device arrays of g in n_chunks pieces, each projected
+// as soon as it has landed (copy engine and SMs overlap).
+static int plan_impl(const dgsm_gaussians_t* g, const dgsm_gaussians_t* g_host, int n_chunks,
+                     const dgsm_light_t* lights, int n_lights, int atlas_res, int n_shells,
+                     const dgsm_build_opts_t* opts, void* plan_ws, size_t plan_ws_bytes, dgsm_plan_t* plan,
+                     void* stream);
+
 int dgsm_build_plan(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_lights, int atlas_res,
                     int n_shells, const dgsm_build_opts_t* opts, void* plan_ws, size_t plan_ws_bytes,
                     dgsm_plan_t* plan, void* stream) {
+    return plan_impl(g, nullptr, 1, lights, n_lights, atlas_res, n_shells, opts, plan_ws, plan_ws_bytes, plan,
+                     stream);
+}
+
+static int plan_impl(const dgsm_gaussians_t* g, const dgsm_gaussians_t* g_host, int n_chunks,
+                     const dgsm_light_t* lights, int n_lights, int atlas_res, int n_shells,
+                     const dgsm_build_opts_t* opts, void* plan_ws, size_t plan_ws_bytes, dgsm_plan_t* plan,
+                     void* stream) {
     g_launches = 0;
     dgsm_build_opts_t o;
     if (opts) o = *opts; else dgsm_default_opts(&o);
@@ -242,10 +259,26 @@ int dgsm_build_plan(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n
     const LightsParam lp = lights_param(lights, n_lights);
     const int64_t m = (int64_t)n_lights * g->n;
 
-    launch_project(*g, lp, n_lights, atlas_res, n_shells, o, p.recs, p.counts, p.dup, p.stats, s);
+    launch_project_init(p.stats, s);
+    if (g_host && g->n > 0) {
+        const int64_t n = g->n, per = (n + n_chunks - 1) / n_chunks;
+        for (int64_t i0 = 0; i0 < n; i0 += per) {
+            const int64_t cnt = std::min<int64_t>(per, n - i0);
+            cudaMemcpyAsync((float*)g->means + 3 * i0, g_host->means + 3 * i0, 12 * cnt, cudaMemcpyHostToDevice, s);
+            cudaMemcpyAsync((float*)g->scales + 3 * i0, g_host->scales + 3 * i0, 12 * cnt, cudaMemcpyHostToDevice, s);
+            cudaMemcpyAsync((float*)g->rotations + 4 * i0, g_host->rotations + 4 * i0, 16 * cnt,
+                            cudaMemcpyHostToDevice, s);
+            cudaMemcpyAsync((float*)g->opacities + i0, g_host->opacities + i0, 4 * cnt, cudaMemcpyHostToDevice, s);
+            launch_project(*g, lp, n_lights, atlas_res, n_shells, o, i0, cnt, p.recs, p.counts, p.dup, p.stats, s);
+            g_launches += 1;
+        }
+    } else {
+        launch_project(*g, lp, n_lights, atlas_res, n_shells, o, 0, g->n, p.recs, p.counts, p.dup, p.stats, s);
+        g_launches += 1;
+    }
     launch_scan_u32_to_u64(p.counts, p.offsets, m, p.scan_temp, s);
     launch_plan_stats(p.offsets, g->n, n_lights, p.stats, s);
-    g_launches += 6;
+    g_launches += 5;
     if ((rc = cuda_check("plan launch"))) return rc;
     PlanStats hs;
     cudaMemcpyAsync(&hs, p.stats, sizeof(PlanStats), cudaMemcpyDeviceToHost, s);
@@ -403,6 +436,73 @@ int dgsm_build(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_ligh
     if (ws_bytes < need) return fail(DGSM_ENOSPC, "workspace %zu < %zu bytes", ws_bytes, need);
     return dgsm_build_run(g, lights, n_lights, opts, &plan, ws, pb, (char*)ws + pb, ws_bytes - pb, atlas_out,
                           stream);
+}
+
+// Upload pipeline depth of dgsm_frame_host (chunks of the Gaussian arrays).
+constexpr int kUploadChunks = 4;
+
+int dgsm_frame_host(const dgsm_gaussians_t* g_host, const dgsm_light_t* lights, int n_lights, int atlas_res,
+                    int n_shells, const dgsm_build_opts_t* opts, const float* receivers_host, int64_t m,
+                    float* T_host, void* ws, size_t ws_bytes, size_t* ws_required, float* atlas_out,
+                    void* stream) {
+    if (!g_host) return fail(DGSM_EINVAL, "null gaussians");
+    const int64_t n = g_host->n;
+    if (n < 0 || m < 0) return fail(DGSM_EINVAL, "n < 0 or m < 0");
+    if (n > 0 && (!g_host->means || !g_host->scales || !g_host->rotations || !g_host->opacities))
+        return fail(DGSM_EINVAL, "null host Gaussian array");
+    if (m > 0 && (!receivers_host || !T_host)) return fail(DGSM_EINVAL, "null receivers or T");
+    if (!atlas_out) return fail(DGSM_EINVAL, "null atlas");
+    if (n_lights < 1 || n_lights > DGSM_MAX_LIGHTS) return fail(DGSM_EINVAL, "n_lights %d outside [1, %d]", n_lights, DGSM_MAX_LIGHTS);
+    if ((uintptr_t)ws % kAlign) return fail(DGSM_EINVAL, "workspace not 256-B aligned");
+    Carver c(ws);
+    dgsm_gaussians_t gd;
+    gd.means = c.take<float>(3 * n);
+    gd.scales = c.take<float>(3 * n);
+    gd.rotations = c.take<float>(4 * n);
+    gd.opacities = c.take<float>(n);
+    gd.n = n;
+    float* rec = c.take<float>(3 * m);
+    float* Td = c.take<float>(m);
+    const size_t fixed = c.off;
+    const size_t pb = dgsm_plan_workspace_bytes(n, n_lights);
+    if (ws_required) *ws_required = fixed + pb;
+    if (!ws || ws_bytes < fixed + pb) return fail(DGSM_ENOSPC, "workspace %zu < %zu bytes (plan part)", ws_bytes, fixed + pb);
+    void* plan_ws = (char*)ws + fixed;
+    dgsm_plan_t plan;
+    int rc = plan_impl(&gd, g_host, kUploadChunks, lights, n_lights, atlas_res, n_shells, opts, plan_ws, pb, &plan,
+                       stream);
+    if (rc) return rc;
+    int launches = g_launches;
+    const size_t need = fixed + pb + plan.run_workspace_bytes;
+    if (ws_required) *ws_required = need;
+    if (ws_bytes < need) return fail(DGSM_ENOSPC, "workspace %zu < %zu bytes", ws_bytes, need);
+    cudaStream_t s = (cudaStream_t)stream;
+    // receivers ride the copy engine on a side stream while the atlas is built
+    thread_local cudaStream_t aux = nullptr;
+    thread_local cudaEvent_t ev_rec = nullptr;
+    thread_local int aux_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!aux || aux_dev != dev) {
+        cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&ev_rec, cudaEventDisableTiming);
+        aux_dev = dev;
+    }
+    cudaEventRecord(ev_rec, s);  // after the plan's uploads (the aux stream must not race them on PCIe)
+    cudaStreamWaitEvent(aux, ev_rec, 0);
+    if (m > 0) cudaMemcpyAsync(rec, receivers_host, 12 * (size_t)m, cudaMemcpyHostToDevice, aux);
+    cudaEventRecord(ev_rec, aux);
+    rc = dgsm_build_run(&gd, lights, n_lights, opts, &plan, plan_ws, pb, (char*)plan_ws + pb,
+                        ws_bytes - fixed - pb, atlas_out, stream);
+    if (rc) return rc;
+    launches += g_launches;
+    cudaStreamWaitEvent(s, ev_rec, 0);
+    rc = dgsm_query(atlas_out, lights, n_lights, atlas_res, n_shells, rec, m, Td, nullptr, stream);
+    if (rc) return rc;
+    launches += g_launches;
+    if (m > 0) cudaMemcpyAsync(T_host, Td, 4 * (size_t)m, cudaMemcpyDeviceToHost, s);
+    g_launches = launches;
+    return cuda_check("frame");
 }
 
 int dgsm_exp_epilogue(const float* tau, float* T, int64_t count, void* stream) {

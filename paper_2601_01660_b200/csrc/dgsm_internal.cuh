@@ -165,9 +165,11 @@ __device__ inline uint32_t count_active_tiles(int c0, int c1, int r0, int r1, in
 // ---------------------------------------------------------------- kernels
 // (declared here, defined in the .cu files, launched from dgsm_api.cu)
 namespace dgsm {
+void launch_project_init(PlanStats* stats, cudaStream_t s);
+// Gaussians [i0, i0 + cnt) of every light (after launch_project_init)
 void launch_project(const dgsm_gaussians_t& g, const LightsParam& lp, int n_lights, int res, int K,
-                    const dgsm_build_opts_t& o, PairRec* recs, uint32_t* counts, uint4* dup,
-                    PlanStats* stats, cudaStream_t s);
+                    const dgsm_build_opts_t& o, int64_t i0, int64_t cnt, PairRec* recs, uint32_t* counts,
+                    uint4* dup, PlanStats* stats, cudaStream_t s);
 size_t scan_u32_to_u64_temp_bytes(int64_t n);
 void launch_scan_u32_to_u64(const uint32_t* in, uint64_t* out, int64_t n, void* temp, cudaStream_t s);
 void launch_scan_u64(const uint64_t* in, uint64_t* out, int64_t n, void* temp, cudaStream_t s);

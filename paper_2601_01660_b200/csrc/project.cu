@@ -16,7 +16,7 @@ __device__ __forceinline__ double sgn_pos(double x) { return x >= 0.0 ? 1.0 : -1
 
 __global__ void __launch_bounds__(256, 3) k_project(
     const float* __restrict__ means, const float* __restrict__ scales,
-    const float* __restrict__ rotations, const float* __restrict__ opacities, int64_t n,
+    const float* __restrict__ rotations, const float* __restrict__ opacities, int64_t n, int64_t i0, int64_t cnt,
     LightsParam lp, int n_lights, int res, int K, double kappa, double k_sigma, double rho,
     int bin_mode, int absorption, bool no_cull, const uint64_t* __restrict__ slab_mask,
     PairRec* __restrict__ recs, uint32_t* __restrict__ counts,
@@ -25,11 +25,13 @@ __global__ void __launch_bounds__(256, 3) k_project(
     __shared__ uint32_t s_dmin[DGSM_MAX_LIGHTS], s_dmax[DGSM_MAX_LIGHTS];
     if (threadIdx.x < DGSM_MAX_LIGHTS) { s_dmin[threadIdx.x] = 0xffffffffu; s_dmax[threadIdx.x] = 0u; }
     __syncthreads();
+    // Gaussians [i0, i0 + cnt) of every light (a chunk of an upload pipeline, or all)
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool active = idx < (int64_t)n_lights * n;
-    if (!active) idx = (int64_t)n_lights * n - 1;  // recompute the last element; results not stored twice
-    const int l = (int)(idx / n);
-    const int64_t i = idx - (int64_t)l * n;
+    const bool active = idx < (int64_t)n_lights * cnt;
+    if (!active) idx = (int64_t)n_lights * cnt - 1;  // recompute the last element; results not stored twice
+    const int l = (int)(idx / cnt);
+    const int64_t i = i0 + (idx - (int64_t)l * cnt);
+    const int64_t oi = (int64_t)l * n + i;  // output slot [l][i]
     uint32_t dbits = 0u;
     const float4 L = lp.l[l];
     const int W = res, H = res;
@@ -39,7 +41,7 @@ __global__ void __launch_bounds__(256, 3) k_project(
     const double my = (double)means[3 * i + 1] - (double)L.y;
     const double mz = (double)means[3 * i + 2] - (double)L.z;
     const double D = sqrt((mx * mx + my * my) + mz * mz);
-    uint32_t cnt = 0;
+    uint32_t tcnt = 0;
     PairRec rec;
     rec.c0 = 1; rec.c1 = 0; rec.r0 = 1; rec.r1 = 0;
     if (D > 1e-6) {
@@ -98,19 +100,19 @@ __global__ void __launch_bounds__(256, 3) k_project(
         }
         const int ic0 = (int)c0, ic1 = (int)c1, ir0 = (int)r0, ir1 = (int)r1;
         if (ic0 > ic1 || ir0 > ir1) {
-            cnt = 0;
+            tcnt = 0;
         } else if (slab_mask) {  // NEXT-1: only the tiles holding a texel of the ROI pixel set
-            cnt = count_active_tiles(ic0, ic1, ir0, ir1, res, bin_mode,
+            tcnt = count_active_tiles(ic0, ic1, ir0, ir1, res, bin_mode,
                                      slab_mask + (int64_t)l * (res / kTile) * (res / kTile));
         } else if (ic0 >= 0 && ic1 <= W - 1 && ir0 >= 0 && ir1 <= H - 1) {  // common case: inside the grid
-            cnt = (uint32_t)((ic1 >> 3) - (ic0 >> 3) + 1) * (uint32_t)((ir1 >> 3) - (ir0 >> 3) + 1);
+            tcnt = (uint32_t)((ic1 >> 3) - (ic0 >> 3) + 1) * (uint32_t)((ir1 >> 3) - (ir0 >> 3) + 1);
         } else {
             TileRects TR;
             make_tile_rects(ic0, ic1, ir0, ir1, res, bin_mode, TR);
-            cnt = count_tiles(TR);
+            tcnt = count_tiles(TR);
         }
 
-        if (cnt > 0) {
+        if (tcnt > 0) {
             rec.c0 = (int16_t)c0; rec.c1 = (int16_t)c1; rec.r0 = (int16_t)r0; rec.r1 = (int16_t)r1;
             rec.di[0] = dx; rec.di[1] = dy; rec.di[2] = dz;
             // record fields (not part of the binning contract): reciprocal multiplies
@@ -145,14 +147,14 @@ __global__ void __launch_bounds__(256, 3) k_project(
         }
     }
     if (active) {
-        counts[idx] = cnt;
-        recs[idx] = rec;
-        dup[idx] = make_uint4(dbits, (uint32_t)(uint16_t)rec.c0 | ((uint32_t)(uint16_t)rec.c1 << 16),
-                              (uint32_t)(uint16_t)rec.r0 | ((uint32_t)(uint16_t)rec.r1 << 16), cnt);
+        counts[oi] = tcnt;
+        recs[oi] = rec;
+        dup[oi] = make_uint4(dbits, (uint32_t)(uint16_t)rec.c0 | ((uint32_t)(uint16_t)rec.c1 << 16),
+                              (uint32_t)(uint16_t)rec.r0 | ((uint32_t)(uint16_t)rec.r1 << 16), tcnt);
     }
     // per-light min/max of the depth key over binned Gaussians: shared-memory
     // atomics per block, one global atomic per (block, light)
-    if (cnt > 0) {
+    if (tcnt > 0) {
         atomicMin(&s_dmin[l], dbits);
         atomicMax(&s_dmax[l], dbits);
     }
@@ -169,15 +171,18 @@ __global__ void k_init_stats(PlanStats* stats) {
 }
 }  // namespace
 
-void launch_project(const dgsm_gaussians_t& g, const LightsParam& lp, int n_lights, int res, int K,
-                    const dgsm_build_opts_t& o, PairRec* recs, uint32_t* counts, uint4* dup,
-                    PlanStats* stats, cudaStream_t s) {
+void launch_project_init(PlanStats* stats, cudaStream_t s) {
     k_init_stats<<<1, DGSM_MAX_LIGHTS, 0, s>>>(stats);
-    const int64_t total = (int64_t)n_lights * g.n;
+}
+
+void launch_project(const dgsm_gaussians_t& g, const LightsParam& lp, int n_lights, int res, int K,
+                    const dgsm_build_opts_t& o, int64_t i0, int64_t cnt, PairRec* recs, uint32_t* counts,
+                    uint4* dup, PlanStats* stats, cudaStream_t s) {
+    const int64_t total = (int64_t)n_lights * cnt;
     if (total == 0) return;
     const int bs = 256;
     const int64_t grid = (total + bs - 1) / bs;
-    k_project<<<(unsigned)grid, bs, 0, s>>>(g.means, g.scales, g.rotations, g.opacities, g.n, lp,
+    k_project<<<(unsigned)grid, bs, 0, s>>>(g.means, g.scales, g.rotations, g.opacities, g.n, i0, cnt, lp,
                                             n_lights, res, K, (double)o.kappa, (double)o.k_sigma,
                                             (double)o.rho_scale * (double)(2 * res) / (2.0 * kPi), o.bin_mode,
                                             o.absorption, (o.flags & DGSM_NO_TILE_CULL) != 0,

@@ -33,7 +33,7 @@ _STATUS = {0: "DGSM_OK", 1: "DGSM_EINVAL", 2: "DGSM_ENOSPC", 3: "DGSM_ECUDA", 4:
 EXPORTED = ["dgsm_default_opts", "dgsm_plan_workspace_bytes", "dgsm_build_plan", "dgsm_build_run",
             "dgsm_build_bins", "dgsm_build", "dgsm_exp_epilogue", "dgsm_query", "dgsm_query_footprint", "dgsm_strerror",
             "dgsm_last_error", "dgsm_last_launch_count", "dgsm_build_stats", "dgsm_set_accumulate_events",
-            "dgsm_slab_bytes", "dgsm_active_slab"]
+            "dgsm_slab_bytes", "dgsm_active_slab", "dgsm_frame_host"]
 
 
 class Gaussians(C.Structure):
@@ -103,6 +103,9 @@ def lib() -> C.CDLL:
         L.dgsm_query.argtypes = [vp, P(Light), C.c_int, C.c_int, C.c_int, vp, i64, vp, vp, vp]
         L.dgsm_query_footprint.argtypes = [vp, P(Light), C.c_int, C.c_int, C.c_int, vp, vp, vp, i64, vp, vp,
                                            C.c_int, vp, vp, vp]
+        L.dgsm_frame_host.argtypes = [P(Gaussians), P(Light), C.c_int, C.c_int, C.c_int, P(BuildOpts), vp, i64,
+                                      vp, vp, sz, P(sz), vp, vp]
+        L.dgsm_frame_host.restype = C.c_int
         L.dgsm_slab_bytes.argtypes = [C.c_int, C.c_int]
         L.dgsm_slab_bytes.restype = sz
         L.dgsm_active_slab.argtypes = [vp, i64, P(Roi), P(Light), C.c_int, C.c_int, C.c_int, vp, sz, vp]
@@ -337,6 +340,43 @@ def query(atlas: torch.Tensor, lights, positions: torch.Tensor, colors: Optional
 
 
 DGSM_MAX_FOOTPRINT_SAMPLES = 64
+
+
+class FrameHost:
+    """dgsm_frame_host: one frame (build + query) from HOST tensors (pinned for
+    overlap), the device workspace kept across calls.  Returns the device atlas;
+    ``T_host`` (CPU float32 [m]) is filled when the stream completes."""
+
+    def __init__(self, lights, atlas_res: int, n_shells: int, opts: Optional[Options] = None, device="cuda"):
+        self.lights, self.n_lights = _lights(lights)
+        self.res, self.K = int(atlas_res), int(n_shells)
+        self.opts = opts or Options()
+        self._oc = self.opts.c()
+        self.device = torch.device(device)
+        self.ws = _alloc(0, self.device)
+        self.atlas = torch.empty((self.n_lights, self.K, self.res, self.res), dtype=torch.float32,
+                                 device=self.device)
+
+    def __call__(self, g_host: Dict[str, torch.Tensor], receivers_host: torch.Tensor, T_host: torch.Tensor,
+                 stream=None) -> torch.Tensor:
+        arrs = [g_host[k] for k in ("means", "scales", "rotations", "opacities")]
+        for a in arrs + [receivers_host, T_host]:
+            if a.is_cuda or a.dtype != torch.float32 or not a.is_contiguous():
+                raise DgsmError("frame_host takes contiguous float32 CPU tensors")
+        n, m = arrs[0].shape[0], receivers_host.shape[0]
+        g = Gaussians(*[C.c_void_p(a.data_ptr()) for a in arrs], n)
+        need = C.c_size_t(0)
+        for _ in range(3):
+            rc = lib().dgsm_frame_host(C.byref(g), self.lights, self.n_lights, self.res, self.K, C.byref(self._oc),
+                                       C.c_void_p(receivers_host.data_ptr()), m, C.c_void_p(T_host.data_ptr()),
+                                       C.c_void_p(self.ws.data_ptr()), self.ws.numel(), C.byref(need),
+                                       C.c_void_p(self.atlas.data_ptr()), C.c_void_p(_stream_ptr(stream)))
+            if rc != 2:  # DGSM_ENOSPC: grow the workspace and retry
+                break
+            self.ws = _alloc(int(need.value * 1.25) + (1 << 20), self.device)
+        _check(rc, "dgsm_frame_host")
+        self.launches = last_launch_count()
+        return self.atlas
 
 
 def active_slab(receivers: torch.Tensor, roi, lights, atlas_res: int, n_shells: int,

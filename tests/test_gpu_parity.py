@@ -321,6 +321,27 @@ def test_slab_empty_roi_all_ones(dg):
     assert torch.all(T == 1.0)
 
 
+def test_frame_host_equals_device_path(dg, oracle_mod):
+    """dgsm_frame_host (HOST inputs, chunked upload + projection, side-stream
+    receiver upload) gives exactly the device-path build + query, and the
+    oracle's within tolerance."""
+    s = synth.config2(scale=0.02, res=64, K=16)
+    gh = {k: torch.from_numpy(np.ascontiguousarray(v, np.float32)).pin_memory() for k, v in s.gaussians.items()}
+    rh = torch.from_numpy(s.queries).pin_memory()
+    Th = torch.empty(rh.shape[0]).pin_memory()
+    fr = dg.FrameHost(s.lights, s.res, s.K)
+    at = fr(gh, rh, Th)
+    torch.cuda.synchronize()
+    at2 = dg.build(dg.to_device(s.gaussians), s.lights, s.res, s.K)
+    T2 = dg.query(at2, s.lights, torch.from_numpy(s.queries).cuda())
+    assert torch.equal(at, at2) and torch.equal(Th, T2.cpu())
+    at = fr(gh, rh, Th)  # workspace reused
+    torch.cuda.synchronize()
+    assert torch.equal(Th, T2.cpu()) and fr.launches > 10
+    To, _ = oracle_mod.build(s.gaussians, s.lights, s.res, s.K)
+    assert np.abs(Th.numpy() - oracle_mod.query(To, s.lights, s.queries)).max() <= TOL_T
+
+
 def test_query_empty(dg):
     atlas = torch.ones(1, 4, 16, 16, device="cuda")
     out = dg.query(atlas, dict(position=[[0, 0, 0]], t_max=[1.0]), torch.zeros(0, 3, device="cuda"))
