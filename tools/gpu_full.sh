@@ -1,6 +1,7 @@
 #!/bin/bash
 # Round-end style measurement: build, gpu tests, smoke, full bench (with cpu baseline),
-# reference arm, ncu launch list + full capture of k_accumulate.
+# reference arm, ncu launch list (one ncu run per call; the --set full capture is
+# tools/gpu_prof2.sh, a separate call).
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || exit 1
 timeout 900 python -m pytest tests -m gpu -q --timeout 300 -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1
@@ -13,7 +14,5 @@ nproc > gpurun_out/nproc.txt; grep -m1 "model name" /proc/cpuinfo >> gpurun_out/
 SMALL="bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
 timeout 300 python $SMALL > gpurun_out/b_small.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
-    python $SMALL > gpurun_out/ncu1.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_accumulate -s 2 -c 1 -o gpurun_out/prof \
-    python $SMALL > gpurun_out/ncu2.log 2>&1
-echo "ncu exit $?" >> gpurun_out/ncu2.log
+    python $SMALL > gpurun_out/ncu1.log 2>&1
+echo "ncu exit $?" >> gpurun_out/ncu1.log
