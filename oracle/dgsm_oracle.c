@@ -728,3 +728,110 @@ int64_t or_active_slab(const float* x, int64_t m, const float* roi, const float*
     }
     return inside;
 }
+
+/* ------------------------------------------------------------------ */
+/* NEXT-4  SH lighting transfer (§3.5)             */
+/* ------------------------------------------------------------------ */
+/* Real spherical-harmonic basis up to degree d ("real spherical-
+ * harmonic (SH) basis up to degree d", K = (d+1)^2), orthonormal on the
+ * sphere, Condon-Shortley phase, index k = l^2 + l + m (m = -l..l):
+ *   Y_l0 = K_l0 P_l^0(cos t),  Y_lm = sqrt2 K_lm P_l^m(cos t) cos(m p)  (m > 0),
+ *   Y_l,-m = sqrt2 K_lm P_l^m(cos t) sin(m p),  K_lm = sqrt((2l+1)/(4 pi) (l-m)!/(l+m)!),
+ * P_l^m by the textbook three-term recurrence (P_m^m = (-1)^m (2m-1)!! (1-z^2)^{m/2}).
+ * DESIGN.md reading R-SH. */
+void or_sh_basis(int d, const double dir[3], double* out)
+{
+    double x = dir[0], y = dir[1], z = dir[2];
+    double r = sqrt((x * x + y * y) + z * z);
+    x /= r; y /= r; z /= r;
+    double phi = atan2(y, x);
+    double st = sqrt(fmax(0.0, 1.0 - z * z));
+    for (int m = 0; m <= d; ++m) {
+        /* P_m^m */
+        double pmm = 1.0;
+        for (int i = 1; i <= m; ++i) pmm *= -(2.0 * i - 1.0) * st;
+        double plm2 = 0.0, plm1 = pmm;
+        for (int l = m; l <= d; ++l) {
+            double p;
+            if (l == m) p = pmm;
+            else if (l == m + 1) p = z * (2.0 * m + 1.0) * pmm;
+            else p = ((2.0 * l - 1.0) * z * plm1 - (double)(l + m - 1) * plm2) / (double)(l - m);
+            if (l > m) { plm2 = plm1; plm1 = p; }
+            /* K_lm */
+            double ratio = 1.0; /* (l-m)!/(l+m)! */
+            for (int i = l - m + 1; i <= l + m; ++i) ratio /= (double)i;
+            double K = sqrt((2.0 * l + 1.0) / (4.0 * OR_PI) * ratio);
+            if (m == 0) out[l * l + l] = K * p;
+            else {
+                out[l * l + l + m] = sqrt(2.0) * K * p * cos(m * phi);
+                out[l * l + l - m] = sqrt(2.0) * K * p * sin(m * phi);
+            }
+        }
+    }
+}
+
+/* Lat-long grid point j = i * n_phi + k ("latitude-longitude grid
+ * {w_j} with quadrature weights w_j ~ sin theta_j"): theta_i = (i+1/2) pi/n_theta
+ * from +z, phi_k = (k+1/2) 2 pi/n_phi, w = sin(theta) (pi/n_theta)(2 pi/n_phi)
+ * (reading R-SH: the midpoint-rule weights, sum ~ 4 pi). */
+void or_transfer_dir(int n_theta, int n_phi, int64_t j, double dir[3], double* w)
+{
+    int64_t i = j / n_phi, k = j % n_phi;
+    double th = ((double)i + 0.5) * OR_PI / n_theta;
+    double ph = ((double)k + 0.5) * 2.0 * OR_PI / n_phi;
+    dir[0] = sin(th) * cos(ph);
+    dir[1] = sin(th) * sin(ph);
+    dir[2] = cos(th);
+    *w = sin(th) * (OR_PI / n_theta) * (2.0 * OR_PI / n_phi);
+}
+
+/* Per-channel lighting scale and relit colour:
+ *   L_c(w_j) = max(0, B(w_j) A_c)          (radiance from the fitted SH, Eq. before
+ *                                           P:L209; negative ringing clamped: R-SH)
+ *   S(w, n)  = max(0, <w, n>)^q            (S = 0 where <w,n> <= 0)
+ *   s_c(n)   = clip_[0, s_max]( sum_j w_j L_c S / (sum_j w_j S + eps) )
+ *   c'       = max(0, gamma c (.) s(n))
+ * sh: [3][K] coefficients; normals, colors: [n][3] (colors nullable);
+ * scales_out [n][3], colors_out [n][3] (nullable). */
+void or_sh_transfer(const double* sh, int d, int n_theta, int n_phi, double q, double eps, double s_max,
+                    double gamma, const double* normals, const double* colors, int64_t n, double* scales_out,
+                    double* colors_out)
+{
+    int K = (d + 1) * (d + 1);
+    int64_t M = (int64_t)n_theta * n_phi;
+    double* B = (double*)malloc(sizeof(double) * (size_t)K);
+    double* L = (double*)malloc(sizeof(double) * 3 * (size_t)M);
+    double* W = (double*)malloc(sizeof(double) * (size_t)M);
+    double* Dir = (double*)malloc(sizeof(double) * 3 * (size_t)M);
+    for (int64_t j = 0; j < M; ++j) {
+        or_transfer_dir(n_theta, n_phi, j, Dir + 3 * j, W + j);
+        or_sh_basis(d, Dir + 3 * j, B);
+        for (int c = 0; c < 3; ++c) {
+            double v = 0.0;
+            for (int k = 0; k < K; ++k) v += B[k] * sh[c * K + k];
+            L[3 * j + c] = v > 0.0 ? v : 0.0;
+        }
+    }
+    for (int64_t g = 0; g < n; ++g) {
+        const double* nn = normals + 3 * g;
+        double num[3] = {0.0, 0.0, 0.0}, den = 0.0;
+        for (int64_t j = 0; j < M; ++j) {
+            double dt = nn[0] * Dir[3 * j] + nn[1] * Dir[3 * j + 1] + nn[2] * Dir[3 * j + 2];
+            if (dt <= 0.0) continue;
+            double S = pow(dt, q);
+            den += W[j] * S;
+            for (int c = 0; c < 3; ++c) num[c] += W[j] * L[3 * j + c] * S;
+        }
+        for (int c = 0; c < 3; ++c) {
+            double s = num[c] / (den + eps);
+            if (s < 0.0) s = 0.0;
+            if (s > s_max) s = s_max;
+            if (scales_out) scales_out[3 * g + c] = s;
+            if (colors_out && colors) {
+                double v = gamma * colors[3 * g + c] * s;
+                colors_out[3 * g + c] = v > 0.0 ? v : 0.0;
+            }
+        }
+    }
+    free(B); free(L); free(W); free(Dir);
+}

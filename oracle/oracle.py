@@ -67,6 +67,10 @@ def lib():
         L.or_active_slab.restype = C.c_int64
         L.or_active_slab.argtypes = [fp, C.c_int64, fp, fp, fp, C.c_int, C.c_int, C.c_int,
                                      C.POINTER(C.c_ubyte), C.POINTER(C.c_int32)]
+        L.or_sh_basis.argtypes = [C.c_int, dp, dp]
+        L.or_transfer_dir.argtypes = [C.c_int, C.c_int, C.c_int64, dp, dp]
+        L.or_sh_transfer.argtypes = [dp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                     C.c_double, dp, dp, C.c_int64, dp, dp]
         L.or_query_footprint.argtypes = [dp, C.c_int, C.c_int, C.c_int, fp, fp, fp, fp, fp, C.c_int64,
                                          dp, dp, C.c_int, dp]
         L.or_beta_mode.restype = C.c_double
@@ -276,3 +280,42 @@ def query_footprint(atlas, lights, g, z, w):
                              _p(mu, C.c_float), _p(s, C.c_float), _p(q, C.c_float), mu.shape[0],
                              _p(z, C.c_double), _p(w, C.c_double), z.shape[0], _p(out, C.c_double))
     return out
+
+
+def sh_basis(dirs, d):
+    """NEXT-4: real SH basis (orthonormal, Condon-Shortley phase, k = l^2+l+m) [N, (d+1)^2]."""
+    x = _f64(dirs).reshape(-1, 3)
+    out = np.zeros((x.shape[0], (d + 1) ** 2))
+    row = np.zeros((d + 1) ** 2)
+    for i in range(x.shape[0]):
+        lib().or_sh_basis(int(d), _p(np.ascontiguousarray(x[i]), C.c_double), _p(row, C.c_double))
+        out[i] = row
+    return out
+
+
+def transfer_grid(n_theta=64, n_phi=128):
+    """Lat-long directions [M, 3] and midpoint quadrature weights [M] of the transfer."""
+    M = n_theta * n_phi
+    D = np.zeros((M, 3))
+    W = np.zeros(M)
+    d3 = np.zeros(3)
+    w = C.c_double(0.0)
+    for j in range(M):
+        lib().or_transfer_dir(n_theta, n_phi, j, _p(d3, C.c_double), C.byref(w))
+        D[j] = d3
+        W[j] = w.value
+    return D, W
+
+
+def sh_transfer(sh, d, normals, colors=None, n_theta=64, n_phi=128, q=1.0, eps=1e-6, s_max=4.0, gamma=1.0):
+    """NEXT-4: per-channel scales s [n, 3] and relit colours [n, 3] (or None)."""
+    A = _f64(sh).reshape(3, (d + 1) ** 2)
+    nr = _f64(normals).reshape(-1, 3)
+    n = nr.shape[0]
+    col = None if colors is None else _f64(colors).reshape(-1, 3)
+    s = np.zeros((n, 3))
+    co = np.zeros((n, 3)) if col is not None else None
+    lib().or_sh_transfer(_p(A, C.c_double), int(d), int(n_theta), int(n_phi), float(q), float(eps), float(s_max),
+                         float(gamma), _p(nr, C.c_double), None if col is None else _p(col, C.c_double), n,
+                         _p(s, C.c_double), None if co is None else _p(co, C.c_double))
+    return s, co

@@ -537,3 +537,73 @@ def test_query_seam_continuity(oracle_mod):
         d /= np.linalg.norm(d)
         v = oracle_mod.query(at, lights, (2.0 * d)[None])[0]
         assert abs(v - (0.5 + 0.4 * d[0] - 0.3 * d[1] + 0.2 * d[2])) < 0.02
+
+
+# ---------------------------------------------------------------- NEXT-4 SH transfer
+def test_sh_basis_pins(oracle_mod):
+    """Real SH basis (R-SH): equals scipy's complex Y_l^m (Condon-Shortley phase)
+    mapped to the real basis (sqrt2 Re for m > 0, sqrt2 Im of Y_l^|m| for m < 0);
+    Y_00 = 1/(2 sqrt(pi)); orthonormal under the transfer's own quadrature."""
+    import scipy.special as ss
+    rng = np.random.default_rng(0)
+    d = 4
+    dirs = rng.normal(size=(40, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    B = oracle_mod.sh_basis(dirs, d)
+    pol, az = np.arccos(dirs[:, 2]), np.arctan2(dirs[:, 1], dirs[:, 0])
+    for l in range(d + 1):
+        for m in range(-l, l + 1):
+            Y = ss.sph_harm_y(l, abs(m), pol, az)
+            want = Y.real if m == 0 else np.sqrt(2) * (Y.real if m > 0 else Y.imag)
+            assert np.abs(B[:, l * l + l + m] - want).max() < 1e-12, (l, m)
+    assert np.abs(B[:, 0] - 0.5 / np.sqrt(np.pi)).max() < 1e-15
+    D, W = oracle_mod.transfer_grid(128, 256)
+    assert abs(W.sum() - 4 * np.pi) < 1e-3
+    BB = oracle_mod.sh_basis(D, 3)
+    assert np.abs((BB * W[:, None]).T @ BB - np.eye(16)).max() < 1e-3
+
+
+def _zonal_step_sh(d):
+    """SH coefficients of the hemisphere light L = [w_z > 0], zonal: c_l Y_l0 with
+    c_l = 2 pi sqrt((2l+1)/(4 pi)) int_0^1 P_l(x) dx (scipy quadrature, not the oracle)."""
+    from scipy.integrate import quad
+    from scipy.special import eval_legendre
+    A = np.zeros((d + 1) ** 2)
+    for l in range(d + 1):
+        A[l * l + l] = 2 * np.pi * np.sqrt((2 * l + 1) / (4 * np.pi)) * quad(lambda x: eval_legendre(l, x), 0, 1)[0]
+    return np.stack([A, A, A])
+
+
+def test_sh_transfer_pins(oracle_mod):
+    """P:L214-222 against closed forms.  Constant environment (A = 2 sqrt(pi) e_0,
+    L = 1): s = den/(den + eps) with den -> pi for q = 1.  Hemisphere light
+    projected to degree 1: L = 1/2 + 3/4 z, and by Funk-Hecke s(n) = 1/2 + cos(a)/2
+    for a normal at angle a < 41.8 deg (the lobe never meets L < 0, so the clamp is
+    idle).  Degree 3, n = z: s = 1 exactly (the step has only odd l >= 1 beyond
+    l = 0, the clamped cosine only even l >= 2: the truncated sum equals the full
+    one).  Linearity in L, the clip at s_max, gamma and the floor of c'."""
+    nrm = np.array([[0, 0, 1.0], [0.3, -0.2, 0.93], [-1, 0, 0], [0, 0, -1.0]])
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    const = np.zeros((3, 16))
+    const[:, 0] = 2 * np.sqrt(np.pi)
+    s, _ = oracle_mod.sh_transfer(const, 3, nrm, eps=0.0)
+    assert np.abs(s - 1.0).max() < 1e-12
+    s, _ = oracle_mod.sh_transfer(const, 3, nrm, eps=1e-2)
+    assert np.abs(s - np.pi / (np.pi + 1e-2)).max() < 2e-4
+    for a_deg in (0.0, 20.0, 35.0):
+        a = np.radians(a_deg)
+        n1 = np.array([[np.sin(a), 0.0, np.cos(a)]])
+        s, _ = oracle_mod.sh_transfer(_zonal_step_sh(1), 1, n1, n_theta=128, n_phi=256, eps=0.0)
+        assert np.abs(s - (0.5 + 0.5 * np.cos(a))).max() < 2e-4, (a_deg, s)
+    s, _ = oracle_mod.sh_transfer(_zonal_step_sh(3), 3, np.array([[0, 0, 1.0]]), n_theta=128, n_phi=256, eps=0.0)
+    assert np.abs(s - 1.0).max() < 2e-4
+    rng = np.random.default_rng(3)
+    A = rng.normal(0, 0.3, (3, 16))
+    A[:, 0] = 2.0
+    col = rng.random((4, 3))
+    s1, c1 = oracle_mod.sh_transfer(A, 3, nrm, col, eps=0.0, gamma=1.5)
+    s2, c2 = oracle_mod.sh_transfer(2 * A, 3, nrm, col, eps=0.0, gamma=1.5)
+    assert np.abs(s2 - 2 * s1).max() < 1e-12 and (s1 > 0).all()
+    assert np.abs(c1 - 1.5 * col * s1).max() < 1e-12
+    s3, c3 = oracle_mod.sh_transfer(50 * A, 3, nrm, col, s_max=4.0, gamma=0.0)
+    assert (s3 == 4.0).all() and (c3 == 0.0).all()
