@@ -273,6 +273,42 @@ int dgsm_active_slab(const float* receivers, int64_t m, const dgsm_roi_t* roi, c
                      int n_lights, int atlas_res, int n_shells, void* slab, size_t slab_bytes,
                      void* stream);
 
+/* ------------------------------------------------------------------
+ * SH lighting transfer (§3.5)
+ * ------------------------------------------------------------------ */
+#define DGSM_MAX_SH_DEGREE 3
+
+typedef struct dgsm_transfer_opts {
+    int32_t grid_theta, grid_phi;  /* lat-long grid, M = grid_theta * grid_phi (default 64 x 128) */
+    float q;                       /* cosine-lobe exponent >= 0 (default 1: Lambertian) */
+    float eps;                     /* denominator guard (default 1e-6) */
+    float s_max;                   /* clip bound, the paper's second "t_max" (default 4) */
+    float gamma;                   /* global intensity (default 1) */
+} dgsm_transfer_opts_t;
+
+void dgsm_default_transfer_opts(dgsm_transfer_opts_t* opts);
+
+/* Device workspace bytes of dgsm_sh_transfer for n Gaussians (0 on bad input). */
+size_t dgsm_transfer_workspace_bytes(const dgsm_transfer_opts_t* opts, int64_t n);
+
+/* Per-channel lighting scale of each Gaussian from an SH environment probe
+ * and, if colors_in/colors_out are given, the relit colour:
+ *   L_c(w_j) = max(0, sum_k Y_k(w_j) sh[c][k])    (negative ringing clamped: reading R-SH)
+ *   S(w, n)  = max(0, <w, n>)^q
+ *   s_c(n)   = clip_[0, s_max]( sum_j w_j L_c(w_j) S(w_j, n) / (sum_j w_j S(w_j, n) + eps) )
+ *   c'       = max(0, gamma c (.) s(n))
+ * over the lat-long grid theta_i = (i + 1/2) pi / grid_theta (from +z),
+ * phi_k = (k + 1/2) 2 pi / grid_phi, w = sin(theta) (pi/grid_theta)(2 pi/grid_phi).
+ *   sh        HOST float [3][(sh_degree+1)^2]: real orthonormal SH with the
+ *             Condon-Shortley phase, index l^2 + l + m (the 3DGS convention)
+ *   normals   DEVICE float [n][3], unit; colors_in / colors_out DEVICE [n][3] or NULL;
+ *   scales_out DEVICE float [n][3] or NULL.
+ * Errors: DGSM_EINVAL (sh_degree outside [0, DGSM_MAX_SH_DEGREE], grid < 1,
+ * q < 0, eps < 0, s_max <= 0, null arrays), DGSM_ENOSPC (workspace). */
+int dgsm_sh_transfer(const float* sh, int sh_degree, const float* normals, const float* colors_in, int64_t n,
+                     const dgsm_transfer_opts_t* opts, float* scales_out, float* colors_out, void* ws,
+                     size_t ws_bytes, void* stream);
+
 /* Read the counters of the last DGSM_COLLECT_STATS dgsm_build_run that used
  * this run workspace (synchronises `stream`). */
 int dgsm_build_stats(const dgsm_plan_t* plan, void* run_ws, size_t run_ws_bytes,

@@ -22,7 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
           "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
-SOURCES = ["project.cu", "slab.cu", "scan.cu", "binning.cu", "onesweep.cu", "accumulate.cu", "query.cu", "dgsm_api.cu"]
+SOURCES = ["project.cu", "slab.cu", "scan.cu", "binning.cu", "onesweep.cu", "accumulate.cu", "query.cu", "transfer.cu", "dgsm_api.cu"]
 PER_FILE = {"project.cu": ["-fmad=false"], "slab.cu": ["-fmad=false"]}
 HEADERS = ["dgsm_internal.cuh"]
 

@@ -560,6 +560,57 @@ int dgsm_query_footprint(const float* atlas, const dgsm_light_t* lights, int n_l
     return cuda_check("query footprint");
 }
 
+void dgsm_default_transfer_opts(dgsm_transfer_opts_t* o) {
+    if (!o) return;
+    o->grid_theta = 64;
+    o->grid_phi = 128;
+    o->q = 1.0f;
+    o->eps = 1e-6f;
+    o->s_max = 4.0f;
+    o->gamma = 1.0f;
+}
+
+static int check_transfer_opts(const dgsm_transfer_opts_t& o) {
+    if (o.grid_theta < 1 || o.grid_phi < 1 || (int64_t)o.grid_theta * o.grid_phi > (1 << 24))
+        return fail(DGSM_EINVAL, "bad transfer grid %d x %d", o.grid_theta, o.grid_phi);
+    if (!(o.q >= 0.0f) || !(o.eps >= 0.0f) || !(o.s_max > 0.0f))
+        return fail(DGSM_EINVAL, "transfer: need q >= 0, eps >= 0, s_max > 0");
+    return DGSM_OK;
+}
+
+size_t dgsm_transfer_workspace_bytes(const dgsm_transfer_opts_t* opts, int64_t n) {
+    dgsm_transfer_opts_t o;
+    if (opts) o = *opts; else dgsm_default_transfer_opts(&o);
+    if (n < 0 || o.grid_theta < 1 || o.grid_phi < 1) return 0;
+    return transfer_workspace_bytes(o.grid_theta, o.grid_phi, n);
+}
+
+int dgsm_sh_transfer(const float* sh, int sh_degree, const float* normals, const float* colors_in, int64_t n,
+                     const dgsm_transfer_opts_t* opts, float* scales_out, float* colors_out, void* ws,
+                     size_t ws_bytes, void* stream) {
+    g_launches = 0;
+    dgsm_transfer_opts_t o;
+    if (opts) o = *opts; else dgsm_default_transfer_opts(&o);
+    if (int rc = check_transfer_opts(o)) return rc;
+    if (!sh) return fail(DGSM_EINVAL, "null sh");
+    if (sh_degree < 0 || sh_degree > DGSM_MAX_SH_DEGREE) return fail(DGSM_EINVAL, "sh_degree %d outside [0, %d]", sh_degree, DGSM_MAX_SH_DEGREE);
+    if (n < 0) return fail(DGSM_EINVAL, "n < 0");
+    if (n > 0 && !normals) return fail(DGSM_EINVAL, "null normals");
+    if (colors_out && !colors_in) return fail(DGSM_EINVAL, "colors_out without colors_in");
+    if (!ws || (uintptr_t)ws % kAlign) return fail(DGSM_EINVAL, "null or unaligned workspace");
+    const size_t need = transfer_workspace_bytes(o.grid_theta, o.grid_phi, n);
+    if (ws_bytes < need) return fail(DGSM_ENOSPC, "transfer workspace %zu < %zu bytes", ws_bytes, need);
+    ShParam sp;
+    memset(&sp, 0, sizeof(sp));
+    sp.d = sh_degree;
+    const int K = (sh_degree + 1) * (sh_degree + 1);
+    for (int c = 0; c < 3; ++c)
+        for (int k = 0; k < K; ++k) sp.a[c][k] = sh[c * K + k];
+    launch_transfer(sp, o.grid_theta, o.grid_phi, o.q, o.eps, o.s_max, o.gamma, normals, colors_in, n, scales_out,
+                    colors_out, ws, (cudaStream_t)stream, &g_launches);
+    return cuda_check("sh transfer");
+}
+
 int dgsm_set_accumulate_events(void* before, void* after) {
     g_ev_before = (cudaEvent_t)before;
     g_ev_after = (cudaEvent_t)after;

@@ -37,6 +37,12 @@ struct FootprintParam {
     float4 zw[DGSM_MAX_FOOTPRINT_SAMPLES];
 };
 
+// SH probe coefficients of the transfer (NEXT-4): [channel][l^2 + l + m], degree <= 3.
+struct ShParam {
+    float a[3][16];
+    int d;
+};
+
 // Device-side statistics of a plan, copied back to the host once.
 struct PlanStats {
     uint32_t depth_min[DGSM_MAX_LIGHTS];
@@ -204,6 +210,11 @@ void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint3
                        uint32_t* unit_counter, float* atlas, unsigned long long* stats,
                        const uint64_t* slab_mask, const int2* slab_k,
                        cudaEvent_t ev_before, cudaEvent_t ev_after, cudaStream_t s);
+int transfer_chunks(int64_t n, int64_t M);
+size_t transfer_workspace_bytes(int n_theta, int n_phi, int64_t n);
+void launch_transfer(const ShParam& sp, int n_theta, int n_phi, float q, float eps, float s_max, float gamma,
+                     const float* normals, const float* colors, int64_t n, float* scales_out, float* colors_out,
+                     void* ws, cudaStream_t s, int* launches);
 void launch_active_slab(const float* x, int64_t m, const dgsm_roi_t& roi, const LightsParam& lp, int n_lights,
                         int res, int K, uint64_t* mask, int2* kr, cudaStream_t s, int* launches);
 void launch_exp(const float* tau, float* T, int64_t count, cudaStream_t s);

@@ -33,7 +33,8 @@ _STATUS = {0: "DGSM_OK", 1: "DGSM_EINVAL", 2: "DGSM_ENOSPC", 3: "DGSM_ECUDA", 4:
 EXPORTED = ["dgsm_default_opts", "dgsm_plan_workspace_bytes", "dgsm_build_plan", "dgsm_build_run",
             "dgsm_build_bins", "dgsm_build", "dgsm_exp_epilogue", "dgsm_query", "dgsm_query_footprint", "dgsm_strerror",
             "dgsm_last_error", "dgsm_last_launch_count", "dgsm_build_stats", "dgsm_set_accumulate_events",
-            "dgsm_slab_bytes", "dgsm_active_slab", "dgsm_frame_host"]
+            "dgsm_slab_bytes", "dgsm_active_slab", "dgsm_frame_host", "dgsm_default_transfer_opts",
+            "dgsm_transfer_workspace_bytes", "dgsm_sh_transfer"]
 
 
 class Gaussians(C.Structure):
@@ -49,6 +50,11 @@ class BuildOpts(C.Structure):
     _fields_ = [("kappa", C.c_float), ("k_sigma", C.c_float), ("rho_scale", C.c_float),
                 ("bin_mode", C.c_int32), ("flags", C.c_uint32), ("absorption", C.c_int32),
                 ("slab", C.c_void_p)]
+
+
+class TransferOpts(C.Structure):
+    _fields_ = [("grid_theta", C.c_int32), ("grid_phi", C.c_int32), ("q", C.c_float), ("eps", C.c_float),
+                ("s_max", C.c_float), ("gamma", C.c_float)]
 
 
 class Roi(C.Structure):
@@ -106,6 +112,12 @@ def lib() -> C.CDLL:
         L.dgsm_frame_host.argtypes = [P(Gaussians), P(Light), C.c_int, C.c_int, C.c_int, P(BuildOpts), vp, i64,
                                       vp, vp, sz, P(sz), vp, vp]
         L.dgsm_frame_host.restype = C.c_int
+        L.dgsm_default_transfer_opts.argtypes = [P(TransferOpts)]
+        L.dgsm_default_transfer_opts.restype = None
+        L.dgsm_transfer_workspace_bytes.argtypes = [P(TransferOpts), i64]
+        L.dgsm_transfer_workspace_bytes.restype = sz
+        L.dgsm_sh_transfer.argtypes = [vp, C.c_int, vp, vp, i64, P(TransferOpts), vp, vp, vp, sz, vp]
+        L.dgsm_sh_transfer.restype = C.c_int
         L.dgsm_slab_bytes.argtypes = [C.c_int, C.c_int]
         L.dgsm_slab_bytes.restype = sz
         L.dgsm_active_slab.argtypes = [vp, i64, P(Roi), P(Light), C.c_int, C.c_int, C.c_int, vp, sz, vp]
@@ -340,6 +352,29 @@ def query(atlas: torch.Tensor, lights, positions: torch.Tensor, colors: Optional
 
 
 DGSM_MAX_FOOTPRINT_SAMPLES = 64
+
+
+def sh_transfer(sh, sh_degree: int, normals: torch.Tensor, colors: Optional[torch.Tensor] = None,
+                grid=(64, 128), q: float = 1.0, eps: float = 1e-6, s_max: float = 4.0, gamma: float = 1.0,
+                stream=None):
+    """NEXT-4 SH lighting transfer (§3.5): per-channel scales
+    s [n, 3] of unit normals (CUDA float32 [n, 3]) under the SH probe ``sh``
+    (host [3, (d+1)^2]); with ``colors`` (CUDA [n, 3]) also the relit colours
+    max(0, gamma c * s).  Returns (scales, colors_out or None)."""
+    nr = _dev_f32(normals, "normals", (3,))
+    n = nr.shape[0]
+    A = np.ascontiguousarray(np.asarray(sh, np.float32).reshape(3, (sh_degree + 1) ** 2))
+    o = TransferOpts(int(grid[0]), int(grid[1]), float(q), float(eps), float(s_max), float(gamma))
+    col = None if colors is None else _dev_f32(colors, "colors", (3,))
+    scales = torch.empty((n, 3), dtype=torch.float32, device=nr.device)
+    cout = torch.empty((n, 3), dtype=torch.float32, device=nr.device) if col is not None else None
+    ws = _alloc(lib().dgsm_transfer_workspace_bytes(C.byref(o), n), nr.device)
+    rc = lib().dgsm_sh_transfer(A.ctypes.data_as(C.c_void_p), int(sh_degree), C.c_void_p(nr.data_ptr()),
+                                None if col is None else C.c_void_p(col.data_ptr()), n, C.byref(o),
+                                C.c_void_p(scales.data_ptr()), None if cout is None else C.c_void_p(cout.data_ptr()),
+                                C.c_void_p(ws.data_ptr()), ws.numel(), C.c_void_p(_stream_ptr(stream)))
+    _check(rc, "dgsm_sh_transfer")
+    return scales, cout
 
 
 class FrameHost:

@@ -129,3 +129,20 @@ def test_binding_refuses_cpu_tensors():
     g["opacities"] = torch.zeros(4)
     with pytest.raises(dgsm.DgsmError):
         dgsm.build(g, dict(position=[[0, 0, 0]], t_max=[1.0]), 16, 4)
+
+
+def test_transfer_validation(lib):
+    """NEXT-4 ABI: defaults, workspace size, argument checks before device work."""
+    o = dgsm.TransferOpts()
+    lib.dgsm_default_transfer_opts(C.byref(o))
+    assert (o.grid_theta, o.grid_phi, o.q, o.s_max, o.gamma) == (64, 128, 1.0, 4.0, 1.0)
+    assert lib.dgsm_transfer_workspace_bytes(C.byref(o), 1000) >= 2 * 16 * 64 * 128 + 16 * 1000
+    assert lib.dgsm_transfer_workspace_bytes(C.byref(o), -1) == 0
+    sh = (C.c_float * 48)()
+    ws = C.c_void_p(256)
+    assert lib.dgsm_sh_transfer(sh, 4, None, None, 0, C.byref(o), None, None, ws, 1 << 30, None) == 1
+    assert lib.dgsm_sh_transfer(None, 3, None, None, 0, C.byref(o), None, None, ws, 1 << 30, None) == 1
+    assert lib.dgsm_sh_transfer(sh, 3, None, None, 5, C.byref(o), None, None, ws, 1 << 30, None) == 1
+    assert lib.dgsm_sh_transfer(sh, 3, None, None, 0, C.byref(o), None, None, ws, 16, None) == 2
+    o.s_max = 0.0
+    assert lib.dgsm_sh_transfer(sh, 3, None, None, 0, C.byref(o), None, None, ws, 1 << 30, None) == 1

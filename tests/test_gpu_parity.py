@@ -356,3 +356,44 @@ def test_end_to_end_cfg1(dg, oracle_mod):
     To, _ = oracle_mod.build(s.gaussians, s.lights, s.res, s.K)
     Tq = oracle_mod.query(To, s.lights, s.queries)
     assert np.abs(T - Tq).max() <= TOL_T
+
+
+def _probe(seed, d):
+    rng = np.random.default_rng(seed)
+    A = np.zeros((3, (d + 1) ** 2))
+    A[:, 0] = rng.uniform(1.5, 3.0, 3)
+    for l in range(1, d + 1):
+        A[:, l * l:(l + 1) ** 2] = rng.normal(0, 0.8 / l, (3, 2 * l + 1))
+    return A
+
+
+@pytest.mark.parametrize("d,q,grid", [(3, 1.0, (64, 128)), (2, 2.0, (32, 64)), (3, 0.5, (48, 96)), (0, 1.0, (16, 32))])
+def test_sh_transfer_parity(dg, oracle_mod, d, q, grid):
+    """NEXT-4: scales and relit colours against the fp64 oracle."""
+    rng = np.random.default_rng(7 + d)
+    n = 3000
+    nr = rng.normal(size=(n, 3))
+    nr /= np.linalg.norm(nr, axis=1, keepdims=True)
+    nr = nr.astype(np.float32)
+    col = rng.random((n, 3)).astype(np.float32)
+    A = _probe(d, d).astype(np.float32)
+    s, co = dg.sh_transfer(A, d, torch.from_numpy(nr).cuda(), torch.from_numpy(col).cuda(), grid=grid, q=q,
+                           gamma=1.3)
+    so, coo = oracle_mod.sh_transfer(A.astype(np.float64), d, nr.astype(np.float64), col.astype(np.float64),
+                                     n_theta=grid[0], n_phi=grid[1], q=q, gamma=1.3)
+    assert np.abs(s.cpu().numpy() - so).max() <= 2e-5 * max(1.0, np.abs(so).max())
+    assert np.abs(co.cpu().numpy() - coo).max() <= 2e-5 * max(1.0, np.abs(coo).max())
+    s2, _ = dg.sh_transfer(A, d, torch.from_numpy(nr).cuda(), grid=grid, q=q, gamma=1.3)
+    assert torch.equal(s, s2)  # deterministic
+
+
+def test_sh_transfer_edge_cases(dg):
+    nr = torch.tensor([[0, 0, 1.0]], device="cuda")
+    A = np.zeros((3, 16), np.float32)
+    A[:, 0] = 2 * np.sqrt(np.pi)  # L = 1 everywhere
+    s, _ = dg.sh_transfer(A, 3, nr, eps=0.0)
+    assert torch.allclose(s, torch.ones_like(s), atol=2e-6)
+    s, _ = dg.sh_transfer(100 * A, 3, nr, s_max=4.0)
+    assert torch.all(s == 4.0)
+    s, c = dg.sh_transfer(A, 3, torch.zeros(0, 3, device="cuda"), torch.zeros(0, 3, device="cuda"))
+    assert s.numel() == 0 and c.numel() == 0
