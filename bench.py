@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle sample time")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-transfer", action="store_true", help="skip the NEXT-4 transfer timing")
     return ap.parse_args()
 
 
@@ -102,6 +103,42 @@ def query_roofline(ms: float, m: int, L: int, peaks: dict):
             "sector_frac": sec / (ms * 1e-3) / 1e9 / peak,
             "peak_src": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md 7.7 TB/s",
             "timing": "L2 flushed before each launch, CUDA events, host launch overhead excluded"}
+
+
+def transfer_timing(dev, n: int = 150_000, d: int = 3):
+    """NEXT-4 SH lighting transfer (not part of the step): n avatar Gaussians
+    (ActorsHQ scale, SURVEY cfg4) x the 64 x 128 lat-long grid, degree-3 probe,
+    q = 1; L2 flushed, device time; 8 FP32 ops per (Gaussian, direction)."""
+    import torch
+    from paper_2601_01660_b200 import dgsm
+    rng = np.random.default_rng(4)
+    nr = rng.normal(size=(n, 3))
+    nr /= np.linalg.norm(nr, axis=1, keepdims=True)
+    nr = torch.from_numpy(nr.astype(np.float32)).to(dev)
+    col = torch.from_numpy(rng.random((n, 3)).astype(np.float32)).to(dev)
+    A = rng.normal(0, 0.5, (3, (d + 1) ** 2)).astype(np.float32)
+    A[:, 0] = 2.5
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    for _ in range(3):
+        dgsm.sh_transfer(A, d, nr, col)
+    ts = []
+    for _ in range(10):
+        flush.zero_()
+        torch.cuda._sleep(200_000)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dgsm.sh_transfer(A, d, nr, col)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = float(np.median(ts))
+    ops = n * 64 * 128 * 8
+    peak = torch.cuda.get_device_properties(dev).multi_processor_count * 128 * 1965e6 / 1e12
+    return {"workload": f"{n} avatar Gaussians x 64x128 directions, SH degree {d}, q=1", "ms": ms,
+            "gaussians_per_s": n / (ms * 1e-3), "gpu_launches": 3,
+            "roofline": {"bound": "alu", "achieved": ops / (ms * 1e-3) / 1e12, "peak": peak, "unit": "TFLOP/s",
+                         "frac": ops / (ms * 1e-3) / 1e12 / peak,
+                         "alg_def": "8 FP32 ops per (Gaussian, direction): <w,n> 3, max 1, 4 FMA"}}
 
 
 def cores():
@@ -372,6 +409,7 @@ def run_dgsm(args):
         b.record()
     torch.cuda.synchronize()
     tq = [ev[i][0].elapsed_time(ev[i][4]) for i in range(K)]
+    transfer = None if args.no_transfer else transfer_timing(dev)
     total_ms = float(np.sum(t_step))
     if world > 1:
         t = torch.tensor([total_ms, float(64 * P)], device=dev, dtype=torch.float64)
@@ -471,6 +509,7 @@ def run_dgsm(args):
                          "needed_ops_per_launch": int(needed_ops),
                          "needed_ops_frac": needed_ops / (acc_ms * 1e-3) / 1e12 / peak_tops},
             "query_roofline": query_roofline(float(np.mean(tq)), m, s.L, peaks),
+            "transfer": transfer,
             "clocks": clocks,
         }
         if e2e:
