@@ -41,7 +41,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
         o = os.path.join(BUILD, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _mtime(o) < max(_mtime(s), hdr_time, _mtime(__file__)):
-            cmd = [NVCC, *ARCH, *COMMON, *PER_FILE.get(src, []), "-c", s, "-o", o]
+            cmd = [NVCC, *ARCH, *COMMON, *PER_FILE.get(src, []), *os.environ.get("DGSM_NVCC_EXTRA", "").split(),
+                   "-c", s, "-o", o]
             if ptxas_verbose:
                 cmd += ["-Xptxas", "-v"]
             if verbose:

@@ -39,9 +39,15 @@ __global__ void __launch_bounds__(256) k_gather_counts(const uint4* __restrict__
     cperm[j] = dup[perm[j]].w;
 }
 
-// One thread per Gaussian in depth-rank order: emit its tiles in the fixed
-// rectangle order (the same enumeration that produced its count) as
-// (key = tile, value = Gaussian index) at base + offs[j].
+// One warp per 32 consecutive Gaussians in depth-rank order.  Their outputs
+// are one contiguous segment [offs[j0], offs[j0 + 32]) (offs is the exclusive
+// scan in this order), so the warp writes it cooperatively, 32 consecutive
+// keys per store: lane l takes segment position p + l, finds the Gaussian that
+// owns it (binary search over the lanes' offsets) and the k-th tile of that
+// Gaussian's in-grid tile rectangle (row-major, the counting order).
+// Gaussians whose footprint wraps across the atlas border, or any Gaussian when
+// a ROI slab masks tiles, emit their own run in the fixed rectangle order
+// (the enumeration that produced their count), as before.
 __global__ void __launch_bounds__(256) k_duplicate_ranked(const uint4* __restrict__ dup,
                                                           const uint32_t* __restrict__ perm,
                                                           const uint64_t* __restrict__ offs, int64_t n,
@@ -50,16 +56,47 @@ __global__ void __launch_bounds__(256) k_duplicate_ranked(const uint4* __restric
                                                           uint32_t* __restrict__ keys,
                                                           uint32_t* __restrict__ vals) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    const uint32_t i = perm[j];
-    const uint4 r = dup[i];
-    if (r.w == 0) return;  // no tile
+    const int lane = threadIdx.x & 31;
+    const int64_t j0 = j - lane;
+    if (j0 >= n) return;  // whole warp past the end (warp-uniform)
+    const bool valid = j < n;
+    const uint32_t i = valid ? perm[j] : 0u;
+    const uint4 r = valid ? dup[i] : make_uint4(0u, 0u, 0u, 0u);
     const int TW = res / kTile;
-    uint64_t o = base + offs[j];
-    const uint64_t end = o + r.w;  // never more keys than the plan counted (a slab changed since the plan)
     int c0, c1, r0, r1;
     unpack_rect(r, c0, c1, r0, r1);
-    if (c0 >= 0 && c1 <= res - 1 && r0 >= 0 && r1 <= res - 1) {  // common case: inside the grid
+    const bool in_grid = c0 >= 0 && c1 <= res - 1 && r0 >= 0 && r1 <= res - 1;
+    const bool coop = r.w > 0 && in_grid && tm == nullptr;
+    // segment of this warp and each lane's start within it
+    const uint64_t seg0 = offs[j0];
+    const uint32_t excl = (uint32_t)((valid ? offs[j] : offs[n]) - seg0);
+    const uint32_t seg_len = __shfl_sync(0xffffffffu, excl + (valid ? r.w : 0u), 31);
+    const int tx0 = c0 >> 3, ty0 = r0 >> 3, wt = (c1 >> 3) - tx0 + 1;
+    for (uint32_t p = 0; p < seg_len; p += 32) {
+        const uint32_t q = p + (uint32_t)lane;
+        int lo = 0;  // owner: the last lane whose start is <= q
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            const uint32_t e = __shfl_sync(0xffffffffu, excl, lo + step < 32 ? lo + step : 31);
+            if (lo + step < 32 && e <= q) lo += step;
+        }
+        const uint32_t ek = __shfl_sync(0xffffffffu, excl, lo);
+        const int o_coop = __shfl_sync(0xffffffffu, (int)coop, lo);
+        const int o_tx0 = __shfl_sync(0xffffffffu, tx0, lo);
+        const int o_ty0 = __shfl_sync(0xffffffffu, ty0, lo);
+        const int o_wt = __shfl_sync(0xffffffffu, wt, lo);
+        const uint32_t o_i = __shfl_sync(0xffffffffu, i, lo);
+        if (q < seg_len && o_coop) {
+            const uint32_t k = q - ek;
+            const uint32_t dy = k / (uint32_t)o_wt, dx = k - dy * (uint32_t)o_wt;
+            keys[base + seg0 + q] = (uint32_t)((o_ty0 + (int)dy) * TW + o_tx0 + (int)dx);
+            vals[base + seg0 + q] = o_i;
+        }
+    }
+    if (!valid || r.w == 0 || coop) return;
+    uint64_t o = base + offs[j];
+    const uint64_t end = o + r.w;  // never more keys than the plan counted (a slab changed since the plan)
+    if (in_grid) {  // in the grid, under a ROI slab mask
         for (int ty = r0 >> 3; ty <= (r1 >> 3); ++ty)
             for (int tx = c0 >> 3; tx <= (c1 >> 3); ++tx) {
                 if (tm && (tm[ty * TW + tx] == 0ull || o == end)) continue;  // outside the ROI slab
