@@ -34,8 +34,8 @@
 static void or_rotation(const float q4[4], double R[3][3])
 {
     double w = q4[0], x = q4[1], y = q4[2], z = q4[3];
-    double qn = sqrt(((w * w + x * x) + y * y) + z * z);
-    w = w / qn; x = x / qn; y = y / qn; z = z / qn;
+    double inv = 1.0 / sqrt(((w * w + x * x) + y * y) + z * z);  /* binning contract v2: one division */
+    w = w * inv; x = x * inv; y = y * inv; z = z * inv;
     R[0][0] = 1.0 - 2.0 * (y * y + z * z);
     R[0][1] = 2.0 * (x * y - w * z);
     R[0][2] = 2.0 * (x * z + w * y);
@@ -171,7 +171,7 @@ double or_bin_center(int k, int K, double t_max) { return (k + 0.5) * t_max / K;
 /*         rect[0..3] = c0,c1,r0,r1 (unclamped integer texel range).     */
 /* Returns 0 when the Gaussian is excluded (D <= 1e-6, Q17), else 1.      */
 /* The eigenvalue uses the basis-free form of Sigma_perp (Q7/R5):         */
-/*   tr_perp = sum s_j^2 (1 - w_j^2),  det_perp = prod s_j^2 * sum w_j^2/s_j^2, */
+/*   tr_perp = sum s_j^2 (1 - w_j^2),  det_perp = sum_j w_j^2 prod_{i!=j} s_i^2, */
 /*   w = R^T (m/D); lambda1 = tr/2 + sqrt(max(tr^2/4 - det, 0)).          */
 /* ------------------------------------------------------------------ */
 int or_footprint(const float mu[3], const float s3[3], const float q4[4],
@@ -185,14 +185,18 @@ int or_footprint(const float mu[3], const float s3[3], const float q4[4],
     double D = sqrt((mx * mx + my * my) + mz * mz);
     if (!(D > 1e-6)) return 0;
 
-    double m[3] = {mx, my, mz}, uv[2];
-    or_oct_encode(m, uv);
-    double px = (uv[0] + 1.0) * (0.5 * W) - 0.5;
-    double py = (uv[1] + 1.0) * (0.5 * H) - 0.5;
+    /* psi(m) with one division: q = m * (1/|m|_1) (contract v2) */
+    double inv1 = 1.0 / ((fabs(mx) + fabs(my)) + fabs(mz));
+    double qx = mx * inv1, qy = my * inv1, qz = mz * inv1, u, v;
+    if (qz >= 0.0) { u = qx; v = qy; }
+    else { u = or_sgn(qx) * (1.0 - fabs(qy)); v = or_sgn(qy) * (1.0 - fabs(qx)); }
+    double px = (u + 1.0) * (0.5 * W) - 0.5;
+    double py = (v + 1.0) * (0.5 * H) - 0.5;
 
     double R[3][3];
     or_rotation(q4, R);
-    double dx = mx / D, dy = my / D, dz = mz / D;
+    double invD = 1.0 / D;
+    double dx = mx * invD, dy = my * invD, dz = mz * invD;
     double w[3], s2[3];
     for (int j = 0; j < 3; ++j) {
         w[j] = (R[0][j] * dx + R[1][j] * dy) + R[2][j] * dz;
@@ -200,13 +204,14 @@ int or_footprint(const float mu[3], const float s3[3], const float q4[4],
     }
     double tr = (s2[0] * (1.0 - w[0] * w[0]) + s2[1] * (1.0 - w[1] * w[1])) +
                 s2[2] * (1.0 - w[2] * w[2]);
-    double det = ((s2[0] * s2[1]) * s2[2]) *
-                 (((w[0] * w[0]) / s2[0] + (w[1] * w[1]) / s2[1]) + (w[2] * w[2]) / s2[2]);
+    /* det_perp = prod s^2 * sum w_j^2/s_j^2, written without divisions */
+    double det = ((s2[1] * s2[2]) * (w[0] * w[0]) + (s2[0] * s2[2]) * (w[1] * w[1])) +
+                 (s2[0] * s2[1]) * (w[2] * w[2]);
     double disc = (tr * tr) * 0.25 - det;
     if (disc < 0.0) disc = 0.0;
     double lam1 = tr * 0.5 + sqrt(disc);
     double rho = (rho_scale * (double)(H + W)) / (2.0 * OR_PI); /* P:L172, Q5 */
-    double p1 = ((k_sigma * sqrt(lam1)) / D) * rho;
+    double p1 = ((k_sigma * sqrt(lam1)) * invD) * rho;
 
     fp[0] = D; fp[1] = px; fp[2] = py; fp[3] = p1; fp[4] = lam1;
     double c0 = ceil(px - p1), c1 = floor(px + p1);

@@ -46,8 +46,8 @@ __global__ void __launch_bounds__(256, 3) k_project(
     rec.c0 = 1; rec.c1 = 0; rec.r0 = 1; rec.r1 = 0;
     if (D > 1e-6) {
         // footprint centre: octahedral encode psi(m) -> texel coords (pixel centres, Q3)
-        const double n1 = (fabs(mx) + fabs(my)) + fabs(mz);
-        const double qx = mx / n1, qy = my / n1, qz = mz / n1;
+        const double inv1 = 1.0 / ((fabs(mx) + fabs(my)) + fabs(mz));  // contract v2: one division
+        const double qx = mx * inv1, qy = my * inv1, qz = mz * inv1;
         double u, v;
         if (qz >= 0.0) { u = qx; v = qy; }
         else { u = sgn_pos(qx) * (1.0 - fabs(qy)); v = sgn_pos(qy) * (1.0 - fabs(qx)); }
@@ -57,8 +57,8 @@ __global__ void __launch_bounds__(256, 3) k_project(
         // rotation from the quaternion (w,x,y,z), normalised in fp64
         double qw = rotations[4 * i], qxr = rotations[4 * i + 1], qyr = rotations[4 * i + 2],
                qzr = rotations[4 * i + 3];
-        const double qn = sqrt(((qw * qw + qxr * qxr) + qyr * qyr) + qzr * qzr);
-        qw = qw / qn; qxr = qxr / qn; qyr = qyr / qn; qzr = qzr / qn;
+        const double iqn = 1.0 / sqrt(((qw * qw + qxr * qxr) + qyr * qyr) + qzr * qzr);
+        qw = qw * iqn; qxr = qxr * iqn; qyr = qyr * iqn; qzr = qzr * iqn;
         double R[3][3];
         R[0][0] = 1.0 - 2.0 * (qyr * qyr + qzr * qzr);
         R[0][1] = 2.0 * (qxr * qyr - qw * qzr);
@@ -71,7 +71,8 @@ __global__ void __launch_bounds__(256, 3) k_project(
         R[2][2] = 1.0 - 2.0 * (qxr * qxr + qyr * qyr);
 
         // R5: lambda1 of Sigma_perp = [u v]^T Sigma [u v], basis-free form
-        const double dx = mx / D, dy = my / D, dz = mz / D;
+        const double invD = 1.0 / D;
+        const double dx = mx * invD, dy = my * invD, dz = mz * invD;
         double w[3], s2[3], s[3];
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
@@ -81,13 +82,13 @@ __global__ void __launch_bounds__(256, 3) k_project(
         }
         const double tr = (s2[0] * (1.0 - w[0] * w[0]) + s2[1] * (1.0 - w[1] * w[1])) +
                           s2[2] * (1.0 - w[2] * w[2]);
-        const double det = ((s2[0] * s2[1]) * s2[2]) *
-                           (((w[0] * w[0]) / s2[0] + (w[1] * w[1]) / s2[1]) + (w[2] * w[2]) / s2[2]);
+        const double det = ((s2[1] * s2[2]) * (w[0] * w[0]) + (s2[0] * s2[2]) * (w[1] * w[1])) +
+                           (s2[0] * s2[1]) * (w[2] * w[2]);
         double disc = (tr * tr) * 0.25 - det;
         if (disc < 0.0) disc = 0.0;
         const double lam1 = tr * 0.5 + sqrt(disc);
         // rho = (rho_scale * (H + W)) / (2 pi) (Q5), the same IEEE double computed on the host
-        const double p1 = ((k_sigma * sqrt(lam1)) / D) * rho;
+        const double p1 = ((k_sigma * sqrt(lam1)) * invD) * rho;
 
         // R6: integer texel range of the closed square, clamped to [-W, 2W-1]
         double c0 = ceil(px - p1), c1 = floor(px + p1), r0 = ceil(py - p1), r1 = floor(py + p1);
@@ -116,9 +117,8 @@ __global__ void __launch_bounds__(256, 3) k_project(
             rec.c0 = (int16_t)c0; rec.c1 = (int16_t)c1; rec.r0 = (int16_t)r0; rec.r1 = (int16_t)r1;
             rec.di[0] = dx; rec.di[1] = dy; rec.di[2] = dz;
             // record fields (not part of the binning contract): reciprocal multiplies
-            double inv_s[3];
-#pragma unroll
-            for (int j = 0; j < 3; ++j) inv_s[j] = 1.0 / s[j];
+            const double inv_all = 1.0 / ((s[0] * s[1]) * s[2]);  // one division for the three 1/s_j
+            const double inv_s[3] = {(s[1] * s[2]) * inv_all, (s[0] * s[2]) * inv_all, (s[0] * s[1]) * inv_all};
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
                 rec.g[j] = (float)(w[j] * inv_s[j]);  // g = W d_i = diag(1/s) R^T d_i
@@ -133,9 +133,10 @@ __global__ void __launch_bounds__(256, 3) k_project(
             rec.kD = kD;
             rec.eD = (float)((kD + 0.5) * dt - D);
             // Eq.5 with the clamp of Q16; times sqrt(pi/2) from Eq.3's prefactor
-            double alpha = (double)opacities[i];
-            alpha = alpha < 1e-4 ? 1e-4 : (alpha > 1.0 - 1e-4 ? 1.0 - 1e-4 : alpha);
-            const double tau_star = -log1p(-alpha);
+            // tau* in fp32 (log1pf: no fp64 table lookups; betap is stored in fp32)
+            float alpha = opacities[i];
+            alpha = alpha < 1e-4f ? 1e-4f : (alpha > 1.0f - 1e-4f ? 1.0f - 1e-4f : alpha);
+            const double tau_star = (double)(-log1pf(-alpha));
             const double trA = inv_s[0] * inv_s[0] + inv_s[1] * inv_s[1] + inv_s[2] * inv_s[2];
             // beta * sqrt(pi/2) for the chosen alpha -> beta mapping (ablation B)
             double betap;
