@@ -14,7 +14,7 @@ constexpr double kPi = 3.141592653589793;
 
 __device__ __forceinline__ double sgn_pos(double x) { return x >= 0.0 ? 1.0 : -1.0; }  // sgn(0)=+1 (Q4)
 
-__global__ void __launch_bounds__(256, 3) k_project(
+__global__ void __launch_bounds__(256, 4) k_project(
     const float* __restrict__ means, const float* __restrict__ scales,
     const float* __restrict__ rotations, const float* __restrict__ opacities, int64_t n, int64_t i0, int64_t cnt,
     LightsParam lp, int n_lights, int res, int K, double kappa, double k_sigma, double rho,
