@@ -253,6 +253,58 @@ __device__ __forceinline__ void pair_live(const PairTest& p, float D, float eD, 
 
 // kStats: count the work (live pairs, window shells, steps) for the benchmark's
 // roofline accounting; the timed path is <false>.
+// The same live path executed by the whole warp when any lane is live
+// (uniform branch, straight-line body): lanes that are not live compute and
+// discard.  The first two window shells are evaluated unconditionally (two
+// independent erf chains), further shells in a rarely taken loop.
+template <bool kStats>
+__device__ __forceinline__ void pair_live_warp(const PairTest& p, bool live, float D, float eD, float betap, int kD,
+                                               float* s_acc, int tid, int K, float dt, float dtlo, float idt,
+                                               uint32_t& st_live, uint32_t& st_win, uint32_t& st_step) {
+    const float ia = rcp_approx(p.a);
+    const float r_over_D2 = p.ia * ia;
+    const float rr = r_over_D2 * D * D;
+    const float sD = -D * fmaf(p.ux, p.wx, fmaf(p.uy, p.wy, p.uz * p.wz)) * ia;
+    const float ra = rsqrt_approx(p.a);
+    const float h = 0.70710678118654752f * p.a * ra;
+    const float x0 = -h * (D + sD);
+    float e0 = -1.0f;
+    if (x0 > -kXS) e0 = erf_fast(x0);
+    live = live && e0 < 1.0f;
+    if (kStats) st_live += live;
+    const float pref = betap * ra * ex2_approx(-0.72134752044448170f * rr);
+    const float e = eD - sD;
+    const float xsh = (kXS * 1.41421356237309505f) * ra;
+    const float kf_lo = fmaf(-xsh - e, idt, (float)kD);
+    const float kf_hi = fmaf(xsh - e, idt, (float)kD);
+    const int klo = (int)ceilf(fminf(fmaxf(kf_lo, 0.0f), (float)K));
+    const int khi = max((int)ceilf(fminf(fmaxf(kf_hi, 0.0f), (float)K)), klo);
+    const int n = live ? khi - klo : 0;
+    if (kStats) { st_win += (uint32_t)n; st_step += (live && khi < K) ? 1u : 0u; }
+    float fk = (float)(klo - kD);
+    float* ap = s_acc + klo * kThreads + tid;
+    const float tk1 = fmaf(fk, dt, fmaf(fk, dtlo, e));
+    const float fk2 = fk + 1.0f;
+    const float tk2 = fmaf(fk2, dt, fmaf(fk2, dtlo, e));
+    const float w1 = pref * (erf_fast(h * tk1) - e0);
+    const float w2 = pref * (erf_fast(h * tk2) - e0);
+    float prev = 0.0f;
+    if (n >= 1) { ap[0] += w1; prev = w1; }
+    if (n >= 2) { ap[kThreads] += w2 - w1; prev = w2; }
+    if (__any_sync(0xffffffffu, n > 2)) {
+        fk += 2.0f;
+        ap += 2 * kThreads;
+#pragma unroll 1
+        for (int i = 2; i < n; ++i, fk += 1.0f, ap += kThreads) {
+            const float tk = fmaf(fk, dt, fmaf(fk, dtlo, e));
+            const float w = pref * (erf_fast(h * tk) - e0);
+            *ap += w - prev;
+            prev = w;
+        }
+    }
+    if (live && khi < K) s_acc[khi * kThreads + tid] += fmaf(pref, 1.0f - e0, -prev);
+}
+
 template <bool kStats>
 __global__ void __launch_bounds__(kThreads) k_accumulate(
     const WorkUnit* __restrict__ units, const uint32_t* __restrict__ n_units_dev,
@@ -358,8 +410,12 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
                     my_live += (uint32_t)T2.A.live + (uint32_t)T2.B.live;
                     st_wany += (ba != 0u) + (bb != 0u);
                 }
-                if (T2.A.live) pair_live<kStats>(T2.A, T2.DA, T2.eDA, T2.bpA, T2.kDA, s_acc, tid, K, dt, dtlo, idt, st_live, st_win, st_step);
-                if (T2.B.live) pair_live<kStats>(T2.B, T2.DB, T2.eDB, T2.bpB, T2.kDB, s_acc, tid, K, dt, dtlo, idt, st_live, st_win, st_step);
+                if (__any_sync(0xffffffffu, T2.A.live))
+                    pair_live_warp<kStats>(T2.A, T2.A.live, T2.DA, T2.eDA, T2.bpA, T2.kDA, s_acc, tid, K, dt, dtlo,
+                                           idt, st_live, st_win, st_step);
+                if (__any_sync(0xffffffffu, T2.B.live))
+                    pair_live_warp<kStats>(T2.B, T2.B.live, T2.DB, T2.eDB, T2.bpB, T2.kDB, s_acc, tid, K, dt, dtlo,
+                                           idt, st_live, st_win, st_step);
             }
             if (kStats) st_wmax += __reduce_max_sync(0xffffffffu, my_live);
             cta_sync();  // compact copy consumed
