@@ -284,18 +284,14 @@ __device__ __forceinline__ void pair_live_warp(const PairTest& p, bool live, flo
     float fk = (float)(klo - kD);
     float* ap = s_acc + klo * kThreads + tid;
     const float tk1 = fmaf(fk, dt, fmaf(fk, dtlo, e));
-    const float fk2 = fk + 1.0f;
-    const float tk2 = fmaf(fk2, dt, fmaf(fk2, dtlo, e));
     const float w1 = pref * (erf_fast(h * tk1) - e0);
-    const float w2 = pref * (erf_fast(h * tk2) - e0);
     float prev = 0.0f;
     if (n >= 1) { ap[0] += w1; prev = w1; }
-    if (n >= 2) { ap[kThreads] += w2 - w1; prev = w2; }
-    if (__any_sync(0xffffffffu, n > 2)) {
-        fk += 2.0f;
-        ap += 2 * kThreads;
+    if (__any_sync(0xffffffffu, n > 1)) {
+        fk += 1.0f;
+        ap += kThreads;
 #pragma unroll 1
-        for (int i = 2; i < n; ++i, fk += 1.0f, ap += kThreads) {
+        for (int i = 1; i < n; ++i, fk += 1.0f, ap += kThreads) {
             const float tk = fmaf(fk, dt, fmaf(fk, dtlo, e));
             const float w = pref * (erf_fast(h * tk) - e0);
             *ap += w - prev;
