@@ -269,7 +269,10 @@ __device__ __forceinline__ void pair_live_warp(const PairTest& p, bool live, flo
     const float h = 0.70710678118654752f * p.a * ra;
     const float x0 = -h * (D + sD);
     float e0 = -1.0f;
-    if (x0 > -kXS) e0 = erf_fast(x0);
+    if (__any_sync(0xffffffffu, x0 > -kXS)) {  // a Gaussian near the light (rare): uniform branch
+        const float t = erf_fast(x0);
+        if (x0 > -kXS) e0 = t;
+    }
     live = live && e0 < 1.0f;
     if (kStats) st_live += live;
     const float pref = betap * ra * ex2_approx(-0.72134752044448170f * rr);
