@@ -38,7 +38,6 @@ __device__ __forceinline__ void cta_sync() {
     if (kThreads == 32) __syncwarp(); else __syncthreads();
 }
 constexpr float kXS = 3.92f;      // |x| >= kXS  ->  erf_fast(x) == +-1 exactly
-constexpr float kRCut = 180.0f;   // r > kRCut -> ex2.approx.ftz(-r/(2 ln 2)) == 0 exactly
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -377,17 +376,8 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
             if ((uint32_t)tid < nb) {  // transform: raw record -> compact, relative to d_c
                 const PairRec& R = s_raw[tid];
                 float* q = reinterpret_cast<float*>(s_cr) + (tid >> 1) * (2 * kPairFields) + (tid & 1);
-                // negligible-pair cut (R8'): a pair contributes at most
-                // 2 pref <= 2 betap s_max exp(-r/2) to any tau_k (1/sqrt(a) <= s_max);
-                // skip it when that bound is < 2^-32, i.e. r > r_cut; never above 180
-                // (beyond which exp(-r/2) is exactly 0 in fp32 anyway).
-                const float w0 = R.W[0] * R.W[0] + R.W[1] * R.W[1] + R.W[2] * R.W[2];  // 1/s_0^2
-                const float w1 = R.W[3] * R.W[3] + R.W[4] * R.W[4] + R.W[5] * R.W[5];
-                const float w2 = R.W[6] * R.W[6] + R.W[7] * R.W[7] + R.W[8] * R.W[8];
-                const float smax = rsqrtf(fminf(w0, fminf(w1, w2)));
-                const float rcut = fminf(2.0f * logf(2.0f * R.betap * smax) + 44.3614195558365f, kRCut);
                 float v[kPairFields] = {(float)(R.di[0] - c0), (float)(R.di[1] - c1), (float)(R.di[2] - c2),
-                                        rcut / (R.D * R.D), R.g[0], R.g[1], R.g[2], R.D,
+                                        R.rcut_D2, R.g[0], R.g[1], R.g[2], R.D,
                                         R.W[0], R.W[1], R.W[2], R.W[3], R.W[4], R.W[5], R.W[6], R.W[7], R.W[8],
                                         R.eD, R.betap, __int_as_float(R.kD)};
 #pragma unroll

@@ -23,7 +23,8 @@ struct __align__(16) PairRec {
     float eD;         // t_{kD} - D (fp64 -> fp32), anchors the shell arguments
     int32_t kD;       // anchor shell
     float betap;      // beta * sqrt(pi/2) = kappa tau* sqrt(tr A / 3) / 2  (Eq.3 x Eq.5)
-    int16_t c0, c1, r0, r1;  // clamped integer texel range of the footprint square (R6)
+    float rcut_D2;    // negligible-pair bound r_cut / D^2 (R8', per Gaussian-light)
+    float pad;
 };
 static_assert(sizeof(PairRec) == 96, "PairRec must be 96 B");
 

@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(256, 4) k_project(
     const double D = sqrt((mx * mx + my * my) + mz * mz);
     uint32_t tcnt = 0;
     PairRec rec;
-    rec.c0 = 1; rec.c1 = 0; rec.r0 = 1; rec.r1 = 0;
+    int16_t rc0 = 1, rc1 = 0, rr0 = 1, rr1 = 0;  // packed footprint rect of the dup record
     if (D > 1e-6) {
         // footprint centre: octahedral encode psi(m) -> texel coords (pixel centres, Q3)
         const double inv1 = 1.0 / ((fabs(mx) + fabs(my)) + fabs(mz));  // contract v2: one division
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(256, 4) k_project(
         }
 
         if (tcnt > 0) {
-            rec.c0 = (int16_t)c0; rec.c1 = (int16_t)c1; rec.r0 = (int16_t)r0; rec.r1 = (int16_t)r1;
+            rc0 = (int16_t)c0; rc1 = (int16_t)c1; rr0 = (int16_t)r0; rr1 = (int16_t)r1;
             rec.di[0] = dx; rec.di[1] = dy; rec.di[2] = dz;
             // record fields (not part of the binning contract): reciprocal multiplies
             const double inv_all = 1.0 / ((s[0] * s[1]) * s[2]);  // one division for the three 1/s_j
@@ -144,14 +144,27 @@ __global__ void __launch_bounds__(256, 4) k_project(
             else if (absorption == DGSM_ABS_TRACEAVG) betap = kappa * tau_star * sqrt(trA / 3.0) * 0.5;
             else betap = kappa * tau_star * (inv_s[0] * inv_s[1] * inv_s[2]) * (1.0 / (4.0 * kPi));  // MASS, DIAG
             rec.betap = (float)betap;
+            // negligible-pair cut (R8'): a pair contributes at most 2 pref <=
+            // 2 betap s_max exp(-r/2) to any tau_k (1/sqrt(a) <= s_max); it is skipped
+            // when that bound is < 2^-32, i.e. r > r_cut, never above 180 (beyond which
+            // exp(-r/2) is exactly 0 in fp32).  fp32, from the stored fp32 W rows.
+            {
+                const float w0 = rec.W[0] * rec.W[0] + rec.W[1] * rec.W[1] + rec.W[2] * rec.W[2];  // 1/s_0^2
+                const float w1 = rec.W[3] * rec.W[3] + rec.W[4] * rec.W[4] + rec.W[5] * rec.W[5];
+                const float w2 = rec.W[6] * rec.W[6] + rec.W[7] * rec.W[7] + rec.W[8] * rec.W[8];
+                const float smax = rsqrtf(fminf(w0, fminf(w1, w2)));
+                const float rcut = fminf(2.0f * logf(2.0f * rec.betap * smax) + 44.3614195558365f, 180.0f);
+                rec.rcut_D2 = rcut / (Df * Df);
+            }
+            rec.pad = 0.0f;
             dbits = __float_as_uint(Df);
         }
     }
     if (active) {
         counts[oi] = tcnt;
         recs[oi] = rec;
-        dup[oi] = make_uint4(dbits, (uint32_t)(uint16_t)rec.c0 | ((uint32_t)(uint16_t)rec.c1 << 16),
-                              (uint32_t)(uint16_t)rec.r0 | ((uint32_t)(uint16_t)rec.r1 << 16), tcnt);
+        dup[oi] = make_uint4(dbits, (uint32_t)(uint16_t)rc0 | ((uint32_t)(uint16_t)rc1 << 16),
+                              (uint32_t)(uint16_t)rr0 | ((uint32_t)(uint16_t)rr1 << 16), tcnt);
     }
     // per-light min/max of the depth key over binned Gaussians: shared-memory
     // atomics per block, one global atomic per (block, light)
