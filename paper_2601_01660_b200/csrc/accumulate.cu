@@ -136,6 +136,14 @@ struct AccLights {
 // tile reference direction d_c, stored interleaved by record pairs (below).
 constexpr int kCompact = 5;  // float4 per record
 
+// s_acc read-modify-write through a 32-bit shared address (the generic pointer
+// form had the shared window base recomputed on every use)
+__device__ __forceinline__ void acc_add(uint32_t a, float v) {
+    float x;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(a) : "memory");
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(x + v) : "memory");
+}
+
 // ---- per (texel, Gaussian) pair ---------------------------------------------
 // delta-formulation (R9) of one (texel, record) pair up to the negligible-pair
 // test (R8'): W delta, u = g + W delta, a = |u|^2, and |g x W delta|^2 (in `ia`
@@ -258,7 +266,7 @@ __device__ __forceinline__ void pair_live(const PairTest& p, float D, float eD, 
 // independent erf chains), further shells in a rarely taken loop.
 template <bool kStats>
 __device__ __forceinline__ void pair_live_warp(const PairTest& p, bool live, float D, float eD, float betap, int kD,
-                                               float* s_acc, int tid, int K, float dt, float dtlo, float idt,
+                                               uint32_t acc_base, int K, float dt, float dtlo, float idt,
                                                uint32_t& st_live, uint32_t& st_win, uint32_t& st_step) {
     const float ia = rcp_approx(p.a);
     const float r_over_D2 = p.ia * ia;
@@ -284,23 +292,23 @@ __device__ __forceinline__ void pair_live_warp(const PairTest& p, bool live, flo
     const int n = live ? khi - klo : 0;
     if (kStats) { st_win += (uint32_t)n; st_step += (live && khi < K) ? 1u : 0u; }
     float fk = (float)(klo - kD);
-    float* ap = s_acc + klo * kThreads + tid;
+    uint32_t ap = acc_base + (uint32_t)klo * (kThreads * 4);
     const float tk1 = fmaf(fk, dt, fmaf(fk, dtlo, e));
     const float w1 = pref * (erf_fast(h * tk1) - e0);
     float prev = 0.0f;
-    if (n >= 1) { ap[0] += w1; prev = w1; }
+    if (n >= 1) { acc_add(ap, w1); prev = w1; }
     if (__any_sync(0xffffffffu, n > 1)) {
         fk += 1.0f;
-        ap += kThreads;
+        ap += kThreads * 4;
 #pragma unroll 1
-        for (int i = 1; i < n; ++i, fk += 1.0f, ap += kThreads) {
+        for (int i = 1; i < n; ++i, fk += 1.0f, ap += kThreads * 4) {
             const float tk = fmaf(fk, dt, fmaf(fk, dtlo, e));
             const float w = pref * (erf_fast(h * tk) - e0);
-            *ap += w - prev;
+            acc_add(ap, w - prev);
             prev = w;
         }
     }
-    if (live && khi < K) s_acc[khi * kThreads + tid] += fmaf(pref, 1.0f - e0, -prev);
+    if (live && khi < K) acc_add(acc_base + (uint32_t)khi * (kThreads * 4), fmaf(pref, 1.0f - e0, -prev));
 }
 
 template <bool kStats>
@@ -351,6 +359,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
         const float etx = (float)(t0 - c0), ety = (float)(t1 - c1), etz = (float)(t2 - c2);
         const f2_t ETX = f2pack(etx, etx), ETY = f2pack(ety, ety), ETZ = f2pack(etz, etz);
         for (int k = 0; k < K; ++k) s_acc[k * kThreads + tid] = 0.0f;
+        const uint32_t acc_base = smem_addr(s_acc) + 4u * (uint32_t)tid;  // &s_acc[0][tid]
         uint32_t st_live = 0, st_win = 0, st_step = 0, st_wany = 0, st_wmax = 0;
 
         const float dt = al.dt[l], dtlo = al.dtlo[l], idt = al.idt[l];
@@ -400,10 +409,10 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
                     st_wany += (ba != 0u) + (bb != 0u);
                 }
                 if (__any_sync(0xffffffffu, T2.A.live))
-                    pair_live_warp<kStats>(T2.A, T2.A.live, T2.DA, T2.eDA, T2.bpA, T2.kDA, s_acc, tid, K, dt, dtlo,
+                    pair_live_warp<kStats>(T2.A, T2.A.live, T2.DA, T2.eDA, T2.bpA, T2.kDA, acc_base, K, dt, dtlo,
                                            idt, st_live, st_win, st_step);
                 if (__any_sync(0xffffffffu, T2.B.live))
-                    pair_live_warp<kStats>(T2.B, T2.B.live, T2.DB, T2.eDB, T2.bpB, T2.kDB, s_acc, tid, K, dt, dtlo,
+                    pair_live_warp<kStats>(T2.B, T2.B.live, T2.DB, T2.eDB, T2.bpB, T2.kDB, acc_base, K, dt, dtlo,
                                            idt, st_live, st_win, st_step);
             }
             if (kStats) st_wmax += __reduce_max_sync(0xffffffffu, my_live);
