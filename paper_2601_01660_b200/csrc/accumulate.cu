@@ -180,9 +180,10 @@ constexpr int kPairFields = 20;
 constexpr int kPairBytes = kPairFields * 8;
 
 struct PairTest2 {
-    PairTest A, B;
-    float DA, DB, eDA, eDB, bpA, bpB;
+    f2_t A, C2, DOT;      // a = |u|^2, |g x W delta|^2, u . W delta  (records A | B)
+    f2_t D, ED, BP;       // D, e_D, beta sqrt(pi/2)
     int kDA, kDB;
+    bool liveA, liveB;
 };
 
 __device__ __forceinline__ PairTest2 pair_test2(uint32_t addr, f2_t ETX, f2_t ETY, f2_t ETZ) {
@@ -203,77 +204,30 @@ __device__ __forceinline__ PairTest2 pair_test2(uint32_t addr, f2_t ETX, f2_t ET
     const f2_t C2 = f2fma(CX, CX, f2fma(CY, CY, f2mul(CZ, CZ)));
     const f2_t T = f2mul(F[3], A);  // live  <=>  |g x W delta|^2 <= (r_cut/D^2) a
     PairTest2 R;
-    R.A.wx = f2lo(WX); R.A.wy = f2lo(WY); R.A.wz = f2lo(WZ);
-    R.A.ux = f2lo(UX); R.A.uy = f2lo(UY); R.A.uz = f2lo(UZ);
-    R.A.a = f2lo(A); R.A.ia = f2lo(C2);  // ia holds |c|^2 until the live path
-    R.A.live = f2lo(C2) <= f2lo(T);
-    R.B.wx = f2hi(WX); R.B.wy = f2hi(WY); R.B.wz = f2hi(WZ);
-    R.B.ux = f2hi(UX); R.B.uy = f2hi(UY); R.B.uz = f2hi(UZ);
-    R.B.a = f2hi(A); R.B.ia = f2hi(C2);
-    R.B.live = f2hi(C2) <= f2hi(T);
-    R.DA = f2lo(F[7]); R.DB = f2hi(F[7]);
-    R.eDA = f2lo(F[17]); R.eDB = f2hi(F[17]);
-    R.bpA = f2lo(F[18]); R.bpB = f2hi(F[18]);
+    R.A = A;
+    R.C2 = C2;
+    R.DOT = f2fma(UX, WX, f2fma(UY, WY, f2mul(UZ, WZ)));  // u . W delta (closest approach)
+    R.D = F[7]; R.ED = F[17]; R.BP = F[18];
     R.kDA = __float_as_int(f2lo(F[19])); R.kDB = __float_as_int(f2hi(F[19]));
+    R.liveA = f2lo(C2) <= f2lo(T);
+    R.liveB = f2hi(C2) <= f2hi(T);
     return R;
 }
 
-// Eq.3 over the shells for a live pair: window shells (|x_k| < kXS) as differences,
-// then the saturated step pref (1 - erf(x_0)) at the first saturated shell.
-template <bool kStats>
-__device__ __forceinline__ void pair_live(const PairTest& p, float D, float eD, float betap, int kD, float* s_acc,
-                                          int tid, int K, float dt, float dtlo, float idt, uint32_t& st_live,
-                                          uint32_t& st_win, uint32_t& st_step) {
-    const float ia = rcp_approx(p.a);
-    const float r_over_D2 = p.ia * ia;  // p.ia carries |g x W delta|^2 from the test
-    const float rr = r_over_D2 * D * D;
-    // s* - D = -D (u . W delta)/a: closest approach relative to D
-    const float sD = -D * fmaf(p.ux, p.wx, fmaf(p.uy, p.wy, p.uz * p.wz)) * ia;
-    const float ra = rsqrt_approx(p.a);
-    const float h = 0.70710678118654752f * p.a * ra;  // sqrt(a/2)
-    const float x0 = -h * (D + sD);                      // sqrt(a/2) * (b/a) of Eq.3
-    const float e0 = x0 <= -kXS ? -1.0f : erf_fast(x0);
-    if (e0 >= 1.0f) return;  // whole Gaussian behind the light
-    if (kStats) ++st_live;
-    // Eq.3 prefactor beta sqrt(pi/(2a)) exp(-(c - b^2/a)/2)
-    const float pref = betap * ra * ex2_approx(-0.72134752044448170f * rr);
-    // t_k - s* = (k - kD) dt + e ; window |x_k| < kXS <=> |t_k - s*| < kXS / h
-    const float e = eD - sD;
-    const float xsh = (kXS * 1.41421356237309505f) * ra;  // kXS / h
-    const float kf_lo = fmaf(-xsh - e, idt, (float)kD);   // x_k <= -kXS for k <= kf_lo
-    const float kf_hi = fmaf(xsh - e, idt, (float)kD);    // x_k >= +kXS for k >= kf_hi
-    const int klo = (int)ceilf(fminf(fmaxf(kf_lo, 0.0f), (float)K));
-    const int khi = max((int)ceilf(fminf(fmaxf(kf_hi, 0.0f), (float)K)), klo);
-    if (kStats) { st_win += (uint32_t)(khi - klo); st_step += khi < K ? 1u : 0u; }
-    float prev = 0.0f;
-    float fk = (float)(klo - kD);  // k - kD, exact in fp32
-    float* ap = s_acc + klo * kThreads + tid;
-#pragma unroll 1
-    for (int k = klo; k < khi; ++k, fk += 1.0f, ap += kThreads) {
-        const float tk = fmaf(fk, dt, fmaf(fk, dtlo, e));
-        const float w = pref * (erf_fast(h * tk) - e0);
-        *ap += w - prev;
-        prev = w;
-    }
-    if (khi < K) s_acc[khi * kThreads + tid] += fmaf(pref, 1.0f - e0, -prev);
-}
-
-// kStats: count the work (live pairs, window shells, steps) for the benchmark's
-// roofline accounting; the timed path is <false>.
 // The same live path executed by the whole warp when any lane is live
 // (uniform branch, straight-line body): lanes that are not live compute and
 // discard.  The first two window shells are evaluated unconditionally (two
 // independent erf chains), further shells in a rarely taken loop.
 template <bool kStats>
-__device__ __forceinline__ void pair_live_warp(const PairTest& p, bool live, float D, float eD, float betap, int kD,
-                                               uint32_t acc_base, int K, float dt, float dtlo, float idt,
+__device__ __forceinline__ void pair_live_warp(float pa, float pc2, float pdot, bool live, float D, float eD,
+                                               float betap, int kD, uint32_t acc_base, int K, float dt, float dtlo, float idt,
                                                uint32_t& st_live, uint32_t& st_win, uint32_t& st_step) {
-    const float ia = rcp_approx(p.a);
-    const float r_over_D2 = p.ia * ia;
+    const float ia = rcp_approx(pa);
+    const float r_over_D2 = pc2 * ia;
     const float rr = r_over_D2 * D * D;
-    const float sD = -D * fmaf(p.ux, p.wx, fmaf(p.uy, p.wy, p.uz * p.wz)) * ia;
-    const float ra = rsqrt_approx(p.a);
-    const float h = 0.70710678118654752f * p.a * ra;
+    const float sD = -D * pdot * ia;
+    const float ra = rsqrt_approx(pa);
+    const float h = 0.70710678118654752f * pa * ra;
     const float x0 = -h * (D + sD);
     float e0 = -1.0f;
     if (__any_sync(0xffffffffu, x0 > -kXS)) {  // a Gaussian near the light (rare): uniform branch
@@ -309,6 +263,97 @@ __device__ __forceinline__ void pair_live_warp(const PairTest& p, bool live, flo
         }
     }
     if (live && khi < K) acc_add(acc_base + (uint32_t)khi * (kThreads * 4), fmaf(pref, 1.0f - e0, -prev));
+}
+
+__device__ __forceinline__ f2_t f2bc(float x) { return f2pack(x, x); }
+
+// erf_fast of both halves: the polynomial on the paired pipe, clamp/select and
+// the MUFU ex2 per half
+__device__ __forceinline__ f2_t erf_fast2(f2_t X) {
+    const float xa = f2lo(X), xb = f2hi(X);
+    const float ta = fminf(fabsf(xa), kXS), tb = fminf(fabsf(xb), kXS);
+    const f2_t Tt = f2pack(ta, tb);
+    f2_t q = f2bc(1.063312357e-05f);
+    q = f2fma(q, Tt, f2bc(-1.446070382e-04f));
+    q = f2fma(q, Tt, f2bc(8.202550816e-04f));
+    q = f2fma(q, Tt, f2bc(-2.228778088e-03f));
+    q = f2fma(q, Tt, f2bc(4.658136095e-05f));
+    q = f2fma(q, Tt, f2bc(2.773877792e-02f));
+    q = f2fma(q, Tt, f2bc(-1.483091265e-01f));
+    q = f2fma(q, Tt, f2bc(-9.184432626e-01f));
+    q = f2fma(q, Tt, f2bc(-1.627907276e+00f));
+    q = f2fma(q, Tt, f2bc(4.901340445e-10f));
+    const float qa = ta >= kXS ? -256.0f : f2lo(q), qb = tb >= kXS ? -256.0f : f2hi(q);
+    return f2pack(copysignf(1.0f - ex2_approx(qa), xa), copysignf(1.0f - ex2_approx(qb), xb));
+}
+
+// Window + step of one record after the shared setup (scalar: the rare longer
+// windows and the ordered shared-memory updates).
+template <bool kStats>
+__device__ __forceinline__ void live_finish(bool live, int klo, int khi, float fk, float w1, float pref, float h,
+                                            float e, float e0, uint32_t acc_base, int K, float dt, float dtlo,
+                                            uint32_t& st_live, uint32_t& st_win, uint32_t& st_step) {
+    const int n = live ? khi - klo : 0;
+    if (kStats) { st_live += live; st_win += (uint32_t)n; st_step += (live && khi < K) ? 1u : 0u; }
+    uint32_t ap = acc_base + (uint32_t)klo * (kThreads * 4);
+    float prev = 0.0f;
+    if (n >= 1) { acc_add(ap, w1); prev = w1; }
+    if (__any_sync(0xffffffffu, n > 1)) {
+        fk += 1.0f;
+        ap += kThreads * 4;
+#pragma unroll 1
+        for (int i = 1; i < n; ++i, fk += 1.0f, ap += kThreads * 4) {
+            const float tk = fmaf(fk, dt, fmaf(fk, dtlo, e));
+            const float w = pref * (erf_fast(h * tk) - e0);
+            acc_add(ap, w - prev);
+            prev = w;
+        }
+    }
+    if (live && khi < K) acc_add(acc_base + (uint32_t)khi * (kThreads * 4), fmaf(pref, 1.0f - e0, -prev));
+}
+
+// Both records of the pair have a live lane in this warp: the setup and the
+// first window shell of both on the paired-FP32 pipe, then the per-record
+// updates in record order (A before B: the summation order of the scalar path).
+template <bool kStats>
+__device__ __forceinline__ void pair_live_warp2(const PairTest2& T, uint32_t acc_base, int K, float dt, float dtlo,
+                                                float idt, uint32_t& st_live, uint32_t& st_win, uint32_t& st_step) {
+    const f2_t Z = 0ull;
+    const float aA = f2lo(T.A), aB = f2hi(T.A);
+    const f2_t IA = f2pack(rcp_approx(aA), rcp_approx(aB));
+    const f2_t RA = f2pack(rsqrt_approx(aA), rsqrt_approx(aB));
+    const f2_t RR = f2mul(f2mul(f2mul(T.C2, IA), T.D), T.D);
+    const f2_t SD = f2mul(f2mul(f2sub(Z, T.D), T.DOT), IA);
+    const f2_t H = f2mul(f2mul(f2bc(0.70710678118654752f), T.A), RA);
+    const f2_t X0 = f2mul(f2sub(Z, H), f2add(T.D, SD));
+    float e0A = -1.0f, e0B = -1.0f;
+    const float x0A = f2lo(X0), x0B = f2hi(X0);
+    if (__any_sync(0xffffffffu, x0A > -kXS || x0B > -kXS)) {
+        const float ta = erf_fast(x0A), tb = erf_fast(x0B);
+        if (x0A > -kXS) e0A = ta;
+        if (x0B > -kXS) e0B = tb;
+    }
+    const bool liveA = T.liveA && e0A < 1.0f, liveB = T.liveB && e0B < 1.0f;
+    const f2_t E0 = f2pack(e0A, e0B);
+    const f2_t M = f2mul(f2bc(-0.72134752044448170f), RR);
+    const f2_t PREF = f2mul(f2mul(T.BP, RA), f2pack(ex2_approx(f2lo(M)), ex2_approx(f2hi(M))));
+    const f2_t E = f2sub(T.ED, SD);
+    const f2_t XSH = f2mul(f2bc(kXS * 1.41421356237309505f), RA);
+    const f2_t KD = f2pack((float)T.kDA, (float)T.kDB);
+    const f2_t KLO = f2fma(f2sub(f2sub(Z, XSH), E), f2bc(idt), KD);
+    const f2_t KHI = f2fma(f2sub(XSH, E), f2bc(idt), KD);
+    const float fK = (float)K;
+    const int kloA = (int)ceilf(fminf(fmaxf(f2lo(KLO), 0.0f), fK));
+    const int kloB = (int)ceilf(fminf(fmaxf(f2hi(KLO), 0.0f), fK));
+    const int khiA = max((int)ceilf(fminf(fmaxf(f2lo(KHI), 0.0f), fK)), kloA);
+    const int khiB = max((int)ceilf(fminf(fmaxf(f2hi(KHI), 0.0f), fK)), kloB);
+    const f2_t FK = f2pack((float)(kloA - T.kDA), (float)(kloB - T.kDB));
+    const f2_t TK1 = f2fma(FK, f2bc(dt), f2fma(FK, f2bc(dtlo), E));
+    const f2_t W1 = f2mul(PREF, f2sub(erf_fast2(f2mul(H, TK1)), E0));
+    live_finish<kStats>(liveA, kloA, khiA, f2lo(FK), f2lo(W1), f2lo(PREF), f2lo(H), f2lo(E), e0A, acc_base, K, dt,
+                        dtlo, st_live, st_win, st_step);
+    live_finish<kStats>(liveB, kloB, khiB, f2hi(FK), f2hi(W1), f2hi(PREF), f2hi(H), f2hi(E), e0B, acc_base, K, dt,
+                        dtlo, st_live, st_win, st_step);
 }
 
 template <bool kStats>
@@ -402,18 +447,23 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
             uint32_t pr_addr = smem_addr(s_cr);  // induction variable: record pair (r, r+1)
             for (uint32_t r = 0; r < nb; r += 2, pr_addr += kPairBytes) {
                 PairTest2 T2 = pair_test2(pr_addr, ETX, ETY, ETZ);
-                T2.B.live = T2.B.live && (r + 1 < nb);
+                T2.liveB = T2.liveB && (r + 1 < nb);
                 if (kStats) {
-                    const uint32_t ba = __ballot_sync(0xffffffffu, T2.A.live), bb = __ballot_sync(0xffffffffu, T2.B.live);
-                    my_live += (uint32_t)T2.A.live + (uint32_t)T2.B.live;
+                    const uint32_t ba = __ballot_sync(0xffffffffu, T2.liveA), bb = __ballot_sync(0xffffffffu, T2.liveB);
+                    my_live += (uint32_t)T2.liveA + (uint32_t)T2.liveB;
                     st_wany += (ba != 0u) + (bb != 0u);
                 }
-                if (__any_sync(0xffffffffu, T2.A.live))
-                    pair_live_warp<kStats>(T2.A, T2.A.live, T2.DA, T2.eDA, T2.bpA, T2.kDA, acc_base, K, dt, dtlo,
-                                           idt, st_live, st_win, st_step);
-                if (__any_sync(0xffffffffu, T2.B.live))
-                    pair_live_warp<kStats>(T2.B, T2.B.live, T2.DB, T2.eDB, T2.bpB, T2.kDB, acc_base, K, dt, dtlo,
-                                           idt, st_live, st_win, st_step);
+                const bool anyA = __any_sync(0xffffffffu, T2.liveA), anyB = __any_sync(0xffffffffu, T2.liveB);
+                if (anyA && anyB) {
+                    pair_live_warp2<kStats>(T2, acc_base, K, dt, dtlo, idt, st_live, st_win, st_step);
+                    continue;
+                }
+                if (anyA)
+                    pair_live_warp<kStats>(f2lo(T2.A), f2lo(T2.C2), f2lo(T2.DOT), T2.liveA, f2lo(T2.D), f2lo(T2.ED),
+                                           f2lo(T2.BP), T2.kDA, acc_base, K, dt, dtlo, idt, st_live, st_win, st_step);
+                if (anyB)
+                    pair_live_warp<kStats>(f2hi(T2.A), f2hi(T2.C2), f2hi(T2.DOT), T2.liveB, f2hi(T2.D), f2hi(T2.ED),
+                                           f2hi(T2.BP), T2.kDB, acc_base, K, dt, dtlo, idt, st_live, st_win, st_step);
             }
             if (kStats) st_wmax += __reduce_max_sync(0xffffffffu, my_live);
             cta_sync();  // compact copy consumed
