@@ -431,11 +431,14 @@ int dgsm_build(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_ligh
     dgsm_plan_t plan;
     int rc = dgsm_build_plan(g, lights, n_lights, atlas_res, n_shells, opts, ws, pb, &plan, stream);
     if (rc) return rc;
+    const int plan_launches = g_launches;
     const size_t need = pb + plan.run_workspace_bytes;
     if (ws_required) *ws_required = need;
     if (ws_bytes < need) return fail(DGSM_ENOSPC, "workspace %zu < %zu bytes", ws_bytes, need);
-    return dgsm_build_run(g, lights, n_lights, opts, &plan, ws, pb, (char*)ws + pb, ws_bytes - pb, atlas_out,
-                          stream);
+    rc = dgsm_build_run(g, lights, n_lights, opts, &plan, ws, pb, (char*)ws + pb, ws_bytes - pb, atlas_out,
+                        stream);
+    g_launches += plan_launches;
+    return rc;
 }
 
 // Upload pipeline depth of dgsm_frame_host (chunks of the Gaussian arrays).

@@ -309,6 +309,34 @@ class BuildPlan:
         return tuple(u32(o[:P]) for o in outs), (u32(ts), u32(te))
 
 
+class Builder:
+    """dgsm_build (plan + run in one C call, one host synchronisation inside)
+    with a device workspace kept across frames: the per-frame entry point of a
+    renderer (no Python between the plan's key count and the run's launches)."""
+
+    def __init__(self, lights, atlas_res: int, n_shells: int, opts: Optional[Options] = None, device="cuda"):
+        self.lights, self.n_lights = _lights(lights)
+        self.res, self.K = int(atlas_res), int(n_shells)
+        self.opts = opts or Options()
+        self._oc = self.opts.c()
+        self.device = torch.device(device)
+        self.ws = _alloc(0, self.device)
+
+    def __call__(self, gaussians, out: torch.Tensor, stream=None) -> torch.Tensor:
+        g, keep = _gaussians(gaussians)
+        need = C.c_size_t(0)
+        for _ in range(3):
+            rc = lib().dgsm_build(C.byref(g), self.lights, self.n_lights, self.res, self.K, C.byref(self._oc),
+                                  C.c_void_p(self.ws.data_ptr()), self.ws.numel(), C.byref(need),
+                                  C.c_void_p(out.data_ptr()), C.c_void_p(_stream_ptr(stream)))
+            if rc != 2:  # DGSM_ENOSPC: grow and retry
+                break
+            self.ws = _alloc(int(need.value * 1.25) + (1 << 20), self.device)
+        _check(rc, "dgsm_build")
+        self.launches = last_launch_count()
+        return out
+
+
 def build(gaussians: Dict[str, torch.Tensor], lights, atlas_res: int, n_shells: int,
           opts: Optional[Options] = None, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
     """DGSM build (§3.2): atlas [L, K, H, W] float32 of T = exp(-tau) (or tau)."""

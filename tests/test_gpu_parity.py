@@ -397,3 +397,15 @@ def test_sh_transfer_edge_cases(dg):
     assert torch.all(s == 4.0)
     s, c = dg.sh_transfer(A, 3, torch.zeros(0, 3, device="cuda"), torch.zeros(0, 3, device="cuda"))
     assert s.numel() == 0 and c.numel() == 0
+
+
+def test_builder_one_call_equals_plan_run(dg):
+    """dgsm_build (plan + run in one C call, workspace reused) == dgsm_build_plan + dgsm_build_run."""
+    s = synth.config1_seam("corner")
+    g = dg.to_device(s.gaussians)
+    out = torch.empty((s.L, s.K, s.res, s.res), device="cuda")
+    b = dg.Builder(s.lights, s.res, s.K)
+    for _ in range(2):
+        b(g, out)
+        assert torch.equal(out, dg.build(g, s.lights, s.res, s.K))
+    assert b.launches > 20
