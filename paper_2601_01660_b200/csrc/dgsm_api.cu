@@ -83,6 +83,7 @@ struct RunLayout {
     void* unit_scan_temp;
     WorkUnit *units, *units_tmp;
     uint32_t* counters;  // [0] n_units, [1] unit counter, [32..63] unit class histogram, [64..95] class fill
+    int64_t zero_words;  // counters .. tile_end, cleared by one memset per run
     uint32_t* tile_arrive;
     unsigned long long* stats;  // [4] pairs, live pairs, window shells, steps (DGSM_COLLECT_STATS)
     float* scratch;
@@ -111,8 +112,7 @@ RunLayout run_layout(void* ws, const dgsm_plan_t& pl) {
     r.offs_perm = c.take<uint64_t>(n + 1);
     r.gscan_temp = c.take<char>(scan_u32_to_u64_temp_bytes(n));
     r.sort_temp = c.take<char>(onesweep_temp_bytes(std::max<int64_t>(pmax, n)));
-    r.tile_start = c.take<uint32_t>(nt);
-    r.tile_end = c.take<uint32_t>(nt);
+
     r.unit_cnt = c.take<uint64_t>(nt);
     r.unit_off = c.take<uint64_t>(nt + 1);
     r.unit_scan_temp = c.take<char>(scan_u32_to_u64_temp_bytes(nt));
@@ -120,8 +120,12 @@ RunLayout run_layout(void* ws, const dgsm_plan_t& pl) {
     r.max_units = (uint32_t)max_units;
     r.units = c.take<WorkUnit>(max_units);
     r.units_tmp = c.take<WorkUnit>(max_units);
-    r.counters = c.take<uint32_t>(96);
-    r.tile_arrive = c.take<uint32_t>(kTileSplit * nt);
+    // zeroed together at the start of a run: counters, arrival counters, tile ranges
+    r.counters = c.take<uint32_t>(96 + kTileSplit * nt + 2 * nt);
+    r.tile_arrive = r.counters + 96;
+    r.tile_start = r.tile_arrive + kTileSplit * nt;
+    r.tile_end = r.tile_start + nt;
+    r.zero_words = 96 + (kTileSplit + 2) * nt;
     r.stats = c.take<unsigned long long>(8);
     const int64_t max_slots = kTileSplit * (2 * (P / pl.chunk) + 1);
     r.scratch = c.take<float>((size_t)max_slots * pl.n_shells * (kTexels / kTileSplit));
@@ -331,9 +335,7 @@ static void run_binning(const dgsm_gaussians_t* g, int n_lights, const dgsm_buil
     const int res = plan->atlas_res;
     const int64_t n = g->n;
     const int64_t n_tiles = (int64_t)(res / kTile) * (res / kTile);
-    const int64_t nt = n_lights * n_tiles;
-    cudaMemsetAsync(r.tile_start, 0, sizeof(uint32_t) * nt, s);
-    cudaMemsetAsync(r.tile_end, 0, sizeof(uint32_t) * nt, s);
+    // (tile ranges zeroed by the caller's run memset)
     for (int l = 0; l < n_lights; ++l) {
         const int64_t b = plan->light_key_begin[l], e = plan->light_key_begin[l + 1];
         if (e == b) continue;
@@ -380,11 +382,10 @@ int dgsm_build_run(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_
     const int res = plan->atlas_res, K = plan->n_shells;
     const int64_t nt = n_lights * (int64_t)(res / kTile) * (res / kTile);
 
+    cudaMemsetAsync(r.counters, 0, sizeof(uint32_t) * r.zero_words, s);
     run_binning(g, n_lights, o, plan, p, r, s);
-    cudaMemsetAsync(r.counters, 0, sizeof(uint32_t) * 96, s);
     launch_units(r.tile_start, r.tile_end, nt, plan->chunk, r.unit_cnt, r.unit_off, r.unit_scan_temp, r.units_tmp,
                  r.units, r.max_units, r.counters, r.counters + 32, r.counters + 64, s, &g_launches);
-    cudaMemsetAsync(r.tile_arrive, 0, sizeof(uint32_t) * kTileSplit * nt, s);
     if (o.flags & DGSM_COLLECT_STATS) cudaMemsetAsync(r.stats, 0, sizeof(unsigned long long) * 8, s);
     // a6: accumulate + exp
     launch_accumulate(r.units, r.counters, r.max_units, r.vals_a, p.recs, g->n, lp, n_lights, res, K, o.flags,
@@ -411,6 +412,7 @@ int dgsm_build_bins(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n
     const RunLayout r = run_layout(run_ws, *plan);
     const int res = plan->atlas_res;
     const int64_t nt = n_lights * (int64_t)(res / kTile) * (res / kTile);
+    cudaMemsetAsync(r.counters, 0, sizeof(uint32_t) * r.zero_words, s);
     run_binning(g, n_lights, o, plan, p, r, s);
     launch_decode_keys(r.keys_a, r.vals_a, p.dup, *plan, light_out, tile_out, depth_bits_out, index_out, s);
     g_launches += 1;

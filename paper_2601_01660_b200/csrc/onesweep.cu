@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ k
                                                       const uint32_t* __restrict__ vin,
                                                       KeyT* __restrict__ kout, uint32_t* __restrict__ vout,
                                                       int64_t n, int shift, const uint32_t* __restrict__ gofs,
-                                                      uint32_t* status, uint32_t* part_ctr) {
+                                                      uint32_t* status, uint32_t* status_next,
+                                                      uint32_t* part_ctr) {
     extern __shared__ __align__(16) unsigned char os_smem[];
     KeyT* s_keys = reinterpret_cast<KeyT*>(os_smem);
     uint32_t* s_vals = reinterpret_cast<uint32_t*>(os_smem + sizeof(KeyT) * kTileKeys);
@@ -107,6 +108,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ k
     for (int t = tid; t < (kThreads / 32) * kRadix; t += kThreads) (&s_warp_hist[0][0])[t] = 0;
     __syncthreads();
     const uint32_t part = s_part;
+    // clear this partition's row of the next pass's status buffer (double
+    // buffered: no memset between passes; kernel boundaries order it)
+    status_next[(size_t)part * kRadix + tid] = 0u;
     const int64_t base = (int64_t)part * kTileKeys + warp * (32 * kItems);
 
     KeyT k[kItems];
@@ -202,17 +206,18 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ k
 }
 
 struct OnesweepTemp {
-    uint32_t* hist;      // [kMaxPasses][256]
-    uint32_t* part_ctr;  // [kMaxPasses]
-    uint32_t* status;    // [parts][256]
+    uint32_t* hist;       // [kMaxPasses][256]
+    uint32_t* part_ctr;   // [kMaxPasses]
+    uint32_t* status[2];  // [parts][256] each, by pass parity
 };
 
-OnesweepTemp carve(void* temp) {
+OnesweepTemp carve(void* temp, int64_t parts) {
     OnesweepTemp t;
     char* p = (char*)temp;
     t.hist = (uint32_t*)p; p += sizeof(uint32_t) * kMaxPasses * kRadix;
     t.part_ctr = (uint32_t*)p; p += 256;
-    t.status = (uint32_t*)p;
+    t.status[0] = (uint32_t*)p; p += sizeof(uint32_t) * kRadix * (size_t)parts;
+    t.status[1] = (uint32_t*)p;
     return t;
 }
 
@@ -221,15 +226,17 @@ int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt
                   void* temp, cudaStream_t s, int* launches) {
     if (n <= 1 || nbits <= 0) return 0;
     const int passes = (nbits + 7) / 8;
-    OnesweepTemp t = carve(temp);
+    const int64_t parts = (n + kTileKeys - 1) / kTileKeys;
+    OnesweepTemp t = carve(temp, parts);
     static bool attr_set = false;
     const int dyn = (int)(sizeof(KeyT) + sizeof(uint32_t)) * kTileKeys;
     if (!attr_set) {
         cudaFuncSetAttribute(k_pass<KeyT>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
         attr_set = true;
     }
-    cudaMemsetAsync(t.hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix + 256, s);
-    const int64_t parts = (n + kTileKeys - 1) / kTileKeys;
+    // histograms, partition counters and the first pass's status in one memset
+    cudaMemsetAsync(t.hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix + 256 + sizeof(uint32_t) * kRadix * (size_t)parts,
+                    s);
     const int hist_grid = (int)std::min<int64_t>(148 * 4, (n + 2047) / 2048);
     k_hist<KeyT><<<hist_grid, 256, 0, s>>>(keys, n, passes, t.hist);
     k_hist_scan<<<passes, 256, 0, s>>>(t.hist);
@@ -238,9 +245,9 @@ int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt
     uint32_t *vi = vals, *vo = vals_alt;
     int flipped = 0;
     for (int p = 0; p < passes; ++p) {
-        cudaMemsetAsync(t.status, 0, sizeof(uint32_t) * kRadix * (size_t)parts, s);
         k_pass<KeyT><<<(unsigned)parts, kThreads, dyn, s>>>(ki, vi, ko, vo, n, 8 * p, t.hist + p * kRadix,
-                                                           t.status, t.part_ctr + p);
+                                                           t.status[p & 1], t.status[(p + 1) & 1],
+                                                           t.part_ctr + p);
         *launches += 1;
         KeyT* tk = ki; ki = ko; ko = tk;
         uint32_t* tv = vi; vi = vo; vo = tv;
@@ -252,7 +259,7 @@ int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt
 
 size_t onesweep_temp_bytes(int64_t n_max) {
     const int64_t parts = (n_max + kTileKeys - 1) / kTileKeys;
-    return sizeof(uint32_t) * kMaxPasses * kRadix + 256 + sizeof(uint32_t) * kRadix * (size_t)(parts + 1);
+    return sizeof(uint32_t) * kMaxPasses * kRadix + 256 + 2 * sizeof(uint32_t) * kRadix * (size_t)(parts + 1);
 }
 
 int launch_onesweep(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int64_t n,
