@@ -145,13 +145,8 @@ __device__ __forceinline__ void acc_add(uint32_t a, float v) {
 }
 
 // ---- per (texel, Gaussian) pair ---------------------------------------------
-// delta-formulation (R9) of one (texel, record) pair up to the negligible-pair
-// test (R8'): W delta, u = g + W delta, a = |u|^2, and |g x W delta|^2 (in `ia`
-// until the live path turns it into r/D^2 = |g x W delta|^2 / a).
-struct PairTest {
-    float wx, wy, wz, ux, uy, uz, a, ia;
-    bool live;
-};
+// delta-formulation (R9) of a (texel, record) pair up to the negligible-pair
+// test (R8'): W delta, u = g + W delta, a = |u|^2, |g x W delta|^2 and u . W delta.
 
 // ---- two records at once on the paired-FP32 pipe (sm_100 FFMA2/FADD2/FMUL2) --
 // A packed value holds record A (even) in the low half and record B (odd) in
@@ -553,8 +548,8 @@ void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint3
         al.idt[l] = (float)(1.0 / dt);
     }
     const size_t smem = accumulate_smem_bytes(K);
-    static int dev_cached = -1, n_sm = 0;
-    static size_t smem_set = 0;
+    thread_local int dev_cached = -1, n_sm = 0;  // per thread: a thread may switch devices
+    thread_local size_t smem_set = 0;
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev != dev_cached) {

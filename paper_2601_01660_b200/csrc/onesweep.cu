@@ -13,6 +13,8 @@
 // that depth order — an LSD radix sort whose low passes run on the
 // un-duplicated array.  Stability gives the order (tile, D bits, Gaussian index)
 // of DESIGN.md R7.
+#include <atomic>
+
 #include "dgsm_internal.cuh"
 
 namespace dgsm {
@@ -228,11 +230,15 @@ int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt
     const int passes = (nbits + 7) / 8;
     const int64_t parts = (n + kTileKeys - 1) / kTileKeys;
     OnesweepTemp t = carve(temp, parts);
-    static bool attr_set = false;
+    // the dynamic shared-memory opt-in is per device: set once for each device used
+    static std::atomic<unsigned long long> attr_set{0ull};
     const int dyn = (int)(sizeof(KeyT) + sizeof(uint32_t)) * kTileKeys;
-    if (!attr_set) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_set.load() & bit)) {
         cudaFuncSetAttribute(k_pass<KeyT>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-        attr_set = true;
+        attr_set.fetch_or(bit);
     }
     // histograms, partition counters and the first pass's status in one memset
     cudaMemsetAsync(t.hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix + 256 + sizeof(uint32_t) * kRadix * (size_t)parts,
