@@ -230,6 +230,30 @@ size_t dgsm_plan_workspace_bytes(int64_t n, int n_lights) {
     return plan_layout(nullptr, n, n_lights).bytes;
 }
 
+// Upload pipeline depth of dgsm_frame_host (chunks of the Gaussian arrays).
+constexpr int kUploadChunks = 2;
+
+// A copy stream + events per (thread, device) for the host-buffer entry point.
+struct CopyStream {
+    cudaStream_t st = nullptr;
+    cudaEvent_t start = nullptr, done = nullptr;
+    cudaEvent_t chunk[kUploadChunks];
+    int dev = -1;
+};
+static CopyStream& copy_stream() {
+    thread_local CopyStream cs;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cs.dev != dev) {
+        cudaStreamCreateWithFlags(&cs.st, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&cs.start, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&cs.done, cudaEventDisableTiming);
+        for (int i = 0; i < kUploadChunks; ++i) cudaEventCreateWithFlags(&cs.chunk[i], cudaEventDisableTiming);
+        cs.dev = dev;
+    }
+    return cs;
+}
+
 // The plan; with g_host != NULL the Gaussian arrays are first uploaded from
 // host memory into the device arrays of g in n_chunks pieces, each projected
 // as soon as it has landed (copy engine and SMs overlap).
@@ -265,14 +289,23 @@ static int plan_impl(const dgsm_gaussians_t* g, const dgsm_gaussians_t* g_host, 
 
     launch_project_init(p.stats, s);
     if (g_host && g->n > 0) {
+        // chunks are copied on the copy stream, each projected on `s` as soon as it
+        // has landed (copy engine and SMs overlap); the copy stream first waits for
+        // the work already queued on `s` (the device arrays may still be in use)
+        CopyStream& cs = copy_stream();
+        cudaEventRecord(cs.start, s);
+        cudaStreamWaitEvent(cs.st, cs.start, 0);
         const int64_t n = g->n, per = (n + n_chunks - 1) / n_chunks;
-        for (int64_t i0 = 0; i0 < n; i0 += per) {
+        int c = 0;
+        for (int64_t i0 = 0; i0 < n; i0 += per, ++c) {
             const int64_t cnt = std::min<int64_t>(per, n - i0);
-            cudaMemcpyAsync((float*)g->means + 3 * i0, g_host->means + 3 * i0, 12 * cnt, cudaMemcpyHostToDevice, s);
-            cudaMemcpyAsync((float*)g->scales + 3 * i0, g_host->scales + 3 * i0, 12 * cnt, cudaMemcpyHostToDevice, s);
+            cudaMemcpyAsync((float*)g->means + 3 * i0, g_host->means + 3 * i0, 12 * cnt, cudaMemcpyHostToDevice, cs.st);
+            cudaMemcpyAsync((float*)g->scales + 3 * i0, g_host->scales + 3 * i0, 12 * cnt, cudaMemcpyHostToDevice, cs.st);
             cudaMemcpyAsync((float*)g->rotations + 4 * i0, g_host->rotations + 4 * i0, 16 * cnt,
-                            cudaMemcpyHostToDevice, s);
-            cudaMemcpyAsync((float*)g->opacities + i0, g_host->opacities + i0, 4 * cnt, cudaMemcpyHostToDevice, s);
+                            cudaMemcpyHostToDevice, cs.st);
+            cudaMemcpyAsync((float*)g->opacities + i0, g_host->opacities + i0, 4 * cnt, cudaMemcpyHostToDevice, cs.st);
+            cudaEventRecord(cs.chunk[c], cs.st);
+            cudaStreamWaitEvent(s, cs.chunk[c], 0);
             launch_project(*g, lp, n_lights, atlas_res, n_shells, o, i0, cnt, p.recs, p.counts, p.dup, p.stats, s);
             g_launches += 1;
         }
@@ -443,9 +476,6 @@ int dgsm_build(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_ligh
     return rc;
 }
 
-// Upload pipeline depth of dgsm_frame_host (chunks of the Gaussian arrays).
-constexpr int kUploadChunks = 4;
-
 int dgsm_frame_host(const dgsm_gaussians_t* g_host, const dgsm_light_t* lights, int n_lights, int atlas_res,
                     int n_shells, const dgsm_build_opts_t* opts, const float* receivers_host, int64_t m,
                     float* T_host, void* ws, size_t ws_bytes, size_t* ws_required, float* atlas_out,
@@ -482,26 +512,15 @@ int dgsm_frame_host(const dgsm_gaussians_t* g_host, const dgsm_light_t* lights, 
     if (ws_required) *ws_required = need;
     if (ws_bytes < need) return fail(DGSM_ENOSPC, "workspace %zu < %zu bytes", ws_bytes, need);
     cudaStream_t s = (cudaStream_t)stream;
-    // receivers ride the copy engine on a side stream while the atlas is built
-    thread_local cudaStream_t aux = nullptr;
-    thread_local cudaEvent_t ev_rec = nullptr;
-    thread_local int aux_dev = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!aux || aux_dev != dev) {
-        cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking);
-        cudaEventCreateWithFlags(&ev_rec, cudaEventDisableTiming);
-        aux_dev = dev;
-    }
-    cudaEventRecord(ev_rec, s);  // after the plan's uploads (the aux stream must not race them on PCIe)
-    cudaStreamWaitEvent(aux, ev_rec, 0);
-    if (m > 0) cudaMemcpyAsync(rec, receivers_host, 12 * (size_t)m, cudaMemcpyHostToDevice, aux);
-    cudaEventRecord(ev_rec, aux);
+    // receivers ride the copy stream (after the Gaussian chunks) while the atlas is built
+    CopyStream& cs = copy_stream();
+    if (m > 0) cudaMemcpyAsync(rec, receivers_host, 12 * (size_t)m, cudaMemcpyHostToDevice, cs.st);
+    cudaEventRecord(cs.done, cs.st);
     rc = dgsm_build_run(&gd, lights, n_lights, opts, &plan, plan_ws, pb, (char*)plan_ws + pb,
                         ws_bytes - fixed - pb, atlas_out, stream);
     if (rc) return rc;
     launches += g_launches;
-    cudaStreamWaitEvent(s, ev_rec, 0);
+    cudaStreamWaitEvent(s, cs.done, 0);
     rc = dgsm_query(atlas_out, lights, n_lights, atlas_res, n_shells, rec, m, Td, nullptr, stream);
     if (rc) return rc;
     launches += g_launches;
