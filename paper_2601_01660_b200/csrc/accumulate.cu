@@ -24,6 +24,10 @@
 //    constant pref*(1 - erf(x_0)) beyond it: window shells and the step are
 //    written as differences into acc and a prefix sum over k restores tau_k.
 //    No tensor cores: this is not a dense contraction (FP32 FMA + MUFU bound).
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
 #include "dgsm_internal.cuh"
 
 namespace dgsm {
@@ -31,6 +35,10 @@ namespace dgsm {
 namespace {
 constexpr int kThreads = kTexels / kTileSplit;  // one warp = one half of an 8x8 tile
 constexpr int kStage = 32;        // records per pipeline stage
+// Staging of the records (template kTMA): TMA bulk copies into a raw shared
+// buffer (kTMA), or 16-B loads into registers one stage ahead (no raw buffer).
+// launch_accumulate takes TMA unless the raw buffer costs a CTA per SM.
+constexpr size_t kRawBytesTMA = kStage * 96;
 
 // One-warp CTAs synchronise with __syncwarp (no CTA barrier between the halves
 // of a tile: each half is an independent work unit).
@@ -351,7 +359,7 @@ __device__ __forceinline__ void pair_live_warp2(const PairTest2& T, uint32_t acc
                         dtlo, st_live, st_win, st_step);
 }
 
-template <bool kStats>
+template <bool kStats, bool kTMA>
 __global__ void __launch_bounds__(kThreads) k_accumulate(
     const WorkUnit* __restrict__ units, const uint32_t* __restrict__ n_units_dev,
     const uint32_t* __restrict__ vals, const PairRec* __restrict__ recs, int64_t n, AccLights al,
@@ -359,20 +367,20 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
     uint32_t* unit_counter, float* __restrict__ atlas, unsigned long long* __restrict__ stats,
     const uint64_t* __restrict__ slab_mask, const int2* __restrict__ slab_k) {
     extern __shared__ __align__(128) unsigned char acc_smem[];
-    PairRec* s_raw = reinterpret_cast<PairRec*>(acc_smem);                                   // [kStage]
-    float4* s_cr = reinterpret_cast<float4*>(acc_smem + kStage * sizeof(PairRec));           // [kStage][5]
-    float* s_acc = reinterpret_cast<float*>(acc_smem + kStage * sizeof(PairRec) +
-                                            kStage * kCompact * sizeof(float4));             // [K][64]
+    constexpr size_t kRawBytes = kTMA ? kRawBytesTMA : 0;
+    PairRec* s_raw = reinterpret_cast<PairRec*>(acc_smem);                                   // [kStage] (TMA)
+    float4* s_cr = reinterpret_cast<float4*>(acc_smem + kRawBytes);                          // [kStage][5]
+    float* s_acc = reinterpret_cast<float*>(acc_smem + kRawBytes + kStage * kCompact * sizeof(float4));  // [K][64]
     __shared__ __align__(8) uint64_t s_bar;
     __shared__ uint32_t s_unit, s_last;
 
     const int tid = threadIdx.x;
-    if (tid == 0) {
+    if (kTMA && tid == 0) {
         mbar_init(&s_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    cta_sync();
     uint32_t phase = 0u;
+    cta_sync();
     const uint32_t n_units = *n_units_dev;
     const int TW = res / kTile;
     const int n_tiles = TW * TW;
@@ -407,7 +415,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
         const uint32_t n_batches = (n_rec + kStage - 1) / kStage;
         const PairRec* lrecs = recs + (int64_t)l * n;
 
-        auto issue = [&](uint32_t b) {
+        auto issue = [&](uint32_t b) {  // TMA: bulk copies of the stage's records into s_raw
             const uint32_t j0 = wu.jbeg + b * kStage;
             const uint32_t nb = min((uint32_t)kStage, wu.jend - j0);
             if (tid == 0) mbar_arrive_expect_tx(&s_bar, nb * (uint32_t)sizeof(PairRec));
@@ -416,14 +424,29 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
                 bulk_g2s(s_raw + tid, lrecs + gi, (uint32_t)sizeof(PairRec), &s_bar);
             }
         };
-        if (n_batches > 0) issue(0);
+        // register staging: thread t < 32 holds record t of the next stage (6 x 16-B
+        // loads issued before the current stage's compute)
+        union RecRegs { uint4 u[6]; PairRec r; } rr;
+        auto fetch = [&](uint32_t b) {
+            const uint32_t j0 = wu.jbeg + b * kStage;
+            if ((uint32_t)tid < min((uint32_t)kStage, wu.jend - j0)) {
+                const uint4* src = reinterpret_cast<const uint4*>(lrecs + vals[j0 + tid]);
+#pragma unroll
+                for (int k = 0; k < 6; ++k) rr.u[k] = __ldg(src + k);
+            }
+        };
+        if (n_batches > 0) {
+            if (kTMA) issue(0); else fetch(0);
+        }
 
         for (uint32_t b = 0; b < n_batches; ++b) {
-            mbar_wait(&s_bar, phase);
-            phase ^= 1u;
+            if (kTMA) {
+                mbar_wait(&s_bar, phase);
+                phase ^= 1u;
+            }
             const uint32_t nb = min((uint32_t)kStage, n_rec - b * kStage);
             if ((uint32_t)tid < nb) {  // transform: raw record -> compact, relative to d_c
-                const PairRec& R = s_raw[tid];
+                const PairRec& R = kTMA ? s_raw[tid] : rr.r;
                 float* q = reinterpret_cast<float*>(s_cr) + (tid >> 1) * (2 * kPairFields) + (tid & 1);
                 float v[kPairFields] = {(float)(R.di[0] - c0), (float)(R.di[1] - c1), (float)(R.di[2] - c2),
                                         R.rcut_D2, R.g[0], R.g[1], R.g[2], R.D,
@@ -434,8 +457,12 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
             }
             cta_sync();  // compact copy ready; raw buffer free
             if (b + 1 < n_batches) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue(b + 1);
+                if (kTMA) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    issue(b + 1);
+                } else {
+                    fetch(b + 1);
+                }
             }
             // two records per iteration: independent dependency chains for the pair test
             uint32_t my_live = 0;
@@ -529,9 +556,11 @@ __global__ void k_exp(const float* tau, float* T, int64_t count) {
 }
 }  // namespace
 
-size_t accumulate_smem_bytes(int K) {
-    return kStage * sizeof(PairRec) + kStage * kCompact * sizeof(float4) +
-           (size_t)K * kThreads * sizeof(float);
+thread_local bool last_staging_tma = false;
+bool accumulate_last_used_tma() { return last_staging_tma; }
+
+size_t accumulate_smem_bytes(int K, bool tma) {
+    return (tma ? kRawBytesTMA : 0) + kStage * kCompact * sizeof(float4) + (size_t)K * kThreads * sizeof(float);
 }
 
 void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint32_t max_units,
@@ -547,36 +576,44 @@ void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint3
         al.dtlo[l] = (float)(dt - (double)al.dt[l]);
         al.idt[l] = (float)(1.0 / dt);
     }
-    const size_t smem = accumulate_smem_bytes(K);
     thread_local int dev_cached = -1, n_sm = 0;  // per thread: a thread may switch devices
-    thread_local size_t smem_set = 0;
+    thread_local int cached_K = -1, per_sm_tma = 0, per_sm_reg = 0;
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev != dev_cached) {
+    const size_t smem_tma = accumulate_smem_bytes(K, true), smem_reg = accumulate_smem_bytes(K, false);
+    if (dev != dev_cached || K != cached_K) {
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(k_accumulate<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tma);
+        cudaFuncSetAttribute(k_accumulate<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tma);
+        cudaFuncSetAttribute(k_accumulate<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_reg);
+        cudaFuncSetAttribute(k_accumulate<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_reg);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_tma, k_accumulate<false, true>, kThreads, smem_tma);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_reg, k_accumulate<false, false>, kThreads, smem_reg);
         dev_cached = dev;
-        smem_set = 0;
+        cached_K = K;
     }
-    if (smem > smem_set) {
-        cudaFuncSetAttribute(k_accumulate<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_accumulate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        smem_set = smem;
+    // TMA staging unless its raw buffer costs a CTA per SM (K = 64 on sm_100: 10 vs 11 CTAs;
+    // register staging measured 1.07 vs 1.10 ms on cfg2)
+    bool tma = per_sm_tma >= per_sm_reg;
+    if (const char* f = getenv("DGSM_ACC_STAGING")) {  // tests: force "tma" or "reg"
+        if (!strcmp(f, "tma")) tma = true;
+        else if (!strcmp(f, "reg")) tma = false;
     }
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_accumulate<false>, kThreads, smem);
-    if (per_sm < 1) per_sm = 1;
+    const int per_sm = std::max(1, tma ? per_sm_tma : per_sm_reg);
+    const size_t smem = tma ? smem_tma : smem_reg;
     uint32_t grid = (uint32_t)per_sm * (uint32_t)n_sm;
     if (grid > max_units) grid = max_units;
     if (grid == 0) grid = 1;
     if (ev_before) cudaEventRecord(ev_before, s);
-    if (flags & DGSM_COLLECT_STATS)
-        k_accumulate<true><<<grid, kThreads, smem, s>>>(units, n_units_dev, vals, recs, n, al, res, K, flags,
-                                                        scratch, tile_arrive, unit_counter, atlas, stats,
-                                                        slab_mask, slab_k);
-    else
-        k_accumulate<false><<<grid, kThreads, smem, s>>>(units, n_units_dev, vals, recs, n, al, res, K,
-                                                         flags, scratch, tile_arrive, unit_counter, atlas,
-                                                         stats, slab_mask, slab_k);
+    const bool st = (flags & DGSM_COLLECT_STATS) != 0;
+#define DGSM_ACC_ARGS units, n_units_dev, vals, recs, n, al, res, K, flags, scratch, tile_arrive, unit_counter, atlas, \
+                      stats, slab_mask, slab_k
+    if (st && tma) k_accumulate<true, true><<<grid, kThreads, smem, s>>>(DGSM_ACC_ARGS);
+    else if (st) k_accumulate<true, false><<<grid, kThreads, smem, s>>>(DGSM_ACC_ARGS);
+    else if (tma) k_accumulate<false, true><<<grid, kThreads, smem, s>>>(DGSM_ACC_ARGS);
+    else k_accumulate<false, false><<<grid, kThreads, smem, s>>>(DGSM_ACC_ARGS);
+#undef DGSM_ACC_ARGS
+    last_staging_tma = tma;
     if (ev_after) cudaEventRecord(ev_after, s);
 }
 

@@ -204,7 +204,8 @@ void launch_units(const uint32_t* tile_start, const uint32_t* tile_end, int64_t 
                   uint64_t* unit_counts, uint64_t* unit_offsets, void* scan_temp, WorkUnit* units_tmp,
                   WorkUnit* units, uint32_t max_units, uint32_t* n_units_dev, uint32_t* class_hist,
                   uint32_t* class_fill, cudaStream_t s, int* launches);
-size_t accumulate_smem_bytes(int K);
+size_t accumulate_smem_bytes(int K, bool tma);
+bool accumulate_last_used_tma();  // staging of the last launch on this thread (benchmark info)
 void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint32_t max_units,
                        const uint32_t* vals, const PairRec* recs, int64_t n, const LightsParam& lp,
                        int n_lights, int res, int K, uint32_t flags, float* scratch, uint32_t* tile_arrive,

@@ -409,3 +409,18 @@ def test_builder_one_call_equals_plan_run(dg):
         b(g, out)
         assert torch.equal(out, dg.build(g, s.lights, s.res, s.K))
     assert b.launches > 20
+
+
+@pytest.mark.parametrize("staging", ["tma", "reg"])
+def test_accumulate_staging_variants(dg, oracle_mod, staging, monkeypatch):
+    """Both record-staging variants of the accumulation kernel (TMA bulk copies /
+    register prefetch) against the oracle, and identical to each other."""
+    monkeypatch.setenv("DGSM_ACC_STAGING", staging)
+    for name in ("cfg1-seam-corner", "random-3lights", "cfg2-small"):
+        T, To = build_both(dg, oracle_mod, SCENES[name]())
+        assert np.abs(T - To).max() <= TOL_T, name
+    s = synth.random_scene(31, 400, res=32, K=64, L=2, dist=(0.3, 3.0), scale=(0.01, 0.4))
+    g = dg.to_device(s.gaussians)
+    T = dg.build(g, s.lights, s.res, s.K)
+    monkeypatch.setenv("DGSM_ACC_STAGING", "reg" if staging == "tma" else "tma")
+    assert torch.equal(T, dg.build(g, s.lights, s.res, s.K))
