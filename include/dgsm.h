@@ -206,6 +206,11 @@ int dgsm_query(const float* atlas, const dgsm_light_t* lights, int n_lights, int
  *                 the run part after the plan — a call that returns
  *                 DGSM_ENOSPC has done no device work beyond the plan; grow the
  *                 workspace to *ws_required and call again.
+ * Pipelining: the uploads of a frame wait only for the end of the previous frame
+ * that used the SAME workspace (tracked per workspace address, 4 most recent),
+ * not for work queued on `stream` in general: a caller alternating two
+ * workspaces overlaps frame i+1's uploads with frame i's build.  The host
+ * arrays must stay valid and unmodified until `stream` has passed the frame.
  * Errors: as dgsm_build_plan / dgsm_build_run / dgsm_query; DGSM_EINVAL for null
  * host arrays, DGSM_ENOSPC as above.  One host synchronisation (the plan). */
 int dgsm_frame_host(const dgsm_gaussians_t* g_host, const dgsm_light_t* lights, int n_lights, int atlas_res,

@@ -237,6 +237,13 @@ constexpr int kUploadChunks = 2;
 struct CopyStream {
     cudaStream_t st = nullptr;
     cudaEvent_t start = nullptr, done = nullptr;
+    // end of the last frame that used a workspace (by workspace address): a
+    // frame's uploads wait only for the previous frame in the SAME workspace, so
+    // a caller alternating two workspaces overlaps frame i+1's uploads with
+    // frame i's build (the layout may shift with n, m: the whole frame must be done)
+    void* slot_ws[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t slot_ev[4];
+    int slot_next = 0;
     cudaEvent_t chunk[kUploadChunks];
     int dev = -1;
 };
@@ -248,6 +255,10 @@ static CopyStream& copy_stream() {
         cudaStreamCreateWithFlags(&cs.st, cudaStreamNonBlocking);
         cudaEventCreateWithFlags(&cs.start, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&cs.done, cudaEventDisableTiming);
+        for (int i = 0; i < 4; ++i) {
+            cudaEventCreateWithFlags(&cs.slot_ev[i], cudaEventDisableTiming);
+            cs.slot_ws[i] = nullptr;
+        }
         for (int i = 0; i < kUploadChunks; ++i) cudaEventCreateWithFlags(&cs.chunk[i], cudaEventDisableTiming);
         cs.dev = dev;
     }
@@ -258,21 +269,21 @@ static CopyStream& copy_stream() {
 // host memory into the device arrays of g in n_chunks pieces, each projected
 // as soon as it has landed (copy engine and SMs overlap).
 static int plan_impl(const dgsm_gaussians_t* g, const dgsm_gaussians_t* g_host, int n_chunks,
-                     const dgsm_light_t* lights, int n_lights, int atlas_res, int n_shells,
-                     const dgsm_build_opts_t* opts, void* plan_ws, size_t plan_ws_bytes, dgsm_plan_t* plan,
-                     void* stream);
+                     cudaEvent_t upload_after, const dgsm_light_t* lights, int n_lights, int atlas_res,
+                     int n_shells, const dgsm_build_opts_t* opts, void* plan_ws, size_t plan_ws_bytes,
+                     dgsm_plan_t* plan, void* stream);
 
 int dgsm_build_plan(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_lights, int atlas_res,
                     int n_shells, const dgsm_build_opts_t* opts, void* plan_ws, size_t plan_ws_bytes,
                     dgsm_plan_t* plan, void* stream) {
-    return plan_impl(g, nullptr, 1, lights, n_lights, atlas_res, n_shells, opts, plan_ws, plan_ws_bytes, plan,
-                     stream);
+    return plan_impl(g, nullptr, 1, nullptr, lights, n_lights, atlas_res, n_shells, opts, plan_ws, plan_ws_bytes,
+                     plan, stream);
 }
 
 static int plan_impl(const dgsm_gaussians_t* g, const dgsm_gaussians_t* g_host, int n_chunks,
-                     const dgsm_light_t* lights, int n_lights, int atlas_res, int n_shells,
-                     const dgsm_build_opts_t* opts, void* plan_ws, size_t plan_ws_bytes, dgsm_plan_t* plan,
-                     void* stream) {
+                     cudaEvent_t upload_after, const dgsm_light_t* lights, int n_lights, int atlas_res,
+                     int n_shells, const dgsm_build_opts_t* opts, void* plan_ws, size_t plan_ws_bytes,
+                     dgsm_plan_t* plan, void* stream) {
     g_launches = 0;
     dgsm_build_opts_t o;
     if (opts) o = *opts; else dgsm_default_opts(&o);
@@ -293,8 +304,7 @@ static int plan_impl(const dgsm_gaussians_t* g, const dgsm_gaussians_t* g_host, 
         // has landed (copy engine and SMs overlap); the copy stream first waits for
         // the work already queued on `s` (the device arrays may still be in use)
         CopyStream& cs = copy_stream();
-        cudaEventRecord(cs.start, s);
-        cudaStreamWaitEvent(cs.st, cs.start, 0);
+        if (upload_after) cudaStreamWaitEvent(cs.st, upload_after, 0);  // the workspace's previous frame is done
         const int64_t n = g->n, per = (n + n_chunks - 1) / n_chunks;
         int c = 0;
         for (int64_t i0 = 0; i0 < n; i0 += per, ++c) {
@@ -503,9 +513,23 @@ int dgsm_frame_host(const dgsm_gaussians_t* g_host, const dgsm_light_t* lights, 
     if (ws_required) *ws_required = fixed + pb;
     if (!ws || ws_bytes < fixed + pb) return fail(DGSM_ENOSPC, "workspace %zu < %zu bytes (plan part)", ws_bytes, fixed + pb);
     void* plan_ws = (char*)ws + fixed;
+    // the event marking the end of the previous frame in this workspace
+    CopyStream& cs = copy_stream();
+    int slot = -1;
+    for (int i = 0; i < 4; ++i)
+        if (cs.slot_ws[i] == ws) slot = i;
+    const bool known = slot >= 0;
+    if (!known) {
+        slot = cs.slot_next;
+        cs.slot_next = (cs.slot_next + 1) % 4;
+        cs.slot_ws[slot] = ws;
+    }
+    cudaEvent_t slot_ev = cs.slot_ev[slot];
     dgsm_plan_t plan;
-    int rc = plan_impl(&gd, g_host, kUploadChunks, lights, n_lights, atlas_res, n_shells, opts, plan_ws, pb, &plan,
-                       stream);
+    // a workspace not seen before (or evicted): wait for everything queued on `stream`
+    if (!known) cudaEventRecord(slot_ev, (cudaStream_t)stream);
+    int rc = plan_impl(&gd, g_host, kUploadChunks, slot_ev, lights, n_lights, atlas_res, n_shells, opts, plan_ws,
+                       pb, &plan, stream);
     if (rc) return rc;
     int launches = g_launches;
     const size_t need = fixed + pb + plan.run_workspace_bytes;
@@ -513,7 +537,6 @@ int dgsm_frame_host(const dgsm_gaussians_t* g_host, const dgsm_light_t* lights, 
     if (ws_bytes < need) return fail(DGSM_ENOSPC, "workspace %zu < %zu bytes", ws_bytes, need);
     cudaStream_t s = (cudaStream_t)stream;
     // receivers ride the copy stream (after the Gaussian chunks) while the atlas is built
-    CopyStream& cs = copy_stream();
     if (m > 0) cudaMemcpyAsync(rec, receivers_host, 12 * (size_t)m, cudaMemcpyHostToDevice, cs.st);
     cudaEventRecord(cs.done, cs.st);
     rc = dgsm_build_run(&gd, lights, n_lights, opts, &plan, plan_ws, pb, (char*)plan_ws + pb,
@@ -525,6 +548,7 @@ int dgsm_frame_host(const dgsm_gaussians_t* g_host, const dgsm_light_t* lights, 
     if (rc) return rc;
     launches += g_launches;
     if (m > 0) cudaMemcpyAsync(T_host, Td, 4 * (size_t)m, cudaMemcpyDeviceToHost, s);
+    cudaEventRecord(slot_ev, s);  // this workspace is free again after this point
     g_launches = launches;
     return cuda_check("frame");
 }

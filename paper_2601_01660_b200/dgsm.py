@@ -416,7 +416,10 @@ class FrameHost:
         self.opts = opts or Options()
         self._oc = self.opts.c()
         self.device = torch.device(device)
-        self.ws = _alloc(0, self.device)
+        # two workspaces used alternately: frame i+1's uploads only wait for frame i-1
+        # (the library orders uploads after the previous frame in the same workspace)
+        self.wss = [_alloc(0, self.device), _alloc(0, self.device)]
+        self.frame = 0
         self.atlas = torch.empty((self.n_lights, self.K, self.res, self.res), dtype=torch.float32,
                                  device=self.device)
 
@@ -429,14 +432,17 @@ class FrameHost:
         n, m = arrs[0].shape[0], receivers_host.shape[0]
         g = Gaussians(*[C.c_void_p(a.data_ptr()) for a in arrs], n)
         need = C.c_size_t(0)
+        k = self.frame & 1
+        self.frame += 1
         for _ in range(3):
+            ws = self.wss[k]
             rc = lib().dgsm_frame_host(C.byref(g), self.lights, self.n_lights, self.res, self.K, C.byref(self._oc),
                                        C.c_void_p(receivers_host.data_ptr()), m, C.c_void_p(T_host.data_ptr()),
-                                       C.c_void_p(self.ws.data_ptr()), self.ws.numel(), C.byref(need),
+                                       C.c_void_p(ws.data_ptr()), ws.numel(), C.byref(need),
                                        C.c_void_p(self.atlas.data_ptr()), C.c_void_p(_stream_ptr(stream)))
             if rc != 2:  # DGSM_ENOSPC: grow the workspace and retry
                 break
-            self.ws = _alloc(int(need.value * 1.25) + (1 << 20), self.device)
+            self.wss[k] = _alloc(int(need.value * 1.25) + (1 << 20), self.device)
         _check(rc, "dgsm_frame_host")
         self.launches = last_launch_count()
         return self.atlas

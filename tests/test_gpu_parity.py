@@ -424,3 +424,27 @@ def test_accumulate_staging_variants(dg, oracle_mod, staging, monkeypatch):
     T = dg.build(g, s.lights, s.res, s.K)
     monkeypatch.setenv("DGSM_ACC_STAGING", "reg" if staging == "tma" else "tma")
     assert torch.equal(T, dg.build(g, s.lights, s.res, s.K))
+
+
+def test_frame_host_pipelined_frames(dg):
+    """Back-to-back frames with different inputs, no synchronisation between them
+    (frame i+1's uploads overlap frame i's build): each equals its device path."""
+    frames = []
+    for seed in (51, 52, 53):
+        s = synth.random_scene(seed, 3000, res=32, K=16, L=1, dist=(0.3, 3.0), scale=(0.01, 0.3))
+        frames.append(s)
+    s0 = frames[0]
+    fr = dg.FrameHost(s0.lights, s0.res, s0.K)
+    outs = []
+    for s in frames:
+        gh = {k: torch.from_numpy(np.ascontiguousarray(v, np.float32)).pin_memory() for k, v in s.gaussians.items()}
+        rh = torch.from_numpy(np.ascontiguousarray(s.queries, np.float32)).pin_memory()
+        Th = torch.empty(rh.shape[0]).pin_memory()
+        at = fr(gh, rh, Th).clone()
+        outs.append((gh, rh, Th, at))
+    torch.cuda.synchronize()
+    for s, (gh, rh, Th, at) in zip(frames, outs):
+        at2 = dg.build(dg.to_device(s.gaussians), s0.lights, s0.res, s0.K)
+        assert torch.equal(at, at2)
+        T2 = dg.query(at2, s0.lights, torch.from_numpy(np.ascontiguousarray(s.queries, np.float32)).cuda())
+        assert torch.equal(Th, T2.cpu())
