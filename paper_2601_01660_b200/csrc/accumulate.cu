@@ -159,18 +159,6 @@ __device__ __forceinline__ void acc_add(uint32_t a, float v) {
 // A packed value holds record A (even) in the low half and record B (odd) in
 // the high half; one f32x2 instruction does both records' operation, halving
 // the issue slots of the pair test (the kernel is issue/latency bound).
-typedef unsigned long long f2_t;
-__device__ __forceinline__ f2_t f2add(f2_t a, f2_t b) { f2_t d; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
-__device__ __forceinline__ f2_t f2sub(f2_t a, f2_t b) { f2_t d; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
-__device__ __forceinline__ f2_t f2mul(f2_t a, f2_t b) { f2_t d; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
-__device__ __forceinline__ f2_t f2fma(f2_t a, f2_t b, f2_t c) {
-    f2_t d;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-    return d;
-}
-__device__ __forceinline__ f2_t f2pack(float lo, float hi) { f2_t r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi)); return r; }
-__device__ __forceinline__ float f2lo(f2_t r) { float lo; asm("mov.b64 {%0, _}, %1;" : "=f"(lo) : "l"(r)); return lo; }
-__device__ __forceinline__ float f2hi(f2_t r) { float hi; asm("mov.b64 {_, %0}, %1;" : "=f"(hi) : "l"(r)); return hi; }
 __device__ __forceinline__ void lds_f2x2(uint32_t a, f2_t& x, f2_t& y) {
     asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(a) : "memory");
 }
@@ -267,7 +255,6 @@ __device__ __forceinline__ void pair_live_warp(float pa, float pc2, float pdot, 
     if (live && khi < K) acc_add(acc_base + (uint32_t)khi * (kThreads * 4), fmaf(pref, 1.0f - e0, -prev));
 }
 
-__device__ __forceinline__ f2_t f2bc(float x) { return f2pack(x, x); }
 
 // erf_fast of both halves: the polynomial on the paired pipe, clamp/select and
 // the MUFU ex2 per half

@@ -133,6 +133,22 @@ __host__ __device__ inline uint32_t count_tiles(const TileRects& R) {
     return cnt;
 }
 
+// Paired FP32 (sm_100 FFMA2 / FADD2 / FMUL2): a packed value holds two fp32
+// operands (low, high); one f32x2 instruction does both.
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2add(f2_t a, f2_t b) { f2_t d; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ f2_t f2sub(f2_t a, f2_t b) { f2_t d; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ f2_t f2mul(f2_t a, f2_t b) { f2_t d; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ f2_t f2fma(f2_t a, f2_t b, f2_t c) {
+    f2_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f2_t f2pack(float lo, float hi) { f2_t r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi)); return r; }
+__device__ __forceinline__ float f2lo(f2_t r) { float lo; asm("mov.b64 {%0, _}, %1;" : "=f"(lo) : "l"(r)); return lo; }
+__device__ __forceinline__ float f2hi(f2_t r) { float hi; asm("mov.b64 {_, %0}, %1;" : "=f"(hi) : "l"(r)); return hi; }
+__device__ __forceinline__ f2_t f2bc(float x) { return f2pack(x, x); }
+
 // ROI slab buffer (include/dgsm.h dgsm_slab_bytes): per-tile texel masks, then k ranges.
 inline size_t slab_mask_bytes(int n_lights, int res) {
     const size_t b = sizeof(uint64_t) * (size_t)n_lights * (res / kTile) * (res / kTile);

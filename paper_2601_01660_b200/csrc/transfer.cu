@@ -109,24 +109,60 @@ __global__ void __launch_bounds__(kThreadsT) k_transfer_part(const float4* __res
         }
         __syncthreads();
         // per tile in fp32, tile sums added once (short fp32 sums)
-        float4 tacc[kG];
+        if constexpr (kQ == 1 || kQ == 2) {
+            // Gaussian pairs on the paired FP32 pipe: (u, u+1) in one f32x2 register,
+            // the direction's values broadcast
+            f2_t TX[kG / 2], TY[kG / 2], TZ[kG / 2], TW[kG / 2], NX[kG / 2], NY[kG / 2], NZ[kG / 2];
 #pragma unroll
-        for (int u = 0; u < kG; ++u) tacc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int p = 0; p < kG / 2; ++p) {
+                TX[p] = TY[p] = TZ[p] = TW[p] = 0ull;
+                NX[p] = f2pack(nx[2 * p], nx[2 * p + 1]);
+                NY[p] = f2pack(ny[2 * p], ny[2 * p + 1]);
+                NZ[p] = f2pack(nz[2 * p], nz[2 * p + 1]);
+            }
 #pragma unroll 4
-        for (int t = 0; t < nt; ++t) {
-            const float4 dv = s_dir[t], wv = s_wl[t];
+            for (int t = 0; t < nt; ++t) {
+                const float4 dv = s_dir[t], wv = s_wl[t];
+                const f2_t DX = f2bc(dv.x), DY = f2bc(dv.y), DZ = f2bc(dv.z);
+                const f2_t WX = f2bc(wv.x), WY = f2bc(wv.y), WZ = f2bc(wv.z), WW = f2bc(wv.w);
+#pragma unroll
+                for (int p = 0; p < kG / 2; ++p) {
+                    const f2_t X = f2fma(NX[p], DX, f2fma(NY[p], DY, f2mul(NZ[p], DZ)));
+                    f2_t S = f2pack(fmaxf(f2lo(X), 0.0f), fmaxf(f2hi(X), 0.0f));
+                    if (kQ == 2) S = f2mul(S, S);
+                    TX[p] = f2fma(S, WX, TX[p]);
+                    TY[p] = f2fma(S, WY, TY[p]);
+                    TZ[p] = f2fma(S, WZ, TZ[p]);
+                    TW[p] = f2fma(S, WW, TW[p]);
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < kG / 2; ++p) {
+                acc[2 * p].x += f2lo(TX[p]); acc[2 * p + 1].x += f2hi(TX[p]);
+                acc[2 * p].y += f2lo(TY[p]); acc[2 * p + 1].y += f2hi(TY[p]);
+                acc[2 * p].z += f2lo(TZ[p]); acc[2 * p + 1].z += f2hi(TZ[p]);
+                acc[2 * p].w += f2lo(TW[p]); acc[2 * p + 1].w += f2hi(TW[p]);
+            }
+        } else {
+            float4 tacc[kG];
+#pragma unroll
+            for (int u = 0; u < kG; ++u) tacc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+            for (int t = 0; t < nt; ++t) {
+                const float4 dv = s_dir[t], wv = s_wl[t];
+#pragma unroll
+                for (int u = 0; u < kG; ++u) {
+                    const float S = lobe<kQ>(fmaf(nx[u], dv.x, fmaf(ny[u], dv.y, nz[u] * dv.z)), q);
+                    tacc[u].x = fmaf(S, wv.x, tacc[u].x);
+                    tacc[u].y = fmaf(S, wv.y, tacc[u].y);
+                    tacc[u].z = fmaf(S, wv.z, tacc[u].z);
+                    tacc[u].w = fmaf(S, wv.w, tacc[u].w);
+                }
+            }
 #pragma unroll
             for (int u = 0; u < kG; ++u) {
-                const float S = lobe<kQ>(fmaf(nx[u], dv.x, fmaf(ny[u], dv.y, nz[u] * dv.z)), q);
-                tacc[u].x = fmaf(S, wv.x, tacc[u].x);
-                tacc[u].y = fmaf(S, wv.y, tacc[u].y);
-                tacc[u].z = fmaf(S, wv.z, tacc[u].z);
-                tacc[u].w = fmaf(S, wv.w, tacc[u].w);
+                acc[u].x += tacc[u].x; acc[u].y += tacc[u].y; acc[u].z += tacc[u].z; acc[u].w += tacc[u].w;
             }
-        }
-#pragma unroll
-        for (int u = 0; u < kG; ++u) {
-            acc[u].x += tacc[u].x; acc[u].y += tacc[u].y; acc[u].z += tacc[u].z; acc[u].w += tacc[u].w;
         }
     }
 #pragma unroll

@@ -25,5 +25,5 @@ for n in (100_000, 150_000, 1_000_000):
         ts.append(a.elapsed_time(b))
     ms = float(np.median(ts))
     ops = n * 64 * 128 * 8
-    print(f"n={n}: {ms:.3f} ms  {n / ms / 1e3:.3g} Gaussians/s  {ops / ms / 1e9:.2f} TFLOP/s "
+    print(f"n={n}: {ms:.3f} ms  {n / ms * 1e3:.3g} Gaussians/s  {ops / ms / 1e9:.2f} TFLOP/s "
           f"({ops / ms / 1e9 / 37.22 * 100:.1f} % of 37.2)")
