@@ -302,17 +302,23 @@ __device__ __forceinline__ void live_finish(bool live, int klo, int khi, float f
 // Both records of the pair have a live lane in this warp: the setup and the
 // first window shell of both on the paired-FP32 pipe, then the per-record
 // updates in record order (A before B: the summation order of the scalar path).
+// Two (texel, record) pairs at once on the paired FP32 pipe: two records at one
+// texel (the two-warp kernel) or one record at two texels (the one-warp kernel).
+// Setup and first window shell packed; the shared-memory updates per half, A
+// before B (the summation order of the scalar path when both are one texel).
 template <bool kStats>
-__device__ __forceinline__ void pair_live_warp2(const PairTest2& T, uint32_t acc_base, int K, float dt, float dtlo,
-                                                float idt, uint32_t& st_live, uint32_t& st_win, uint32_t& st_step) {
+__device__ __forceinline__ void live_packed(f2_t A2, f2_t C2, f2_t DOT, f2_t D2, f2_t ED2, f2_t BP2, int kDA, int kDB,
+                                            bool liveA_in, bool liveB_in, uint32_t baseA, uint32_t baseB, int K,
+                                            float dt, float dtlo, float idt, uint32_t& st_live, uint32_t& st_win,
+                                            uint32_t& st_step) {
     const f2_t Z = 0ull;
-    const float aA = f2lo(T.A), aB = f2hi(T.A);
+    const float aA = f2lo(A2), aB = f2hi(A2);
     const f2_t IA = f2pack(rcp_approx(aA), rcp_approx(aB));
     const f2_t RA = f2pack(rsqrt_approx(aA), rsqrt_approx(aB));
-    const f2_t RR = f2mul(f2mul(f2mul(T.C2, IA), T.D), T.D);
-    const f2_t SD = f2mul(f2mul(f2sub(Z, T.D), T.DOT), IA);
-    const f2_t H = f2mul(f2mul(f2bc(0.70710678118654752f), T.A), RA);
-    const f2_t X0 = f2mul(f2sub(Z, H), f2add(T.D, SD));
+    const f2_t RR = f2mul(f2mul(f2mul(C2, IA), D2), D2);
+    const f2_t SD = f2mul(f2mul(f2sub(Z, D2), DOT), IA);
+    const f2_t H = f2mul(f2mul(f2bc(0.70710678118654752f), A2), RA);
+    const f2_t X0 = f2mul(f2sub(Z, H), f2add(D2, SD));
     float e0A = -1.0f, e0B = -1.0f;
     const float x0A = f2lo(X0), x0B = f2hi(X0);
     if (__any_sync(0xffffffffu, x0A > -kXS || x0B > -kXS)) {
@@ -320,13 +326,13 @@ __device__ __forceinline__ void pair_live_warp2(const PairTest2& T, uint32_t acc
         if (x0A > -kXS) e0A = ta;
         if (x0B > -kXS) e0B = tb;
     }
-    const bool liveA = T.liveA && e0A < 1.0f, liveB = T.liveB && e0B < 1.0f;
+    const bool liveA = liveA_in && e0A < 1.0f, liveB = liveB_in && e0B < 1.0f;
     const f2_t E0 = f2pack(e0A, e0B);
     const f2_t M = f2mul(f2bc(-0.72134752044448170f), RR);
-    const f2_t PREF = f2mul(f2mul(T.BP, RA), f2pack(ex2_approx(f2lo(M)), ex2_approx(f2hi(M))));
-    const f2_t E = f2sub(T.ED, SD);
+    const f2_t PREF = f2mul(f2mul(BP2, RA), f2pack(ex2_approx(f2lo(M)), ex2_approx(f2hi(M))));
+    const f2_t E = f2sub(ED2, SD);
     const f2_t XSH = f2mul(f2bc(kXS * 1.41421356237309505f), RA);
-    const f2_t KD = f2pack((float)T.kDA, (float)T.kDB);
+    const f2_t KD = f2pack((float)kDA, (float)kDB);
     const f2_t KLO = f2fma(f2sub(f2sub(Z, XSH), E), f2bc(idt), KD);
     const f2_t KHI = f2fma(f2sub(XSH, E), f2bc(idt), KD);
     const float fK = (float)K;
@@ -334,13 +340,20 @@ __device__ __forceinline__ void pair_live_warp2(const PairTest2& T, uint32_t acc
     const int kloB = (int)ceilf(fminf(fmaxf(f2hi(KLO), 0.0f), fK));
     const int khiA = max((int)ceilf(fminf(fmaxf(f2lo(KHI), 0.0f), fK)), kloA);
     const int khiB = max((int)ceilf(fminf(fmaxf(f2hi(KHI), 0.0f), fK)), kloB);
-    const f2_t FK = f2pack((float)(kloA - T.kDA), (float)(kloB - T.kDB));
+    const f2_t FK = f2pack((float)(kloA - kDA), (float)(kloB - kDB));
     const f2_t TK1 = f2fma(FK, f2bc(dt), f2fma(FK, f2bc(dtlo), E));
     const f2_t W1 = f2mul(PREF, f2sub(erf_fast2(f2mul(H, TK1)), E0));
-    live_finish<kStats>(liveA, kloA, khiA, f2lo(FK), f2lo(W1), f2lo(PREF), f2lo(H), f2lo(E), e0A, acc_base, K, dt,
+    live_finish<kStats>(liveA, kloA, khiA, f2lo(FK), f2lo(W1), f2lo(PREF), f2lo(H), f2lo(E), e0A, baseA, K, dt,
                         dtlo, st_live, st_win, st_step);
-    live_finish<kStats>(liveB, kloB, khiB, f2hi(FK), f2hi(W1), f2hi(PREF), f2hi(H), f2hi(E), e0B, acc_base, K, dt,
+    live_finish<kStats>(liveB, kloB, khiB, f2hi(FK), f2hi(W1), f2hi(PREF), f2hi(H), f2hi(E), e0B, baseB, K, dt,
                         dtlo, st_live, st_win, st_step);
+}
+
+template <bool kStats>
+__device__ __forceinline__ void pair_live_warp2(const PairTest2& T, uint32_t acc_base, int K, float dt, float dtlo,
+                                                float idt, uint32_t& st_live, uint32_t& st_win, uint32_t& st_step) {
+    live_packed<kStats>(T.A, T.C2, T.DOT, T.D, T.ED, T.BP, T.kDA, T.kDB, T.liveA, T.liveB, acc_base, acc_base, K, dt,
+                        dtlo, idt, st_live, st_win, st_step);
 }
 
 template <bool kStats, bool kTMA>
