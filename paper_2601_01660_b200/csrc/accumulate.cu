@@ -63,6 +63,21 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
     return y;
 }
 
+// Window bounds: ceil(kf) for kf in [0, K] as round-to-nearest(kf + 1/2) through
+// the 1.5 * 2^23 magic constant (FADD instead of F2I/I2F on the XU pipe).  It is
+// ceil(kf) + 1 when kf + 1/2 is a tie rounding up (kf an exact integer): the
+// window then drops (klo) or adds (khi) one boundary shell with |x_k| = 3.92 up
+// to rounding, whose erf is +-1 to 3e-8 either way.
+constexpr float kMagic = 12582912.0f;
+constexpr int kMagicBits = 0x4B400000;
+__device__ __forceinline__ float win_round(float kfh, int K) {  // kfh = kf + 1/2
+    return fminf(fmaxf(kfh, 0.0f), (float)K) + kMagic;
+}
+__device__ __forceinline__ f2_t win_round2(f2_t KFH, int K) {
+    const float fK = (float)K;
+    return f2add(f2pack(fminf(fmaxf(f2lo(KFH), 0.0f), fK), fminf(fmaxf(f2hi(KFH), 0.0f), fK)), f2bc(kMagic));
+}
+
 // fp32 erf, branch-free: 1 - 2^Q(|x|) with Q of degree 7 on [0, 3.92]
 // (max abs error 3.8e-7, tools/fit_erf.py 7), exactly +-1 for |x| >= 3.92.
 // Error budget: |d tau| <= 2 * 3.8e-7 * sum(pref) -> < 1e-5 in T for tau <~ 10.
@@ -172,7 +187,7 @@ constexpr int kPairBytes = kPairFields * 8;
 struct PairTest2 {
     f2_t A, C2, DOT;      // a = |u|^2, |g x W delta|^2, u . W delta  (records A | B)
     f2_t D, ED, BP;       // D, e_D, beta sqrt(pi/2)
-    int kDA, kDB;
+    f2_t KD;              // anchor shell k_D (as float)
     bool liveA, liveB;
 };
 
@@ -198,7 +213,7 @@ __device__ __forceinline__ PairTest2 pair_test2(uint32_t addr, f2_t ETX, f2_t ET
     R.C2 = C2;
     R.DOT = f2fma(UX, WX, f2fma(UY, WY, f2mul(UZ, WZ)));  // u . W delta (closest approach)
     R.D = F[7]; R.ED = F[17]; R.BP = F[18];
-    R.kDA = __float_as_int(f2lo(F[19])); R.kDB = __float_as_int(f2hi(F[19]));
+    R.KD = F[19];
     R.liveA = f2lo(C2) <= f2lo(T);
     R.liveB = f2hi(C2) <= f2hi(T);
     return R;
@@ -210,7 +225,7 @@ __device__ __forceinline__ PairTest2 pair_test2(uint32_t addr, f2_t ETX, f2_t ET
 // independent erf chains), further shells in a rarely taken loop.
 template <bool kStats>
 __device__ __forceinline__ void pair_live_warp(float pa, float pc2, float pdot, bool live, float D, float eD,
-                                               float betap, int kD, uint32_t acc_base, int K, float dt, float dtlo, float idt,
+                                               float betap, float kD, uint32_t acc_base, int K, float dt, float dtlo, float idt,
                                                uint32_t& st_live, uint32_t& st_win, uint32_t& st_step) {
     const float ia = rcp_approx(pa);
     const float r_over_D2 = pc2 * ia;
@@ -229,13 +244,15 @@ __device__ __forceinline__ void pair_live_warp(float pa, float pc2, float pdot, 
     const float pref = betap * ra * ex2_approx(-0.72134752044448170f * rr);
     const float e = eD - sD;
     const float xsh = (kXS * 1.41421356237309505f) * ra;
-    const float kf_lo = fmaf(-xsh - e, idt, (float)kD);
-    const float kf_hi = fmaf(xsh - e, idt, (float)kD);
-    const int klo = (int)ceilf(fminf(fmaxf(kf_lo, 0.0f), (float)K));
-    const int khi = max((int)ceilf(fminf(fmaxf(kf_hi, 0.0f), (float)K)), klo);
+    // window [klo, khi): ceil of the clamped bounds by round-to-nearest of kf + 1/2 (win_round)
+    const float kdh = kD + 0.5f;
+    const float ylo = win_round(fmaf(-xsh - e, idt, kdh), K);
+    const float yhi = win_round(fmaf(xsh - e, idt, kdh), K);
+    const int klo = __float_as_int(ylo) - kMagicBits;
+    const int khi = max(__float_as_int(yhi) - kMagicBits, klo);
     const int n = live ? khi - klo : 0;
     if (kStats) { st_win += (uint32_t)n; st_step += (live && khi < K) ? 1u : 0u; }
-    float fk = (float)(klo - kD);
+    float fk = (ylo - kMagic) - kD;
     uint32_t ap = acc_base + (uint32_t)klo * (kThreads * 4);
     const float tk1 = fmaf(fk, dt, fmaf(fk, dtlo, e));
     const float w1 = pref * (erf_fast(h * tk1) - e0);
@@ -307,7 +324,7 @@ __device__ __forceinline__ void live_finish(bool live, int klo, int khi, float f
 // Setup and first window shell packed; the shared-memory updates per half, A
 // before B (the summation order of the scalar path when both are one texel).
 template <bool kStats>
-__device__ __forceinline__ void live_packed(f2_t A2, f2_t C2, f2_t DOT, f2_t D2, f2_t ED2, f2_t BP2, int kDA, int kDB,
+__device__ __forceinline__ void live_packed(f2_t A2, f2_t C2, f2_t DOT, f2_t D2, f2_t ED2, f2_t BP2, f2_t KD,
                                             bool liveA_in, bool liveB_in, uint32_t baseA, uint32_t baseB, int K,
                                             float dt, float dtlo, float idt, uint32_t& st_live, uint32_t& st_win,
                                             uint32_t& st_step) {
@@ -332,15 +349,14 @@ __device__ __forceinline__ void live_packed(f2_t A2, f2_t C2, f2_t DOT, f2_t D2,
     const f2_t PREF = f2mul(f2mul(BP2, RA), f2pack(ex2_approx(f2lo(M)), ex2_approx(f2hi(M))));
     const f2_t E = f2sub(ED2, SD);
     const f2_t XSH = f2mul(f2bc(kXS * 1.41421356237309505f), RA);
-    const f2_t KD = f2pack((float)kDA, (float)kDB);
-    const f2_t KLO = f2fma(f2sub(f2sub(Z, XSH), E), f2bc(idt), KD);
-    const f2_t KHI = f2fma(f2sub(XSH, E), f2bc(idt), KD);
-    const float fK = (float)K;
-    const int kloA = (int)ceilf(fminf(fmaxf(f2lo(KLO), 0.0f), fK));
-    const int kloB = (int)ceilf(fminf(fmaxf(f2hi(KLO), 0.0f), fK));
-    const int khiA = max((int)ceilf(fminf(fmaxf(f2lo(KHI), 0.0f), fK)), kloA);
-    const int khiB = max((int)ceilf(fminf(fmaxf(f2hi(KHI), 0.0f), fK)), kloB);
-    const f2_t FK = f2pack((float)(kloA - kDA), (float)(kloB - kDB));
+    const f2_t KDH = f2add(KD, f2bc(0.5f));
+    const f2_t KLO = f2fma(f2sub(f2sub(Z, XSH), E), f2bc(idt), KDH);
+    const f2_t KHI = f2fma(f2sub(XSH, E), f2bc(idt), KDH);
+    const f2_t YLO = win_round2(KLO, K), YHI = win_round2(KHI, K);
+    const int kloA = __float_as_int(f2lo(YLO)) - kMagicBits, kloB = __float_as_int(f2hi(YLO)) - kMagicBits;
+    const int khiA = max(__float_as_int(f2lo(YHI)) - kMagicBits, kloA);
+    const int khiB = max(__float_as_int(f2hi(YHI)) - kMagicBits, kloB);
+    const f2_t FK = f2sub(f2sub(YLO, f2bc(kMagic)), KD);
     const f2_t TK1 = f2fma(FK, f2bc(dt), f2fma(FK, f2bc(dtlo), E));
     const f2_t W1 = f2mul(PREF, f2sub(erf_fast2(f2mul(H, TK1)), E0));
     live_finish<kStats>(liveA, kloA, khiA, f2lo(FK), f2lo(W1), f2lo(PREF), f2lo(H), f2lo(E), e0A, baseA, K, dt,
@@ -352,7 +368,7 @@ __device__ __forceinline__ void live_packed(f2_t A2, f2_t C2, f2_t DOT, f2_t D2,
 template <bool kStats>
 __device__ __forceinline__ void pair_live_warp2(const PairTest2& T, uint32_t acc_base, int K, float dt, float dtlo,
                                                 float idt, uint32_t& st_live, uint32_t& st_win, uint32_t& st_step) {
-    live_packed<kStats>(T.A, T.C2, T.DOT, T.D, T.ED, T.BP, T.kDA, T.kDB, T.liveA, T.liveB, acc_base, acc_base, K, dt,
+    live_packed<kStats>(T.A, T.C2, T.DOT, T.D, T.ED, T.BP, T.KD, T.liveA, T.liveB, acc_base, acc_base, K, dt,
                         dtlo, idt, st_live, st_win, st_step);
 }
 
@@ -448,7 +464,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
                 float v[kPairFields] = {(float)(R.di[0] - c0), (float)(R.di[1] - c1), (float)(R.di[2] - c2),
                                         R.rcut_D2, R.g[0], R.g[1], R.g[2], R.D,
                                         R.W[0], R.W[1], R.W[2], R.W[3], R.W[4], R.W[5], R.W[6], R.W[7], R.W[8],
-                                        R.eD, R.betap, __int_as_float(R.kD)};
+                                        R.eD, R.betap, (float)R.kD};
 #pragma unroll
                 for (int f = 0; f < kPairFields; ++f) q[2 * f] = v[f];
             }
@@ -479,10 +495,10 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
                 }
                 if (anyA)
                     pair_live_warp<kStats>(f2lo(T2.A), f2lo(T2.C2), f2lo(T2.DOT), T2.liveA, f2lo(T2.D), f2lo(T2.ED),
-                                           f2lo(T2.BP), T2.kDA, acc_base, K, dt, dtlo, idt, st_live, st_win, st_step);
+                                           f2lo(T2.BP), f2lo(T2.KD), acc_base, K, dt, dtlo, idt, st_live, st_win, st_step);
                 if (anyB)
                     pair_live_warp<kStats>(f2hi(T2.A), f2hi(T2.C2), f2hi(T2.DOT), T2.liveB, f2hi(T2.D), f2hi(T2.ED),
-                                           f2hi(T2.BP), T2.kDB, acc_base, K, dt, dtlo, idt, st_live, st_win, st_step);
+                                           f2hi(T2.BP), f2hi(T2.KD), acc_base, K, dt, dtlo, idt, st_live, st_win, st_step);
             }
             if (kStats) st_wmax += __reduce_max_sync(0xffffffffu, my_live);
             cta_sync();  // compact copy consumed
