@@ -276,7 +276,7 @@ void launch_units(const uint32_t* tile_start, const uint32_t* tile_end, int64_t 
                               class_hist);
     const unsigned gl = (unsigned)std::min<uint32_t>((max_units + 255) / 256, 148u * 8u);
     k_units_lpt<<<gl, 256, 0, s>>>(units_tmp, n_units_dev, class_hist, class_fill, units);
-    *launches += 6;
+    *launches += 3 + kScanLaunches;
 }
 
 }  // namespace dgsm

@@ -325,7 +325,7 @@ static int plan_impl(const dgsm_gaussians_t* g, const dgsm_gaussians_t* g_host, 
     }
     launch_scan_u32_to_u64(p.counts, p.offsets, m, p.scan_temp, s);
     launch_plan_stats(p.offsets, g->n, n_lights, p.stats, s);
-    g_launches += 5;
+    g_launches += 2 + kScanLaunches;  // init, scan, plan stats
     if ((rc = cuda_check("plan launch"))) return rc;
     PlanStats hs;
     cudaMemcpyAsync(&hs, p.stats, sizeof(PlanStats), cudaMemcpyDeviceToHost, s);
@@ -395,7 +395,7 @@ static void run_binning(const dgsm_gaussians_t* g, int n_lights, const dgsm_buil
         const uint64_t* tm = o.slab ? slab_mask_ptr(o.slab) + (int64_t)l * n_tiles : nullptr;
         launch_duplicate_ranked(dup, perm, r.offs_perm, n, res, o.bin_mode, (uint64_t)b, tm, r.keys_a, r.vals_a,
                                 s);
-        g_launches += 6;
+        g_launches += 3 + kScanLaunches;  // depth keys, gather, scan, duplication
         // 4. stable sort of the tile digits
         const int ft = launch_onesweep_u32(r.keys_a + b, r.vals_a + b, r.keys_b + b, r.vals_b + b, e - b,
                                            plan->tile_bits, r.sort_temp, s, &g_launches);

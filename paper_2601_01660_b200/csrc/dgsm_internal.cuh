@@ -194,6 +194,7 @@ void launch_project(const dgsm_gaussians_t& g, const LightsParam& lp, int n_ligh
                     const dgsm_build_opts_t& o, int64_t i0, int64_t cnt, PairRec* recs, uint32_t* counts,
                     uint4* dup, PlanStats* stats, cudaStream_t s);
 size_t scan_u32_to_u64_temp_bytes(int64_t n);
+constexpr int kScanLaunches = 2;  // kernels per launch_scan_* call
 void launch_scan_u32_to_u64(const uint32_t* in, uint64_t* out, int64_t n, void* temp, cudaStream_t s);
 void launch_scan_u64(const uint64_t* in, uint64_t* out, int64_t n, void* temp, cudaStream_t s);
 void launch_plan_stats(const uint64_t* offsets, int64_t n, int n_lights, PlanStats* stats, cudaStream_t s);

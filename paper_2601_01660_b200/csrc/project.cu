@@ -14,7 +14,7 @@ constexpr double kPi = 3.141592653589793;
 
 __device__ __forceinline__ double sgn_pos(double x) { return x >= 0.0 ? 1.0 : -1.0; }  // sgn(0)=+1 (Q4)
 
-__global__ void __launch_bounds__(256, 4) k_project(
+__global__ void __launch_bounds__(256, 4) k_project(  // (256, 3) and (256, 2) measured slower
     const float* __restrict__ means, const float* __restrict__ scales,
     const float* __restrict__ rotations, const float* __restrict__ opacities, int64_t n, int64_t i0, int64_t cnt,
     LightsParam lp, int n_lights, int res, int K, double kappa, double k_sigma, double rho,
@@ -22,9 +22,6 @@ __global__ void __launch_bounds__(256, 4) k_project(
     PairRec* __restrict__ recs, uint32_t* __restrict__ counts,
     uint4* __restrict__ dup,
     PlanStats* stats) {
-    __shared__ uint32_t s_dmin[DGSM_MAX_LIGHTS], s_dmax[DGSM_MAX_LIGHTS];
-    if (threadIdx.x < DGSM_MAX_LIGHTS) { s_dmin[threadIdx.x] = 0xffffffffu; s_dmax[threadIdx.x] = 0u; }
-    __syncthreads();
     // Gaussians [i0, i0 + cnt) of every light (a chunk of an upload pipeline, or all)
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = idx < (int64_t)n_lights * cnt;
@@ -36,10 +33,15 @@ __global__ void __launch_bounds__(256, 4) k_project(
     const float4 L = lp.l[l];
     const int W = res, H = res;
 
+    // all inputs of the Gaussian loaded up front (one memory latency, not four)
+    const float m0 = means[3 * i], m1 = means[3 * i + 1], m2 = means[3 * i + 2];
+    const float q0 = rotations[4 * i], q1 = rotations[4 * i + 1], q2 = rotations[4 * i + 2], q3 = rotations[4 * i + 3];
+    const float sc0 = scales[3 * i], sc1 = scales[3 * i + 1], sc2 = scales[3 * i + 2];
+    const float alpha_in = opacities[i];
     // R4: m = mu - o, D = |m|; excluded when D <= 1e-6 (Q17)
-    const double mx = (double)means[3 * i] - (double)L.x;
-    const double my = (double)means[3 * i + 1] - (double)L.y;
-    const double mz = (double)means[3 * i + 2] - (double)L.z;
+    const double mx = (double)m0 - (double)L.x;
+    const double my = (double)m1 - (double)L.y;
+    const double mz = (double)m2 - (double)L.z;
     const double D = sqrt((mx * mx + my * my) + mz * mz);
     uint32_t tcnt = 0;
     PairRec rec;
@@ -55,8 +57,7 @@ __global__ void __launch_bounds__(256, 4) k_project(
         const double py = (v + 1.0) * (0.5 * H) - 0.5;
 
         // rotation from the quaternion (w,x,y,z), normalised in fp64
-        double qw = rotations[4 * i], qxr = rotations[4 * i + 1], qyr = rotations[4 * i + 2],
-               qzr = rotations[4 * i + 3];
+        double qw = q0, qxr = q1, qyr = q2, qzr = q3;
         const double iqn = 1.0 / sqrt(((qw * qw + qxr * qxr) + qyr * qyr) + qzr * qzr);
         qw = qw * iqn; qxr = qxr * iqn; qyr = qyr * iqn; qzr = qzr * iqn;
         double R[3][3];
@@ -73,11 +74,11 @@ __global__ void __launch_bounds__(256, 4) k_project(
         // R5: lambda1 of Sigma_perp = [u v]^T Sigma [u v], basis-free form
         const double invD = 1.0 / D;
         const double dx = mx * invD, dy = my * invD, dz = mz * invD;
-        double w[3], s2[3], s[3];
+        double w[3], s2[3];
+        const double s[3] = {(double)sc0, (double)sc1, (double)sc2};
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
             w[j] = (R[0][j] * dx + R[1][j] * dy) + R[2][j] * dz;
-            s[j] = (double)scales[3 * i + j];
             s2[j] = s[j] * s[j];
         }
         const double tr = (s2[0] * (1.0 - w[0] * w[0]) + s2[1] * (1.0 - w[1] * w[1])) +
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(256, 4) k_project(
             rec.eD = (float)((kD + 0.5) * dt - D);
             // Eq.5 with the clamp of Q16; times sqrt(pi/2) from Eq.3's prefactor
             // tau* in fp32 (log1pf: no fp64 table lookups; betap is stored in fp32)
-            float alpha = opacities[i];
+            float alpha = alpha_in;
             alpha = alpha < 1e-4f ? 1e-4f : (alpha > 1.0f - 1e-4f ? 1.0f - 1e-4f : alpha);
             const double tau_star = (double)(-log1pf(-alpha));
             const double trA = inv_s[0] * inv_s[0] + inv_s[1] * inv_s[1] + inv_s[2] * inv_s[2];
@@ -166,16 +167,17 @@ __global__ void __launch_bounds__(256, 4) k_project(
         dup[oi] = make_uint4(dbits, (uint32_t)(uint16_t)rc0 | ((uint32_t)(uint16_t)rc1 << 16),
                               (uint32_t)(uint16_t)rr0 | ((uint32_t)(uint16_t)rr1 << 16), tcnt);
     }
-    // per-light min/max of the depth key over binned Gaussians: shared-memory
-    // atomics per block, one global atomic per (block, light)
-    if (tcnt > 0) {
-        atomicMin(&s_dmin[l], dbits);
-        atomicMax(&s_dmax[l], dbits);
-    }
-    __syncthreads();
-    if (threadIdx.x < DGSM_MAX_LIGHTS && s_dmax[threadIdx.x] != 0u) {
-        atomicMin(&stats->depth_min[threadIdx.x], s_dmin[threadIdx.x]);
-        atomicMax(&stats->depth_max[threadIdx.x], s_dmax[threadIdx.x]);
+    // per-light min/max of the depth key over binned Gaussians: warp reductions
+    // (no CTA barrier), a global atomic only when it would change the value
+    // (the running extremes settle after a few warps)
+    const uint32_t peers = __match_any_sync(0xffffffffu, l);  // lanes of the same light
+    const uint32_t dmin = __reduce_min_sync(peers, tcnt > 0 ? dbits : 0xffffffffu);
+    const uint32_t dmax = __reduce_max_sync(peers, tcnt > 0 ? dbits : 0u);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1 && dmax != 0u) {
+        volatile uint32_t* vmin = &stats->depth_min[l];
+        volatile uint32_t* vmax = &stats->depth_max[l];
+        if (dmin < *vmin) atomicMin(&stats->depth_min[l], dmin);
+        if (dmax > *vmax) atomicMax(&stats->depth_max[l], dmax);
     }
 }
 

@@ -1,4 +1,4 @@
-// scan.cu — exclusive prefix sums (reduce-then-scan, 3 launches) used for the
+// scan.cu — exclusive prefix sums (reduce-then-scan, 2 launches) used for the
 // per-(light, Gaussian) key offsets and the per-tile work-unit offsets.
 #include "dgsm_internal.cuh"
 
@@ -38,63 +38,75 @@ __device__ __forceinline__ uint64_t block_excl_scan(uint64_t x, uint64_t* total)
     return warp_prefix + inc - x;
 }
 
+// Two launches: k_reduce sums each block's contiguous run of 4096-element tiles;
+// k_downsweep adds the partials of the blocks before it (<= kMaxBlocks values,
+// L2-resident) and scans its run tile by tile, storing coalesced through shared
+// memory.  The grid is capped at kMaxBlocks so that prefix read stays small.
+constexpr int64_t kMaxBlocks = 1024;
+
 template <typename T>
-__global__ void __launch_bounds__(kScanThreads) k_reduce(const T* __restrict__ in, int64_t n,
+__global__ void __launch_bounds__(kScanThreads) k_reduce(const T* __restrict__ in, int64_t n, int64_t tpb,
                                                          uint64_t* __restrict__ partials) {
-    const int64_t base = (int64_t)blockIdx.x * kScanTile;
+    const int64_t t0 = (int64_t)blockIdx.x * tpb;
     uint64_t s = 0;
+    for (int64_t t = t0; t < t0 + tpb; ++t) {
+        const int64_t base = t * kScanTile;
+        if (base >= n) break;
 #pragma unroll
-    for (int j = 0; j < kScanItems; ++j) {
-        int64_t k = base + (int64_t)j * kScanThreads + threadIdx.x;
-        if (k < n) s += in[k];
+        for (int j = 0; j < kScanItems; ++j) {
+            const int64_t k = base + (int64_t)j * kScanThreads + threadIdx.x;
+            if (k < n) s += in[k];
+        }
     }
     uint64_t total;
     block_excl_scan(s, &total);
     if (threadIdx.x == 0) partials[blockIdx.x] = total;
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_partials(uint64_t* partials, int64_t nb) {
-    uint64_t carry = 0;
-    for (int64_t b0 = 0; b0 < nb; b0 += kScanThreads) {
-        int64_t k = b0 + threadIdx.x;
-        uint64_t v = k < nb ? partials[k] : 0;
-        uint64_t total;
-        uint64_t ex = block_excl_scan(v, &total);
-        if (k < nb) partials[k] = carry + ex;
-        carry += total;
-    }
-    if (threadIdx.x == 0) partials[nb] = carry;
-}
-
 template <typename T, typename O>
-__global__ void __launch_bounds__(kScanThreads) k_downsweep(const T* __restrict__ in, int64_t n,
+__global__ void __launch_bounds__(kScanThreads) k_downsweep(const T* __restrict__ in, int64_t n, int64_t tpb,
                                                             const uint64_t* __restrict__ partials,
-                                                            int64_t nb, O* __restrict__ out) {
-    const int64_t base = (int64_t)blockIdx.x * kScanTile;
-    // blocked arrangement: thread t owns items [base + t*16, base + t*16 + 16)
-    __shared__ T tile[kScanTile];
+                                                            O* __restrict__ out) {
+    __shared__ uint64_t tile[kScanTile];
+    // exclusive prefix of this block: the partials of the blocks before it
+    uint64_t pre = 0;
+    for (int64_t b = threadIdx.x; b < (int64_t)blockIdx.x; b += kScanThreads) pre += partials[b];
+    uint64_t carry;
+    block_excl_scan(pre, &carry);
+    const int64_t t0 = (int64_t)blockIdx.x * tpb;
+    for (int64_t t = t0; t < t0 + tpb; ++t) {
+        const int64_t base = t * kScanTile;
+        if (base >= n) break;
 #pragma unroll
-    for (int j = 0; j < kScanItems; ++j) {
-        int64_t k = base + (int64_t)j * kScanThreads + threadIdx.x;
-        tile[j * kScanThreads + threadIdx.x] = k < n ? in[k] : T(0);
-    }
-    __syncthreads();
-    uint64_t v[kScanItems];
-    uint64_t s = 0;
+        for (int j = 0; j < kScanItems; ++j) {  // coalesced load
+            const int64_t k = base + (int64_t)j * kScanThreads + threadIdx.x;
+            tile[j * kScanThreads + threadIdx.x] = k < n ? (uint64_t)in[k] : 0ull;
+        }
+        __syncthreads();
+        uint64_t v[kScanItems];
+        uint64_t s = 0;
 #pragma unroll
-    for (int j = 0; j < kScanItems; ++j) {
-        v[j] = tile[threadIdx.x * kScanItems + j];
-        s += v[j];
-    }
-    uint64_t total;
-    uint64_t run = block_excl_scan(s, &total) + partials[blockIdx.x];
+        for (int j = 0; j < kScanItems; ++j) {  // blocked: thread t owns items [16 t, 16 t + 16)
+            v[j] = tile[threadIdx.x * kScanItems + j];
+            s += v[j];
+        }
+        uint64_t total;
+        uint64_t run = carry + block_excl_scan(s, &total);  // (its barriers also order the tile reads)
 #pragma unroll
-    for (int j = 0; j < kScanItems; ++j) {
-        int64_t k = base + (int64_t)threadIdx.x * kScanItems + j;
-        if (k < n) out[k] = (O)run;
-        run += v[j];
+        for (int j = 0; j < kScanItems; ++j) {
+            tile[threadIdx.x * kScanItems + j] = run;
+            run += v[j];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kScanItems; ++j) {  // coalesced store
+            const int64_t k = base + (int64_t)j * kScanThreads + threadIdx.x;
+            if (k < n) out[k] = (O)tile[j * kScanThreads + threadIdx.x];
+        }
+        carry += total;
+        if (base + kScanTile >= n && threadIdx.x == 0) out[n] = (O)carry;
+        __syncthreads();
     }
-    if (blockIdx.x == nb - 1 && threadIdx.x == 0) out[n] = (O)partials[nb];
 }
 
 template <typename T, typename O>
@@ -104,10 +116,11 @@ void scan_impl(const T* in, O* out, int64_t n, void* temp, cudaStream_t s) {
         cudaMemsetAsync(out, 0, sizeof(O), s);
         return;
     }
-    const int64_t nb = (n + kScanTile - 1) / kScanTile;
-    k_reduce<T><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, partials);
-    k_scan_partials<<<1, kScanThreads, 0, s>>>(partials, nb);
-    k_downsweep<T, O><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, partials, nb, out);
+    const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+    const int64_t tpb = (tiles + kMaxBlocks - 1) / kMaxBlocks;
+    const int64_t nb = (tiles + tpb - 1) / tpb;
+    k_reduce<T><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, tpb, partials);
+    k_downsweep<T, O><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, tpb, partials, out);
 }
 
 __global__ void k_plan_stats(const uint64_t* __restrict__ offsets, int64_t n, int n_lights,
