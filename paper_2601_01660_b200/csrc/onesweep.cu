@@ -1,7 +1,7 @@
 // onesweep.cu — stable LSD radix sort of (key, u32 value) pairs, key = u32 or
 // u64, in the "onesweep" style: one histogram pass over all digits, then ONE
 // kernel per 8-bit digit that ranks a 2048-key partition in shared memory (warp
-// multi-split via match.any), obtains its global digit offsets by decoupled
+// multi-split by ballots, or match.any on a narrow top digit), obtains its global digit offsets by decoupled
 // look-back over earlier partitions (8 predecessors per round trip), and
 // scatters through shared memory for coalesced writes.  Partition ids come from
 // an atomic counter, so a CTA only ever waits on partitions that are already
@@ -93,7 +93,8 @@ template <typename KeyT>
 __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ kin,
                                                       const uint32_t* __restrict__ vin,
                                                       KeyT* __restrict__ kout, uint32_t* __restrict__ vout,
-                                                      int64_t n, int shift, const uint32_t* __restrict__ gofs,
+                                                      int64_t n, int shift, int bits,
+                                                      const uint32_t* __restrict__ gofs,
                                                       uint32_t* status, uint32_t* status_next,
                                                       uint32_t* part_ctr) {
     extern __shared__ __align__(16) unsigned char os_smem[];
@@ -129,7 +130,23 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ k
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
         const uint32_t d = dig[j];
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        // warp multi-split (lanes holding the same digit, or 256 = invalid): one ballot
+        // per digit bit on full 8-bit passes; match.any on a key's narrow top pass
+        // (few distinct digits per warp: measured faster there, slower on 8 bits)
+        uint32_t peers;
+        if (bits < 8) {  // uniform
+            peers = __match_any_sync(0xffffffffu, d);
+        } else {
+            const bool inv = d >> 8;
+            const uint32_t bv = __ballot_sync(0xffffffffu, inv);
+            peers = inv ? bv : ~bv;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const bool bit = (d >> b) & 1u;
+                const uint32_t bb = __ballot_sync(0xffffffffu, bit);
+                peers &= bit ? bb : ~bb;
+            }
+        }
         uint32_t cnt = 0;
         if (d < 256u) cnt = s_warp_hist[warp][d];
         rank[j] = cnt + __popc(peers & lt);
@@ -251,7 +268,8 @@ int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt
     uint32_t *vi = vals, *vo = vals_alt;
     int flipped = 0;
     for (int p = 0; p < passes; ++p) {
-        k_pass<KeyT><<<(unsigned)parts, kThreads, dyn, s>>>(ki, vi, ko, vo, n, 8 * p, t.hist + p * kRadix,
+        const int bits = std::min(8, nbits - 8 * p);  // digit bits above the key's top bit are 0
+        k_pass<KeyT><<<(unsigned)parts, kThreads, dyn, s>>>(ki, vi, ko, vo, n, 8 * p, bits, t.hist + p * kRadix,
                                                            t.status[p & 1], t.status[(p + 1) & 1],
                                                            t.part_ctr + p);
         *launches += 1;

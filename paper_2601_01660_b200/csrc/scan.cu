@@ -67,7 +67,9 @@ template <typename T, typename O>
 __global__ void __launch_bounds__(kScanThreads) k_downsweep(const T* __restrict__ in, int64_t n, int64_t tpb,
                                                             const uint64_t* __restrict__ partials,
                                                             O* __restrict__ out) {
-    __shared__ uint64_t tile[kScanTile];
+    // padded: element e at e + e/16, so the blocked accesses (stride 16) spread over banks
+    __shared__ uint64_t tile[kScanTile + kScanTile / kScanItems];
+    auto at = [](int e) { return e + (e >> 4); };
     // exclusive prefix of this block: the partials of the blocks before it
     uint64_t pre = 0;
     for (int64_t b = threadIdx.x; b < (int64_t)blockIdx.x; b += kScanThreads) pre += partials[b];
@@ -80,28 +82,28 @@ __global__ void __launch_bounds__(kScanThreads) k_downsweep(const T* __restrict_
 #pragma unroll
         for (int j = 0; j < kScanItems; ++j) {  // coalesced load
             const int64_t k = base + (int64_t)j * kScanThreads + threadIdx.x;
-            tile[j * kScanThreads + threadIdx.x] = k < n ? (uint64_t)in[k] : 0ull;
+            tile[at(j * kScanThreads + threadIdx.x)] = k < n ? (uint64_t)in[k] : 0ull;
         }
         __syncthreads();
         uint64_t v[kScanItems];
         uint64_t s = 0;
 #pragma unroll
         for (int j = 0; j < kScanItems; ++j) {  // blocked: thread t owns items [16 t, 16 t + 16)
-            v[j] = tile[threadIdx.x * kScanItems + j];
+            v[j] = tile[at(threadIdx.x * kScanItems + j)];
             s += v[j];
         }
         uint64_t total;
         uint64_t run = carry + block_excl_scan(s, &total);  // (its barriers also order the tile reads)
 #pragma unroll
         for (int j = 0; j < kScanItems; ++j) {
-            tile[threadIdx.x * kScanItems + j] = run;
+            tile[at(threadIdx.x * kScanItems + j)] = run;
             run += v[j];
         }
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < kScanItems; ++j) {  // coalesced store
             const int64_t k = base + (int64_t)j * kScanThreads + threadIdx.x;
-            if (k < n) out[k] = (O)tile[j * kScanThreads + threadIdx.x];
+            if (k < n) out[k] = (O)tile[at(j * kScanThreads + threadIdx.x)];
         }
         carry += total;
         if (base + kScanTile >= n && threadIdx.x == 0) out[n] = (O)carry;
