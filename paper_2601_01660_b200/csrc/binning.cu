@@ -31,12 +31,14 @@ __global__ void __launch_bounds__(256) k_depth_keys(const uint4* __restrict__ du
     vals[i] = (uint32_t)i;
 }
 
-__global__ void __launch_bounds__(256) k_gather_counts(const uint4* __restrict__ dup,
+// key counts in depth-rank order (a 4-B gather from the count array, which
+// stays L2-resident, rather than from the 16-B dup records)
+__global__ void __launch_bounds__(256) k_gather_counts(const uint32_t* __restrict__ counts,
                                                        const uint32_t* __restrict__ perm, int64_t n,
                                                        uint32_t* __restrict__ cperm) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
-    cperm[j] = dup[perm[j]].w;
+    cperm[j] = counts[perm[j]];
 }
 
 // One warp per 32 consecutive Gaussians in depth-rank order.  Their outputs
@@ -71,7 +73,13 @@ __global__ void __launch_bounds__(256) k_duplicate_ranked(const uint4* __restric
     const uint64_t seg0 = offs[j0];
     const uint32_t excl = (uint32_t)((valid ? offs[j] : offs[n]) - seg0);
     const uint32_t seg_len = __shfl_sync(0xffffffffu, excl + (valid ? r.w : 0u), 31);
-    const int tx0 = c0 >> 3, ty0 = r0 >> 3, wt = (c1 >> 3) - tx0 + 1;
+    // the owner's rectangle packed in one word (tx0 | ty0 << 11 | wt << 22, wt = 0:
+    // not cooperative) and 1/wt for the row split (exact: (k + 1/2)/wt is at least
+    // 1/(2 wt) from an integer, far above fp32 rounding for k, wt < 2^11)
+    const uint32_t tx0 = (uint32_t)(c0 >> 3), ty0 = (uint32_t)(r0 >> 3);
+    const uint32_t wt = coop ? (uint32_t)((c1 >> 3) - (c0 >> 3) + 1) : 0u;
+    const uint32_t rect = tx0 | (ty0 << 11) | (wt << 22);
+    const float iwt = coop ? 1.0f / (float)wt : 0.0f;
     for (uint32_t p = 0; p < seg_len; p += 32) {
         const uint32_t q = p + (uint32_t)lane;
         int lo = 0;  // owner: the last lane whose start is <= q
@@ -81,15 +89,14 @@ __global__ void __launch_bounds__(256) k_duplicate_ranked(const uint4* __restric
             if (lo + step < 32 && e <= q) lo += step;
         }
         const uint32_t ek = __shfl_sync(0xffffffffu, excl, lo);
-        const int o_coop = __shfl_sync(0xffffffffu, (int)coop, lo);
-        const int o_tx0 = __shfl_sync(0xffffffffu, tx0, lo);
-        const int o_ty0 = __shfl_sync(0xffffffffu, ty0, lo);
-        const int o_wt = __shfl_sync(0xffffffffu, wt, lo);
+        const uint32_t o_rect = __shfl_sync(0xffffffffu, rect, lo);
+        const float o_iwt = __shfl_sync(0xffffffffu, iwt, lo);
         const uint32_t o_i = __shfl_sync(0xffffffffu, i, lo);
-        if (q < seg_len && o_coop) {
+        const uint32_t o_wt = o_rect >> 22;
+        if (q < seg_len && o_wt) {
             const uint32_t k = q - ek;
-            const uint32_t dy = k / (uint32_t)o_wt, dx = k - dy * (uint32_t)o_wt;
-            keys[base + seg0 + q] = (uint32_t)((o_ty0 + (int)dy) * TW + o_tx0 + (int)dx);
+            const uint32_t dy = (uint32_t)(((float)k + 0.5f) * o_iwt), dx = k - dy * o_wt;
+            keys[base + seg0 + q] = ((o_rect >> 11) & 2047u) * (uint32_t)TW + dy * (uint32_t)TW + (o_rect & 2047u) + dx;
             vals[base + seg0 + q] = o_i;
         }
     }
@@ -124,11 +131,22 @@ __global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ key
                                                 int64_t end, uint32_t tile_base,
                                                 uint32_t* __restrict__ tile_start,
                                                 uint32_t* __restrict__ tile_end) {
-    const int64_t j = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= end) return;
-    const uint32_t t = keys[j];
-    if (j == begin || keys[j - 1] != t) tile_start[tile_base + t] = (uint32_t)j;
-    if (j == end - 1 || keys[j + 1] != t) tile_end[tile_base + t] = (uint32_t)(j + 1);
+    // four consecutive keys per thread (loads issued together), neighbours through L1
+    const int64_t j0 = begin + 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+    if (j0 >= end) return;
+    uint32_t k[6];
+#pragma unroll
+    for (int u = 0; u < 6; ++u) {
+        const int64_t j = j0 - 1 + u;
+        k[u] = (j >= begin && j < end) ? keys[j] : 0xffffffffu;
+    }
+#pragma unroll
+    for (int u = 1; u <= 4; ++u) {
+        const int64_t j = j0 - 1 + u;
+        if (j >= end) break;
+        if (k[u - 1] != k[u]) tile_start[tile_base + k[u]] = (uint32_t)j;
+        if (k[u + 1] != k[u]) tile_end[tile_base + k[u]] = (uint32_t)(j + 1);
+    }
 }
 
 // Per (light, tile): number of chunks (>= 1, an empty tile still writes T = 1)
@@ -234,9 +252,10 @@ void launch_depth_keys(const uint4* dup, int64_t n, uint32_t dmin, uint32_t* key
     k_depth_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dup, n, dmin, keys, vals);
 }
 
-void launch_gather_counts(const uint4* dup, const uint32_t* perm, int64_t n, uint32_t* cperm, cudaStream_t s) {
+void launch_gather_counts(const uint32_t* counts, const uint32_t* perm, int64_t n, uint32_t* cperm,
+                          cudaStream_t s) {
     if (n <= 0) return;
-    k_gather_counts<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dup, perm, n, cperm);
+    k_gather_counts<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(counts, perm, n, cperm);
 }
 
 void launch_duplicate_ranked(const uint4* dup, const uint32_t* perm, const uint64_t* offs, int64_t n, int res,
@@ -261,7 +280,7 @@ void launch_decode_keys(const uint32_t* keys, const uint32_t* vals, const uint4*
 void launch_ranges(const uint32_t* keys, int64_t begin, int64_t end, uint32_t tile_base, uint32_t* tile_start,
                    uint32_t* tile_end, cudaStream_t s) {
     if (end <= begin) return;
-    k_ranges<<<(unsigned)((end - begin + 255) / 256), 256, 0, s>>>(keys, begin, end, tile_base, tile_start,
+    k_ranges<<<(unsigned)((end - begin + 1023) / 1024), 256, 0, s>>>(keys, begin, end, tile_base, tile_start,
                                                                     tile_end);
 }
 

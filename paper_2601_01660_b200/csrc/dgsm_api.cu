@@ -389,7 +389,7 @@ static void run_binning(const dgsm_gaussians_t* g, int n_lights, const dgsm_buil
                                            r.sort_temp, s, &g_launches);
         const uint32_t* perm = fl ? r.gvals_b : r.gvals_a;
         // 2. emission offsets in depth-rank order
-        launch_gather_counts(dup, perm, n, r.cperm, s);
+        launch_gather_counts(p.counts + (int64_t)l * n, perm, n, r.cperm, s);
         launch_scan_u32_to_u64(r.cperm, r.offs_perm, n, r.gscan_temp, s);
         // 3. key duplication (key = tile, value = Gaussian index)
         const uint64_t* tm = o.slab ? slab_mask_ptr(o.slab) + (int64_t)l * n_tiles : nullptr;

@@ -201,7 +201,8 @@ void launch_plan_stats(const uint64_t* offsets, int64_t n, int n_lights, PlanSta
 // dup[l*n + i] = {fp32 bits of D, c0 | c1 << 16, r0 | r1 << 16, tile count} (16 B per (light, Gaussian))
 void launch_depth_keys(const uint4* dup, int64_t n, uint32_t dmin, uint32_t* keys, uint32_t* vals,
                        cudaStream_t s);
-void launch_gather_counts(const uint4* dup, const uint32_t* perm, int64_t n, uint32_t* cperm, cudaStream_t s);
+void launch_gather_counts(const uint32_t* counts, const uint32_t* perm, int64_t n, uint32_t* cperm,
+                          cudaStream_t s);
 void launch_duplicate_ranked(const uint4* dup, const uint32_t* perm, const uint64_t* offs, int64_t n, int res,
                              int bin_mode, uint64_t base, const uint64_t* tile_mask, uint32_t* keys,
                              uint32_t* vals, cudaStream_t s);
