@@ -439,13 +439,13 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
         };
         // register staging: thread t < 32 holds record t of the next stage (6 x 16-B
         // loads issued before the current stage's compute)
-        union RecRegs { uint4 u[6]; PairRec r; } rr;
+        uint4 ru[6];  // PairRec as six 16-B words (no union: the loads land in place)
         auto fetch = [&](uint32_t b) {
             const uint32_t j0 = wu.jbeg + b * kStage;
             if ((uint32_t)tid < min((uint32_t)kStage, wu.jend - j0)) {
                 const uint4* src = reinterpret_cast<const uint4*>(lrecs + vals[j0 + tid]);
 #pragma unroll
-                for (int k = 0; k < 6; ++k) rr.u[k] = __ldg(src + k);
+                for (int k = 0; k < 6; ++k) ru[k] = __ldg(src + k);
             }
         };
         if (n_batches > 0) {
@@ -459,12 +459,33 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
             }
             const uint32_t nb = min((uint32_t)kStage, n_rec - b * kStage);
             if ((uint32_t)tid < nb) {  // transform: raw record -> compact, relative to d_c
-                const PairRec& R = kTMA ? s_raw[tid] : rr.r;
                 float* q = reinterpret_cast<float*>(s_cr) + (tid >> 1) * (2 * kPairFields) + (tid & 1);
-                float v[kPairFields] = {(float)(R.di[0] - c0), (float)(R.di[1] - c1), (float)(R.di[2] - c2),
-                                        R.rcut_D2, R.g[0], R.g[1], R.g[2], R.D,
-                                        R.W[0], R.W[1], R.W[2], R.W[3], R.W[4], R.W[5], R.W[6], R.W[7], R.W[8],
-                                        R.eD, R.betap, (float)R.kD};
+                float v[kPairFields];
+                if (kTMA) {
+                    const PairRec& R = s_raw[tid];
+                    const float vv[kPairFields] = {(float)(R.di[0] - c0), (float)(R.di[1] - c1), (float)(R.di[2] - c2),
+                                                   R.rcut_D2, R.g[0], R.g[1], R.g[2], R.D,
+                                                   R.W[0], R.W[1], R.W[2], R.W[3], R.W[4], R.W[5], R.W[6], R.W[7],
+                                                   R.W[8], R.eD, R.betap, (float)R.kD};
+#pragma unroll
+                    for (int f = 0; f < kPairFields; ++f) v[f] = vv[f];
+                } else {  // field offsets of PairRec (static_assert'ed 96 B layout)
+                    const float vv[kPairFields] = {
+                        (float)(__hiloint2double((int)ru[0].y, (int)ru[0].x) - c0),
+                        (float)(__hiloint2double((int)ru[0].w, (int)ru[0].z) - c1),
+                        (float)(__hiloint2double((int)ru[1].y, (int)ru[1].x) - c2),
+                        __uint_as_float(ru[5].z),                                                   // rcut_D2
+                        __uint_as_float(ru[1].z), __uint_as_float(ru[1].w), __uint_as_float(ru[2].x),  // g
+                        __uint_as_float(ru[4].z),                                                   // D
+                        __uint_as_float(ru[2].y), __uint_as_float(ru[2].z), __uint_as_float(ru[2].w),  // W
+                        __uint_as_float(ru[3].x), __uint_as_float(ru[3].y), __uint_as_float(ru[3].z),
+                        __uint_as_float(ru[3].w), __uint_as_float(ru[4].x), __uint_as_float(ru[4].y),
+                        __uint_as_float(ru[4].w),                                                   // eD
+                        __uint_as_float(ru[5].y),                                                   // betap
+                        (float)(int)ru[5].x};                                                       // kD
+#pragma unroll
+                    for (int f = 0; f < kPairFields; ++f) v[f] = vv[f];
+                }
 #pragma unroll
                 for (int f = 0; f < kPairFields; ++f) q[2 * f] = v[f];
             }

@@ -1,6 +1,7 @@
 // dgsm_internal.cuh — internal layouts and launch helpers of libdgsm.so.
 // Nothing here is shared with oracle/ (which has its own independent code).
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -27,6 +28,11 @@ struct __align__(16) PairRec {
     float pad;
 };
 static_assert(sizeof(PairRec) == 96, "PairRec must be 96 B");
+// field offsets the accumulation kernel's register staging reads by word (accumulate.cu)
+static_assert(offsetof(PairRec, g) == 24 && offsetof(PairRec, W) == 36 && offsetof(PairRec, D) == 72 &&
+                  offsetof(PairRec, eD) == 76 && offsetof(PairRec, kD) == 80 && offsetof(PairRec, betap) == 84 &&
+                  offsetof(PairRec, rcut_D2) == 88,
+              "PairRec layout");
 
 struct LightsParam {
     float4 l[DGSM_MAX_LIGHTS];  // xyz = o_L, w = t_max
