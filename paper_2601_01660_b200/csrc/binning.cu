@@ -100,30 +100,46 @@ __global__ void __launch_bounds__(256) k_duplicate_ranked(const uint4* __restric
             vals[base + seg0 + q] = o_i;
         }
     }
-    if (!valid || r.w == 0 || coop) return;
-    uint64_t o = base + offs[j];
-    const uint64_t end = o + r.w;  // never more keys than the plan counted (a slab changed since the plan)
-    if (in_grid) {  // in the grid, under a ROI slab mask
-        for (int ty = r0 >> 3; ty <= (r1 >> 3); ++ty)
-            for (int tx = c0 >> 3; tx <= (c1 >> 3); ++tx) {
-                if (tm && (tm[ty * TW + tx] == 0ull || o == end)) continue;  // outside the ROI slab
-                keys[o] = (uint32_t)(ty * TW + tx);
-                vals[o] = i;
-                ++o;
+    // The rest (Gaussians whose footprint wraps across the atlas border, or any
+    // Gaussian under a ROI slab mask) one Gaussian at a time by the whole warp:
+    // the lanes walk its tile rectangles 32 tiles per round and place the kept
+    // tiles by ballot prefix.  A Gaussian's tiles are distinct, so the order
+    // inside its run does not change the sorted result (the tile sort is stable
+    // across Gaussians only).
+    uint32_t pend = __ballot_sync(0xffffffffu, valid && r.w > 0 && !coop);
+    const uint64_t my_o = valid ? offs[j] : 0ull;
+    const uint32_t lt = (1u << lane) - 1u;
+    while (pend) {
+        const int L = __ffs(pend) - 1;
+        pend &= pend - 1u;
+        const int Lc0 = __shfl_sync(0xffffffffu, c0, L), Lc1 = __shfl_sync(0xffffffffu, c1, L);
+        const int Lr0 = __shfl_sync(0xffffffffu, r0, L), Lr1 = __shfl_sync(0xffffffffu, r1, L);
+        const uint32_t Li = __shfl_sync(0xffffffffu, i, L), Lw = __shfl_sync(0xffffffffu, r.w, L);
+        uint64_t o = base + __shfl_sync(0xffffffffu, my_o, L);
+        const uint64_t end = o + Lw;  // never more keys than the plan counted (a slab changed since the plan)
+        TileRects TR;
+        make_tile_rects(Lc0, Lc1, Lr0, Lr1, res, Lc0 >= 0 && Lc1 <= res - 1 && Lr0 >= 0 && Lr1 <= res - 1
+                                                     ? DGSM_BIN_CLAMP : bin_mode, TR);
+#pragma unroll 1
+        for (int q = 0; q < TR.n; ++q) {
+            const int w = TR.tx1[q] - TR.tx0[q] + 1;
+            const int cnt = w * (TR.ty1[q] - TR.ty0[q] + 1);
+            for (int b0 = 0; b0 < cnt; b0 += 32) {
+                const int idx = b0 + lane;
+                const int ty = TR.ty0[q] + idx / w, tx = TR.tx0[q] + idx % w;
+                bool ok = idx < cnt;
+                if (ok && q > 0) ok = !in_earlier_rect(TR, q, tx, ty);
+                if (ok && tm) ok = tm[ty * TW + tx] != 0ull;
+                const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+                const uint64_t at = o + __popc(bal & lt);
+                if (ok && at < end) {
+                    keys[at] = (uint32_t)(ty * TW + tx);
+                    vals[at] = Li;
+                }
+                o += __popc(bal);
             }
-        return;
+        }
     }
-    TileRects TR;
-    make_tile_rects(c0, c1, r0, r1, res, bin_mode, TR);
-    for (int q = 0; q < TR.n; ++q)
-        for (int ty = TR.ty0[q]; ty <= TR.ty1[q]; ++ty)
-            for (int tx = TR.tx0[q]; tx <= TR.tx1[q]; ++tx) {
-                if (q > 0 && in_earlier_rect(TR, q, tx, ty)) continue;
-                if (tm && (tm[ty * TW + tx] == 0ull || o == end)) continue;
-                keys[o] = (uint32_t)(ty * TW + tx);
-                vals[o] = i;
-                ++o;
-            }
 }
 
 // Tile ranges over one light's sorted segment [begin, end): absolute positions.
