@@ -1,6 +1,6 @@
 // onesweep.cu — stable LSD radix sort of (key, u32 value) pairs, key = u32 or
 // u64, in the "onesweep" style: one histogram pass over all digits, then ONE
-// kernel per 8-bit digit that ranks a 2048-key partition in shared memory (warp
+// kernel per digit (<= 8 bits) that ranks a 2048-key partition in shared memory (warp
 // multi-split by ballots, or match.any on a narrow top digit), obtains its global digit offsets by decoupled
 // look-back over earlier partitions (8 predecessors per round trip), and
 // scatters through shared memory for coalesced writes.  Partition ids come from
@@ -27,9 +27,15 @@ constexpr int kRadix = 256;
 constexpr int kMaxPasses = 8;
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
 
+// Digit of each pass: bits [shift, shift + bits) of the key, bits <= 8.  The
+// passes split the key's significant bits evenly (a 12-bit tile key: 6 + 6).
+struct PassDigits {
+    int shift[kMaxPasses], bits[kMaxPasses];
+};
+
 template <typename KeyT>
 __global__ void __launch_bounds__(256) k_hist(const KeyT* __restrict__ keys, int64_t n, int passes,
-                                              uint32_t* __restrict__ hist) {
+                                              PassDigits pd, uint32_t* __restrict__ hist) {
     __shared__ uint32_t sh[kMaxPasses][kRadix];
     for (int t = threadIdx.x; t < kMaxPasses * kRadix; t += blockDim.x) (&sh[0][0])[t] = 0;
     __syncthreads();
@@ -45,7 +51,8 @@ __global__ void __launch_bounds__(256) k_hist(const KeyT* __restrict__ keys, int
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             if (j0 + u * stride >= n) break;
-            for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(uint32_t)(k[u] >> (8 * p)) & 255u], 1u);
+            for (int p = 0; p < passes; ++p)
+                atomicAdd(&sh[p][(uint32_t)(k[u] >> pd.shift[p]) & ((1u << pd.bits[p]) - 1u)], 1u);
         }
     }
     __syncthreads();
@@ -93,7 +100,7 @@ template <typename KeyT>
 __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ kin,
                                                       const uint32_t* __restrict__ vin,
                                                       KeyT* __restrict__ kout, uint32_t* __restrict__ vout,
-                                                      int64_t n, int shift, int bits,
+                                                      int64_t n, int shift, int bits, bool top,
                                                       const uint32_t* __restrict__ gofs,
                                                       uint32_t* status, uint32_t* status_next,
                                                       uint32_t* part_ctr) {
@@ -118,23 +125,25 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ k
 
     KeyT k[kItems];
     uint32_t v[kItems], dig[kItems], rank[kItems];
+    const uint32_t dmask = (1u << bits) - 1u;
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
         const int64_t idx = base + j * 32 + lane;
         const bool valid = idx < n;
         k[j] = valid ? kin[idx] : (KeyT)0;
         v[j] = valid ? vin[idx] : 0u;
-        dig[j] = valid ? ((uint32_t)(k[j] >> shift) & 255u) : 256u;
+        dig[j] = valid ? ((uint32_t)(k[j] >> shift) & dmask) : 256u;
     }
     const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
         const uint32_t d = dig[j];
         // warp multi-split (lanes holding the same digit, or 256 = invalid): one ballot
-        // per digit bit on full 8-bit passes; match.any on a key's narrow top pass
-        // (few distinct digits per warp: measured faster there, slower on 8 bits)
+        // per digit bit, except on the key's top pass, whose digits are few within a
+        // warp (light distance and tile row are coherent there): match.any, measured
+        // faster there and slower on the low digits
         uint32_t peers;
-        if (bits < 8) {  // uniform
+        if (top) {  // uniform
             peers = __match_any_sync(0xffffffffu, d);
         } else {
             const bool inv = d >> 8;
@@ -142,9 +151,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ k
             peers = inv ? bv : ~bv;
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
-                const bool bit = (d >> b) & 1u;
-                const uint32_t bb = __ballot_sync(0xffffffffu, bit);
-                peers &= bit ? bb : ~bb;
+                if (b < bits) {  // uniform
+                    const bool bit = (d >> b) & 1u;
+                    const uint32_t bb = __ballot_sync(0xffffffffu, bit);
+                    peers &= bit ? bb : ~bb;
+                }
             }
         }
         uint32_t cnt = 0;
@@ -167,9 +178,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ k
     }
     const uint32_t tile_count = run;
 
-    // decoupled look-back (one thread per digit)
+    // decoupled look-back (one thread per digit; digits >= 2^bits never occur)
     volatile uint32_t* st = status;
-    if (part == 0) {
+    if (d > dmask) {
+        s_global[d] = 0u;
+    } else if (part == 0) {
         st[d] = kFlagInc | tile_count;
         s_global[d] = gofs[d];
     } else {
@@ -217,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ k
     const int n_valid = rem < kTileKeys ? (int)rem : kTileKeys;
     for (int x = tid; x < n_valid; x += kThreads) {
         const KeyT key = s_keys[x];
-        const uint32_t dd = (uint32_t)(key >> shift) & 255u;
+        const uint32_t dd = (uint32_t)(key >> shift) & dmask;
         const uint32_t o = s_global[dd] + (uint32_t)x - s_tile_start[dd];
         kout[o] = key;
         vout[o] = s_vals[x];
@@ -260,16 +273,22 @@ int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt
     // histograms, partition counters and the first pass's status in one memset
     cudaMemsetAsync(t.hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix + 256 + sizeof(uint32_t) * kRadix * (size_t)parts,
                     s);
+    PassDigits pd;
+    for (int p = 0, sh = 0; p < passes; ++p) {
+        pd.bits[p] = nbits / passes + (p < nbits % passes ? 1 : 0);
+        pd.shift[p] = sh;
+        sh += pd.bits[p];
+    }
     const int hist_grid = (int)std::min<int64_t>(148 * 4, (n + 2047) / 2048);
-    k_hist<KeyT><<<hist_grid, 256, 0, s>>>(keys, n, passes, t.hist);
+    k_hist<KeyT><<<hist_grid, 256, 0, s>>>(keys, n, passes, pd, t.hist);
     k_hist_scan<<<passes, 256, 0, s>>>(t.hist);
     *launches += 2;
     KeyT *ki = keys, *ko = keys_alt;
     uint32_t *vi = vals, *vo = vals_alt;
     int flipped = 0;
     for (int p = 0; p < passes; ++p) {
-        const int bits = std::min(8, nbits - 8 * p);  // digit bits above the key's top bit are 0
-        k_pass<KeyT><<<(unsigned)parts, kThreads, dyn, s>>>(ki, vi, ko, vo, n, 8 * p, bits, t.hist + p * kRadix,
+        k_pass<KeyT><<<(unsigned)parts, kThreads, dyn, s>>>(ki, vi, ko, vo, n, pd.shift[p], pd.bits[p],
+                                                           p == passes - 1, t.hist + p * kRadix,
                                                            t.status[p & 1], t.status[(p + 1) & 1],
                                                            t.part_ctr + p);
         *launches += 1;
