@@ -21,7 +21,12 @@ namespace dgsm {
 
 namespace {
 constexpr int kThreads = 256;
-constexpr int kItems = 8;
+// tuning knobs (tools/ab_sort.sh on cfg2: 8 items and an 8-wide look-back window
+// measured best; 6/12/16 items and 16/32-wide windows slower)
+#ifndef DGSM_OS_ITEMS
+#define DGSM_OS_ITEMS 8
+#endif
+constexpr int kItems = DGSM_OS_ITEMS;
 constexpr int kTileKeys = kThreads * kItems;  // 2048 keys per partition (<= 64 regs: 4 CTAs/SM)
 constexpr int kRadix = 256;
 constexpr int kMaxPasses = 8;
@@ -94,6 +99,39 @@ __global__ void __launch_bounds__(256) k_hist_scan(uint32_t* hist) {
     const uint32_t v = h[threadIdx.x];
     const uint32_t e = block_excl_scan_u32(v, ws);
     h[threadIdx.x] = e;
+}
+
+#ifndef DGSM_OS_WIN_NARROW
+#define DGSM_OS_WIN_NARROW 8
+#endif
+#ifndef DGSM_OS_NARROW_BITS
+#define DGSM_OS_NARROW_BITS 6
+#endif
+// Decoupled look-back of digit d for partition `part`: sum the aggregates of the
+// predecessors, kWin per round trip, until an inclusive prefix is found;
+// re-poll from the first predecessor that has not published yet.
+template <int kWin>
+__device__ __forceinline__ uint32_t look_back(volatile uint32_t* st, uint32_t part, uint32_t d) {
+    uint32_t excl = 0;
+    int64_t q = (int64_t)part - 1;
+    while (true) {
+        uint32_t s[kWin];
+#pragma unroll
+        for (int i = 0; i < kWin; ++i) s[i] = (q - i >= 0) ? st[(size_t)(q - i) * kRadix + d] : 0u;
+        int i = 0;
+        bool done = false;
+#pragma unroll
+        for (int w = 0; w < kWin; ++w) {
+            if (done || w != i) continue;
+            const uint32_t f = s[w] & ~kValMask;
+            if (f == 0) continue;  // not ready: stop consuming this window
+            excl += s[w] & kValMask;
+            if (f == kFlagInc) done = true;
+            ++i;
+        }
+        if (done) return excl;
+        q -= i;
+    }
 }
 
 template <typename KeyT>
@@ -187,30 +225,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ k
         s_global[d] = gofs[d];
     } else {
         st[(size_t)part * kRadix + d] = kFlagAgg | tile_count;
-        // look back through a window of 8 predecessors per round trip: sum their
-        // aggregates until an inclusive prefix is found; re-poll from the first
-        // predecessor that has not published yet
-        uint32_t excl = 0;
-        int64_t q = (int64_t)part - 1;
-        constexpr int kWin = 8;
-        while (true) {
-            uint32_t s[kWin];
-#pragma unroll
-            for (int i = 0; i < kWin; ++i) s[i] = (q - i >= 0) ? st[(size_t)(q - i) * kRadix + d] : 0u;
-            int i = 0;
-            bool done = false;
-#pragma unroll
-            for (int w = 0; w < kWin; ++w) {
-                if (done || w != i) continue;
-                const uint32_t f = s[w] & ~kValMask;
-                if (f == 0) continue;  // not ready: stop consuming this window
-                excl += s[w] & kValMask;
-                if (f == kFlagInc) done = true;
-                ++i;
-            }
-            if (done) break;
-            q -= i;
-        }
+        // look back through a window of predecessors per round trip (wider when
+        // the pass has few digits: fewer look-back requests in flight per CTA)
+        const uint32_t excl = bits <= DGSM_OS_NARROW_BITS ? look_back<DGSM_OS_WIN_NARROW>(st, part, d)
+                                                          : look_back<8>(st, part, d);
         st[(size_t)part * kRadix + d] = kFlagInc | (excl + tile_count);
         s_global[d] = gofs[d] + excl;
     }
