@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(256, 4) k_project(  // (256, 3) and (256, 2) m
     const float q0 = rotations[4 * i], q1 = rotations[4 * i + 1], q2 = rotations[4 * i + 2], q3 = rotations[4 * i + 3];
     const float sc0 = scales[3 * i], sc1 = scales[3 * i + 1], sc2 = scales[3 * i + 2];
     const float alpha_in = opacities[i];
+    const float kappa_f = (float)kappa;
     // R4: m = mu - o, D = |m|; excluded when D <= 1e-6 (Q17)
     const double mx = (double)m0 - (double)L.x;
     const double my = (double)m1 - (double)L.y;
@@ -117,14 +118,13 @@ __global__ void __launch_bounds__(256, 4) k_project(  // (256, 3) and (256, 2) m
         if (tcnt > 0) {
             rc0 = (int16_t)c0; rc1 = (int16_t)c1; rr0 = (int16_t)r0; rr1 = (int16_t)r1;
             rec.di[0] = dx; rec.di[1] = dy; rec.di[2] = dz;
-            // record fields (not part of the binning contract): reciprocal multiplies
-            const double inv_all = 1.0 / ((s[0] * s[1]) * s[2]);  // one division for the three 1/s_j
-            const double inv_s[3] = {(s[1] * s[2]) * inv_all, (s[0] * s[2]) * inv_all, (s[0] * s[1]) * inv_all};
+            // record fields (not part of the binning contract; stored in fp32): fp32 math
+            const float is[3] = {1.0f / sc0, 1.0f / sc1, 1.0f / sc2};  // 1/s_j
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
-                rec.g[j] = (float)(w[j] * inv_s[j]);  // g = W d_i = diag(1/s) R^T d_i
+                rec.g[j] = (float)w[j] * is[j];  // g = W d_i = diag(1/s) R^T d_i
 #pragma unroll
-                for (int c = 0; c < 3; ++c) rec.W[3 * j + c] = (float)(R[c][j] * inv_s[j]);
+                for (int c = 0; c < 3; ++c) rec.W[3 * j + c] = (float)R[c][j] * is[j];
             }
             const float Df = (float)D;
             rec.D = Df;
@@ -137,23 +137,20 @@ __global__ void __launch_bounds__(256, 4) k_project(  // (256, 3) and (256, 2) m
             // tau* in fp32 (log1pf: no fp64 table lookups; betap is stored in fp32)
             float alpha = alpha_in;
             alpha = alpha < 1e-4f ? 1e-4f : (alpha > 1.0f - 1e-4f ? 1.0f - 1e-4f : alpha);
-            const double tau_star = (double)(-log1pf(-alpha));
-            const double trA = inv_s[0] * inv_s[0] + inv_s[1] * inv_s[1] + inv_s[2] * inv_s[2];
+            const float tau_star = -log1pf(-alpha);
+            const float trA = is[0] * is[0] + is[1] * is[1] + is[2] * is[2];
             // beta * sqrt(pi/2) for the chosen alpha -> beta mapping (ablation B)
-            double betap;
-            if (absorption == DGSM_ABS_SIMPLE) betap = kappa * tau_star * 1.2533141373155003;  // sqrt(pi/2)
-            else if (absorption == DGSM_ABS_TRACEAVG) betap = kappa * tau_star * sqrt(trA / 3.0) * 0.5;
-            else betap = kappa * tau_star * (inv_s[0] * inv_s[1] * inv_s[2]) * (1.0 / (4.0 * kPi));  // MASS, DIAG
-            rec.betap = (float)betap;
+            float betap;
+            if (absorption == DGSM_ABS_SIMPLE) betap = kappa_f * tau_star * 1.2533141373155003f;  // sqrt(pi/2)
+            else if (absorption == DGSM_ABS_TRACEAVG) betap = kappa_f * tau_star * sqrtf(trA / 3.0f) * 0.5f;
+            else betap = kappa_f * tau_star * (is[0] * is[1] * is[2]) * (float)(1.0 / (4.0 * kPi));  // MASS, DIAG
+            rec.betap = betap;
             // negligible-pair cut (R8'): a pair contributes at most 2 pref <=
             // 2 betap s_max exp(-r/2) to any tau_k (1/sqrt(a) <= s_max); it is skipped
             // when that bound is < 2^-32, i.e. r > r_cut, never above 180 (beyond which
-            // exp(-r/2) is exactly 0 in fp32).  fp32, from the stored fp32 W rows.
+            // exp(-r/2) is exactly 0 in fp32).  fp32.
             {
-                const float w0 = rec.W[0] * rec.W[0] + rec.W[1] * rec.W[1] + rec.W[2] * rec.W[2];  // 1/s_0^2
-                const float w1 = rec.W[3] * rec.W[3] + rec.W[4] * rec.W[4] + rec.W[5] * rec.W[5];
-                const float w2 = rec.W[6] * rec.W[6] + rec.W[7] * rec.W[7] + rec.W[8] * rec.W[8];
-                const float smax = rsqrtf(fminf(w0, fminf(w1, w2)));
+                const float smax = fmaxf(sc0, fmaxf(sc1, sc2));
                 const float rcut = fminf(2.0f * logf(2.0f * rec.betap * smax) + 44.3614195558365f, 180.0f);
                 rec.rcut_D2 = rcut / (Df * Df);
             }
