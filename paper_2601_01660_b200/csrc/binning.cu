@@ -260,6 +260,83 @@ __global__ void __launch_bounds__(256) k_decode(const uint32_t* __restrict__ key
     dout[j] = dup[(int64_t)l * n + i].x;
     io[j] = i;
 }
+
+// All of the above in one CTA for up to kFusedTiles (light, tile) pairs: unit
+// counts, their exclusive scan, the units and the longest-first scatter (one
+// launch instead of five; the scan and the class offsets stay in shared memory).
+constexpr int kFusedThreads = 1024;
+constexpr int64_t kFusedTiles = 64 * kFusedThreads;
+
+__global__ void __launch_bounds__(kFusedThreads) k_units_fused(const uint32_t* __restrict__ ts,
+                                                               const uint32_t* __restrict__ te, int64_t nt,
+                                                               int chunk, WorkUnit* __restrict__ units,
+                                                               uint32_t* n_units) {
+    __shared__ uint32_t s_class[kUnitClasses], s_base[kUnitClasses], s_fill[kUnitClasses];
+    __shared__ uint32_t s_wu[kFusedThreads / 32], s_ws[kFusedThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid < kUnitClasses) { s_class[tid] = 0u; s_fill[tid] = 0u; }
+    __syncthreads();
+    const int64_t per = (nt + kFusedThreads - 1) / kFusedThreads;
+    const int64_t t0 = (int64_t)tid * per, t1 = t0 + per < nt ? t0 + per : nt;
+    uint32_t nu = 0, ns = 0;  // units and scratch slots of this thread's tiles
+    for (int64_t t = t0; t < t1; ++t) {
+        const uint32_t len = te[t] - ts[t];
+        uint32_t c = (len + chunk - 1) / chunk;
+        if (c == 0) c = 1;
+        nu += c * kTileSplit;
+        ns += c > 1 ? c * kTileSplit : 0u;
+        for (uint32_t k = 0; k < c; ++k) {  // the sizes k_units gives these units
+            const uint32_t jb = min(k * (uint32_t)chunk, len), je = min(len, k * (uint32_t)chunk + (uint32_t)chunk);
+            atomicAdd(&s_class[unit_class(je - jb)], (uint32_t)kTileSplit);
+        }
+    }
+    // block exclusive scans of nu and ns
+    uint32_t iu = nu, is = ns;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t a = __shfl_up_sync(0xffffffffu, iu, o), b = __shfl_up_sync(0xffffffffu, is, o);
+        if (lane >= o) { iu += a; is += b; }
+    }
+    if (lane == 31) { s_wu[wid] = iu; s_ws[wid] = is; }
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t a = s_wu[lane], b = s_ws[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(0xffffffffu, a, o), y = __shfl_up_sync(0xffffffffu, b, o);
+            if (lane >= o) { a += x; b += y; }
+        }
+        s_wu[lane] = a; s_ws[lane] = b;
+        if (lane == 0) {
+            uint32_t base = 0;
+            for (int c = kUnitClasses - 1; c >= 0; --c) { s_base[c] = base; base += s_class[c]; }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) *n_units = s_wu[kFusedThreads / 32 - 1];
+    uint32_t slot = (wid ? s_ws[wid - 1] : 0u) + is - ns;
+    for (int64_t t = t0; t < t1; ++t) {
+        const uint32_t s = ts[t], e = te[t], len = e - s;
+        uint32_t nc = (len + chunk - 1) / chunk;
+        if (nc == 0) nc = 1;
+        for (uint32_t part = 0; part < (uint32_t)kTileSplit; ++part)
+            for (uint32_t c = 0; c < nc; ++c) {
+                WorkUnit w;
+                w.tile = (uint32_t)t;
+                w.jbeg = s + c * (uint32_t)chunk;
+                w.jend = min(e, w.jbeg + (uint32_t)chunk);
+                if (w.jbeg > e) w.jbeg = e;
+                w.chunk = c;
+                w.nchunks = nc;
+                w.slot = slot + part * nc;
+                w.part = part;
+                w.pad1 = 0;
+                const int cls = unit_class(w.jend - w.jbeg);
+                units[s_base[cls] + atomicAdd(&s_fill[cls], 1u)] = w;  // longest first (order within a class free)
+            }
+        if (nc > 1) slot += nc * kTileSplit;
+    }
+}
 }  // namespace
 
 void launch_depth_keys(const uint4* dup, int64_t n, uint32_t dmin, uint32_t* keys, uint32_t* vals,
@@ -304,6 +381,11 @@ void launch_units(const uint32_t* tile_start, const uint32_t* tile_end, int64_t 
                   uint64_t* unit_counts, uint64_t* unit_offsets, void* scan_temp, WorkUnit* units_tmp,
                   WorkUnit* units, uint32_t max_units, uint32_t* n_units_dev, uint32_t* class_hist,
                   uint32_t* class_fill, cudaStream_t s, int* launches) {
+    if (n_tiles_total <= kFusedTiles) {
+        k_units_fused<<<1, kFusedThreads, 0, s>>>(tile_start, tile_end, n_tiles_total, chunk, units, n_units_dev);
+        *launches += 1;
+        return;
+    }
     const unsigned g = (unsigned)((n_tiles_total + 255) / 256);
     k_unit_counts<<<g, 256, 0, s>>>(tile_start, tile_end, n_tiles_total, chunk, unit_counts);
     launch_scan_u64(unit_counts, unit_offsets, n_tiles_total, scan_temp, s);
