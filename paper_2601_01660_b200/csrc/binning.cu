@@ -261,64 +261,45 @@ __global__ void __launch_bounds__(256) k_decode(const uint32_t* __restrict__ key
     io[j] = i;
 }
 
-// All of the above in one CTA for up to kFusedTiles (light, tile) pairs: unit
-// counts, their exclusive scan, the units and the longest-first scatter (one
-// launch instead of five; the scan and the class offsets stay in shared memory).
+// All of the above in one CTA for up to kFusedTiles (light, tile) pairs: pass 1
+// counts the units per size class, pass 2 writes each unit at its class's next
+// position (longest first) and gives multi-chunk tiles their scratch slots from
+// a shared counter (slot positions are free: a tile's partials are combined in
+// chunk order from its own slots).  One launch instead of five.
 constexpr int kFusedThreads = 1024;
+
 constexpr int64_t kFusedTiles = 64 * kFusedThreads;
 
 __global__ void __launch_bounds__(kFusedThreads) k_units_fused(const uint32_t* __restrict__ ts,
                                                                const uint32_t* __restrict__ te, int64_t nt,
                                                                int chunk, WorkUnit* __restrict__ units,
                                                                uint32_t* n_units) {
-    __shared__ uint32_t s_class[kUnitClasses], s_base[kUnitClasses], s_fill[kUnitClasses];
-    __shared__ uint32_t s_wu[kFusedThreads / 32], s_ws[kFusedThreads / 32];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    __shared__ uint32_t s_class[kUnitClasses], s_fill[kUnitClasses], s_slots;
+    const int tid = threadIdx.x;
     if (tid < kUnitClasses) { s_class[tid] = 0u; s_fill[tid] = 0u; }
+    if (tid == 0) s_slots = 0u;
     __syncthreads();
-    const int64_t per = (nt + kFusedThreads - 1) / kFusedThreads;
-    const int64_t t0 = (int64_t)tid * per, t1 = t0 + per < nt ? t0 + per : nt;
-    uint32_t nu = 0, ns = 0;  // units and scratch slots of this thread's tiles
-    for (int64_t t = t0; t < t1; ++t) {
+    for (int64_t t = tid; t < nt; t += kFusedThreads) {
         const uint32_t len = te[t] - ts[t];
         uint32_t c = (len + chunk - 1) / chunk;
         if (c == 0) c = 1;
-        nu += c * kTileSplit;
-        ns += c > 1 ? c * kTileSplit : 0u;
-        for (uint32_t k = 0; k < c; ++k) {  // the sizes k_units gives these units
+        for (uint32_t k = 0; k < c; ++k) {  // the sizes pass 2 gives these units
             const uint32_t jb = min(k * (uint32_t)chunk, len), je = min(len, k * (uint32_t)chunk + (uint32_t)chunk);
             atomicAdd(&s_class[unit_class(je - jb)], (uint32_t)kTileSplit);
         }
     }
-    // block exclusive scans of nu and ns
-    uint32_t iu = nu, is = ns;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t a = __shfl_up_sync(0xffffffffu, iu, o), b = __shfl_up_sync(0xffffffffu, is, o);
-        if (lane >= o) { iu += a; is += b; }
-    }
-    if (lane == 31) { s_wu[wid] = iu; s_ws[wid] = is; }
     __syncthreads();
-    if (wid == 0) {
-        uint32_t a = s_wu[lane], b = s_ws[lane];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t x = __shfl_up_sync(0xffffffffu, a, o), y = __shfl_up_sync(0xffffffffu, b, o);
-            if (lane >= o) { a += x; b += y; }
-        }
-        s_wu[lane] = a; s_ws[lane] = b;
-        if (lane == 0) {
-            uint32_t base = 0;
-            for (int c = kUnitClasses - 1; c >= 0; --c) { s_base[c] = base; base += s_class[c]; }
-        }
+    if (tid == 0) {  // class bases, largest class first: s_class becomes the base
+        uint32_t base = 0;
+        for (int c = kUnitClasses - 1; c >= 0; --c) { const uint32_t k = s_class[c]; s_class[c] = base; base += k; }
+        *n_units = base;
     }
     __syncthreads();
-    if (tid == 0) *n_units = s_wu[kFusedThreads / 32 - 1];
-    uint32_t slot = (wid ? s_ws[wid - 1] : 0u) + is - ns;
-    for (int64_t t = t0; t < t1; ++t) {
+    for (int64_t t = tid; t < nt; t += kFusedThreads) {
         const uint32_t s = ts[t], e = te[t], len = e - s;
         uint32_t nc = (len + chunk - 1) / chunk;
         if (nc == 0) nc = 1;
+        const uint32_t slot = nc > 1 ? atomicAdd(&s_slots, nc * kTileSplit) : 0u;
         for (uint32_t part = 0; part < (uint32_t)kTileSplit; ++part)
             for (uint32_t c = 0; c < nc; ++c) {
                 WorkUnit w;
@@ -332,9 +313,8 @@ __global__ void __launch_bounds__(kFusedThreads) k_units_fused(const uint32_t* _
                 w.part = part;
                 w.pad1 = 0;
                 const int cls = unit_class(w.jend - w.jbeg);
-                units[s_base[cls] + atomicAdd(&s_fill[cls], 1u)] = w;  // longest first (order within a class free)
+                units[s_class[cls] + atomicAdd(&s_fill[cls], 1u)] = w;
             }
-        if (nc > 1) slot += nc * kTileSplit;
     }
 }
 }  // namespace
