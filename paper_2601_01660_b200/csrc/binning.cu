@@ -9,6 +9,8 @@
 //   2. k_gather_counts + scan                                 -> emission offsets in that order
 //   3. k_duplicate_ranked: each Gaussian, in depth-rank order, emits (tile, index)
 //   4. onesweep (stable) on the P tile keys                   -> (tile, D bits, index)
+#include <cstdlib>
+
 #include "dgsm_internal.cuh"
 
 namespace dgsm {
@@ -178,9 +180,16 @@ __global__ void __launch_bounds__(256) k_unit_counts(const uint32_t* __restrict_
     cnt[t] = (uint64_t)(c * kTileSplit) | ((uint64_t)(c > 1 ? c * kTileSplit : 0) << 32);
 }
 
-// Size class of a work unit for the longest-first dispatch order: 0 for an
-// empty tile, else 1 + floor(log2(keys)) (<= 31).
-__device__ __forceinline__ int unit_class(uint32_t len) { return len ? 32 - __clz(len) : 0; }
+// Size class of a work unit for the longest-first dispatch order, monotone in
+// its length: four classes per octave (len < 4: len itself).  Measured on cfg2:
+// a6 1.05 -> 1.01 ms against one class per octave (a tail of same-class units
+// that differ up to 2x in length).
+__device__ __forceinline__ int unit_class(uint32_t len) {
+    if (len < 4u) return (int)len;
+    const int msb = 31 - __clz(len);
+    const int c = 4 * (msb - 1) + (int)((len >> (msb - 2)) & 3u);
+    return c < kUnitClasses ? c : kUnitClasses - 1;
+}
 
 __global__ void __launch_bounds__(256) k_units(const uint32_t* __restrict__ ts,
                                                const uint32_t* __restrict__ te,
@@ -267,7 +276,6 @@ __global__ void __launch_bounds__(256) k_decode(const uint32_t* __restrict__ key
 // a shared counter (slot positions are free: a tile's partials are combined in
 // chunk order from its own slots).  One launch instead of five.
 constexpr int kFusedThreads = 1024;
-
 constexpr int64_t kFusedTiles = 64 * kFusedThreads;
 
 __global__ void __launch_bounds__(kFusedThreads) k_units_fused(const uint32_t* __restrict__ ts,
@@ -361,7 +369,8 @@ void launch_units(const uint32_t* tile_start, const uint32_t* tile_end, int64_t 
                   uint64_t* unit_counts, uint64_t* unit_offsets, void* scan_temp, WorkUnit* units_tmp,
                   WorkUnit* units, uint32_t max_units, uint32_t* n_units_dev, uint32_t* class_hist,
                   uint32_t* class_fill, cudaStream_t s, int* launches) {
-    if (n_tiles_total <= kFusedTiles) {
+    const bool force_multi = getenv("DGSM_UNITS_MULTI") != nullptr;  // tests: the > 64K-tile path
+    if (n_tiles_total <= kFusedTiles && !force_multi) {
         k_units_fused<<<1, kFusedThreads, 0, s>>>(tile_start, tile_end, n_tiles_total, chunk, units, n_units_dev);
         *launches += 1;
         return;

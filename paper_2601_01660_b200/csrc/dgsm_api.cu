@@ -29,7 +29,8 @@ int cuda_check(const char* where) {
 }
 
 constexpr size_t kAlign = 256;
-constexpr int kChunk = 1024;  // Gaussians per accumulation work unit
+constexpr int kChunk = 1024;  // Gaussians per accumulation work unit (512, 768, 2048 measured slower on cfg2)
+constexpr int kCounterWords = 8 + 2 * kUnitClasses;  // n_units, unit counter, class histogram + fill
 
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
@@ -82,7 +83,7 @@ struct RunLayout {
     uint64_t *unit_cnt, *unit_off;
     void* unit_scan_temp;
     WorkUnit *units, *units_tmp;
-    uint32_t* counters;  // [0] n_units, [1] unit counter, [32..63] unit class histogram, [64..95] class fill
+    uint32_t* counters;  // [0] n_units, [1] unit counter, then the unit class histogram and class fill (kUnitClasses each)
     int64_t zero_words;  // counters .. tile_end, cleared by one memset per run
     uint32_t* tile_arrive;
     unsigned long long* stats;  // [4] pairs, live pairs, window shells, steps (DGSM_COLLECT_STATS)
@@ -121,11 +122,11 @@ RunLayout run_layout(void* ws, const dgsm_plan_t& pl) {
     r.units = c.take<WorkUnit>(max_units);
     r.units_tmp = c.take<WorkUnit>(max_units);
     // zeroed together at the start of a run: counters, arrival counters, tile ranges
-    r.counters = c.take<uint32_t>(96 + kTileSplit * nt + 2 * nt);
-    r.tile_arrive = r.counters + 96;
+    r.counters = c.take<uint32_t>(kCounterWords + kTileSplit * nt + 2 * nt);
+    r.tile_arrive = r.counters + kCounterWords;
     r.tile_start = r.tile_arrive + kTileSplit * nt;
     r.tile_end = r.tile_start + nt;
-    r.zero_words = 96 + (kTileSplit + 2) * nt;
+    r.zero_words = kCounterWords + (kTileSplit + 2) * nt;
     r.stats = c.take<unsigned long long>(8);
     const int64_t max_slots = kTileSplit * (2 * (P / pl.chunk) + 1);
     r.scratch = c.take<float>((size_t)max_slots * pl.n_shells * (kTexels / kTileSplit));
@@ -428,7 +429,7 @@ int dgsm_build_run(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_
     cudaMemsetAsync(r.counters, 0, sizeof(uint32_t) * r.zero_words, s);
     run_binning(g, n_lights, o, plan, p, r, s);
     launch_units(r.tile_start, r.tile_end, nt, plan->chunk, r.unit_cnt, r.unit_off, r.unit_scan_temp, r.units_tmp,
-                 r.units, r.max_units, r.counters, r.counters + 32, r.counters + 64, s, &g_launches);
+                 r.units, r.max_units, r.counters, r.counters + 8, r.counters + 8 + kUnitClasses, s, &g_launches);
     if (o.flags & DGSM_COLLECT_STATS) cudaMemsetAsync(r.stats, 0, sizeof(unsigned long long) * 8, s);
     // a6: accumulate + exp
     launch_accumulate(r.units, r.counters, r.max_units, r.vals_a, p.recs, g->n, lp, n_lights, res, K, o.flags,

@@ -223,7 +223,7 @@ void launch_decode_keys(const uint32_t* keys, const uint32_t* vals, const uint4*
                         cudaStream_t s);
 void launch_ranges(const uint32_t* keys, int64_t begin, int64_t end, uint32_t tile_base, uint32_t* tile_start,
                    uint32_t* tile_end, cudaStream_t s);
-constexpr int kUnitClasses = 32;  // work-unit size classes (LPT dispatch order)
+constexpr int kUnitClasses = 128;  // work-unit size classes (LPT dispatch order, binning.cu unit_class)
 void launch_units(const uint32_t* tile_start, const uint32_t* tile_end, int64_t n_tiles_total, int chunk,
                   uint64_t* unit_counts, uint64_t* unit_offsets, void* scan_temp, WorkUnit* units_tmp,
                   WorkUnit* units, uint32_t max_units, uint32_t* n_units_dev, uint32_t* class_hist,

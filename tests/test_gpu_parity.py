@@ -426,6 +426,23 @@ def test_accumulate_staging_variants(dg, oracle_mod, staging, monkeypatch):
     assert torch.equal(T, dg.build(g, s.lights, s.res, s.K))
 
 
+def test_work_unit_paths_identical(dg, oracle_mod, monkeypatch):
+    """The single-CTA work-unit builder (<= 64 K tiles) and the multi-kernel one
+    (larger atlases; forced here) give the same atlas, bit for bit, on a scene
+    with multi-chunk tiles (> 1024 keys), and it matches the oracle."""
+    s = synth.random_scene(33, 20000, res=32, K=16, L=2, dist=(0.3, 3.0), scale=(0.01, 0.3))
+    g = dg.to_device(s.gaussians)
+    plan = dg.BuildPlan(g, s.lights, s.res, s.K)
+    (_, t, _, _), (ts, te) = plan.bins()
+    assert int((te - ts).max()) > 2 * 1024  # several chunks per tile
+    T = dg.build(g, s.lights, s.res, s.K)
+    monkeypatch.setenv("DGSM_UNITS_MULTI", "1")
+    assert torch.equal(T, dg.build(g, s.lights, s.res, s.K))
+    To, _ = oracle_mod.build(s.gaussians, s.lights, s.res, s.K, tile_stride=5)
+    m = ~np.isnan(To)
+    assert np.abs(T.cpu().numpy()[m] - To[m]).max() <= TOL_T
+
+
 def test_frame_host_pipelined_frames(dg):
     """Back-to-back frames with different inputs, no synchronisation between them
     (frame i+1's uploads overlap frame i's build): each equals its device path."""
