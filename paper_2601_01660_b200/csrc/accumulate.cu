@@ -373,7 +373,7 @@ __device__ __forceinline__ void pair_live_warp2(const PairTest2& T, uint32_t acc
 }
 
 template <bool kStats, bool kTMA>
-__global__ void __launch_bounds__(kThreads) k_accumulate(
+__global__ void __launch_bounds__(kThreads, 11) k_accumulate(  // 11 CTAs/SM at K = 64 (<= 88 registers)
     const WorkUnit* __restrict__ units, const uint32_t* __restrict__ n_units_dev,
     const uint32_t* __restrict__ vals, const PairRec* __restrict__ recs, int64_t n, AccLights al,
     int res, int K, uint32_t flags, float* __restrict__ scratch, uint32_t* tile_arrive,
@@ -570,11 +570,24 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(
             if (s_last) {
                 __threadfence();
                 const float* base = scratch + ((size_t)wu.slot * K) * kThreads + tid;
-                for (int k = 0; k < K; ++k) {
-                    float t = 0.0f;
-                    for (uint32_t c = 0; c < wu.nchunks; ++c)
-                        t += __ldcg(base + ((size_t)c * K + k) * kThreads);
-                    out[(size_t)k * plane] = (k < klo || k > khi) ? one : (want_tau ? t : expf(-t));
+                // kCB shells at a time: kCB independent L2 loads per chunk in flight
+                // (the summation order per shell stays chunk 0, 1, ...: deterministic)
+                constexpr int kCB = 16;
+                for (int k0 = 0; k0 < K; k0 += kCB) {
+                    float t[kCB];
+#pragma unroll
+                    for (int u = 0; u < kCB; ++u) t[u] = 0.0f;
+                    for (uint32_t c = 0; c < wu.nchunks; ++c) {
+                        const float* pc = base + ((size_t)c * K + k0) * kThreads;
+#pragma unroll
+                        for (int u = 0; u < kCB; ++u)
+                            if (k0 + u < K) t[u] += __ldcg(pc + (size_t)u * kThreads);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kCB; ++u) {
+                        const int k = k0 + u;
+                        if (k < K) out[(size_t)k * plane] = (k < klo || k > khi) ? one : (want_tau ? t[u] : expf(-t[u]));
+                    }
                 }
                 if (tid == 0) tile_arrive[tslot] = 0u;
             }

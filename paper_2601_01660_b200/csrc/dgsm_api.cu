@@ -29,7 +29,7 @@ int cuda_check(const char* where) {
 }
 
 constexpr size_t kAlign = 256;
-constexpr int kChunk = 1024;  // Gaussians per accumulation work unit (512, 768, 2048 measured slower on cfg2)
+constexpr int kChunk = 1024;  // Gaussians per accumulation work unit (512, 768, 1536, 2048 measured slower on cfg2)
 constexpr int kCounterWords = 8 + 2 * kUnitClasses;  // n_units, unit counter, class histogram + fill
 
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
