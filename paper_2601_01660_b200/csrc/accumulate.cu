@@ -373,7 +373,9 @@ __device__ __forceinline__ void pair_live_warp2(const PairTest2& T, uint32_t acc
 }
 
 template <bool kStats, bool kTMA>
-__global__ void __launch_bounds__(kThreads, 11) k_accumulate(  // 11 CTAs/SM at K = 64 (<= 88 registers)
+// (no min-blocks bound: 72 registers; forcing 11 CTAs/SM capped it at 80 with
+// extra instructions in the live path, and a wider combine batch raised it)
+__global__ void __launch_bounds__(kThreads) k_accumulate(  // 11 CTAs/SM at K = 64 (<= 88 registers)
     const WorkUnit* __restrict__ units, const uint32_t* __restrict__ n_units_dev,
     const uint32_t* __restrict__ vals, const PairRec* __restrict__ recs, int64_t n, AccLights al,
     int res, int K, uint32_t flags, float* __restrict__ scratch, uint32_t* tile_arrive,
@@ -572,7 +574,7 @@ __global__ void __launch_bounds__(kThreads, 11) k_accumulate(  // 11 CTAs/SM at 
                 const float* base = scratch + ((size_t)wu.slot * K) * kThreads + tid;
                 // kCB shells at a time: kCB independent L2 loads per chunk in flight
                 // (the summation order per shell stays chunk 0, 1, ...: deterministic)
-                constexpr int kCB = 16;
+                constexpr int kCB = 4;  // 2: slower; 6, 16: more registers for the whole kernel
                 for (int k0 = 0; k0 < K; k0 += kCB) {
                     float t[kCB];
 #pragma unroll
