@@ -35,6 +35,7 @@ namespace dgsm {
 namespace {
 constexpr int kThreads = kTexels / kTileSplit;  // one warp = one half of an 8x8 tile
 constexpr int kStage = 32;        // records per pipeline stage
+
 // Staging of the records (template kTMA): TMA bulk copies into a raw shared
 // buffer (kTMA), or 16-B loads into registers one stage ahead (no raw buffer).
 // launch_accumulate takes TMA unless the raw buffer costs a CTA per SM.
@@ -502,10 +503,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(  // 11 CTAs/SM at K = 
             }
             // two records per iteration: independent dependency chains for the pair test
             uint32_t my_live = 0;
-            uint32_t pr_addr = smem_addr(s_cr);  // induction variable: record pair (r, r+1)
-            for (uint32_t r = 0; r < nb; r += 2, pr_addr += kPairBytes) {
-                PairTest2 T2 = pair_test2(pr_addr, ETX, ETY, ETZ);
-                T2.liveB = T2.liveB && (r + 1 < nb);
+            auto process = [&](PairTest2& T2) {
                 if (kStats) {
                     const uint32_t ba = __ballot_sync(0xffffffffu, T2.liveA), bb = __ballot_sync(0xffffffffu, T2.liveB);
                     my_live += (uint32_t)T2.liveA + (uint32_t)T2.liveB;
@@ -514,7 +512,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(  // 11 CTAs/SM at K = 
                 const bool anyA = __any_sync(0xffffffffu, T2.liveA), anyB = __any_sync(0xffffffffu, T2.liveB);
                 if (anyA && anyB) {
                     pair_live_warp2<kStats>(T2, acc_base, K, dt, dtlo, idt, st_live, st_win, st_step);
-                    continue;
+                    return;
                 }
                 if (anyA)
                     pair_live_warp<kStats>(f2lo(T2.A), f2lo(T2.C2), f2lo(T2.DOT), T2.liveA, f2lo(T2.D), f2lo(T2.ED),
@@ -522,6 +520,22 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(  // 11 CTAs/SM at K = 
                 if (anyB)
                     pair_live_warp<kStats>(f2hi(T2.A), f2hi(T2.C2), f2hi(T2.DOT), T2.liveB, f2hi(T2.D), f2hi(T2.ED),
                                            f2hi(T2.BP), f2hi(T2.KD), acc_base, K, dt, dtlo, idt, st_live, st_win, st_step);
+            };
+            uint32_t pr_addr = smem_addr(s_cr);  // induction variable: record pair (r, r+1)
+            uint32_t r = 0;
+            // two record pairs' tests per iteration (twice the independent chains:
+            // 0.95 -> 0.93 ms at 80 registers; four pairs need 128 and are slower)
+            for (; r + 2 < nb; r += 4, pr_addr += 2 * kPairBytes) {
+                PairTest2 Ta = pair_test2(pr_addr, ETX, ETY, ETZ);
+                PairTest2 Tb = pair_test2(pr_addr + kPairBytes, ETX, ETY, ETZ);
+                Tb.liveB = Tb.liveB && (r + 3 < nb);
+                process(Ta);
+                process(Tb);
+            }
+            for (; r < nb; r += 2, pr_addr += kPairBytes) {
+                PairTest2 T2 = pair_test2(pr_addr, ETX, ETY, ETZ);
+                T2.liveB = T2.liveB && (r + 1 < nb);
+                process(T2);
             }
             if (kStats) st_wmax += __reduce_max_sync(0xffffffffu, my_live);
             cta_sync();  // compact copy consumed
