@@ -581,7 +581,9 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(  // 11 CTAs/SM at K = 
             }
             __threadfence();
             cta_sync();
-            if (tid == 0) s_last = (atomicAdd(&tile_arrive[tslot], 1u) == wu.nchunks - 1) ? 1u : 0u;
+            // (tiles of more than kInlineCombine chunks: k_combine_deferred sums them)
+            if (tid == 0) s_last = wu.nchunks <= kInlineCombine &&
+                                   atomicAdd(&tile_arrive[tslot], 1u) == wu.nchunks - 1 ? 1u : 0u;
             cta_sync();
             if (s_last) {
                 __threadfence();
@@ -612,6 +614,51 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(  // 11 CTAs/SM at K = 
     }
 }
 
+// Tiles with more than kInlineCombine chunks (a few dense tiles, e.g. an avatar
+// close to the light): their partial tau are summed here, by (tile, 4 shells)
+// items over the whole GPU instead of by the one CTA that finished last (which
+// made that CTA the kernel's tail).  Thread = (shell, texel); chunk order kept.
+__global__ void __launch_bounds__(256) k_combine_deferred(const WorkUnit* __restrict__ units,
+                                                          const uint32_t* __restrict__ deferred,
+                                                          const uint32_t* deferred_count, const float* __restrict__ scratch,
+                                                          int res, int K, uint32_t flags, float* __restrict__ atlas,
+                                                          const uint64_t* __restrict__ slab_mask,
+                                                          const int2* __restrict__ slab_k) {
+    const uint32_t nd = *deferred_count;
+    const int groups = (K + 3) / 4;
+    const int TW = res / kTile, n_tiles = TW * TW;
+    const size_t plane = (size_t)res * res;
+    const bool want_tau = (flags & DGSM_OUTPUT_TAU) != 0;
+    const float one = want_tau ? 0.0f : 1.0f;
+    for (uint32_t item = blockIdx.x; item < nd * (uint32_t)groups; item += gridDim.x) {
+        const WorkUnit wu = units[deferred[item / groups]];
+        const int k = (int)(item % groups) * 4 + (int)(threadIdx.x >> 6), tt = (int)(threadIdx.x & 63);
+        if (k >= K) continue;
+        const int l = (int)(wu.tile / (uint32_t)n_tiles), tile = (int)(wu.tile - (uint32_t)l * n_tiles);
+        const int row = (tile / TW) * kTile + (tt >> 3), col = (tile % TW) * kTile + (tt & 7);
+        const float* p = scratch + ((size_t)wu.slot * K + k) * kThreads + tt;
+        const size_t cs = (size_t)K * kThreads;  // one chunk's partials
+        float t = 0.0f;
+        uint32_t c = 0;
+        for (; c + 8 <= wu.nchunks; c += 8) {  // 8 loads in flight, added in chunk order
+            float v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldcg(p + (size_t)(c + u) * cs);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t += v[u];
+        }
+        for (; c < wu.nchunks; ++c) t += __ldcg(p + (size_t)c * cs);
+        int klo = 0, khi = K - 1;
+        if (slab_mask) {
+            const int2 kr = slab_k[l];
+            klo = kr.x;
+            khi = ((slab_mask[wu.tile] >> tt) & 1ull) ? kr.y : -1;
+        }
+        atlas[((size_t)l * K + k) * plane + (size_t)row * res + col] =
+            (k < klo || k > khi) ? one : (want_tau ? t : expf(-t));
+    }
+}
+
 __global__ void k_exp(const float* tau, float* T, int64_t count) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -631,7 +678,8 @@ void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint3
                        int n_lights, int res, int K, uint32_t flags, float* scratch,
                        uint32_t* tile_arrive, uint32_t* unit_counter, float* atlas,
                        unsigned long long* stats, const uint64_t* slab_mask, const int2* slab_k,
-                       cudaEvent_t ev_before, cudaEvent_t ev_after, cudaStream_t s) {
+                       const uint32_t* deferred, const uint32_t* deferred_count, cudaEvent_t ev_before,
+                       cudaEvent_t ev_after, cudaStream_t s) {
     AccLights al;
     for (int l = 0; l < DGSM_MAX_LIGHTS; ++l) {
         const double dt = l < n_lights ? (double)lp.l[l].w / K : 1.0;
@@ -676,6 +724,8 @@ void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint3
     else if (tma) k_accumulate<false, true><<<grid, kThreads, smem, s>>>(DGSM_ACC_ARGS);
     else k_accumulate<false, false><<<grid, kThreads, smem, s>>>(DGSM_ACC_ARGS);
 #undef DGSM_ACC_ARGS
+    k_combine_deferred<<<(unsigned)n_sm * 8, 256, 0, s>>>(units, deferred, deferred_count, scratch, res, K, flags, atlas,
+                                                         slab_mask, slab_k);
     last_staging_tma = tma;
     if (ev_after) cudaEventRecord(ev_after, s);
 }

@@ -233,7 +233,8 @@ __global__ void __launch_bounds__(256) k_units(const uint32_t* __restrict__ ts,
 __global__ void __launch_bounds__(256) k_units_lpt(const WorkUnit* __restrict__ in, const uint32_t* n_units,
                                                    const uint32_t* __restrict__ class_hist,
                                                    uint32_t* __restrict__ class_fill,
-                                                   WorkUnit* __restrict__ out) {
+                                                   WorkUnit* __restrict__ out, uint32_t* __restrict__ deferred,
+                                                   uint32_t* deferred_count) {
     __shared__ uint32_t s_base[kUnitClasses];
     if (threadIdx.x == 0) {
         uint32_t b = 0;
@@ -244,7 +245,9 @@ __global__ void __launch_bounds__(256) k_units_lpt(const WorkUnit* __restrict__ 
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
         const WorkUnit w = in[j];
         const int c = unit_class(w.jend - w.jbeg);
-        out[s_base[c] + atomicAdd(&class_fill[c], 1u)] = w;
+        const uint32_t pos = s_base[c] + atomicAdd(&class_fill[c], 1u);
+        out[pos] = w;
+        if (w.chunk == 0 && w.part == 0 && w.nchunks > kInlineCombine) deferred[atomicAdd(deferred_count, 1u)] = pos;
     }
 }
 
@@ -281,7 +284,8 @@ constexpr int64_t kFusedTiles = 64 * kFusedThreads;
 __global__ void __launch_bounds__(kFusedThreads) k_units_fused(const uint32_t* __restrict__ ts,
                                                                const uint32_t* __restrict__ te, int64_t nt,
                                                                int chunk, WorkUnit* __restrict__ units,
-                                                               uint32_t* n_units) {
+                                                               uint32_t* n_units, uint32_t* __restrict__ deferred,
+                                                               uint32_t* deferred_count) {
     __shared__ uint32_t s_class[kUnitClasses], s_fill[kUnitClasses], s_slots;
     const int tid = threadIdx.x;
     if (tid < kUnitClasses) { s_class[tid] = 0u; s_fill[tid] = 0u; }
@@ -321,7 +325,9 @@ __global__ void __launch_bounds__(kFusedThreads) k_units_fused(const uint32_t* _
                 w.part = part;
                 w.pad1 = 0;
                 const int cls = unit_class(w.jend - w.jbeg);
-                units[s_class[cls] + atomicAdd(&s_fill[cls], 1u)] = w;
+                const uint32_t pos = s_class[cls] + atomicAdd(&s_fill[cls], 1u);
+                units[pos] = w;
+                if (c == 0 && part == 0 && nc > kInlineCombine) deferred[atomicAdd(deferred_count, 1u)] = pos;
             }
     }
 }
@@ -368,10 +374,12 @@ void launch_ranges(const uint32_t* keys, int64_t begin, int64_t end, uint32_t ti
 void launch_units(const uint32_t* tile_start, const uint32_t* tile_end, int64_t n_tiles_total, int chunk,
                   uint64_t* unit_counts, uint64_t* unit_offsets, void* scan_temp, WorkUnit* units_tmp,
                   WorkUnit* units, uint32_t max_units, uint32_t* n_units_dev, uint32_t* class_hist,
-                  uint32_t* class_fill, cudaStream_t s, int* launches) {
+                  uint32_t* class_fill, uint32_t* deferred, uint32_t* deferred_count, cudaStream_t s,
+                  int* launches) {
     const bool force_multi = getenv("DGSM_UNITS_MULTI") != nullptr;  // tests: the > 64K-tile path
     if (n_tiles_total <= kFusedTiles && !force_multi) {
-        k_units_fused<<<1, kFusedThreads, 0, s>>>(tile_start, tile_end, n_tiles_total, chunk, units, n_units_dev);
+        k_units_fused<<<1, kFusedThreads, 0, s>>>(tile_start, tile_end, n_tiles_total, chunk, units, n_units_dev,
+                                                  deferred, deferred_count);
         *launches += 1;
         return;
     }
@@ -381,7 +389,7 @@ void launch_units(const uint32_t* tile_start, const uint32_t* tile_end, int64_t 
     k_units<<<g, 256, 0, s>>>(tile_start, tile_end, unit_offsets, n_tiles_total, chunk, units_tmp, n_units_dev,
                               class_hist);
     const unsigned gl = (unsigned)std::min<uint32_t>((max_units + 255) / 256, 148u * 8u);
-    k_units_lpt<<<gl, 256, 0, s>>>(units_tmp, n_units_dev, class_hist, class_fill, units);
+    k_units_lpt<<<gl, 256, 0, s>>>(units_tmp, n_units_dev, class_hist, class_fill, units, deferred, deferred_count);
     *launches += 3 + kScanLaunches;
 }
 

@@ -30,6 +30,8 @@ int cuda_check(const char* where) {
 
 constexpr size_t kAlign = 256;
 constexpr int kChunk = 1024;  // Gaussians per accumulation work unit (512, 768, 1536, 2048 measured slower on cfg2)
+constexpr int kMinChunk = 128;
+constexpr int64_t kMinUnits = 2048;
 constexpr int kCounterWords = 8 + 2 * kUnitClasses;  // n_units, unit counter, class histogram + fill
 
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
@@ -83,6 +85,7 @@ struct RunLayout {
     uint64_t *unit_cnt, *unit_off;
     void* unit_scan_temp;
     WorkUnit *units, *units_tmp;
+    uint32_t* deferred;  // see dgsm_internal.cuh kInlineCombine; count in counters[2]
     uint32_t* counters;  // [0] n_units, [1] unit counter, then the unit class histogram and class fill (kUnitClasses each)
     int64_t zero_words;  // counters .. tile_end, cleared by one memset per run
     uint32_t* tile_arrive;
@@ -121,6 +124,7 @@ RunLayout run_layout(void* ws, const dgsm_plan_t& pl) {
     r.max_units = (uint32_t)max_units;
     r.units = c.take<WorkUnit>(max_units);
     r.units_tmp = c.take<WorkUnit>(max_units);
+    r.deferred = c.take<uint32_t>(nt);  // units[] positions of the tiles k_combine_deferred sums
     // zeroed together at the start of a run: counters, arrival counters, tile ranges
     r.counters = c.take<uint32_t>(kCounterWords + kTileSplit * nt + 2 * nt);
     r.tile_arrive = r.counters + kCounterWords;
@@ -337,8 +341,12 @@ static int plan_impl(const dgsm_gaussians_t* g, const dgsm_gaussians_t* g_host, 
     plan->n_lights = n_lights;
     plan->atlas_res = atlas_res;
     plan->n_shells = n_shells;
-    plan->chunk = kChunk;
     plan->n_keys = (int64_t)hs.light_key_begin[n_lights];
+    // keys per accumulation work unit: kChunk, halved (down to kMinChunk) while
+    // the build would have fewer than kMinUnits full chunks, so that a small key
+    // set (an avatar's occluders) still spreads over the ~1600 resident CTAs
+    plan->chunk = kChunk;
+    while (plan->chunk > kMinChunk && plan->n_keys / plan->chunk < kMinUnits) plan->chunk /= 2;
     const int64_t n_tiles = (int64_t)(atlas_res / kTile) * (atlas_res / kTile);
     plan->tile_bits = bits_for((uint64_t)(n_tiles - 1));
     for (int l = 0; l <= n_lights; ++l) plan->light_key_begin[l] = (int64_t)hs.light_key_begin[l];
@@ -429,13 +437,14 @@ int dgsm_build_run(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_
     cudaMemsetAsync(r.counters, 0, sizeof(uint32_t) * r.zero_words, s);
     run_binning(g, n_lights, o, plan, p, r, s);
     launch_units(r.tile_start, r.tile_end, nt, plan->chunk, r.unit_cnt, r.unit_off, r.unit_scan_temp, r.units_tmp,
-                 r.units, r.max_units, r.counters, r.counters + 8, r.counters + 8 + kUnitClasses, s, &g_launches);
+                 r.units, r.max_units, r.counters, r.counters + 8, r.counters + 8 + kUnitClasses, r.deferred,
+                 r.counters + 2, s, &g_launches);
     if (o.flags & DGSM_COLLECT_STATS) cudaMemsetAsync(r.stats, 0, sizeof(unsigned long long) * 8, s);
     // a6: accumulate + exp
     launch_accumulate(r.units, r.counters, r.max_units, r.vals_a, p.recs, g->n, lp, n_lights, res, K, o.flags,
                       r.scratch, r.tile_arrive, r.counters + 1, atlas_out, r.stats, slab_mask_ptr(o.slab),
-                      slab_k_ptr(o.slab, n_lights, res), g_ev_before, g_ev_after, s);
-    g_launches += 1;
+                      slab_k_ptr(o.slab, n_lights, res), r.deferred, r.counters + 2, g_ev_before, g_ev_after, s);
+    g_launches += 2;  // accumulate + deferred combine
     return cuda_check("build run");
 }
 

@@ -223,19 +223,24 @@ void launch_decode_keys(const uint32_t* keys, const uint32_t* vals, const uint4*
                         cudaStream_t s);
 void launch_ranges(const uint32_t* keys, int64_t begin, int64_t end, uint32_t tile_base, uint32_t* tile_start,
                    uint32_t* tile_end, cudaStream_t s);
+// Multi-chunk tiles with at most this many chunks are combined by the
+// accumulation CTA that finishes their last chunk; the others (listed by the
+// unit builder) by k_combine_deferred after it (accumulate.cu).
+constexpr uint32_t kInlineCombine = 16;
 constexpr int kUnitClasses = 128;  // work-unit size classes (LPT dispatch order, binning.cu unit_class)
 void launch_units(const uint32_t* tile_start, const uint32_t* tile_end, int64_t n_tiles_total, int chunk,
                   uint64_t* unit_counts, uint64_t* unit_offsets, void* scan_temp, WorkUnit* units_tmp,
                   WorkUnit* units, uint32_t max_units, uint32_t* n_units_dev, uint32_t* class_hist,
-                  uint32_t* class_fill, cudaStream_t s, int* launches);
+                  uint32_t* class_fill, uint32_t* deferred, uint32_t* deferred_count, cudaStream_t s,
+                  int* launches);
 size_t accumulate_smem_bytes(int K, bool tma);
 bool accumulate_last_used_tma();  // staging of the last launch on this thread (benchmark info)
 void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint32_t max_units,
                        const uint32_t* vals, const PairRec* recs, int64_t n, const LightsParam& lp,
                        int n_lights, int res, int K, uint32_t flags, float* scratch, uint32_t* tile_arrive,
                        uint32_t* unit_counter, float* atlas, unsigned long long* stats,
-                       const uint64_t* slab_mask, const int2* slab_k,
-                       cudaEvent_t ev_before, cudaEvent_t ev_after, cudaStream_t s);
+                       const uint64_t* slab_mask, const int2* slab_k, const uint32_t* deferred,
+                       const uint32_t* deferred_count, cudaEvent_t ev_before, cudaEvent_t ev_after, cudaStream_t s);
 int transfer_chunks(int64_t n, int64_t M);
 size_t transfer_workspace_bytes(int n_theta, int n_phi, int64_t n);
 void launch_transfer(const ShParam& sp, int n_theta, int n_phi, float q, float eps, float s_max, float gamma,
