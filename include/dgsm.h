@@ -199,8 +199,10 @@ int dgsm_query(const float* atlas, const dgsm_light_t* lights, int n_lights, int
  * chunks, each projected as soon as it lands; build the atlas (plan + run, as
  * dgsm_build) into atlas_out (DEVICE, [L][K][H][W]); upload the receivers
  * (receivers_host, HOST float [m][3]) on a side stream while the atlas is
- * built; query them (dgsm_query) and copy T (HOST float [m]) back.  Stream-
- * ordered on `stream`: T_host is valid once `stream` has completed.
+ * built; query them (dgsm_query) and return T (HOST float [m]): a page-locked
+ * T_host is written directly by the query kernel over the bus, a pageable one
+ * through a device buffer and a copy.  Stream-ordered on `stream`: T_host is
+ * valid once `stream` has completed.
  *   ws, ws_bytes  caller-owned DEVICE workspace (256-B aligned).  *ws_required
  *                 receives the bytes needed: the plan part is known up front,
  *                 the run part after the plan — a call that returns

@@ -554,10 +554,22 @@ int dgsm_frame_host(const dgsm_gaussians_t* g_host, const dgsm_light_t* lights, 
     if (rc) return rc;
     launches += g_launches;
     cudaStreamWaitEvent(s, cs.done, 0);
-    rc = dgsm_query(atlas_out, lights, n_lights, atlas_res, n_shells, rec, m, Td, nullptr, stream);
+    // page-locked T_host: the query writes it directly over the bus (no separate
+    // device-to-host copy on the stream); pageable: device buffer + copy
+    float* Tq = Td;
+    bool direct = false;
+    if (m > 0) {
+        cudaPointerAttributes pa;
+        if (cudaPointerGetAttributes(&pa, T_host) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer) {
+            Tq = (float*)pa.devicePointer;
+            direct = true;
+        }
+        cudaGetLastError();  // (a pageable pointer is not an error here)
+    }
+    rc = dgsm_query(atlas_out, lights, n_lights, atlas_res, n_shells, rec, m, Tq, nullptr, stream);
     if (rc) return rc;
     launches += g_launches;
-    if (m > 0) cudaMemcpyAsync(T_host, Td, 4 * (size_t)m, cudaMemcpyDeviceToHost, s);
+    if (m > 0 && !direct) cudaMemcpyAsync(T_host, Td, 4 * (size_t)m, cudaMemcpyDeviceToHost, s);
     cudaEventRecord(slot_ev, s);  // this workspace is free again after this point
     g_launches = launches;
     return cuda_check("frame");

@@ -338,6 +338,10 @@ def test_frame_host_equals_device_path(dg, oracle_mod):
     at = fr(gh, rh, Th)  # workspace reused
     torch.cuda.synchronize()
     assert torch.equal(Th, T2.cpu()) and fr.launches > 10
+    Tp = torch.empty(rh.shape[0])  # pageable T: device buffer + copy instead of direct writes
+    fr(gh, rh, Tp)
+    torch.cuda.synchronize()
+    assert torch.equal(Tp, T2.cpu())
     To, _ = oracle_mod.build(s.gaussians, s.lights, s.res, s.K)
     assert np.abs(Th.numpy() - oracle_mod.query(To, s.lights, s.queries)).max() <= TOL_T
 
