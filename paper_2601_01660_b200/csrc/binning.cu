@@ -70,7 +70,10 @@ __global__ void __launch_bounds__(256) k_duplicate_ranked(const uint4* __restric
     int c0, c1, r0, r1;
     unpack_rect(r, c0, c1, r0, r1);
     const bool in_grid = c0 >= 0 && c1 <= res - 1 && r0 >= 0 && r1 <= res - 1;
-    const bool coop = r.w > 0 && in_grid && tm == nullptr;
+    // a footprint covering the whole texel grid bins every tile once (its wrapped
+    // rectangles only repeat tiles): the full grid as one cooperative rectangle
+    const bool full = c0 <= 0 && c1 >= res - 1 && r0 <= 0 && r1 >= res - 1;
+    const bool coop = r.w > 0 && (in_grid || full) && tm == nullptr;
     // segment of this warp and each lane's start within it
     const uint64_t seg0 = offs[j0];
     const uint32_t excl = (uint32_t)((valid ? offs[j] : offs[n]) - seg0);
@@ -78,8 +81,8 @@ __global__ void __launch_bounds__(256) k_duplicate_ranked(const uint4* __restric
     // the owner's rectangle packed in one word (tx0 | ty0 << 11 | wt << 22, wt = 0:
     // not cooperative) and 1/wt for the row split (exact: (k + 1/2)/wt is at least
     // 1/(2 wt) from an integer, far above fp32 rounding for k, wt < 2^11)
-    const uint32_t tx0 = (uint32_t)(c0 >> 3), ty0 = (uint32_t)(r0 >> 3);
-    const uint32_t wt = coop ? (uint32_t)((c1 >> 3) - (c0 >> 3) + 1) : 0u;
+    const uint32_t tx0 = full ? 0u : (uint32_t)(c0 >> 3), ty0 = full ? 0u : (uint32_t)(r0 >> 3);
+    const uint32_t wt = !coop ? 0u : (full ? (uint32_t)TW : (uint32_t)((c1 >> 3) - (c0 >> 3) + 1));
     const uint32_t rect = tx0 | (ty0 << 11) | (wt << 22);
     const float iwt = coop ? 1.0f / (float)wt : 0.0f;
     for (uint32_t p = 0; p < seg_len; p += 32) {

@@ -109,6 +109,8 @@ __global__ void __launch_bounds__(256, 4) k_project(  // (256, 3) and (256, 2) m
                                      slab_mask + (int64_t)l * (res / kTile) * (res / kTile));
         } else if (ic0 >= 0 && ic1 <= W - 1 && ir0 >= 0 && ir1 <= H - 1) {  // common case: inside the grid
             tcnt = (uint32_t)((ic1 >> 3) - (ic0 >> 3) + 1) * (uint32_t)((ir1 >> 3) - (ir0 >> 3) + 1);
+        } else if (ic0 <= 0 && ic1 >= W - 1 && ir0 <= 0 && ir1 >= H - 1) {  // covers the grid: every tile once
+            tcnt = (uint32_t)(W / kTile) * (uint32_t)(H / kTile);
         } else {
             TileRects TR;
             make_tile_rects(ic0, ic1, ir0, ir1, res, bin_mode, TR);
