@@ -92,15 +92,6 @@ __device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t x, uint32_t* wa
     return r;
 }
 
-// Exclusive scan of each pass's 256-bin histogram, in place (one CTA per pass).
-__global__ void __launch_bounds__(256) k_hist_scan(uint32_t* hist) {
-    __shared__ uint32_t ws[kThreads / 32];
-    uint32_t* h = hist + blockIdx.x * kRadix;
-    const uint32_t v = h[threadIdx.x];
-    const uint32_t e = block_excl_scan_u32(v, ws);
-    h[threadIdx.x] = e;
-}
-
 #ifndef DGSM_OS_WIN_NARROW
 #define DGSM_OS_WIN_NARROW 8
 #endif
@@ -139,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ k
                                                       const uint32_t* __restrict__ vin,
                                                       KeyT* __restrict__ kout, uint32_t* __restrict__ vout,
                                                       int64_t n, int shift, int bits, bool top,
-                                                      const uint32_t* __restrict__ gofs,
+                                                      const uint32_t* __restrict__ hist,
                                                       uint32_t* status, uint32_t* status_next,
                                                       uint32_t* part_ctr) {
     extern __shared__ __align__(16) unsigned char os_smem[];
@@ -172,6 +163,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ k
         v[j] = valid ? vin[idx] : 0u;
         dig[j] = valid ? ((uint32_t)(k[j] >> shift) & dmask) : 256u;
     }
+    // global digit offsets: exclusive scan of this pass's histogram (every CTA
+    // redoes it, 256 values from L2, instead of a separate scan launch)
+    const uint32_t gofs_d = block_excl_scan_u32(hist[tid], s_ws);
     const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
@@ -222,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ k
         s_global[d] = 0u;
     } else if (part == 0) {
         st[d] = kFlagInc | tile_count;
-        s_global[d] = gofs[d];
+        s_global[d] = gofs_d;
     } else {
         st[(size_t)part * kRadix + d] = kFlagAgg | tile_count;
         // look back through a window of predecessors per round trip (wider when
@@ -230,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ k
         const uint32_t excl = bits <= DGSM_OS_NARROW_BITS ? look_back<DGSM_OS_WIN_NARROW>(st, part, d)
                                                           : look_back<8>(st, part, d);
         st[(size_t)part * kRadix + d] = kFlagInc | (excl + tile_count);
-        s_global[d] = gofs[d] + excl;
+        s_global[d] = gofs_d + excl;
     }
     s_tile_start[d] = block_excl_scan_u32(tile_count, s_ws);
     __syncthreads();
@@ -299,8 +293,7 @@ int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt
     }
     const int hist_grid = (int)std::min<int64_t>(148 * 4, (n + 2047) / 2048);
     k_hist<KeyT><<<hist_grid, 256, 0, s>>>(keys, n, passes, pd, t.hist);
-    k_hist_scan<<<passes, 256, 0, s>>>(t.hist);
-    *launches += 2;
+    *launches += 1;
     KeyT *ki = keys, *ko = keys_alt;
     uint32_t *vi = vals, *vo = vals_alt;
     int flipped = 0;
