@@ -328,9 +328,9 @@ static int plan_impl(const dgsm_gaussians_t* g, const dgsm_gaussians_t* g_host, 
         launch_project(*g, lp, n_lights, atlas_res, n_shells, o, 0, g->n, p.recs, p.counts, p.dup, p.stats, s);
         g_launches += 1;
     }
-    launch_scan_u32_to_u64(p.counts, p.offsets, m, p.scan_temp, s);
-    launch_plan_stats(p.offsets, g->n, n_lights, p.stats, s);
-    g_launches += 2 + kScanLaunches;  // init, scan, plan stats
+    // key offsets; the scan also writes light_key_begin[l] = offsets[l n] into the plan stats
+    launch_scan_u32_to_u64_marks(p.counts, p.offsets, m, p.scan_temp, p.stats->light_key_begin, g->n, n_lights, s);
+    g_launches += 1 + kScanLaunches;  // init, scan
     if ((rc = cuda_check("plan launch"))) return rc;
     PlanStats hs;
     cudaMemcpyAsync(&hs, p.stats, sizeof(PlanStats), cudaMemcpyDeviceToHost, s);

@@ -203,7 +203,9 @@ size_t scan_u32_to_u64_temp_bytes(int64_t n);
 constexpr int kScanLaunches = 2;  // kernels per launch_scan_* call
 void launch_scan_u32_to_u64(const uint32_t* in, uint64_t* out, int64_t n, void* temp, cudaStream_t s);
 void launch_scan_u64(const uint64_t* in, uint64_t* out, int64_t n, void* temp, cudaStream_t s);
-void launch_plan_stats(const uint64_t* offsets, int64_t n, int n_lights, PlanStats* stats, cudaStream_t s);
+// ... and marks[i] = out[i * mark_stride] for i <= n_marks (written by the scan itself)
+void launch_scan_u32_to_u64_marks(const uint32_t* in, uint64_t* out, int64_t n, void* temp, uint64_t* marks,
+                                  int64_t mark_stride, int n_marks, cudaStream_t s);
 // dup[l*n + i] = {fp32 bits of D, c0 | c1 << 16, r0 | r1 << 16, tile count} (16 B per (light, Gaussian))
 void launch_depth_keys(const uint4* dup, int64_t n, uint32_t dmin, uint32_t* keys, uint32_t* vals,
                        cudaStream_t s);

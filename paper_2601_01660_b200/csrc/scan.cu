@@ -66,7 +66,8 @@ __global__ void __launch_bounds__(kScanThreads) k_reduce(const T* __restrict__ i
 template <typename T, typename O>
 __global__ void __launch_bounds__(kScanThreads) k_downsweep(const T* __restrict__ in, int64_t n, int64_t tpb,
                                                             const uint64_t* __restrict__ partials,
-                                                            O* __restrict__ out) {
+                                                            O* __restrict__ out, uint64_t* __restrict__ marks,
+                                                            int64_t mark_stride, int n_marks) {
     // padded: element e at e + e/16, so the blocked accesses (stride 16) spread over banks
     __shared__ uint64_t tile[kScanTile + kScanTile / kScanItems];
     auto at = [](int e) { return e + (e >> 4); };
@@ -105,31 +106,37 @@ __global__ void __launch_bounds__(kScanThreads) k_downsweep(const T* __restrict_
             const int64_t k = base + (int64_t)j * kScanThreads + threadIdx.x;
             if (k < n) out[k] = (O)tile[at(j * kScanThreads + threadIdx.x)];
         }
+        // marks[i] = out[i * mark_stride] (i <= n_marks; the plan's per-light key begins)
+        if (marks && threadIdx.x <= (unsigned)n_marks) {
+            const int64_t k = (int64_t)threadIdx.x * mark_stride;
+            if (k >= base && k < base + kScanTile && k < n) marks[threadIdx.x] = tile[at((int)(k - base))];
+        }
         carry += total;
         if (base + kScanTile >= n && threadIdx.x == 0) out[n] = (O)carry;
+        if (base + kScanTile >= n && marks && threadIdx.x <= (unsigned)n_marks &&
+            (int64_t)threadIdx.x * mark_stride >= n)
+            marks[threadIdx.x] = carry;
         __syncthreads();
     }
 }
 
 template <typename T, typename O>
-void scan_impl(const T* in, O* out, int64_t n, void* temp, cudaStream_t s) {
+void scan_impl(const T* in, O* out, int64_t n, void* temp, cudaStream_t s, uint64_t* marks = nullptr,
+               int64_t mark_stride = 1, int n_marks = 0) {
     uint64_t* partials = (uint64_t*)temp;
     if (n == 0) {
         cudaMemsetAsync(out, 0, sizeof(O), s);
+        if (marks) cudaMemsetAsync(marks, 0, sizeof(uint64_t) * (n_marks + 1), s);
         return;
     }
     const int64_t tiles = (n + kScanTile - 1) / kScanTile;
     const int64_t tpb = (tiles + kMaxBlocks - 1) / kMaxBlocks;
     const int64_t nb = (tiles + tpb - 1) / tpb;
     k_reduce<T><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, tpb, partials);
-    k_downsweep<T, O><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, tpb, partials, out);
+    k_downsweep<T, O><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, tpb, partials, out, marks, mark_stride,
+                                                            n_marks);
 }
 
-__global__ void k_plan_stats(const uint64_t* __restrict__ offsets, int64_t n, int n_lights,
-                             PlanStats* stats) {
-    int l = threadIdx.x;
-    if (l <= n_lights) stats->light_key_begin[l] = offsets[(int64_t)l * n];
-}
 }  // namespace
 
 size_t scan_u32_to_u64_temp_bytes(int64_t n) {
@@ -144,9 +151,9 @@ void launch_scan_u64(const uint64_t* in, uint64_t* out, int64_t n, void* temp, c
     scan_impl<uint64_t, uint64_t>(in, out, n, temp, s);
 }
 
-void launch_plan_stats(const uint64_t* offsets, int64_t n, int n_lights, PlanStats* stats,
-                       cudaStream_t s) {
-    k_plan_stats<<<1, DGSM_MAX_LIGHTS + 1, 0, s>>>(offsets, n, n_lights, stats);
+void launch_scan_u32_to_u64_marks(const uint32_t* in, uint64_t* out, int64_t n, void* temp, uint64_t* marks,
+                                  int64_t mark_stride, int n_marks, cudaStream_t s) {
+    scan_impl<uint32_t, uint64_t>(in, out, n, temp, s, marks, mark_stride, n_marks);
 }
 
 }  // namespace dgsm
