@@ -394,17 +394,20 @@ static void run_binning(const dgsm_gaussians_t* g, int n_lights, const dgsm_buil
         const uint4* dup = p.dup + (int64_t)l * n;
         // 1. light-distance digits on the Gaussians
         launch_depth_keys(dup, n, plan->depth_min[l], r.gkeys_a, r.gvals_a, s);
+        // (its last pass also gathers the key counts into depth-rank order)
+        const uint32_t* counts_l = p.counts + (int64_t)l * n;
+        const bool sorted = plan->depth_bits[l] > 0 && n > 1;
         const int fl = launch_onesweep_u32(r.gkeys_a, r.gvals_a, r.gkeys_b, r.gvals_b, n, plan->depth_bits[l],
-                                           r.sort_temp, s, &g_launches);
+                                           r.sort_temp, s, &g_launches, counts_l, r.cperm);
         const uint32_t* perm = fl ? r.gvals_b : r.gvals_a;
         // 2. emission offsets in depth-rank order
-        launch_gather_counts(p.counts + (int64_t)l * n, perm, n, r.cperm, s);
+        if (!sorted) launch_gather_counts(counts_l, perm, n, r.cperm, s);  // (no sort pass ran)
         launch_scan_u32_to_u64(r.cperm, r.offs_perm, n, r.gscan_temp, s);
         // 3. key duplication (key = tile, value = Gaussian index)
         const uint64_t* tm = o.slab ? slab_mask_ptr(o.slab) + (int64_t)l * n_tiles : nullptr;
         launch_duplicate_ranked(dup, perm, r.offs_perm, n, res, o.bin_mode, (uint64_t)b, tm, r.keys_a, r.vals_a,
                                 s);
-        g_launches += 3 + kScanLaunches;  // depth keys, gather, scan, duplication
+        g_launches += (sorted ? 2 : 3) + kScanLaunches;  // depth keys, (gather,) scan, duplication
         // 4. stable sort of the tile digits
         const int ft = launch_onesweep_u32(r.keys_a + b, r.vals_a + b, r.keys_b + b, r.vals_b + b, e - b,
                                            plan->tile_bits, r.sort_temp, s, &g_launches);

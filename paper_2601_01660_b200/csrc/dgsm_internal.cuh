@@ -218,8 +218,11 @@ size_t onesweep_temp_bytes(int64_t n_max);
 // returns 1 if the sorted result ended in the *_alt buffers
 int launch_onesweep(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int64_t n,
                     int nbits, void* temp, cudaStream_t s, int* launches);
+// (gsrc/gdst optional: the last pass also writes gdst[o] = gsrc[value] at each output
+// position o, i.e. a gather by the sorted permutation; only when nbits > 0 and n > 1)
 int launch_onesweep_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n,
-                        int nbits, void* temp, cudaStream_t s, int* launches);
+                        int nbits, void* temp, cudaStream_t s, int* launches, const uint32_t* gsrc = nullptr,
+                        uint32_t* gdst = nullptr);
 void launch_decode_keys(const uint32_t* keys, const uint32_t* vals, const uint4* dup, const dgsm_plan_t& plan,
                         uint32_t* light_out, uint32_t* tile_out, uint32_t* depth_out, uint32_t* index_out,
                         cudaStream_t s);

@@ -132,7 +132,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ k
                                                       int64_t n, int shift, int bits, bool top,
                                                       const uint32_t* __restrict__ hist,
                                                       uint32_t* status, uint32_t* status_next,
-                                                      uint32_t* part_ctr) {
+                                                      uint32_t* part_ctr, const uint32_t* __restrict__ gsrc,
+                                                      uint32_t* __restrict__ gdst) {
     extern __shared__ __align__(16) unsigned char os_smem[];
     KeyT* s_keys = reinterpret_cast<KeyT*>(os_smem);
     uint32_t* s_vals = reinterpret_cast<uint32_t*>(os_smem + sizeof(KeyT) * kTileKeys);
@@ -246,6 +247,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ k
         const uint32_t o = s_global[dd] + (uint32_t)x - s_tile_start[dd];
         kout[o] = key;
         vout[o] = s_vals[x];
+        if (gdst) gdst[o] = gsrc[s_vals[x]];  // optional gather by the sorted values (last pass)
     }
 }
 
@@ -267,7 +269,8 @@ OnesweepTemp carve(void* temp, int64_t parts) {
 
 template <typename KeyT>
 int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt, int64_t n, int nbits,
-                  void* temp, cudaStream_t s, int* launches) {
+                  void* temp, cudaStream_t s, int* launches, const uint32_t* gsrc = nullptr,
+                  uint32_t* gdst = nullptr) {
     if (n <= 1 || nbits <= 0) return 0;
     const int passes = (nbits + 7) / 8;
     const int64_t parts = (n + kTileKeys - 1) / kTileKeys;
@@ -301,7 +304,7 @@ int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt
         k_pass<KeyT><<<(unsigned)parts, kThreads, dyn, s>>>(ki, vi, ko, vo, n, pd.shift[p], pd.bits[p],
                                                            p == passes - 1, t.hist + p * kRadix,
                                                            t.status[p & 1], t.status[(p + 1) & 1],
-                                                           t.part_ctr + p);
+                                                           t.part_ctr + p, gsrc, p == passes - 1 ? gdst : nullptr);
         *launches += 1;
         KeyT* tk = ki; ki = ko; ko = tk;
         uint32_t* tv = vi; vi = vo; vo = tv;
@@ -322,8 +325,9 @@ int launch_onesweep(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t
 }
 
 int launch_onesweep_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n,
-                        int nbits, void* temp, cudaStream_t s, int* launches) {
-    return onesweep_impl<uint32_t>(keys, vals, keys_alt, vals_alt, n, nbits, temp, s, launches);
+                        int nbits, void* temp, cudaStream_t s, int* launches, const uint32_t* gsrc,
+                        uint32_t* gdst) {
+    return onesweep_impl<uint32_t>(keys, vals, keys_alt, vals_alt, n, nbits, temp, s, launches, gsrc, gdst);
 }
 
 }  // namespace dgsm

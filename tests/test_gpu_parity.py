@@ -77,7 +77,25 @@ def build_both(dg, oracle, scene, **opt):
     return T, To
 
 
+def equal_depth_scene(n_sign=8):
+    """Gaussians at exactly the same distance from the light (sign flips and
+    permutations of one offset): the depth key has 0 significant bits, so the
+    depth sort runs no pass (the unsorted-count path of the build)."""
+    import itertools
+    base = np.array([0.5, 0.3, 0.2])
+    offs = sorted({tuple(sg * base[list(pm)]) for pm in itertools.permutations(range(3))
+                   for sg in itertools.product((-1.0, 1.0), repeat=3)})[:max(n_sign, 1)]
+    m = np.asarray(offs, np.float32)
+    n = len(m)
+    g = dict(means=m, scales=np.full((n, 3), 0.05, np.float32),
+             rotations=np.tile(np.array([1, 0, 0, 0], np.float32), (n, 1)), opacities=np.full(n, 0.6, np.float32))
+    lights = dict(position=np.zeros((1, 3), np.float32), t_max=np.array([2.0], np.float32))
+    return synth.Scene("equal-depth", g, lights, 32, 16, m.copy())
+
+
 SCENES = {
+    "equal-depth": lambda: equal_depth_scene(48),
+    "single-gaussian": lambda: equal_depth_scene(1),
     "cfg1": lambda: synth.config1(),
     "cfg1-seam-z": lambda: synth.config1_seam("-z"),
     "cfg1-seam-x": lambda: synth.config1_seam("+x"),
