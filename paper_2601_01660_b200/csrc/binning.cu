@@ -9,6 +9,7 @@
 //   2. k_gather_counts + scan                                 -> emission offsets in that order
 //   3. k_duplicate_ranked: each Gaussian, in depth-rank order, emits (tile, index)
 //   4. onesweep (stable) on the P tile keys                   -> (tile, D bits, index)
+#include <algorithm>
 #include <cstdlib>
 
 #include "dgsm_internal.cuh"
@@ -23,14 +24,27 @@ __device__ __forceinline__ void unpack_rect(const uint4& r, int& c0, int& c1, in
 }
 
 // Depth key of each Gaussian of one light (0 for Gaussians that bin no tile:
-// they emit nothing, their position in the order is irrelevant).
+// they emit nothing, their position in the order is irrelevant), and the
+// onesweep digit histograms of those keys (the sort's own histogram pass is
+// skipped): grid-stride, per-CTA shared histograms, one global add per bin.
 __global__ void __launch_bounds__(256) k_depth_keys(const uint4* __restrict__ dup, int64_t n, uint32_t dmin,
-                                                    uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint4 r = dup[i];
-    keys[i] = r.w ? r.x - dmin : 0u;
-    vals[i] = (uint32_t)i;
+                                                    uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                                    PassDigits pd, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t sh[kSortMaxPasses][kSortRadix];
+    for (int t = threadIdx.x; t < pd.passes * kSortRadix; t += blockDim.x) (&sh[0][0])[t] = 0u;
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 r = dup[i];
+        const uint32_t k = r.w ? r.x - dmin : 0u;
+        keys[i] = k;
+        vals[i] = (uint32_t)i;
+        for (int p = 0; p < pd.passes; ++p) atomicAdd(&sh[p][(k >> pd.shift[p]) & ((1u << pd.bits[p]) - 1u)], 1u);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < pd.passes * kSortRadix; t += blockDim.x) {
+        const uint32_t c = (&sh[0][0])[t];
+        if (c) atomicAdd(&hist[t], c);
+    }
 }
 
 // key counts in depth-rank order (a 4-B gather from the count array, which
@@ -337,9 +351,10 @@ __global__ void __launch_bounds__(kFusedThreads) k_units_fused(const uint32_t* _
 }  // namespace
 
 void launch_depth_keys(const uint4* dup, int64_t n, uint32_t dmin, uint32_t* keys, uint32_t* vals,
-                       cudaStream_t s) {
+                       const PassDigits& pd, uint32_t* hist, cudaStream_t s) {
     if (n <= 0) return;
-    k_depth_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dup, n, dmin, keys, vals);
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 4);
+    k_depth_keys<<<(unsigned)blocks, 256, 0, s>>>(dup, n, dmin, keys, vals, pd, hist);
 }
 
 void launch_gather_counts(const uint32_t* counts, const uint32_t* perm, int64_t n, uint32_t* cperm,

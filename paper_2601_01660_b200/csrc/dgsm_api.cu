@@ -392,13 +392,18 @@ static void run_binning(const dgsm_gaussians_t* g, int n_lights, const dgsm_buil
         const int64_t b = plan->light_key_begin[l], e = plan->light_key_begin[l + 1];
         if (e == b) continue;
         const uint4* dup = p.dup + (int64_t)l * n;
-        // 1. light-distance digits on the Gaussians
-        launch_depth_keys(dup, n, plan->depth_min[l], r.gkeys_a, r.gvals_a, s);
-        // (its last pass also gathers the key counts into depth-rank order)
+        // 1. light-distance digits on the Gaussians (the key kernel also fills the
+        //    sort's digit histograms; the sort's last pass gathers the key counts
+        //    into depth-rank order)
         const uint32_t* counts_l = p.counts + (int64_t)l * n;
         const bool sorted = plan->depth_bits[l] > 0 && n > 1;
+        PassDigits pd = onesweep_digits(plan->depth_bits[l]);
+        uint32_t* hist = nullptr;
+        if (sorted) hist = onesweep_prepare(r.sort_temp, n, s);
+        else pd.passes = 0;
+        launch_depth_keys(dup, n, plan->depth_min[l], r.gkeys_a, r.gvals_a, pd, hist, s);
         const int fl = launch_onesweep_u32(r.gkeys_a, r.gvals_a, r.gkeys_b, r.gvals_b, n, plan->depth_bits[l],
-                                           r.sort_temp, s, &g_launches, counts_l, r.cperm);
+                                           r.sort_temp, s, &g_launches, counts_l, r.cperm, true);
         const uint32_t* perm = fl ? r.gvals_b : r.gvals_a;
         // 2. emission offsets in depth-rank order
         if (!sorted) launch_gather_counts(counts_l, perm, n, r.cperm, s);  // (no sort pass ran)

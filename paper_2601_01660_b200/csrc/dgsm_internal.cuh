@@ -207,8 +207,7 @@ void launch_scan_u64(const uint64_t* in, uint64_t* out, int64_t n, void* temp, c
 void launch_scan_u32_to_u64_marks(const uint32_t* in, uint64_t* out, int64_t n, void* temp, uint64_t* marks,
                                   int64_t mark_stride, int n_marks, cudaStream_t s);
 // dup[l*n + i] = {fp32 bits of D, c0 | c1 << 16, r0 | r1 << 16, tile count} (16 B per (light, Gaussian))
-void launch_depth_keys(const uint4* dup, int64_t n, uint32_t dmin, uint32_t* keys, uint32_t* vals,
-                       cudaStream_t s);
+
 void launch_gather_counts(const uint32_t* counts, const uint32_t* perm, int64_t n, uint32_t* cperm,
                           cudaStream_t s);
 void launch_duplicate_ranked(const uint4* dup, const uint32_t* perm, const uint64_t* offs, int64_t n, int res,
@@ -218,11 +217,27 @@ size_t onesweep_temp_bytes(int64_t n_max);
 // returns 1 if the sorted result ended in the *_alt buffers
 int launch_onesweep(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int64_t n,
                     int nbits, void* temp, cudaStream_t s, int* launches);
+// Onesweep digits: pass p sorts bits [shift[p], shift[p] + bits[p]) of the key,
+// bits <= 8; the passes split the key's significant bits evenly (a 12-bit tile
+// key: 6 + 6).  onesweep_prepare clears the sort's histograms, partition
+// counters and first status buffer and returns the histograms [passes][256]; a
+// key producer may fill them (hist_ready) instead of the sort's own k_hist.
+constexpr int kSortRadix = 256;
+constexpr int kSortMaxPasses = 8;
+struct PassDigits {
+    int shift[kSortMaxPasses], bits[kSortMaxPasses];
+    int passes;
+};
+PassDigits onesweep_digits(int nbits);
+uint32_t* onesweep_prepare(void* temp, int64_t n, cudaStream_t s);
+// depth keys of one light's Gaussians + their digit histograms into hist (pd.passes = 0: none)
+void launch_depth_keys(const uint4* dup, int64_t n, uint32_t dmin, uint32_t* keys, uint32_t* vals,
+                       const PassDigits& pd, uint32_t* hist, cudaStream_t s);
 // (gsrc/gdst optional: the last pass also writes gdst[o] = gsrc[value] at each output
 // position o, i.e. a gather by the sorted permutation; only when nbits > 0 and n > 1)
 int launch_onesweep_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n,
                         int nbits, void* temp, cudaStream_t s, int* launches, const uint32_t* gsrc = nullptr,
-                        uint32_t* gdst = nullptr);
+                        uint32_t* gdst = nullptr, bool hist_ready = false);
 void launch_decode_keys(const uint32_t* keys, const uint32_t* vals, const uint4* dup, const dgsm_plan_t& plan,
                         uint32_t* light_out, uint32_t* tile_out, uint32_t* depth_out, uint32_t* index_out,
                         cudaStream_t s);

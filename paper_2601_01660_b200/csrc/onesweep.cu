@@ -28,15 +28,10 @@ constexpr int kThreads = 256;
 #endif
 constexpr int kItems = DGSM_OS_ITEMS;
 constexpr int kTileKeys = kThreads * kItems;  // 2048 keys per partition (<= 64 regs: 4 CTAs/SM)
-constexpr int kRadix = 256;
-constexpr int kMaxPasses = 8;
+constexpr int kRadix = kSortRadix;
+constexpr int kMaxPasses = kSortMaxPasses;
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
 
-// Digit of each pass: bits [shift, shift + bits) of the key, bits <= 8.  The
-// passes split the key's significant bits evenly (a 12-bit tile key: 6 + 6).
-struct PassDigits {
-    int shift[kMaxPasses], bits[kMaxPasses];
-};
 
 template <typename KeyT>
 __global__ void __launch_bounds__(256) k_hist(const KeyT* __restrict__ keys, int64_t n, int passes,
@@ -270,7 +265,7 @@ OnesweepTemp carve(void* temp, int64_t parts) {
 template <typename KeyT>
 int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt, int64_t n, int nbits,
                   void* temp, cudaStream_t s, int* launches, const uint32_t* gsrc = nullptr,
-                  uint32_t* gdst = nullptr) {
+                  uint32_t* gdst = nullptr, bool hist_ready = false) {
     if (n <= 1 || nbits <= 0) return 0;
     const int passes = (nbits + 7) / 8;
     const int64_t parts = (n + kTileKeys - 1) / kTileKeys;
@@ -285,18 +280,14 @@ int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt
         cudaFuncSetAttribute(k_pass<KeyT>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
         attr_set.fetch_or(bit);
     }
-    // histograms, partition counters and the first pass's status in one memset
-    cudaMemsetAsync(t.hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix + 256 + sizeof(uint32_t) * kRadix * (size_t)parts,
-                    s);
-    PassDigits pd;
-    for (int p = 0, sh = 0; p < passes; ++p) {
-        pd.bits[p] = nbits / passes + (p < nbits % passes ? 1 : 0);
-        pd.shift[p] = sh;
-        sh += pd.bits[p];
+    const PassDigits pd = onesweep_digits(nbits);
+    if (!hist_ready) {
+        // histograms, partition counters and the first pass's status in one memset
+        onesweep_prepare(temp, n, s);
+        const int hist_grid = (int)std::min<int64_t>(148 * 4, (n + 2047) / 2048);
+        k_hist<KeyT><<<hist_grid, 256, 0, s>>>(keys, n, passes, pd, t.hist);
+        *launches += 1;
     }
-    const int hist_grid = (int)std::min<int64_t>(148 * 4, (n + 2047) / 2048);
-    k_hist<KeyT><<<hist_grid, 256, 0, s>>>(keys, n, passes, pd, t.hist);
-    *launches += 1;
     KeyT *ki = keys, *ko = keys_alt;
     uint32_t *vi = vals, *vo = vals_alt;
     int flipped = 0;
@@ -326,8 +317,28 @@ int launch_onesweep(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t
 
 int launch_onesweep_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n,
                         int nbits, void* temp, cudaStream_t s, int* launches, const uint32_t* gsrc,
-                        uint32_t* gdst) {
-    return onesweep_impl<uint32_t>(keys, vals, keys_alt, vals_alt, n, nbits, temp, s, launches, gsrc, gdst);
+                        uint32_t* gdst, bool hist_ready) {
+    return onesweep_impl<uint32_t>(keys, vals, keys_alt, vals_alt, n, nbits, temp, s, launches, gsrc, gdst,
+                                   hist_ready);
+}
+
+PassDigits onesweep_digits(int nbits) {
+    PassDigits pd{};
+    pd.passes = nbits > 0 ? (nbits + 7) / 8 : 0;
+    for (int p = 0, sh = 0; p < pd.passes; ++p) {
+        pd.bits[p] = nbits / pd.passes + (p < nbits % pd.passes ? 1 : 0);
+        pd.shift[p] = sh;
+        sh += pd.bits[p];
+    }
+    return pd;
+}
+
+uint32_t* onesweep_prepare(void* temp, int64_t n, cudaStream_t s) {
+    const int64_t parts = (n + kTileKeys - 1) / kTileKeys;
+    OnesweepTemp t = carve(temp, parts);
+    cudaMemsetAsync(t.hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix + 256 + sizeof(uint32_t) * kRadix * (size_t)parts,
+                    s);
+    return t.hist;
 }
 
 }  // namespace dgsm
