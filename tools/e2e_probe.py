@@ -34,3 +34,23 @@ out = torch.empty((1, s.K, s.res, s.res), device="cuda")
 xq = rh.cuda()
 To = torch.empty(rh.shape[0], device="cuda")
 print(f"device build+query: {timeit(lambda: (b(gd, out), dgsm.query(out, s.lights, xq, out=To))):.3f} ms")
+
+
+def span(fn, k=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(k):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / k
+
+
+print(f"frame_host pipelined: {span(lambda: fr(gh, rh, Th)):.3f} ms/frame")
+print(f"device build+query pipelined: {span(lambda: (b(gd, out), dgsm.query(out, s.lights, xq, out=To))):.3f} ms/frame")
+print(f"device build only pipelined: {span(lambda: b(gd, out)):.3f} ms/frame")
+Tp = torch.empty(rh.shape[0])
+print(f"frame_host pipelined, pageable T: {span(lambda: fr(gh, rh, Tp)):.3f} ms/frame")
