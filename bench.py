@@ -499,7 +499,7 @@ def run_dgsm(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": total_ms_max / K, "higher_is_better": True,
-            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32 (fp64 geometry)",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32", "dtype_note": "accumulation and query taps in fp32; binning geometry and query index math in fp64",
             "data": "synthetic",
             "config": dict(cfg_desc(s, args.config),
                            parallelism=(f"{world} rank(s): lights dealt to ranks, {gsz} rank(s) per light "
