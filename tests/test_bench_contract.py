@@ -41,3 +41,27 @@ def test_product_arm_needs_a_gpu():
         pytest.skip("a GPU is present")
     r = run_bench("--config", "1", "--steps", "3", "--warmup", "3")
     assert r.returncode != 0 and not r.stdout.strip()  # no line, no CPU fallback
+
+
+@pytest.mark.gpu
+def test_product_arm_line():
+    """The product arm on a GPU (small cfg1 run): one line with the contract's
+    keys, the roofline and e2e objects, clocks and a positive launch count."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    r = run_bench("--config", "1", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-transfer", timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "clocks", "gpu_launches"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0
+    assert d["gpu_launches"] > 0 and d["dtype"] == "f32"
+    rf = d["roofline"]
+    assert rf["bound"] in ("hbm", "tensor", "alu") and rf["peak"] > 0 and abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
