@@ -93,7 +93,22 @@ def equal_depth_scene(n_sign=8):
     return synth.Scene("equal-depth", g, lights, 32, 16, m.copy())
 
 
+def light_coincident_scene():
+    """A random scene plus Gaussians at the light (D = 0) and within 1e-7 of it
+    (excluded, Q17) and one 2 cm from it (a footprint over the whole atlas)."""
+    s = synth.random_scene(21, 200, res=32, K=16, dist=(0.3, 3.0), scale=(0.01, 0.3))
+    o = s.lights["position"][0].astype(np.float32)
+    extra = np.stack([o, o + np.float32(1e-7), o + np.array([0.02, 0.0, 0.0], np.float32)])
+    g = dict(s.gaussians)
+    g["means"] = np.concatenate([g["means"], extra]).astype(np.float32)
+    g["scales"] = np.concatenate([g["scales"], np.full((3, 3), 0.05, np.float32)])
+    g["rotations"] = np.concatenate([g["rotations"], np.tile(np.array([1, 0, 0, 0], np.float32), (3, 1))])
+    g["opacities"] = np.concatenate([g["opacities"], np.full(3, 0.5, np.float32)])
+    return synth.Scene("light-coincident", g, s.lights, s.res, s.K, s.queries)
+
+
 SCENES = {
+    "light-coincident": light_coincident_scene,
     "equal-depth": lambda: equal_depth_scene(48),
     "single-gaussian": lambda: equal_depth_scene(1),
     "cfg1": lambda: synth.config1(),
