@@ -114,13 +114,6 @@ double or_beta_mode(const float s3[3], const float q4[4], float alpha, double ka
     return kappa * tau_star / (two_pi_32 * ((double)s3[0] * (double)s3[1] * (double)s3[2]));
 }
 
-void or_calibrate(const float* scales, const float* rotations, const float* opacities,
-                  int64_t n, double kappa, double* beta_out)
-{
-    for (int64_t i = 0; i < n; ++i)
-        beta_out[i] = or_beta(scales + 3 * i, rotations + 4 * i, opacities[i], kappa);
-}
-
 /* ------------------------------------------------------------------ */
 /* Octahedral map psi                                      */
 /* ------------------------------------------------------------------ */
@@ -268,10 +261,12 @@ static uint32_t or_float_bits(double D)
 
 /* Tile set of one (light, Gaussian): every integer texel centre inside the
  * closed square [px-p1,px+p1]x[py-p1,py+p1] (clamped to the extended lattice)
- * is mapped (wrap: mirror-wrap; clamp: dropped if outside) and the set of
- * tiles containing a mapped centre is marked in `mark` (n_tiles bytes).
- * Returns the number of distinct tiles. */
-static int64_t or_tile_set(const int64_t rect[4], int res, int bin_mode, unsigned char* mark)
+ * is mapped (wrap: mirror-wrap; clamp: dropped if outside) and every tile
+ * containing a mapped centre is listed once in `list` (the first time it is
+ * seen; `mark` is the per-tile "already listed" flag, n_tiles bytes, all 0 on
+ * entry and on return).  Returns the number of distinct tiles. */
+static int64_t or_tile_set(const int64_t rect[4], int res, int bin_mode, unsigned char* mark,
+                           int64_t* list)
 {
     int H = res, W = res, TW = res / 8;
     int64_t n = 0;
@@ -285,21 +280,22 @@ static int64_t or_tile_set(const int64_t rect[4], int res, int bin_mode, unsigne
                 or_mirror_wrap(col, row, H, W, cr);
             }
             int64_t t = (cr[1] >> 3) * TW + (cr[0] >> 3);
-            if (!mark[t]) { mark[t] = 1; ++n; }
+            if (!mark[t]) { mark[t] = 1; list[n++] = t; }
         }
+    for (int64_t j = 0; j < n; ++j) mark[list[j]] = 0;
     return n;
 }
 
-/* Bin every (light, Gaussian); returns P (number of entries).  When
- * `capacity` >= P the sorted entries are written to the four output arrays.
+/* Bin every (light, Gaussian) and sort the entries by (light, tile, depth
+ * bits, index) (R7); returns the malloc'd entries, *P_out = their number.
  * bin_mode: 0 = wrap (default), 1 = clamp. */
-int64_t or_bin(const float* means, const float* scales, const float* rotations, int64_t n,
-               const float* light_pos /*[L][3]*/, int L, int res, double k_sigma,
-               double rho_scale, int bin_mode, uint32_t* out_light, uint32_t* out_tile,
-               uint32_t* out_depth, uint32_t* out_index, int64_t capacity)
+static or_entry* or_bin_sorted(const float* means, const float* scales, const float* rotations, int64_t n,
+                               const float* light_pos /*[L][3]*/, int L, int res, double k_sigma,
+                               double rho_scale, int bin_mode, int64_t* P_out)
 {
     int64_t n_tiles = (int64_t)(res / 8) * (res / 8);
     unsigned char* mark = (unsigned char*)calloc((size_t)n_tiles, 1);
+    int64_t* list = (int64_t*)malloc(sizeof(int64_t) * (size_t)n_tiles);
     int64_t P = 0, cap = 1024;
     or_entry* e = (or_entry*)malloc(sizeof(or_entry) * cap);
     for (int l = 0; l < L; ++l)
@@ -310,24 +306,37 @@ int64_t or_bin(const float* means, const float* scales, const float* rotations, 
                               res, k_sigma, rho_scale, fp, rect))
                 continue;
             if (rect[0] > rect[1] || rect[2] > rect[3]) continue;
-            int64_t cnt = or_tile_set(rect, res, bin_mode, mark);
-            if (cnt == 0) continue;
+            int64_t cnt = or_tile_set(rect, res, bin_mode, mark, list);
             uint32_t db = or_float_bits(fp[0]);
-            for (int64_t t = 0; t < n_tiles; ++t) {
-                if (!mark[t]) continue;
-                mark[t] = 0;
+            for (int64_t j = 0; j < cnt; ++j) {
                 if (P == cap) {
                     cap *= 2;
                     e = (or_entry*)realloc(e, sizeof(or_entry) * cap);
                 }
                 e[P].light = (uint32_t)l;
-                e[P].tile = (uint32_t)t;
+                e[P].tile = (uint32_t)list[j];
                 e[P].depth_bits = db;
                 e[P].index = (uint32_t)i;
                 ++P;
             }
         }
     qsort(e, (size_t)P, sizeof(or_entry), or_entry_cmp);
+    free(list);
+    free(mark);
+    *P_out = P;
+    return e;
+}
+
+/* Bin every (light, Gaussian); returns P (number of entries).  When
+ * `capacity` >= P the sorted entries are written to the four output arrays. */
+int64_t or_bin(const float* means, const float* scales, const float* rotations, int64_t n,
+               const float* light_pos /*[L][3]*/, int L, int res, double k_sigma,
+               double rho_scale, int bin_mode, uint32_t* out_light, uint32_t* out_tile,
+               uint32_t* out_depth, uint32_t* out_index, int64_t capacity)
+{
+    int64_t P = 0;
+    or_entry* e = or_bin_sorted(means, scales, rotations, n, light_pos, L, res, k_sigma, rho_scale,
+                                bin_mode, &P);
     if (capacity >= P && out_light) {
         for (int64_t j = 0; j < P; ++j) {
             out_light[j] = e[j].light;
@@ -337,7 +346,6 @@ int64_t or_bin(const float* means, const float* scales, const float* rotations, 
         }
     }
     free(e);
-    free(mark);
     return P;
 }
 
@@ -383,18 +391,29 @@ typedef struct {
     double* beta; /* [n] */
     int64_t n_tiles;
     /* culled lists */
-    const uint32_t *e_light, *e_tile, *e_index;
+    const uint32_t* e_index;
     const int64_t* range; /* [L*n_tiles+1] start offsets into the sorted entries */
     unsigned char* excluded; /* [L][n] */
     double* T;               /* [L][K][res][res] */
     const unsigned char* slab_mask; /* [L][res][res] or NULL: the ROI pixel set P */
     const int32_t* slab_krange;     /* [L][2] k_min, k_max (k_min > k_max: empty) */
+    const int64_t* items;    /* or_build_tiles: the (light, tile) items to compute, or NULL (all) */
+    int64_t n_items_list;
+    double* T_items;         /* or_build_tiles output [n_items_list][K][8][8] */
     int64_t next;            /* work counter */
     int64_t evals;           /* (texel, Gaussian) evaluations performed */
     pthread_mutex_t lock;
 } or_build_ctx;
 
-static void or_build_item(or_build_ctx* c, int64_t item)
+/* T value of texel (row, col), shell k of work item `item` (list position q):
+ * the atlas [L][K][H][W], or the compact [q][K][8][8] of or_build_tiles. */
+static double* or_T_at(or_build_ctx* c, int64_t q, int l, int k, int row, int col)
+{
+    if (c->T_items) return c->T_items + ((q * c->K + k) * 8 + (row & 7)) * 8 + (col & 7);
+    return c->T + (((int64_t)l * c->K + k) * c->res + row) * c->res + col;
+}
+
+static void or_build_item(or_build_ctx* c, int64_t item, int64_t q)
 {
     int l = (int)(item / c->n_tiles);
     int64_t tile = item % c->n_tiles;
@@ -414,7 +433,7 @@ static void or_build_item(or_build_ctx* c, int64_t item)
                 khi = c->slab_krange[2 * l + 1];
                 if (!c->slab_mask[((int64_t)l * H + row) * W + col]) khi = -1;
                 for (int k = 0; k < K; ++k)
-                    if (k < klo || k > khi) c->T[(((int64_t)l * K + k) * H + row) * W + col] = 1.0;
+                    if (k < klo || k > khi) *or_T_at(c, q, l, k, row, col) = 1.0;
                 if (klo > khi) continue;
             }
             double d[3];
@@ -436,7 +455,7 @@ static void or_build_item(or_build_ctx* c, int64_t item)
                                                or_bin_center(k, K, tmax));
             }
             for (int k = klo; k <= khi; ++k)
-                c->T[(((int64_t)l * K + k) * H + row) * W + col] = exp(-tau[k]);
+                *or_T_at(c, q, l, k, row, col) = exp(-tau[k]);
         }
     free(tau);
 }
@@ -444,20 +463,21 @@ static void or_build_item(or_build_ctx* c, int64_t item)
 static void* or_build_worker(void* arg)
 {
     or_build_ctx* c = (or_build_ctx*)arg;
-    int64_t n_items = (int64_t)c->L * c->n_tiles;
+    int64_t n_items = c->items ? c->n_items_list : (int64_t)c->L * c->n_tiles;
     for (;;) {
         pthread_mutex_lock(&c->lock);
-        int64_t item = c->next;
+        int64_t q = c->next;
         c->next += 1;
         pthread_mutex_unlock(&c->lock);
-        while (item < n_items && item % c->tile_stride != 0) {
+        while (!c->items && q < n_items && q % c->tile_stride != 0) {
             pthread_mutex_lock(&c->lock);
-            item = c->next;
+            q = c->next;
             c->next += 1;
             pthread_mutex_unlock(&c->lock);
         }
-        if (item >= n_items) break;
-        or_build_item(c, item);
+        if (q >= n_items) break;
+        int64_t item = c->items ? c->items[q] : q;
+        or_build_item(c, item, q);
         int64_t ev = 64 * (c->culled ? (c->range[item + 1] - c->range[item]) : c->n);
         pthread_mutex_lock(&c->lock);
         c->evals += ev;
@@ -489,6 +509,79 @@ int64_t or_build(const float* means, const float* scales, const float* rotations
                          NULL, NULL, T_out, evals_out);
 }
 
+/* The build (R8) over all work items (atlas output, `tile_stride` sampling)
+ * or over a list of items (compact output).  Shared by or_build_slab and
+ * or_build_tiles. */
+static int64_t or_build_impl(or_build_ctx* cp, int absorption, int n_threads)
+{
+    or_build_ctx* c = cp;
+    const float *means = c->means, *scales = c->scales, *rotations = c->rotations;
+    int64_t n = c->n;
+    int L = c->L, res = c->res;
+    c->n_tiles = (int64_t)(res / 8) * (res / 8);
+    c->A = (double*)malloc(sizeof(double) * 9 * (n > 0 ? n : 1));
+    c->beta = (double*)malloc(sizeof(double) * (n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; ++i) {
+        double Ai[3][3];
+        or_precision(scales + 3 * i, rotations + 4 * i, Ai);
+        memcpy(c->A + 9 * i, Ai, sizeof(Ai));
+        c->beta[i] = or_beta_mode(scales + 3 * i, rotations + 4 * i, c->opacities[i], c->kappa, absorption);
+    }
+    c->excluded = (unsigned char*)calloc((size_t)L * (n > 0 ? n : 1), 1);
+    for (int l = 0; l < L; ++l)
+        for (int64_t i = 0; i < n; ++i) {
+            double fp[5];
+            int64_t rect[4];
+            c->excluded[(int64_t)l * n + i] =
+                !or_footprint(means + 3 * i, scales + 3 * i, rotations + 4 * i, c->light_pos + 3 * l,
+                              res, c->k_sigma, c->rho_scale, fp, rect);
+        }
+
+    int64_t P = 0;
+    or_entry* e = NULL;
+    uint32_t* ei = NULL;
+    int64_t* range = NULL;
+    if (c->culled) {
+        e = or_bin_sorted(means, scales, rotations, n, c->light_pos, L, res, c->k_sigma, c->rho_scale,
+                          c->bin_mode, &P);
+        ei = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(P > 0 ? P : 1));
+        for (int64_t j = 0; j < P; ++j) ei[j] = e[j].index;
+        int64_t n_items = (int64_t)L * c->n_tiles;
+        range = (int64_t*)malloc(sizeof(int64_t) * (n_items + 1));
+        int64_t j = 0;
+        for (int64_t it = 0; it <= n_items; ++it) {
+            while (j < P && (int64_t)e[j].light * c->n_tiles + e[j].tile < it) ++j;
+            range[it] = j;
+        }
+        c->e_index = ei; c->range = range;
+    }
+
+    if (n_threads < 1) n_threads = 1;
+    pthread_mutex_init(&c->lock, NULL);
+    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * n_threads);
+    for (int t = 0; t < n_threads; ++t) pthread_create(&th[t], NULL, or_build_worker, c);
+    for (int t = 0; t < n_threads; ++t) pthread_join(th[t], NULL);
+    pthread_mutex_destroy(&c->lock);
+    free(th);
+
+    free(c->A); free(c->beta); free(c->excluded);
+    free(e); free(ei); free(range);
+    return P;
+}
+
+static void or_build_ctx_init(or_build_ctx* c, const float* means, const float* scales,
+                              const float* rotations, const float* opacities, int64_t n,
+                              const float* light_pos, const float* t_max, int L, int res, int K,
+                              double kappa, double k_sigma, double rho_scale, int bin_mode, int culled)
+{
+    memset(c, 0, sizeof(*c));
+    c->means = means; c->scales = scales; c->rotations = rotations; c->opacities = opacities;
+    c->n = n; c->light_pos = light_pos; c->t_max = t_max; c->L = L; c->res = res; c->K = K;
+    c->kappa = kappa; c->k_sigma = k_sigma; c->rho_scale = rho_scale;
+    c->bin_mode = bin_mode; c->culled = culled;
+    c->tile_stride = 1;
+}
+
 /* As or_build, restricted to the ROI slab (slab_mask [L][res][res], slab_krange
  * [L][2] from or_active_slab); NULL slab_mask = the full atlas. */
 int64_t or_build_slab(const float* means, const float* scales, const float* rotations,
@@ -500,69 +593,41 @@ int64_t or_build_slab(const float* means, const float* scales, const float* rota
 {
     if (res < 8 || res % 8 != 0 || K < 1 || L < 1 || n < 0) return -1;
     or_build_ctx c;
-    memset(&c, 0, sizeof(c));
-    c.means = means; c.scales = scales; c.rotations = rotations; c.opacities = opacities;
-    c.n = n; c.light_pos = light_pos; c.t_max = t_max; c.L = L; c.res = res; c.K = K;
-    c.kappa = kappa; c.k_sigma = k_sigma; c.rho_scale = rho_scale;
-    c.bin_mode = bin_mode; c.culled = culled;
+    or_build_ctx_init(&c, means, scales, rotations, opacities, n, light_pos, t_max, L, res, K, kappa,
+                      k_sigma, rho_scale, bin_mode, culled);
     c.tile_stride = tile_stride < 1 ? 1 : tile_stride;
-    c.n_tiles = (int64_t)(res / 8) * (res / 8);
     c.T = T_out;
     c.slab_mask = slab_mask;
     c.slab_krange = slab_krange;
     int64_t total = (int64_t)L * K * res * res;
     for (int64_t j = 0; j < total; ++j) T_out[j] = NAN;
-
-    c.A = (double*)malloc(sizeof(double) * 9 * (n > 0 ? n : 1));
-    c.beta = (double*)malloc(sizeof(double) * (n > 0 ? n : 1));
-    for (int64_t i = 0; i < n; ++i) {
-        double Ai[3][3];
-        or_precision(scales + 3 * i, rotations + 4 * i, Ai);
-        memcpy(c.A + 9 * i, Ai, sizeof(Ai));
-        c.beta[i] = or_beta_mode(scales + 3 * i, rotations + 4 * i, opacities[i], kappa, absorption);
-    }
-    c.excluded = (unsigned char*)calloc((size_t)L * (n > 0 ? n : 1), 1);
-    for (int l = 0; l < L; ++l)
-        for (int64_t i = 0; i < n; ++i) {
-            double fp[5];
-            int64_t rect[4];
-            c.excluded[(int64_t)l * n + i] =
-                !or_footprint(means + 3 * i, scales + 3 * i, rotations + 4 * i, light_pos + 3 * l,
-                              res, k_sigma, rho_scale, fp, rect);
-        }
-
-    int64_t P = 0;
-    uint32_t *el = NULL, *et = NULL, *ed = NULL, *ei = NULL;
-    int64_t* range = NULL;
-    if (culled) {
-        P = or_bin(means, scales, rotations, n, light_pos, L, res, k_sigma, rho_scale, bin_mode,
-                   NULL, NULL, NULL, NULL, 0);
-        size_t sz = sizeof(uint32_t) * (size_t)(P > 0 ? P : 1);
-        el = (uint32_t*)malloc(sz); et = (uint32_t*)malloc(sz);
-        ed = (uint32_t*)malloc(sz); ei = (uint32_t*)malloc(sz);
-        or_bin(means, scales, rotations, n, light_pos, L, res, k_sigma, rho_scale, bin_mode, el,
-               et, ed, ei, P);
-        int64_t n_items = (int64_t)L * c.n_tiles;
-        range = (int64_t*)malloc(sizeof(int64_t) * (n_items + 1));
-        int64_t j = 0;
-        for (int64_t it = 0; it <= n_items; ++it) {
-            while (j < P && (int64_t)el[j] * c.n_tiles + et[j] < it) ++j;
-            range[it] = j;
-        }
-        c.e_light = el; c.e_tile = et; c.e_index = ei; c.range = range;
-    }
-
-    if (n_threads < 1) n_threads = 1;
-    pthread_mutex_init(&c.lock, NULL);
-    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * n_threads);
-    for (int t = 0; t < n_threads; ++t) pthread_create(&th[t], NULL, or_build_worker, &c);
-    for (int t = 0; t < n_threads; ++t) pthread_join(th[t], NULL);
-    pthread_mutex_destroy(&c.lock);
-    free(th);
-
-    free(c.A); free(c.beta); free(c.excluded);
+    int64_t P = or_build_impl(&c, absorption, n_threads);
     if (evals_out) *evals_out = c.evals;
-    free(el); free(et); free(ed); free(ei); free(range);
+    return P;
+}
+
+/* As or_build (culled, full atlas semantics) for the listed work items only:
+ * items[q] = l * (res/8)^2 + tile; T_items[q][K][8][8] receives T of the 64
+ * texels (row-major within the tile) of item q.  For parity on a sample of
+ * tiles of atlases too large to hold in double (2048^2 x 128 x 8 lights). */
+int64_t or_build_tiles(const float* means, const float* scales, const float* rotations,
+                       const float* opacities, int64_t n, const float* light_pos, const float* t_max,
+                       int L, int res, int K, double kappa, double k_sigma, double rho_scale,
+                       int bin_mode, int absorption, const int64_t* items, int64_t n_items,
+                       int n_threads, double* T_items, int64_t* evals_out)
+{
+    if (res < 8 || res % 8 != 0 || K < 1 || L < 1 || n < 0 || n_items < 0) return -1;
+    int64_t n_all = (int64_t)L * (res / 8) * (res / 8);
+    for (int64_t q = 0; q < n_items; ++q)
+        if (items[q] < 0 || items[q] >= n_all) return -1;
+    or_build_ctx c;
+    or_build_ctx_init(&c, means, scales, rotations, opacities, n, light_pos, t_max, L, res, K, kappa,
+                      k_sigma, rho_scale, bin_mode, 1);
+    c.items = items;
+    c.n_items_list = n_items;
+    c.T_items = T_items;
+    int64_t P = or_build_impl(&c, absorption, n_threads);
+    if (evals_out) *evals_out = c.evals;
     return P;
 }
 

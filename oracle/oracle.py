@@ -60,6 +60,10 @@ def lib():
         L.or_build.argtypes = [fp, fp, fp, fp, C.c_int64, fp, fp, C.c_int, C.c_int, C.c_int,
                                C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int64,
                                C.c_int, dp, i64p]
+        L.or_build_tiles.restype = C.c_int64
+        L.or_build_tiles.argtypes = [fp, fp, fp, fp, C.c_int64, fp, fp, C.c_int, C.c_int, C.c_int,
+                                     C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, i64p, C.c_int64,
+                                     C.c_int, dp, i64p]
         L.or_build_slab.restype = C.c_int64
         L.or_build_slab.argtypes = [fp, fp, fp, fp, C.c_int64, fp, fp, C.c_int, C.c_int, C.c_int,
                                     C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int64,
@@ -220,6 +224,28 @@ def build(g, lights, res, K, kappa=1.0, k_sigma=3.0, rho_scale=1.0, bin_mode=BIN
         raise ValueError("oracle build: invalid arguments")
     if return_evals:
         return T, int(P), int(evals.value)
+    return T, int(P)
+
+
+def build_tiles(g, lights, res, K, items, kappa=1.0, k_sigma=3.0, rho_scale=1.0, bin_mode=BIN_WRAP,
+                absorption="traceavg", n_threads=None):
+    """R8 on a list of work items only (culled build, full-atlas semantics):
+    ``items`` = l * (res/8)^2 + tile.  Returns (T [n_items, K, 8, 8] float64 —
+    the 64 texels of each item's tile, row-major — and P).  For sampled-tile
+    parity on atlases too large for a float64 copy (2048^2 x 128 x 8 lights)."""
+    mode = ABSORPTION[absorption] if isinstance(absorption, str) else int(absorption)
+    mu, s, q, a = _f32(g["means"]), _f32(g["scales"]), _f32(g["rotations"]), _f32(g["opacities"])
+    lp, tm = _f32(lights["position"]).reshape(-1, 3), _f32(lights["t_max"]).reshape(-1)
+    it = np.ascontiguousarray(items, dtype=np.int64).reshape(-1)
+    T = np.empty((len(it), K, 8, 8), dtype=np.float64)
+    n_threads = n_threads or os.cpu_count() or 1
+    evals = C.c_int64(0)
+    P = lib().or_build_tiles(_p(mu, C.c_float), _p(s, C.c_float), _p(q, C.c_float), _p(a, C.c_float),
+                             mu.shape[0], _p(lp, C.c_float), _p(tm, C.c_float), lp.shape[0], int(res), int(K),
+                             _opt(kappa), _opt(k_sigma), _opt(rho_scale), int(bin_mode), mode,
+                             _p(it, C.c_int64), len(it), int(n_threads), _p(T, C.c_double), C.byref(evals))
+    if P < 0:
+        raise ValueError("oracle build_tiles: invalid arguments")
     return T, int(P)
 
 

@@ -272,6 +272,89 @@ def test_binning_brute_force(oracle_mod, seed, mode):
             assert np.all(D_[sel] == np.float32(f["D"]).view(np.uint32))
 
 
+def _numpy_footprint(mu, s, q, o, res, k_sigma=3.0):
+    """Footprint (centre pixel, radius) by independent arithmetic: the octahedral
+    map of P:L144-150 in numpy, the projected covariance Sigma_perp = B^T Sigma B
+     with an explicit tangent basis B and numpy.linalg.eigvalsh,
+    p1 = k_sigma sqrt(lambda1) / D * (H + W) / (2 pi)."""
+    m = np.asarray(mu, np.float64) - np.asarray(o, np.float64)
+    D = np.linalg.norm(m)
+    qv = m / np.abs(m).sum()
+    if qv[2] >= 0:
+        u, v = qv[0], qv[1]
+    else:
+        u = (1.0 if qv[0] >= 0 else -1.0) * (1 - abs(qv[1]))
+        v = (1.0 if qv[1] >= 0 else -1.0) * (1 - abs(qv[0]))
+    px, py = (u + 1) * res / 2 - 0.5, (v + 1) * res / 2 - 0.5
+    R = synth.quaternion_to_matrix(np.asarray(q, np.float64)[None])[0]
+    Sig = R @ np.diag(np.asarray(s, np.float64) ** 2) @ R.T
+    d = m / D
+    a = np.array([1.0, 0, 0]) if abs(d[0]) < 0.9 else np.array([0, 1.0, 0])
+    t1 = np.cross(d, a); t1 /= np.linalg.norm(t1)
+    t2 = np.cross(d, t1)
+    B = np.stack([t1, t2], 1)
+    lam1 = np.linalg.eigvalsh(B.T @ Sig @ B)[-1]
+    p1 = k_sigma * np.sqrt(lam1) / D * (2 * res) / (2 * np.pi)
+    return px, py, p1
+
+
+def _brute_tiles_vec(px, py, p1, res):
+    """Vectorised _brute_tiles: tiles holding a grid texel one of whose nine
+    inverse mirror images lies in the closed square (clamped to [-W, 2W-1]^2)."""
+    c, r = np.meshgrid(np.arange(res), np.arange(res))
+    W = H = res
+    imgs = [(c, r), (-1 - c, H - 1 - r), (2 * W - 1 - c, H - 1 - r), (W - 1 - c, -1 - r),
+            (W - 1 - c, 2 * H - 1 - r), (c - W, r - H), (c - W, r + H), (c + W, r - H), (c + W, r + H)]
+    hit = np.zeros((res, res), bool)
+    for x, y in imgs:
+        hit |= ((x >= -W) & (x <= 2 * W - 1) & (y >= -H) & (y <= 2 * H - 1) &
+                (px - p1 <= x) & (x <= px + p1) & (py - p1 <= y) & (y <= py + p1))
+    rr, cc = np.nonzero(hit)
+    return set(((rr // 8) * (res // 8) + cc // 8).tolist())
+
+
+@pytest.mark.parametrize("res", [512, 2048])
+def test_binning_geometry_production_resolution(oracle_mod, res):
+    """The oracle's binning (contract-v2 operation order, DESIGN.md "Binning
+    arithmetic contract") against a geometric brute force at production atlas
+    resolutions (cfg2 512^2, cfg5 2048^2): footprints from independent numpy
+    arithmetic (explicit tangent basis + eigvalsh), tile sets from the inverse
+    mirror map over every texel.  The op order is a rounding convention: the
+    two may differ only where a square edge lies within 1e-9 px of a lattice
+    line (then either answer is a correct reading of R6)."""
+    sc = synth.random_scene(31 + res, 40 if res == 2048 else 120, res=res, dist=(0.5, 6.0), scale=(0.002, 0.3))
+    g = sc.gaussians
+    o = sc.lights["position"][0]
+    _, T_, _, I_ = oracle_mod.bin_entries(g["means"], g["scales"], g["rotations"], o[None], res)
+    got = {}
+    for t, i in zip(T_, I_):
+        got.setdefault(int(i), set()).add(int(t))
+    ambiguous = 0
+    for i in range(g["means"].shape[0]):
+        px, py, p1 = _numpy_footprint(g["means"][i], g["scales"][i], g["rotations"][i], o, res)
+        want = _brute_tiles_vec(px, py, p1, res)
+        if got.get(i, set()) != want:
+            edges = np.array([px - p1, px + p1, py - p1, py + p1])
+            assert np.abs(edges - np.round(edges)).min() < 1e-9, (i, len(want), len(got.get(i, ())))
+            ambiguous += 1
+    assert ambiguous <= 1
+    assert len(T_) > (2000 if res == 512 else 500)
+
+
+def test_build_tiles_equals_build(oracle_mod):
+    """or_build_tiles (sampled items, compact output) is the same R8 computation
+    as or_build on those items."""
+    s = synth.random_scene(3, 150, res=32, K=8, L=2, dist=(0.3, 3.0))
+    T, P = oracle_mod.build(s.gaussians, s.lights, s.res, s.K)
+    items = np.array([0, 5, 16, 17, 31], np.int64)  # (light, tile) ids, 16 tiles per light
+    Tt, P2 = oracle_mod.build_tiles(s.gaussians, s.lights, s.res, s.K, items)
+    assert P2 == P
+    for q, it in enumerate(items):
+        l, t = divmod(int(it), 16)
+        ty, tx = divmod(t, 4)
+        assert np.array_equal(Tt[q], T[l, :, ty * 8:ty * 8 + 8, tx * 8:tx * 8 + 8])
+
+
 def test_binning_counts_simple(oracle_mod):
     """a footprint inside one tile -> 1 entry; spanning 2x2 tiles -> 4."""
     res = 64
