@@ -40,7 +40,7 @@ extern "C" {
                            n_lights outside [1, DGSM_MAX_LIGHTS], t_max<=0, bad opts, plan/run mismatch */
 #define DGSM_ENOSPC 2   /* workspace smaller than required (required size is returned) */
 #define DGSM_ECUDA 3    /* CUDA launch/runtime error */
-#define DGSM_ERANGE 4   /* problem too large: > 2^30 keys for one light, or > 2^32-1 keys in total */
+#define DGSM_ERANGE 4   /* problem too large: n >= 2^30 Gaussians, > 2^30 keys for one light, or > 2^32-1 keys in total */
 
 #define DGSM_MAX_LIGHTS 64
 #define DGSM_MAX_SHELLS 256
@@ -315,6 +315,23 @@ size_t dgsm_transfer_workspace_bytes(const dgsm_transfer_opts_t* opts, int64_t n
 int dgsm_sh_transfer(const float* sh, int sh_degree, const float* normals, const float* colors_in, int64_t n,
                      const dgsm_transfer_opts_t* opts, float* scales_out, float* colors_out, void* ws,
                      size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------
+ * The sort primitive of step a4 (the (tile, light-distance)
+ * order of R7 — the paper itself never names a sort, P:L173 only buckets).
+ * ------------------------------------------------------------------ */
+/* Device scratch bytes for sorting up to n pairs (0 for n < 0). */
+size_t dgsm_sort_temp_bytes(int64_t n);
+
+/* Stable LSD onesweep radix sort of (key, value) pairs by key bits [0, nbits)
+ * (higher key bits are ignored by the order and carried along).  keys/vals
+ * and keys_alt/vals_alt are DEVICE uint32 [n] ping-pong buffers; the sorted
+ * pairs end in (keys, vals) if *result_in_alt == 0 on return, else in
+ * (keys_alt, vals_alt).  temp: DEVICE, >= dgsm_sort_temp_bytes(n), 256-B aligned.
+ * Errors: DGSM_EINVAL (null buffers, nbits outside [0, 32]), DGSM_ENOSPC,
+ * DGSM_ERANGE (n >= 2^30: the look-back status words hold 30-bit counts). */
+int dgsm_sort_pairs_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n,
+                        int nbits, void* temp, size_t temp_bytes, int* result_in_alt, void* stream);
 
 /* Read the counters of the last DGSM_COLLECT_STATS dgsm_build_run that used
  * this run workspace (synchronises `stream`). */

@@ -349,6 +349,30 @@ int64_t or_bin(const float* means, const float* scales, const float* rotations, 
     return P;
 }
 
+/* or_bin in two calls without binning twice: or_bin_start bins and sorts and
+ * returns the entries (opaque) and P; or_bin_take copies them into the four
+ * arrays (NULL arrays: discard) and frees them. */
+void* or_bin_start(const float* means, const float* scales, const float* rotations, int64_t n,
+                   const float* light_pos, int L, int res, double k_sigma, double rho_scale, int bin_mode,
+                   int64_t* P_out)
+{
+    return or_bin_sorted(means, scales, rotations, n, light_pos, L, res, k_sigma, rho_scale, bin_mode, P_out);
+}
+
+void or_bin_take(void* h, int64_t P, uint32_t* out_light, uint32_t* out_tile, uint32_t* out_depth,
+                 uint32_t* out_index)
+{
+    or_entry* e = (or_entry*)h;
+    if (out_light)
+        for (int64_t j = 0; j < P; ++j) {
+            out_light[j] = e[j].light;
+            out_tile[j] = e[j].tile;
+            out_depth[j] = e[j].depth_bits;
+            out_index[j] = e[j].index;
+        }
+    free(e);
+}
+
 /* ------------------------------------------------------------------ */
 /* Eq.2-3: optical depth of one Gaussian along o + s d, s in [0,t] */
 /* ------------------------------------------------------------------ */

@@ -53,6 +53,11 @@ def lib():
         L.or_bin.restype = C.c_int64
         L.or_bin.argtypes = [fp, fp, fp, C.c_int64, fp, C.c_int, C.c_int, C.c_double, C.c_double,
                              C.c_int, u32p, u32p, u32p, u32p, C.c_int64]
+        L.or_bin_start.restype = C.c_void_p
+        L.or_bin_start.argtypes = [fp, fp, fp, C.c_int64, fp, C.c_int, C.c_int, C.c_double, C.c_double,
+                                   C.c_int, i64p]
+        L.or_bin_take.restype = None
+        L.or_bin_take.argtypes = [C.c_void_p, C.c_int64, u32p, u32p, u32p, u32p]
         L.or_ray_quadratic.argtypes = [dp, dp, dp, dp, dp]
         L.or_segment_depth.restype = C.c_double
         L.or_segment_depth.argtypes = [C.c_double] * 5
@@ -166,9 +171,11 @@ def bin_entries(means, scales, rotations, light_pos, res, k_sigma=3.0, rho_scale
     n, L = mu.shape[0], lp.reshape(-1, 3).shape[0]
     args = [_p(mu, C.c_float), _p(s, C.c_float), _p(q, C.c_float), n, _p(lp, C.c_float), L,
             int(res), _opt(k_sigma), _opt(rho_scale), int(bin_mode)]
-    P = lib().or_bin(*args, None, None, None, None, 0)
+    Pc = C.c_int64(0)
+    h = lib().or_bin_start(*args, C.byref(Pc))
+    P = int(Pc.value)
     outs = [np.zeros(max(P, 1), dtype=np.uint32) for _ in range(4)]
-    lib().or_bin(*args, *[_p(o, C.c_uint32) for o in outs], P)
+    lib().or_bin_take(h, P, *[_p(o, C.c_uint32) for o in outs])
     return tuple(o[:P] for o in outs)
 
 

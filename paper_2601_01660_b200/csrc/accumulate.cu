@@ -25,6 +25,7 @@
 //    written as differences into acc and a prefix sum over k restores tau_k.
 //    No tensor cores: this is not a dense contraction (FP32 FMA + MUFU bound).
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 
@@ -687,17 +688,26 @@ void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint3
         al.dtlo[l] = (float)(dt - (double)al.dt[l]);
         al.idt[l] = (float)(1.0 / dt);
     }
-    thread_local int dev_cached = -1, n_sm = 0;  // per thread: a thread may switch devices
+    // The dynamic shared-memory limit is a process-wide attribute of the kernel
+    // (per device): set it once to the largest size any K needs, so a launch on
+    // one thread never runs under a smaller limit set by another; the occupancy
+    // figures (which depend on K) are cached per thread.
+    static std::atomic<uint64_t> attr_set_mask{0};  // bit = device ordinal
+    thread_local int dev_cached = -1, n_sm = 0;
     thread_local int cached_K = -1, per_sm_tma = 0, per_sm_reg = 0;
     int dev = 0;
     cudaGetDevice(&dev);
     const size_t smem_tma = accumulate_smem_bytes(K, true), smem_reg = accumulate_smem_bytes(K, false);
+    if (dev < 64 && !(attr_set_mask.load() & (1ull << dev))) {
+        const int smax = (int)accumulate_smem_bytes(DGSM_MAX_SHELLS, true);
+        cudaFuncSetAttribute(k_accumulate<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        cudaFuncSetAttribute(k_accumulate<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        cudaFuncSetAttribute(k_accumulate<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        cudaFuncSetAttribute(k_accumulate<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+        attr_set_mask.fetch_or(1ull << dev);
+    }
     if (dev != dev_cached || K != cached_K) {
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_accumulate<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tma);
-        cudaFuncSetAttribute(k_accumulate<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tma);
-        cudaFuncSetAttribute(k_accumulate<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_reg);
-        cudaFuncSetAttribute(k_accumulate<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_reg);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_tma, k_accumulate<false, true>, kThreads, smem_tma);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_reg, k_accumulate<false, false>, kThreads, smem_reg);
         dev_cached = dev;

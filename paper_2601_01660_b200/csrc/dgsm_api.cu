@@ -165,7 +165,9 @@ int validate(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int L, int r
     if (g->n < 0) return fail(DGSM_EINVAL, "n < 0");
     if (g->n > 0 && (!g->means || !g->scales || !g->rotations || !g->opacities))
         return fail(DGSM_EINVAL, "null Gaussian array");
-    if (g->n >= (int64_t)1 << 32) return fail(DGSM_ERANGE, "n >= 2^32");
+    // the depth sort runs over all n Gaussians of a light: its look-back status
+    // words hold 30-bit counts (onesweep.cu)
+    if (g->n >= (int64_t)1 << 30) return fail(DGSM_ERANGE, "n >= 2^30");
     if (L < 1 || L > DGSM_MAX_LIGHTS) return fail(DGSM_EINVAL, "n_lights %d outside [1, %d]", L, DGSM_MAX_LIGHTS);
     if (res < 8 || res % 8 != 0 || res > 2048) return fail(DGSM_EINVAL, "atlas_res %d: need 8..2048, multiple of 8", res);
     if (K < 1 || K > DGSM_MAX_SHELLS) return fail(DGSM_EINVAL, "n_shells %d outside [1, %d]", K, DGSM_MAX_SHELLS);
@@ -694,6 +696,27 @@ int dgsm_sh_transfer(const float* sh, int sh_degree, const float* normals, const
     launch_transfer(sp, o.grid_theta, o.grid_phi, o.q, o.eps, o.s_max, o.gamma, normals, colors_in, n, scales_out,
                     colors_out, ws, (cudaStream_t)stream, &g_launches);
     return cuda_check("sh transfer");
+}
+
+size_t dgsm_sort_temp_bytes(int64_t n) {
+    if (n < 0) return 0;
+    return onesweep_temp_bytes(std::max<int64_t>(n, 1));
+}
+
+int dgsm_sort_pairs_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n,
+                        int nbits, void* temp, size_t temp_bytes, int* result_in_alt, void* stream) {
+    g_launches = 0;
+    if (!result_in_alt) return fail(DGSM_EINVAL, "null result_in_alt");
+    *result_in_alt = 0;
+    if (n < 0 || nbits < 0 || nbits > 32) return fail(DGSM_EINVAL, "need n >= 0 and 0 <= nbits <= 32");
+    if (n >= ((int64_t)1 << 30)) return fail(DGSM_ERANGE, "n >= 2^30");
+    if (n > 0 && (!keys || !vals || !keys_alt || !vals_alt || !temp)) return fail(DGSM_EINVAL, "null buffer");
+    if ((uintptr_t)temp % kAlign) return fail(DGSM_EINVAL, "temp not 256-B aligned");
+    if (temp_bytes < dgsm_sort_temp_bytes(n)) return fail(DGSM_ENOSPC, "temp %zu < %zu bytes", temp_bytes, dgsm_sort_temp_bytes(n));
+    if (n <= 1 || nbits == 0) return DGSM_OK;
+    *result_in_alt = launch_onesweep_u32(keys, vals, keys_alt, vals_alt, n, nbits, temp, (cudaStream_t)stream,
+                                         &g_launches);
+    return cuda_check("sort");
 }
 
 int dgsm_set_accumulate_events(void* before, void* after) {

@@ -34,7 +34,7 @@ EXPORTED = ["dgsm_default_opts", "dgsm_plan_workspace_bytes", "dgsm_build_plan",
             "dgsm_build_bins", "dgsm_build", "dgsm_exp_epilogue", "dgsm_query", "dgsm_query_footprint", "dgsm_strerror",
             "dgsm_last_error", "dgsm_last_launch_count", "dgsm_build_stats", "dgsm_set_accumulate_events",
             "dgsm_slab_bytes", "dgsm_active_slab", "dgsm_frame_host", "dgsm_default_transfer_opts",
-            "dgsm_transfer_workspace_bytes", "dgsm_sh_transfer"]
+            "dgsm_transfer_workspace_bytes", "dgsm_sh_transfer", "dgsm_sort_temp_bytes", "dgsm_sort_pairs_u32"]
 
 
 class Gaussians(C.Structure):
@@ -122,6 +122,10 @@ def lib() -> C.CDLL:
         L.dgsm_slab_bytes.restype = sz
         L.dgsm_active_slab.argtypes = [vp, i64, P(Roi), P(Light), C.c_int, C.c_int, C.c_int, vp, sz, vp]
         L.dgsm_active_slab.restype = C.c_int
+        L.dgsm_sort_temp_bytes.argtypes = [i64]
+        L.dgsm_sort_temp_bytes.restype = sz
+        L.dgsm_sort_pairs_u32.argtypes = [vp, vp, vp, vp, i64, C.c_int, vp, sz, P(C.c_int), vp]
+        L.dgsm_sort_pairs_u32.restype = C.c_int
         L.dgsm_strerror.argtypes = [C.c_int]
         L.dgsm_strerror.restype = C.c_char_p
         L.dgsm_last_error.argtypes = []
@@ -158,6 +162,21 @@ def _dev_f32(t: torch.Tensor, name: str, shape_tail) -> torch.Tensor:
     if tuple(t.shape[1:]) != tuple(shape_tail):
         raise DgsmError(f"{name} has shape {tuple(t.shape)}, expected [n, {shape_tail}]")
     return t.contiguous()
+
+
+def _out_f32(t: Optional[torch.Tensor], shape, device, name: str) -> torch.Tensor:
+    """An output buffer the library writes: a new tensor, or a caller tensor
+    checked to be contiguous float32 of exactly `shape` on `device` (the C ABI
+    takes raw pointers and cannot check sizes itself)."""
+    if t is None:
+        return torch.empty(shape, dtype=torch.float32, device=device)
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float32 or not t.is_contiguous():
+        raise DgsmError(f"{name} must be a contiguous float32 tensor")
+    if t.device != torch.device(device):
+        raise DgsmError(f"{name} is on {t.device}, expected {device}")
+    if tuple(t.shape) != tuple(shape):
+        raise DgsmError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    return t
 
 
 def _gaussians(g: Dict[str, torch.Tensor]):
@@ -268,10 +287,7 @@ class BuildPlan:
 
     def run(self, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
         shape = (self.n_lights, self.n_shells, self.atlas_res, self.atlas_res)
-        if out is None:
-            out = torch.empty(shape, dtype=torch.float32, device=self.device)
-        elif tuple(out.shape) != shape or out.dtype != torch.float32 or not out.is_contiguous():
-            raise DgsmError(f"out must be contiguous float32 {shape}")
+        out = _out_f32(out, shape, self.device, "out")
         ws = self._ensure_run_ws()
         rc = lib().dgsm_build_run(C.byref(self._g), self._lights, self.n_lights, C.byref(self._opts_c),
                                   C.byref(self.plan), C.c_void_p(self.plan_ws.data_ptr()), self.plan_ws.numel(),
@@ -324,6 +340,9 @@ class Builder:
 
     def __call__(self, gaussians, out: torch.Tensor, stream=None) -> torch.Tensor:
         g, keep = _gaussians(gaussians)
+        if not isinstance(out, torch.Tensor):
+            raise DgsmError("out must be a tensor")
+        out = _out_f32(out, (self.n_lights, self.K, self.res, self.res), keep[0].device, "out")
         need = C.c_size_t(0)
         for _ in range(3):
             rc = lib().dgsm_build(C.byref(g), self.lights, self.n_lights, self.res, self.K, C.byref(self._oc),
@@ -347,7 +366,7 @@ def exp_epilogue(tau: torch.Tensor, out: Optional[torch.Tensor] = None, stream=N
     """T = exp(-tau) (Eq.4), elementwise on the device; out may alias tau."""
     if not tau.is_cuda or tau.dtype != torch.float32 or not tau.is_contiguous():
         raise DgsmError("tau must be a contiguous float32 CUDA tensor")
-    out = torch.empty_like(tau) if out is None else out
+    out = _out_f32(out, tuple(tau.shape), tau.device, "out")
     rc = lib().dgsm_exp_epilogue(C.c_void_p(tau.data_ptr()), C.c_void_p(out.data_ptr()), tau.numel(),
                                  C.c_void_p(_stream_ptr(stream)))
     _check(rc, "dgsm_exp_epilogue")
@@ -367,12 +386,12 @@ def query(atlas: torch.Tensor, lights, positions: torch.Tensor, colors: Optional
         raise DgsmError(f"atlas has {L} lights, got {nl}")
     x = _dev_f32(positions, "positions", (3,))
     m = x.shape[0]
-    out = torch.empty(m, dtype=torch.float32, device=x.device) if out is None else out
+    if x.device != atlas.device:
+        raise DgsmError("positions and atlas must be on the same device")
+    out = _out_f32(out, (m,), x.device, "out")
     cptr = None
     if colors is not None:
-        if colors.dtype != torch.float32 or not colors.is_contiguous() or tuple(colors.shape) != (m, 3):
-            raise DgsmError("colors must be contiguous float32 [m, 3]")
-        cptr = C.c_void_p(colors.data_ptr())
+        cptr = C.c_void_p(_out_f32(colors, (m, 3), x.device, "colors").data_ptr())
     rc = lib().dgsm_query(C.c_void_p(atlas.data_ptr()), arr, nl, int(H), int(K), C.c_void_p(x.data_ptr()), m,
                           C.c_void_p(out.data_ptr()), cptr, C.c_void_p(_stream_ptr(stream)))
     _check(rc, "dgsm_query")
@@ -430,6 +449,14 @@ class FrameHost:
             if a.is_cuda or a.dtype != torch.float32 or not a.is_contiguous():
                 raise DgsmError("frame_host takes contiguous float32 CPU tensors")
         n, m = arrs[0].shape[0], receivers_host.shape[0]
+        tails = ((3,), (3,), (4,), ())
+        for name, a, tail in zip(("means", "scales", "rotations", "opacities"), arrs, tails):
+            if a.shape[0] != n or tuple(a.shape[1:]) not in (tail, (1,) if tail == () else tail):
+                raise DgsmError(f"{name} has shape {tuple(a.shape)}, expected [{n}, {tail}]")
+        if tuple(receivers_host.shape) != (m, 3):
+            raise DgsmError("receivers must be [m, 3]")
+        if T_host.numel() < m:
+            raise DgsmError(f"T_host holds {T_host.numel()} floats, needs {m}")
         g = Gaussians(*[C.c_void_p(a.data_ptr()) for a in arrs], n)
         need = C.c_size_t(0)
         k = self.frame & 1
@@ -512,18 +539,39 @@ def query_footprint(atlas: torch.Tensor, lights, gaussians, offsets, weights,
     w = np.ascontiguousarray(np.asarray(weights, np.float32).reshape(-1))
     if len(z) != len(w) or not 1 <= len(w) <= DGSM_MAX_FOOTPRINT_SAMPLES:
         raise DgsmError(f"need 1..{DGSM_MAX_FOOTPRINT_SAMPLES} offsets with one weight each")
-    out = torch.empty(m, dtype=torch.float32, device=mu.device) if out is None else out
+    if mu.device != atlas.device:
+        raise DgsmError("receivers and atlas must be on the same device")
+    out = _out_f32(out, (m,), mu.device, "out")
     cptr = None
     if colors is not None:
-        if colors.dtype != torch.float32 or not colors.is_contiguous() or tuple(colors.shape) != (m, 3):
-            raise DgsmError("colors must be contiguous float32 [m, 3]")
-        cptr = C.c_void_p(colors.data_ptr())
+        cptr = C.c_void_p(_out_f32(colors, (m, 3), mu.device, "colors").data_ptr())
     rc = lib().dgsm_query_footprint(C.c_void_p(atlas.data_ptr()), arr, nl, int(H), int(K),
                                     C.c_void_p(mu.data_ptr()), C.c_void_p(sc.data_ptr()), C.c_void_p(q.data_ptr()),
                                     m, z.ctypes.data_as(C.c_void_p), w.ctypes.data_as(C.c_void_p), len(w),
                                     C.c_void_p(out.data_ptr()), cptr, C.c_void_p(_stream_ptr(stream)))
     _check(rc, "dgsm_query_footprint")
     return out
+
+
+def sort_pairs(keys: torch.Tensor, vals: torch.Tensor, nbits: int, stream=None):
+    """a4's stable onesweep radix sort of (key, value) uint32 pairs by key bits
+    [0, nbits) (int32 CUDA tensors holding the uint32 bit patterns).  Returns
+    the sorted (keys, vals) as new tensors; the inputs are used as scratch."""
+    for t, nm in ((keys, "keys"), (vals, "vals")):
+        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.int32 or not t.is_contiguous() \
+                or t.dim() != 1:
+            raise DgsmError(f"{nm} must be a contiguous 1-D int32 CUDA tensor")
+    n = keys.numel()
+    if vals.numel() != n or vals.device != keys.device:
+        raise DgsmError("keys and vals must have the same length and device")
+    ka, va = torch.empty_like(keys), torch.empty_like(vals)
+    temp = _alloc(lib().dgsm_sort_temp_bytes(n), keys.device)
+    alt = C.c_int(0)
+    rc = lib().dgsm_sort_pairs_u32(*[C.c_void_p(t.data_ptr()) for t in (keys, vals, ka, va)], n, int(nbits),
+                                   C.c_void_p(temp.data_ptr()), temp.numel(), C.byref(alt),
+                                   C.c_void_p(_stream_ptr(stream)))
+    _check(rc, "dgsm_sort_pairs_u32")
+    return (ka, va) if alt.value else (keys, vals)
 
 
 def set_accumulate_events(before: Optional[torch.cuda.Event], after: Optional[torch.cuda.Event]):
