@@ -194,6 +194,37 @@ int dgsm_query(const float* atlas, const dgsm_light_t* lights, int n_lights, int
                int n_shells, const float* positions, int64_t m, float* T_out, float* colors_inout,
                void* stream);
 
+/* ------------------------------------------------------------------
+ * Receiver access order for the query (not in the paper: a B200 memory-
+ * access choice, DESIGN.md §6 a8).  A query gathers 8 taps per light from a
+ * [K][H][W] atlas of up to 2 GiB per light; receivers in arbitrary order make
+ * every lane of a warp a random DRAM access.  Sorting the receivers by a
+ * Morton code of their position makes neighbouring threads neighbours in
+ * space, hence in every light's atlas.  The receivers of P:L185-187 are the
+ * static scene Gaussians, so the order can be computed once per scene and
+ * reused every frame (or per call: dgsm_query_ordered's cost then includes it).
+ * ------------------------------------------------------------------ */
+/* Device workspace bytes of dgsm_receiver_order for m receivers. */
+size_t dgsm_order_workspace_bytes(int64_t m);
+
+/* order_out (DEVICE uint32 [m]) = the permutation of 0..m-1 sorting the
+ * receivers (DEVICE float [m][3]) by the 30-bit Morton code (10 bits per
+ * axis) of their position in the receivers' own bounding box (stable: equal
+ * codes keep index order).  ws: DEVICE, >= dgsm_order_workspace_bytes(m),
+ * 256-B aligned.  Errors: DGSM_EINVAL, DGSM_ENOSPC, DGSM_ERANGE (m >= 2^30). */
+int dgsm_receiver_order(const float* positions, int64_t m, uint32_t* order_out, void* ws, size_t ws_bytes,
+                        void* stream);
+
+/* dgsm_query visiting the receivers in the given order: thread j serves
+ * receiver order[j] (position gathered, T_out[order[j]] and colours written
+ * in place).  Every receiver's arithmetic is that of dgsm_query, so the result
+ * is bit-identical to dgsm_query for any permutation `order` (DEVICE uint32
+ * [m]); only the memory-access pattern changes.  order must be a permutation
+ * of 0..m-1 (not checked: a repeated index races on its outputs). */
+int dgsm_query_ordered(const float* atlas, const dgsm_light_t* lights, int n_lights, int atlas_res,
+                       int n_shells, const float* positions, const uint32_t* order, int64_t m, float* T_out,
+                       float* colors_inout, void* stream);
+
 /* One frame end to end from HOST memory (the benchmark's e2e path): upload the
  * occluder Gaussians (g_host: HOST arrays, pinned for copy/compute overlap) in
  * chunks, each projected as soon as it lands; build the atlas (plan + run, as

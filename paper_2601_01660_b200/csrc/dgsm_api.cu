@@ -625,6 +625,62 @@ int dgsm_query(const float* atlas, const dgsm_light_t* lights, int n_lights, int
     return cuda_check("query");
 }
 
+#ifndef DGSM_ORDER_BITS
+#define DGSM_ORDER_BITS 30
+#endif
+constexpr int kOrderBits = DGSM_ORDER_BITS;  // significant Morton bits sorted (top bits of the 30-bit code)
+
+size_t dgsm_order_workspace_bytes(int64_t m) {
+    if (m < 0) return 0;
+    Carver c(nullptr);
+    c.take<uint32_t>(m);  // Morton keys
+    c.take<uint32_t>(m);  // keys (ping-pong)
+    c.take<uint32_t>(m);  // values (ping-pong)
+    c.take<uint32_t>(8);  // bounding box
+    c.take<char>(onesweep_temp_bytes(std::max<int64_t>(m, 1)));
+    return c.off;
+}
+
+int dgsm_receiver_order(const float* positions, int64_t m, uint32_t* order_out, void* ws, size_t ws_bytes,
+                        void* stream) {
+    g_launches = 0;
+    if (m < 0) return fail(DGSM_EINVAL, "m < 0");
+    if (m >= ((int64_t)1 << 30)) return fail(DGSM_ERANGE, "m >= 2^30");
+    if (m == 0) return DGSM_OK;
+    if (!positions || !order_out || !ws) return fail(DGSM_EINVAL, "null positions, order or workspace");
+    if ((uintptr_t)ws % kAlign) return fail(DGSM_EINVAL, "workspace not 256-B aligned");
+    if (ws_bytes < dgsm_order_workspace_bytes(m))
+        return fail(DGSM_ENOSPC, "workspace %zu < %zu bytes", ws_bytes, dgsm_order_workspace_bytes(m));
+    cudaStream_t s = (cudaStream_t)stream;
+    Carver c(ws);
+    uint32_t* keys = c.take<uint32_t>(m);
+    uint32_t* keys_alt = c.take<uint32_t>(m);
+    uint32_t* vals_alt = c.take<uint32_t>(m);
+    uint32_t* box = c.take<uint32_t>(8);
+    void* temp = c.take<char>(onesweep_temp_bytes(m));
+    // the Morton kernel fills the sort's digit histograms (no separate histogram pass)
+    uint32_t* hist = onesweep_prepare(temp, m, s);
+    launch_morton(positions, m, box, keys, order_out, onesweep_digits(kOrderBits), hist, s);
+    g_launches += 2;
+    const int alt = launch_onesweep_u32(keys, order_out, keys_alt, vals_alt, m, kOrderBits, temp, s, &g_launches,
+                                        nullptr, nullptr, /*hist_ready=*/true, /*top_match=*/false);
+    if (alt) cudaMemcpyAsync(order_out, vals_alt, sizeof(uint32_t) * m, cudaMemcpyDeviceToDevice, s);
+    return cuda_check("receiver order");
+}
+
+int dgsm_query_ordered(const float* atlas, const dgsm_light_t* lights, int n_lights, int atlas_res, int n_shells,
+                       const float* positions, const uint32_t* order, int64_t m, float* T_out, float* colors_inout,
+                       void* stream) {
+    g_launches = 0;
+    if (int rc = check_query_args(atlas, lights, n_lights, atlas_res, n_shells, m)) return rc;
+    if (m > 0 && (!positions || !T_out || !order)) return fail(DGSM_EINVAL, "null positions, order or T_out");
+    const LightsParam lp = lights_param(lights, n_lights);
+    launch_query_ordered(atlas, lp, n_lights, atlas_res, n_shells, positions, order, m, T_out, colors_inout,
+                         (cudaStream_t)stream);
+    g_launches = m > 0 ? 1 : 0;
+    return cuda_check("query ordered");
+}
+
 int dgsm_query_footprint(const float* atlas, const dgsm_light_t* lights, int n_lights, int atlas_res,
                          int n_shells, const float* means, const float* scales, const float* rotations, int64_t m,
                          const float* offsets, const float* weights, int n_samples, float* T_out,

@@ -234,10 +234,12 @@ uint32_t* onesweep_prepare(void* temp, int64_t n, cudaStream_t s);
 void launch_depth_keys(const uint4* dup, int64_t n, uint32_t dmin, uint32_t* keys, uint32_t* vals,
                        const PassDigits& pd, uint32_t* hist, cudaStream_t s);
 // (gsrc/gdst optional: the last pass also writes gdst[o] = gsrc[value] at each output
-// position o, i.e. a gather by the sorted permutation; only when nbits > 0 and n > 1)
+// position o, i.e. a gather by the sorted permutation; only when nbits > 0 and n > 1.
+// top_match: rank the top pass with match.any (few distinct digits per warp, as in
+// tile keys); false: ballots on every pass (random top digits, e.g. Morton codes))
 int launch_onesweep_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n,
                         int nbits, void* temp, cudaStream_t s, int* launches, const uint32_t* gsrc = nullptr,
-                        uint32_t* gdst = nullptr, bool hist_ready = false);
+                        uint32_t* gdst = nullptr, bool hist_ready = false, bool top_match = true);
 void launch_decode_keys(const uint32_t* keys, const uint32_t* vals, const uint4* dup, const dgsm_plan_t& plan,
                         uint32_t* light_out, uint32_t* tile_out, uint32_t* depth_out, uint32_t* index_out,
                         cudaStream_t s);
@@ -271,6 +273,13 @@ void launch_active_slab(const float* x, int64_t m, const dgsm_roi_t& roi, const 
 void launch_exp(const float* tau, float* T, int64_t count, cudaStream_t s);
 void launch_query(const float* atlas, const LightsParam& lp, int n_lights, int res, int K,
                   const float* positions, int64_t m, float* T_out, float* colors, cudaStream_t s);
+void launch_query_ordered(const float* atlas, const LightsParam& lp, int n_lights, int res, int K,
+                          const float* positions, const uint32_t* order, int64_t m, float* T_out, float* colors,
+                          cudaStream_t s);
+// receivers' bounding box (box: 6 device words) + Morton keys, vals = index, and
+// their onesweep digit histograms into hist (from onesweep_prepare) (2 kernels)
+void launch_morton(const float* positions, int64_t m, uint32_t* box, uint32_t* keys, uint32_t* vals,
+                   const PassDigits& pd, uint32_t* hist, cudaStream_t s);
 void launch_query_footprint(const float* atlas, const LightsParam& lp, const FootprintParam& fp, int n_lights,
                             int res, int K, const float* means, const float* scales, const float* rotations,
                             int64_t m, float* T_out, float* colors, cudaStream_t s);

@@ -265,7 +265,7 @@ OnesweepTemp carve(void* temp, int64_t parts) {
 template <typename KeyT>
 int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt, int64_t n, int nbits,
                   void* temp, cudaStream_t s, int* launches, const uint32_t* gsrc = nullptr,
-                  uint32_t* gdst = nullptr, bool hist_ready = false) {
+                  uint32_t* gdst = nullptr, bool hist_ready = false, bool top_match = true) {
     if (n <= 1 || nbits <= 0) return 0;
     const int passes = (nbits + 7) / 8;
     const int64_t parts = (n + kTileKeys - 1) / kTileKeys;
@@ -293,7 +293,7 @@ int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt
     int flipped = 0;
     for (int p = 0; p < passes; ++p) {
         k_pass<KeyT><<<(unsigned)parts, kThreads, dyn, s>>>(ki, vi, ko, vo, n, pd.shift[p], pd.bits[p],
-                                                           p == passes - 1, t.hist + p * kRadix,
+                                                           top_match && p == passes - 1, t.hist + p * kRadix,
                                                            t.status[p & 1], t.status[(p + 1) & 1],
                                                            t.part_ctr + p, gsrc, p == passes - 1 ? gdst : nullptr);
         *launches += 1;
@@ -317,9 +317,9 @@ int launch_onesweep(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t
 
 int launch_onesweep_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n,
                         int nbits, void* temp, cudaStream_t s, int* launches, const uint32_t* gsrc,
-                        uint32_t* gdst, bool hist_ready) {
+                        uint32_t* gdst, bool hist_ready, bool top_match) {
     return onesweep_impl<uint32_t>(keys, vals, keys_alt, vals_alt, n, nbits, temp, s, launches, gsrc, gdst,
-                                   hist_ready);
+                                   hist_ready, top_match);
 }
 
 PassDigits onesweep_digits(int nbits) {

@@ -34,7 +34,8 @@ EXPORTED = ["dgsm_default_opts", "dgsm_plan_workspace_bytes", "dgsm_build_plan",
             "dgsm_build_bins", "dgsm_build", "dgsm_exp_epilogue", "dgsm_query", "dgsm_query_footprint", "dgsm_strerror",
             "dgsm_last_error", "dgsm_last_launch_count", "dgsm_build_stats", "dgsm_set_accumulate_events",
             "dgsm_slab_bytes", "dgsm_active_slab", "dgsm_frame_host", "dgsm_default_transfer_opts",
-            "dgsm_transfer_workspace_bytes", "dgsm_sh_transfer", "dgsm_sort_temp_bytes", "dgsm_sort_pairs_u32"]
+            "dgsm_transfer_workspace_bytes", "dgsm_sh_transfer", "dgsm_sort_temp_bytes", "dgsm_sort_pairs_u32",
+            "dgsm_order_workspace_bytes", "dgsm_receiver_order", "dgsm_query_ordered"]
 
 
 class Gaussians(C.Structure):
@@ -122,6 +123,12 @@ def lib() -> C.CDLL:
         L.dgsm_slab_bytes.restype = sz
         L.dgsm_active_slab.argtypes = [vp, i64, P(Roi), P(Light), C.c_int, C.c_int, C.c_int, vp, sz, vp]
         L.dgsm_active_slab.restype = C.c_int
+        L.dgsm_order_workspace_bytes.argtypes = [i64]
+        L.dgsm_order_workspace_bytes.restype = sz
+        L.dgsm_receiver_order.argtypes = [vp, i64, vp, vp, sz, vp]
+        L.dgsm_receiver_order.restype = C.c_int
+        L.dgsm_query_ordered.argtypes = [vp, P(Light), C.c_int, C.c_int, C.c_int, vp, vp, i64, vp, vp, vp]
+        L.dgsm_query_ordered.restype = C.c_int
         L.dgsm_sort_temp_bytes.argtypes = [i64]
         L.dgsm_sort_temp_bytes.restype = sz
         L.dgsm_sort_pairs_u32.argtypes = [vp, vp, vp, vp, i64, C.c_int, vp, sz, P(C.c_int), vp]
@@ -373,9 +380,27 @@ def exp_epilogue(tau: torch.Tensor, out: Optional[torch.Tensor] = None, stream=N
     return out
 
 
+def receiver_order(positions: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Spatially coherent visiting order of the receivers (dgsm_receiver_order):
+    int32 CUDA tensor [m] holding the permutation (Morton order of the positions)."""
+    x = _dev_f32(positions, "positions", (3,))
+    m = x.shape[0]
+    if out is None:
+        out = torch.empty(m, dtype=torch.int32, device=x.device)
+    elif out.dtype != torch.int32 or not out.is_contiguous() or out.numel() != m or out.device != x.device:
+        raise DgsmError("order out must be a contiguous int32 tensor [m] on the receivers' device")
+    ws = _alloc(lib().dgsm_order_workspace_bytes(m), x.device)
+    rc = lib().dgsm_receiver_order(C.c_void_p(x.data_ptr()), m, C.c_void_p(out.data_ptr()),
+                                   C.c_void_p(ws.data_ptr()), ws.numel(), C.c_void_p(_stream_ptr(stream)))
+    _check(rc, "dgsm_receiver_order")
+    return out
+
+
 def query(atlas: torch.Tensor, lights, positions: torch.Tensor, colors: Optional[torch.Tensor] = None,
-          out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
-    """DGSM sampling (§3.3): T[m] = prod_l trilinear(atlas_l, x); colors *= T in place."""
+          out: Optional[torch.Tensor] = None, stream=None, order: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """DGSM sampling (§3.3): T[m] = prod_l trilinear(atlas_l, x); colors *= T in place.
+    ``order`` (from receiver_order): visit the receivers in that order
+    (dgsm_query_ordered; bit-identical results, coherent memory access)."""
     if not atlas.is_cuda or atlas.dtype != torch.float32 or atlas.dim() != 4 or not atlas.is_contiguous():
         raise DgsmError("atlas must be a contiguous float32 CUDA tensor [L, K, H, W]")
     L, K, H, W = atlas.shape
@@ -392,6 +417,14 @@ def query(atlas: torch.Tensor, lights, positions: torch.Tensor, colors: Optional
     cptr = None
     if colors is not None:
         cptr = C.c_void_p(_out_f32(colors, (m, 3), x.device, "colors").data_ptr())
+    if order is not None:
+        if order.dtype != torch.int32 or not order.is_contiguous() or order.numel() != m or order.device != x.device:
+            raise DgsmError("order must be a contiguous int32 tensor [m] on the receivers' device")
+        rc = lib().dgsm_query_ordered(C.c_void_p(atlas.data_ptr()), arr, nl, int(H), int(K), C.c_void_p(x.data_ptr()),
+                                      C.c_void_p(order.data_ptr()), m, C.c_void_p(out.data_ptr()), cptr,
+                                      C.c_void_p(_stream_ptr(stream)))
+        _check(rc, "dgsm_query_ordered")
+        return out
     rc = lib().dgsm_query(C.c_void_p(atlas.data_ptr()), arr, nl, int(H), int(K), C.c_void_p(x.data_ptr()), m,
                           C.c_void_p(out.data_ptr()), cptr, C.c_void_p(_stream_ptr(stream)))
     _check(rc, "dgsm_query")
