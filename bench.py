@@ -17,8 +17,11 @@ onesweep sort, ranges, accumulate + exp) + dgsm_query over the receivers.
            work per launch from an instrumented (untimed) run.
 * cpu_baseline = the oracle (oracle/, fp64 C, all host cores) on a bounded
            sample: full binning + every s-th tile accumulated.
-N > 1 (torchrun): weak scaling — every rank builds and queries its own frame
-(independent light, no data-path collective); time = max over ranks.
+N > 1 (torchrun, or bench.py spawns it when WORLD_SIZE is unset): cfg1/2/4 weak
+scaling — every rank builds and queries its own frame (independent light, no
+data-path collective); cfg3/cfg5 strong scaling through distributed.StrongStep
+(--layout light | shells | gaussian); every line also carries the cfg5 strong-
+scaling run on the same N GPUs (strong_cfg5).  Time = max over ranks.
 """
 from __future__ import annotations
 
@@ -33,6 +36,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+
+from paper_2601_01660_b200 import synth  # noqa: E402  (seeded inputs only: no method arithmetic)
 
 METRIC = "DGSM build Gaussian-ray evals/s and query Gaussians/s at 1/2/4/8 B200"
 UNIT = "Gaussian-ray evals/s"
@@ -62,6 +67,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-transfer", action="store_true", help="skip the NEXT-4 transfer timing")
+    ap.add_argument("--no-strong", action="store_true", help="skip the cfg5 strong-scaling sub-record")
+    ap.add_argument("--layout", default="auto", choices=["auto", "light", "shells", "gaussian"],
+                    help="multi-GPU layout of cfg3/cfg5 (distributed.plan_layout)")
     return ap.parse_args()
 
 
@@ -89,20 +97,25 @@ def cfg_desc(s, cfg):
             "l2": "flushed before every step (256 MiB write)", "data": "synthetic, seeded (synth.py)"}
 
 
-def query_roofline(ms: float, m: int, L: int, peaks: dict):
+def query_roofline(ms: float, m: int, L: int, peaks: dict, ms_raw: float = None):
     """a8 against HBM: algorithmic bytes and the sector-realistic
-    count of a random-order gather (each row of taps is its own 32-B sector)."""
+    count of a random-order gather (each row of taps is its own 32-B sector).
+    ms: receivers in the scene's spatial (Morton) order; ms_raw: as generated."""
     peak = float(peaks.get("hbm_gbs", 7700.0))
     alg = m * (16 + 32 * L) * 1.0
     sec = m * (16 + 128 * L) * 1.0
     ach = alg / (ms * 1e-3) / 1e9
-    return {"kernel": "k_query (a8)", "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-            "frac": ach / peak, "alg_bytes_per_query": 16 + 32 * L,
-            "alg_def": "SURVEY §8(d): 12 B position + 4 B T + 8 x 4 B taps per light",
-            "sector_bytes_per_query": 16 + 128 * L,
-            "sector_frac": sec / (ms * 1e-3) / 1e9 / peak,
-            "peak_src": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md 7.7 TB/s",
-            "timing": "L2 flushed before each launch, CUDA events, host launch overhead excluded"}
+    out = {"kernel": "k_query (a8)", "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+           "frac": ach / peak, "alg_bytes_per_query": 16 + 32 * L,
+           "alg_def": "SURVEY §8(d): 12 B position + 4 B T + 8 x 4 B taps per light",
+           "sector_bytes_per_query": 16 + 128 * L,
+           "sector_frac": sec / (ms * 1e-3) / 1e9 / peak,
+           "peak_src": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md 7.7 TB/s",
+           "timing": "L2 flushed before each launch, CUDA events, host launch overhead excluded",
+           "receivers": "Morton-ordered scene receivers"}
+    if ms_raw is not None:
+        out["raw_order_frac"] = alg / (ms_raw * 1e-3) / 1e9 / peak
+    return out
 
 
 def transfer_timing(dev, n: int = 150_000, d: int = 3):
@@ -272,284 +285,464 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------- GPU leg
-def run_dgsm(args):
+PAPER_CONTEXT = {
+    "build_s_per_frame": {"roi_and_light_space_culling": 0.13, "no_light_space_culling": 17.1,
+                          "no_roi_culling": 29.1},
+    "hardware": "NVIDIA A100", "source": "PAPER.md:335 (§4.4 ablation D), 'across 5 scenes'",
+    "note": "context only: other hardware; atlas size, K, occluder counts not stated by the paper",
+}
+
+
+class Ctx:
+    """Process / device context of one rank."""
+
+    def __init__(self, args):
+        import torch
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        if self.world != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={self.world}")
+        if not torch.cuda.is_available():
+            sys.exit("bench.py: no CUDA device (the product arm has no CPU fallback)")
+        if torch.cuda.device_count() < self.world and self.world > 1 and self.local >= torch.cuda.device_count():
+            sys.exit(f"bench.py: rank {self.rank} needs GPU {self.local}, {torch.cuda.device_count()} visible")
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device("cuda", self.local)
+        self.peaks = {}
+        pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        if os.path.exists(pk):
+            self.peaks = json.load(open(pk))
+        self.n_sm = torch.cuda.get_device_properties(self.dev).multi_processor_count
+        self.flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=self.dev)  # 256 MiB > 126 MB L2
+        self.flush.zero_()  # first touch (page mapping) outside any timing
+
+    def barrier(self):
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.barrier()
+
+    def max_over_ranks(self, x: float) -> float:
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return x
+        t = torch.tensor([x], device=self.dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0])
+
+    def sum_over_ranks(self, x: float) -> float:
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return x
+        t = torch.tensor([x], device=self.dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t[0])
+
+
+def fp32_peak(ctx):
+    sm_mhz = float(ctx.peaks.get("sm_max_mhz", 1965.0))
+    return ctx.n_sm * 128 * sm_mhz * 1e6 / 1e12, f"{ctx.n_sm} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (FMA = 1 op)"
+
+
+def time_steps(step, K: int, warmup: int, ctx, sample_clocks: bool = True):
+    """W untimed warm-up steps, then EXACTLY K timed steps, each after an L2 flush
+    (outside the step's events), bracketed by barrier + synchronize; device time
+    by CUDA events on the launching stream; the accumulation kernel's events are
+    recorded by the library around its launch."""
     import torch
-    import torch.distributed as dist
-
-    from paper_2601_01660_b200 import build_ext, dgsm
-
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    if rank == 0:
-        build_ext.build()
-    if world > 1:
-        dist.barrier()
-    from paper_2601_01660_b200 import distributed as Dd
-
-    # multi-light configs (3, 5): strong scaling over the node: lights
-    # dealt to ranks; with fewer lights than ranks, Gaussian shards + partial-tau
-    # reduce-scatter over K + exp epilogue; the query product is an all-reduce(PRODUCT).
-    strong = args.config in (3, 5)
-    s = workload(args.config, args.scale, 0 if strong else rank)
-    g_host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in s.gaussians.items()}
-    q_host = torch.from_numpy(np.ascontiguousarray(s.queries)).pin_memory()
-    g = {k: v.to(dev) for k, v in g_host.items()}
-    xq = q_host.to(dev)
-    m = xq.shape[0]
-    lights_b, g_b, gsz, first_of_group, pgroup = s.lights, g, 1, True, None
-    if strong:
-        lay = Dd.plan_layout(s.L, world)
-        pgroups = Dd.make_groups(lay) if world > 1 else [None] * len(lay.groups)
-        j = lay.group_index(rank)
-        my = lay.lights_of[j] if j >= 0 else []
-        idx, gsz = lay.shard_of(rank)
-        first_of_group = j >= 0 and lay.groups[j][0] == rank
-        pgroup = pgroups[j] if j >= 0 else None
-        lights_b = dict(position=s.lights["position"][my], t_max=s.lights["t_max"][my])
-        if gsz > 1:
-            s0, s1 = Dd.shard_range(s.n, idx, gsz)
-            g_b = {k: v[s0:s1] for k, v in g.items()}
-    L_b = int(np.asarray(lights_b["position"]).reshape(-1, 3).shape[0])
-    atlas = torch.empty((L_b, s.K, s.res, s.res), dtype=torch.float32, device=dev)
-    chunk = torch.empty((s.K // gsz, s.res, s.res), dtype=torch.float32, device=dev) if gsz > 1 else None
-    T_out = torch.empty(m, dtype=torch.float32, device=dev)
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
-
-    builder = dgsm.Builder(lights_b, s.res, s.K, dgsm.Options(output_tau=gsz > 1))
-
-    def step():
-        builder(g_b, atlas)  # dgsm_build: plan + run in one C call
-        nl = builder.launches
-        if gsz > 1:  # partial tau -> reduce-scatter over K -> exp on the owned shells -> all-gather
-            for q in range(L_b):
-                dist.reduce_scatter_tensor(chunk, atlas[q], op=dist.ReduceOp.SUM, group=pgroup)
-                dgsm.exp_epilogue(chunk, out=chunk)
-                nl += dgsm.last_launch_count()
-                dist.all_gather_into_tensor(atlas[q], chunk, group=pgroup)
-        if first_of_group:
-            dgsm.query(atlas, lights_b, xq, out=T_out)
-            nl += dgsm.last_launch_count()
-        else:
-            T_out.fill_(1.0)
-        if strong and world > 1:
-            dist.all_reduce(T_out, op=dist.ReduceOp.PRODUCT)
-        return n_keys_frame, nl
-
-    # instrumented (untimed) run: algorithmic work of the accumulation kernel
-    sp = dgsm.BuildPlan(g_b, lights_b, s.res, s.K, dgsm.Options(collect_stats=True))
-    sp.run(out=atlas)
-    st = sp.stats()
-    n_keys_frame = sp.n_keys  # P of this frame (the build is deterministic)
-    del sp
-    alg_ops = OPS_PER_PAIR_SURVEY * st["pairs"]
-    needed_ops = (OPS_PAIR * st["pairs"] + OPS_LIVE * st["pairs_live"] + OPS_SHELL * st["window_shells"]
-                  + OPS_STEP * st["steps"])
-
-    flush.zero_()  # first touch of the flush buffer is slow (page mapping): keep it out of the timing
-    for _ in range(args.warmup):
-        flush.zero_()
+    from paper_2601_01660_b200 import dgsm
+    for _ in range(warmup):
+        ctx.flush.zero_()
         step()
     torch.cuda.synchronize()
-
-    K = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
     for e in ev:  # create the CUDA events now (torch creates them lazily on record)
         for x in e:
             x.record()
     torch.cuda.synchronize()
-    sampler = ClockSampler(local)
-    sampler.start()
-    if world > 1:
-        dist.barrier()
+    sampler = ClockSampler(ctx.local)
+    if sample_clocks:
+        sampler.start()
+    ctx.barrier()
     torch.cuda.synchronize()
-    P = 0
     launches = 0
-    host_ms = []
     wall0 = time.perf_counter()
-    flush_ms = []
     for i in range(K):
-        e0, e_acc0, e_acc1, e_q, e1 = ev[i]
-        e_q.record()  # before the L2 flush (not part of the step)
-        f0 = time.perf_counter()
-        flush.zero_()
-        flush_ms.append((time.perf_counter() - f0) * 1e3)
-        dgsm.set_accumulate_events(e_acc0, e_acc1)
+        e0, ea, eb, e1 = ev[i]
+        ctx.flush.zero_()
+        dgsm.set_accumulate_events(ea, eb)
         e0.record()
-        h0 = time.perf_counter()
-        n_keys, nl = step()
-        host_ms.append((time.perf_counter() - h0) * 1e3)
+        launches += step()
         e1.record()
-        launches += nl
-        P = n_keys
     dgsm.set_accumulate_events(None, None)
     torch.cuda.synchronize()
     wall1 = time.perf_counter()
-    wall_ms = (wall1 - wall0) * 1e3
-    if world > 1:
-        dist.barrier()
-    clocks = sampler.stop(wall0, wall1)
-    t_step = [ev[i][0].elapsed_time(ev[i][4]) for i in range(K)]          # ms
+    ctx.barrier()
+    clocks = sampler.stop(wall0, wall1) if sample_clocks else None
+    t_step = [ev[i][0].elapsed_time(ev[i][3]) for i in range(K)]
     t_acc = [ev[i][1].elapsed_time(ev[i][2]) for i in range(K)]
-    t_flush = [ev[i][3].elapsed_time(ev[i][0]) for i in range(K)]
-    t_gap = [ev[i][4].elapsed_time(ev[i + 1][3]) for i in range(K - 1)]
-    # query time: separate short timing loop (same kernel, L2 flushed); a ~0.2 ms
-    # device spin before the start event keeps the host's launch overhead out of it
-    tq = []
-    for i in range(K):
-        flush.zero_()
-        torch.cuda._sleep(400_000)
-        a, b = ev[i][0], ev[i][4]
-        a.record()
-        dgsm.query(atlas, lights_b, xq, out=T_out)
-        b.record()
-    torch.cuda.synchronize()
-    tq = [ev[i][0].elapsed_time(ev[i][4]) for i in range(K)]
-    transfer = None if args.no_transfer else transfer_timing(dev)
-    total_ms = float(np.sum(t_step))
-    if world > 1:
-        t = torch.tensor([total_ms, float(64 * P)], device=dev, dtype=torch.float64)
-        tmax = t.clone(); dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-        units = t[1:].clone(); dist.all_reduce(units, op=dist.ReduceOp.SUM)
-        total_ms_max, units_all = float(tmax[0]), float(units[0])
-    else:
-        total_ms_max, units_all = total_ms, float(64 * P)
-    value = units_all * K / (total_ms_max * 1e-3)
+    return {"t_step": t_step, "t_acc": t_acc, "launches": launches, "wall_ms": (wall1 - wall0) * 1e3,
+            "clocks": clocks}
 
-    # e2e through the public API with host buffers (pinned), copies inside the timed region
+
+def time_fn(fn, reps: int, ctx):
+    """Device time of fn() per call (median), L2 flushed before each; a ~0.2 ms
+    device spin before the start event keeps the host's launch overhead out."""
+    import torch
+    ts = []
+    for _ in range(reps):
+        ctx.flush.zero_()
+        torch.cuda._sleep(400_000)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def accumulate_roofline(st, acc_ms, ctx, cfg, scale):
+    """a6 against the FP32 pipe: SURVEY §8(d)'s per-pair figure (frac) and the
+    work the kernel actually does per pair class (work_frac)."""
+    peak, peak_def = fp32_peak(ctx)
+    alg_ops = OPS_PER_PAIR_SURVEY * st["pairs"]
+    needed = OPS_PAIR * st["pairs"] + OPS_LIVE * st["pairs_live"] + OPS_SHELL * st["window_shells"] + OPS_STEP * st["steps"]
+    achieved = alg_ops / (acc_ms * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "accumulate_traffic.json")
+    if os.path.exists(prof):
+        try:
+            pj = json.load(open(prof))
+            if pj.get("config") == f"cfg{cfg}" and abs(pj.get("scale", 1.0) - scale) < 1e-9:
+                traffic = pj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    return {"kernel": "k_accumulate (a6)", "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "peak_def": peak_def, "frac": achieved / peak, "traffic": traffic, "alg_ops_per_launch": int(alg_ops),
+            "alg_def": f"SURVEY §8(d): {OPS_PER_PAIR_SURVEY} FP32+MUFU ops per Gaussian-ray pair x {int(st['pairs'])} pairs",
+            "work_ops_per_launch": int(needed),
+            "work_frac": needed / (acc_ms * 1e-3) / 1e12 / peak,
+            "work_def": (f"ops the kernel needs per pair class (DESIGN.md §6): {OPS_PAIR} per pair, +{OPS_LIVE} per live "
+                         f"pair, +{OPS_SHELL} per window shell, +{OPS_STEP} per saturated step")}
+
+
+def build_stats(dgsm, g, lights, res, K):
+    """Instrumented (untimed) build: the accumulation's work counters and P."""
+    sp = dgsm.BuildPlan(g, lights, res, K, dgsm.Options(collect_stats=True))
+    sp.run()
+    st = sp.stats()
+    P = sp.n_keys
+    del sp
+    return st, P
+
+
+def order_receivers(dgsm, xq, ctx):
+    """Spatially coherent layout of the static scene receivers (done once per
+    scene, DESIGN.md §6 a8): the Morton permutation, its device time, and the
+    receivers in that order."""
+    order = dgsm.receiver_order(xq)
+    ms = time_fn(lambda: dgsm.receiver_order(xq, out=order), 3, ctx)
+    return order.long(), ms
+
+
+def cpu_baseline_line(s, cfg, seconds):
+    cb = oracle_sample(s, seconds, cores())
+    return {"value": cb["value"], "unit": UNIT, "cores": cores(), "kind": "oracle",
+            "sample": f"cfg{cfg}: full oracle binning ({cb['P']} keys) + Eq.3 accumulation on every "
+                      f"{cb['stride']}-th (light, tile): {cb['evals']} evals in {cb['seconds']:.1f} s; "
+                      f"full oracle build estimated {cb['est_full_build_s']:.0f} s"}
+
+
+# ----------------------------------------------------------- weak scaling
+def weak_bench(args, ctx):
+    """cfg1/2/4: every rank builds and queries its own frame (an independent
+    light), no data-path collective; time = max over ranks."""
+    import torch
+    from paper_2601_01660_b200 import dgsm
+
+    s = workload(args.config, args.scale, ctx.rank)
+    g_host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in s.gaussians.items()}
+    g = {k: v.to(ctx.dev) for k, v in g_host.items()}
+    xq_raw = torch.from_numpy(np.ascontiguousarray(s.queries)).to(ctx.dev)
+    order, order_ms = order_receivers(dgsm, xq_raw, ctx)
+    xq = xq_raw[order].contiguous()
+    q_host = xq.cpu().pin_memory()
+    m = xq.shape[0]
+    atlas = torch.empty((s.L, s.K, s.res, s.res), dtype=torch.float32, device=ctx.dev)
+    T_out = torch.empty(m, dtype=torch.float32, device=ctx.dev)
+    builder = dgsm.Builder(s.lights, s.res, s.K, device=ctx.dev)
+
+    def step():
+        builder(g, atlas)  # dgsm_build: plan + run in one C call
+        nl = builder.launches
+        dgsm.query(atlas, s.lights, xq, out=T_out)
+        return nl + dgsm.last_launch_count()
+
+    st, P = build_stats(dgsm, g, s.lights, s.res, s.K)
+    r = time_steps(step, args.steps, args.warmup, ctx)
+    K = args.steps
+    total_ms = float(np.sum(r["t_step"]))
+    total_max = ctx.max_over_ranks(total_ms)
+    units_all = ctx.sum_over_ranks(64.0 * P)
+    value = units_all * K / (total_max * 1e-3)
+    tq = time_fn(lambda: dgsm.query(atlas, s.lights, xq, out=T_out), K, ctx)
+    tq_raw = time_fn(lambda: dgsm.query(atlas, s.lights, xq_raw, out=T_out), K, ctx)
+
     e2e = None
     if not args.no_e2e:
         T_host = torch.empty(m, dtype=torch.float32).pin_memory()
-        # one rank per frame (no collective in the step): the library's host-buffer
-        # entry point dgsm_frame_host (chunked upload overlapped with projection,
-        # receivers uploaded under the build, T copied back); otherwise torch copies
-        # around the collective step
-        use_frame = gsz == 1 and (not strong or world == 1)
-        if use_frame:
-            fr = dgsm.FrameHost(lights_b, s.res, s.K)
-            for _ in range(2):
-                fr(g_host, q_host, T_host)
+        fr = dgsm.FrameHost(s.lights, s.res, s.K, device=ctx.dev)
+        for _ in range(2):
+            fr(g_host, q_host, T_host)
+        torch.cuda.synchronize()
+        # frames back to back (the steady state of a frame stream): frame i+1's uploads
+        # (copy stream) overlap frame i's build; time = the K-frame span minus the flushes
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fl = []
+        e0.record()
+        for i in range(K):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            ctx.flush.zero_()
+            b.record()
+            fl.append((a, b))
+            fr(g_host, q_host, T_host)
+        e1.record()
+        torch.cuda.synchronize()
+        te_ms = e0.elapsed_time(e1) - float(np.sum([a.elapsed_time(b) for a, b in fl]))
+        # one isolated frame at a time (synchronised: no overlap with a neighbour)
+        iso = []
+        for i in range(K):
+            ctx.flush.zero_()
             torch.cuda.synchronize()
-        te = []
-        if use_frame:
-            # frames back to back: frame i+1's uploads (copy stream) overlap frame i's
-            # build (dgsm_frame_host waits only for the previous frame's last readers of
-            # its input buffers); time = the whole K-frame span minus the L2 flushes
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for i in range(K):
-                a, b = ev[i][0], ev[i][4]
-                a.record()
-                flush.zero_()
-                b.record()
-                te.append((a, b))
-                fr(g_host, q_host, T_host)
-            e1.record()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fr(g_host, q_host, T_host)
+            b.record()
             torch.cuda.synchronize()
-            te_ms = e0.elapsed_time(e1) - float(np.sum([a.elapsed_time(b) for a, b in te]))
-        else:
-            for i in range(K):
-                flush.zero_()
-                a, b = ev[i][0], ev[i][4]
-                a.record()
-                for k_, v_ in g_host.items():          # this step's inputs, host -> device
-                    g[k_].copy_(v_, non_blocking=True)
-                xq.copy_(q_host, non_blocking=True)
-                step()
-                T_host.copy_(T_out, non_blocking=True)  # the step's result, device -> host
-                b.record()
-                te.append((a, b))
-            torch.cuda.synchronize()
-            te_ms = float(np.sum([a.elapsed_time(b) for a, b in te]))
-        if world > 1:
-            t = torch.tensor([te_ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            te_ms = float(t[0])
+            iso.append(a.elapsed_time(b))
+        te_max = ctx.max_over_ranks(te_ms)
         h2d = sum(v.numel() * 4 for v in g_host.values()) + q_host.numel() * 4
-        e2e = {"value": units_all * K / (te_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(m * 4), "ms_per_step": te_ms / K,
-               "api": ("dgsm_frame_host (host buffers), frames pipelined: each frame's uploads overlap the "
-                       "previous frame's build; K-frame span minus L2 flushes") if use_frame
-                      else "torch copies + dgsm_build_plan/run/query"}
+        e2e = {"value": units_all * K / (te_max * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(m * 4), "ms_per_step": te_max / K,
+               "isolated_ms_per_frame": float(np.median(iso)),
+               "isolated_value": units_all / (ctx.max_over_ranks(float(np.median(iso))) * 1e-3),
+               "api": ("dgsm_frame_host (host buffers): value = frames back to back, each frame's uploads "
+                       "overlapping the previous frame's build (K-frame span minus L2 flushes); "
+                       "isolated_* = one synchronised frame at a time")}
+    acc_ms = float(np.mean(r["t_acc"]))
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ctx.world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": total_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "dtype_note": "accumulation and query taps in fp32; binning geometry and query index math in fp64",
+        "data": "synthetic",
+        "config": dict(cfg_desc(s, args.config),
+                       parallelism=f"{ctx.world} independent frame(s), one per rank, no data-path collective",
+                       receivers=("scene receivers stored in Morton order (dgsm_receiver_order, once per scene: "
+                                  f"{order_ms * 1e3:.0f} us)")),
+        "step_ms_each": [round(x, 3) for x in r["t_step"]], "step_ms_median": float(np.median(r["t_step"])),
+        "wall_ms_per_step_incl_flush": r["wall_ms"] / K,
+        "accumulate_ms": acc_ms, "accumulate_share": acc_ms / float(np.mean(r["t_step"])),
+        "query_ms": tq, "query_ms_raw_order": tq_raw, "receiver_order_ms_once": order_ms,
+        "query_gaussians_per_s": m / (tq * 1e-3) * ctx.world,
+        "keys_P": int(P), "gaussian_ray_evals_per_step": int(64 * P),
+        "accumulate_work": {k: int(v) for k, v in st.items()},
+        "gpu_launches": int(r["launches"]),
+        "roofline": accumulate_roofline(st, acc_ms, ctx, args.config, args.scale),
+        "query_roofline": query_roofline(tq, m, s.L, ctx.peaks, tq_raw),
+        "clocks": r["clocks"], "paper_context": PAPER_CONTEXT,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    return line, s
 
-    if rank == 0:
-        peaks = {}
-        pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-        if os.path.exists(pk_path):
-            peaks = json.load(open(pk_path))
-        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-        props = torch.cuda.get_device_properties(dev)
-        n_sm = props.multi_processor_count
-        peak_tops = n_sm * 128 * sm_mhz * 1e6 / 1e12   # FP32 lanes x clock
-        acc_ms = float(np.mean(t_acc))
-        achieved = alg_ops / (acc_ms * 1e-3) / 1e12
-        traffic = None
-        prof = os.path.join(ROOT, "profiles", "accumulate_traffic.json")
-        if os.path.exists(prof):
-            try:
-                pj = json.load(open(prof))
-                if pj.get("config") == f"cfg{args.config}" and abs(pj.get("scale", 1.0) - args.scale) < 1e-9:
-                    traffic = pj.get("dram_bytes_per_launch")
-            except Exception:
-                traffic = None
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
-            "warmup": args.warmup, "ms_per_step": total_ms_max / K, "higher_is_better": True,
-            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32", "dtype_note": "accumulation and query taps in fp32; binning geometry and query index math in fp64",
-            "data": "synthetic",
-            "config": dict(cfg_desc(s, args.config),
-                           parallelism=(f"{world} rank(s): lights dealt to ranks, {gsz} rank(s) per light "
-                                        f"(Gaussian shards + NCCL reduce-scatter of tau when > 1)" if strong else
-                                        f"{world} independent frame(s), one per rank, no data-path collective")),
-            "step_ms_each": [round(x, 3) for x in t_step],
-            "step_ms_median": float(np.median(t_step)),
-            "wall_ms_per_step_incl_flush": wall_ms / K,
-            "accumulate_ms": acc_ms,
-            "accumulate_share": acc_ms / float(np.mean(t_step)),
-            "query_ms": float(np.mean(tq)),
-            "query_gaussians_per_s": m / (float(np.mean(tq)) * 1e-3) * (1 if strong else world),
-            "keys_P": int(P), "gaussian_ray_evals_per_step": int(64 * P),
-            "accumulate_work": {k: int(v) for k, v in st.items()},
-            "gpu_launches": int(launches),
-            "roofline": {"kernel": "k_accumulate (a6)", "bound": "alu", "achieved": achieved,
-                         "peak": peak_tops, "unit": "TFLOP/s",
-                         "peak_def": f"{n_sm} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (FMA = 1 op)",
-                         "frac": achieved / peak_tops, "traffic": traffic,
-                         "alg_ops_per_launch": int(alg_ops),
-                         "alg_def": f"SURVEY §8(d): {OPS_PER_PAIR_SURVEY} FP32+MUFU ops per Gaussian-ray pair "
-                                    f"x {int(st['pairs'])} pairs",
-                         "needed_ops_per_launch": int(needed_ops),
-                         "needed_ops_frac": needed_ops / (acc_ms * 1e-3) / 1e12 / peak_tops},
-            "query_roofline": query_roofline(float(np.mean(tq)), m, s.L, peaks),
-            "transfer": transfer,
-            "clocks": clocks,
-        }
-        if e2e:
-            line["e2e"] = e2e
-        if not args.no_cpu_baseline and world == 1:
-            cb = oracle_sample(s, args.cpu_seconds, cores())
-            line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": cores(), "kind": "oracle",
-                                    "sample": f"cfg{args.config}: full oracle binning ({cb['P']} keys) + Eq.3 "
-                                              f"accumulation on every {cb['stride']}-th (light, tile): "
-                                              f"{cb['evals']} evals in {cb['seconds']:.1f} s; "
-                                              f"full oracle build estimated {cb['est_full_build_s']:.0f} s"}
+
+# --------------------------------------------------------- strong scaling
+def strong_bench(cfg, steps, warmup, ctx, scale=1.0, layout_mode="auto", e2e=True, clocks=True):
+    """cfg3/cfg5 over the node: distributed.StrongStep — the
+    layout's sharded build (light-parallel, or Gaussian shards + one NCCL
+    reduce-scatter + exp) and the sharded query (chunk query + all-reduce SUM of
+    split lights + all-reduce PRODUCT).  Total work is fixed (strong scaling)."""
+    import torch
+    from paper_2601_01660_b200 import dgsm
+    from paper_2601_01660_b200 import distributed as D
+
+    s = synth.make_config(cfg, scale=scale)
+    g_host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in s.gaussians.items()}
+    g = {k: v.to(ctx.dev) for k, v in g_host.items()}
+    xq_raw = torch.from_numpy(np.ascontiguousarray(s.queries)).to(ctx.dev)
+    order, order_ms = order_receivers(dgsm, xq_raw, ctx)
+    xq = xq_raw[order].contiguous()
+    del xq_raw, order
+    m = xq.shape[0]
+    # LPT costs: per-light key counts P_l from one replicated plan (once per scene here;
+    # per frame a renderer would reuse the previous frame's counts)
+    plan = dgsm.BuildPlan(g, s.lights, s.res, s.K)
+    ranges = plan.light_key_ranges()
+    P_all = plan.n_keys
+    del plan
+    layout = D.plan_layout(s.L, ctx.world, s.K, D.light_costs(ranges), layout_mode)
+    pgroups = D.make_groups(layout) if ctx.world > 1 else [None] * len(layout.groups)
+    cache = {}
+    step_obj = D.StrongStep(layout, pgroups, s.lights, s.res, D.cuda_build_fn(cache, s.res, s.K), D.cuda_exp_fn,
+                            D.cuda_chunks_fn(s.res, s.K), D.cuda_combine_fn, ctx.dev)
+    b = step_obj.builder
+    if b.g > 1:
+        s0, s1 = D.shard_range(s.n, b.idx, b.g)
+    else:
+        s0, s1 = 0, s.n
+    g_mine = {k: v[s0:s1] for k, v in g.items()}
+    st, P_mine = build_stats(dgsm, g_mine, b.sub, s.res, s.K)
+
+    # launch count of one step on this rank (library counters, one untimed step):
+    # the build, the exp epilogue (Gaussian shards), the chunk query, the combine
+    step_obj(g, xq)
+    j = layout.group_index(ctx.rank)
+    split = layout.split_lights(j) if j >= 0 else []
+    nl = (sum(cb[0].launches for cb in cache.values()) + (1 if b.g > 1 else 0) + 1
+          + (1 if split and layout.groups[j][0] == ctx.rank else 0))
+
+    def step_counted():
+        step_obj(g, xq)
+        return nl
+
+    r = time_steps(step_counted, steps, warmup, ctx, sample_clocks=clocks)
+    total_ms = float(np.sum(r["t_step"]))
+    total_max = ctx.max_over_ranks(total_ms)
+    value = 64.0 * P_all * steps / (total_max * 1e-3)
+    acc_ms = float(np.mean(r["t_acc"]))
+    acc_max = ctx.max_over_ranks(acc_ms)
+    tq = time_fn(lambda: D.query_sharded(step_obj.atlas, s.lights, xq, layout, pgroups, step_obj.chunks_fn,
+                                         step_obj.combine_fn, s.res), steps, ctx)
+    tq = ctx.max_over_ranks(tq)
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ctx.world, "steps": steps, "warmup": warmup,
+        "ms_per_step": total_max / steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "dtype_note": "accumulation and query taps in fp32; binning geometry and query index math in fp64",
+        "data": "synthetic",
+        "config": dict(cfg_desc(s, cfg), parallelism=(
+            f"{ctx.world} rank(s), layout {layout.mode}: groups {layout.groups}, lights {layout.lights_of}"
+            + (" (Gaussian shards + one NCCL reduce-scatter of tau over the group's (light, shell) planes + exp; "
+               "query: chunk sums all-reduced, product all-reduced)" if max(len(x) for x in layout.groups) > 1
+               else " (lights dealt by LPT on per-light key counts; no build communication; query product "
+                    "all-reduced)")),
+            receivers=f"Morton-ordered once per scene ({order_ms * 1e3:.0f} us)"),
+        "step_ms_each": [round(x, 3) for x in r["t_step"]],
+        "keys_P": int(P_all), "keys_P_per_light": [int(e - b_) for b_, e in ranges],
+        "gaussian_ray_evals_per_step": int(64 * P_all),
+        "accumulate_ms_rank0": acc_ms, "accumulate_ms_max": acc_max,
+        "accumulate_share": acc_ms / float(np.mean(r["t_step"])),
+        "query_ms": tq, "query_gaussians_per_s": m / (tq * 1e-3),
+        "gpu_launches": int(r["launches"]),
+        "roofline": accumulate_roofline(st, acc_ms, ctx, cfg, scale),
+        "query_roofline": query_roofline(tq, m, s.L, ctx.peaks) if ctx.world == 1 else None,
+        "clocks": r["clocks"],
+    }
+    if e2e:
+        # this rank's inputs host -> device each step (its Gaussian range and all
+        # receivers), the product T device -> host on rank 0, inside the timed region
+        g_h = {k: v[s0:s1] for k, v in g_host.items()}
+        g_d = {k: v[s0:s1] for k, v in g.items()}
+        q_host = xq.cpu().pin_memory()
+        T_host = torch.empty(m, dtype=torch.float32).pin_memory()
+        te = []
+        ctx.barrier()
+        for i in range(steps):
+            ctx.flush.zero_()
+            a, bb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for k_, v_ in g_h.items():
+                g_d[k_].copy_(v_, non_blocking=True)
+            xq.copy_(q_host, non_blocking=True)
+            T = step_obj(g, xq)
+            if ctx.rank == 0:
+                T_host.copy_(T, non_blocking=True)
+            bb.record()
+            te.append((a, bb))
+        torch.cuda.synchronize()
+        te_ms = ctx.max_over_ranks(float(np.sum([a.elapsed_time(bb) for a, bb in te])))
+        out["e2e"] = {"value": 64.0 * P_all * steps / (te_ms * 1e-3), "unit": UNIT,
+                      "h2d_bytes_per_step": int(sum(v.numel() * 4 for v in g_h.values()) + m * 12),
+                      "d2h_bytes_per_step": int(m * 4) if ctx.rank == 0 else 0, "ms_per_step": te_ms / steps,
+                      "api": "torch copies (pinned host) + distributed.StrongStep (dgsm_build / exp / query_chunks)"}
+    del cache, step_obj, g, g_mine
+    torch.cuda.empty_cache()
+    return out, s
+
+
+def run_dgsm(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_01660_b200 import build_ext
+
+    ctx = Ctx(args)
+    if ctx.world > 1:
+        dist.init_process_group("nccl", device_id=ctx.dev)
+    if ctx.rank == 0:
+        build_ext.build()
+    ctx.barrier()
+    strong = args.config in (3, 5)
+    if strong:
+        line, s = strong_bench(args.config, args.steps, args.warmup, ctx, args.scale, args.layout,
+                               e2e=not args.no_e2e)
+    else:
+        line, s = weak_bench(args, ctx)
+    if not args.no_strong and args.config == 2:
+        # the strong-scaling configuration of BASELINE (cfg5) on the same N GPUs
+        try:
+            sub, _ = strong_bench(5, min(args.steps, 5), 3, ctx, 1.0, args.layout, e2e=False, clocks=False)
+            line["strong_cfg5"] = {k: sub[k] for k in ("value", "unit", "ms_per_step", "n_gpus", "scaling", "config",
+                                                        "keys_P", "keys_P_per_light", "accumulate_ms_max",
+                                                        "query_ms", "roofline", "step_ms_each")}
+        except Exception as e:  # reported, not fatal for the main line
+            line["strong_cfg5"] = {"error": f"{type(e).__name__}: {e}"[:300]}
+    if ctx.rank == 0:
+        if not args.no_transfer:
+            line["transfer"] = transfer_timing(ctx.dev)
+        if not args.no_cpu_baseline and ctx.world == 1:
+            if 64 * line["keys_P"] <= 64 * 60_000_000:
+                line["cpu_baseline"] = cpu_baseline_line(s, args.config, args.cpu_seconds)
+            else:
+                line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": cores(), "kind": "oracle",
+                                        "sample": "skipped: the oracle's full binning of this many keys exceeds "
+                                                  "the bounded sample (see the cfg2 line)"}
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
+    if ctx.world > 1:
+        ctx.barrier()
         dist.destroy_process_group()
+
+
+def spawn(args):
+    """`bench.py --gpus N` without a torchrun environment: launch N ranks with
+    torch.distributed.run on this node (127.0.0.1) and pass the line through."""
+    import torch
+    n = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if n < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {n}")
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_dgsm(args)
+        return 0
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn(args)
+    run_dgsm(args)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

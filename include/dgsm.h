@@ -225,6 +225,33 @@ int dgsm_query_ordered(const float* atlas, const dgsm_light_t* lights, int n_lig
                        int n_shells, const float* positions, const uint32_t* order, int64_t m, float* T_out,
                        float* colors_inout, void* stream);
 
+/* ------------------------------------------------------------------
+ * Multi-GPU query of sharded atlases (the product over lights
+ * Q13 and the linearity of the trilinear sample in the atlas values).  After
+ * a reduce-scatter of the partial optical depth a rank holds, per light, a
+ * chunk of shells [k_begin, k_end) of T.  dgsm_query_chunks samples each held
+ * chunk at the receivers with the taps of dgsm_query, counting taps on shells
+ * outside the chunk as 0:
+ *   split[l] == 0 (the chunk holds every shell, k_begin = 0, k_end = K):
+ *       T_out[q] = prod of T_l(x_q) over these lights (1 if none); an empty
+ *       chunk (k_begin == k_end) with split[l] == 0 is skipped;
+ *   split[l] != 0: partial_out[j][q] = the chunk's share of T_l(x_q), j = the
+ *       rank of l among the split lights; summing partial_out over the ranks
+ *       holding the light's other shells (all-reduce SUM) gives T_l(x_q).
+ * dgsm_query_combine then folds the summed split lights in:
+ *   T_inout[q] *= prod_j partial[j][q].
+ *   chunks, k_begin, k_end, split: HOST arrays [n_lights]; chunks[l] is a DEVICE
+ *       pointer to float [k_end - k_begin][res][res] (unused, may be NULL, when
+ *       k_begin == k_end); 0 <= k_begin <= k_end <= n_shells.
+ *   T_out: DEVICE float [m] (may be NULL when every light is split);
+ *   partial_out: DEVICE float [n_split][m] (may be NULL when none is split).
+ * Errors: DGSM_EINVAL (bad ranges, null pointers, a complete light whose
+ * chunk is not [0, K)). */
+int dgsm_query_chunks(const float* const* chunks, const int32_t* k_begin, const int32_t* k_end,
+                      const int32_t* split, const dgsm_light_t* lights, int n_lights, int atlas_res, int n_shells,
+                      const float* positions, int64_t m, float* T_out, float* partial_out, void* stream);
+int dgsm_query_combine(const float* partial, int n_split, int64_t m, float* T_inout, void* stream);
+
 /* One frame end to end from HOST memory (the benchmark's e2e path): upload the
  * occluder Gaussians (g_host: HOST arrays, pinned for copy/compute overlap) in
  * chunks, each projected as soon as it lands; build the atlas (plan + run, as

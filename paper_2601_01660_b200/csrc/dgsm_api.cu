@@ -681,6 +681,43 @@ int dgsm_query_ordered(const float* atlas, const dgsm_light_t* lights, int n_lig
     return cuda_check("query ordered");
 }
 
+int dgsm_query_chunks(const float* const* chunks, const int32_t* k_begin, const int32_t* k_end,
+                      const int32_t* split, const dgsm_light_t* lights, int n_lights, int atlas_res, int n_shells,
+                      const float* positions, int64_t m, float* T_out, float* partial_out, void* stream) {
+    g_launches = 0;
+    if (!chunks || !k_begin || !k_end || !split) return fail(DGSM_EINVAL, "null chunk arrays");
+    if (int rc = check_query_args(nullptr, lights, n_lights, atlas_res, n_shells, 0)) return rc;
+    if (m < 0) return fail(DGSM_EINVAL, "m < 0");
+    int n_split = 0, n_full = 0;
+    for (int l = 0; l < n_lights; ++l) {
+        if (k_begin[l] < 0 || k_begin[l] > k_end[l] || k_end[l] > n_shells)
+            return fail(DGSM_EINVAL, "light %d: bad shell chunk [%d, %d)", l, k_begin[l], k_end[l]);
+        if (k_end[l] > k_begin[l] && !chunks[l]) return fail(DGSM_EINVAL, "light %d: null chunk", l);
+        if (split[l]) ++n_split;
+        else if (k_end[l] == k_begin[l]) continue;  // not held here: skipped
+        else if (k_begin[l] != 0 || k_end[l] != n_shells)
+            return fail(DGSM_EINVAL, "light %d: a complete light needs the chunk [0, %d)", l, n_shells);
+        else ++n_full;
+    }
+    if (m > 0 && !positions) return fail(DGSM_EINVAL, "null positions");
+    if (m > 0 && n_split > 0 && !partial_out) return fail(DGSM_EINVAL, "null partial_out");
+    if (m > 0 && !T_out && n_full > 0) return fail(DGSM_EINVAL, "null T_out");
+    const LightsParam lp = lights_param(lights, n_lights);
+    launch_query_chunks(chunks, k_begin, k_end, split, lp, n_lights, atlas_res, n_shells, positions, m, T_out,
+                        partial_out, (cudaStream_t)stream);
+    g_launches = m > 0 ? 1 : 0;
+    return cuda_check("query chunks");
+}
+
+int dgsm_query_combine(const float* partial, int n_split, int64_t m, float* T_inout, void* stream) {
+    g_launches = 0;
+    if (n_split < 0 || m < 0) return fail(DGSM_EINVAL, "n_split < 0 or m < 0");
+    if (m > 0 && (!T_inout || (n_split > 0 && !partial))) return fail(DGSM_EINVAL, "null partial or T");
+    launch_query_combine(partial, n_split, m, T_inout, (cudaStream_t)stream);
+    g_launches = m > 0 ? 1 : 0;
+    return cuda_check("query combine");
+}
+
 int dgsm_query_footprint(const float* atlas, const dgsm_light_t* lights, int n_lights, int atlas_res,
                          int n_shells, const float* means, const float* scales, const float* rotations, int64_t m,
                          const float* offsets, const float* weights, int n_samples, float* T_out,

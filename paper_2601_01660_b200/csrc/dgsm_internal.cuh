@@ -280,6 +280,10 @@ void launch_query_ordered(const float* atlas, const LightsParam& lp, int n_light
 // their onesweep digit histograms into hist (from onesweep_prepare) (2 kernels)
 void launch_morton(const float* positions, int64_t m, uint32_t* box, uint32_t* keys, uint32_t* vals,
                    const PassDigits& pd, uint32_t* hist, cudaStream_t s);
+void launch_query_chunks(const float* const* chunks, const int* kb, const int* ke, const int* split,
+                         const LightsParam& lp, int n_lights, int res, int K, const float* positions, int64_t m,
+                         float* T_out, float* partial_out, cudaStream_t s);
+void launch_query_combine(const float* partial, int n, int64_t m, float* T, cudaStream_t s);
 void launch_query_footprint(const float* atlas, const LightsParam& lp, const FootprintParam& fp, int n_lights,
                             int res, int K, const float* means, const float* scales, const float* rotations,
                             int64_t m, float* T_out, float* colors, cudaStream_t s);

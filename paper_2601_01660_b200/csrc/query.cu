@@ -6,6 +6,7 @@
 // Index math in fp64 (at 2048^2 the fp32 texel coordinate has ulp 2.4e-4).
 // HBM/L2 bound: 12 B position + 8 x 4 B taps per light + 4 B output per query.
 #include <algorithm>
+#include <cstring>
 
 #include "dgsm_internal.cuh"
 
@@ -43,7 +44,11 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 // mirror-wrapped on its own (Q12).  Rare: only receivers whose bilinear cell
 // touches the border of the octahedral square.
 __device__ __noinline__ float sample_border(const float* __restrict__ A, int W, int plane, int k0, int k1, int ix,
-                                            int iy, float wx, float wy, float wk) {
+                                            int iy, float wx, float wy, float wk, int kb, int ke) {
+    // shells outside [kb, ke) are not held (a multi-GPU shell chunk): their taps count 0
+    const float w0 = (k0 >= kb && k0 < ke) ? 1.0f - wk : 0.0f, w1 = (k1 >= kb && k1 < ke) ? wk : 0.0f;
+    k0 = w0 != 0.0f ? k0 - kb : 0;
+    k1 = w1 != 0.0f ? k1 - kb : 0;
     float acc = 0.0f;
 #pragma unroll
     for (int dy = 0; dy < 2; ++dy)
@@ -53,8 +58,8 @@ __device__ __noinline__ float sample_border(const float* __restrict__ A, int W, 
             wrap_tap(c, r, W, W);
             const int o = r * W + c;
             const float wxy = (dx ? wx : 1.0f - wx) * (dy ? wy : 1.0f - wy);
-            acc = fmaf(wxy * (1.0f - wk), __ldg(A + k0 * plane + o), acc);
-            acc = fmaf(wxy * wk, __ldg(A + k1 * plane + o), acc);
+            if (w0 != 0.0f) acc = fmaf(wxy * w0, __ldg(A + k0 * plane + o), acc);
+            if (w1 != 0.0f) acc = fmaf(wxy * w1, __ldg(A + k1 * plane + o), acc);
         }
     return acc;
 }
@@ -65,8 +70,12 @@ __device__ __noinline__ float sample_border(const float* __restrict__ A, int W, 
 // MUFU seed plus one fp64 Newton step (relative error ~1e-14, not correctly
 // rounded: no integer decision here needs bit-exactness, the trilinear
 // result is continuous in them).  Taps in fp32.
+// kRange: A holds only shells [kb, ke) of the light (a multi-GPU shell chunk,
+// A = shell kb); taps on other shells count 0, so the sum over the chunks of
+// all ranks is the full trilinear value (it is linear in the atlas).
+template <bool kRange = false>
 __device__ __forceinline__ float sample_light(const float* __restrict__ A, const QLight& L, int W, int K,
-                                              double px, double py, double pz) {
+                                              double px, double py, double pz, int kb = 0, int ke = 0) {
     const double mx = px - L.ox, my = py - L.oy, mz = pz - L.oz;
     const double t2 = fma(mx, mx, fma(my, my, mz * mz));
     if (t2 == 0.0) return 1.0f;  // at the light (Q18)
@@ -96,7 +105,7 @@ __device__ __forceinline__ float sample_light(const float* __restrict__ A, const
     const int ix = (int)x0, iy = (int)y0;
     const int plane = W * W;  // K * plane < 2^31 for K <= 256, W <= 2048
     if ((unsigned)ix >= (unsigned)(W - 1) || (unsigned)iy >= (unsigned)(W - 1))
-        return sample_border(A, W, plane, k0, k1, ix, iy, wx, wy, wk);
+        return sample_border(A, W, plane, k0, k1, ix, iy, wx, wy, wk, kRange ? kb : 0, kRange ? ke : K);
     // interior: each of the 4 tap rows (2 rows x 2 shells) is one aligned 16-B
     // load holding both column taps, plus a 4-B load when the pair straddles
     // the 16-B boundary; the column weights are placed at the taps' positions
@@ -108,8 +117,28 @@ __device__ __forceinline__ float sample_light(const float* __restrict__ A, const
     const float c2 = sub == 1 ? cx1 : (sub == 2 ? cx0 : 0.0f);
     const float c3 = sub == 2 ? cx1 : (sub == 3 ? cx0 : 0.0f);
     const float c4 = sub == 3 ? cx1 : 0.0f;
-    const float* p00 = A + (k0 * plane + iy * W + (ix - sub));
-    const float* p10 = A + (k1 * plane + iy * W + (ix - sub));
+    const int cofs = iy * W + (ix - sub);
+    if (kRange) {
+        const bool own0 = k0 >= kb && k0 < ke, own1 = k1 >= kb && k1 < ke;
+        const float* p00 = A + ((own0 ? k0 - kb : 0) * plane + cofs);
+        const float* p10 = A + ((own1 ? k1 - kb : 0) * plane + cofs);
+        const float* rows[4] = {p00, p00 + W, p10, p10 + W};
+        const bool own[4] = {own0, own0, own1, own1};
+        float4 q[4];
+        float e[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            q[j] = own[j] ? __ldg(reinterpret_cast<const float4*>(rows[j])) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) e[j] = (own[j] && sub == 3) ? __ldg(rows[j] + 4) : 0.0f;
+        float s[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) s[j] = fmaf(c4, e[j], fmaf(c3, q[j].w, fmaf(c2, q[j].z, fmaf(c1, q[j].y, c0 * q[j].x))));
+        const float wy0 = 1.0f - wy, wk0 = 1.0f - wk;
+        return fmaf(wy * wk, s[3], fmaf(wy0 * wk, s[2], fmaf(wy * wk0, s[1], wy0 * wk0 * s[0])));
+    }
+    const float* p00 = A + (k0 * plane + cofs);
+    const float* p10 = A + (k1 * plane + cofs);
     const float* rows[4] = {p00, p00 + W, p10, p10 + W};
     float4 q[4];
     float e[4];
@@ -281,6 +310,46 @@ __global__ void __launch_bounds__(256) k_aabb(const float* __restrict__ pos, int
 #ifndef DGSM_ORDER_BITS
 #define DGSM_ORDER_BITS 30
 #endif
+// Sharded atlases (multi-GPU): per light, the chunk of shells
+// [kb, ke) this rank holds.  Complete lights (every shell held) multiply into
+// T_out; split lights write the partial trilinear sum of their held taps into
+// partial_out[j][q] (j = running index of the split lights), to be summed over
+// the ranks sharing the light (all-reduce SUM) and multiplied in by
+// k_query_combine.
+struct ChunkParam {
+    const float* data[DGSM_MAX_LIGHTS];
+    int kb[DGSM_MAX_LIGHTS], ke[DGSM_MAX_LIGHTS];
+    int split[DGSM_MAX_LIGHTS];
+};
+
+__global__ void __launch_bounds__(kQThreads) k_query_chunks(ChunkParam cp, QueryLights ql, int n_lights, int res,
+                                                            int K, const float* __restrict__ pos, int64_t m,
+                                                            float* __restrict__ T_out,
+                                                            float* __restrict__ partial_out) {
+    const int64_t q = (int64_t)blockIdx.x * kQThreads + threadIdx.x;
+    if (q >= m) return;
+    const double px = __ldg(pos + 3 * q), py = __ldg(pos + 3 * q + 1), pz = __ldg(pos + 3 * q + 2);
+    float T = 1.0f;
+    int j = 0;
+    for (int l = 0; l < n_lights; ++l) {
+        if (cp.kb[l] >= cp.ke[l] && !cp.split[l]) continue;  // (an empty complete chunk cannot occur)
+        const float v = sample_light<true>(cp.data[l], ql.l[l], res, K, px, py, pz, cp.kb[l], cp.ke[l]);
+        if (cp.split[l]) partial_out[(size_t)(j++) * m + q] = v;
+        else T *= v;
+    }
+    if (T_out) T_out[q] = T;
+}
+
+// T *= prod_j partial[j] (the product over lights, Q13, of the summed shell chunks)
+__global__ void __launch_bounds__(256) k_query_combine(const float* __restrict__ partial, int n, int64_t m,
+                                                       float* __restrict__ T) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= m) return;
+    float t = T[q];
+    for (int j = 0; j < n; ++j) t *= __ldg(partial + (size_t)j * m + q);
+    T[q] = t;
+}
+
 // 30-bit Morton code (10 bits per axis) of each receiver in its bounding box
 // (positions outside are clamped: they only sort less tightly), value = index;
 // the onesweep digit histograms of the keys are counted here (no k_hist pass).
@@ -418,6 +487,27 @@ void launch_query_ordered(const float* atlas, const LightsParam& lp, int n_light
     if (m <= 0) return;
     k_query_ordered<<<query_blocks(m), kQThreads, 0, s>>>(atlas, query_lights(lp, n_lights, K), n_lights, res, K,
                                                           positions, order, m, T_out, colors);
+}
+
+void launch_query_chunks(const float* const* chunks, const int* kb, const int* ke, const int* split,
+                         const LightsParam& lp, int n_lights, int res, int K, const float* positions, int64_t m,
+                         float* T_out, float* partial_out, cudaStream_t s) {
+    if (m <= 0) return;
+    ChunkParam cp;
+    memset(&cp, 0, sizeof(cp));
+    for (int l = 0; l < n_lights; ++l) {
+        cp.data[l] = chunks[l];
+        cp.kb[l] = kb[l];
+        cp.ke[l] = ke[l];
+        cp.split[l] = split[l];
+    }
+    k_query_chunks<<<(unsigned)((m + kQThreads - 1) / kQThreads), kQThreads, 0, s>>>(
+        cp, query_lights(lp, n_lights, K), n_lights, res, K, positions, m, T_out, partial_out);
+}
+
+void launch_query_combine(const float* partial, int n, int64_t m, float* T, cudaStream_t s) {
+    if (m <= 0) return;
+    k_query_combine<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(partial, n, m, T);
 }
 
 void launch_morton(const float* positions, int64_t m, uint32_t* box, uint32_t* keys, uint32_t* vals,

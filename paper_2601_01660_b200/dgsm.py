@@ -35,7 +35,8 @@ EXPORTED = ["dgsm_default_opts", "dgsm_plan_workspace_bytes", "dgsm_build_plan",
             "dgsm_last_error", "dgsm_last_launch_count", "dgsm_build_stats", "dgsm_set_accumulate_events",
             "dgsm_slab_bytes", "dgsm_active_slab", "dgsm_frame_host", "dgsm_default_transfer_opts",
             "dgsm_transfer_workspace_bytes", "dgsm_sh_transfer", "dgsm_sort_temp_bytes", "dgsm_sort_pairs_u32",
-            "dgsm_order_workspace_bytes", "dgsm_receiver_order", "dgsm_query_ordered"]
+            "dgsm_order_workspace_bytes", "dgsm_receiver_order", "dgsm_query_ordered", "dgsm_query_chunks",
+            "dgsm_query_combine"]
 
 
 class Gaussians(C.Structure):
@@ -129,6 +130,11 @@ def lib() -> C.CDLL:
         L.dgsm_receiver_order.restype = C.c_int
         L.dgsm_query_ordered.argtypes = [vp, P(Light), C.c_int, C.c_int, C.c_int, vp, vp, i64, vp, vp, vp]
         L.dgsm_query_ordered.restype = C.c_int
+        L.dgsm_query_chunks.argtypes = [P(vp), P(C.c_int32), P(C.c_int32), P(C.c_int32), P(Light), C.c_int,
+                                        C.c_int, C.c_int, vp, i64, vp, vp, vp]
+        L.dgsm_query_chunks.restype = C.c_int
+        L.dgsm_query_combine.argtypes = [vp, C.c_int, i64, vp, vp]
+        L.dgsm_query_combine.restype = C.c_int
         L.dgsm_sort_temp_bytes.argtypes = [i64]
         L.dgsm_sort_temp_bytes.restype = sz
         L.dgsm_sort_pairs_u32.argtypes = [vp, vp, vp, vp, i64, C.c_int, vp, sz, P(C.c_int), vp]
@@ -429,6 +435,48 @@ def query(atlas: torch.Tensor, lights, positions: torch.Tensor, colors: Optional
                           C.c_void_p(out.data_ptr()), cptr, C.c_void_p(_stream_ptr(stream)))
     _check(rc, "dgsm_query")
     return out
+
+
+def query_chunks(chunks, lights, positions: torch.Tensor, res: int, K: int, stream=None):
+    """Sharded-atlas query (dgsm_query_chunks, multi-GPU): ``chunks`` lists, per
+    light of ``lights``, (k_begin, k_end, split, tensor [k_end-k_begin, res, res]
+    or None).  Returns (T [m]: product over the complete lights, partial
+    [n_split, m]: each split light's share of its trilinear sample)."""
+    arr, nl = _lights(lights)
+    if len(chunks) != nl:
+        raise DgsmError(f"{len(chunks)} chunks for {nl} lights")
+    x = _dev_f32(positions, "positions", (3,))
+    m = x.shape[0]
+    ptrs = (C.c_void_p * nl)()
+    kb, ke, sp = (C.c_int32 * nl)(), (C.c_int32 * nl)(), (C.c_int32 * nl)()
+    for l, (b, e, split, t) in enumerate(chunks):
+        if e > b:
+            if t is None or t.dtype != torch.float32 or not t.is_contiguous() or t.device != x.device or \
+                    tuple(t.shape) != (e - b, res, res):
+                raise DgsmError(f"chunk {l} must be contiguous float32 [{e - b}, {res}, {res}] on {x.device}")
+            ptrs[l] = t.data_ptr()
+        kb[l], ke[l], sp[l] = int(b), int(e), int(bool(split))
+    n_split = sum(1 for c in chunks if c[2])
+    T = torch.empty(m, dtype=torch.float32, device=x.device)
+    part = torch.empty((max(n_split, 1), m), dtype=torch.float32, device=x.device)
+    rc = lib().dgsm_query_chunks(ptrs, kb, ke, sp, arr, nl, int(res), int(K), C.c_void_p(x.data_ptr()), m,
+                                 C.c_void_p(T.data_ptr()), C.c_void_p(part.data_ptr()),
+                                 C.c_void_p(_stream_ptr(stream)))
+    _check(rc, "dgsm_query_chunks")
+    return T, part[:n_split]
+
+
+def query_combine(partial: torch.Tensor, T: torch.Tensor, stream=None) -> torch.Tensor:
+    """T *= prod_j partial[j] in place (dgsm_query_combine)."""
+    m = T.numel()
+    T = _out_f32(T, (m,), T.device, "T")
+    n = partial.shape[0] if partial.dim() == 2 else 0
+    if n:
+        partial = _out_f32(partial.contiguous(), (n, m), T.device, "partial")
+    rc = lib().dgsm_query_combine(C.c_void_p(partial.data_ptr()) if n else None, n, m, C.c_void_p(T.data_ptr()),
+                                  C.c_void_p(_stream_ptr(stream)))
+    _check(rc, "dgsm_query_combine")
+    return T
 
 
 DGSM_MAX_FOOTPRINT_SAMPLES = 64

@@ -263,6 +263,28 @@ def test_query_ordered_parity(dg, oracle_mod, L, K, res):
     assert np.median(step) < 0.2 * np.median(rand)
 
 
+def test_query_chunks_sum_to_query(dg, oracle_mod):
+    """dgsm_query_chunks + dgsm_query_combine (the multi-GPU query): light 1's
+    shells split over two 'ranks' as [0, 3) and [3, 8); lights 0 and 2 complete.
+    The summed shares times the complete lights equal dgsm_query and the oracle."""
+    L, K, res = 3, 8, 32
+    atlas = synth.random_atlas(77, L, K, res)
+    rng = np.random.default_rng(5)
+    lights = dict(position=rng.uniform(-1, 1, (L, 3)).astype(np.float32), t_max=rng.uniform(2, 5, L).astype(np.float32))
+    x = torch.from_numpy(synth.random_queries(9, lights, 30000, 6.0)).cuda()
+    at = torch.from_numpy(atlas).cuda()
+    want = dg.query(at, lights, x)
+    full = [(0, K, False, at[0].contiguous()), None, (0, K, False, at[2].contiguous())]
+    T_a, p_a = dg.query_chunks([full[0], (0, 3, True, at[1, 0:3].contiguous()), full[2]], lights, x, res, K)
+    T_b, p_b = dg.query_chunks([(0, 0, False, None), (3, K, True, at[1, 3:K].contiguous()), (0, 0, False, None)],
+                               lights, x, res, K)
+    assert p_a.shape == (1, x.shape[0]) and torch.all(T_b == 1.0)
+    T = dg.query_combine(p_a + p_b, T_a)
+    assert (T - want).abs().max().item() <= 2e-6
+    wo = oracle_mod.query(atlas.astype(np.float64), lights, x.cpu().numpy())
+    assert np.abs(T.cpu().numpy() - wo).max() <= 2e-6
+
+
 def _receivers(seed, lights, m, K):
     rng = np.random.default_rng(seed)
     return dict(means=synth.random_queries(K, lights, m, 6.0),

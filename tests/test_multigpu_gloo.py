@@ -18,22 +18,40 @@ from paper_2601_01660_b200 import synth
 
 
 def test_plan_layout_light_parallel():
-    lay = D.plan_layout(8, 4, light_cost=[8, 7, 6, 5, 4, 3, 2, 1])
-    assert lay.groups == [[0], [1], [2], [3]]
+    lay = D.plan_layout(8, 4, K=16, light_cost=[8, 7, 6, 5, 4, 3, 2, 1])
+    assert lay.groups == [[0], [1], [2], [3]] and lay.mode == "light"
     assert sorted(sum(lay.lights_of, [])) == list(range(8))
     loads = [sum(8 - l for l in ls) for ls in lay.lights_of]
     assert max(loads) - min(loads) <= 1  # LPT balances 8..1 over 4 ranks perfectly
-    lay = D.plan_layout(4, 4)
+    lay = D.plan_layout(4, 4, K=16)
     assert lay.lights_of == [[0], [1], [2], [3]]
+    assert lay.chunks_of(2) == {2: (0, 16)} and lay.split_lights(2) == []
 
 
-def test_plan_layout_gaussian_sharded():
-    lay = D.plan_layout(1, 8)
-    assert lay.groups == [list(range(8))] and lay.lights_of == [[0]]
-    lay = D.plan_layout(3, 8)
+def test_plan_layout_shells():
+    lay = D.plan_layout(1, 8, K=64)
+    assert lay.groups == [list(range(8))] and lay.lights_of == [[0]] and lay.mode == "shells"
+    assert lay.chunks_of(3) == {0: (24, 32)} and lay.split_lights(0) == [0]
+    lay = D.plan_layout(3, 8, K=6)
     assert [len(g) for g in lay.groups] == [3, 3, 2]
     assert sorted(sum(lay.groups, [])) == list(range(8))
     assert lay.shard_of(4) == (1, 3)
+    with pytest.raises(ValueError):
+        D.plan_layout(3, 8, K=8)  # 8 shells cannot be split over a 3-rank group
+
+
+def test_plan_layout_gaussian():
+    """BASELINE cfg5: 8 lights, Gaussians sharded over all 8 ranks, the
+    reduce-scatter over the [L][K] planes hands each rank one whole light."""
+    lay = D.plan_layout(8, 8, K=128, mode="gaussian")
+    assert lay.groups == [list(range(8))] and lay.lights_of == [list(range(8))]
+    for r in range(8):
+        assert lay.planes_of(r) == (128 * r, 128 * (r + 1))
+        assert {l: c for l, c in lay.chunks_of(r).items() if c != (0, 0)} == {r: (0, 128)}
+    assert lay.split_lights(0) == []
+    lay = D.plan_layout(3, 2, K=4, mode="gaussian")  # 12 planes over 2 ranks: light 1 is split
+    assert lay.planes_of(1) == (6, 12) and lay.split_lights(0) == [1]
+    assert lay.chunks_of(0) == {0: (0, 4), 1: (0, 2), 2: (0, 0)}
 
 
 def test_shard_range_partitions():
@@ -53,45 +71,83 @@ def _free_port():
     return p
 
 
-def oracle_build_fn(g_t, lights, res, K, output_tau=False):
+def oracle_build_fn(g_t, lights, output_tau):
     from oracle import oracle
     g = {k: v.numpy() for k, v in g_t.items()}
-    T, _ = oracle.build(g, lights, res, K, n_threads=2)
+    T, _ = oracle.build(g, lights, RES[0], RES[1], n_threads=2)
     out = -np.log(T) if output_tau else T
     return torch.from_numpy(out.astype(np.float32))
 
 
-def oracle_query_fn(atlas, lights, positions):
+def oracle_exp_fn(t):
+    t.copy_(torch.exp(-t))
+    return t
+
+
+def oracle_chunks_fn(chunk_list, lights, positions):
+    """dgsm_query_chunks on the CPU: the oracle query of a full atlas whose
+    shells outside the held chunk are 0 (the trilinear sample is linear)."""
     from oracle import oracle
-    return torch.from_numpy(oracle.query(atlas.numpy().astype(np.float64), lights, positions.numpy()).astype(np.float32))
+    res, K = RES
+    x = positions.numpy()
+    T = np.ones(x.shape[0])
+    parts = []
+    pos = np.asarray(lights["position"], np.float32).reshape(-1, 3)
+    tm = np.asarray(lights["t_max"], np.float32).reshape(-1)
+    for i, (kb, ke, split, t) in enumerate(chunk_list):
+        full = np.zeros((1, K, res, res))
+        if ke > kb:
+            full[0, kb:ke] = t.numpy()
+        v = oracle.query(full, dict(position=pos[i:i + 1], t_max=tm[i:i + 1]), x)
+        if split:
+            parts.append(v)
+        else:
+            T = T * v
+    part = np.stack(parts) if parts else np.zeros((0, x.shape[0]))
+    return torch.from_numpy(T.astype(np.float32)), torch.from_numpy(part.astype(np.float32))
 
 
-def _worker(rank, world, port, case, q):
+def oracle_combine_fn(part, T):
+    T *= torch.prod(part, dim=0)
+    return T
+
+
+RES = [16, 4]
+
+
+def _scene(case):
+    if case in ("shells", "gaussian1"):
+        s = synth.config1()
+        return synth.Scene("c", {k: v[:400] for k, v in s.gaussians.items()}, s.lights, 32, 8, s.queries[:300])
+    return synth.random_scene(3, 200, res=16, K=4, L=3, dist=(0.5, 3.0))
+
+
+def _worker(rank, world, port, case, mode, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        if case == "gaussian":
-            s = synth.config1()
-            s = synth.Scene("c", {k: v[:400] for k, v in s.gaussians.items()}, s.lights, 32, 8, s.queries[:300])
-        else:
-            s = synth.random_scene(3, 200, res=16, K=4, L=3, dist=(0.5, 3.0))
+        s = _scene(case)
+        RES[0], RES[1] = s.res, s.K
         g = {k: torch.from_numpy(v) for k, v in s.gaussians.items()}
-        lay = D.plan_layout(s.L, world)
+        lay = D.plan_layout(s.L, world, K=s.K, light_cost=[3.0, 1.0, 2.0][:s.L], mode=mode)
         pg = D.make_groups(lay)
-        atl = D.build_sharded(g, s.lights, s.res, s.K, lay, pg, oracle_build_fn, lambda t: torch.exp(-t))
-        T = D.query_sharded(atl, s.lights, torch.from_numpy(s.queries), lay, oracle_query_fn)
-        q.put((rank, {l: a.numpy() for l, a in atl.items()}, T.numpy()))
+        # the exact per-frame step bench.py runs at N > 1 (oracle functions instead of CUDA)
+        step = D.StrongStep(lay, pg, s.lights, s.res, oracle_build_fn, oracle_exp_fn, oracle_chunks_fn,
+                            oracle_combine_fn)
+        T = step(g, torch.from_numpy(s.queries))
+        held = {l: (kb, ke, t.numpy().copy()) for l, (kb, ke, t) in step.atlas.chunks().items()}
+        q.put((rank, held, T.numpy()))
         dist.barrier()
     finally:
         dist.destroy_process_group()
 
 
-def _run(world, case):
+def _run(world, case, mode="auto"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, mode, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
@@ -103,38 +159,42 @@ def _run(world, case):
 
 def _reference(case):
     from oracle import oracle
-    if case == "gaussian":
-        s = synth.config1()
-        s = synth.Scene("c", {k: v[:400] for k, v in s.gaussians.items()}, s.lights, 32, 8, s.queries[:300])
-    else:
-        s = synth.random_scene(3, 200, res=16, K=4, L=3, dist=(0.5, 3.0))
+    s = _scene(case)
     T, _ = oracle.build(s.gaussians, s.lights, s.res, s.K)
     Tf = T.astype(np.float32).astype(np.float64)
     return s, T, oracle.query(Tf, s.lights, s.queries)
 
 
+def _check(res, case, tol_atlas, tol_q):
+    s, T, Tq = _reference(case)
+    seen = {}
+    for rank, held, Tr in res:
+        for l, (kb, ke, a) in held.items():
+            assert np.abs(a - T[l, kb:ke]).max() < tol_atlas
+            for k in range(kb, ke):
+                assert (l, k) not in seen  # every shell held by exactly one rank
+                seen[(l, k)] = rank
+        assert np.abs(Tr - Tq).max() < tol_q
+    assert len(seen) == s.L * s.K
+
+
 @pytest.mark.parametrize("world", [2, 4])
-def test_gaussian_sharded_reduce_scatter(world):
+def test_gaussian_sharded_shell_reduce_scatter(world):
     """1 light on `world` ranks: partial tau per Gaussian shard, reduce-scatter
-    over K, exp on the owned shells, all-gather == unsharded oracle atlas."""
-    res = _run(world, "gaussian")
-    s, T, Tq = _reference("gaussian")
-    for rank, atl, Tr in res:
-        assert list(atl) == [0]
-        assert np.abs(atl[0] - T[0]).max() < 2e-6
-        assert np.abs(Tr - Tq).max() < 2e-6
+    over K, exp on the owned shells; the query sums the shell chunks (all-reduce
+    SUM) — equal to the unsharded oracle atlas and query."""
+    _check(_run(world, "shells"), "shells", 2e-6, 2e-6)
 
 
 def test_light_parallel_query_product():
-    """3 lights on 2 ranks (light-parallel, no build communication); the query
-    product over lights is an all-reduce(PRODUCT)."""
-    res = _run(2, "lights")
-    s, T, Tq = _reference("lights")
-    owned = {}
-    for rank, atl, Tr in res:
-        for l, a in atl.items():
-            owned[l] = a
-        assert np.abs(Tr - Tq).max() < 1e-5
-    assert sorted(owned) == [0, 1, 2]
-    for l, a in owned.items():
-        assert np.abs(a - T[l]).max() < 1e-6
+    """3 lights on 2 ranks (light-parallel by LPT on the light costs, no build
+    communication); the product over lights is an all-reduce(PRODUCT)."""
+    _check(_run(2, "lights"), "lights", 1e-6, 1e-5)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gaussian_layout_all_lights(world):
+    """BASELINE cfg5's layout: every rank builds every light on its Gaussian
+    shard; one reduce-scatter over the [L][K] planes (3 lights x 4 shells over
+    2 or 4 ranks: lights split across ranks); chunk query + SUM + PRODUCT."""
+    _check(_run(world, "lights", "gaussian"), "lights", 2e-6, 1e-5)
