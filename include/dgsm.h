@@ -20,7 +20,10 @@
  *    returns a thread-local message for the last failure on this thread.
  *    Arguments are validated before any work is enqueued.  A CUDA launch or
  *    runtime error yields DGSM_ECUDA (the stream may then hold partial work).
- *    Data errors (non-finite means, scales <= 0) are not checked: the results
+ *    Data errors (non-finite values, scales <= 0, a zero quaternion: P:L86
+ *    needs an SPD Sigma and alpha in (0,1)) are checked on the device with the
+ *    DGSM_VALIDATE build flag (dgsm_build_plan then returns DGSM_EDATA; a
+ *    sync-free build reports them in its status word); without it the results
  *    for such Gaussians are unspecified.  Opacities outside [1e-4, 1-1e-4] are
  *    clamped (Q16), not rejected.
  */
@@ -40,7 +43,8 @@ extern "C" {
                            n_lights outside [1, DGSM_MAX_LIGHTS], t_max<=0, bad opts, plan/run mismatch */
 #define DGSM_ENOSPC 2   /* workspace smaller than required (required size is returned) */
 #define DGSM_ECUDA 3    /* CUDA launch/runtime error */
-#define DGSM_ERANGE 4   /* problem too large: n >= 2^30 Gaussians, > 2^30 keys for one light, or > 2^32-1 keys in total */
+#define DGSM_ERANGE 4   /* problem too large: n >= 2^30 Gaussians or >= 2^30 keys in total */
+#define DGSM_EDATA 5    /* DGSM_VALIDATE found invalid Gaussians (see the message) */
 
 #define DGSM_MAX_LIGHTS 64
 #define DGSM_MAX_SHELLS 256
@@ -58,6 +62,8 @@ extern "C" {
                                  dgsm_build_stats); instrumented kernel variant, for roofline accounting */
 #define DGSM_NO_TILE_CULL 4u  /* ablation D: bin every non-excluded Gaussian into every
                                  tile (no light-space culling); P = L * n * (res/8)^2 keys */
+#define DGSM_VALIDATE 8u      /* check every Gaussian on the device: finite mean, finite scales > 0,
+                                 finite non-zero quaternion, finite opacity (SPD Sigma) */
 
 /* Work counted by a DGSM_COLLECT_STATS build. */
 typedef struct dgsm_build_stats {
@@ -93,7 +99,7 @@ typedef struct dgsm_build_opts {
     float k_sigma;     /* footprint k_sigma rule, default 3 (Q6); > 0 */
     float rho_scale;   /* multiplies rho = (H+W)/(2 pi) pixels per radian, default 1 (Q5); > 0 */
     int32_t bin_mode;  /* DGSM_BIN_WRAP (default) or DGSM_BIN_CLAMP */
-    uint32_t flags;    /* DGSM_OUTPUT_TAU | DGSM_COLLECT_STATS | DGSM_NO_TILE_CULL, or 0 */
+    uint32_t flags;    /* DGSM_OUTPUT_TAU | DGSM_COLLECT_STATS | DGSM_NO_TILE_CULL | DGSM_VALIDATE, or 0 */
     int32_t absorption; /* DGSM_ABS_* alpha -> beta mapping (ablation B), default TRACEAVG */
     const void* slab;   /* NULL (default): the full atlas.  Else a device slab written by
                            dgsm_active_slab for the same n_lights, atlas_res and n_shells: only
@@ -178,6 +184,37 @@ int dgsm_build_bins(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n
 int dgsm_build(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_lights,
                int atlas_res, int n_shells, const dgsm_build_opts_t* opts, void* ws,
                size_t ws_bytes, size_t* ws_required, float* atlas_out, void* stream);
+
+/* ------------------------------------------------------------------
+ * Sync-free build (no host synchronisation, capturable in a CUDA graph):
+ * plan + run with the key arrays sized for a caller-chosen capacity instead
+ * of the key count P (which dgsm_build_plan reads back).  Every launch size
+ * is a function of (n, n_lights, atlas_res, n_shells, key_capacity); the
+ * kernels read P and the per-light key segments on the device.
+ * ------------------------------------------------------------------ */
+typedef struct dgsm_build_status {
+    uint64_t n_keys;    /* P of the build */
+    uint32_t overflow;  /* 1: P > key_capacity — the atlas is NOT valid (all 1): rebuild with
+                           key_capacity >= n_keys (dgsm_async_workspace_bytes grows with it) */
+    uint32_t n_invalid; /* DGSM_VALIDATE: invalid Gaussians found (0 without the flag) */
+} dgsm_build_status_t;
+
+/* Device workspace bytes of dgsm_build_async (0 on bad input). */
+size_t dgsm_async_workspace_bytes(int64_t n, int n_lights, int atlas_res, int n_shells, int64_t key_capacity);
+
+/* As dgsm_build (Eq.2-4), enqueued on `stream`
+ * without any host synchronisation.  key_capacity: 1 .. 2^30-1 keys;
+ * ws: DEVICE, >= dgsm_async_workspace_bytes(...), 256-B aligned;
+ * status: DEVICE dgsm_build_status_t written by the build (read it after the
+ * stream has passed the build: overflow == 1 means the atlas is invalid).
+ * The chunking of the accumulation follows key_capacity (the count the host
+ * knows), so the result equals dgsm_build's up to fp32 summation order when
+ * key_capacity differs from P, and bit for bit when key_capacity == P.
+ * DGSM_COLLECT_STATS is not available here.
+ * Errors: as dgsm_build_plan, DGSM_ENOSPC (workspace), DGSM_EINVAL (null status). */
+int dgsm_build_async(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_lights, int atlas_res,
+                     int n_shells, const dgsm_build_opts_t* opts, int64_t key_capacity, void* ws,
+                     size_t ws_bytes, float* atlas_out, dgsm_build_status_t* status, void* stream);
 
 /* T = exp(-tau) elementwise (Eq.4), in place allowed (tau == T). Device pointers. */
 int dgsm_exp_epilogue(const float* tau, float* T, int64_t count, void* stream);

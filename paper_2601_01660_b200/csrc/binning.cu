@@ -27,10 +27,12 @@ __device__ __forceinline__ void unpack_rect(const uint4& r, int& c0, int& c1, in
 // they emit nothing, their position in the order is irrelevant), and the
 // onesweep digit histograms of those keys (the sort's own histogram pass is
 // skipped): grid-stride, per-CTA shared histograms, one global add per bin.
-__global__ void __launch_bounds__(256) k_depth_keys(const uint4* __restrict__ dup, int64_t n, uint32_t dmin,
+__global__ void __launch_bounds__(256) k_depth_keys(const uint4* __restrict__ dup, int64_t n,
+                                                    const uint32_t* __restrict__ dmin_dev,
                                                     uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
                                                     PassDigits pd, uint32_t* __restrict__ hist) {
     __shared__ uint32_t sh[kSortMaxPasses][kSortRadix];
+    const uint32_t dmin = *dmin_dev;  // the light's smallest depth key (the plan's reduction, on the device)
     for (int t = threadIdx.x; t < pd.passes * kSortRadix; t += blockDim.x) (&sh[0][0])[t] = 0u;
     __syncthreads();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -69,10 +71,17 @@ __global__ void __launch_bounds__(256) k_gather_counts(const uint32_t* __restric
 __global__ void __launch_bounds__(256) k_duplicate_ranked(const uint4* __restrict__ dup,
                                                           const uint32_t* __restrict__ perm,
                                                           const uint64_t* __restrict__ offs, int64_t n,
-                                                          int res, int bin_mode, uint64_t base,
+                                                          int res, int bin_mode,
+                                                          const uint64_t* __restrict__ base_dev,
+                                                          const uint64_t* __restrict__ n_keys_dev,
+                                                          uint32_t key_hi,
                                                           const uint64_t* __restrict__ tm,
                                                           uint32_t* __restrict__ keys,
                                                           uint32_t* __restrict__ vals) {
+    // keys of this light start at base = the plan's light_key_begin[l] (device);
+    // nothing is written at or past n_keys (0 when the keys overflowed the
+    // workspace capacity of a sync-free build).  key = light << tile_bits | tile.
+    const uint64_t base = *base_dev, kcap = *n_keys_dev;
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const int64_t j0 = j - lane;
@@ -112,10 +121,11 @@ __global__ void __launch_bounds__(256) k_duplicate_ranked(const uint4* __restric
         const float o_iwt = __shfl_sync(0xffffffffu, iwt, lo);
         const uint32_t o_i = __shfl_sync(0xffffffffu, i, lo);
         const uint32_t o_wt = o_rect >> 22;
-        if (q < seg_len && o_wt) {
+        if (q < seg_len && o_wt && base + seg0 + q < kcap) {
             const uint32_t k = q - ek;
             const uint32_t dy = (uint32_t)(((float)k + 0.5f) * o_iwt), dx = k - dy * o_wt;
-            keys[base + seg0 + q] = ((o_rect >> 11) & 2047u) * (uint32_t)TW + dy * (uint32_t)TW + (o_rect & 2047u) + dx;
+            keys[base + seg0 + q] =
+                key_hi | (((o_rect >> 11) & 2047u) * (uint32_t)TW + dy * (uint32_t)TW + (o_rect & 2047u) + dx);
             vals[base + seg0 + q] = o_i;
         }
     }
@@ -135,7 +145,8 @@ __global__ void __launch_bounds__(256) k_duplicate_ranked(const uint4* __restric
         const int Lr0 = __shfl_sync(0xffffffffu, r0, L), Lr1 = __shfl_sync(0xffffffffu, r1, L);
         const uint32_t Li = __shfl_sync(0xffffffffu, i, L), Lw = __shfl_sync(0xffffffffu, r.w, L);
         uint64_t o = base + __shfl_sync(0xffffffffu, my_o, L);
-        const uint64_t end = o + Lw;  // never more keys than the plan counted (a slab changed since the plan)
+        uint64_t end = o + Lw;  // never more keys than the plan counted (a slab changed since the plan)
+        if (end > kcap) end = kcap;
         TileRects TR;
         make_tile_rects(Lc0, Lc1, Lr0, Lr1, res, Lc0 >= 0 && Lc1 <= res - 1 && Lr0 >= 0 && Lr1 <= res - 1
                                                      ? DGSM_BIN_CLAMP : bin_mode, TR);
@@ -152,7 +163,7 @@ __global__ void __launch_bounds__(256) k_duplicate_ranked(const uint4* __restric
                 const uint32_t bal = __ballot_sync(0xffffffffu, ok);
                 const uint64_t at = o + __popc(bal & lt);
                 if (ok && at < end) {
-                    keys[at] = (uint32_t)(ty * TW + tx);
+                    keys[at] = key_hi | (uint32_t)(ty * TW + tx);
                     vals[at] = Li;
                 }
                 o += __popc(bal);
@@ -161,26 +172,47 @@ __global__ void __launch_bounds__(256) k_duplicate_ranked(const uint4* __restric
     }
 }
 
-// Tile ranges over one light's sorted segment [begin, end): absolute positions.
-__global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ keys, int64_t begin,
-                                                int64_t end, uint32_t tile_base,
-                                                uint32_t* __restrict__ tile_start,
+// Tile ranges over the sorted keys of all lights: [start, end) of each (light,
+// tile) = l * n_tiles + tile, absolute positions; key = l << tile_bits | tile.
+// The key count is read on the device (the grid covers the capacity).
+__global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ keys,
+                                                const uint64_t* __restrict__ n_dev, int tile_bits,
+                                                uint32_t n_tiles, uint32_t* __restrict__ tile_start,
                                                 uint32_t* __restrict__ tile_end) {
+    const int64_t end = (int64_t)*n_dev;
     // four consecutive keys per thread (loads issued together), neighbours through L1
-    const int64_t j0 = begin + 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+    const int64_t j0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
     if (j0 >= end) return;
     uint32_t k[6];
 #pragma unroll
     for (int u = 0; u < 6; ++u) {
         const int64_t j = j0 - 1 + u;
-        k[u] = (j >= begin && j < end) ? keys[j] : 0xffffffffu;
+        k[u] = (j >= 0 && j < end) ? keys[j] : 0xffffffffu;
     }
+    const uint32_t tmask = (1u << tile_bits) - 1u;
 #pragma unroll
     for (int u = 1; u <= 4; ++u) {
         const int64_t j = j0 - 1 + u;
         if (j >= end) break;
-        if (k[u - 1] != k[u]) tile_start[tile_base + k[u]] = (uint32_t)j;
-        if (k[u + 1] != k[u]) tile_end[tile_base + k[u]] = (uint32_t)(j + 1);
+        const uint32_t gt = (k[u] >> tile_bits) * n_tiles + (k[u] & tmask);
+        if (k[u - 1] != k[u]) tile_start[gt] = (uint32_t)j;
+        if (k[u + 1] != k[u]) tile_end[gt] = (uint32_t)(j + 1);
+    }
+}
+
+// Sync-free run setup (one thread): the plan's key count P (on the device)
+// against the workspace capacity; n_keys = P, or 0 with the overflow flag set
+// when P exceeds it (the atlas is then all 1 and must be rebuilt with a larger
+// workspace); the caller's status word receives both.
+__global__ void k_run_setup(const PlanStats* __restrict__ ps, int n_lights, uint64_t capacity,
+                            uint64_t* __restrict__ n_keys, dgsm_build_status_t* status) {
+    const uint64_t P = ps->light_key_begin[n_lights];
+    const bool over = P > capacity;
+    *n_keys = over ? 0ull : P;
+    if (status) {
+        status->n_keys = P;
+        status->overflow = over ? 1u : 0u;
+        status->n_invalid = ps->n_invalid;
     }
 }
 
@@ -268,24 +300,18 @@ __global__ void __launch_bounds__(256) k_units_lpt(const WorkUnit* __restrict__ 
     }
 }
 
-struct DecodeParams {
-    int64_t begin[DGSM_MAX_LIGHTS + 1];
-    int n_lights;
-};
-
-// sorted (tile key, Gaussian index) -> (light, tile, fp32 bits of D, index)
+// sorted (light|tile key, Gaussian index) -> (light, tile, fp32 bits of D, index)
 __global__ void __launch_bounds__(256) k_decode(const uint32_t* __restrict__ keys,
                                                 const uint32_t* __restrict__ vals,
                                                 const uint4* __restrict__ dup, int64_t n, int64_t P,
-                                                DecodeParams dp, uint32_t* lo, uint32_t* to, uint32_t* dout,
+                                                int tile_bits, uint32_t* lo, uint32_t* to, uint32_t* dout,
                                                 uint32_t* io) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= P) return;
-    int l = 0;
-    while (l + 1 < dp.n_lights && j >= dp.begin[l + 1]) ++l;
+    const uint32_t l = keys[j] >> tile_bits;
     const uint32_t i = vals[j];
-    lo[j] = (uint32_t)l;
-    to[j] = keys[j];
+    lo[j] = l;
+    to[j] = keys[j] & ((1u << tile_bits) - 1u);
     dout[j] = dup[(int64_t)l * n + i].x;
     io[j] = i;
 }
@@ -350,11 +376,16 @@ __global__ void __launch_bounds__(kFusedThreads) k_units_fused(const uint32_t* _
 }
 }  // namespace
 
-void launch_depth_keys(const uint4* dup, int64_t n, uint32_t dmin, uint32_t* keys, uint32_t* vals,
+void launch_depth_keys(const uint4* dup, int64_t n, const uint32_t* dmin_dev, uint32_t* keys, uint32_t* vals,
                        const PassDigits& pd, uint32_t* hist, cudaStream_t s) {
     if (n <= 0) return;
     const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 4);
-    k_depth_keys<<<(unsigned)blocks, 256, 0, s>>>(dup, n, dmin, keys, vals, pd, hist);
+    k_depth_keys<<<(unsigned)blocks, 256, 0, s>>>(dup, n, dmin_dev, keys, vals, pd, hist);
+}
+
+void launch_run_setup(const PlanStats* ps, int n_lights, uint64_t capacity, uint64_t* n_keys,
+                      dgsm_build_status_t* status, cudaStream_t s) {
+    k_run_setup<<<1, 1, 0, s>>>(ps, n_lights, capacity, n_keys, status);
 }
 
 void launch_gather_counts(const uint32_t* counts, const uint32_t* perm, int64_t n, uint32_t* cperm,
@@ -364,29 +395,27 @@ void launch_gather_counts(const uint32_t* counts, const uint32_t* perm, int64_t 
 }
 
 void launch_duplicate_ranked(const uint4* dup, const uint32_t* perm, const uint64_t* offs, int64_t n, int res,
-                             int bin_mode, uint64_t base, const uint64_t* tile_mask, uint32_t* keys,
-                             uint32_t* vals, cudaStream_t s) {
+                             int bin_mode, const uint64_t* base_dev, const uint64_t* n_keys_dev, uint32_t key_hi,
+                             const uint64_t* tile_mask, uint32_t* keys, uint32_t* vals, cudaStream_t s) {
     if (n <= 0) return;
-    k_duplicate_ranked<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dup, perm, offs, n, res, bin_mode, base,
-                                                                    tile_mask, keys, vals);
+    k_duplicate_ranked<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dup, perm, offs, n, res, bin_mode, base_dev,
+                                                                    n_keys_dev, key_hi, tile_mask, keys, vals);
 }
 
 void launch_decode_keys(const uint32_t* keys, const uint32_t* vals, const uint4* dup, const dgsm_plan_t& plan,
                         uint32_t* light_out, uint32_t* tile_out, uint32_t* depth_out, uint32_t* index_out,
                         cudaStream_t s) {
     if (plan.n_keys <= 0) return;
-    DecodeParams dp;
-    dp.n_lights = plan.n_lights;
-    for (int l = 0; l <= DGSM_MAX_LIGHTS; ++l) dp.begin[l] = l <= plan.n_lights ? plan.light_key_begin[l] : 0;
-    k_decode<<<(unsigned)((plan.n_keys + 255) / 256), 256, 0, s>>>(keys, vals, dup, plan.n, plan.n_keys, dp,
-                                                                  light_out, tile_out, depth_out, index_out);
+    k_decode<<<(unsigned)((plan.n_keys + 255) / 256), 256, 0, s>>>(keys, vals, dup, plan.n, plan.n_keys,
+                                                                  plan.tile_bits, light_out, tile_out, depth_out,
+                                                                  index_out);
 }
 
-void launch_ranges(const uint32_t* keys, int64_t begin, int64_t end, uint32_t tile_base, uint32_t* tile_start,
-                   uint32_t* tile_end, cudaStream_t s) {
-    if (end <= begin) return;
-    k_ranges<<<(unsigned)((end - begin + 1023) / 1024), 256, 0, s>>>(keys, begin, end, tile_base, tile_start,
-                                                                    tile_end);
+void launch_ranges(const uint32_t* keys, const uint64_t* n_dev, int64_t capacity, int tile_bits, uint32_t n_tiles,
+                   uint32_t* tile_start, uint32_t* tile_end, cudaStream_t s) {
+    if (capacity <= 0) return;
+    k_ranges<<<(unsigned)((capacity + 1023) / 1024), 256, 0, s>>>(keys, n_dev, tile_bits, n_tiles, tile_start,
+                                                                 tile_end);
 }
 
 void launch_units(const uint32_t* tile_start, const uint32_t* tile_end, int64_t n_tiles_total, int chunk,

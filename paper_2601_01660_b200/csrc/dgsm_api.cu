@@ -72,9 +72,41 @@ PlanLayout plan_layout(void* ws, int64_t n, int L) {
     return p;
 }
 
+// What the run's launch sizes and workspace depend on: host-known quantities
+// only (the key count P enters as a capacity: P itself for dgsm_build_run,
+// the caller's bound for dgsm_build_async).
+struct RunShape {
+    int64_t n;
+    int n_lights, res, K, chunk, tile_bits, light_bits;
+    int64_t cap;  // key capacity (>= P for a valid build)
+    int depth_bits[DGSM_MAX_LIGHTS];  // significant bits of (D bits - the light's minimum); 32 when unknown
+};
+
+// keys per accumulation work unit: kChunk, halved (down to kMinChunk) while the
+// build would have fewer than kMinUnits full chunks, so that a small key set (an
+// avatar's occluders) still spreads over the ~1600 resident CTAs
+int chunk_for(int64_t P) {
+    int c = kChunk;
+    while (c > kMinChunk && P / c < kMinUnits) c /= 2;
+    return c;
+}
+
+int bits_for(uint64_t v);
+
+RunShape make_shape(int64_t n, int L, int res, int K, int64_t cap) {
+    RunShape sh;
+    sh.n = n; sh.n_lights = L; sh.res = res; sh.K = K; sh.cap = cap;
+    sh.chunk = chunk_for(cap);
+    const int64_t n_tiles = (int64_t)(res / kTile) * (res / kTile);
+    sh.tile_bits = bits_for((uint64_t)(n_tiles - 1));
+    sh.light_bits = bits_for((uint64_t)(L - 1));
+    for (int l = 0; l < DGSM_MAX_LIGHTS; ++l) sh.depth_bits[l] = 32;
+    return sh;
+}
+
 struct RunLayout {
-    uint32_t *keys_a, *keys_b;   // tile keys (P), ping-pong
-    uint32_t *vals_a, *vals_b;   // Gaussian indices (P)
+    uint32_t *keys_a, *keys_b;   // (light | tile) keys (capacity), ping-pong
+    uint32_t *vals_a, *vals_b;   // Gaussian indices (capacity)
     uint32_t *gkeys_a, *gkeys_b; // per-light depth keys of the N Gaussians, ping-pong
     uint32_t *gvals_a, *gvals_b; // Gaussian indices -> depth-rank permutation
     uint32_t* cperm;             // tile counts in depth-rank order (N)
@@ -89,21 +121,19 @@ struct RunLayout {
     uint32_t* counters;  // [0] n_units, [1] unit counter, then the unit class histogram and class fill (kUnitClasses each)
     int64_t zero_words;  // counters .. tile_end, cleared by one memset per run
     uint32_t* tile_arrive;
+    uint64_t* n_keys;    // device: the run's key count (P, or 0 on overflow)
     unsigned long long* stats;  // [4] pairs, live pairs, window shells, steps (DGSM_COLLECT_STATS)
     float* scratch;
     size_t bytes;
     uint32_t max_units;
 };
 
-RunLayout run_layout(void* ws, const dgsm_plan_t& pl) {
+RunLayout run_layout(void* ws, const RunShape& sh) {
     Carver c(ws);
     RunLayout r;
-    const int64_t P = pl.n_keys;
-    int64_t pmax = 0;
-    for (int l = 0; l < pl.n_lights; ++l)
-        pmax = std::max<int64_t>(pmax, pl.light_key_begin[l + 1] - pl.light_key_begin[l]);
-    const int64_t nt = (int64_t)pl.n_lights * (pl.atlas_res / kTile) * (pl.atlas_res / kTile);
-    const int64_t n = pl.n;
+    const int64_t P = sh.cap;
+    const int64_t nt = (int64_t)sh.n_lights * (sh.res / kTile) * (sh.res / kTile);
+    const int64_t n = sh.n;
     r.keys_a = c.take<uint32_t>(P);
     r.keys_b = c.take<uint32_t>(P);
     r.vals_a = c.take<uint32_t>(P);
@@ -115,12 +145,12 @@ RunLayout run_layout(void* ws, const dgsm_plan_t& pl) {
     r.cperm = c.take<uint32_t>(n);
     r.offs_perm = c.take<uint64_t>(n + 1);
     r.gscan_temp = c.take<char>(scan_u32_to_u64_temp_bytes(n));
-    r.sort_temp = c.take<char>(onesweep_temp_bytes(std::max<int64_t>(pmax, n)));
+    r.sort_temp = c.take<char>(onesweep_temp_bytes(std::max<int64_t>(P, n)));
 
     r.unit_cnt = c.take<uint64_t>(nt);
     r.unit_off = c.take<uint64_t>(nt + 1);
     r.unit_scan_temp = c.take<char>(scan_u32_to_u64_temp_bytes(nt));
-    const int64_t max_units = kTileSplit * (nt + P / pl.chunk + 1);
+    const int64_t max_units = kTileSplit * (nt + P / sh.chunk + 1);
     r.max_units = (uint32_t)max_units;
     r.units = c.take<WorkUnit>(max_units);
     r.units_tmp = c.take<WorkUnit>(max_units);
@@ -131,11 +161,20 @@ RunLayout run_layout(void* ws, const dgsm_plan_t& pl) {
     r.tile_start = r.tile_arrive + kTileSplit * nt;
     r.tile_end = r.tile_start + nt;
     r.zero_words = kCounterWords + (kTileSplit + 2) * nt;
+    r.n_keys = c.take<uint64_t>(2);
     r.stats = c.take<unsigned long long>(8);
-    const int64_t max_slots = kTileSplit * (2 * (P / pl.chunk) + 1);
-    r.scratch = c.take<float>((size_t)max_slots * pl.n_shells * (kTexels / kTileSplit));
+    const int64_t max_slots = kTileSplit * (2 * (P / sh.chunk) + 1);
+    r.scratch = c.take<float>((size_t)max_slots * sh.K * (kTexels / kTileSplit));
     r.bytes = c.off;
     return r;
+}
+
+RunShape plan_shape(const dgsm_plan_t& pl) {
+    RunShape sh = make_shape(pl.n, pl.n_lights, pl.atlas_res, pl.n_shells, pl.n_keys);
+    sh.chunk = pl.chunk;
+    // the plan read the depth range back: sort only its significant bits (fewer digits per pass)
+    for (int l = 0; l < pl.n_lights; ++l) sh.depth_bits[l] = pl.depth_bits[l];
+    return sh;
 }
 
 int bits_for(uint64_t v) {  // bits needed to represent 0..v
@@ -176,7 +215,7 @@ int validate(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int L, int r
     if (!(o.kappa > 0.0f) || !(o.k_sigma > 0.0f) || !(o.rho_scale > 0.0f))
         return fail(DGSM_EINVAL, "kappa, k_sigma, rho_scale must be > 0");
     if (o.bin_mode != DGSM_BIN_WRAP && o.bin_mode != DGSM_BIN_CLAMP) return fail(DGSM_EINVAL, "bad bin_mode");
-    if (o.flags & ~(DGSM_OUTPUT_TAU | DGSM_COLLECT_STATS | DGSM_NO_TILE_CULL))
+    if (o.flags & ~(DGSM_OUTPUT_TAU | DGSM_COLLECT_STATS | DGSM_NO_TILE_CULL | DGSM_VALIDATE))
         return fail(DGSM_EINVAL, "unknown flags");
     if (o.absorption < DGSM_ABS_TRACEAVG || o.absorption > DGSM_ABS_DIAG) return fail(DGSM_EINVAL, "bad absorption");
     if ((uintptr_t)o.slab % 8) return fail(DGSM_EINVAL, "slab not 8-B aligned");
@@ -279,36 +318,13 @@ static CopyStream& copy_stream() {
     return cs;
 }
 
-// The plan; with g_host != NULL the Gaussian arrays are first uploaded from
-// host memory into the device arrays of g in n_chunks pieces, each projected
-// as soon as it has landed (copy engine and SMs overlap).
-static int plan_impl(const dgsm_gaussians_t* g, const dgsm_gaussians_t* g_host, int n_chunks,
-                     cudaEvent_t upload_after, const dgsm_light_t* lights, int n_lights, int atlas_res,
-                     int n_shells, const dgsm_build_opts_t* opts, void* plan_ws, size_t plan_ws_bytes,
-                     dgsm_plan_t* plan, void* stream);
-
-int dgsm_build_plan(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_lights, int atlas_res,
-                    int n_shells, const dgsm_build_opts_t* opts, void* plan_ws, size_t plan_ws_bytes,
-                    dgsm_plan_t* plan, void* stream) {
-    return plan_impl(g, nullptr, 1, nullptr, lights, n_lights, atlas_res, n_shells, opts, plan_ws, plan_ws_bytes,
-                     plan, stream);
-}
-
-static int plan_impl(const dgsm_gaussians_t* g, const dgsm_gaussians_t* g_host, int n_chunks,
-                     cudaEvent_t upload_after, const dgsm_light_t* lights, int n_lights, int atlas_res,
-                     int n_shells, const dgsm_build_opts_t* opts, void* plan_ws, size_t plan_ws_bytes,
-                     dgsm_plan_t* plan, void* stream) {
-    g_launches = 0;
-    dgsm_build_opts_t o;
-    if (opts) o = *opts; else dgsm_default_opts(&o);
-    int rc = validate(g, lights, n_lights, atlas_res, n_shells, o);
-    if (rc) return rc;
-    if (!plan || !plan_ws) return fail(DGSM_EINVAL, "null plan or plan workspace");
-    if ((uintptr_t)plan_ws % kAlign) return fail(DGSM_EINVAL, "plan workspace not 256-B aligned");
-    const size_t need = plan_layout(nullptr, g->n, n_lights).bytes;
-    if (plan_ws_bytes < need) return fail(DGSM_ENOSPC, "plan workspace %zu < %zu bytes", plan_ws_bytes, need);
-    cudaStream_t s = (cudaStream_t)stream;
-    PlanLayout p = plan_layout(plan_ws, g->n, n_lights);
+// The plan's kernels (a1, a2 and the key-count scan) on stream s, no
+// synchronisation; with g_host != NULL the Gaussian arrays are first uploaded
+// from host memory into the device arrays of g in n_chunks pieces, each
+// projected as soon as it has landed (copy engine and SMs overlap).
+static void enqueue_plan(const dgsm_gaussians_t* g, const dgsm_gaussians_t* g_host, int n_chunks,
+                         cudaEvent_t upload_after, const dgsm_light_t* lights, int n_lights, int atlas_res,
+                         int n_shells, const dgsm_build_opts_t& o, const PlanLayout& p, cudaStream_t s) {
     const LightsParam lp = lights_param(lights, n_lights);
     const int64_t m = (int64_t)n_lights * g->n;
 
@@ -340,11 +356,47 @@ static int plan_impl(const dgsm_gaussians_t* g, const dgsm_gaussians_t* g_host, 
     // key offsets; the scan also writes light_key_begin[l] = offsets[l n] into the plan stats
     launch_scan_u32_to_u64_marks(p.counts, p.offsets, m, p.scan_temp, p.stats->light_key_begin, g->n, n_lights, s);
     g_launches += 1 + kScanLaunches;  // init, scan
+}
+
+// The plan; with g_host != NULL the Gaussian arrays are first uploaded from
+// host memory into the device arrays of g in n_chunks pieces, each projected
+// as soon as it has landed (copy engine and SMs overlap).
+static int plan_impl(const dgsm_gaussians_t* g, const dgsm_gaussians_t* g_host, int n_chunks,
+                     cudaEvent_t upload_after, const dgsm_light_t* lights, int n_lights, int atlas_res,
+                     int n_shells, const dgsm_build_opts_t* opts, void* plan_ws, size_t plan_ws_bytes,
+                     dgsm_plan_t* plan, void* stream);
+
+int dgsm_build_plan(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_lights, int atlas_res,
+                    int n_shells, const dgsm_build_opts_t* opts, void* plan_ws, size_t plan_ws_bytes,
+                    dgsm_plan_t* plan, void* stream) {
+    return plan_impl(g, nullptr, 1, nullptr, lights, n_lights, atlas_res, n_shells, opts, plan_ws, plan_ws_bytes,
+                     plan, stream);
+}
+
+static int plan_impl(const dgsm_gaussians_t* g, const dgsm_gaussians_t* g_host, int n_chunks,
+                     cudaEvent_t upload_after, const dgsm_light_t* lights, int n_lights, int atlas_res,
+                     int n_shells, const dgsm_build_opts_t* opts, void* plan_ws, size_t plan_ws_bytes,
+                     dgsm_plan_t* plan, void* stream) {
+    g_launches = 0;
+    dgsm_build_opts_t o;
+    if (opts) o = *opts; else dgsm_default_opts(&o);
+    int rc = validate(g, lights, n_lights, atlas_res, n_shells, o);
+    if (rc) return rc;
+    if (!plan || !plan_ws) return fail(DGSM_EINVAL, "null plan or plan workspace");
+    if ((uintptr_t)plan_ws % kAlign) return fail(DGSM_EINVAL, "plan workspace not 256-B aligned");
+    const size_t need = plan_layout(nullptr, g->n, n_lights).bytes;
+    if (plan_ws_bytes < need) return fail(DGSM_ENOSPC, "plan workspace %zu < %zu bytes", plan_ws_bytes, need);
+    cudaStream_t s = (cudaStream_t)stream;
+    PlanLayout p = plan_layout(plan_ws, g->n, n_lights);
+    enqueue_plan(g, g_host, n_chunks, upload_after, lights, n_lights, atlas_res, n_shells, o, p, s);
     if ((rc = cuda_check("plan launch"))) return rc;
     PlanStats hs;
     cudaMemcpyAsync(&hs, p.stats, sizeof(PlanStats), cudaMemcpyDeviceToHost, s);
     if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_check("plan sync");
 
+    if (hs.n_invalid)
+        return fail(DGSM_EDATA, "%u invalid Gaussians (non-finite mean / scale / rotation / opacity, scale <= 0 "
+                                "or zero quaternion), the first at index %u", hs.n_invalid, hs.first_invalid);
     memset(plan, 0, sizeof(*plan));
     plan->n = g->n;
     plan->n_lights = n_lights;
@@ -354,20 +406,19 @@ static int plan_impl(const dgsm_gaussians_t* g, const dgsm_gaussians_t* g_host, 
     // keys per accumulation work unit: kChunk, halved (down to kMinChunk) while
     // the build would have fewer than kMinUnits full chunks, so that a small key
     // set (an avatar's occluders) still spreads over the ~1600 resident CTAs
-    plan->chunk = kChunk;
-    while (plan->chunk > kMinChunk && plan->n_keys / plan->chunk < kMinUnits) plan->chunk /= 2;
+    plan->chunk = chunk_for(plan->n_keys);
     const int64_t n_tiles = (int64_t)(atlas_res / kTile) * (atlas_res / kTile);
     plan->tile_bits = bits_for((uint64_t)(n_tiles - 1));
     for (int l = 0; l <= n_lights; ++l) plan->light_key_begin[l] = (int64_t)hs.light_key_begin[l];
     for (int l = 0; l < n_lights; ++l) {
         const int64_t pl = plan->light_key_begin[l + 1] - plan->light_key_begin[l];
-        if (pl >= ((int64_t)1 << 30)) return fail(DGSM_ERANGE, "light %d has %lld keys (>= 2^30)", l, (long long)pl);
         plan->depth_min[l] = pl ? hs.depth_min[l] : 0u;
         plan->depth_max[l] = pl ? hs.depth_max[l] : 0u;
         plan->depth_bits[l] = pl ? bits_for((uint64_t)(hs.depth_max[l] - hs.depth_min[l])) : 0;
     }
-    if (plan->n_keys >= ((int64_t)1 << 32) - 1) return fail(DGSM_ERANGE, "%lld keys (>= 2^32)", (long long)plan->n_keys);
-    plan->run_workspace_bytes = run_layout(nullptr, *plan).bytes;
+    // one onesweep sorts all lights' keys: its look-back status words hold 30-bit counts
+    if (plan->n_keys >= ((int64_t)1 << 30)) return fail(DGSM_ERANGE, "%lld keys (>= 2^30)", (long long)plan->n_keys);
+    plan->run_workspace_bytes = run_layout(nullptr, plan_shape(*plan)).bytes;
     plan->signature = signature(g, n_lights, atlas_res, n_shells, o, lights);
     return DGSM_OK;
 }
@@ -388,51 +439,79 @@ static int check_run_args(const dgsm_gaussians_t* g, const dgsm_light_t* lights,
     return DGSM_OK;
 }
 
-// a3-a5 per light: depth sort of the N Gaussians (low LSD digits), key
-// duplication in depth-rank order, stable onesweep on the tile digits, tile
-// ranges.  Sorted (tile, index) result in keys_a/vals_a.
-static void run_binning(const dgsm_gaussians_t* g, int n_lights, const dgsm_build_opts_t& o,
-                        const dgsm_plan_t* plan, const PlanLayout& p, const RunLayout& r, cudaStream_t s) {
-    const int res = plan->atlas_res;
+// a3-a5: per light, the depth sort of its N Gaussians (low LSD digits: fp32 bits
+// of D) and the key duplication in depth-rank order into the light's key
+// segment; then ONE stable onesweep of all lights' (light | tile) keys and the
+// tile ranges.  Every count that depends on the build (P, the per-light key
+// segments, the depth minimum) is read on the device: no host synchronisation.
+// Returns the sorted (key, Gaussian index) arrays.
+struct Sorted {
+    const uint32_t *keys, *vals;
+};
+
+static Sorted run_binning(const dgsm_gaussians_t* g, const dgsm_build_opts_t& o, const RunShape& sh,
+                          const PlanLayout& p, const RunLayout& r, dgsm_build_status_t* status, cudaStream_t s) {
+    const int res = sh.res;
     const int64_t n = g->n;
     const int64_t n_tiles = (int64_t)(res / kTile) * (res / kTile);
     // (tile ranges zeroed by the caller's run memset)
-    for (int l = 0; l < n_lights; ++l) {
-        const int64_t b = plan->light_key_begin[l], e = plan->light_key_begin[l + 1];
-        if (e == b) continue;
+    launch_run_setup(p.stats, sh.n_lights, (uint64_t)sh.cap, r.n_keys, status, s);
+    g_launches += 1;
+    PassDigits pd0 = onesweep_digits(32);
+    pd0.passes = 0;
+    for (int l = 0; l < sh.n_lights; ++l) {
         const uint4* dup = p.dup + (int64_t)l * n;
-        // 1. light-distance digits on the Gaussians (the key kernel also fills the
-        //    sort's digit histograms; the sort's last pass gathers the key counts
-        //    into depth-rank order)
         const uint32_t* counts_l = p.counts + (int64_t)l * n;
-        const bool sorted = plan->depth_bits[l] > 0 && n > 1;
-        PassDigits pd = onesweep_digits(plan->depth_bits[l]);
-        uint32_t* hist = nullptr;
-        if (sorted) hist = onesweep_prepare(r.sort_temp, n, s);
-        else pd.passes = 0;
-        launch_depth_keys(dup, n, plan->depth_min[l], r.gkeys_a, r.gvals_a, pd, hist, s);
-        const int fl = launch_onesweep_u32(r.gkeys_a, r.gvals_a, r.gkeys_b, r.gvals_b, n, plan->depth_bits[l],
-                                           r.sort_temp, s, &g_launches, counts_l, r.cperm, true);
-        const uint32_t* perm = fl ? r.gvals_b : r.gvals_a;
-        // 2. emission offsets in depth-rank order
-        if (!sorted) launch_gather_counts(counts_l, perm, n, r.cperm, s);  // (no sort pass ran)
-        launch_scan_u32_to_u64(r.cperm, r.offs_perm, n, r.gscan_temp, s);
-        // 3. key duplication (key = tile, value = Gaussian index)
-        const uint64_t* tm = o.slab ? slab_mask_ptr(o.slab) + (int64_t)l * n_tiles : nullptr;
-        launch_duplicate_ranked(dup, perm, r.offs_perm, n, res, o.bin_mode, (uint64_t)b, tm, r.keys_a, r.vals_a,
-                                s);
-        g_launches += (sorted ? 2 : 3) + kScanLaunches;  // depth keys, (gather,) scan, duplication
-        // 4. stable sort of the tile digits
-        const int ft = launch_onesweep_u32(r.keys_a + b, r.vals_a + b, r.keys_b + b, r.vals_b + b, e - b,
-                                           plan->tile_bits, r.sort_temp, s, &g_launches);
-        if (ft) {
-            cudaMemcpyAsync(r.keys_a + b, r.keys_b + b, sizeof(uint32_t) * (e - b), cudaMemcpyDeviceToDevice, s);
-            cudaMemcpyAsync(r.vals_a + b, r.vals_b + b, sizeof(uint32_t) * (e - b), cudaMemcpyDeviceToDevice, s);
+        const uint32_t* perm = r.gvals_a;
+        const int db = sh.depth_bits[l];
+        if (n > 1 && db > 0) {
+            const PassDigits pd = onesweep_digits(db);
+            // 1. light-distance digits on the Gaussians (the key kernel fills the sort's
+            //    digit histograms; the sort's last pass gathers the key counts into
+            //    depth-rank order)
+            uint32_t* hist = onesweep_prepare(r.sort_temp, n, s);
+            launch_depth_keys(dup, n, p.stats->depth_min + l, r.gkeys_a, r.gvals_a, pd, hist, s);
+            const int fl = launch_onesweep_u32(r.gkeys_a, r.gvals_a, r.gkeys_b, r.gvals_b, n, db, r.sort_temp, s,
+                                               &g_launches, counts_l, r.cperm, true);
+            perm = fl ? r.gvals_b : r.gvals_a;
+            g_launches += 1;
+        } else {
+            launch_depth_keys(dup, n, p.stats->depth_min + l, r.gkeys_a, r.gvals_a, pd0, nullptr, s);
+            launch_gather_counts(counts_l, r.gvals_a, n, r.cperm, s);
+            g_launches += 2;
         }
-        // 5. tile ranges
-        launch_ranges(r.keys_a, b, e, (uint32_t)(l * n_tiles), r.tile_start, r.tile_end, s);
-        g_launches += 1;
+        // 2. emission offsets in depth-rank order
+        launch_scan_u32_to_u64(r.cperm, r.offs_perm, n, r.gscan_temp, s);
+        // 3. key duplication (key = light | tile, value = Gaussian index) into the light's segment
+        const uint64_t* tm = o.slab ? slab_mask_ptr(o.slab) + (int64_t)l * n_tiles : nullptr;
+        launch_duplicate_ranked(dup, perm, r.offs_perm, n, res, o.bin_mode, p.stats->light_key_begin + l, r.n_keys,
+                                (uint32_t)l << sh.tile_bits, tm, r.keys_a, r.vals_a, s);
+        g_launches += kScanLaunches + 1;
     }
+    // 4. one stable sort of the (light | tile) digits of all keys (grid: the capacity)
+    const int ft = launch_onesweep_u32(r.keys_a, r.vals_a, r.keys_b, r.vals_b, sh.cap, sh.light_bits + sh.tile_bits,
+                                       r.sort_temp, s, &g_launches, nullptr, nullptr, false, true, r.n_keys);
+    Sorted out{ft ? r.keys_b : r.keys_a, ft ? r.vals_b : r.vals_a};
+    // 5. tile ranges
+    launch_ranges(out.keys, r.n_keys, sh.cap, sh.tile_bits, (uint32_t)n_tiles, r.tile_start, r.tile_end, s);
+    g_launches += 1;
+    return out;
+}
+
+// a5 work units + a6 accumulation (+ Eq.4) of a run whose binning is done.
+static void run_accumulate(const dgsm_gaussians_t* g, const dgsm_light_t* lights, const dgsm_build_opts_t& o,
+                           const RunShape& sh, const PlanLayout& p, const RunLayout& r, const Sorted& so,
+                           float* atlas_out, cudaStream_t s) {
+    const LightsParam lp = lights_param(lights, sh.n_lights);
+    const int64_t nt = sh.n_lights * (int64_t)(sh.res / kTile) * (sh.res / kTile);
+    launch_units(r.tile_start, r.tile_end, nt, sh.chunk, r.unit_cnt, r.unit_off, r.unit_scan_temp, r.units_tmp,
+                 r.units, r.max_units, r.counters, r.counters + 8, r.counters + 8 + kUnitClasses, r.deferred,
+                 r.counters + 2, s, &g_launches);
+    if (o.flags & DGSM_COLLECT_STATS) cudaMemsetAsync(r.stats, 0, sizeof(unsigned long long) * 8, s);
+    launch_accumulate(r.units, r.counters, r.max_units, so.vals, p.recs, g->n, lp, sh.n_lights, sh.res, sh.K,
+                      o.flags, r.scratch, r.tile_arrive, r.counters + 1, atlas_out, r.stats, slab_mask_ptr(o.slab),
+                      slab_k_ptr(o.slab, sh.n_lights, sh.res), r.deferred, r.counters + 2, g_ev_before, g_ev_after, s);
+    g_launches += 2;  // accumulate + deferred combine
 }
 
 int dgsm_build_run(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_lights,
@@ -445,23 +524,12 @@ int dgsm_build_run(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_
     if (rc) return rc;
     if (!atlas_out) return fail(DGSM_EINVAL, "null atlas");
     cudaStream_t s = (cudaStream_t)stream;
+    const RunShape sh = plan_shape(*plan);
     const PlanLayout p = plan_layout(plan_ws, g->n, n_lights);
-    const RunLayout r = run_layout(run_ws, *plan);
-    const LightsParam lp = lights_param(lights, n_lights);
-    const int res = plan->atlas_res, K = plan->n_shells;
-    const int64_t nt = n_lights * (int64_t)(res / kTile) * (res / kTile);
-
+    const RunLayout r = run_layout(run_ws, sh);
     cudaMemsetAsync(r.counters, 0, sizeof(uint32_t) * r.zero_words, s);
-    run_binning(g, n_lights, o, plan, p, r, s);
-    launch_units(r.tile_start, r.tile_end, nt, plan->chunk, r.unit_cnt, r.unit_off, r.unit_scan_temp, r.units_tmp,
-                 r.units, r.max_units, r.counters, r.counters + 8, r.counters + 8 + kUnitClasses, r.deferred,
-                 r.counters + 2, s, &g_launches);
-    if (o.flags & DGSM_COLLECT_STATS) cudaMemsetAsync(r.stats, 0, sizeof(unsigned long long) * 8, s);
-    // a6: accumulate + exp
-    launch_accumulate(r.units, r.counters, r.max_units, r.vals_a, p.recs, g->n, lp, n_lights, res, K, o.flags,
-                      r.scratch, r.tile_arrive, r.counters + 1, atlas_out, r.stats, slab_mask_ptr(o.slab),
-                      slab_k_ptr(o.slab, n_lights, res), r.deferred, r.counters + 2, g_ev_before, g_ev_after, s);
-    g_launches += 2;  // accumulate + deferred combine
+    const Sorted so = run_binning(g, o, sh, p, r, nullptr, s);
+    run_accumulate(g, lights, o, sh, p, r, so, atlas_out, s);
     return cuda_check("build run");
 }
 
@@ -479,12 +547,13 @@ int dgsm_build_bins(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n
         return fail(DGSM_EINVAL, "null output array");
     cudaStream_t s = (cudaStream_t)stream;
     const PlanLayout p = plan_layout(plan_ws, g->n, n_lights);
-    const RunLayout r = run_layout(run_ws, *plan);
+    const RunShape sh = plan_shape(*plan);
+    const RunLayout r = run_layout(run_ws, sh);
     const int res = plan->atlas_res;
     const int64_t nt = n_lights * (int64_t)(res / kTile) * (res / kTile);
     cudaMemsetAsync(r.counters, 0, sizeof(uint32_t) * r.zero_words, s);
-    run_binning(g, n_lights, o, plan, p, r, s);
-    launch_decode_keys(r.keys_a, r.vals_a, p.dup, *plan, light_out, tile_out, depth_bits_out, index_out, s);
+    const Sorted so = run_binning(g, o, sh, p, r, nullptr, s);
+    launch_decode_keys(so.keys, so.vals, p.dup, *plan, light_out, tile_out, depth_bits_out, index_out, s);
     g_launches += 1;
     if (tile_start_out) cudaMemcpyAsync(tile_start_out, r.tile_start, sizeof(uint32_t) * nt, cudaMemcpyDeviceToDevice, s);
     if (tile_end_out) cudaMemcpyAsync(tile_end_out, r.tile_end, sizeof(uint32_t) * nt, cudaMemcpyDeviceToDevice, s);
@@ -511,6 +580,40 @@ int dgsm_build(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_ligh
                         stream);
     g_launches += plan_launches;
     return rc;
+}
+
+size_t dgsm_async_workspace_bytes(int64_t n, int n_lights, int atlas_res, int n_shells, int64_t key_capacity) {
+    if (n < 0 || n_lights < 1 || n_lights > DGSM_MAX_LIGHTS || atlas_res < 8 || atlas_res % 8 || atlas_res > 2048 ||
+        n_shells < 1 || n_shells > DGSM_MAX_SHELLS || key_capacity < 1 || key_capacity >= ((int64_t)1 << 30))
+        return 0;
+    return plan_layout(nullptr, n, n_lights).bytes + run_layout(nullptr, make_shape(n, n_lights, atlas_res, n_shells,
+                                                                                   key_capacity)).bytes;
+}
+
+int dgsm_build_async(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_lights, int atlas_res,
+                     int n_shells, const dgsm_build_opts_t* opts, int64_t key_capacity, void* ws, size_t ws_bytes,
+                     float* atlas_out, dgsm_build_status_t* status, void* stream) {
+    g_launches = 0;
+    dgsm_build_opts_t o;
+    if (opts) o = *opts; else dgsm_default_opts(&o);
+    int rc = validate(g, lights, n_lights, atlas_res, n_shells, o);
+    if (rc) return rc;
+    if (o.flags & DGSM_COLLECT_STATS) return fail(DGSM_EINVAL, "DGSM_COLLECT_STATS needs dgsm_build_plan/run");
+    if (!atlas_out || !status || !ws) return fail(DGSM_EINVAL, "null atlas, status or workspace");
+    if (key_capacity < 1 || key_capacity >= ((int64_t)1 << 30))
+        return fail(DGSM_EINVAL, "key_capacity %lld outside [1, 2^30 - 1]", (long long)key_capacity);
+    if ((uintptr_t)ws % kAlign) return fail(DGSM_EINVAL, "workspace not 256-B aligned");
+    const size_t need = dgsm_async_workspace_bytes(g->n, n_lights, atlas_res, n_shells, key_capacity);
+    if (ws_bytes < need) return fail(DGSM_ENOSPC, "workspace %zu < %zu bytes", ws_bytes, need);
+    cudaStream_t s = (cudaStream_t)stream;
+    const PlanLayout p = plan_layout(ws, g->n, n_lights);
+    const RunShape sh = make_shape(g->n, n_lights, atlas_res, n_shells, key_capacity);
+    const RunLayout r = run_layout((char*)ws + p.bytes, sh);
+    enqueue_plan(g, nullptr, 1, nullptr, lights, n_lights, atlas_res, n_shells, o, p, s);
+    cudaMemsetAsync(r.counters, 0, sizeof(uint32_t) * r.zero_words, s);
+    const Sorted so = run_binning(g, o, sh, p, r, status, s);
+    run_accumulate(g, lights, o, sh, p, r, so, atlas_out, s);
+    return cuda_check("build async");
 }
 
 int dgsm_frame_host(const dgsm_gaussians_t* g_host, const dgsm_light_t* lights, int n_lights, int atlas_res,
@@ -822,7 +925,7 @@ int dgsm_build_stats(const dgsm_plan_t* plan, void* run_ws, size_t run_ws_bytes,
                      void* stream) {
     if (!plan || !run_ws || !out) return fail(DGSM_EINVAL, "null argument");
     if (run_ws_bytes < plan->run_workspace_bytes) return fail(DGSM_ENOSPC, "run workspace too small");
-    const RunLayout r = run_layout(run_ws, *plan);
+    const RunLayout r = run_layout(run_ws, plan_shape(*plan));
     unsigned long long h[7];
     cudaMemcpyAsync(h, r.stats, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
     if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return cuda_check("stats");
@@ -843,6 +946,7 @@ const char* dgsm_strerror(int code) {
         case DGSM_ENOSPC: return "workspace too small";
         case DGSM_ECUDA: return "CUDA error";
         case DGSM_ERANGE: return "problem too large";
+        case DGSM_EDATA: return "invalid Gaussian data";
         default: return "unknown error";
     }
 }

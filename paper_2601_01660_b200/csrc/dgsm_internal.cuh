@@ -55,6 +55,7 @@ struct PlanStats {
     uint32_t depth_min[DGSM_MAX_LIGHTS];
     uint32_t depth_max[DGSM_MAX_LIGHTS];
     uint64_t light_key_begin[DGSM_MAX_LIGHTS + 1];
+    uint32_t n_invalid, first_invalid;  // DGSM_VALIDATE: invalid Gaussians, the smallest invalid index
 };
 
 // Work unit of the accumulation kernel: one chunk of one (light, tile) list.
@@ -210,9 +211,11 @@ void launch_scan_u32_to_u64_marks(const uint32_t* in, uint64_t* out, int64_t n, 
 
 void launch_gather_counts(const uint32_t* counts, const uint32_t* perm, int64_t n, uint32_t* cperm,
                           cudaStream_t s);
+// keys written from base = *base_dev (the light's first key), none at or past *n_keys_dev;
+// key = key_hi | tile (key_hi = light << tile_bits)
 void launch_duplicate_ranked(const uint4* dup, const uint32_t* perm, const uint64_t* offs, int64_t n, int res,
-                             int bin_mode, uint64_t base, const uint64_t* tile_mask, uint32_t* keys,
-                             uint32_t* vals, cudaStream_t s);
+                             int bin_mode, const uint64_t* base_dev, const uint64_t* n_keys_dev, uint32_t key_hi,
+                             const uint64_t* tile_mask, uint32_t* keys, uint32_t* vals, cudaStream_t s);
 size_t onesweep_temp_bytes(int64_t n_max);
 // returns 1 if the sorted result ended in the *_alt buffers
 int launch_onesweep(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int64_t n,
@@ -230,21 +233,27 @@ struct PassDigits {
 };
 PassDigits onesweep_digits(int nbits);
 uint32_t* onesweep_prepare(void* temp, int64_t n, cudaStream_t s);
-// depth keys of one light's Gaussians + their digit histograms into hist (pd.passes = 0: none)
-void launch_depth_keys(const uint4* dup, int64_t n, uint32_t dmin, uint32_t* keys, uint32_t* vals,
+// depth keys (fp32 bits of D - the light's minimum, read on the device) of one light's
+// Gaussians + their digit histograms into hist (pd.passes = 0: none)
+void launch_depth_keys(const uint4* dup, int64_t n, const uint32_t* dmin_dev, uint32_t* keys, uint32_t* vals,
                        const PassDigits& pd, uint32_t* hist, cudaStream_t s);
+// n_keys = P (light_key_begin[n_lights], device) or 0 + overflow when P > capacity
+void launch_run_setup(const PlanStats* ps, int n_lights, uint64_t capacity, uint64_t* n_keys,
+                      dgsm_build_status_t* status, cudaStream_t s);
 // (gsrc/gdst optional: the last pass also writes gdst[o] = gsrc[value] at each output
 // position o, i.e. a gather by the sorted permutation; only when nbits > 0 and n > 1.
 // top_match: rank the top pass with match.any (few distinct digits per warp, as in
 // tile keys); false: ballots on every pass (random top digits, e.g. Morton codes))
 int launch_onesweep_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n,
                         int nbits, void* temp, cudaStream_t s, int* launches, const uint32_t* gsrc = nullptr,
-                        uint32_t* gdst = nullptr, bool hist_ready = false, bool top_match = true);
+                        uint32_t* gdst = nullptr, bool hist_ready = false, bool top_match = true,
+                        const uint64_t* n_dev = nullptr);
 void launch_decode_keys(const uint32_t* keys, const uint32_t* vals, const uint4* dup, const dgsm_plan_t& plan,
                         uint32_t* light_out, uint32_t* tile_out, uint32_t* depth_out, uint32_t* index_out,
                         cudaStream_t s);
-void launch_ranges(const uint32_t* keys, int64_t begin, int64_t end, uint32_t tile_base, uint32_t* tile_start,
-                   uint32_t* tile_end, cudaStream_t s);
+// tile ranges of all lights' sorted keys (*n_dev keys, grid for `capacity`)
+void launch_ranges(const uint32_t* keys, const uint64_t* n_dev, int64_t capacity, int tile_bits, uint32_t n_tiles,
+                   uint32_t* tile_start, uint32_t* tile_end, cudaStream_t s);
 // Multi-chunk tiles with at most this many chunks are combined by the
 // accumulation CTA that finishes their last chunk; the others (listed by the
 // unit builder) by k_combine_deferred after it (accumulate.cu).

@@ -35,7 +35,9 @@ constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 3
 
 template <typename KeyT>
 __global__ void __launch_bounds__(256) k_hist(const KeyT* __restrict__ keys, int64_t n, int passes,
-                                              PassDigits pd, uint32_t* __restrict__ hist) {
+                                              PassDigits pd, uint32_t* __restrict__ hist,
+                                              const uint64_t* __restrict__ n_dev) {
+    if (n_dev) n = (int64_t)*n_dev;  // device-side count (<= the launch capacity)
     __shared__ uint32_t sh[kMaxPasses][kRadix];
     for (int t = threadIdx.x; t < kMaxPasses * kRadix; t += blockDim.x) (&sh[0][0])[t] = 0;
     __syncthreads();
@@ -128,7 +130,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ k
                                                       const uint32_t* __restrict__ hist,
                                                       uint32_t* status, uint32_t* status_next,
                                                       uint32_t* part_ctr, const uint32_t* __restrict__ gsrc,
-                                                      uint32_t* __restrict__ gdst) {
+                                                      uint32_t* __restrict__ gdst,
+                                                      const uint64_t* __restrict__ n_dev) {
     extern __shared__ __align__(16) unsigned char os_smem[];
     KeyT* s_keys = reinterpret_cast<KeyT*>(os_smem);
     uint32_t* s_vals = reinterpret_cast<uint32_t*>(os_smem + sizeof(KeyT) * kTileKeys);
@@ -143,6 +146,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ k
     for (int t = tid; t < (kThreads / 32) * kRadix; t += kThreads) (&s_warp_hist[0][0])[t] = 0;
     __syncthreads();
     const uint32_t part = s_part;
+    // device-side count: the grid is sized for a capacity, partitions past the
+    // keys present exit (partition ids are handed out in order: the CTAs that
+    // stay are exactly partitions 0 .. parts(n) - 1)
+    if (n_dev) {
+        n = (int64_t)*n_dev;
+        if ((int64_t)part * kTileKeys >= n) return;
+    }
     // clear this partition's row of the next pass's status buffer (double
     // buffered: no memset between passes; kernel boundaries order it)
     status_next[(size_t)part * kRadix + tid] = 0u;
@@ -265,7 +275,10 @@ OnesweepTemp carve(void* temp, int64_t parts) {
 template <typename KeyT>
 int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt, int64_t n, int nbits,
                   void* temp, cudaStream_t s, int* launches, const uint32_t* gsrc = nullptr,
-                  uint32_t* gdst = nullptr, bool hist_ready = false, bool top_match = true) {
+                  uint32_t* gdst = nullptr, bool hist_ready = false, bool top_match = true,
+                  const uint64_t* n_dev = nullptr) {
+    // n: the key count, or (n_dev != NULL) the capacity the grid is sized for while
+    // the kernels read the count from n_dev (no host synchronisation)
     if (n <= 1 || nbits <= 0) return 0;
     const int passes = (nbits + 7) / 8;
     const int64_t parts = (n + kTileKeys - 1) / kTileKeys;
@@ -285,7 +298,7 @@ int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt
         // histograms, partition counters and the first pass's status in one memset
         onesweep_prepare(temp, n, s);
         const int hist_grid = (int)std::min<int64_t>(148 * 4, (n + 2047) / 2048);
-        k_hist<KeyT><<<hist_grid, 256, 0, s>>>(keys, n, passes, pd, t.hist);
+        k_hist<KeyT><<<hist_grid, 256, 0, s>>>(keys, n, passes, pd, t.hist, n_dev);
         *launches += 1;
     }
     KeyT *ki = keys, *ko = keys_alt;
@@ -295,7 +308,8 @@ int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt
         k_pass<KeyT><<<(unsigned)parts, kThreads, dyn, s>>>(ki, vi, ko, vo, n, pd.shift[p], pd.bits[p],
                                                            top_match && p == passes - 1, t.hist + p * kRadix,
                                                            t.status[p & 1], t.status[(p + 1) & 1],
-                                                           t.part_ctr + p, gsrc, p == passes - 1 ? gdst : nullptr);
+                                                           t.part_ctr + p, gsrc, p == passes - 1 ? gdst : nullptr,
+                                                           n_dev);
         *launches += 1;
         KeyT* tk = ki; ki = ko; ko = tk;
         uint32_t* tv = vi; vi = vo; vo = tv;
@@ -317,9 +331,9 @@ int launch_onesweep(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t
 
 int launch_onesweep_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n,
                         int nbits, void* temp, cudaStream_t s, int* launches, const uint32_t* gsrc,
-                        uint32_t* gdst, bool hist_ready, bool top_match) {
+                        uint32_t* gdst, bool hist_ready, bool top_match, const uint64_t* n_dev) {
     return onesweep_impl<uint32_t>(keys, vals, keys_alt, vals_alt, n, nbits, temp, s, launches, gsrc, gdst,
-                                   hist_ready, top_match);
+                                   hist_ready, top_match, n_dev);
 }
 
 PassDigits onesweep_digits(int nbits) {

@@ -18,7 +18,7 @@ __global__ void __launch_bounds__(256, 4) k_project(  // (256, 3) and (256, 2) m
     const float* __restrict__ means, const float* __restrict__ scales,
     const float* __restrict__ rotations, const float* __restrict__ opacities, int64_t n, int64_t i0, int64_t cnt,
     LightsParam lp, int n_lights, int res, int K, double kappa, double k_sigma, double rho,
-    int bin_mode, int absorption, bool no_cull, const uint64_t* __restrict__ slab_mask,
+    int bin_mode, int absorption, bool no_cull, bool validate, const uint64_t* __restrict__ slab_mask,
     PairRec* __restrict__ recs, uint32_t* __restrict__ counts,
     uint4* __restrict__ dup,
     PlanStats* stats) {
@@ -39,6 +39,16 @@ __global__ void __launch_bounds__(256, 4) k_project(  // (256, 3) and (256, 2) m
     const float sc0 = scales[3 * i], sc1 = scales[3 * i + 1], sc2 = scales[3 * i + 2];
     const float alpha_in = opacities[i];
     const float kappa_f = (float)kappa;
+    if (validate && active && l == 0) {  // DGSM_VALIDATE: once per Gaussian (light 0's thread)
+        const bool ok = isfinite(m0) && isfinite(m1) && isfinite(m2) && isfinite(sc0) && isfinite(sc1) &&
+                        isfinite(sc2) && sc0 > 0.0f && sc1 > 0.0f && sc2 > 0.0f && isfinite(q0) && isfinite(q1) &&
+                        isfinite(q2) && isfinite(q3) && (q0 != 0.0f || q1 != 0.0f || q2 != 0.0f || q3 != 0.0f) &&
+                        isfinite(alpha_in);
+        if (!ok) {
+            atomicAdd(&stats->n_invalid, 1u);
+            atomicMin(&stats->first_invalid, (uint32_t)i);
+        }
+    }
     // R4: m = mu - o, D = |m|; excluded when D <= 1e-6 (Q17)
     const double mx = (double)m0 - (double)L.x;
     const double my = (double)m1 - (double)L.y;
@@ -183,6 +193,7 @@ __global__ void __launch_bounds__(256, 4) k_project(  // (256, 3) and (256, 2) m
 __global__ void k_init_stats(PlanStats* stats) {
     int t = threadIdx.x;
     if (t < DGSM_MAX_LIGHTS) { stats->depth_min[t] = 0xffffffffu; stats->depth_max[t] = 0u; }
+    if (t == 0) { stats->n_invalid = 0u; stats->first_invalid = 0xffffffffu; }
 }
 }  // namespace
 
@@ -201,6 +212,7 @@ void launch_project(const dgsm_gaussians_t& g, const LightsParam& lp, int n_ligh
                                             n_lights, res, K, (double)o.kappa, (double)o.k_sigma,
                                             (double)o.rho_scale * (double)(2 * res) / (2.0 * kPi), o.bin_mode,
                                             o.absorption, (o.flags & DGSM_NO_TILE_CULL) != 0,
+                                            (o.flags & DGSM_VALIDATE) != 0,
                                             slab_mask_ptr(o.slab), recs, counts, dup,
                                             stats);
 }

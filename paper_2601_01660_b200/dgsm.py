@@ -27,8 +27,9 @@ DGSM_BIN_WRAP, DGSM_BIN_CLAMP = 0, 1
 DGSM_OUTPUT_TAU = 1
 DGSM_COLLECT_STATS = 2
 DGSM_NO_TILE_CULL = 4
+DGSM_VALIDATE = 8
 ABSORPTION = {"traceavg": 0, "simple": 1, "mass": 2, "diag": 3}
-_STATUS = {0: "DGSM_OK", 1: "DGSM_EINVAL", 2: "DGSM_ENOSPC", 3: "DGSM_ECUDA", 4: "DGSM_ERANGE"}
+_STATUS = {0: "DGSM_OK", 1: "DGSM_EINVAL", 2: "DGSM_ENOSPC", 3: "DGSM_ECUDA", 4: "DGSM_ERANGE", 5: "DGSM_EDATA"}
 
 EXPORTED = ["dgsm_default_opts", "dgsm_plan_workspace_bytes", "dgsm_build_plan", "dgsm_build_run",
             "dgsm_build_bins", "dgsm_build", "dgsm_exp_epilogue", "dgsm_query", "dgsm_query_footprint", "dgsm_strerror",
@@ -36,7 +37,7 @@ EXPORTED = ["dgsm_default_opts", "dgsm_plan_workspace_bytes", "dgsm_build_plan",
             "dgsm_slab_bytes", "dgsm_active_slab", "dgsm_frame_host", "dgsm_default_transfer_opts",
             "dgsm_transfer_workspace_bytes", "dgsm_sh_transfer", "dgsm_sort_temp_bytes", "dgsm_sort_pairs_u32",
             "dgsm_order_workspace_bytes", "dgsm_receiver_order", "dgsm_query_ordered", "dgsm_query_chunks",
-            "dgsm_query_combine"]
+            "dgsm_query_combine", "dgsm_async_workspace_bytes", "dgsm_build_async"]
 
 
 class Gaussians(C.Structure):
@@ -70,6 +71,10 @@ class Plan(C.Structure):
                 ("depth_min", C.c_uint32 * DGSM_MAX_LIGHTS), ("depth_max", C.c_uint32 * DGSM_MAX_LIGHTS),
                 ("depth_bits", C.c_int32 * DGSM_MAX_LIGHTS), ("tile_bits", C.c_int32),
                 ("run_workspace_bytes", C.c_size_t), ("signature", C.c_uint64)]
+
+
+class BuildStatus(C.Structure):
+    _fields_ = [("n_keys", C.c_uint64), ("overflow", C.c_uint32), ("n_invalid", C.c_uint32)]
 
 
 class BuildStats(C.Structure):
@@ -135,6 +140,11 @@ def lib() -> C.CDLL:
         L.dgsm_query_chunks.restype = C.c_int
         L.dgsm_query_combine.argtypes = [vp, C.c_int, i64, vp, vp]
         L.dgsm_query_combine.restype = C.c_int
+        L.dgsm_async_workspace_bytes.argtypes = [i64, C.c_int, C.c_int, C.c_int, i64]
+        L.dgsm_async_workspace_bytes.restype = sz
+        L.dgsm_build_async.argtypes = [P(Gaussians), P(Light), C.c_int, C.c_int, C.c_int, P(BuildOpts), i64, vp, sz,
+                                       vp, vp, vp]
+        L.dgsm_build_async.restype = C.c_int
         L.dgsm_sort_temp_bytes.argtypes = [i64]
         L.dgsm_sort_temp_bytes.restype = sz
         L.dgsm_sort_pairs_u32.argtypes = [vp, vp, vp, vp, i64, C.c_int, vp, sz, P(C.c_int), vp]
@@ -240,6 +250,7 @@ class Options:
     collect_stats: bool = False
     absorption: str = "traceavg"   # traceavg (Eq.5) | simple | mass | diag (ablation B)
     tile_cull: bool = True         # False: ablation D, every Gaussian in every tile
+    validate: bool = False         # DGSM_VALIDATE: reject non-finite / degenerate Gaussians (DGSM_EDATA)
     slab: Optional[torch.Tensor] = None  # NEXT-1 ROI slab from active_slab(); None = full atlas
 
     def c(self) -> BuildOpts:
@@ -249,7 +260,8 @@ class Options:
                          DGSM_BIN_WRAP if self.bin_mode == "wrap" else DGSM_BIN_CLAMP,
                          (DGSM_OUTPUT_TAU if self.output_tau else 0) |
                          (DGSM_COLLECT_STATS if self.collect_stats else 0) |
-                         (0 if self.tile_cull else DGSM_NO_TILE_CULL),
+                         (0 if self.tile_cull else DGSM_NO_TILE_CULL) |
+                         (DGSM_VALIDATE if self.validate else 0),
                          ABSORPTION[self.absorption],
                          None if self.slab is None else C.c_void_p(self.slab.data_ptr()))
 
@@ -367,6 +379,44 @@ class Builder:
         _check(rc, "dgsm_build")
         self.launches = last_launch_count()
         return out
+
+
+class AsyncBuilder:
+    """dgsm_build_async: the sync-free build (no host synchronisation, capturable
+    in a CUDA graph) with a workspace sized for `key_capacity` keys.  The device
+    status (keys, overflow, invalid) of the last build is read by status()."""
+
+    def __init__(self, lights, atlas_res: int, n_shells: int, n: int, key_capacity: int,
+                 opts: Optional[Options] = None, device="cuda"):
+        self.lights, self.n_lights = _lights(lights)
+        self.res, self.K, self.n = int(atlas_res), int(n_shells), int(n)
+        self.opts = opts or Options()
+        self._oc = self.opts.c()
+        self.device = torch.device(device)
+        self.key_capacity = int(key_capacity)
+        need = lib().dgsm_async_workspace_bytes(self.n, self.n_lights, self.res, self.K, self.key_capacity)
+        if need == 0:
+            raise DgsmError("bad sizes for dgsm_build_async")
+        self.ws = _alloc(need, self.device)
+        self.status_buf = torch.zeros(16, dtype=torch.uint8, device=self.device)
+
+    def __call__(self, gaussians, out: torch.Tensor, stream=None) -> torch.Tensor:
+        g, keep = _gaussians(gaussians)
+        if g.n != self.n:
+            raise DgsmError(f"AsyncBuilder sized for n={self.n}, got {g.n}")
+        out = _out_f32(out, (self.n_lights, self.K, self.res, self.res), keep[0].device, "out")
+        rc = lib().dgsm_build_async(C.byref(g), self.lights, self.n_lights, self.res, self.K, C.byref(self._oc),
+                                    self.key_capacity, C.c_void_p(self.ws.data_ptr()), self.ws.numel(),
+                                    C.c_void_p(out.data_ptr()), C.c_void_p(self.status_buf.data_ptr()),
+                                    C.c_void_p(_stream_ptr(stream)))
+        _check(rc, "dgsm_build_async")
+        self.launches = last_launch_count()
+        return out
+
+    def status(self) -> dict:
+        b = self.status_buf.cpu().numpy()
+        st = BuildStatus.from_buffer_copy(b.tobytes())
+        return {"n_keys": int(st.n_keys), "overflow": bool(st.overflow), "n_invalid": int(st.n_invalid)}
 
 
 def build(gaussians: Dict[str, torch.Tensor], lights, atlas_res: int, n_shells: int,
