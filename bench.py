@@ -68,6 +68,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-transfer", action="store_true", help="skip the NEXT-4 transfer timing")
     ap.add_argument("--no-strong", action="store_true", help="skip the cfg5 strong-scaling sub-record")
+    ap.add_argument("--no-sequence", action="store_true", help="skip the cfg4 120-frame sequence sub-record")
     ap.add_argument("--layout", default="auto", choices=["auto", "light", "shells", "gaussian"],
                     help="multi-GPU layout of cfg3/cfg5 (distributed.plan_layout)")
     return ap.parse_args()
@@ -673,6 +674,122 @@ def strong_bench(cfg, steps, warmup, ctx, scale=1.0, layout_mode="auto", e2e=Tru
     return out, s
 
 
+# ------------------------------------------------ cfg4 animated sequence
+def _seq_frame(f):
+    from paper_2601_01660_b200 import synth as sy
+    return sy.Config4Sequence.frame_static(f)
+
+
+def sequence_frames(seq, frames):
+    """The occluders (walking avatar + prop) of every frame, generated on the
+    host before any timing (a process pool: ~0.3 s of numpy per frame)."""
+    import concurrent.futures as cf
+    import multiprocessing as mpc
+    workers = max(1, min(16, cores()))
+    with cf.ProcessPoolExecutor(max_workers=workers, mp_context=mpc.get_context("spawn")) as ex:
+        return list(ex.map(_seq_frame, frames))
+
+
+def sequence_bench(ctx, frames=None, warmup=3, modes=("full", "roi_slab")):
+    """cfg4 as BASELINE defines it: 120 frames of the walking
+    avatar + prop (the occluders of the paper's setting) over the static
+    2 M-Gaussian room (the receivers, Morton-ordered once).  Per frame: the
+    frame's occluders host -> device (pinned), the sync-free build
+    (dgsm_build_async) and the query of all 2 M receivers, replayed from ONE
+    CUDA graph (no host synchronisation inside a frame); in roi_slab mode the
+    receiver-driven ROI slab (dgsm_active_slab) restricts the build
+    first — the paper's own timed setting (0.13 s/frame on an A100).
+    Per-frame device time by CUDA events, L2 flushed between frames."""
+    import torch
+    from paper_2601_01660_b200 import dgsm
+    seq = synth.Config4Sequence()
+    frames = list(range(seq.n_frames)) if frames is None else list(frames)
+    occ = sequence_frames(seq, sorted(set(frames)))
+    occ = dict(zip(sorted(set(frames)), occ))
+    n = occ[frames[0]]["means"].shape[0]
+    host = {f: {k: torch.from_numpy(v).pin_memory() for k, v in o.items()} for f, o in occ.items()}
+    g = {k: v.to(ctx.dev) for k, v in host[frames[0]].items()}
+    xq_raw = torch.from_numpy(seq.queries).to(ctx.dev)
+    order, order_ms = order_receivers(dgsm, xq_raw, ctx)
+    xq = xq_raw[order].contiguous()
+    del xq_raw, order
+    m = xq.shape[0]
+    res, K, L = seq.res, seq.K, 1
+    atlas = torch.empty((L, K, res, res), dtype=torch.float32, device=ctx.dev)
+    T = torch.empty(m, dtype=torch.float32, device=ctx.dev)
+    out = {"workload": f"cfg4: {len(frames)} frames, walking 150k avatar + 50k prop occluders over a 2M-Gaussian "
+                       f"room (receivers), 1 light, {res}^2 x {K}",
+           "frames": len(frames), "receivers": m, "occluders_per_frame": n,
+           "receiver_order_ms_once": order_ms, "paper_context_s_per_frame": PAPER_CONTEXT["build_s_per_frame"],
+           "api": "per frame: H2D of the occluders, then one CUDA-graph replay of dgsm_build_async + dgsm_query "
+                  "(roi_slab: dgsm_active_slab first)"}
+    slab = torch.empty(dgsm.lib().dgsm_slab_bytes(1, res), dtype=torch.uint8, device=ctx.dev)
+    for mode in modes:
+        opts = dgsm.Options(slab=slab) if mode == "roi_slab" else dgsm.Options()
+        if mode == "roi_slab":
+            dgsm.active_slab(xq, seq.roi(frames[0]), seq.lights, res, K, out=slab)
+        # key capacity from a few frames' plans (the walk changes P slowly), with margin
+        Ps = []
+        for f in frames[:: max(1, len(frames) // 4)]:
+            gd = dgsm.to_device({k: v.numpy() for k, v in host[f].items()}, ctx.dev)
+            if mode == "roi_slab":
+                dgsm.active_slab(xq, seq.roi(f), seq.lights, res, K, out=slab)
+            Ps.append(dgsm.BuildPlan(gd, seq.lights, res, K, opts).n_keys)
+        cap = int(1.5 * max(Ps)) + 4096
+        ab = dgsm.AsyncBuilder(seq.lights, res, K, n, cap, opts, device=ctx.dev)
+        side = torch.cuda.Stream(device=ctx.dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                ab(g, atlas)
+                dgsm.query(atlas, seq.lights, xq, out=T)
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            ab(g, atlas)
+            dgsm.query(atlas, seq.lights, xq, out=T)
+        launches = ab.launches + 1
+        status = torch.zeros((len(frames), 16), dtype=torch.uint8, device=ctx.dev)
+
+        def frame(i, f):
+            for k_, v_ in host[f].items():
+                g[k_].copy_(v_, non_blocking=True)
+            if mode == "roi_slab":
+                dgsm.active_slab(xq, seq.roi(f), seq.lights, res, K, out=slab)
+            graph.replay()
+            status[i].copy_(ab.status_buf)
+
+        for i in range(warmup):
+            ctx.flush.zero_()
+            frame(i % len(frames), frames[i % len(frames)])
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in frames]
+        for a, b in ev:
+            a.record(); b.record()
+        torch.cuda.synchronize()
+        for i, f in enumerate(frames):
+            ctx.flush.zero_()
+            ev[i][0].record()
+            frame(i, f)
+            ev[i][1].record()
+        torch.cuda.synchronize()
+        t = np.array([a.elapsed_time(b) for a, b in ev])
+        st = status.cpu().numpy()
+        nk = st[:, :8].copy().view(np.uint64).reshape(-1).astype(np.int64)
+        over = st[:, 8:12].copy().view(np.uint32).reshape(-1)
+        out[mode] = {"ms_per_frame_mean": float(t.mean()), "ms_per_frame_p50": float(np.percentile(t, 50)),
+                     "ms_per_frame_p99": float(np.percentile(t, 99)), "ms_total": float(t.sum()),
+                     "value": float(64.0 * nk.sum() / (t.sum() * 1e-3)), "unit": UNIT,
+                     "keys_P_min": int(nk.min()), "keys_P_max": int(nk.max()), "key_capacity": cap,
+                     "overflow_frames": int((over != 0).sum()), "gpu_launches_per_frame": int(launches),
+                     "h2d_bytes_per_frame": int(n * 44),
+                     "vs_paper_s_per_frame": (PAPER_CONTEXT["build_s_per_frame"]["roi_and_light_space_culling"]
+                                              / (t.mean() * 1e-3)) if mode == "roi_slab" else None}
+        del graph, ab
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_dgsm(args):
     import torch
     import torch.distributed as dist
@@ -691,6 +808,11 @@ def run_dgsm(args):
                                e2e=not args.no_e2e)
     else:
         line, s = weak_bench(args, ctx)
+    if not args.no_sequence and args.config in (2, 4):
+        try:
+            line["cfg4_sequence"] = sequence_bench(ctx)
+        except Exception as e:  # reported, not fatal for the main line
+            line["cfg4_sequence"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     if not args.no_strong and args.config == 2:
         # the strong-scaling configuration of BASELINE (cfg5) on the same N GPUs
         try:

@@ -436,6 +436,40 @@ def config3(scale: float = 1.0, res: int = 1024, K: int = 64) -> Scene:
                  f"outdoor 80x80 m, {n} Gaussians, 4 lights, {res}^2 x {K}")
 
 
+def _config4_light():
+    size = (10.0, 8.0, 3.5)
+    lp = np.array([[5.5, 3.5, 3.1]])
+    return size, lp, dict(position=lp.astype(np.float32), t_max=t_max_for(lp, (0, 0, 0), size))
+
+
+def _config4_prop(scale: float = 1.0):
+    """cfg4's 50 k prop (its own seed: frames can be generated without the room)."""
+    _, lp, _ = _config4_light()
+    return _fill(rng_for(4, 3), int(round(50_000 * scale)),
+                 lambda r, m: surface_set(r, *sample_box(r, m, (6.2, 4.6, 0.0), (6.7, 5.1, 0.9)), 0.01, 0.5), lp)
+
+
+def _config4_static(scale: float = 1.0, room: bool = True):
+    """cfg4's static part: the 2.0 M room (the receivers), the 50 k prop, the light."""
+    size, lp, lights = _config4_light()
+    n_room, n_av = (int(round(x * scale)) for x in (2_000_000, 150_000))
+    room_g = _fill(rng_for(4), n_room, lambda r, m: room_scene(r, m, size, furniture=8), lp) if room else None
+    return room_g, _config4_prop(scale), lights, n_av
+
+
+def config4_avatar(frame: int, n_av: int, light_pos) -> Dict[str, np.ndarray]:
+    """The walking avatar of cfg4 at `frame` (30 fps): root +3.33 cm/frame along x,
+    limbs swinging at 1 Hz; its Gaussians keep their body-relative sampling
+    (the same seed every frame)."""
+    arng = rng_for(4, 7)
+    caps = human_capsules(config4_root(frame), phase=2 * np.pi * frame / 30.0)
+    return keep_clear_of_lights(avatar_set(arng, n_av, caps), light_pos)
+
+
+def config4_root(frame: int):
+    return (3.0 + 0.0333 * frame, 4.0, 0.0)
+
+
 def config4(frame: int = 0, scale: float = 1.0, occluders: str = "avatar+prop",
             res: int = 512, K: int = 64) -> Scene:
     """cfg4 (animated avatar): 2.0 M-Gaussian 10x8x3.5 m room, a 150 k avatar
@@ -443,21 +477,42 @@ def config4(frame: int = 0, scale: float = 1.0, occluders: str = "avatar+prop",
     30 fps) and a 50 k prop (0.5x0.5x0.9 m box); 1 light at 512^2 x 64.
     Occluders are avatar + prop (the paper's setting) or 'all'; the query
     runs over the 2.0 M scene centres."""
-    rng = rng_for(4)
-    size = (10.0, 8.0, 3.5)
-    lp = np.array([[5.5, 3.5, 3.1]])
-    n_room, n_av, n_prop = (int(round(x * scale)) for x in (2_000_000, 150_000, 50_000))
-    room = _fill(rng, n_room, lambda r, m: room_scene(r, m, size, furniture=8), lp)
-    prop = _fill(rng, n_prop, lambda r, m: surface_set(r, *sample_box(r, m, (6.2, 4.6, 0.0), (6.7, 5.1, 0.9)), 0.01, 0.5), lp)
-    # the avatar's Gaussians keep their body-relative sampling across frames
-    arng = rng_for(4, 7)
-    root = (3.0 + 0.0333 * frame, 4.0, 0.0)
-    caps = human_capsules(root, phase=2 * np.pi * frame / 30.0)
-    avatar = keep_clear_of_lights(avatar_set(arng, n_av, caps), lp)
+    room, prop, lights, n_av = _config4_static(scale)
+    avatar = config4_avatar(frame, n_av, lights["position"])
     occ = concat_gaussians(avatar, prop) if occluders != "all" else concat_gaussians(room, avatar, prop)
-    lights = dict(position=lp.astype(np.float32), t_max=t_max_for(lp, (0, 0, 0), size))
     return Scene(f"cfg4-f{frame}", occ, lights, res, K, room["means"].copy(),
                  f"room + walking avatar frame {frame}, occluders={occluders}, {res}^2 x {K}")
+
+
+class Config4Sequence:
+    """cfg4 as BASELINE defines it: 120 frames of the walking avatar + the prop
+    (the occluders of the paper's setting) over the static 2 M room
+    (the receivers).  frame(f) = the occluders of frame f (== config4(f).gaussians)."""
+
+    def __init__(self, n_frames: int = 120, scale: float = 1.0, res: int = 512, K: int = 64, room: bool = True):
+        self.room, self.prop, self.lights, self.n_av = _config4_static(scale, room)
+        self.n_frames, self.res, self.K = n_frames, res, K
+        self.queries = self.room["means"].copy() if room else None
+
+    def frame(self, f: int) -> Dict[str, np.ndarray]:
+        return concat_gaussians(config4_avatar(f, self.n_av, self.lights["position"]), self.prop)
+
+    _static = None
+
+    @classmethod
+    def frame_static(cls, f: int) -> Dict[str, np.ndarray]:
+        """frame(f) of the full-scale sequence, the static part built once per
+        process (for generating frames in worker processes)."""
+        if cls._static is None:
+            cls._static = cls(room=False)
+        return cls._static.frame(f)
+
+    def roi(self, f: int):
+        """ROI B of P:L156-158 around the avatar: centre = its root at mid-height
+        (the paper's alpha-weighted avatar centroid, here from the synthetic rig),
+        R = 2 m (the paper's example), z in [-0.1, 2.5] m."""
+        x, y, _ = config4_root(f)
+        return (x, y, 0.9, 2.0, -0.1, 2.5)
 
 
 def config5(scale: float = 1.0, res: int = 2048, K: int = 128) -> Scene:

@@ -50,7 +50,7 @@ def test_product_arm_line():
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    r = run_bench("--config", "1", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-transfer", "--no-strong",
+    r = run_bench("--config", "1", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-transfer", "--no-strong", "--no-sequence",
                   timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
