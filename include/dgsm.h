@@ -335,6 +335,20 @@ int dgsm_query_footprint(const float* atlas, const dgsm_light_t* lights, int n_l
                          int64_t m, const float* offsets, const float* weights, int n_samples,
                          float* T_out, float* colors_inout, void* stream);
 
+/* Footprint sample sets for dgsm_query_footprint (host arithmetic, no device
+ * work).  kind DGSM_STENCIL_CENTER: the single point z = 0, weight 1 (equals
+ * dgsm_query at the means).  kind DGSM_STENCIL_7: the deterministic 7-point
+ * stencil {0, +-delta e_1, +-delta e_2, +-delta e_3} in the receiver's
+ * principal-axes frame with weights proportional to the standard normal
+ * density exp(-|z|^2 / 2), normalised to sum 1 ("7-point";
+ * centre weight 1 / (1 + 6 e^{-delta^2/2}) = 0.2156 at delta = 1).
+ *   offsets_out HOST float [7][3], weights_out HOST float [7]; *n_out = the
+ *   number of samples written (1 or 7).  Errors: DGSM_EINVAL (null pointers,
+ *   unknown kind, delta not finite or <= 0 for the stencil). */
+#define DGSM_STENCIL_CENTER 0
+#define DGSM_STENCIL_7 1
+int dgsm_footprint_stencil(int kind, float delta, float* offsets_out, float* weights_out, int* n_out);
+
 /* ------------------------------------------------------------------
  * Receiver-driven region of interest and active voxel slab (SURVEY §8(f)
  * NEXT-1; §3.2).

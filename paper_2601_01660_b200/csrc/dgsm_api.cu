@@ -1,6 +1,7 @@
 // dgsm_api.cu — the C ABI of include/dgsm.h: argument validation, workspace
 // layout (caller-owned memory only), stream-ordered launches, error strings.
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -841,6 +842,29 @@ int dgsm_query_footprint(const float* atlas, const dgsm_light_t* lights, int n_l
                            colors_inout, (cudaStream_t)stream);
     g_launches = m > 0 ? 1 : 0;
     return cuda_check("query footprint");
+}
+
+int dgsm_footprint_stencil(int kind, float delta, float* offsets_out, float* weights_out, int* n_out) {
+    if (!offsets_out || !weights_out || !n_out) return fail(DGSM_EINVAL, "null output");
+    if (kind == DGSM_STENCIL_CENTER) {
+        offsets_out[0] = offsets_out[1] = offsets_out[2] = 0.0f;
+        weights_out[0] = 1.0f;
+        *n_out = 1;
+        return DGSM_OK;
+    }
+    if (kind != DGSM_STENCIL_7) return fail(DGSM_EINVAL, "unknown stencil kind %d", kind);
+    if (!(delta > 0.0f) || !(delta < 1e30f)) return fail(DGSM_EINVAL, "stencil delta must be finite and > 0");
+    // {0, +-delta e_j}; w_i proportional to exp(-|z_i|^2 / 2), normalised (fp64 host arithmetic)
+    const double d = delta, wc = 1.0, wa = exp(-0.5 * d * d), sum = wc + 6.0 * wa;
+    for (int i = 0; i < 21; ++i) offsets_out[i] = 0.0f;
+    weights_out[0] = (float)(wc / sum);
+    for (int j = 0; j < 3; ++j) {
+        offsets_out[3 * (1 + 2 * j) + j] = delta;
+        offsets_out[3 * (2 + 2 * j) + j] = -delta;
+        weights_out[1 + 2 * j] = weights_out[2 + 2 * j] = (float)(wa / sum);
+    }
+    *n_out = 7;
+    return DGSM_OK;
 }
 
 void dgsm_default_transfer_opts(dgsm_transfer_opts_t* o) {

@@ -37,7 +37,7 @@ EXPORTED = ["dgsm_default_opts", "dgsm_plan_workspace_bytes", "dgsm_build_plan",
             "dgsm_slab_bytes", "dgsm_active_slab", "dgsm_frame_host", "dgsm_default_transfer_opts",
             "dgsm_transfer_workspace_bytes", "dgsm_sh_transfer", "dgsm_sort_temp_bytes", "dgsm_sort_pairs_u32",
             "dgsm_order_workspace_bytes", "dgsm_receiver_order", "dgsm_query_ordered", "dgsm_query_chunks",
-            "dgsm_query_combine", "dgsm_async_workspace_bytes", "dgsm_build_async"]
+            "dgsm_query_combine", "dgsm_async_workspace_bytes", "dgsm_build_async", "dgsm_footprint_stencil"]
 
 
 class Gaussians(C.Structure):
@@ -145,6 +145,8 @@ def lib() -> C.CDLL:
         L.dgsm_build_async.argtypes = [P(Gaussians), P(Light), C.c_int, C.c_int, C.c_int, P(BuildOpts), i64, vp, sz,
                                        vp, vp, vp]
         L.dgsm_build_async.restype = C.c_int
+        L.dgsm_footprint_stencil.argtypes = [C.c_int, C.c_float, vp, vp, P(C.c_int)]
+        L.dgsm_footprint_stencil.restype = C.c_int
         L.dgsm_sort_temp_bytes.argtypes = [i64]
         L.dgsm_sort_temp_bytes.restype = sz
         L.dgsm_sort_pairs_u32.argtypes = [vp, vp, vp, vp, i64, C.c_int, vp, sz, P(C.c_int), vp]
@@ -629,20 +631,19 @@ def active_slab(receivers: torch.Tensor, roi, lights, atlas_res: int, n_shells: 
 
 
 def footprint_stencil(kind: str = "stencil7", delta: float = 1.0):
-    """Standard-normal footprint samples for query_footprint (NEXT-2).
-    "center": the single point z = 0 (equals query at the means).  "stencil7":
-    {0, +-delta e_j} weighted by the standard normal density exp(-|z|^2/2),
-    normalised to sum 1 (the SPEC's 7-point soft-shadow stencil)."""
-    if kind == "center":
-        return np.zeros((1, 3), np.float32), np.ones(1, np.float32)
-    if kind != "stencil7":
+    """Standard-normal footprint samples for query_footprint (NEXT-2),
+    from the library (dgsm_footprint_stencil): "center" = the single point z = 0;
+    "stencil7" = {0, +-delta e_j} weighted by exp(-|z|^2/2), normalised."""
+    kinds = {"center": 0, "stencil7": 1}
+    if kind not in kinds:
         raise DgsmError(f"unknown footprint stencil {kind!r}")
-    z = np.zeros((7, 3))
-    for j in range(3):
-        z[1 + 2 * j, j] = delta
-        z[2 + 2 * j, j] = -delta
-    w = np.exp(-0.5 * (z * z).sum(1))
-    return z.astype(np.float32), (w / w.sum()).astype(np.float32)
+    z = np.zeros((7, 3), np.float32)
+    w = np.zeros(7, np.float32)
+    n = C.c_int(0)
+    rc = lib().dgsm_footprint_stencil(kinds[kind], float(delta), z.ctypes.data_as(C.c_void_p),
+                                      w.ctypes.data_as(C.c_void_p), C.byref(n))
+    _check(rc, "dgsm_footprint_stencil")
+    return z[:n.value].copy(), w[:n.value].copy()
 
 
 def query_footprint(atlas: torch.Tensor, lights, gaussians, offsets, weights,

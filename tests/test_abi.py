@@ -7,6 +7,7 @@ import os
 import re
 import subprocess
 
+import numpy as np
 import pytest
 
 from paper_2601_01660_b200 import build_ext, dgsm
@@ -146,3 +147,16 @@ def test_transfer_validation(lib):
     assert lib.dgsm_sh_transfer(sh, 3, None, None, 0, C.byref(o), None, None, ws, 16, None) == 2
     o.s_max = 0.0
     assert lib.dgsm_sh_transfer(sh, 3, None, None, 0, C.byref(o), None, None, ws, 1 << 30, None) == 1
+
+
+def test_footprint_stencil_host_entry(lib, oracle_mod):
+    """dgsm_footprint_stencil (host arithmetic, no device) against the oracle's
+    7-point stencil and SPEC's centre weight 0.2156; bad arguments fail."""
+    z, w = dgsm.footprint_stencil("stencil7", 1.0)
+    zo, wo = oracle_mod.stencil7(1.0)
+    assert np.allclose(z, zo) and np.allclose(w, wo, atol=1e-7)
+    assert abs(w[0] - 0.2156) < 5e-5 and abs(w.sum() - 1.0) < 1e-6
+    z, w = dgsm.footprint_stencil("center")
+    assert z.shape == (1, 3) and w.tolist() == [1.0]
+    with pytest.raises(dgsm.DgsmError):
+        dgsm.footprint_stencil("stencil7", -1.0)
