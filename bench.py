@@ -98,7 +98,7 @@ def cfg_desc(s, cfg):
             "l2": "flushed before every step (256 MiB write)", "data": "synthetic, seeded (synth.py)"}
 
 
-def query_roofline(ms: float, m: int, L: int, peaks: dict, ms_raw: float = None):
+def query_roofline(ms: float, m: int, L: int, peaks: dict, ms_raw: float = None, cfg: int = 2, scale: float = 1.0):
     """a8 against HBM: algorithmic bytes and the sector-realistic
     count of a random-order gather (each row of taps is its own 32-B sector).
     ms: receivers in the scene's spatial (Morton) order; ms_raw: as generated."""
@@ -113,7 +113,8 @@ def query_roofline(ms: float, m: int, L: int, peaks: dict, ms_raw: float = None)
            "sector_frac": sec / (ms * 1e-3) / 1e9 / peak,
            "peak_src": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md 7.7 TB/s",
            "timing": "L2 flushed before each launch, CUDA events, host launch overhead excluded",
-           "receivers": "Morton-ordered scene receivers"}
+           "receivers": "Morton-ordered scene receivers",
+           "traffic": profiled_traffic("query_traffic.json", cfg, scale)}
     if ms_raw is not None:
         out["raw_order_frac"] = alg / (ms_raw * 1e-3) / 1e9 / peak
     return out
@@ -405,6 +406,18 @@ def time_fn(fn, reps: int, ctx):
     return float(np.median(ts))
 
 
+def profiled_traffic(name, cfg, scale):
+    """DRAM bytes per launch of a kernel from the committed ncu --set full capture
+    (profiles/<name>, per config), or None when this workload was not captured."""
+    prof = os.path.join(ROOT, "profiles", name)
+    if not os.path.exists(prof) or abs(scale - 1.0) > 1e-9:
+        return None
+    try:
+        return json.load(open(prof)).get(f"cfg{cfg}", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
 def accumulate_roofline(st, acc_ms, ctx, cfg, scale):
     """a6 against the FP32 pipe: SURVEY §8(d)'s per-pair figure (frac) and the
     work the kernel actually does per pair class (work_frac)."""
@@ -412,15 +425,7 @@ def accumulate_roofline(st, acc_ms, ctx, cfg, scale):
     alg_ops = OPS_PER_PAIR_SURVEY * st["pairs"]
     needed = OPS_PAIR * st["pairs"] + OPS_LIVE * st["pairs_live"] + OPS_SHELL * st["window_shells"] + OPS_STEP * st["steps"]
     achieved = alg_ops / (acc_ms * 1e-3) / 1e12
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "accumulate_traffic.json")
-    if os.path.exists(prof):
-        try:
-            pj = json.load(open(prof))
-            if pj.get("config") == f"cfg{cfg}" and abs(pj.get("scale", 1.0) - scale) < 1e-9:
-                traffic = pj.get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    traffic = profiled_traffic("accumulate_traffic.json", cfg, scale)
     return {"kernel": "k_accumulate (a6)", "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "peak_def": peak_def, "frac": achieved / peak, "traffic": traffic, "alg_ops_per_launch": int(alg_ops),
             "alg_def": f"SURVEY §8(d): {OPS_PER_PAIR_SURVEY} FP32+MUFU ops per Gaussian-ray pair x {int(st['pairs'])} pairs",
@@ -553,7 +558,7 @@ def weak_bench(args, ctx):
         "accumulate_work": {k: int(v) for k, v in st.items()},
         "gpu_launches": int(r["launches"]),
         "roofline": accumulate_roofline(st, acc_ms, ctx, args.config, args.scale),
-        "query_roofline": query_roofline(tq, m, s.L, ctx.peaks, tq_raw),
+        "query_roofline": query_roofline(tq, m, s.L, ctx.peaks, tq_raw, args.config, args.scale),
         "clocks": r["clocks"], "paper_context": PAPER_CONTEXT,
     }
     if e2e:
@@ -639,7 +644,7 @@ def strong_bench(cfg, steps, warmup, ctx, scale=1.0, layout_mode="auto", e2e=Tru
         "query_ms": tq, "query_gaussians_per_s": m / (tq * 1e-3),
         "gpu_launches": int(r["launches"]),
         "roofline": accumulate_roofline(st, acc_ms, ctx, cfg, scale),
-        "query_roofline": query_roofline(tq, m, s.L, ctx.peaks) if ctx.world == 1 else None,
+        "query_roofline": query_roofline(tq, m, s.L, ctx.peaks, None, cfg, scale) if ctx.world == 1 else None,
         "clocks": r["clocks"],
     }
     if e2e:

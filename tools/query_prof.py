@@ -1,5 +1,6 @@
-"""One launch of each query variant (for ncu): cfg2 raw, cfg2 pre-permuted,
-cfg5 raw, cfg5 pre-permuted (device-random atlases).  argv: configs."""
+"""One launch of the query on Morton-ordered receivers per config (for ncu):
+cfg2 (1 M receivers, 512^2 x 64, 1 light) and cfg5 (5.4 M, 2048^2 x 128, 8 lights),
+device-random atlases.  argv: configs."""
 import sys
 
 import torch
@@ -15,7 +16,6 @@ for cfg in [int(c) for c in (sys.argv[1:] or ["2", "5"])]:
     order = dgsm.receiver_order(x)
     xp = x[order.long()].contiguous()
     torch.cuda.synchronize()
-    dgsm.query(atlas, s.lights, x)
     dgsm.query(atlas, s.lights, xp)
     torch.cuda.synchronize()
     del atlas

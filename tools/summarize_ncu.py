@@ -105,15 +105,15 @@ def report(path):
         print()
 
 
-def traffic(path, cfg, scale=1.0):
-    for d in raw(path):
-        if "accumulate" not in d.get("Kernel Name", ("", ""))[0]:
-            continue
+def traffic(path, cfg, scale=1.0, kernel="accumulate", index=0):
+    """DRAM bytes of the index-th captured launch of `kernel` (json on stdout)."""
+    hits = [d for d in raw(path) if kernel in d.get("Kernel Name", ("", ""))[0]]
+    for d in hits[index:index + 1]:
         def mb(k):
             v, u = d[k]
             f = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
             return float(v) * f
-        print(json.dumps({"config": cfg, "scale": scale, "kernel": "k_accumulate",
+        print(json.dumps({"config": cfg, "scale": scale, "kernel": f"k_{kernel}",
                           "dram_bytes_per_launch": mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum"),
                           "dram_read": mb("dram__bytes_read.sum"), "dram_write": mb("dram__bytes_write.sum"),
                           "source": path}, indent=1))
@@ -126,5 +126,6 @@ if __name__ == "__main__":
         launches(path)
     elif mode == "report":
         report(path)
-    else:
-        traffic(path, sys.argv[3] if len(sys.argv) > 3 else "cfg2")
+    else:  # traffic <rep> <cfg> [kernel] [index]
+        traffic(path, sys.argv[3] if len(sys.argv) > 3 else "cfg2", 1.0,
+                sys.argv[4] if len(sys.argv) > 4 else "accumulate", int(sys.argv[5]) if len(sys.argv) > 5 else 0)
