@@ -479,16 +479,23 @@ def weak_bench(args, ctx):
     m = xq.shape[0]
     atlas = torch.empty((s.L, s.K, s.res, s.res), dtype=torch.float32, device=ctx.dev)
     T_out = torch.empty(m, dtype=torch.float32, device=ctx.dev)
-    builder = dgsm.Builder(s.lights, s.res, s.K, device=ctx.dev)
+    st, P = build_stats(dgsm, g, s.lights, s.res, s.K)
+    # the per-frame entry point of a renderer: the sync-free build (no host
+    # synchronisation inside the step) with a key capacity of 1.25 P, as a frame
+    # stream would size it from an earlier frame; the status word is checked after
+    cap = int(1.25 * P) + 4096
+    builder = dgsm.AsyncBuilder(s.lights, s.res, s.K, s.n, cap, device=ctx.dev)
 
     def step():
-        builder(g, atlas)  # dgsm_build: plan + run in one C call
+        builder(g, atlas)  # dgsm_build_async: plan + run, no host sync
         nl = builder.launches
         dgsm.query(atlas, s.lights, xq, out=T_out)
         return nl + dgsm.last_launch_count()
 
-    st, P = build_stats(dgsm, g, s.lights, s.res, s.K)
     r = time_steps(step, args.steps, args.warmup, ctx)
+    bst = builder.status()
+    if bst["overflow"] or bst["n_keys"] != P:
+        sys.exit(f"bench.py: sync-free build status {bst} (expected {P} keys)")
     K = args.steps
     total_ms = float(np.sum(r["t_step"]))
     total_max = ctx.max_over_ranks(total_ms)
@@ -547,6 +554,7 @@ def weak_bench(args, ctx):
         "data": "synthetic",
         "config": dict(cfg_desc(s, args.config),
                        parallelism=f"{ctx.world} independent frame(s), one per rank, no data-path collective",
+                       build=f"dgsm_build_async (no host sync), key capacity {cap} (1.25 P); status checked",
                        receivers=("scene receivers stored in Morton order (dgsm_receiver_order, once per scene: "
                                   f"{order_ms * 1e3:.0f} us)")),
         "step_ms_each": [round(x, 3) for x in r["t_step"]], "step_ms_median": float(np.median(r["t_step"])),
@@ -813,7 +821,7 @@ def run_dgsm(args):
                                e2e=not args.no_e2e)
     else:
         line, s = weak_bench(args, ctx)
-    if not args.no_sequence and args.config in (2, 4):
+    if not args.no_sequence and args.config in (2, 4) and ctx.rank == 0:  # a single-GPU workload
         try:
             line["cfg4_sequence"] = sequence_bench(ctx)
         except Exception as e:  # reported, not fatal for the main line
