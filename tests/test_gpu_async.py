@@ -109,3 +109,22 @@ def test_validate_flag(dg):
     ab = dg.AsyncBuilder(s.lights, s.res, s.K, s.n, 100000, dg.Options(validate=True))
     ab(gd, torch.empty((1, s.K, s.res, s.res), device="cuda"))
     assert ab.status()["n_invalid"] == 2
+
+
+def test_async_empty_and_slab(dg, oracle_mod):
+    """n = 0 (T == 1 exactly, P = 0) and a ROI-slab build through the sync-free path."""
+    s = synth.random_scene(11, 400, res=32, K=8, L=3, dist=(0.3, 3.0), scale=(0.01, 0.5))
+    empty = {k: v[:0] for k, v in s.gaussians.items()}
+    ab = dg.AsyncBuilder(s.lights, s.res, s.K, 0, 1)
+    out = torch.zeros((s.L, s.K, s.res, s.res), device="cuda")
+    ab(dg.to_device(empty), out)
+    assert torch.all(out == 1.0) and ab.status()["n_keys"] == 0 and not ab.status()["overflow"]
+    g = dg.to_device(s.gaussians)
+    x = torch.from_numpy(s.queries).cuda()
+    slab = dg.active_slab(x, (0.0, 0.0, 0.0, 2.0, -1.0, 1.0), s.lights, s.res, s.K)
+    opts = dg.Options(slab=slab)
+    ref = dg.build(g, s.lights, s.res, s.K, opts)
+    P = dg.BuildPlan(g, s.lights, s.res, s.K, opts).n_keys
+    ab = dg.AsyncBuilder(s.lights, s.res, s.K, s.n, P, opts)
+    ab(g, out)
+    assert torch.equal(out, ref) and ab.status()["n_keys"] == P
