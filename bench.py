@@ -652,6 +652,7 @@ def strong_bench(cfg, steps, warmup, ctx, scale=1.0, layout_mode="auto", e2e=Tru
         "query_ms": tq, "query_gaussians_per_s": m / (tq * 1e-3),
         "gpu_launches": int(r["launches"]),
         "roofline": accumulate_roofline(st, acc_ms, ctx, cfg, scale),
+        "accumulate_work_rank0": {k: int(v) for k, v in st.items()},
         "query_roofline": query_roofline(tq, m, s.L, ctx.peaks, None, cfg, scale) if ctx.world == 1 else None,
         "clocks": r["clocks"],
     }

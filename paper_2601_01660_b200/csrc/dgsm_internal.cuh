@@ -25,13 +25,15 @@ struct __align__(16) PairRec {
     int32_t kD;       // anchor shell
     float betap;      // beta * sqrt(pi/2) = kappa tau* sqrt(tr A / 3) / 2  (Eq.3 x Eq.5)
     float rcut_D2;    // negligible-pair bound r_cut / D^2 (R8', per Gaussian-light)
-    float pad;
+    uint32_t shells;  // lo | hi << 16: conservative bounds of the shells any live pair of this
+                      // record writes (window rows and step row, hi inclusive, <= K): the
+                      // accumulation's shell bands (accumulate.cu, DESIGN.md §6 a6)
 };
 static_assert(sizeof(PairRec) == 96, "PairRec must be 96 B");
 // field offsets the accumulation kernel's register staging reads by word (accumulate.cu)
 static_assert(offsetof(PairRec, g) == 24 && offsetof(PairRec, W) == 36 && offsetof(PairRec, D) == 72 &&
                   offsetof(PairRec, eD) == 76 && offsetof(PairRec, kD) == 80 && offsetof(PairRec, betap) == 84 &&
-                  offsetof(PairRec, rcut_D2) == 88,
+                  offsetof(PairRec, rcut_D2) == 88 && offsetof(PairRec, shells) == 92,
               "PairRec layout");
 
 struct LightsParam {

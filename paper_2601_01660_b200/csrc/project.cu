@@ -165,8 +165,26 @@ __global__ void __launch_bounds__(256, 4) k_project(  // (256, 3) and (256, 2) m
                 const float smax = fmaxf(sc0, fmaxf(sc1, sc2));
                 const float rcut = fminf(2.0f * logf(2.0f * rec.betap * smax) + 44.3614195558365f, 180.0f);
                 rec.rcut_D2 = rcut / (Df * Df);
+                // Shell bounds of the writes of any live pair (r <= r_cut): its window
+                // shells and step row lie where the ray is within Mahalanobis radius
+                // rho = sqrt(r + 2 * 3.92^2) of mu (|x_k| < 3.92 in the window; +1 for the
+                // rounding of the fp32 live test), i.e. at points mu + y with y^T A y <= rho^2.
+                // Their distance t = |mu + y| from the light satisfies
+                //   t >= D + y.d >= D - rho s_d,   s_d^2 = d^T Sigma d = sum_j s_j^2 w_j^2,
+                //   t <= D + rho s_d + (rho s_max)^2 / (2 (D - rho s_d))   (|y_perp| <= rho s_max)
+                // (t <= D + rho s_max when D <= rho s_d).  Shell k is at t_k = (k + 1/2) dt;
+                // the kernel's window bounds are ceil((s* -+ xsh)/dt - 1/2) (+1 on a rounding
+                // tie): 0.01 shell of slack for its fp32 arithmetic, one more row above.
+                const double rho = sqrt(fmax((double)rcut, 0.0) + 31.7312);
+                const double s_d = sqrt((s2[0] * (w[0] * w[0]) + s2[1] * (w[1] * w[1])) + s2[2] * (w[2] * w[2]));
+                const double rs = rho * (double)smax, near = D - rho * s_d;
+                const double t_lo = near, t_hi = near > 0.25 * D ? D + rho * s_d + rs * rs / (2.0 * near) : D + rs;
+                const double idt = (double)K / (double)L.w;
+                double klo = floor(t_lo * idt - 0.51), khi = ceil(t_hi * idt - 0.49) + 1.0;
+                klo = klo < 0.0 ? 0.0 : (klo > K - 1.0 ? K - 1.0 : klo);
+                khi = khi < klo ? klo : (khi > (double)K ? (double)K : khi);
+                rec.shells = (uint32_t)klo | ((uint32_t)khi << 16);
             }
-            rec.pad = 0.0f;
             dbits = __float_as_uint(Df);
         }
     }
