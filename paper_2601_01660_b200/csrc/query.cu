@@ -168,8 +168,15 @@ __device__ __forceinline__ void apply_colors(float* colors, int64_t q, float T) 
 // their light loops interleaved: independent index chains and tap gathers in flight.
 constexpr int kQPT = DGSM_QPT;
 constexpr int kQThreads = 256;
+// 8 CTAs of 256 per SM (32 registers, full occupancy): more gathers in flight.
+// Measured (tools/query_bench2.py, L2 flushed, pre-permuted receivers): cfg2
+// 20.5 -> 18.5 us, cfg5 397 -> 358 us against no bound (56 registers, 4 CTAs/SM);
+// 5 and 6 CTAs/SM lie between.
+#ifndef DGSM_QMINB
+#define DGSM_QMINB 8
+#endif
 
-__global__ void __launch_bounds__(kQThreads) k_query(const float* __restrict__ atlas, QueryLights ql,
+__global__ void __launch_bounds__(kQThreads, DGSM_QMINB) k_query(const float* __restrict__ atlas, QueryLights ql,
                                                      int n_lights, int res, int K,
                                                      const float* __restrict__ pos, int64_t m,
                                                      float* __restrict__ T_out, float* __restrict__ colors) {
@@ -203,7 +210,7 @@ __global__ void __launch_bounds__(kQThreads) k_query(const float* __restrict__ a
 // 32 lanes of a warp sit next to each other in space and, for every light, hit
 // neighbouring atlas texels and shells: shared 32-B sectors, open DRAM pages,
 // few TLB entries, instead of one random gather per lane into a multi-GiB atlas.
-__global__ void __launch_bounds__(kQThreads) k_query_ordered(const float* __restrict__ atlas, QueryLights ql,
+__global__ void __launch_bounds__(kQThreads, DGSM_QMINB) k_query_ordered(const float* __restrict__ atlas, QueryLights ql,
                                                              int n_lights, int res, int K,
                                                              const float* __restrict__ pos,
                                                              const uint32_t* __restrict__ order, int64_t m,
