@@ -41,9 +41,13 @@ constexpr int kStage = 32;        // records per pipeline stage
 // buffer (kTMA), or 16-B loads into registers one stage ahead (no raw buffer).
 // launch_accumulate takes TMA unless the raw buffer costs a CTA per SM.
 constexpr size_t kRawBytesTMA = kStage * 96;
-// Shell bands: the shared table holds at most kBandRows shells; K > kBandRows runs
-// one pass per band of kBandRows shells over the records meeting it (DESIGN.md §6 a6).
-constexpr int kBandRows = 64;
+// Shell bands: K <= kTableRows runs k_accumulate with a K-row table; larger K runs
+// k_accumulate_band, one pass per band of kBandRows shells over the records meeting
+// it (DESIGN.md §6 a6).  48 rows (3 bands at K = 128) leave 12 CTAs/SM (the register
+// limit) where 64 rows (2 bands) leave 11: cfg5 a6 48.7 -> 45.7 ms (32 / 40 / 43 / 56
+// rows: 52.2 / 51.5 / 50.8 / 47.7 ms).
+constexpr int kTableRows = 64;
+constexpr int kBandRows = 48;
 constexpr int kMinBandRows = 32;  // DGSM_BAND_ROWS (A/B) is clamped to [32, 256]
 constexpr int kMaxBands = DGSM_MAX_SHELLS / kMinBandRows;
 constexpr int kAccMinBlocks = 11;  // band kernel: caps registers at 80 (ptxas otherwise takes 96-168)
@@ -1068,7 +1072,7 @@ __global__ void k_exp(const float* tau, float* T, int64_t count) {
 thread_local bool last_staging_tma = false;
 bool accumulate_last_used_tma() { return last_staging_tma; }
 
-// Table rows of the accumulation for K shells: K up to kBandRows, else kBandRows
+// Table rows of the accumulation for K shells: K up to kTableRows, else kBandRows
 // (bands); DGSM_BAND_ROWS overrides kBandRows (A/B), clamped to [32, 256].
 int accumulate_rows(int K) {
     static const int band_rows = [] {
@@ -1076,7 +1080,7 @@ int accumulate_rows(int K) {
         if (const char* e = getenv("DGSM_BAND_ROWS")) r = atoi(e);
         return std::min(std::max(r, kMinBandRows), DGSM_MAX_SHELLS);
     }();
-    return std::min(K, band_rows);
+    return K <= kTableRows ? K : std::min(K, band_rows);
 }
 
 size_t accumulate_smem_bytes(int K, bool tma) {
@@ -1112,7 +1116,9 @@ void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint3
     cudaGetDevice(&dev);
     const size_t smem_tma = accumulate_smem_bytes(K, true), smem_reg = accumulate_smem_bytes(K, false);
     if (dev < 64 && !(attr_set_mask.load() & (1ull << dev))) {
-        const int smax = (int)accumulate_smem_bytes(DGSM_MAX_SHELLS, true);
+        // (the largest table of either kernel: DGSM_MAX_SHELLS rows + 2 dump rows)
+        const int smax = (int)(kRawBytesTMA + kStage * kCompact * sizeof(float4) +
+                               (size_t)(DGSM_MAX_SHELLS + 2) * kThreads * sizeof(float));
 #define DGSM_ACC_ATTR(F) cudaFuncSetAttribute(F, cudaFuncAttributeMaxDynamicSharedMemorySize, smax)
         DGSM_ACC_ATTR((k_accumulate<false, true>)); DGSM_ACC_ATTR((k_accumulate<true, true>));
         DGSM_ACC_ATTR((k_accumulate<false, false>)); DGSM_ACC_ATTR((k_accumulate<true, false>));
