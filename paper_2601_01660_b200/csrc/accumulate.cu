@@ -64,6 +64,9 @@ __device__ __forceinline__ float ex2_approx(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// T = exp(-tau) (Eq.4) as one MUFU ex2: relative error ~2^-22 (|dT| < 3e-7), exactly 1 at
+// tau = 0 and 0 below 2^-126; the same function in every epilogue and in k_exp.
+__device__ __forceinline__ float t_of_tau(float tau) { return ex2_approx(-1.4426950408889634f * tau); }
 __device__ __forceinline__ float rcp_approx(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -626,9 +629,11 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(  // 11 CTAs/SM at K = 
         const float one = want_tau ? 0.0f : 1.0f;
         if (wu.nchunks == 1) {
             float tau = 0.0f;
+            // (one loop: a separate select-free path for the common case costs this
+            // kernel 16 registers; the band kernel has one)
             for (int k = 0; k < K; ++k) {
                 tau += s_acc[k * kThreads + tid];
-                out[(size_t)k * plane] = (k < klo || k > khi) ? one : (want_tau ? tau : expf(-tau));
+                out[(size_t)k * plane] = (k < klo || k > khi) ? one : (want_tau ? tau : t_of_tau(tau));
             }
         } else {
             float* part = scratch + ((size_t)(wu.slot + wu.chunk) * K) * kThreads + tid;
@@ -662,7 +667,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(  // 11 CTAs/SM at K = 
 #pragma unroll
                     for (int u = 0; u < kCB; ++u) {
                         const int k = k0 + u;
-                        if (k < K) out[(size_t)k * plane] = (k < klo || k > khi) ? one : (want_tau ? t[u] : expf(-t[u]));
+                        if (k < K) out[(size_t)k * plane] = (k < klo || k > khi) ? one : (want_tau ? t[u] : t_of_tau(t[u]));
                     }
                 }
                 if (tid == 0) tile_arrive[tslot] = 0u;
@@ -937,12 +942,21 @@ __global__ void __launch_bounds__(kThreads, kAccMinBlocks) k_accumulate_band(
                 const bool want_tau = (flags & DGSM_OUTPUT_TAU) != 0;
                 const float one = want_tau ? 0.0f : 1.0f;
                 const size_t plane = (size_t)H * W;
-                float* out = atlas + ((size_t)l * K + kb0) * plane + (size_t)row * W + col;
-                for (int k = 0; k < nrows; ++k) {
-                    tau += s_acc[(k + 1) * kThreads + tid];
-                    s_acc[(k + 1) * kThreads + tid] = 0.0f;
-                    const int ks = kb0 + k;
-                    out[(size_t)k * plane] = (ks < sklo || ks > skhi) ? one : (want_tau ? tau : expf(-tau));
+                float* o = atlas + ((size_t)l * K + kb0) * plane + (size_t)row * W + col;
+                if (!slab_mask && !want_tau) {  // the common case: no per-shell selects
+#pragma unroll 4
+                    for (int k = 0; k < nrows; ++k, o += plane) {
+                        tau += s_acc[(k + 1) * kThreads + tid];
+                        s_acc[(k + 1) * kThreads + tid] = 0.0f;
+                        *o = t_of_tau(tau);
+                    }
+                } else {
+                    for (int k = 0; k < nrows; ++k, o += plane) {
+                        tau += s_acc[(k + 1) * kThreads + tid];
+                        s_acc[(k + 1) * kThreads + tid] = 0.0f;
+                        const int ks = kb0 + k;
+                        *o = (ks < sklo || ks > skhi) ? one : (want_tau ? tau : t_of_tau(tau));
+                    }
                 }
             } else {
                 float* part = scratch + ((size_t)(wu.slot + wu.chunk) * K + kb0) * kThreads + tid;
@@ -1007,7 +1021,7 @@ __global__ void __launch_bounds__(kThreads, kAccMinBlocks) k_accumulate_band(
 #pragma unroll
                     for (int u = 0; u < kCB; ++u) {
                         const int k = k0 + u;
-                        if (k < K) out[(size_t)k * plane] = (k < sklo || k > skhi) ? one : (want_tau ? t[u] : expf(-t[u]));
+                        if (k < K) out[(size_t)k * plane] = (k < sklo || k > skhi) ? one : (want_tau ? t[u] : t_of_tau(t[u]));
                     }
                 }
                 if (tid == 0) tile_arrive[tslot] = 0u;
@@ -1058,14 +1072,14 @@ __global__ void __launch_bounds__(256) k_combine_deferred(const WorkUnit* __rest
             khi = ((slab_mask[wu.tile] >> tt) & 1ull) ? kr.y : -1;
         }
         atlas[((size_t)l * K + k) * plane + (size_t)row * res + col] =
-            (k < klo || k > khi) ? one : (want_tau ? t : expf(-t));
+            (k < klo || k > khi) ? one : (want_tau ? t : t_of_tau(t));
     }
 }
 
 __global__ void k_exp(const float* tau, float* T, int64_t count) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
          i += (int64_t)gridDim.x * blockDim.x)
-        T[i] = expf(-tau[i]);
+        T[i] = t_of_tau(tau[i]);
 }
 }  // namespace
 

@@ -175,6 +175,11 @@ constexpr int kQThreads = 256;
 #ifndef DGSM_QMINB
 #define DGSM_QMINB 8
 #endif
+// k_query_chunks (the multi-GPU step's query, also at N = 1): 6 CTAs/SM (40 registers);
+// cfg5 0.427 / 0.374 / 0.458 ms at no bound / 6 / 8 (8: 32 registers with spills)
+#ifndef DGSM_QCMINB
+#define DGSM_QCMINB 6
+#endif
 
 __global__ void __launch_bounds__(kQThreads, DGSM_QMINB) k_query(const float* __restrict__ atlas, QueryLights ql,
                                                      int n_lights, int res, int K,
@@ -329,7 +334,7 @@ struct ChunkParam {
     int split[DGSM_MAX_LIGHTS];
 };
 
-__global__ void __launch_bounds__(kQThreads) k_query_chunks(ChunkParam cp, QueryLights ql, int n_lights, int res,
+__global__ void __launch_bounds__(kQThreads, DGSM_QCMINB) k_query_chunks(ChunkParam cp, QueryLights ql, int n_lights, int res,
                                                             int K, const float* __restrict__ pos, int64_t m,
                                                             float* __restrict__ T_out,
                                                             float* __restrict__ partial_out) {
