@@ -175,14 +175,17 @@ __global__ void __launch_bounds__(256, 4) k_project(  // (256, 3) and (256, 2) m
                 // (t <= D + rho s_max when D <= rho s_d).  Shell k is at t_k = (k + 1/2) dt;
                 // the kernel's window bounds are ceil((s* -+ xsh)/dt - 1/2) (+1 on a rounding
                 // tie): 0.01 shell of slack for its fp32 arithmetic, one more row above.
-                const double rho = sqrt(fmax((double)rcut, 0.0) + 31.7312);
-                const double s_d = sqrt((s2[0] * (w[0] * w[0]) + s2[1] * (w[1] * w[1])) + s2[2] * (w[2] * w[2]));
-                const double rs = rho * (double)smax, near = D - rho * s_d;
-                const double t_lo = near, t_hi = near > 0.25 * D ? D + rho * s_d + rs * rs / (2.0 * near) : D + rs;
-                const double idt = (double)K / (double)L.w;
-                double klo = floor(t_lo * idt - 0.51), khi = ceil(t_hi * idt - 0.49) + 1.0;
-                klo = klo < 0.0 ? 0.0 : (klo > K - 1.0 ? K - 1.0 : klo);
-                khi = khi < klo ? klo : (khi > (double)K ? (double)K : khi);
+                // Computed in fp32 (a conservative bound, not part of the binning
+                // contract): 0.02 shell of slack more for its own rounding (~1e-4 shell).
+                const float rho = sqrtf(fmaxf(rcut, 0.0f) + 31.7312f);
+                const float wf0 = (float)w[0], wf1 = (float)w[1], wf2 = (float)w[2];
+                const float s_d = sqrtf((sc0 * sc0) * (wf0 * wf0) + (sc1 * sc1) * (wf1 * wf1) + (sc2 * sc2) * (wf2 * wf2));
+                const float rs = rho * smax, near = Df - rho * s_d;
+                const float t_hi = near > 0.25f * Df ? Df + rho * s_d + rs * rs / (2.0f * near) : Df + rs;
+                const float idt = (float)K / L.w;
+                float klo = floorf(near * idt - 0.53f), khi = ceilf(t_hi * idt - 0.47f) + 1.0f;
+                klo = klo < 0.0f ? 0.0f : (klo > K - 1.0f ? K - 1.0f : klo);
+                khi = khi < klo ? klo : (khi > (float)K ? (float)K : khi);
                 rec.shells = (uint32_t)klo | ((uint32_t)khi << 16);
             }
             dbits = __float_as_uint(Df);
