@@ -220,7 +220,10 @@ int dgsm_build_async(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int 
                      int n_shells, const dgsm_build_opts_t* opts, int64_t key_capacity, void* ws,
                      size_t ws_bytes, float* atlas_out, dgsm_build_status_t* status, void* stream);
 
-/* T = exp(-tau) elementwise (Eq.4), in place allowed (tau == T). Device pointers. */
+/* T = exp(-tau) elementwise (Eq.4), in place allowed (tau == T). Device pointers.
+ * Computed as 2^(-tau log2 e) with the hardware ex2 (relative error ~2^-22, T = 1
+ * exactly at tau = 0), the same form as the build's own epilogue, so a sharded
+ * build's tau -> T equals a single-GPU build's T up to the summation order of tau. */
 int dgsm_exp_epilogue(const float* tau, float* T, int64_t count, void* stream);
 
 /* DGSM sampling: for each receiver x_q (device [m][3]),
