@@ -14,6 +14,9 @@ namespace {
 thread_local char g_err[512] = "";
 thread_local int g_launches = 0;
 thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;
+// dgsm_frame_host: recorded on the build stream right before the accumulation
+// (a5/a6) of the frame being enqueued (nullptr: not recorded)
+thread_local cudaEvent_t g_ev_frame_acc = nullptr;
 
 int fail(int code, const char* fmt, ...) {
     va_list ap;
@@ -299,6 +302,12 @@ struct CopyStream {
     cudaEvent_t slot_ev[4];
     int slot_next = 0;
     cudaEvent_t chunk[kUploadChunks];
+    // the accumulation of the last frame enqueued: the next frame's uploads start
+    // there (overlapping the FP32-bound a6 kernel, not the L2-resident sorts, which a
+    // concurrent 60 MB upload slowed by 28 %: tools/e2e_probe3.py).  cfg2 frames back
+    // to back: 1.51-1.65 -> 1.50-1.51 ms (recording it before the tile sort instead: same)
+    cudaEvent_t acc = nullptr;
+    bool acc_valid = false;
     int dev = -1;
 };
 static CopyStream& copy_stream() {
@@ -314,6 +323,8 @@ static CopyStream& copy_stream() {
             cs.slot_ws[i] = nullptr;
         }
         for (int i = 0; i < kUploadChunks; ++i) cudaEventCreateWithFlags(&cs.chunk[i], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&cs.acc, cudaEventDisableTiming);
+        cs.acc_valid = false;
         cs.dev = dev;
     }
     return cs;
@@ -336,6 +347,7 @@ static void enqueue_plan(const dgsm_gaussians_t* g, const dgsm_gaussians_t* g_ho
         // the work already queued on `s` (the device arrays may still be in use)
         CopyStream& cs = copy_stream();
         if (upload_after) cudaStreamWaitEvent(cs.st, upload_after, 0);  // the workspace's previous frame is done
+        if (cs.acc_valid) cudaStreamWaitEvent(cs.st, cs.acc, 0);       // the previous frame's a6 has started
         const int64_t n = g->n, per = (n + n_chunks - 1) / n_chunks;
         int c = 0;
         for (int64_t i0 = 0; i0 < n; i0 += per, ++c) {
@@ -505,6 +517,7 @@ static void run_accumulate(const dgsm_gaussians_t* g, const dgsm_light_t* lights
                            float* atlas_out, cudaStream_t s) {
     const LightsParam lp = lights_param(lights, sh.n_lights);
     const int64_t nt = sh.n_lights * (int64_t)(sh.res / kTile) * (sh.res / kTile);
+    if (g_ev_frame_acc) cudaEventRecord(g_ev_frame_acc, s);
     launch_units(r.tile_start, r.tile_end, nt, sh.chunk, r.unit_cnt, r.unit_off, r.unit_scan_temp, r.units_tmp,
                  r.units, r.max_units, r.counters, r.counters + 8, r.counters + 8 + kUnitClasses, r.deferred,
                  r.counters + 2, s, &g_launches);
@@ -670,9 +683,12 @@ int dgsm_frame_host(const dgsm_gaussians_t* g_host, const dgsm_light_t* lights, 
     // receivers ride the copy stream (after the Gaussian chunks) while the atlas is built
     if (m > 0) cudaMemcpyAsync(rec, receivers_host, 12 * (size_t)m, cudaMemcpyHostToDevice, cs.st);
     cudaEventRecord(cs.done, cs.st);
+    g_ev_frame_acc = cs.acc;
     rc = dgsm_build_run(&gd, lights, n_lights, opts, &plan, plan_ws, pb, (char*)plan_ws + pb,
                         ws_bytes - fixed - pb, atlas_out, stream);
+    g_ev_frame_acc = nullptr;
     if (rc) return rc;
+    cs.acc_valid = true;
     launches += g_launches;
     cudaStreamWaitEvent(s, cs.done, 0);
     // page-locked T_host: the query writes it directly over the bus (no separate

@@ -1,0 +1,4 @@
+#!/bin/bash
+# e2e probe (cfg2).  Under gpurun.
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1 || exit 1
+timeout 600 python tools/e2e_probe2.py
