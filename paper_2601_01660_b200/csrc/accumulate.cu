@@ -41,6 +41,13 @@ constexpr int kStage = 32;        // records per pipeline stage
 // buffer (kTMA), or 16-B loads into registers one stage ahead (no raw buffer).
 // launch_accumulate takes TMA unless the raw buffer costs a CTA per SM.
 constexpr size_t kRawBytesTMA = kStage * 96;
+// Records per stage of the single-table kernel (K <= 64): 24 keep its shared memory
+// (16 KB table + 1.9 KB compact copy) within 12 CTAs/SM, the register limit at 80
+// registers, where 32 allowed 11: cfg2 a6 0.930 -> 0.917 ms, cfg3 6.31 -> 6.19 ms
+// (16 records: 0.926 ms; 64: 0.953 ms at 10 CTAs/SM).  The band kernel keeps 32
+// (its band filter compacts one warp's ballot).
+constexpr int kStageA = 24;
+constexpr size_t kRawBytesTMA_A = kStageA * 96;
 // Shell bands: K <= kTableRows runs k_accumulate with a K-row table; larger K runs
 // k_accumulate_band, one pass per band of kBandRows shells over the records meeting
 // it (DESIGN.md §6 a6).  48 rows (3 bands at K = 128) leave 12 CTAs/SM (the register
@@ -439,10 +446,10 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(  // 11 CTAs/SM at K = 
     uint32_t* unit_counter, float* __restrict__ atlas, unsigned long long* __restrict__ stats,
     const uint64_t* __restrict__ slab_mask, const int2* __restrict__ slab_k) {
     extern __shared__ __align__(128) unsigned char acc_smem[];
-    constexpr size_t kRawBytes = kTMA ? kRawBytesTMA : 0;
-    PairRec* s_raw = reinterpret_cast<PairRec*>(acc_smem);                                   // [kStage] (TMA)
-    float4* s_cr = reinterpret_cast<float4*>(acc_smem + kRawBytes);                          // [kStage][5]
-    float* s_acc = reinterpret_cast<float*>(acc_smem + kRawBytes + kStage * kCompact * sizeof(float4));  // [K][64]
+    constexpr size_t kRawBytes = kTMA ? kRawBytesTMA_A : 0;
+    PairRec* s_raw = reinterpret_cast<PairRec*>(acc_smem);                                   // [kStageA] (TMA)
+    float4* s_cr = reinterpret_cast<float4*>(acc_smem + kRawBytes);                          // [kStageA][5]
+    float* s_acc = reinterpret_cast<float*>(acc_smem + kRawBytes + kStageA * kCompact * sizeof(float4));  // [K][64]
     __shared__ __align__(8) uint64_t s_bar;
     __shared__ uint32_t s_unit, s_last;
 
@@ -484,12 +491,12 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(  // 11 CTAs/SM at K = 
 
         const float dt = al.dt[l], dtlo = al.dtlo[l], idt = al.idt[l];
         const uint32_t n_rec = wu.jend - wu.jbeg;
-        const uint32_t n_batches = (n_rec + kStage - 1) / kStage;
+        const uint32_t n_batches = (n_rec + kStageA - 1) / kStageA;
         const PairRec* lrecs = recs + (int64_t)l * n;
 
         auto issue = [&](uint32_t b) {  // TMA: bulk copies of the stage's records into s_raw
-            const uint32_t j0 = wu.jbeg + b * kStage;
-            const uint32_t nb = min((uint32_t)kStage, wu.jend - j0);
+            const uint32_t j0 = wu.jbeg + b * kStageA;
+            const uint32_t nb = min((uint32_t)kStageA, wu.jend - j0);
             if (tid == 0) mbar_arrive_expect_tx(&s_bar, nb * (uint32_t)sizeof(PairRec));
             if ((uint32_t)tid < nb) {
                 const uint32_t gi = vals[j0 + tid];
@@ -500,8 +507,8 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(  // 11 CTAs/SM at K = 
         // loads issued before the current stage's compute)
         uint4 ru[6];  // PairRec as six 16-B words (no union: the loads land in place)
         auto fetch = [&](uint32_t b) {
-            const uint32_t j0 = wu.jbeg + b * kStage;
-            if ((uint32_t)tid < min((uint32_t)kStage, wu.jend - j0)) {
+            const uint32_t j0 = wu.jbeg + b * kStageA;
+            if ((uint32_t)tid < min((uint32_t)kStageA, wu.jend - j0)) {
                 const uint4* src = reinterpret_cast<const uint4*>(lrecs + vals[j0 + tid]);
 #pragma unroll
                 for (int k = 0; k < 6; ++k) ru[k] = __ldg(src + k);
@@ -516,7 +523,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(  // 11 CTAs/SM at K = 
                 mbar_wait(&s_bar, phase);
                 phase ^= 1u;
             }
-            const uint32_t nb = min((uint32_t)kStage, n_rec - b * kStage);
+            const uint32_t nb = min((uint32_t)kStageA, n_rec - b * kStageA);
             if ((uint32_t)tid < nb) {  // transform: raw record -> compact, relative to d_c
                 float* q = reinterpret_cast<float*>(s_cr) + (tid >> 1) * (2 * kPairFields) + (tid & 1);
                 float v[kPairFields];
@@ -1099,6 +1106,8 @@ int accumulate_rows(int K) {
 
 size_t accumulate_smem_bytes(int K, bool tma) {
     const int rows = accumulate_rows(K);
+    if (rows == K)  // single-table kernel
+        return (tma ? kRawBytesTMA_A : 0) + kStageA * kCompact * sizeof(float4) + (size_t)K * kThreads * sizeof(float);
     return (tma ? kRawBytesTMA : 0) + kStage * kCompact * sizeof(float4) +
            (size_t)(rows < K ? rows + 2 : rows) * kThreads * sizeof(float);  // (+2 dump rows with bands)
 }
@@ -1153,8 +1162,8 @@ void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint3
         dev_cached = dev;
         cached_K = K;
     }
-    // TMA staging unless its raw buffer costs a CTA per SM (K = 64 on sm_100: 10 vs 11 CTAs;
-    // register staging measured 0.936 vs 0.998 ms on cfg2)
+    // TMA staging unless its raw buffer costs a CTA per SM (K = 64 on sm_100: 10 vs 12 CTAs;
+    // register staging measured 0.917 vs 0.998 ms on cfg2; ncu: profiles/r02_k_accumulate_cfg2_tma.md)
     bool tma = per_sm_tma >= per_sm_reg;
     if (const char* f = getenv("DGSM_ACC_STAGING")) {  // tests: force "tma" or "reg"
         if (!strcmp(f, "tma")) tma = true;
