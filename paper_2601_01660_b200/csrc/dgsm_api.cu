@@ -463,7 +463,8 @@ struct Sorted {
 };
 
 static Sorted run_binning(const dgsm_gaussians_t* g, const dgsm_build_opts_t& o, const RunShape& sh,
-                          const PlanLayout& p, const RunLayout& r, dgsm_build_status_t* status, cudaStream_t s) {
+                          const PlanLayout& p, const RunLayout& r, dgsm_build_status_t* status, cudaStream_t s,
+                          const int64_t* key_begin_host = nullptr) {
     const int res = sh.res;
     const int64_t n = g->n;
     const int64_t n_tiles = (int64_t)(res / kTile) * (res / kTile);
@@ -501,9 +502,31 @@ static Sorted run_binning(const dgsm_gaussians_t* g, const dgsm_build_opts_t& o,
                                 (uint32_t)l << sh.tile_bits, tm, r.keys_a, r.vals_a, s);
         g_launches += kScanLaunches + 1;
     }
-    // 4. one stable sort of the (light | tile) digits of all keys (grid: the capacity)
-    const int ft = launch_onesweep_u32(r.keys_a, r.vals_a, r.keys_b, r.vals_b, sh.cap, sh.light_bits + sh.tile_bits,
-                                       r.sort_temp, s, &g_launches, nullptr, nullptr, false, true, r.n_keys);
+    // 4. one stable sort of the (light | tile) digits of all keys (grid: the capacity),
+    //    or — when the per-light key segments are known on the host (the planned build)
+    //    and it saves a pass (cfg5: 3 + 16 bits = 3 passes, 16 bits = 2) — one sort of
+    //    the tile digits per light segment (the keys are emitted grouped by light)
+    const int tb = sh.tile_bits;
+    int ft;
+    if (key_begin_host && sh.n_lights > 1 && (tb + 7) / 8 < (sh.light_bits + tb + 7) / 8) {
+        const int target = onesweep_digits(tb).passes & 1;  // where a sorted segment of > 1 key ends
+        for (int l = 0; l < sh.n_lights; ++l) {
+            const int64_t b = key_begin_host[l], nl = key_begin_host[l + 1] - key_begin_host[l];
+            if (nl <= 0) continue;
+            const int fl = launch_onesweep_u32(r.keys_a + b, r.vals_a + b, r.keys_b + b, r.vals_b + b, nl, tb,
+                                               r.sort_temp, s, &g_launches);
+            if (fl != target) {  // (a segment of one key: no pass ran)
+                cudaMemcpyAsync((target ? r.keys_b : r.keys_a) + b, (fl ? r.keys_b : r.keys_a) + b, 4 * nl,
+                                cudaMemcpyDeviceToDevice, s);
+                cudaMemcpyAsync((target ? r.vals_b : r.vals_a) + b, (fl ? r.vals_b : r.vals_a) + b, 4 * nl,
+                                cudaMemcpyDeviceToDevice, s);
+            }
+        }
+        ft = target;
+    } else {
+        ft = launch_onesweep_u32(r.keys_a, r.vals_a, r.keys_b, r.vals_b, sh.cap, sh.light_bits + tb, r.sort_temp, s,
+                                 &g_launches, nullptr, nullptr, false, true, r.n_keys);
+    }
     Sorted out{ft ? r.keys_b : r.keys_a, ft ? r.vals_b : r.vals_a};
     // 5. tile ranges
     launch_ranges(out.keys, r.n_keys, sh.cap, sh.tile_bits, (uint32_t)n_tiles, r.tile_start, r.tile_end, s);
@@ -542,7 +565,7 @@ int dgsm_build_run(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n_
     const PlanLayout p = plan_layout(plan_ws, g->n, n_lights);
     const RunLayout r = run_layout(run_ws, sh);
     cudaMemsetAsync(r.counters, 0, sizeof(uint32_t) * r.zero_words, s);
-    const Sorted so = run_binning(g, o, sh, p, r, nullptr, s);
+    const Sorted so = run_binning(g, o, sh, p, r, nullptr, s, plan->light_key_begin);
     run_accumulate(g, lights, o, sh, p, r, so, atlas_out, s);
     return cuda_check("build run");
 }
@@ -566,7 +589,7 @@ int dgsm_build_bins(const dgsm_gaussians_t* g, const dgsm_light_t* lights, int n
     const int res = plan->atlas_res;
     const int64_t nt = n_lights * (int64_t)(res / kTile) * (res / kTile);
     cudaMemsetAsync(r.counters, 0, sizeof(uint32_t) * r.zero_words, s);
-    const Sorted so = run_binning(g, o, sh, p, r, nullptr, s);
+    const Sorted so = run_binning(g, o, sh, p, r, nullptr, s, plan->light_key_begin);
     launch_decode_keys(so.keys, so.vals, p.dup, *plan, light_out, tile_out, depth_bits_out, index_out, s);
     g_launches += 1;
     if (tile_start_out) cudaMemcpyAsync(tile_start_out, r.tile_start, sizeof(uint32_t) * nt, cudaMemcpyDeviceToDevice, s);

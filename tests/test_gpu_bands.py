@@ -114,3 +114,26 @@ def test_band_rows_override(dg, oracle_mod, tmp_path, rows, K):
     s = synth.random_scene(81, 1500, res=32, K=K, L=2, dist=(0.3, 3.0), scale=(0.01, 0.5))
     To, _ = oracle_mod.build(s.gaussians, s.lights, s.res, s.K)
     assert np.abs(T - To).max() <= TOL_T
+
+
+def _near_light_scene(K):
+    """Gaussians at / within 1e-7 of / 2 cm from the light (an excluded pair, a
+    footprint over the whole atlas, shell bounds clamped at shell 0) and large
+    Gaussians 0.1-1 m from it (windows over many bands)."""
+    s = synth.random_scene(13, 60, res=64, K=K, dist=(0.1, 1.0), scale=(0.05, 0.8))
+    o = s.lights["position"][0].astype(np.float32)
+    extra = np.stack([o, o + np.float32(1e-7), o + np.array([0.02, 0.0, 0.0], np.float32)])
+    g = dict(s.gaussians)
+    g["means"] = np.concatenate([g["means"], extra]).astype(np.float32)
+    g["scales"] = np.concatenate([g["scales"], np.full((3, 3), 0.05, np.float32)])
+    g["rotations"] = np.concatenate([g["rotations"], np.tile(np.array([1, 0, 0, 0], np.float32), (3, 1))])
+    g["opacities"] = np.concatenate([g["opacities"], np.full(3, 0.5, np.float32)])
+    return synth.Scene("near-light", g, s.lights, s.res, s.K, s.queries)
+
+
+@pytest.mark.parametrize("K", [97, 160])
+def test_band_near_light_and_big_footprints(dg, oracle_mod, K):
+    s = _near_light_scene(K)
+    T = dg.build(dg.to_device(s.gaussians), s.lights, s.res, s.K).cpu().numpy()
+    To, _ = oracle_mod.build(s.gaussians, s.lights, s.res, s.K)
+    assert np.abs(T - To).max() <= TOL_T
