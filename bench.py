@@ -69,6 +69,8 @@ def parse():
     ap.add_argument("--no-transfer", action="store_true", help="skip the NEXT-4 transfer timing")
     ap.add_argument("--no-strong", action="store_true", help="skip the cfg5 strong-scaling sub-record")
     ap.add_argument("--no-sequence", action="store_true", help="skip the cfg4 120-frame sequence sub-record")
+    ap.add_argument("--no-graph", action="store_true", help="time the cfg1/2/4 step as stream launches "
+                                                             "instead of a CUDA graph replay")
     ap.add_argument("--layout", default="auto", choices=["auto", "light", "shells", "gaussian"],
                     help="multi-GPU layout of cfg3/cfg5 (distributed.plan_layout)")
     return ap.parse_args()
@@ -348,7 +350,7 @@ def fp32_peak(ctx):
     return ctx.n_sm * 128 * sm_mhz * 1e6 / 1e12, f"{ctx.n_sm} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (FMA = 1 op)"
 
 
-def time_steps(step, K: int, warmup: int, ctx, sample_clocks: bool = True):
+def time_steps(step, K: int, warmup: int, ctx, sample_clocks: bool = True, acc_events: bool = True):
     """W untimed warm-up steps, then EXACTLY K timed steps, each after an L2 flush
     (outside the step's events), bracketed by barrier + synchronize; device time
     by CUDA events on the launching stream; the accumulation kernel's events are
@@ -374,7 +376,8 @@ def time_steps(step, K: int, warmup: int, ctx, sample_clocks: bool = True):
     for i in range(K):
         e0, ea, eb, e1 = ev[i]
         ctx.flush.zero_()
-        dgsm.set_accumulate_events(ea, eb)
+        if acc_events:
+            dgsm.set_accumulate_events(ea, eb)
         e0.record()
         launches += step()
         e1.record()
@@ -384,7 +387,7 @@ def time_steps(step, K: int, warmup: int, ctx, sample_clocks: bool = True):
     ctx.barrier()
     clocks = sampler.stop(wall0, wall1) if sample_clocks else None
     t_step = [ev[i][0].elapsed_time(ev[i][3]) for i in range(K)]
-    t_acc = [ev[i][1].elapsed_time(ev[i][2]) for i in range(K)]
+    t_acc = [ev[i][1].elapsed_time(ev[i][2]) for i in range(K)] if acc_events else None
     return {"t_step": t_step, "t_acc": t_acc, "launches": launches, "wall_ms": (wall1 - wall0) * 1e3,
             "clocks": clocks}
 
@@ -492,7 +495,33 @@ def weak_bench(args, ctx):
         dgsm.query(atlas, s.lights, xq, out=T_out)
         return nl + dgsm.last_launch_count()
 
-    r = time_steps(step, args.steps, args.warmup, ctx)
+    # stream launches: the accumulation kernel's duration per step (library events)
+    r = time_steps(step, args.steps, args.warmup, ctx, sample_clocks=args.no_graph)
+    launch_mode = "stream launches"
+    r_stream_ms = float(np.mean(r["t_step"]))
+    if not args.no_graph:
+        # the step as a renderer runs it every frame: the sync-free build + query captured
+        # once in a CUDA graph and replayed (same 21 kernels, same inputs in HBM; only the
+        # host launch overhead and inter-kernel gaps go), L2 flushed before every replay
+        gs = torch.cuda.Stream(ctx.dev)
+        gs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(gs):
+            step()
+        torch.cuda.current_stream().wait_stream(gs)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            step()
+        per_step = r["launches"] // args.steps
+
+        def replay():
+            graph.replay()
+            return per_step
+
+        t_acc = r["t_acc"]
+        r = time_steps(replay, args.steps, args.warmup, ctx, acc_events=False)
+        r["t_acc"] = t_acc
+        launch_mode = "one CUDA graph replay per step (captured once from the stream-launched step)"
     bst = builder.status()
     if bst["overflow"] or bst["n_keys"] != P:
         sys.exit(f"bench.py: sync-free build status {bst} (expected {P} keys)")
@@ -557,6 +586,7 @@ def weak_bench(args, ctx):
                        build=f"dgsm_build_async (no host sync), key capacity {cap} (1.25 P); status checked",
                        receivers=("scene receivers stored in Morton order (dgsm_receiver_order, once per scene: "
                                   f"{order_ms * 1e3:.0f} us)")),
+        "launch_mode": launch_mode, "ms_per_step_stream_launches": r_stream_ms,
         "step_ms_each": [round(x, 3) for x in r["t_step"]], "step_ms_median": float(np.median(r["t_step"])),
         "wall_ms_per_step_incl_flush": r["wall_ms"] / K,
         "accumulate_ms": acc_ms, "accumulate_share": acc_ms / float(np.mean(r["t_step"])),

@@ -61,6 +61,8 @@ def test_product_arm_line():
         assert k in d, k
     assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0
     assert d["gpu_launches"] > 0 and d["dtype"] == "f32"
+    # the step is timed as a CUDA-graph replay; the stream-launched step is reported beside it
+    assert "graph" in d["launch_mode"] and d["ms_per_step_stream_launches"] > 0
     rf = d["roofline"]
     assert rf["bound"] in ("hbm", "tensor", "alu") and rf["peak"] > 0 and abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
     e = d["e2e"]
