@@ -63,3 +63,30 @@ def test_sweep(dg, oracle_mod, monkeypatch, seed, n, res, K, L, staging):
         st = ab.status()
         assert st["n_keys"] == plan.n_keys and not st["overflow"]
         assert np.abs(out.cpu().numpy() - To).max() <= TOL_T
+
+
+def test_sweep_slab_per_light_sort(dg, oracle_mod):
+    """ROI slab at res 128 with 3 lights (the per-light tile sort over the
+    slab-restricted key segments): binning = the oracle's entries on the active
+    tiles, the slab build <= 1e-4 against the oracle's slab build."""
+    s = synth.random_scene(131, 1200, res=128, K=20, L=3, dist=(0.3, 3.0), scale=(0.01, 0.4))
+    rng = np.random.default_rng(131)
+    rec = rng.uniform(-3, 3, (2000, 3)).astype(np.float32)
+    roi = (0.2, -0.1, 0.3, 1.0, -0.8, 0.9)
+    slab = dg.active_slab(torch.from_numpy(rec).cuda(), roi, s.lights, s.res, s.K)
+    g = dg.to_device(s.gaussians)
+    T = dg.build(g, s.lights, s.res, s.K, dg.Options(slab=slab)).cpu().numpy()
+    mask, kr, inside = oracle_mod.active_slab(rec, roi, s.lights, s.res, s.K)
+    assert inside > 0
+    To, _ = oracle_mod.build(s.gaussians, s.lights, s.res, s.K, slab=(mask, kr))
+    assert np.abs(T - To).max() <= TOL_T
+    plan = dg.BuildPlan(g, s.lights, s.res, s.K, dg.Options(slab=slab))
+    (l, t, d, i), _ = plan.bins()
+    want = oracle_mod.bin_entries(s.gaussians["means"], s.gaussians["scales"], s.gaussians["rotations"],
+                                  s.lights["position"], s.res)
+    tile_on = mask.reshape(s.L, s.res // 8, 8, s.res // 8, 8).any(axis=(2, 4)).reshape(s.L, -1)
+    keep = tile_on[want[0].astype(np.int64), want[1].astype(np.int64)]
+    want = [w[keep] for w in want]
+    assert plan.n_keys == len(want[0]) and 0 < plan.n_keys
+    for a, b in zip((l, t, d, i), want):
+        assert np.array_equal(a.cpu().numpy().astype(np.uint32), b)
