@@ -460,6 +460,14 @@ int dgsm_build_stats(const dgsm_plan_t* plan, void* run_ws, size_t run_ws_bytes,
  * disables.  Always returns DGSM_OK. */
 int dgsm_set_accumulate_events(void* before, void* after);
 
+/* Frame pipelining: a caller-owned cudaEvent_t (as void*) that subsequent builds on
+ * this thread record on their stream right before the work units and the
+ * accumulation (a5/a6), with cudaEventRecordExternal: captured in a CUDA graph it is
+ * an event-record node, so a copy stream can start the next frame's uploads when this
+ * frame's FP32-bound accumulation starts (dgsm.FrameStream).  NULL disables.  Always
+ * returns DGSM_OK. */
+int dgsm_set_frame_event(void* ev);
+
 /* Message for a status code / for the last failure on the calling thread. */
 const char* dgsm_strerror(int code);
 const char* dgsm_last_error(void);

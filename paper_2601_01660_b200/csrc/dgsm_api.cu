@@ -17,6 +17,9 @@ thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;
 // dgsm_frame_host: recorded on the build stream right before the accumulation
 // (a5/a6) of the frame being enqueued (nullptr: not recorded)
 thread_local cudaEvent_t g_ev_frame_acc = nullptr;
+// dgsm_set_frame_event: a caller event recorded (as an external event: a record node
+// when the build is captured in a CUDA graph) right before the accumulation
+thread_local cudaEvent_t g_ev_frame_ext = nullptr;
 
 int fail(int code, const char* fmt, ...) {
     va_list ap;
@@ -541,6 +544,7 @@ static void run_accumulate(const dgsm_gaussians_t* g, const dgsm_light_t* lights
     const LightsParam lp = lights_param(lights, sh.n_lights);
     const int64_t nt = sh.n_lights * (int64_t)(sh.res / kTile) * (sh.res / kTile);
     if (g_ev_frame_acc) cudaEventRecord(g_ev_frame_acc, s);
+    if (g_ev_frame_ext) cudaEventRecordWithFlags(g_ev_frame_ext, s, cudaEventRecordExternal);
     launch_units(r.tile_start, r.tile_end, nt, sh.chunk, r.unit_cnt, r.unit_off, r.unit_scan_temp, r.units_tmp,
                  r.units, r.max_units, r.counters, r.counters + 8, r.counters + 8 + kUnitClasses, r.deferred,
                  r.counters + 2, s, &g_launches);
@@ -976,6 +980,11 @@ int dgsm_sort_pairs_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint
     *result_in_alt = launch_onesweep_u32(keys, vals, keys_alt, vals_alt, n, nbits, temp, (cudaStream_t)stream,
                                          &g_launches);
     return cuda_check("sort");
+}
+
+int dgsm_set_frame_event(void* ev) {
+    g_ev_frame_ext = (cudaEvent_t)ev;
+    return DGSM_OK;
 }
 
 int dgsm_set_accumulate_events(void* before, void* after) {

@@ -37,7 +37,8 @@ EXPORTED = ["dgsm_default_opts", "dgsm_plan_workspace_bytes", "dgsm_build_plan",
             "dgsm_slab_bytes", "dgsm_active_slab", "dgsm_frame_host", "dgsm_default_transfer_opts",
             "dgsm_transfer_workspace_bytes", "dgsm_sh_transfer", "dgsm_sort_temp_bytes", "dgsm_sort_pairs_u32",
             "dgsm_order_workspace_bytes", "dgsm_receiver_order", "dgsm_query_ordered", "dgsm_query_chunks",
-            "dgsm_query_combine", "dgsm_async_workspace_bytes", "dgsm_build_async", "dgsm_footprint_stencil"]
+            "dgsm_query_combine", "dgsm_async_workspace_bytes", "dgsm_build_async", "dgsm_footprint_stencil",
+            "dgsm_set_frame_event"]
 
 
 class Gaussians(C.Structure):
@@ -162,6 +163,8 @@ def lib() -> C.CDLL:
         L.dgsm_build_stats.restype = C.c_int
         L.dgsm_set_accumulate_events.argtypes = [vp, vp]
         L.dgsm_set_accumulate_events.restype = C.c_int
+        L.dgsm_set_frame_event.argtypes = [vp]
+        L.dgsm_set_frame_event.restype = C.c_int
         for f in ("dgsm_build_plan", "dgsm_build_run", "dgsm_build_bins", "dgsm_build",
                   "dgsm_exp_epilogue", "dgsm_query", "dgsm_query_footprint"):
             getattr(L, f).restype = C.c_int
@@ -607,6 +610,112 @@ class FrameHost:
         _check(rc, "dgsm_frame_host")
         self.launches = last_launch_count()
         return self.atlas
+
+
+class FrameStream:
+    """Frames back to back from HOST tensors (a renderer's frame loop): per frame the
+    occluders and receivers go up on a copy stream into one of two device buffer
+    sets, the sync-free build (dgsm_build_async, `key_capacity` keys) and the query
+    run as ONE CUDA-graph replay (one graph per buffer set, captured on first use),
+    and T comes back on a second copy stream from one of two device buffers.  Frame
+    i+1's receivers go up as soon as its buffer set is free, its Gaussians when frame
+    i's accumulation starts (dgsm_set_frame_event: an external event recorded inside
+    the graph), so the bulk of the upload overlaps the FP32-bound a6 kernel instead of
+    the L2-resident sorts.  Pinned host tensors give the overlap.
+
+    The call returns an event: T_host is complete once it has (``wait()`` waits for
+    every frame issued); the atlas of the latest frame is ``atlas``.  ``status()``
+    is the sync-free build's status of the latest frame (key overflow)."""
+
+    def __init__(self, lights, atlas_res: int, n_shells: int, n: int, m: int, key_capacity: int,
+                 opts: Optional[Options] = None, device="cuda"):
+        self.lights, self.n_lights = _lights(lights)
+        self._lights_arg = lights
+        self.res, self.K, self.n, self.m = int(atlas_res), int(n_shells), int(n), int(m)
+        self.device = torch.device(device)
+        self.builder = AsyncBuilder(lights, atlas_res, n_shells, n, key_capacity, opts, device)
+        dev = self.device
+        shapes = {"means": (n, 3), "scales": (n, 3), "rotations": (n, 4), "opacities": (n,)}
+        self.bufs = [({k: torch.empty(v, dtype=torch.float32, device=dev) for k, v in shapes.items()},
+                      torch.empty((m, 3), dtype=torch.float32, device=dev)) for _ in range(2)]
+        self.Tdev = [torch.empty(m, dtype=torch.float32, device=dev) for _ in range(2)]
+        self.atlas = torch.empty((self.n_lights, self.K, self.res, self.res), dtype=torch.float32, device=dev)
+        self.up, self.down = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        self.ev_acc = [torch.cuda.Event(external=True) for _ in range(2)]
+        self.ev_up, self.ev_used, self.ev_down = ([torch.cuda.Event() for _ in range(2)] for _ in range(3))
+        cur = torch.cuda.current_stream(dev)
+        for e in self.ev_acc + self.ev_up + self.ev_used + self.ev_down:
+            e.record(cur)
+        self.graphs = [None, None]
+        self.frame = 0
+        self.launches = 0
+
+    def _frame_body(self, k):
+        g, x = self.bufs[k]
+        self.builder(g, self.atlas)
+        nl = self.builder.launches
+        query(self.atlas, self._lights_arg, x, out=self.Tdev[k])
+        return nl + last_launch_count()
+
+    def _capture(self, k):
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            self.launches = self._frame_body(k)  # warm-up run (also counts the kernels)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        lib().dgsm_set_frame_event(C.c_void_p(self.ev_acc[k].cuda_event))
+        try:
+            with torch.cuda.graph(graph, stream=side):
+                self._frame_body(k)
+        finally:
+            lib().dgsm_set_frame_event(None)
+        self.graphs[k] = graph
+
+    def __call__(self, g_host: Dict[str, torch.Tensor], receivers_host: torch.Tensor,
+                 T_host: torch.Tensor) -> torch.cuda.Event:
+        for name, shp in (("means", (self.n, 3)), ("scales", (self.n, 3)), ("rotations", (self.n, 4))):
+            a = g_host[name]
+            if a.is_cuda or a.dtype != torch.float32 or tuple(a.shape) != shp or not a.is_contiguous():
+                raise DgsmError(f"{name} must be a contiguous float32 CPU tensor of shape {shp}")
+        op = g_host["opacities"]
+        if op.is_cuda or op.dtype != torch.float32 or op.numel() != self.n or not op.is_contiguous():
+            raise DgsmError(f"opacities must be a contiguous float32 CPU tensor of {self.n} values")
+        if receivers_host.is_cuda or tuple(receivers_host.shape) != (self.m, 3) or receivers_host.dtype != torch.float32:
+            raise DgsmError(f"receivers must be a float32 CPU tensor of shape ({self.m}, 3)")
+        if T_host.is_cuda or T_host.dtype != torch.float32 or T_host.numel() < self.m:
+            raise DgsmError(f"T_host must be a float32 CPU tensor of at least {self.m} values")
+        k = self.frame & 1
+        self.frame += 1
+        cur = torch.cuda.current_stream(self.device)
+        g, x = self.bufs[k]
+        self.up.wait_event(self.ev_used[k])       # graph k's last replay has read buffer set k
+        with torch.cuda.stream(self.up):          # the receivers first (12 B each, read last)
+            x.copy_(receivers_host, non_blocking=True)
+        self.up.wait_event(self.ev_acc[1 - k])    # the previous frame's accumulation has started
+        with torch.cuda.stream(self.up):
+            for name in ("means", "scales", "rotations", "opacities"):
+                g[name].copy_(g_host[name].reshape(g[name].shape), non_blocking=True)
+            self.ev_up[k].record(self.up)
+        cur.wait_event(self.ev_up[k])
+        cur.wait_event(self.ev_down[k])            # T buffer k has been copied out
+        if self.graphs[k] is None:                 # first use of buffer set k: capture (on its data)
+            self._capture(k)
+        self.graphs[k].replay()
+        self.ev_used[k].record(cur)
+        self.down.wait_event(self.ev_used[k])
+        with torch.cuda.stream(self.down):
+            T_host[:self.m].copy_(self.Tdev[k], non_blocking=True)
+            self.ev_down[k].record(self.down)
+        return self.ev_down[k]
+
+    def wait(self):
+        """Block until every issued frame's T_host is complete."""
+        for e in self.ev_down:
+            e.synchronize()
+
+    def status(self) -> dict:
+        return self.builder.status()
 
 
 def active_slab(receivers: torch.Tensor, roi, lights, atlas_res: int, n_shells: int,
