@@ -334,14 +334,16 @@ __global__ void __launch_bounds__(kFusedThreads) k_units_fused(const uint32_t* _
     if (tid < kUnitClasses) { s_class[tid] = 0u; s_fill[tid] = 0u; }
     if (tid == 0) s_slots = 0u;
     __syncthreads();
+    // A tile's units: nfull full chunks (one size class) and, when the length is not a
+    // multiple of the chunk (or the tile is empty: one empty unit, T = 1), a last one.
+    // Each class counter takes one atomic per tile and kind, not one per unit (a dense
+    // tile of an avatar close to the light has ~30 units of one class).
+    const uint32_t cls_full = (uint32_t)unit_class((uint32_t)chunk);
     for (int64_t t = tid; t < nt; t += kFusedThreads) {
         const uint32_t len = te[t] - ts[t];
-        uint32_t c = (len + chunk - 1) / chunk;
-        if (c == 0) c = 1;
-        for (uint32_t k = 0; k < c; ++k) {  // the sizes pass 2 gives these units
-            const uint32_t jb = min(k * (uint32_t)chunk, len), je = min(len, k * (uint32_t)chunk + (uint32_t)chunk);
-            atomicAdd(&s_class[unit_class(je - jb)], (uint32_t)kTileSplit);
-        }
+        const uint32_t nfull = len / (uint32_t)chunk, rem = len - nfull * (uint32_t)chunk;
+        if (nfull) atomicAdd(&s_class[cls_full], nfull * (uint32_t)kTileSplit);
+        if (rem || len == 0) atomicAdd(&s_class[unit_class(rem)], (uint32_t)kTileSplit);
     }
     __syncthreads();
     if (tid == 0) {  // class bases, largest class first: s_class becomes the base
@@ -352,9 +354,13 @@ __global__ void __launch_bounds__(kFusedThreads) k_units_fused(const uint32_t* _
     __syncthreads();
     for (int64_t t = tid; t < nt; t += kFusedThreads) {
         const uint32_t s = ts[t], e = te[t], len = e - s;
-        uint32_t nc = (len + chunk - 1) / chunk;
-        if (nc == 0) nc = 1;
+        const uint32_t nfull = len / (uint32_t)chunk, rem = len - nfull * (uint32_t)chunk;
+        const bool last = rem || len == 0;
+        const uint32_t nc = nfull + (last ? 1u : 0u);
         const uint32_t slot = nc > 1 ? atomicAdd(&s_slots, nc * kTileSplit) : 0u;
+        const uint32_t pos_full = nfull ? s_class[cls_full] + atomicAdd(&s_fill[cls_full], nfull * (uint32_t)kTileSplit) : 0u;
+        const int cls_last = unit_class(rem);
+        const uint32_t pos_last = last ? s_class[cls_last] + atomicAdd(&s_fill[cls_last], (uint32_t)kTileSplit) : 0u;
         for (uint32_t part = 0; part < (uint32_t)kTileSplit; ++part)
             for (uint32_t c = 0; c < nc; ++c) {
                 WorkUnit w;
@@ -367,8 +373,7 @@ __global__ void __launch_bounds__(kFusedThreads) k_units_fused(const uint32_t* _
                 w.slot = slot + part * nc;
                 w.part = part;
                 w.pad1 = 0;
-                const int cls = unit_class(w.jend - w.jbeg);
-                const uint32_t pos = s_class[cls] + atomicAdd(&s_fill[cls], 1u);
+                const uint32_t pos = c < nfull ? pos_full + part * nfull + c : pos_last + part;
                 units[pos] = w;
                 if (c == 0 && part == 0 && nc > kInlineCombine) deferred[atomicAdd(deferred_count, 1u)] = pos;
             }
