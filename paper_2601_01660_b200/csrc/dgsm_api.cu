@@ -37,8 +37,14 @@ int cuda_check(const char* where) {
 
 constexpr size_t kAlign = 256;
 constexpr int kChunk = 1024;  // Gaussians per accumulation work unit (512, 768, 1536, 2048 measured slower on cfg2)
-constexpr int kMinChunk = 128;
-constexpr int64_t kMinUnits = 2048;
+#ifndef DGSM_MIN_CHUNK
+#define DGSM_MIN_CHUNK 128
+#endif
+#ifndef DGSM_MIN_UNITS
+#define DGSM_MIN_UNITS 2048
+#endif
+constexpr int kMinChunk = DGSM_MIN_CHUNK;
+constexpr int64_t kMinUnits = DGSM_MIN_UNITS;
 constexpr int kCounterWords = 8 + 2 * kUnitClasses;  // n_units, unit counter, class histogram + fill
 
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
