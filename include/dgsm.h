@@ -76,8 +76,6 @@ typedef struct dgsm_build_stats {
     uint64_t warp_live_max; /* sum over (warp, stage) of the max live count of one lane */
     uint64_t band_records;  /* records run through the pair tests, summed over the shell bands
                                (K > 64: a record meeting two bands counts twice; else = P) */
-    uint64_t warp_tested;   /* (warp, record) pair tests actually run after the half-tile cull
-                               (<= warp_records; DESIGN.md §6 a6) */
 } dgsm_build_stats_t;
 
 /* Occluder Gaussians, structure of arrays, DEVICE pointers (mean mu_i,

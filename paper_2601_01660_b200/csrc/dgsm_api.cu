@@ -135,7 +135,7 @@ struct RunLayout {
     int64_t zero_words;  // counters .. tile_end, cleared by one memset per run
     uint32_t* tile_arrive;
     uint64_t* n_keys;    // device: the run's key count (P, or 0 on overflow)
-    unsigned long long* stats;  // [9] dgsm_build_stats_t words (DGSM_COLLECT_STATS)
+    unsigned long long* stats;  // [8] dgsm_build_stats_t words (DGSM_COLLECT_STATS)
     float* scratch;
     size_t bytes;
     uint32_t max_units;
@@ -175,7 +175,7 @@ RunLayout run_layout(void* ws, const RunShape& sh) {
     r.tile_end = r.tile_start + nt;
     r.zero_words = kCounterWords + (kTileSplit + 2) * nt;
     r.n_keys = c.take<uint64_t>(2);
-    r.stats = c.take<unsigned long long>(9);
+    r.stats = c.take<unsigned long long>(8);
     const int64_t max_slots = kTileSplit * (2 * (P / sh.chunk) + 1);
     r.scratch = c.take<float>((size_t)max_slots * sh.K * (kTexels / kTileSplit));
     r.bytes = c.off;
@@ -554,7 +554,7 @@ static void run_accumulate(const dgsm_gaussians_t* g, const dgsm_light_t* lights
     launch_units(r.tile_start, r.tile_end, nt, sh.chunk, r.unit_cnt, r.unit_off, r.unit_scan_temp, r.units_tmp,
                  r.units, r.max_units, r.counters, r.counters + 8, r.counters + 8 + kUnitClasses, r.deferred,
                  r.counters + 2, s, &g_launches);
-    if (o.flags & DGSM_COLLECT_STATS) cudaMemsetAsync(r.stats, 0, sizeof(unsigned long long) * 9, s);
+    if (o.flags & DGSM_COLLECT_STATS) cudaMemsetAsync(r.stats, 0, sizeof(unsigned long long) * 8, s);
     launch_accumulate(r.units, r.counters, r.max_units, so.vals, p.recs, g->n, lp, sh.n_lights, sh.res, sh.K,
                       o.flags, r.scratch, r.tile_arrive, r.counters + 1, atlas_out, r.stats, slab_mask_ptr(o.slab),
                       slab_k_ptr(o.slab, sh.n_lights, sh.res), r.deferred, r.counters + 2, g_ev_before, g_ev_after, s);
@@ -1004,7 +1004,7 @@ int dgsm_build_stats(const dgsm_plan_t* plan, void* run_ws, size_t run_ws_bytes,
     if (!plan || !run_ws || !out) return fail(DGSM_EINVAL, "null argument");
     if (run_ws_bytes < plan->run_workspace_bytes) return fail(DGSM_ENOSPC, "run workspace too small");
     const RunLayout r = run_layout(run_ws, plan_shape(*plan));
-    unsigned long long h[9];
+    unsigned long long h[8];
     cudaMemcpyAsync(h, r.stats, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
     if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return cuda_check("stats");
     out->pairs = h[0];
@@ -1015,7 +1015,6 @@ int dgsm_build_stats(const dgsm_plan_t* plan, void* run_ws, size_t run_ws_bytes,
     out->warp_live_any = h[5];
     out->warp_live_max = h[6];
     out->band_records = h[7];
-    out->warp_tested = h[8];
     return DGSM_OK;
 }
 

@@ -81,8 +81,7 @@ class BuildStatus(C.Structure):
 class BuildStats(C.Structure):
     _fields_ = [("pairs", C.c_uint64), ("pairs_live", C.c_uint64), ("window_shells", C.c_uint64),
                 ("steps", C.c_uint64), ("warp_records", C.c_uint64), ("warp_live_any", C.c_uint64),
-                ("warp_live_max", C.c_uint64), ("band_records", C.c_uint64),
-                ("warp_tested", C.c_uint64)]
+                ("warp_live_max", C.c_uint64), ("band_records", C.c_uint64)]
 
 
 class DgsmError(RuntimeError):
