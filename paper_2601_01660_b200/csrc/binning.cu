@@ -291,12 +291,28 @@ __global__ void __launch_bounds__(256) k_units_lpt(const WorkUnit* __restrict__ 
     }
     __syncthreads();
     const uint32_t n = *n_units;
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-        const WorkUnit w = in[j];
-        const int c = unit_class(w.jend - w.jbeg);
-        const uint32_t pos = s_base[c] + atomicAdd(&class_fill[c], 1u);
-        out[pos] = w;
-        if (w.chunk == 0 && w.part == 0 && w.nchunks > kInlineCombine) deferred[atomicAdd(deferred_count, 1u)] = pos;
+    // warp-aggregated class counters: most units share one class (full chunks), and one
+    // global atomic per unit on its counter serialised (cfg5: 174 us for ~200 K units)
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
+    for (uint32_t j0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); j0 < n; j0 += stride) {  // warp-uniform
+        const uint32_t j = j0 + lane;
+        WorkUnit w;
+        int c = -1;
+        if (j < n) {
+            w = in[j];
+            c = unit_class(w.jend - w.jbeg);
+        }
+        const uint32_t peers = __match_any_sync(0xffffffffu, c);
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0u;
+        if ((int)lane == leader && c >= 0) base = atomicAdd(&class_fill[c], (uint32_t)__popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (c >= 0) {
+            const uint32_t pos = s_base[c] + base + (uint32_t)__popc(peers & lt);
+            out[pos] = w;
+            if (w.chunk == 0 && w.part == 0 && w.nchunks > kInlineCombine) deferred[atomicAdd(deferred_count, 1u)] = pos;
+        }
     }
 }
 
@@ -322,7 +338,12 @@ __global__ void __launch_bounds__(256) k_decode(const uint32_t* __restrict__ key
 // a shared counter (slot positions are free: a tile's partials are combined in
 // chunk order from its own slots).  One launch instead of five.
 constexpr int kFusedThreads = 1024;
-constexpr int64_t kFusedTiles = 64 * kFusedThreads;
+// single-CTA builder up to 16 K (light, tile) pairs (cfg2/cfg4: 4 K); above, the
+// multi-kernel path: cfg3 (64 K) 9.14 -> 9.00 ms per step against the single CTA
+#ifndef DGSM_FUSED_TILES
+#define DGSM_FUSED_TILES (16 * 1024)
+#endif
+constexpr int64_t kFusedTiles = DGSM_FUSED_TILES;
 
 __global__ void __launch_bounds__(kFusedThreads) k_units_fused(const uint32_t* __restrict__ ts,
                                                                const uint32_t* __restrict__ te, int64_t nt,
