@@ -7,7 +7,7 @@ configuration bench.py times:
   61st (light, tile) within 1e-4;
 * a cfg5-shaped scene (the cfg5 hall at 10 % of its Gaussians: 2048^2 x 128,
   8 lights): 16-bit tile keys (two full 8-bit onesweep passes), 524 288
-  (light, tile) pairs (the multi-kernel work-unit builder above 64 K tiles),
+  (light, tile) pairs (the multi-kernel work-unit builder above 16 K tiles),
   K = 128 — binning bit-exact, the atlas on every 61st (light, tile) within 1e-4
   with both record stagings (TMA bulk copies and registers) forced;
 * the onesweep sort itself (a4) against numpy's stable argsort for key widths

@@ -514,7 +514,7 @@ def test_accumulate_staging_variants(dg, oracle_mod, staging, monkeypatch):
 
 
 def test_work_unit_paths_identical(dg, oracle_mod, monkeypatch):
-    """The single-CTA work-unit builder (<= 64 K tiles) and the multi-kernel one
+    """The single-CTA work-unit builder (<= 16 K tiles) and the multi-kernel one
     (larger atlases; forced here) give the same atlas, bit for bit, on a scene
     with multi-chunk tiles, some of them combined after the accumulation kernel
     (> 16 chunks), and it matches the oracle."""
