@@ -445,6 +445,7 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(  // 11 CTAs/SM at K = 
     int res, int K, uint32_t flags, float* __restrict__ scratch, uint32_t* tile_arrive,
     uint32_t* unit_counter, float* __restrict__ atlas, unsigned long long* __restrict__ stats,
     const uint64_t* __restrict__ slab_mask, const int2* __restrict__ slab_k) {
+    pdl_begin();
     extern __shared__ __align__(128) unsigned char acc_smem[];
     constexpr size_t kRawBytes = kTMA ? kRawBytesTMA_A : 0;
     PairRec* s_raw = reinterpret_cast<PairRec*>(acc_smem);                                   // [kStageA] (TMA)
@@ -697,6 +698,7 @@ __global__ void __launch_bounds__(kThreads, kAccMinBlocks) k_accumulate_band(
     int res, int K, int rows, uint32_t flags, float* __restrict__ scratch, uint32_t* tile_arrive,
     uint32_t* unit_counter, float* __restrict__ atlas, unsigned long long* __restrict__ stats,
     const uint64_t* __restrict__ slab_mask, const int2* __restrict__ slab_k) {
+    pdl_begin();
     extern __shared__ __align__(128) unsigned char acc_smem[];
     constexpr size_t kRawBytes = kTMA ? kRawBytesTMA : 0;
     PairRec* s_raw = reinterpret_cast<PairRec*>(acc_smem);                                   // [kStage] (TMA)
@@ -1048,6 +1050,7 @@ __global__ void __launch_bounds__(256) k_combine_deferred(const WorkUnit* __rest
                                                           int res, int K, uint32_t flags, float* __restrict__ atlas,
                                                           const uint64_t* __restrict__ slab_mask,
                                                           const int2* __restrict__ slab_k) {
+    pdl_begin();
     const uint32_t nd = *deferred_count;
     const int groups = (K + 3) / 4;
     const int TW = res / kTile, n_tiles = TW * TW;
@@ -1084,6 +1087,7 @@ __global__ void __launch_bounds__(256) k_combine_deferred(const WorkUnit* __rest
 }
 
 __global__ void k_exp(const float* tau, float* T, int64_t count) {
+    pdl_begin();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
          i += (int64_t)gridDim.x * blockDim.x)
         T[i] = t_of_tau(tau[i]);
@@ -1181,19 +1185,19 @@ void launch_accumulate(const WorkUnit* units, const uint32_t* n_units_dev, uint3
 #define DGSM_ACC_BAND_ARGS units, n_units_dev, vals, recs, n, al, res, K, rows, flags, scratch, tile_arrive, \
                            unit_counter, atlas, stats, slab_mask, slab_k
     if (band) {
-        if (st && tma) k_accumulate_band<true, true><<<grid, kThreads, smem, s>>>(DGSM_ACC_BAND_ARGS);
-        else if (st) k_accumulate_band<true, false><<<grid, kThreads, smem, s>>>(DGSM_ACC_BAND_ARGS);
-        else if (tma) k_accumulate_band<false, true><<<grid, kThreads, smem, s>>>(DGSM_ACC_BAND_ARGS);
-        else k_accumulate_band<false, false><<<grid, kThreads, smem, s>>>(DGSM_ACC_BAND_ARGS);
+        if (st && tma) pdl_launch(k_accumulate_band<true, true>, grid, kThreads, smem, s, DGSM_ACC_BAND_ARGS);
+        else if (st) pdl_launch(k_accumulate_band<true, false>, grid, kThreads, smem, s, DGSM_ACC_BAND_ARGS);
+        else if (tma) pdl_launch(k_accumulate_band<false, true>, grid, kThreads, smem, s, DGSM_ACC_BAND_ARGS);
+        else pdl_launch(k_accumulate_band<false, false>, grid, kThreads, smem, s, DGSM_ACC_BAND_ARGS);
     } else {
-        if (st && tma) k_accumulate<true, true><<<grid, kThreads, smem, s>>>(DGSM_ACC_ARGS);
-        else if (st) k_accumulate<true, false><<<grid, kThreads, smem, s>>>(DGSM_ACC_ARGS);
-        else if (tma) k_accumulate<false, true><<<grid, kThreads, smem, s>>>(DGSM_ACC_ARGS);
-        else k_accumulate<false, false><<<grid, kThreads, smem, s>>>(DGSM_ACC_ARGS);
+        if (st && tma) pdl_launch(k_accumulate<true, true>, grid, kThreads, smem, s, DGSM_ACC_ARGS);
+        else if (st) pdl_launch(k_accumulate<true, false>, grid, kThreads, smem, s, DGSM_ACC_ARGS);
+        else if (tma) pdl_launch(k_accumulate<false, true>, grid, kThreads, smem, s, DGSM_ACC_ARGS);
+        else pdl_launch(k_accumulate<false, false>, grid, kThreads, smem, s, DGSM_ACC_ARGS);
     }
 #undef DGSM_ACC_BAND_ARGS
 #undef DGSM_ACC_ARGS
-    k_combine_deferred<<<(unsigned)n_sm * 8, 256, 0, s>>>(units, deferred, deferred_count, scratch, res, K, flags, atlas,
+    pdl_launch(k_combine_deferred, (unsigned)n_sm * 8, 256, 0, s, units, deferred, deferred_count, scratch, res, K, flags, atlas,
                                                          slab_mask, slab_k);
     last_staging_tma = tma;
     if (ev_after) cudaEventRecord(ev_after, s);
@@ -1203,7 +1207,7 @@ void launch_exp(const float* tau, float* T, int64_t count, cudaStream_t s) {
     if (count <= 0) return;
     int64_t blocks = (count + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    k_exp<<<(unsigned)blocks, 256, 0, s>>>(tau, T, count);
+    pdl_launch(k_exp, (unsigned)blocks, 256, 0, s, tau, T, count);
 }
 
 }  // namespace dgsm

@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(256) k_depth_keys(const uint4* __restrict__ du
                                                     const uint32_t* __restrict__ dmin_dev,
                                                     uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
                                                     PassDigits pd, uint32_t* __restrict__ hist) {
+    pdl_begin();
     __shared__ uint32_t sh[kSortMaxPasses][kSortRadix];
     const uint32_t dmin = *dmin_dev;  // the light's smallest depth key (the plan's reduction, on the device)
     for (int t = threadIdx.x; t < pd.passes * kSortRadix; t += blockDim.x) (&sh[0][0])[t] = 0u;
@@ -54,6 +55,7 @@ __global__ void __launch_bounds__(256) k_depth_keys(const uint4* __restrict__ du
 __global__ void __launch_bounds__(256) k_gather_counts(const uint32_t* __restrict__ counts,
                                                        const uint32_t* __restrict__ perm, int64_t n,
                                                        uint32_t* __restrict__ cperm) {
+    pdl_begin();
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     cperm[j] = counts[perm[j]];
@@ -78,6 +80,7 @@ __global__ void __launch_bounds__(256) k_duplicate_ranked(const uint4* __restric
                                                           const uint64_t* __restrict__ tm,
                                                           uint32_t* __restrict__ keys,
                                                           uint32_t* __restrict__ vals) {
+    pdl_begin();
     // keys of this light start at base = the plan's light_key_begin[l] (device);
     // nothing is written at or past n_keys (0 when the keys overflowed the
     // workspace capacity of a sync-free build).  key = light << tile_bits | tile.
@@ -179,6 +182,7 @@ __global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ key
                                                 const uint64_t* __restrict__ n_dev, int tile_bits,
                                                 uint32_t n_tiles, uint32_t* __restrict__ tile_start,
                                                 uint32_t* __restrict__ tile_end) {
+    pdl_begin();
     const int64_t end = (int64_t)*n_dev;
     // four consecutive keys per thread (loads issued together), neighbours through L1
     const int64_t j0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
@@ -206,6 +210,7 @@ __global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ key
 // workspace); the caller's status word receives both.
 __global__ void k_run_setup(const PlanStats* __restrict__ ps, int n_lights, uint64_t capacity,
                             uint64_t* __restrict__ n_keys, dgsm_build_status_t* status) {
+    pdl_begin();
     const uint64_t P = ps->light_key_begin[n_lights];
     const bool over = P > capacity;
     *n_keys = over ? 0ull : P;
@@ -221,6 +226,7 @@ __global__ void k_run_setup(const PlanStats* __restrict__ ps, int n_lights, uint
 __global__ void __launch_bounds__(256) k_unit_counts(const uint32_t* __restrict__ ts,
                                                      const uint32_t* __restrict__ te, int64_t nt,
                                                      int chunk, uint64_t* __restrict__ cnt) {
+    pdl_begin();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nt) return;
     const uint32_t len = te[t] - ts[t];
@@ -245,6 +251,7 @@ __global__ void __launch_bounds__(256) k_units(const uint32_t* __restrict__ ts,
                                                const uint64_t* __restrict__ off, int64_t nt, int chunk,
                                                WorkUnit* __restrict__ units, uint32_t* n_units,
                                                uint32_t* __restrict__ class_hist) {
+    pdl_begin();
     __shared__ uint32_t s_hist[kUnitClasses];
     if (threadIdx.x < kUnitClasses) s_hist[threadIdx.x] = 0u;
     __syncthreads();
@@ -284,6 +291,7 @@ __global__ void __launch_bounds__(256) k_units_lpt(const WorkUnit* __restrict__ 
                                                    uint32_t* __restrict__ class_fill,
                                                    WorkUnit* __restrict__ out, uint32_t* __restrict__ deferred,
                                                    uint32_t* deferred_count) {
+    pdl_begin();
     __shared__ uint32_t s_base[kUnitClasses];
     if (threadIdx.x == 0) {
         uint32_t b = 0;
@@ -322,6 +330,7 @@ __global__ void __launch_bounds__(256) k_decode(const uint32_t* __restrict__ key
                                                 const uint4* __restrict__ dup, int64_t n, int64_t P,
                                                 int tile_bits, uint32_t* lo, uint32_t* to, uint32_t* dout,
                                                 uint32_t* io) {
+    pdl_begin();
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= P) return;
     const uint32_t l = keys[j] >> tile_bits;
@@ -350,6 +359,7 @@ __global__ void __launch_bounds__(kFusedThreads) k_units_fused(const uint32_t* _
                                                                int chunk, WorkUnit* __restrict__ units,
                                                                uint32_t* n_units, uint32_t* __restrict__ deferred,
                                                                uint32_t* deferred_count) {
+    pdl_begin();
     __shared__ uint32_t s_class[kUnitClasses], s_fill[kUnitClasses], s_slots;
     const int tid = threadIdx.x;
     if (tid < kUnitClasses) { s_class[tid] = 0u; s_fill[tid] = 0u; }
@@ -406,25 +416,25 @@ void launch_depth_keys(const uint4* dup, int64_t n, const uint32_t* dmin_dev, ui
                        const PassDigits& pd, uint32_t* hist, cudaStream_t s) {
     if (n <= 0) return;
     const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 4);
-    k_depth_keys<<<(unsigned)blocks, 256, 0, s>>>(dup, n, dmin_dev, keys, vals, pd, hist);
+    pdl_launch(k_depth_keys, (unsigned)blocks, 256, 0, s, dup, n, dmin_dev, keys, vals, pd, hist);
 }
 
 void launch_run_setup(const PlanStats* ps, int n_lights, uint64_t capacity, uint64_t* n_keys,
                       dgsm_build_status_t* status, cudaStream_t s) {
-    k_run_setup<<<1, 1, 0, s>>>(ps, n_lights, capacity, n_keys, status);
+    pdl_launch(k_run_setup, 1, 1, 0, s, ps, n_lights, capacity, n_keys, status);
 }
 
 void launch_gather_counts(const uint32_t* counts, const uint32_t* perm, int64_t n, uint32_t* cperm,
                           cudaStream_t s) {
     if (n <= 0) return;
-    k_gather_counts<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(counts, perm, n, cperm);
+    pdl_launch(k_gather_counts, (unsigned)((n + 255) / 256), 256, 0, s, counts, perm, n, cperm);
 }
 
 void launch_duplicate_ranked(const uint4* dup, const uint32_t* perm, const uint64_t* offs, int64_t n, int res,
                              int bin_mode, const uint64_t* base_dev, const uint64_t* n_keys_dev, uint32_t key_hi,
                              const uint64_t* tile_mask, uint32_t* keys, uint32_t* vals, cudaStream_t s) {
     if (n <= 0) return;
-    k_duplicate_ranked<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dup, perm, offs, n, res, bin_mode, base_dev,
+    pdl_launch(k_duplicate_ranked, (unsigned)((n + 255) / 256), 256, 0, s, dup, perm, offs, n, res, bin_mode, base_dev,
                                                                     n_keys_dev, key_hi, tile_mask, keys, vals);
 }
 
@@ -432,7 +442,7 @@ void launch_decode_keys(const uint32_t* keys, const uint32_t* vals, const uint4*
                         uint32_t* light_out, uint32_t* tile_out, uint32_t* depth_out, uint32_t* index_out,
                         cudaStream_t s) {
     if (plan.n_keys <= 0) return;
-    k_decode<<<(unsigned)((plan.n_keys + 255) / 256), 256, 0, s>>>(keys, vals, dup, plan.n, plan.n_keys,
+    pdl_launch(k_decode, (unsigned)((plan.n_keys + 255) / 256), 256, 0, s, keys, vals, dup, plan.n, plan.n_keys,
                                                                   plan.tile_bits, light_out, tile_out, depth_out,
                                                                   index_out);
 }
@@ -440,7 +450,7 @@ void launch_decode_keys(const uint32_t* keys, const uint32_t* vals, const uint4*
 void launch_ranges(const uint32_t* keys, const uint64_t* n_dev, int64_t capacity, int tile_bits, uint32_t n_tiles,
                    uint32_t* tile_start, uint32_t* tile_end, cudaStream_t s) {
     if (capacity <= 0) return;
-    k_ranges<<<(unsigned)((capacity + 1023) / 1024), 256, 0, s>>>(keys, n_dev, tile_bits, n_tiles, tile_start,
+    pdl_launch(k_ranges, (unsigned)((capacity + 1023) / 1024), 256, 0, s, keys, n_dev, tile_bits, n_tiles, tile_start,
                                                                  tile_end);
 }
 
@@ -451,18 +461,18 @@ void launch_units(const uint32_t* tile_start, const uint32_t* tile_end, int64_t 
                   int* launches) {
     const bool force_multi = getenv("DGSM_UNITS_MULTI") != nullptr;  // tests: the > 64K-tile path
     if (n_tiles_total <= kFusedTiles && !force_multi) {
-        k_units_fused<<<1, kFusedThreads, 0, s>>>(tile_start, tile_end, n_tiles_total, chunk, units, n_units_dev,
+        pdl_launch(k_units_fused, 1, kFusedThreads, 0, s, tile_start, tile_end, n_tiles_total, chunk, units, n_units_dev,
                                                   deferred, deferred_count);
         *launches += 1;
         return;
     }
     const unsigned g = (unsigned)((n_tiles_total + 255) / 256);
-    k_unit_counts<<<g, 256, 0, s>>>(tile_start, tile_end, n_tiles_total, chunk, unit_counts);
+    pdl_launch(k_unit_counts, g, 256, 0, s, tile_start, tile_end, n_tiles_total, chunk, unit_counts);
     launch_scan_u64(unit_counts, unit_offsets, n_tiles_total, scan_temp, s);
-    k_units<<<g, 256, 0, s>>>(tile_start, tile_end, unit_offsets, n_tiles_total, chunk, units_tmp, n_units_dev,
+    pdl_launch(k_units, g, 256, 0, s, tile_start, tile_end, unit_offsets, n_tiles_total, chunk, units_tmp, n_units_dev,
                               class_hist);
     const unsigned gl = (unsigned)std::min<uint32_t>((max_units + 255) / 256, 148u * 8u);
-    k_units_lpt<<<gl, 256, 0, s>>>(units_tmp, n_units_dev, class_hist, class_fill, units, deferred, deferred_count);
+    pdl_launch(k_units_lpt, gl, 256, 0, s, units_tmp, n_units_dev, class_hist, class_fill, units, deferred, deferred_count);
     *launches += 3 + kScanLaunches;
 }
 

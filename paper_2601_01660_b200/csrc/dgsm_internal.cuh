@@ -144,6 +144,43 @@ __host__ __device__ inline uint32_t count_tiles(const TileRects& R) {
 
 // Paired FP32 (sm_100 FFMA2 / FADD2 / FMUL2): a packed value holds two fp32
 // operands (low, high); one f32x2 instruction does both.
+// ---- programmatic dependent launch (PDL) -------------------------------------
+// Every kernel of the library starts with pdl_begin(): it waits for the grid it
+// depends on (griddepcontrol.wait: that grid has completed and its memory is
+// visible; a no-op when the kernel was not launched as a dependent) and lets the
+// next grid in the stream launch now (griddepcontrol.launch_dependents: its CTAs
+// take SM slots as this grid's retire and wait there, hiding the launch gap).
+// pdl_launch() launches with cudaLaunchAttributeProgrammaticStreamSerialization;
+// captured in a CUDA graph these become programmatic dependency edges.
+#ifndef DGSM_PDL
+#define DGSM_PDL 1
+#endif
+__device__ __forceinline__ void pdl_begin() {
+#if DGSM_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+template <typename... KArgs, typename... Args>
+inline void pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+#if DGSM_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+#else
+    kernel<<<grid, block, smem, s>>>(static_cast<KArgs>(args)...);
+#endif
+}
+
 typedef unsigned long long f2_t;
 __device__ __forceinline__ f2_t f2add(f2_t a, f2_t b) { f2_t d; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
 __device__ __forceinline__ f2_t f2sub(f2_t a, f2_t b) { f2_t d; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }

@@ -37,6 +37,7 @@ template <typename KeyT>
 __global__ void __launch_bounds__(256) k_hist(const KeyT* __restrict__ keys, int64_t n, int passes,
                                               PassDigits pd, uint32_t* __restrict__ hist,
                                               const uint64_t* __restrict__ n_dev) {
+    pdl_begin();
     if (n_dev) n = (int64_t)*n_dev;  // device-side count (<= the launch capacity)
     __shared__ uint32_t sh[kMaxPasses][kRadix];
     for (int t = threadIdx.x; t < kMaxPasses * kRadix; t += blockDim.x) (&sh[0][0])[t] = 0;
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ k
                                                       uint32_t* part_ctr, const uint32_t* __restrict__ gsrc,
                                                       uint32_t* __restrict__ gdst,
                                                       const uint64_t* __restrict__ n_dev) {
+    pdl_begin();
     extern __shared__ __align__(16) unsigned char os_smem[];
     KeyT* s_keys = reinterpret_cast<KeyT*>(os_smem);
     uint32_t* s_vals = reinterpret_cast<uint32_t*>(os_smem + sizeof(KeyT) * kTileKeys);
@@ -298,14 +300,14 @@ int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt
         // histograms, partition counters and the first pass's status in one memset
         onesweep_prepare(temp, n, s);
         const int hist_grid = (int)std::min<int64_t>(148 * 4, (n + 2047) / 2048);
-        k_hist<KeyT><<<hist_grid, 256, 0, s>>>(keys, n, passes, pd, t.hist, n_dev);
+        pdl_launch(k_hist<KeyT>, hist_grid, 256, 0, s, keys, n, passes, pd, t.hist, n_dev);
         *launches += 1;
     }
     KeyT *ki = keys, *ko = keys_alt;
     uint32_t *vi = vals, *vo = vals_alt;
     int flipped = 0;
     for (int p = 0; p < passes; ++p) {
-        k_pass<KeyT><<<(unsigned)parts, kThreads, dyn, s>>>(ki, vi, ko, vo, n, pd.shift[p], pd.bits[p],
+        pdl_launch(k_pass<KeyT>, (unsigned)parts, kThreads, dyn, s, ki, vi, ko, vo, n, pd.shift[p], pd.bits[p],
                                                            top_match && p == passes - 1, t.hist + p * kRadix,
                                                            t.status[p & 1], t.status[(p + 1) & 1],
                                                            t.part_ctr + p, gsrc, p == passes - 1 ? gdst : nullptr,

@@ -22,6 +22,7 @@ __global__ void __launch_bounds__(256, 4) k_project(  // (256, 3) and (256, 2) m
     PairRec* __restrict__ recs, uint32_t* __restrict__ counts,
     uint4* __restrict__ dup,
     PlanStats* stats) {
+    pdl_begin();
     // Gaussians [i0, i0 + cnt) of every light (a chunk of an upload pipeline, or all)
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = idx < (int64_t)n_lights * cnt;
@@ -212,6 +213,7 @@ __global__ void __launch_bounds__(256, 4) k_project(  // (256, 3) and (256, 2) m
 }
 
 __global__ void k_init_stats(PlanStats* stats) {
+    pdl_begin();
     int t = threadIdx.x;
     if (t < DGSM_MAX_LIGHTS) { stats->depth_min[t] = 0xffffffffu; stats->depth_max[t] = 0u; }
     if (t == 0) { stats->n_invalid = 0u; stats->first_invalid = 0xffffffffu; }
@@ -219,7 +221,7 @@ __global__ void k_init_stats(PlanStats* stats) {
 }  // namespace
 
 void launch_project_init(PlanStats* stats, cudaStream_t s) {
-    k_init_stats<<<1, DGSM_MAX_LIGHTS, 0, s>>>(stats);
+    pdl_launch(k_init_stats, 1, DGSM_MAX_LIGHTS, 0, s, stats);
 }
 
 void launch_project(const dgsm_gaussians_t& g, const LightsParam& lp, int n_lights, int res, int K,
@@ -229,7 +231,7 @@ void launch_project(const dgsm_gaussians_t& g, const LightsParam& lp, int n_ligh
     if (total == 0) return;
     const int bs = 256;
     const int64_t grid = (total + bs - 1) / bs;
-    k_project<<<(unsigned)grid, bs, 0, s>>>(g.means, g.scales, g.rotations, g.opacities, g.n, i0, cnt, lp,
+    pdl_launch(k_project, (unsigned)grid, bs, 0, s, g.means, g.scales, g.rotations, g.opacities, g.n, i0, cnt, lp,
                                             n_lights, res, K, (double)o.kappa, (double)o.k_sigma,
                                             (double)o.rho_scale * (double)(2 * res) / (2.0 * kPi), o.bin_mode,
                                             o.absorption, (o.flags & DGSM_NO_TILE_CULL) != 0,

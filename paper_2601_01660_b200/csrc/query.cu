@@ -185,6 +185,7 @@ __global__ void __launch_bounds__(kQThreads, DGSM_QMINB) k_query(const float* __
                                                      int n_lights, int res, int K,
                                                      const float* __restrict__ pos, int64_t m,
                                                      float* __restrict__ T_out, float* __restrict__ colors) {
+    pdl_begin();
     const int64_t base = (int64_t)blockIdx.x * (kQThreads * kQPT) + threadIdx.x;
     const size_t per_light = (size_t)K * res * res;
     double px[kQPT], py[kQPT], pz[kQPT];
@@ -220,6 +221,7 @@ __global__ void __launch_bounds__(kQThreads, DGSM_QMINB) k_query_ordered(const f
                                                              const float* __restrict__ pos,
                                                              const uint32_t* __restrict__ order, int64_t m,
                                                              float* __restrict__ T_out, float* __restrict__ colors) {
+    pdl_begin();
     const int64_t base = (int64_t)blockIdx.x * (kQThreads * kQPT) + threadIdx.x;
     const size_t per_light = (size_t)K * res * res;
     double px[kQPT], py[kQPT], pz[kQPT];
@@ -280,6 +282,7 @@ __device__ __forceinline__ void load4(const float* __restrict__ pos, int64_t m, 
 // skipped.  Warp shuffles, then one shared-memory merge per CTA, then one
 // atomic per CTA and axis.
 __global__ void __launch_bounds__(256) k_aabb(const float* __restrict__ pos, int64_t m, uint32_t* box) {
+    pdl_begin();
     __shared__ uint32_t s_box[6];
     if (threadIdx.x < 6) s_box[threadIdx.x] = threadIdx.x < 3 ? 0xffffffffu : 0u;
     __syncthreads();
@@ -338,6 +341,7 @@ __global__ void __launch_bounds__(kQThreads, DGSM_QCMINB) k_query_chunks(ChunkPa
                                                             int K, const float* __restrict__ pos, int64_t m,
                                                             float* __restrict__ T_out,
                                                             float* __restrict__ partial_out) {
+    pdl_begin();
     const int64_t q = (int64_t)blockIdx.x * kQThreads + threadIdx.x;
     if (q >= m) return;
     const double px = __ldg(pos + 3 * q), py = __ldg(pos + 3 * q + 1), pz = __ldg(pos + 3 * q + 2);
@@ -355,6 +359,7 @@ __global__ void __launch_bounds__(kQThreads, DGSM_QCMINB) k_query_chunks(ChunkPa
 // T *= prod_j partial[j] (the product over lights, Q13, of the summed shell chunks)
 __global__ void __launch_bounds__(256) k_query_combine(const float* __restrict__ partial, int n, int64_t m,
                                                        float* __restrict__ T) {
+    pdl_begin();
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= m) return;
     float t = T[q];
@@ -378,6 +383,7 @@ __global__ void __launch_bounds__(256) k_morton(const float* __restrict__ pos, i
                                                 const uint32_t* __restrict__ box,
                                                 uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
                                                 PassDigits pd, uint32_t* __restrict__ hist) {
+    pdl_begin();
     __shared__ uint32_t sh[kSortMaxPasses][kSortRadix];
     for (int t = threadIdx.x; t < pd.passes * kSortRadix; t += blockDim.x) (&sh[0][0])[t] = 0u;
     float lo[3], ie[3];
@@ -436,6 +442,7 @@ __global__ void __launch_bounds__(128) k_query_footprint(const float* __restrict
                                                          const float* __restrict__ scales,
                                                          const float* __restrict__ rots, int64_t m,
                                                          float* __restrict__ T_out, float* __restrict__ colors) {
+    pdl_begin();
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= m) return;
     const double mx = __ldg(means + 3 * g), my = __ldg(means + 3 * g + 1), mz = __ldg(means + 3 * g + 2);
@@ -489,7 +496,7 @@ unsigned query_blocks(int64_t m) { return (unsigned)((m + kQThreads * kQPT - 1) 
 void launch_query(const float* atlas, const LightsParam& lp, int n_lights, int res, int K,
                   const float* positions, int64_t m, float* T_out, float* colors, cudaStream_t s) {
     if (m <= 0) return;
-    k_query<<<query_blocks(m), kQThreads, 0, s>>>(atlas, query_lights(lp, n_lights, K), n_lights, res, K, positions,
+    pdl_launch(k_query, query_blocks(m), kQThreads, 0, s, atlas, query_lights(lp, n_lights, K), n_lights, res, K, positions,
                                                   m, T_out, colors);
 }
 
@@ -497,7 +504,7 @@ void launch_query_ordered(const float* atlas, const LightsParam& lp, int n_light
                           const float* positions, const uint32_t* order, int64_t m, float* T_out, float* colors,
                           cudaStream_t s) {
     if (m <= 0) return;
-    k_query_ordered<<<query_blocks(m), kQThreads, 0, s>>>(atlas, query_lights(lp, n_lights, K), n_lights, res, K,
+    pdl_launch(k_query_ordered, query_blocks(m), kQThreads, 0, s, atlas, query_lights(lp, n_lights, K), n_lights, res, K,
                                                           positions, order, m, T_out, colors);
 }
 
@@ -513,13 +520,13 @@ void launch_query_chunks(const float* const* chunks, const int* kb, const int* k
         cp.ke[l] = ke[l];
         cp.split[l] = split[l];
     }
-    k_query_chunks<<<(unsigned)((m + kQThreads - 1) / kQThreads), kQThreads, 0, s>>>(
+    pdl_launch(k_query_chunks, (unsigned)((m + kQThreads - 1) / kQThreads), kQThreads, 0, s, 
         cp, query_lights(lp, n_lights, K), n_lights, res, K, positions, m, T_out, partial_out);
 }
 
 void launch_query_combine(const float* partial, int n, int64_t m, float* T, cudaStream_t s) {
     if (m <= 0) return;
-    k_query_combine<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(partial, n, m, T);
+    pdl_launch(k_query_combine, (unsigned)((m + 255) / 256), 256, 0, s, partial, n, m, T);
 }
 
 void launch_morton(const float* positions, int64_t m, uint32_t* box, uint32_t* keys, uint32_t* vals,
@@ -529,15 +536,15 @@ void launch_morton(const float* positions, int64_t m, uint32_t* box, uint32_t* k
     cudaMemsetAsync(box + 3, 0, 3 * sizeof(uint32_t), s);
     const int64_t groups = (m + 3) / 4;
     const unsigned blocks = (unsigned)std::min<int64_t>((groups + 255) / 256, 148 * 4);
-    k_aabb<<<blocks, 256, 0, s>>>(positions, m, box);
-    k_morton<<<blocks, 256, 0, s>>>(positions, m, box, keys, vals, pd, hist);
+    pdl_launch(k_aabb, blocks, 256, 0, s, positions, m, box);
+    pdl_launch(k_morton, blocks, 256, 0, s, positions, m, box, keys, vals, pd, hist);
 }
 
 void launch_query_footprint(const float* atlas, const LightsParam& lp, const FootprintParam& fp, int n_lights,
                             int res, int K, const float* means, const float* scales, const float* rotations,
                             int64_t m, float* T_out, float* colors, cudaStream_t s) {
     if (m <= 0) return;
-    k_query_footprint<<<(unsigned)((m + 127) / 128), 128, 0, s>>>(atlas, query_lights(lp, n_lights, K), fp, n_lights, res, K, means, scales,
+    pdl_launch(k_query_footprint, (unsigned)((m + 127) / 128), 128, 0, s, atlas, query_lights(lp, n_lights, K), fp, n_lights, res, K, means, scales,
                                                                   rotations, m, T_out, colors);
 }
 

@@ -47,6 +47,7 @@ constexpr int64_t kMaxBlocks = 1024;
 template <typename T>
 __global__ void __launch_bounds__(kScanThreads) k_reduce(const T* __restrict__ in, int64_t n, int64_t tpb,
                                                          uint64_t* __restrict__ partials) {
+    pdl_begin();
     const int64_t t0 = (int64_t)blockIdx.x * tpb;
     uint64_t s = 0;
     for (int64_t t = t0; t < t0 + tpb; ++t) {
@@ -68,6 +69,7 @@ __global__ void __launch_bounds__(kScanThreads) k_downsweep(const T* __restrict_
                                                             const uint64_t* __restrict__ partials,
                                                             O* __restrict__ out, uint64_t* __restrict__ marks,
                                                             int64_t mark_stride, int n_marks) {
+    pdl_begin();
     // padded: element e at e + e/16, so the blocked accesses (stride 16) spread over banks
     __shared__ uint64_t tile[kScanTile + kScanTile / kScanItems];
     auto at = [](int e) { return e + (e >> 4); };
@@ -132,8 +134,8 @@ void scan_impl(const T* in, O* out, int64_t n, void* temp, cudaStream_t s, uint6
     const int64_t tiles = (n + kScanTile - 1) / kScanTile;
     const int64_t tpb = (tiles + kMaxBlocks - 1) / kMaxBlocks;
     const int64_t nb = (tiles + tpb - 1) / tpb;
-    k_reduce<T><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, tpb, partials);
-    k_downsweep<T, O><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, tpb, partials, out, marks, mark_stride,
+    pdl_launch(k_reduce<T>, (unsigned)nb, kScanThreads, 0, s, in, n, tpb, partials);
+    pdl_launch(k_downsweep<T, O>, (unsigned)nb, kScanThreads, 0, s, in, n, tpb, partials, out, marks, mark_stride,
                                                             n_marks);
 }
 

@@ -24,6 +24,7 @@ __device__ __forceinline__ void wrap_px(long long& col, long long& row, int W, i
 
 __global__ void k_slab_init(uint64_t* __restrict__ mask, int64_t words, int2* __restrict__ kr, int n_lights,
                             int K) {
+    pdl_begin();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < words) mask[i] = 0ull;
     if (i < n_lights) kr[i] = make_int2(K, -1);
@@ -34,6 +35,7 @@ __global__ void __launch_bounds__(256) k_active_slab(const float* __restrict__ x
                                                      int n_lights, int res, int K,
                                                      unsigned long long* __restrict__ mask,
                                                      int2* __restrict__ kr) {
+    pdl_begin();
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool in = false;
     double px = 0.0, py = 0.0, pz = 0.0;
@@ -97,10 +99,10 @@ void launch_active_slab(const float* x, int64_t m, const dgsm_roi_t& roi, const 
                         int res, int K, uint64_t* mask, int2* kr, cudaStream_t s, int* launches) {
     const int64_t words = (int64_t)n_lights * (res / kTile) * (res / kTile);
     const int64_t init = words > n_lights ? words : n_lights;
-    k_slab_init<<<(unsigned)((init + 255) / 256), 256, 0, s>>>(mask, words, kr, n_lights, K);
+    pdl_launch(k_slab_init, (unsigned)((init + 255) / 256), 256, 0, s, mask, words, kr, n_lights, K);
     *launches += 1;
     if (m <= 0) return;
-    k_active_slab<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(x, m, roi.center[0], roi.center[1], roi.radius,
+    pdl_launch(k_active_slab, (unsigned)((m + 255) / 256), 256, 0, s, x, m, roi.center[0], roi.center[1], roi.radius,
                                                               roi.z_min, roi.z_max, lp, n_lights, res, K,
                                                               (unsigned long long*)mask, kr);
     *launches += 1;

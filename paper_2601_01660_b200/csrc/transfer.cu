@@ -52,6 +52,7 @@ __device__ __forceinline__ void sh_basis3(float x, float y, float z, int d, floa
 
 __global__ void k_transfer_grid(ShParam sp, int n_theta, int n_phi, float4* __restrict__ dirs,
                                 float4* __restrict__ wl) {
+    pdl_begin();
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n_theta * n_phi) return;
     const int i = j / n_phi, k = j - i * n_phi;
@@ -89,6 +90,7 @@ __global__ void __launch_bounds__(kThreadsT) k_transfer_part(const float4* __res
                                                              const float4* __restrict__ wl, int M, int chunk,
                                                              const float* __restrict__ normals, int64_t n,
                                                              float q, float4* __restrict__ part) {
+    pdl_begin();
     __shared__ float4 s_dir[kTileDirs], s_wl[kTileDirs];
     const int64_t g0 = ((int64_t)blockIdx.x * kThreadsT + threadIdx.x) * kG;
     float nx[kG], ny[kG], nz[kG];
@@ -173,6 +175,7 @@ __global__ void __launch_bounds__(kThreadsT) k_transfer_part(const float4* __res
 __global__ void k_transfer_fin(const float4* __restrict__ part, int n_chunks, int64_t n,
                                const float* __restrict__ colors, float eps, float s_max, float gamma,
                                float* __restrict__ scales_out, float* __restrict__ colors_out) {
+    pdl_begin();
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
     double num[3] = {0.0, 0.0, 0.0}, den = 0.0;
@@ -215,7 +218,7 @@ void launch_transfer(const ShParam& sp, int n_theta, int n_phi, float q, float e
     float4* dirs = (float4*)ws;
     float4* wl = (float4*)((char*)ws + al(sizeof(float4) * M));
     float4* part = (float4*)((char*)ws + 2 * al(sizeof(float4) * M));
-    k_transfer_grid<<<(M + 255) / 256, 256, 0, s>>>(sp, n_theta, n_phi, dirs, wl);
+    pdl_launch(k_transfer_grid, (M + 255) / 256, 256, 0, s, sp, n_theta, n_phi, dirs, wl);
     *launches += 1;
     if (n <= 0) return;
     const int chunks = transfer_chunks(n, M);
@@ -223,12 +226,12 @@ void launch_transfer(const ShParam& sp, int n_theta, int n_phi, float q, float e
     const int n_chunks = (M + chunk - 1) / chunk;
     dim3 grid((unsigned)((n + (int64_t)kThreadsT * kG - 1) / ((int64_t)kThreadsT * kG)), (unsigned)n_chunks);
     if (q == 1.0f)
-        k_transfer_part<1><<<grid, kThreadsT, 0, s>>>(dirs, wl, M, chunk, normals, n, q, part);
+        pdl_launch(k_transfer_part<1>, grid, kThreadsT, 0, s, dirs, wl, M, chunk, normals, n, q, part);
     else if (q == 2.0f)
-        k_transfer_part<2><<<grid, kThreadsT, 0, s>>>(dirs, wl, M, chunk, normals, n, q, part);
+        pdl_launch(k_transfer_part<2>, grid, kThreadsT, 0, s, dirs, wl, M, chunk, normals, n, q, part);
     else
-        k_transfer_part<0><<<grid, kThreadsT, 0, s>>>(dirs, wl, M, chunk, normals, n, q, part);
-    k_transfer_fin<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(part, n_chunks, n, colors, eps, s_max, gamma,
+        pdl_launch(k_transfer_part<0>, grid, kThreadsT, 0, s, dirs, wl, M, chunk, normals, n, q, part);
+    pdl_launch(k_transfer_fin, (unsigned)((n + 255) / 256), 256, 0, s, part, n_chunks, n, colors, eps, s_max, gamma,
                                                               scales_out, colors_out);
     *launches += 2;
 }
