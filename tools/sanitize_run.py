@@ -1,6 +1,7 @@
 """Small workloads through every entry point (for compute-sanitizer): cfg1 build
 (plan+run, async, bins), query (plain, ordered, chunks, footprint), slab, sort,
-transfer, exp epilogue, a 2-frame cfg4-small sequence through a CUDA graph."""
+transfer, exp epilogue; the band kernel (K = 100), the per-light tile sort
+(res 128, 3 lights), dgsm_frame_host and dgsm.FrameStream (graphs, PDL)."""
 import sys
 
 import numpy as np
@@ -35,5 +36,18 @@ dgsm.sort_pairs(k, torch.arange(5001, dtype=torch.int32, device="cuda"), 31)
 nr = torch.nn.functional.normalize(torch.randn(1000, 3, device="cuda"), dim=1)
 dgsm.sh_transfer(np.ones((3, 16), np.float32), 3, nr, torch.rand(1000, 3, device="cuda"))
 dgsm.exp_epilogue(torch.rand(1000, device="cuda"))
+b = synth.random_scene(5, 400, res=32, K=100, L=2, dist=(0.3, 3.0), scale=(0.01, 0.5))
+dgsm.build(dgsm.to_device(b.gaussians), b.lights, b.res, b.K)
+pl = synth.random_scene(7, 400, res=128, K=9, L=3, dist=(0.3, 3.0))
+dgsm.build(dgsm.to_device(pl.gaussians), pl.lights, pl.res, pl.K)
+fh = {k: torch.from_numpy(np.ascontiguousarray(v, np.float32)).pin_memory() for k, v in s.gaussians.items()}
+xh = torch.from_numpy(np.ascontiguousarray(s.queries, np.float32)).pin_memory()
+Th = torch.empty(xh.shape[0]).pin_memory()
+fr = dgsm.FrameHost(s.lights, s.res, s.K)
+fr(fh, xh, Th)
+fs = dgsm.FrameStream(s.lights, s.res, s.K, s.n, xh.shape[0], plan.n_keys + 100)
+for _ in range(3):
+    fs(fh, xh, Th)
+fs.wait()
 torch.cuda.synchronize()
 print("ok")
