@@ -117,15 +117,25 @@ RunShape make_shape(int64_t n, int L, int res, int K, int64_t cap) {
     return sh;
 }
 
-struct RunLayout {
-    uint32_t *keys_a, *keys_b;   // (light | tile) keys (capacity), ping-pong
-    uint32_t *vals_a, *vals_b;   // Gaussian indices (capacity)
+// The per-light chains before the tile sort (depth keys, depth sort, emission
+// offsets, key duplication) are independent: up to kLanes of them run at once on
+// side streams (fork / join by events; light l on lane l % kLanes), each lane
+// with its own buffers.  One light: lane 0 is the caller's stream itself.
+constexpr int kLanes = 4;
+struct LaneBufs {
     uint32_t *gkeys_a, *gkeys_b; // per-light depth keys of the N Gaussians, ping-pong
     uint32_t *gvals_a, *gvals_b; // Gaussian indices -> depth-rank permutation
     uint32_t* cperm;             // tile counts in depth-rank order (N)
     uint64_t* offs_perm;         // their exclusive scan (N + 1)
     void* gscan_temp;
-    void* sort_temp;
+    void* sort_temp;             // the depth sort's histograms / partition status (N keys)
+};
+struct RunLayout {
+    uint32_t *keys_a, *keys_b;   // (light | tile) keys (capacity), ping-pong
+    uint32_t *vals_a, *vals_b;   // Gaussian indices (capacity)
+    LaneBufs lane[kLanes];
+    int n_lanes;
+    void* sort_temp;             // the tile sort's (capacity keys)
     uint32_t *tile_start, *tile_end;
     uint64_t *unit_cnt, *unit_off;
     void* unit_scan_temp;
@@ -151,13 +161,18 @@ RunLayout run_layout(void* ws, const RunShape& sh) {
     r.keys_b = c.take<uint32_t>(P);
     r.vals_a = c.take<uint32_t>(P);
     r.vals_b = c.take<uint32_t>(P);
-    r.gkeys_a = c.take<uint32_t>(n);
-    r.gkeys_b = c.take<uint32_t>(n);
-    r.gvals_a = c.take<uint32_t>(n);
-    r.gvals_b = c.take<uint32_t>(n);
-    r.cperm = c.take<uint32_t>(n);
-    r.offs_perm = c.take<uint64_t>(n + 1);
-    r.gscan_temp = c.take<char>(scan_u32_to_u64_temp_bytes(n));
+    r.n_lanes = std::max(1, std::min(sh.n_lights, kLanes));
+    for (int j = 0; j < r.n_lanes; ++j) {
+        LaneBufs& b = r.lane[j];
+        b.gkeys_a = c.take<uint32_t>(n);
+        b.gkeys_b = c.take<uint32_t>(n);
+        b.gvals_a = c.take<uint32_t>(n);
+        b.gvals_b = c.take<uint32_t>(n);
+        b.cperm = c.take<uint32_t>(n);
+        b.offs_perm = c.take<uint64_t>(n + 1);
+        b.gscan_temp = c.take<char>(scan_u32_to_u64_temp_bytes(n));
+        b.sort_temp = c.take<char>(onesweep_temp_bytes(n));
+    }
     r.sort_temp = c.take<char>(onesweep_temp_bytes(std::max<int64_t>(P, n)));
 
     r.unit_cnt = c.take<uint64_t>(nt);
@@ -471,6 +486,27 @@ struct Sorted {
     const uint32_t *keys, *vals;
 };
 
+// Side streams + events of the per-light lanes, per (thread, device).
+struct LaneStreams {
+    cudaStream_t st[kLanes];
+    cudaEvent_t fork, done[kLanes];
+    int dev = -1;
+};
+static LaneStreams& lane_streams() {
+    thread_local LaneStreams ls;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (ls.dev != dev) {
+        for (int j = 0; j < kLanes; ++j) {
+            cudaStreamCreateWithFlags(&ls.st[j], cudaStreamNonBlocking);
+            cudaEventCreateWithFlags(&ls.done[j], cudaEventDisableTiming);
+        }
+        cudaEventCreateWithFlags(&ls.fork, cudaEventDisableTiming);
+        ls.dev = dev;
+    }
+    return ls;
+}
+
 static Sorted run_binning(const dgsm_gaussians_t* g, const dgsm_build_opts_t& o, const RunShape& sh,
                           const PlanLayout& p, const RunLayout& r, dgsm_build_status_t* status, cudaStream_t s,
                           const int64_t* key_begin_host = nullptr) {
@@ -482,34 +518,48 @@ static Sorted run_binning(const dgsm_gaussians_t* g, const dgsm_build_opts_t& o,
     g_launches += 1;
     PassDigits pd0 = onesweep_digits(32);
     pd0.passes = 0;
+    LaneStreams* ls = nullptr;
+    if (r.n_lanes > 1) {  // fork: the lanes start after everything queued on s
+        ls = &lane_streams();
+        cudaEventRecord(ls->fork, s);
+        for (int j = 0; j < r.n_lanes; ++j) cudaStreamWaitEvent(ls->st[j], ls->fork, 0);
+    }
     for (int l = 0; l < sh.n_lights; ++l) {
+        const LaneBufs& lb = r.lane[l % r.n_lanes];
+        const cudaStream_t ss = ls ? ls->st[l % r.n_lanes] : s;
         const uint4* dup = p.dup + (int64_t)l * n;
         const uint32_t* counts_l = p.counts + (int64_t)l * n;
-        const uint32_t* perm = r.gvals_a;
+        const uint32_t* perm = lb.gvals_a;
         const int db = sh.depth_bits[l];
         if (n > 1 && db > 0) {
             const PassDigits pd = onesweep_digits(db);
             // 1. light-distance digits on the Gaussians (the key kernel fills the sort's
             //    digit histograms; the sort's last pass gathers the key counts into
             //    depth-rank order)
-            uint32_t* hist = onesweep_prepare(r.sort_temp, n, s);
-            launch_depth_keys(dup, n, p.stats->depth_min + l, r.gkeys_a, r.gvals_a, pd, hist, s);
-            const int fl = launch_onesweep_u32(r.gkeys_a, r.gvals_a, r.gkeys_b, r.gvals_b, n, db, r.sort_temp, s,
-                                               &g_launches, counts_l, r.cperm, true);
-            perm = fl ? r.gvals_b : r.gvals_a;
+            uint32_t* hist = onesweep_prepare(lb.sort_temp, n, ss);
+            launch_depth_keys(dup, n, p.stats->depth_min + l, lb.gkeys_a, lb.gvals_a, pd, hist, ss);
+            const int fl = launch_onesweep_u32(lb.gkeys_a, lb.gvals_a, lb.gkeys_b, lb.gvals_b, n, db, lb.sort_temp, ss,
+                                               &g_launches, counts_l, lb.cperm, true);
+            perm = fl ? lb.gvals_b : lb.gvals_a;
             g_launches += 1;
         } else {
-            launch_depth_keys(dup, n, p.stats->depth_min + l, r.gkeys_a, r.gvals_a, pd0, nullptr, s);
-            launch_gather_counts(counts_l, r.gvals_a, n, r.cperm, s);
+            launch_depth_keys(dup, n, p.stats->depth_min + l, lb.gkeys_a, lb.gvals_a, pd0, nullptr, ss);
+            launch_gather_counts(counts_l, lb.gvals_a, n, lb.cperm, ss);
             g_launches += 2;
         }
         // 2. emission offsets in depth-rank order
-        launch_scan_u32_to_u64(r.cperm, r.offs_perm, n, r.gscan_temp, s);
+        launch_scan_u32_to_u64(lb.cperm, lb.offs_perm, n, lb.gscan_temp, ss);
         // 3. key duplication (key = light | tile, value = Gaussian index) into the light's segment
         const uint64_t* tm = o.slab ? slab_mask_ptr(o.slab) + (int64_t)l * n_tiles : nullptr;
-        launch_duplicate_ranked(dup, perm, r.offs_perm, n, res, o.bin_mode, p.stats->light_key_begin + l, r.n_keys,
-                                (uint32_t)l << sh.tile_bits, tm, r.keys_a, r.vals_a, s);
+        launch_duplicate_ranked(dup, perm, lb.offs_perm, n, res, o.bin_mode, p.stats->light_key_begin + l, r.n_keys,
+                                (uint32_t)l << sh.tile_bits, tm, r.keys_a, r.vals_a, ss);
         g_launches += kScanLaunches + 1;
+    }
+    if (ls) {  // join
+        for (int j = 0; j < r.n_lanes; ++j) {
+            cudaEventRecord(ls->done[j], ls->st[j]);
+            cudaStreamWaitEvent(s, ls->done[j], 0);
+        }
     }
     // 4. one stable sort of the (light | tile) digits of all keys (grid: the capacity),
     //    or — when the per-light key segments are known on the host (the planned build)
