@@ -162,6 +162,9 @@ RunLayout run_layout(void* ws, const RunShape& sh) {
     r.vals_a = c.take<uint32_t>(P);
     r.vals_b = c.take<uint32_t>(P);
     r.n_lanes = std::max(1, std::min(sh.n_lights, kLanes));
+    // a lane also runs its lights' tile sorts when a per-light sort saves a pass
+    // (run_binning): its sort temp then covers a light's key segment (<= capacity)
+    const bool lane_tile_sort = sh.n_lights > 1 && (sh.tile_bits + 7) / 8 < (sh.light_bits + sh.tile_bits + 7) / 8;
     for (int j = 0; j < r.n_lanes; ++j) {
         LaneBufs& b = r.lane[j];
         b.gkeys_a = c.take<uint32_t>(n);
@@ -171,7 +174,7 @@ RunLayout run_layout(void* ws, const RunShape& sh) {
         b.cperm = c.take<uint32_t>(n);
         b.offs_perm = c.take<uint64_t>(n + 1);
         b.gscan_temp = c.take<char>(scan_u32_to_u64_temp_bytes(n));
-        b.sort_temp = c.take<char>(onesweep_temp_bytes(n));
+        b.sort_temp = c.take<char>(onesweep_temp_bytes(lane_tile_sort ? std::max<int64_t>(P, n) : n));
     }
     r.sort_temp = c.take<char>(onesweep_temp_bytes(std::max<int64_t>(P, n)));
 
@@ -518,6 +521,14 @@ static Sorted run_binning(const dgsm_gaussians_t* g, const dgsm_build_opts_t& o,
     g_launches += 1;
     PassDigits pd0 = onesweep_digits(32);
     pd0.passes = 0;
+    // the tile sort per light segment when the host knows the segments (the planned
+    // build) and it saves a pass (cfg5: 3 + 16 bits = 3 passes over all keys, 16 bits
+    // = 2 per light; the keys are emitted grouped by light): in the light's lane,
+    // right after its duplication
+    const int tb = sh.tile_bits;
+    const bool per_light_sort =
+        key_begin_host && sh.n_lights > 1 && (tb + 7) / 8 < (sh.light_bits + tb + 7) / 8;
+    const int target = onesweep_digits(tb).passes & 1;  // where a sorted segment of > 1 key ends
     LaneStreams* ls = nullptr;
     if (r.n_lanes > 1) {  // fork: the lanes start after everything queued on s
         ls = &lane_streams();
@@ -554,6 +565,19 @@ static Sorted run_binning(const dgsm_gaussians_t* g, const dgsm_build_opts_t& o,
         launch_duplicate_ranked(dup, perm, lb.offs_perm, n, res, o.bin_mode, p.stats->light_key_begin + l, r.n_keys,
                                 (uint32_t)l << sh.tile_bits, tm, r.keys_a, r.vals_a, ss);
         g_launches += kScanLaunches + 1;
+        if (per_light_sort) {
+            const int64_t b = key_begin_host[l], nl = key_begin_host[l + 1] - key_begin_host[l];
+            if (nl > 0) {
+                const int fl = launch_onesweep_u32(r.keys_a + b, r.vals_a + b, r.keys_b + b, r.vals_b + b, nl, tb,
+                                                   lb.sort_temp, ss, &g_launches);
+                if (fl != target) {  // (a segment of one key: no pass ran)
+                    cudaMemcpyAsync((target ? r.keys_b : r.keys_a) + b, (fl ? r.keys_b : r.keys_a) + b, 4 * nl,
+                                    cudaMemcpyDeviceToDevice, ss);
+                    cudaMemcpyAsync((target ? r.vals_b : r.vals_a) + b, (fl ? r.vals_b : r.vals_a) + b, 4 * nl,
+                                    cudaMemcpyDeviceToDevice, ss);
+                }
+            }
+        }
     }
     if (ls) {  // join
         for (int j = 0; j < r.n_lanes; ++j) {
@@ -562,30 +586,11 @@ static Sorted run_binning(const dgsm_gaussians_t* g, const dgsm_build_opts_t& o,
         }
     }
     // 4. one stable sort of the (light | tile) digits of all keys (grid: the capacity),
-    //    or — when the per-light key segments are known on the host (the planned build)
-    //    and it saves a pass (cfg5: 3 + 16 bits = 3 passes, 16 bits = 2) — one sort of
-    //    the tile digits per light segment (the keys are emitted grouped by light)
-    const int tb = sh.tile_bits;
-    int ft;
-    if (key_begin_host && sh.n_lights > 1 && (tb + 7) / 8 < (sh.light_bits + tb + 7) / 8) {
-        const int target = onesweep_digits(tb).passes & 1;  // where a sorted segment of > 1 key ends
-        for (int l = 0; l < sh.n_lights; ++l) {
-            const int64_t b = key_begin_host[l], nl = key_begin_host[l + 1] - key_begin_host[l];
-            if (nl <= 0) continue;
-            const int fl = launch_onesweep_u32(r.keys_a + b, r.vals_a + b, r.keys_b + b, r.vals_b + b, nl, tb,
-                                               r.sort_temp, s, &g_launches);
-            if (fl != target) {  // (a segment of one key: no pass ran)
-                cudaMemcpyAsync((target ? r.keys_b : r.keys_a) + b, (fl ? r.keys_b : r.keys_a) + b, 4 * nl,
-                                cudaMemcpyDeviceToDevice, s);
-                cudaMemcpyAsync((target ? r.vals_b : r.vals_a) + b, (fl ? r.vals_b : r.vals_a) + b, 4 * nl,
-                                cudaMemcpyDeviceToDevice, s);
-            }
-        }
-        ft = target;
-    } else {
+    //    unless the lanes sorted each light's segment above
+    int ft = target;
+    if (!per_light_sort)
         ft = launch_onesweep_u32(r.keys_a, r.vals_a, r.keys_b, r.vals_b, sh.cap, sh.light_bits + tb, r.sort_temp, s,
                                  &g_launches, nullptr, nullptr, false, true, r.n_keys);
-    }
     Sorted out{ft ? r.keys_b : r.keys_a, ft ? r.vals_b : r.vals_a};
     // 5. tile ranges
     launch_ranges(out.keys, r.n_keys, sh.cap, sh.tile_bits, (uint32_t)n_tiles, r.tile_start, r.tile_end, s);
