@@ -15,7 +15,7 @@ import json; d=json.load(open('gpurun_out/abv.log')); r=d['roofline']
 acc=d.get('accumulate_ms', d.get('accumulate_ms_rank0'))
 w=d.get('accumulate_work', d.get('accumulate_work_rank0', {}))
 br=w.get('band_records', 0) / max(1, w.get('warp_records', 2) // 2)
-print('$name cfg$c [$v]', 'acc_ms', round(acc,4), 'step', round(d['ms_per_step'],4), 'frac', round(r['frac'],4), 'work', round(r['work_frac'],4), 'band_rec/P', round(br, 4)"
+print('$name cfg$c [$v]', 'acc_ms', round(acc,4), 'step', round(d['ms_per_step'],4), 'frac', round(r['frac'],4), 'work', round(r['work_frac'],4), 'band_rec/P', round(br, 4))"
     done
   done
 done
