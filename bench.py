@@ -599,9 +599,10 @@ def weak_bench(args, ctx):
         e2e = {"value": units_all * K / (te_max * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(m * 4), "ms_per_step": te_max / K,
                "api": ("dgsm.FrameStream (host buffers in, T to a pinned host buffer): frames back to back, "
-                       "frame i+1's uploads on a copy stream from frame i's accumulation on, the build + "
-                       "query as one CUDA-graph replay, T copied back on a second stream; K-frame span "
-                       "(up to the last T copy) minus the L2 flushes"),
+                       "frame i+1's receivers uploaded on a copy stream as soon as its buffer set is free and "
+                       "its Gaussians from frame i's accumulation on, the build + query as one CUDA-graph "
+                       "replay, T copied back on a second stream; K-frame span (up to the last T copy) minus "
+                       "the L2 flushes"),
                "frame_host_ms_per_step": te_fh / K,
                "frame_host_value": units_all * K / (te_fh * 1e-3),
                "isolated_ms_per_frame": float(np.median(iso)),
