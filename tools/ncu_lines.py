@@ -30,7 +30,11 @@ def lines(rep):
 
 
 def main():
-    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    argv = sys.argv[1:]
+    if "--top" in argv:
+        k = argv.index("--top")
+        argv = argv[:k] + argv[k + 2:]
+    args = [a for a in argv if not a.startswith("--")]
     top = int(sys.argv[sys.argv.index("--top") + 1]) if "--top" in sys.argv else 40
     A = lines(args[0])
     if len(args) == 1:
