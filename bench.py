@@ -926,6 +926,47 @@ def sequence_bench(ctx, frames=None, warmup=3, modes=("full", "roi_slab")):
     return out
 
 
+def next_rows_bench(ctx, reps=3):
+    """The NEXT rows measured on cfg4's frame 0 (the paper's own setting, one B200):
+    f3 / ablation D — the unculled build, every Gaussian in every tile,
+    against the light-space-culled build of the same occluders; f2 (P:L190,
+    P:L308-317) — the footprint-averaged query of the 2 M room Gaussians (7-point
+    stencil and 32 Monte Carlo samples) against the centre query.  Device time by
+    CUDA events, L2 flushed before each call; medians of `reps`."""
+    import torch
+    from paper_2601_01660_b200 import dgsm
+    seq = synth.Config4Sequence()
+    res, K = seq.res, seq.K
+    g = dgsm.to_device(seq.frame(0), ctx.dev)
+    out = {"workload": f"cfg4 frame 0: {g['means'].shape[0]} occluders (avatar + prop), 1 light, {res}^2 x {K}; "
+                       f"receivers = the {seq.room['means'].shape[0]} room Gaussians"}
+    atlas = torch.empty((1, K, res, res), dtype=torch.float32, device=ctx.dev)
+    for name, opts in (("culled", dgsm.Options()), ("unculled", dgsm.Options(tile_cull=False))):
+        b = dgsm.Builder(seq.lights, res, K, opts, device=ctx.dev)
+        b(g, atlas)
+        ms = time_fn(lambda: b(g, atlas), reps, ctx)
+        P = dgsm.BuildPlan(g, seq.lights, res, K, opts).n_keys
+        out[f"build_{name}"] = {"ms": ms, "keys_P": int(P), "gaussian_ray_evals_per_s": 64.0 * P / (ms * 1e-3)}
+        del b
+        torch.cuda.empty_cache()
+    out["ablation_d_slowdown"] = out["build_unculled"]["ms"] / out["build_culled"]["ms"]
+    out["paper_ablation_d"] = {"culled_s": 0.13, "unculled_s": 17.1, "slowdown": 17.1 / 0.13,
+                               "source": "PAPER.md:335 (A100, ROI + light-space culling vs no light-space culling)"}
+    dgsm.Builder(seq.lights, res, K, device=ctx.dev)(g, atlas)
+    rg = dgsm.to_device({k: seq.room[k] for k in ("means", "scales", "rotations")}, ctx.dev)
+    m = rg["means"].shape[0]
+    T = torch.empty(m, dtype=torch.float32, device=ctx.dev)
+    fq = {"center": time_fn(lambda: dgsm.query(atlas, seq.lights, rg["means"], out=T), reps, ctx)}
+    z7, w7 = dgsm.footprint_stencil("stencil7")
+    zmc = synth.mc_offsets(32, 3)
+    wmc = np.full(32, 1.0 / 32, np.float32)
+    for name, (z, w) in (("stencil7", (z7, w7)), ("mc32", (zmc, wmc))):
+        fq[name] = time_fn(lambda: dgsm.query_footprint(atlas, seq.lights, rg, z, w, out=T), reps, ctx)
+    out["query_footprint_ms"] = fq
+    out["query_footprint_receivers_per_s"] = {k: m / (v * 1e-3) for k, v in fq.items()}
+    return out
+
+
 def run_dgsm(args):
     import torch
     import torch.distributed as dist
@@ -949,6 +990,11 @@ def run_dgsm(args):
             line["cfg4_sequence"] = sequence_bench(ctx)
         except Exception as e:  # reported, not fatal for the main line
             line["cfg4_sequence"] = {"error": f"{type(e).__name__}: {e}"[:300]}
+    if not args.no_sequence and args.config in (2, 4) and ctx.rank == 0:
+        try:
+            line["next_rows"] = next_rows_bench(ctx)
+        except Exception as e:  # reported, not fatal for the main line
+            line["next_rows"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     if not args.no_strong and args.config == 2:
         # the strong-scaling configuration of BASELINE (cfg5) on the same N GPUs
         try:
