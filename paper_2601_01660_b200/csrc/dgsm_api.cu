@@ -162,9 +162,9 @@ RunLayout run_layout(void* ws, const RunShape& sh) {
     r.vals_a = c.take<uint32_t>(P);
     r.vals_b = c.take<uint32_t>(P);
     r.n_lanes = std::max(1, std::min(sh.n_lights, kLanes));
-    // a lane also runs its lights' tile sorts when a per-light sort saves a pass
-    // (run_binning): its sort temp then covers a light's key segment (<= capacity)
-    const bool lane_tile_sort = sh.n_lights > 1 && (sh.tile_bits + 7) / 8 < (sh.light_bits + sh.tile_bits + 7) / 8;
+    // a lane also runs its lights' tile sorts (planned multi-light builds, run_binning):
+    // its sort temp then covers a light's key segment (<= capacity)
+    const bool lane_tile_sort = sh.n_lights > 1;
     for (int j = 0; j < r.n_lanes; ++j) {
         LaneBufs& b = r.lane[j];
         b.gkeys_a = c.take<uint32_t>(n);
@@ -522,12 +522,12 @@ static Sorted run_binning(const dgsm_gaussians_t* g, const dgsm_build_opts_t& o,
     PassDigits pd0 = onesweep_digits(32);
     pd0.passes = 0;
     // the tile sort per light segment when the host knows the segments (the planned
-    // build) and it saves a pass (cfg5: 3 + 16 bits = 3 passes over all keys, 16 bits
-    // = 2 per light; the keys are emitted grouped by light): in the light's lane,
-    // right after its duplication
+    // build; the keys are emitted grouped by light): in the light's lane, right after
+    // its duplication.  cfg5: 3 + 16 bits = 3 passes over all keys, 16 bits = 2 per light
     const int tb = sh.tile_bits;
-    const bool per_light_sort =
-        key_begin_host && sh.n_lights > 1 && (tb + 7) / 8 < (sh.light_bits + tb + 7) / 8;
+    // (also when it saves no pass: cfg3's 2 + 14 bits, 2 passes either way, 8.58 -> 8.47 ms
+    // from the lanes' overlap)
+    const bool per_light_sort = key_begin_host && sh.n_lights > 1;
     const int target = onesweep_digits(tb).passes & 1;  // where a sorted segment of > 1 key ends
     LaneStreams* ls = nullptr;
     if (r.n_lanes > 1) {  // fork: the lanes start after everything queued on s
