@@ -123,6 +123,25 @@ def test_cfg5_shape_build_every_61st_tile(dg, oracle_mod, cfg5s, staging, monkey
     torch.cuda.empty_cache()
 
 
+def test_cfg5_shape_sync_free_build_every_61st_tile(dg, oracle_mod, cfg5s):
+    """The sync-free build at the cfg5 shape: one onesweep over all 8 lights'
+    (3 + 16)-bit keys (three passes, the top one with 3 light bits) instead of the
+    planned build's per-light tile sorts, capacity 1.25 P; every 61st tile <= 1e-4."""
+    s = cfg5s
+    g = dg.to_device(s.gaussians)
+    P = dg.BuildPlan(g, s.lights, s.res, s.K).n_keys
+    ab = dg.AsyncBuilder(s.lights, s.res, s.K, s.gaussians["means"].shape[0], int(P * 1.25))
+    out = torch.empty((s.L, s.K, s.res, s.res), dtype=torch.float32, device="cuda")
+    ab(g, out)
+    st = ab.status()
+    assert st["n_keys"] == P and not st["overflow"]
+    items = np.arange(0, s.L * (s.res // 8) ** 2, STRIDE)
+    To, _ = oracle_mod.build_tiles(s.gaussians, s.lights, s.res, s.K, items)
+    assert np.abs(tiles_of(out, items) - To).max() <= TOL_T
+    del out, ab
+    torch.cuda.empty_cache()
+
+
 # ---------------------------------------------------------------- onesweep
 def _keys(kind: str, n: int, nbits: int, rng) -> np.ndarray:
     if kind == "uniform":
