@@ -65,8 +65,6 @@ struct PlanLayout {
     PairRec* recs;
     uint32_t* counts;
     uint4* dup;
-    uint64_t* offsets;
-    void* scan_temp;
     PlanStats* stats;
     size_t bytes;
 };
@@ -78,8 +76,6 @@ PlanLayout plan_layout(void* ws, int64_t n, int L) {
     p.recs = c.take<PairRec>(m);
     p.counts = c.take<uint32_t>(m);
     p.dup = c.take<uint4>(m);
-    p.offsets = c.take<uint64_t>(m + 1);
-    p.scan_temp = c.take<char>(scan_u32_to_u64_temp_bytes(m));
     p.stats = c.take<PlanStats>(1);
     p.bytes = c.off;
     return p;
@@ -365,7 +361,6 @@ static void enqueue_plan(const dgsm_gaussians_t* g, const dgsm_gaussians_t* g_ho
                          cudaEvent_t upload_after, const dgsm_light_t* lights, int n_lights, int atlas_res,
                          int n_shells, const dgsm_build_opts_t& o, const PlanLayout& p, cudaStream_t s) {
     const LightsParam lp = lights_param(lights, n_lights);
-    const int64_t m = (int64_t)n_lights * g->n;
 
     launch_project_init(p.stats, s);
     if (g_host && g->n > 0) {
@@ -393,9 +388,9 @@ static void enqueue_plan(const dgsm_gaussians_t* g, const dgsm_gaussians_t* g_ho
         launch_project(*g, lp, n_lights, atlas_res, n_shells, o, 0, g->n, p.recs, p.counts, p.dup, p.stats, s);
         g_launches += 1;
     }
-    // key offsets; the scan also writes light_key_begin[l] = offsets[l n] into the plan stats
-    launch_scan_u32_to_u64_marks(p.counts, p.offsets, m, p.scan_temp, p.stats->light_key_begin, g->n, n_lights, s);
-    g_launches += 1 + kScanLaunches;  // init, scan
+    // the light segments' key begins (per-light totals of the counts) into the plan stats
+    launch_light_begin(p.counts, g->n, n_lights, p.stats->light_key_begin, s);
+    g_launches += 2;  // init, totals
 }
 
 // The plan; with g_host != NULL the Gaussian arrays are first uploaded from

@@ -243,9 +243,8 @@ size_t scan_u32_to_u64_temp_bytes(int64_t n);
 constexpr int kScanLaunches = 2;  // kernels per launch_scan_* call
 void launch_scan_u32_to_u64(const uint32_t* in, uint64_t* out, int64_t n, void* temp, cudaStream_t s);
 void launch_scan_u64(const uint64_t* in, uint64_t* out, int64_t n, void* temp, cudaStream_t s);
-// ... and marks[i] = out[i * mark_stride] for i <= n_marks (written by the scan itself)
-void launch_scan_u32_to_u64_marks(const uint32_t* in, uint64_t* out, int64_t n, void* temp, uint64_t* marks,
-                                  int64_t mark_stride, int n_marks, cudaStream_t s);
+// the plan's light segment begins: begin[l + 1] += the key counts of lights <= l
+void launch_light_begin(const uint32_t* counts, int64_t n, int n_lights, uint64_t* begin, cudaStream_t s);
 // dup[l*n + i] = {fp32 bits of D, c0 | c1 << 16, r0 | r1 << 16, tile count} (16 B per (light, Gaussian))
 
 void launch_gather_counts(const uint32_t* counts, const uint32_t* perm, int64_t n, uint32_t* cperm,

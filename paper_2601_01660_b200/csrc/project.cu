@@ -216,12 +216,13 @@ __global__ void k_init_stats(PlanStats* stats) {
     pdl_begin();
     int t = threadIdx.x;
     if (t < DGSM_MAX_LIGHTS) { stats->depth_min[t] = 0xffffffffu; stats->depth_max[t] = 0u; }
+    if (t <= DGSM_MAX_LIGHTS) stats->light_key_begin[t] = 0ull;  // k_light_begin adds the totals
     if (t == 0) { stats->n_invalid = 0u; stats->first_invalid = 0xffffffffu; }
 }
 }  // namespace
 
 void launch_project_init(PlanStats* stats, cudaStream_t s) {
-    pdl_launch(k_init_stats, 1, DGSM_MAX_LIGHTS, 0, s, stats);
+    pdl_launch(k_init_stats, 1, DGSM_MAX_LIGHTS + 1, 0, s, stats);
 }
 
 void launch_project(const dgsm_gaussians_t& g, const LightsParam& lp, int n_lights, int res, int K,

@@ -1,5 +1,8 @@
 // scan.cu — exclusive prefix sums (reduce-then-scan, 2 launches) used for the
-// per-(light, Gaussian) key offsets and the per-tile work-unit offsets.
+// per-Gaussian key offsets in depth-rank order and the per-tile work-unit
+// offsets; the plan's per-light key totals (a segmented reduction).
+#include <algorithm>
+
 #include "dgsm_internal.cuh"
 
 namespace dgsm {
@@ -67,8 +70,7 @@ __global__ void __launch_bounds__(kScanThreads) k_reduce(const T* __restrict__ i
 template <typename T, typename O>
 __global__ void __launch_bounds__(kScanThreads) k_downsweep(const T* __restrict__ in, int64_t n, int64_t tpb,
                                                             const uint64_t* __restrict__ partials,
-                                                            O* __restrict__ out, uint64_t* __restrict__ marks,
-                                                            int64_t mark_stride, int n_marks) {
+                                                            O* __restrict__ out) {
     pdl_begin();
     // padded: element e at e + e/16, so the blocked accesses (stride 16) spread over banks
     __shared__ uint64_t tile[kScanTile + kScanTile / kScanItems];
@@ -108,38 +110,67 @@ __global__ void __launch_bounds__(kScanThreads) k_downsweep(const T* __restrict_
             const int64_t k = base + (int64_t)j * kScanThreads + threadIdx.x;
             if (k < n) out[k] = (O)tile[at(j * kScanThreads + threadIdx.x)];
         }
-        // marks[i] = out[i * mark_stride] (i <= n_marks; the plan's per-light key begins)
-        if (marks && threadIdx.x <= (unsigned)n_marks) {
-            const int64_t k = (int64_t)threadIdx.x * mark_stride;
-            if (k >= base && k < base + kScanTile && k < n) marks[threadIdx.x] = tile[at((int)(k - base))];
-        }
         carry += total;
         if (base + kScanTile >= n && threadIdx.x == 0) out[n] = (O)carry;
-        if (base + kScanTile >= n && marks && threadIdx.x <= (unsigned)n_marks &&
-            (int64_t)threadIdx.x * mark_stride >= n)
-            marks[threadIdx.x] = carry;
         __syncthreads();
     }
 }
 
 template <typename T, typename O>
-void scan_impl(const T* in, O* out, int64_t n, void* temp, cudaStream_t s, uint64_t* marks = nullptr,
-               int64_t mark_stride = 1, int n_marks = 0) {
+void scan_impl(const T* in, O* out, int64_t n, void* temp, cudaStream_t s) {
     uint64_t* partials = (uint64_t*)temp;
     if (n == 0) {
         cudaMemsetAsync(out, 0, sizeof(O), s);
-        if (marks) cudaMemsetAsync(marks, 0, sizeof(uint64_t) * (n_marks + 1), s);
         return;
     }
     const int64_t tiles = (n + kScanTile - 1) / kScanTile;
     const int64_t tpb = (tiles + kMaxBlocks - 1) / kMaxBlocks;
     const int64_t nb = (tiles + tpb - 1) / tpb;
     pdl_launch(k_reduce<T>, (unsigned)nb, kScanThreads, 0, s, in, n, tpb, partials);
-    pdl_launch(k_downsweep<T, O>, (unsigned)nb, kScanThreads, 0, s, in, n, tpb, partials, out, marks, mark_stride,
-                                                            n_marks);
+    pdl_launch(k_downsweep<T, O>, (unsigned)nb, kScanThreads, 0, s, in, n, tpb, partials, out);
+}
+
+// Per-light key totals of the plan: only the light segments' begins are used
+// downstream (the per-Gaussian offsets are scanned in depth-rank order by the
+// run), so a reduction replaces the full scan.  Each block sums a contiguous
+// range of counts per light segment, then thread t adds the block's total of
+// the lights < t + 1 to begin[t + 1] (begin zeroed by the plan's init kernel).
+__global__ void __launch_bounds__(kScanThreads) k_light_begin(const uint32_t* __restrict__ counts, int64_t n,
+                                                              int n_lights, uint64_t* begin) {
+    pdl_begin();
+    __shared__ unsigned long long s_tot[DGSM_MAX_LIGHTS];
+    if (threadIdx.x < DGSM_MAX_LIGHTS) s_tot[threadIdx.x] = 0ull;
+    __syncthreads();
+    const int64_t m = n * n_lights;
+    const int64_t per = (m + gridDim.x - 1) / gridDim.x;
+    const int64_t a = (int64_t)blockIdx.x * per, e = a + per < m ? a + per : m;
+    for (int64_t seg = a; seg < e;) {  // block-uniform loop over the light segments of [a, e)
+        const int l = (int)(seg / n);
+        const int64_t se = (int64_t)(l + 1) * n < e ? (int64_t)(l + 1) * n : e;
+        uint64_t t = 0;
+#pragma unroll 4
+        for (int64_t j = seg + threadIdx.x; j < se; j += kScanThreads) t += counts[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if ((threadIdx.x & 31) == 0 && t) atomicAdd(&s_tot[l], (unsigned long long)t);
+        seg = se;
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < n_lights) {
+        unsigned long long pre = 0ull;
+        for (int l = 0; l <= (int)threadIdx.x; ++l) pre += s_tot[l];
+        if (pre) atomicAdd(reinterpret_cast<unsigned long long*>(begin + threadIdx.x + 1), pre);
+    }
 }
 
 }  // namespace
+
+void launch_light_begin(const uint32_t* counts, int64_t n, int n_lights, uint64_t* begin, cudaStream_t s) {
+    const int64_t m = n * n_lights;
+    if (m <= 0) return;
+    const int64_t blocks = std::min<int64_t>((m + kScanThreads * 8 - 1) / (kScanThreads * 8), 148 * 8);
+    pdl_launch(k_light_begin, (unsigned)blocks, kScanThreads, 0, s, counts, n, n_lights, begin);
+}
 
 size_t scan_u32_to_u64_temp_bytes(int64_t n) {
     return sizeof(uint64_t) * (size_t)((n + kScanTile - 1) / kScanTile + 2);
@@ -151,11 +182,6 @@ void launch_scan_u32_to_u64(const uint32_t* in, uint64_t* out, int64_t n, void* 
 
 void launch_scan_u64(const uint64_t* in, uint64_t* out, int64_t n, void* temp, cudaStream_t s) {
     scan_impl<uint64_t, uint64_t>(in, out, n, temp, s);
-}
-
-void launch_scan_u32_to_u64_marks(const uint32_t* in, uint64_t* out, int64_t n, void* temp, uint64_t* marks,
-                                  int64_t mark_stride, int n_marks, cudaStream_t s) {
-    scan_impl<uint32_t, uint64_t>(in, out, n, temp, s, marks, mark_stride, n_marks);
 }
 
 }  // namespace dgsm
