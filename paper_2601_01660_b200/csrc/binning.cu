@@ -30,8 +30,14 @@ __device__ __forceinline__ void unpack_rect(const uint4& r, int& c0, int& c1, in
 __global__ void __launch_bounds__(256) k_depth_keys(const uint4* __restrict__ dup, int64_t n,
                                                     const uint32_t* __restrict__ dmin_dev,
                                                     uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                                                    PassDigits pd, uint32_t* __restrict__ hist) {
+                                                    PassDigits pd, uint32_t* __restrict__ hist,
+                                                    const PassDigits* __restrict__ pd_dev) {
     pdl_begin();
+    if (pd_dev)  // the device's digit plan (same pass count)
+        for (int p = 0; p < pd.passes; ++p) {
+            pd.shift[p] = pd_dev->shift[p];
+            pd.bits[p] = pd_dev->bits[p];
+        }
     __shared__ uint32_t sh[kSortMaxPasses][kSortRadix];
     const uint32_t dmin = *dmin_dev;  // the light's smallest depth key (the plan's reduction, on the device)
     for (int t = threadIdx.x; t < pd.passes * kSortRadix; t += blockDim.x) (&sh[0][0])[t] = 0u;
@@ -208,9 +214,25 @@ __global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ key
 // against the workspace capacity; n_keys = P, or 0 with the overflow flag set
 // when P exceeds it (the atlas is then all 1 and must be rebuilt with a larger
 // workspace); the caller's status word receives both.
-__global__ void k_run_setup(const PlanStats* __restrict__ ps, int n_lights, uint64_t capacity,
-                            uint64_t* __restrict__ n_keys, dgsm_build_status_t* status) {
+__global__ void k_run_setup(PlanStats* __restrict__ ps, int n_lights, uint64_t capacity,
+                            uint64_t* __restrict__ n_keys, dgsm_build_status_t* status, int depth_passes) {
     pdl_begin();
+    // sync-free build (depth_passes > 0): each light's depth keys (D bits - the
+    // light's minimum) have bits(max - min) significant bits, known only here; they
+    // are split evenly over the passes the host launched, as the planned build
+    // splits them (digits that cannot occur stay out of the look-back)
+    for (int l = 0; l < (depth_passes ? n_lights : 0); ++l) {
+        const uint32_t lo = ps->depth_min[l], hi = ps->depth_max[l];
+        const int db = hi > lo ? 32 - __clz(hi - lo) : 0;
+        PassDigits& pd = ps->depth_pd[l];
+        pd.passes = depth_passes;
+        for (int p = 0, sh = 0; p < kSortMaxPasses; ++p) {
+            const int b = p < depth_passes ? db / depth_passes + (p < db % depth_passes ? 1 : 0) : 0;
+            pd.shift[p] = sh;
+            pd.bits[p] = b;
+            sh += b;
+        }
+    }
     const uint64_t P = ps->light_key_begin[n_lights];
     const bool over = P > capacity;
     *n_keys = over ? 0ull : P;
@@ -413,15 +435,15 @@ __global__ void __launch_bounds__(kFusedThreads) k_units_fused(const uint32_t* _
 }  // namespace
 
 void launch_depth_keys(const uint4* dup, int64_t n, const uint32_t* dmin_dev, uint32_t* keys, uint32_t* vals,
-                       const PassDigits& pd, uint32_t* hist, cudaStream_t s) {
+                       const PassDigits& pd, uint32_t* hist, cudaStream_t s, const PassDigits* pd_dev) {
     if (n <= 0) return;
     const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 4);
-    pdl_launch(k_depth_keys, (unsigned)blocks, 256, 0, s, dup, n, dmin_dev, keys, vals, pd, hist);
+    pdl_launch(k_depth_keys, (unsigned)blocks, 256, 0, s, dup, n, dmin_dev, keys, vals, pd, hist, pd_dev);
 }
 
-void launch_run_setup(const PlanStats* ps, int n_lights, uint64_t capacity, uint64_t* n_keys,
-                      dgsm_build_status_t* status, cudaStream_t s) {
-    pdl_launch(k_run_setup, 1, 1, 0, s, ps, n_lights, capacity, n_keys, status);
+void launch_run_setup(PlanStats* ps, int n_lights, uint64_t capacity, uint64_t* n_keys,
+                      dgsm_build_status_t* status, cudaStream_t s, int depth_passes) {
+    pdl_launch(k_run_setup, 1, 1, 0, s, ps, n_lights, capacity, n_keys, status, depth_passes);
 }
 
 void launch_gather_counts(const uint32_t* counts, const uint32_t* perm, int64_t n, uint32_t* cperm,

@@ -512,7 +512,11 @@ static Sorted run_binning(const dgsm_gaussians_t* g, const dgsm_build_opts_t& o,
     const int64_t n = g->n;
     const int64_t n_tiles = (int64_t)(res / kTile) * (res / kTile);
     // (tile ranges zeroed by the caller's run memset)
-    launch_run_setup(p.stats, sh.n_lights, (uint64_t)sh.cap, r.n_keys, status, s);
+    // (sync-free builds: the depth digits are planned on the device from the plan's depth range)
+    bool dev_digits = false;
+    for (int l = 0; l < sh.n_lights; ++l) dev_digits |= sh.depth_bits[l] == 32;
+    launch_run_setup(p.stats, sh.n_lights, (uint64_t)sh.cap, r.n_keys, status, s,
+                     dev_digits ? onesweep_digits(32).passes : 0);
     g_launches += 1;
     PassDigits pd0 = onesweep_digits(32);
     pd0.passes = 0;
@@ -543,9 +547,10 @@ static Sorted run_binning(const dgsm_gaussians_t* g, const dgsm_build_opts_t& o,
             //    digit histograms; the sort's last pass gathers the key counts into
             //    depth-rank order)
             uint32_t* hist = onesweep_prepare(lb.sort_temp, n, ss);
-            launch_depth_keys(dup, n, p.stats->depth_min + l, lb.gkeys_a, lb.gvals_a, pd, hist, ss);
+            const PassDigits* pd_dev = db == 32 ? p.stats->depth_pd + l : nullptr;
+            launch_depth_keys(dup, n, p.stats->depth_min + l, lb.gkeys_a, lb.gvals_a, pd, hist, ss, pd_dev);
             const int fl = launch_onesweep_u32(lb.gkeys_a, lb.gvals_a, lb.gkeys_b, lb.gvals_b, n, db, lb.sort_temp, ss,
-                                               &g_launches, counts_l, lb.cperm, true);
+                                               &g_launches, counts_l, lb.cperm, true, true, nullptr, pd_dev);
             perm = fl ? lb.gvals_b : lb.gvals_a;
             g_launches += 1;
         } else {

@@ -52,12 +52,21 @@ struct ShParam {
     int d;
 };
 
+// Digit plan of an onesweep sort: pass p sorts key bits [shift[p], shift[p] + bits[p]).
+constexpr int kSortRadix = 256;
+constexpr int kSortMaxPasses = 8;
+struct PassDigits {
+    int shift[kSortMaxPasses], bits[kSortMaxPasses];
+    int passes;
+};
+
 // Device-side statistics of a plan, copied back to the host once.
 struct PlanStats {
     uint32_t depth_min[DGSM_MAX_LIGHTS];
     uint32_t depth_max[DGSM_MAX_LIGHTS];
     uint64_t light_key_begin[DGSM_MAX_LIGHTS + 1];
     uint32_t n_invalid, first_invalid;  // DGSM_VALIDATE: invalid Gaussians, the smallest invalid index
+    PassDigits depth_pd[DGSM_MAX_LIGHTS];  // sync-free build: the depth sort's digits (k_run_setup)
 };
 
 // Work unit of the accumulation kernel: one chunk of one (light, tile) list.
@@ -263,21 +272,15 @@ int launch_onesweep(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t
 // key: 6 + 6).  onesweep_prepare clears the sort's histograms, partition
 // counters and first status buffer and returns the histograms [passes][256]; a
 // key producer may fill them (hist_ready) instead of the sort's own k_hist.
-constexpr int kSortRadix = 256;
-constexpr int kSortMaxPasses = 8;
-struct PassDigits {
-    int shift[kSortMaxPasses], bits[kSortMaxPasses];
-    int passes;
-};
 PassDigits onesweep_digits(int nbits);
 uint32_t* onesweep_prepare(void* temp, int64_t n, cudaStream_t s);
 // depth keys (fp32 bits of D - the light's minimum, read on the device) of one light's
 // Gaussians + their digit histograms into hist (pd.passes = 0: none)
 void launch_depth_keys(const uint4* dup, int64_t n, const uint32_t* dmin_dev, uint32_t* keys, uint32_t* vals,
-                       const PassDigits& pd, uint32_t* hist, cudaStream_t s);
+                       const PassDigits& pd, uint32_t* hist, cudaStream_t s, const PassDigits* pd_dev = nullptr);
 // n_keys = P (light_key_begin[n_lights], device) or 0 + overflow when P > capacity
-void launch_run_setup(const PlanStats* ps, int n_lights, uint64_t capacity, uint64_t* n_keys,
-                      dgsm_build_status_t* status, cudaStream_t s);
+void launch_run_setup(PlanStats* ps, int n_lights, uint64_t capacity, uint64_t* n_keys,
+                      dgsm_build_status_t* status, cudaStream_t s, int depth_passes = 0);
 // (gsrc/gdst optional: the last pass also writes gdst[o] = gsrc[value] at each output
 // position o, i.e. a gather by the sorted permutation; only when nbits > 0 and n > 1.
 // top_match: rank the top pass with match.any (few distinct digits per warp, as in
@@ -285,7 +288,7 @@ void launch_run_setup(const PlanStats* ps, int n_lights, uint64_t capacity, uint
 int launch_onesweep_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n,
                         int nbits, void* temp, cudaStream_t s, int* launches, const uint32_t* gsrc = nullptr,
                         uint32_t* gdst = nullptr, bool hist_ready = false, bool top_match = true,
-                        const uint64_t* n_dev = nullptr);
+                        const uint64_t* n_dev = nullptr, const PassDigits* pd_dev = nullptr);
 void launch_decode_keys(const uint32_t* keys, const uint32_t* vals, const uint4* dup, const dgsm_plan_t& plan,
                         uint32_t* light_out, uint32_t* tile_out, uint32_t* depth_out, uint32_t* index_out,
                         cudaStream_t s);

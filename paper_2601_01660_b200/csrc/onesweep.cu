@@ -132,8 +132,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ k
                                                       uint32_t* status, uint32_t* status_next,
                                                       uint32_t* part_ctr, const uint32_t* __restrict__ gsrc,
                                                       uint32_t* __restrict__ gdst,
-                                                      const uint64_t* __restrict__ n_dev) {
+                                                      const uint64_t* __restrict__ n_dev,
+                                                      const PassDigits* __restrict__ pd_dev, int pass) {
     pdl_begin();
+    if (pd_dev) {  // the digit plan made on the device (sync-free build: the depth range)
+        shift = pd_dev->shift[pass];
+        bits = pd_dev->bits[pass];
+    }
     extern __shared__ __align__(16) unsigned char os_smem[];
     KeyT* s_keys = reinterpret_cast<KeyT*>(os_smem);
     uint32_t* s_vals = reinterpret_cast<uint32_t*>(os_smem + sizeof(KeyT) * kTileKeys);
@@ -278,7 +283,7 @@ template <typename KeyT>
 int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt, int64_t n, int nbits,
                   void* temp, cudaStream_t s, int* launches, const uint32_t* gsrc = nullptr,
                   uint32_t* gdst = nullptr, bool hist_ready = false, bool top_match = true,
-                  const uint64_t* n_dev = nullptr) {
+                  const uint64_t* n_dev = nullptr, const PassDigits* pd_dev = nullptr) {
     // n: the key count, or (n_dev != NULL) the capacity the grid is sized for while
     // the kernels read the count from n_dev (no host synchronisation)
     if (n <= 1 || nbits <= 0) return 0;
@@ -311,7 +316,7 @@ int onesweep_impl(KeyT* keys, uint32_t* vals, KeyT* keys_alt, uint32_t* vals_alt
                                                            top_match && p == passes - 1, t.hist + p * kRadix,
                                                            t.status[p & 1], t.status[(p + 1) & 1],
                                                            t.part_ctr + p, gsrc, p == passes - 1 ? gdst : nullptr,
-                                                           n_dev);
+                                                           n_dev, pd_dev, p);
         *launches += 1;
         KeyT* tk = ki; ki = ko; ko = tk;
         uint32_t* tv = vi; vi = vo; vo = tv;
@@ -333,9 +338,10 @@ int launch_onesweep(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t
 
 int launch_onesweep_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n,
                         int nbits, void* temp, cudaStream_t s, int* launches, const uint32_t* gsrc,
-                        uint32_t* gdst, bool hist_ready, bool top_match, const uint64_t* n_dev) {
+                        uint32_t* gdst, bool hist_ready, bool top_match, const uint64_t* n_dev,
+                        const PassDigits* pd_dev) {
     return onesweep_impl<uint32_t>(keys, vals, keys_alt, vals_alt, n, nbits, temp, s, launches, gsrc, gdst,
-                                   hist_ready, top_match, n_dev);
+                                   hist_ready, top_match, n_dev, pd_dev);
 }
 
 PassDigits onesweep_digits(int nbits) {

@@ -24,7 +24,27 @@ def dg():
     return dgsm
 
 
+def _depth_scene(name, n, d0, d1, seed):
+    """Gaussians around one light at the origin with light distances in [d0, d1]
+    (d0 == d1: six axis points at one exact distance): the sync-free build's depth
+    digits, planned on the device from the depth range, at 0 and ~9 significant bits."""
+    rng = np.random.Generator(np.random.PCG64(4242 + seed))
+    if d0 == d1:
+        axes = np.array([[1, 0, 0], [-1, 0, 0], [0, 1, 0], [0, -1, 0], [0, 0, 1], [0, 0, -1]], np.float64)
+        v = axes[np.arange(n) % 6]
+    else:
+        v = rng.standard_normal((n, 3))
+        v /= np.linalg.norm(v, axis=1, keepdims=True)
+    mu = v * rng.uniform(d0, d1, n)[:, None] if d0 != d1 else v * d0
+    g = synth._gaussians(mu, np.exp(rng.uniform(np.log(0.05), np.log(0.4), (n, 3))),
+                         synth.random_quaternions(rng, n), rng.uniform(0.1, 0.9, n))
+    lights = dict(position=np.zeros((1, 3), np.float32), t_max=np.array([4.0], np.float32))
+    return synth.Scene(name, g, lights, 32, 8, g["means"].copy())
+
+
 SCENES = {
+    "equal-depth": lambda: _depth_scene("equal-depth", 60, 2.0, 2.0, 0),
+    "narrow-depth": lambda: _depth_scene("narrow-depth", 500, 2.0, 2.0001, 1),
     "cfg1": lambda: synth.config1(),
     "random-3lights": lambda: synth.random_scene(11, 400, res=32, K=8, L=3, dist=(0.3, 3.0), scale=(0.01, 0.5)),
     "cfg2-small": lambda: synth.config2(scale=0.004, res=64, K=16),
