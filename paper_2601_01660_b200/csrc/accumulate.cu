@@ -213,7 +213,7 @@ __device__ __forceinline__ void lds_f2x2(uint32_t a, f2_t& x, f2_t& y) {
 }
 
 // Compact record pair: 20 packed fields (A, B), 160 B; field order
-//  0-2 f = fl32(d_i - d_c), 3 r_cut/D^2, 4-6 g = W d_i, 7 D, 8-16 W (row-major),
+//  0-2 -W f (f = fl32(d_i - d_c)), 3 r_cut/D^2, 4-6 g = W d_i, 7 D, 8-16 W (row-major),
 //  17 e_D, 18 beta sqrt(pi/2), 19 k_D (int bits)
 constexpr int kPairFields = 20;
 constexpr int kPairBytes = kPairFields * 8;
@@ -229,10 +229,10 @@ __device__ __forceinline__ PairTest2 pair_test2(uint32_t addr, f2_t ETX, f2_t ET
     f2_t F[kPairFields];
 #pragma unroll
     for (int j = 0; j < kPairFields / 2; ++j) lds_f2x2(addr + 16 * j, F[2 * j], F[2 * j + 1]);
-    const f2_t EX = f2sub(ETX, F[0]), EY = f2sub(ETY, F[1]), EZ = f2sub(ETZ, F[2]);
-    const f2_t WX = f2fma(F[8], EX, f2fma(F[9], EY, f2mul(F[10], EZ)));
-    const f2_t WY = f2fma(F[11], EX, f2fma(F[12], EY, f2mul(F[13], EZ)));
-    const f2_t WZ = f2fma(F[14], EX, f2fma(F[15], EY, f2mul(F[16], EZ)));
+    // W delta = W e_t - W f: one FMA chain from the record's -W f
+    const f2_t WX = f2fma(F[8], ETX, f2fma(F[9], ETY, f2fma(F[10], ETZ, F[0])));
+    const f2_t WY = f2fma(F[11], ETX, f2fma(F[12], ETY, f2fma(F[13], ETZ, F[1])));
+    const f2_t WZ = f2fma(F[14], ETX, f2fma(F[15], ETY, f2fma(F[16], ETZ, F[2])));
     const f2_t UX = f2add(F[4], WX), UY = f2add(F[5], WY), UZ = f2add(F[6], WZ);
     const f2_t A = f2fma(UX, UX, f2fma(UY, UY, f2mul(UZ, UZ)));
     const f2_t Z = 0ull;
@@ -552,6 +552,12 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(  // 11 CTAs/SM at K = 
                         (float)(int)ru[5].x};                                                       // kD
 #pragma unroll
                     for (int f = 0; f < kPairFields; ++f) v[f] = vv[f];
+                }
+                {  // fields 0-2: -W f, f = d_i - d_c (the pair test forms W delta = W e_t - W f)
+                    const float f0 = v[0], f1 = v[1], f2 = v[2];
+                    v[0] = -fmaf(v[8], f0, fmaf(v[9], f1, v[10] * f2));
+                    v[1] = -fmaf(v[11], f0, fmaf(v[12], f1, v[13] * f2));
+                    v[2] = -fmaf(v[14], f0, fmaf(v[15], f1, v[16] * f2));
                 }
 #pragma unroll
                 for (int f = 0; f < kPairFields; ++f) q[2 * f] = v[f];
@@ -878,6 +884,12 @@ __global__ void __launch_bounds__(kThreads, kAccMinBlocks) k_accumulate_band(
                             (float)(int)ru[5].x};                                                       // kD
 #pragma unroll
                         for (int f = 0; f < kPairFields; ++f) v[f] = vv[f];
+                    }
+                    {  // fields 0-2: -W f, f = d_i - d_c (the pair test forms W delta = W e_t - W f)
+                        const float f0 = v[0], f1 = v[1], f2 = v[2];
+                        v[0] = -fmaf(v[8], f0, fmaf(v[9], f1, v[10] * f2));
+                        v[1] = -fmaf(v[11], f0, fmaf(v[12], f1, v[13] * f2));
+                        v[2] = -fmaf(v[14], f0, fmaf(v[15], f1, v[16] * f2));
                     }
 #pragma unroll
                     for (int f = 0; f < kPairFields; ++f) q[2 * f] = v[f];
