@@ -213,14 +213,14 @@ __device__ __forceinline__ void lds_f2x2(uint32_t a, f2_t& x, f2_t& y) {
 }
 
 // Compact record pair: 20 packed fields (A, B), 160 B; field order
-//  0-2 -W f (f = fl32(d_i - d_c)), 3 r_cut/D^2, 4-6 g = W d_i, 7 D, 8-16 W (row-major),
+//  0-2 -W f (f = fl32(d_i - d_c)), 3 r_cut/D^2, 4-6 g = W d_i, 7 -D, 8-16 W (row-major),
 //  17 e_D, 18 beta sqrt(pi/2), 19 k_D (int bits)
 constexpr int kPairFields = 20;
 constexpr int kPairBytes = kPairFields * 8;
 
 struct PairTest2 {
     f2_t A, C2, DOT;      // a = |u|^2, |g x W delta|^2, u . W delta  (records A | B)
-    f2_t D, ED, BP;       // D, e_D, beta sqrt(pi/2)
+    f2_t ND, ED, BP;      // -D, e_D, beta sqrt(pi/2)
     f2_t KD;              // anchor shell k_D (as float)
     bool liveA, liveB;
 };
@@ -246,7 +246,7 @@ __device__ __forceinline__ PairTest2 pair_test2(uint32_t addr, f2_t ETX, f2_t ET
     R.A = A;
     R.C2 = C2;
     R.DOT = f2fma(UX, WX, f2fma(UY, WY, f2mul(UZ, WZ)));  // u . W delta (closest approach)
-    R.D = F[7]; R.ED = F[17]; R.BP = F[18];
+    R.ND = F[7]; R.ED = F[17]; R.BP = F[18];
     R.KD = F[19];
     R.liveA = f2lo(C2) <= f2lo(T);
     R.liveB = f2hi(C2) <= f2hi(T);
@@ -275,17 +275,17 @@ __device__ __forceinline__ bool band_live(int khi, int kb0, int nrows, int K) { 
 // discard.  The first window shell is evaluated unconditionally, further
 // shells in a rarely taken loop.
 template <bool kStats, bool kBand>
-__device__ __forceinline__ void pair_live_warp(float pa, float pc2, float pdot, bool live, float D, float eD,
+__device__ __forceinline__ void pair_live_warp(float pa, float pc2, float pdot, bool live, float ND, float eD,
                                                float betap, float kD, uint32_t acc_base, int K, float dt, float dtlo, float idt,
                                                int kb0, int nrows, int wlo, int whi,
                                                uint32_t& st_live, uint32_t& st_win, uint32_t& st_step) {
     const float ia = rcp_approx(pa);
     const float r_over_D2 = pc2 * ia;
-    const float rr = r_over_D2 * D * D;
-    const float sD = -D * pdot * ia;
+    const float rr = r_over_D2 * ND * ND;
+    const float sD = ND * pdot * ia;  // s* - D (ND = -D)
     const float ra = rsqrt_approx(pa);
     const float h = 0.70710678118654752f * pa * ra;
-    const float x0 = -h * (D + sD);
+    const float x0 = h * (ND - sD);  // -h (D + s* - D)
     float e0 = -1.0f;
     if (__any_sync(0xffffffffu, x0 > -kXS)) {  // a Gaussian near the light (rare): uniform branch
         const float t = erf_fast(x0);
@@ -386,18 +386,17 @@ __device__ __forceinline__ void live_finish(bool live, int klo, int khi, float f
 // Setup and first window shell packed; the shared-memory updates per half, A
 // before B (the summation order of the scalar path when both are one texel).
 template <bool kStats, bool kBand>
-__device__ __forceinline__ void live_packed(f2_t A2, f2_t C2, f2_t DOT, f2_t D2, f2_t ED2, f2_t BP2, f2_t KD,
+__device__ __forceinline__ void live_packed(f2_t A2, f2_t C2, f2_t DOT, f2_t ND2, f2_t ED2, f2_t BP2, f2_t KD,
                                             bool liveA_in, bool liveB_in, uint32_t baseA, uint32_t baseB, int K,
                                             float dt, float dtlo, float idt, int kb0, int nrows, int wlo, int whi,
                                             uint32_t& st_live, uint32_t& st_win, uint32_t& st_step) {
-    const f2_t Z = 0ull;
     const float aA = f2lo(A2), aB = f2hi(A2);
     const f2_t IA = f2pack(rcp_approx(aA), rcp_approx(aB));
     const f2_t RA = f2pack(rsqrt_approx(aA), rsqrt_approx(aB));
-    const f2_t RR = f2mul(f2mul(f2mul(C2, IA), D2), D2);
-    const f2_t SD = f2mul(f2mul(f2sub(Z, D2), DOT), IA);
+    const f2_t RR = f2mul(f2mul(f2mul(C2, IA), ND2), ND2);
+    const f2_t SD = f2mul(f2mul(ND2, DOT), IA);  // s* - D = -D (u . W delta) / a
     const f2_t H = f2mul(f2mul(f2bc(0.70710678118654752f), A2), RA);
-    const f2_t X0 = f2mul(f2sub(Z, H), f2add(D2, SD));
+    const f2_t X0 = f2mul(H, f2sub(ND2, SD));  // -h (D + s* - D)
     float e0A = -1.0f, e0B = -1.0f;
     const float x0A = f2lo(X0), x0B = f2hi(X0);
     if (__any_sync(0xffffffffu, x0A > -kXS || x0B > -kXS)) {
@@ -412,7 +411,7 @@ __device__ __forceinline__ void live_packed(f2_t A2, f2_t C2, f2_t DOT, f2_t D2,
     const f2_t E = f2sub(ED2, SD);
     const f2_t XSH = f2mul(f2bc(kXS * 1.41421356237309505f), RA);
     const f2_t KDH = f2add(KD, f2bc(0.5f));
-    const f2_t KLO = f2fma(f2sub(f2sub(Z, XSH), E), f2bc(idt), KDH);
+    const f2_t KLO = f2fma(f2add(XSH, E), f2bc(-idt), KDH);
     const f2_t KHI = f2fma(f2sub(XSH, E), f2bc(idt), KDH);
     const f2_t YLO = kBand ? win_round2_b(KLO, wlo, whi) : win_round2(KLO, K);
     const f2_t YHI = kBand ? win_round2_b(KHI, wlo, whi) : win_round2(KHI, K);
@@ -432,7 +431,7 @@ template <bool kStats, bool kBand>
 __device__ __forceinline__ void pair_live_warp2(const PairTest2& T, uint32_t acc_base, int K, float dt, float dtlo,
                                                 float idt, int kb0, int nrows, int wlo, int whi, uint32_t& st_live,
                                                 uint32_t& st_win, uint32_t& st_step) {
-    live_packed<kStats, kBand>(T.A, T.C2, T.DOT, T.D, T.ED, T.BP, T.KD, T.liveA, T.liveB, acc_base, acc_base, K, dt,
+    live_packed<kStats, kBand>(T.A, T.C2, T.DOT, T.ND, T.ED, T.BP, T.KD, T.liveA, T.liveB, acc_base, acc_base, K, dt,
                                dtlo, idt, kb0, nrows, wlo, whi, st_live, st_win, st_step);
 }
 
@@ -553,11 +552,12 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(  // 11 CTAs/SM at K = 
 #pragma unroll
                     for (int f = 0; f < kPairFields; ++f) v[f] = vv[f];
                 }
-                {  // fields 0-2: -W f, f = d_i - d_c (the pair test forms W delta = W e_t - W f)
+                {  // fields 0-2: -W f, f = d_i - d_c (the pair test forms W delta = W e_t - W f); 7: -D
                     const float f0 = v[0], f1 = v[1], f2 = v[2];
                     v[0] = -fmaf(v[8], f0, fmaf(v[9], f1, v[10] * f2));
                     v[1] = -fmaf(v[11], f0, fmaf(v[12], f1, v[13] * f2));
                     v[2] = -fmaf(v[14], f0, fmaf(v[15], f1, v[16] * f2));
+                    v[7] = -v[7];
                 }
 #pragma unroll
                 for (int f = 0; f < kPairFields; ++f) q[2 * f] = v[f];
@@ -585,11 +585,11 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(  // 11 CTAs/SM at K = 
                     return;
                 }
                 if (anyA)
-                    pair_live_warp<kStats, false>(f2lo(T2.A), f2lo(T2.C2), f2lo(T2.DOT), T2.liveA, f2lo(T2.D),
+                    pair_live_warp<kStats, false>(f2lo(T2.A), f2lo(T2.C2), f2lo(T2.DOT), T2.liveA, f2lo(T2.ND),
                                                   f2lo(T2.ED), f2lo(T2.BP), f2lo(T2.KD), acc_base, K, dt, dtlo, idt, 0, K,
                                                   0, 0, st_live, st_win, st_step);
                 if (anyB)
-                    pair_live_warp<kStats, false>(f2hi(T2.A), f2hi(T2.C2), f2hi(T2.DOT), T2.liveB, f2hi(T2.D),
+                    pair_live_warp<kStats, false>(f2hi(T2.A), f2hi(T2.C2), f2hi(T2.DOT), T2.liveB, f2hi(T2.ND),
                                                   f2hi(T2.ED), f2hi(T2.BP), f2hi(T2.KD), acc_base, K, dt, dtlo, idt, 0, K,
                                                   0, 0, st_live, st_win, st_step);
             };
@@ -885,11 +885,12 @@ __global__ void __launch_bounds__(kThreads, kAccMinBlocks) k_accumulate_band(
 #pragma unroll
                         for (int f = 0; f < kPairFields; ++f) v[f] = vv[f];
                     }
-                    {  // fields 0-2: -W f, f = d_i - d_c (the pair test forms W delta = W e_t - W f)
+                    {  // fields 0-2: -W f, f = d_i - d_c (the pair test forms W delta = W e_t - W f); 7: -D
                         const float f0 = v[0], f1 = v[1], f2 = v[2];
                         v[0] = -fmaf(v[8], f0, fmaf(v[9], f1, v[10] * f2));
                         v[1] = -fmaf(v[11], f0, fmaf(v[12], f1, v[13] * f2));
                         v[2] = -fmaf(v[14], f0, fmaf(v[15], f1, v[16] * f2));
+                        v[7] = -v[7];
                     }
 #pragma unroll
                     for (int f = 0; f < kPairFields; ++f) q[2 * f] = v[f];
@@ -920,11 +921,11 @@ __global__ void __launch_bounds__(kThreads, kAccMinBlocks) k_accumulate_band(
                         return;
                     }
                     if (anyA)
-                        pair_live_warp<kStats, true>(f2lo(T2.A), f2lo(T2.C2), f2lo(T2.DOT), T2.liveA, f2lo(T2.D),
+                        pair_live_warp<kStats, true>(f2lo(T2.A), f2lo(T2.C2), f2lo(T2.DOT), T2.liveA, f2lo(T2.ND),
                                                       f2lo(T2.ED), f2lo(T2.BP), f2lo(T2.KD), acc_base, K, dt, dtlo, idt,
                                                       kb0, nrows, wlo, whi, st_live, st_win, st_step);
                     if (anyB)
-                        pair_live_warp<kStats, true>(f2hi(T2.A), f2hi(T2.C2), f2hi(T2.DOT), T2.liveB, f2hi(T2.D),
+                        pair_live_warp<kStats, true>(f2hi(T2.A), f2hi(T2.C2), f2hi(T2.DOT), T2.liveB, f2hi(T2.ND),
                                                       f2hi(T2.ED), f2hi(T2.BP), f2hi(T2.KD), acc_base, K, dt, dtlo, idt,
                                                       kb0, nrows, wlo, whi, st_live, st_win, st_step);
                 };
