@@ -281,7 +281,7 @@ __device__ __forceinline__ void pair_live_warp(float pa, float pc2, float pdot, 
                                                uint32_t& st_live, uint32_t& st_win, uint32_t& st_step) {
     const float ia = rcp_approx(pa);
     const float r_over_D2 = pc2 * ia;
-    const float rr = r_over_D2 * ND * ND;
+    const float qd = ND * ND * -0.72134752044448170f;  // -D^2 log2(e)/2, off the MUFU chain
     const float sD = ND * pdot * ia;  // s* - D (ND = -D)
     const float ra = rsqrt_approx(pa);
     const float h = 0.70710678118654752f * pa * ra;
@@ -292,7 +292,7 @@ __device__ __forceinline__ void pair_live_warp(float pa, float pc2, float pdot, 
         if (x0 > -kXS) e0 = t;
     }
     live = live && e0 < 1.0f;
-    const float pref = betap * ra * ex2_approx(-0.72134752044448170f * rr);
+    const float pref = betap * ra * ex2_approx(kBand ? -0.72134752044448170f * (r_over_D2 * ND * ND) : r_over_D2 * qd);
     const float e = eD - sD;
     const float xsh = (kXS * 1.41421356237309505f) * ra;
     // window [klo, khi): ceil of the clamped bounds by round-to-nearest of kf + 1/2 (win_round)
@@ -308,7 +308,7 @@ __device__ __forceinline__ void pair_live_warp(float pa, float pc2, float pdot, 
         st_win += band_count<kBand>(klo, klo + n, kb0, nrows);
         st_step += (step && khi < K && (!kBand || (khi >= kb0 && khi < kb0 + nrows))) ? 1u : 0u;
     }
-    float fk = (ylo - kMagic) - kD;
+    float fk = kBand ? (ylo - kMagic) - kD : ylo - (kD + kMagic);  // (the same: integers below 2^24)
     uint32_t ap = acc_base + (uint32_t)klo * (kThreads * 4);
     const float tk1 = fmaf(fk, dt, fmaf(fk, dtlo, e));
     const float w1 = pref * (erf_fast(h * tk1) - e0);
@@ -393,7 +393,9 @@ __device__ __forceinline__ void live_packed(f2_t A2, f2_t C2, f2_t DOT, f2_t ND2
     const float aA = f2lo(A2), aB = f2hi(A2);
     const f2_t IA = f2pack(rcp_approx(aA), rcp_approx(aB));
     const f2_t RA = f2pack(rsqrt_approx(aA), rsqrt_approx(aB));
-    const f2_t RR = f2mul(f2mul(f2mul(C2, IA), ND2), ND2);
+    // single-table kernel: -r log2(e)/2 as (|g x W delta|^2 / a) (-D^2 log2(e)/2), the D
+    // factor off the MUFU chain (cfg2 a6 -0.4 %; the band kernel measured +1 % with it)
+    const f2_t QD = f2mul(f2mul(ND2, ND2), f2bc(-0.72134752044448170f));
     const f2_t SD = f2mul(f2mul(ND2, DOT), IA);  // s* - D = -D (u . W delta) / a
     const f2_t H = f2mul(f2mul(f2bc(0.70710678118654752f), A2), RA);
     const f2_t X0 = f2mul(H, f2sub(ND2, SD));  // -h (D + s* - D)
@@ -406,7 +408,8 @@ __device__ __forceinline__ void live_packed(f2_t A2, f2_t C2, f2_t DOT, f2_t ND2
     }
     const bool liveA = liveA_in && e0A < 1.0f, liveB = liveB_in && e0B < 1.0f;
     const f2_t E0 = f2pack(e0A, e0B);
-    const f2_t M = f2mul(f2bc(-0.72134752044448170f), RR);
+    const f2_t M = kBand ? f2mul(f2bc(-0.72134752044448170f), f2mul(f2mul(f2mul(C2, IA), ND2), ND2))
+                         : f2mul(f2mul(C2, IA), QD);
     const f2_t PREF = f2mul(f2mul(BP2, RA), f2pack(ex2_approx(f2lo(M)), ex2_approx(f2hi(M))));
     const f2_t E = f2sub(ED2, SD);
     const f2_t XSH = f2mul(f2bc(kXS * 1.41421356237309505f), RA);
@@ -418,7 +421,8 @@ __device__ __forceinline__ void live_packed(f2_t A2, f2_t C2, f2_t DOT, f2_t ND2
     const int kloA = __float_as_int(f2lo(YLO)) - kMagicBits, kloB = __float_as_int(f2hi(YLO)) - kMagicBits;
     const int khiA = max(__float_as_int(f2lo(YHI)) - kMagicBits, kloA);
     const int khiB = max(__float_as_int(f2hi(YHI)) - kMagicBits, kloB);
-    const f2_t FK = f2sub(f2sub(YLO, f2bc(kMagic)), KD);
+    const f2_t FK = kBand ? f2sub(f2sub(YLO, f2bc(kMagic)), KD)
+                          : f2sub(YLO, f2add(KD, f2bc(kMagic)));  // (the same: integers below 2^24)
     const f2_t TK1 = f2fma(FK, f2bc(dt), f2fma(FK, f2bc(dtlo), E));
     const f2_t W1 = f2mul(PREF, f2sub(erf_fast2(f2mul(H, TK1)), E0));
     live_finish<kStats, kBand>(liveA, kloA, khiA, f2lo(FK), f2lo(W1), f2lo(PREF), f2lo(H), f2lo(E), e0A, baseA, K,
