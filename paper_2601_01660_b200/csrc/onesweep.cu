@@ -1,6 +1,6 @@
 // onesweep.cu — stable LSD radix sort of (key, u32 value) pairs, key = u32 or
 // u64, in the "onesweep" style: one histogram pass over all digits, then ONE
-// kernel per digit (<= 8 bits) that ranks a 2048-key partition in shared memory (warp
+// kernel per digit (<= 8 bits) that ranks a 4096-key partition in shared memory (warp
 // multi-split by ballots, or match.any on a narrow top digit), obtains its global digit offsets by decoupled
 // look-back over earlier partitions (8 predecessors per round trip), and
 // scatters through shared memory for coalesced writes.  Partition ids come from
@@ -21,13 +21,18 @@ namespace dgsm {
 
 namespace {
 constexpr int kThreads = 256;
-// tuning knobs (tools/ab_sort.sh on cfg2: 8 items and an 8-wide look-back window
-// measured best; 6/12/16 items and 16/32-wide windows slower)
+// tuning knobs: an 8-wide look-back window (tools/ab_sort.sh; 16/32-wide slower);
+// 16 keys per thread at 2 CTAs/SM (tools/ab_os16.sh, whole steps: cfg2 -5 us,
+// cfg5 -0.13 ms, cfg3 +0.02 ms against 8 keys at 4 CTAs/SM; 12 keys at 3 CTAs/SM:
+// cfg5 -0.27 ms but cfg2 +4 us; 12 or 16 under the 4-CTA bound spill)
 #ifndef DGSM_OS_ITEMS
-#define DGSM_OS_ITEMS 8
+#define DGSM_OS_ITEMS 16
 #endif
 constexpr int kItems = DGSM_OS_ITEMS;
-constexpr int kTileKeys = kThreads * kItems;  // 2048 keys per partition (<= 64 regs: 4 CTAs/SM)
+#ifndef DGSM_OS_MINB
+#define DGSM_OS_MINB 2  // CTAs per SM the pass kernel is register-bounded for (126 registers)
+#endif
+constexpr int kTileKeys = kThreads * kItems;  // 4096 keys per partition (126 regs: 2 CTAs/SM)
 constexpr int kRadix = kSortRadix;
 constexpr int kMaxPasses = kSortMaxPasses;
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
@@ -124,7 +129,7 @@ __device__ __forceinline__ uint32_t look_back(volatile uint32_t* st, uint32_t pa
 }
 
 template <typename KeyT>
-__global__ void __launch_bounds__(kThreads, 4) k_pass(const KeyT* __restrict__ kin,
+__global__ void __launch_bounds__(kThreads, DGSM_OS_MINB) k_pass(const KeyT* __restrict__ kin,
                                                       const uint32_t* __restrict__ vin,
                                                       KeyT* __restrict__ kout, uint32_t* __restrict__ vout,
                                                       int64_t n, int shift, int bits, bool top,
